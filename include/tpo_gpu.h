@@ -1,0 +1,163 @@
+/* tpo_gpu.h — C-ABI of the B200 µGraph evaluation backend.
+ *
+ * Drop-in boundary for the reference's µGraph evaluation hot path
+ * (/root/reference/proj/core).  Plain C: opaque handles, plain pointers and
+ * sizes, no exceptions across the ABI.  Every entry point returns 0 on
+ * success or a status:
+ *     1000 + tpo::ErrCode ordinal  (reference proj/core/include/tpo/ir/shape.hpp:27-42)
+ *     2000 + ErrCode               "resample needed" (DivByZero / NonResidue) for the
+ *                                   single-attempt debug entry point
+ *     3000 + cudaError_t            CUDA failure
+ * and tpo_gpu_last_error() returns the message of the calling thread's last
+ * failure.  A context is bound to one device and one CUDA stream; use one
+ * context per host thread for concurrency (the reference API is pure and
+ * re-entrant).
+ *
+ * Reference interfaces replaced (file:line in /root/reference):
+ *   tpo_gpu_eval_mugraph            <- tpo::interp::eval_mugraph
+ *                                      proj/core/include/tpo/interp/interp.hpp:47-48
+ *   tpo_gpu_ff_eval                 <- tpo::verify::ff_eval (+ sample_inputs, sample_omega,
+ *                                      SiluTables::sample) proj/core/include/tpo/verify/ffeval.hpp:58-67,
+ *                                      proj/core/src/equiv.cpp:57-68
+ *   tpo_gpu_random_test_equivalence <- tpo::verify::random_test_equivalence
+ *                                      proj/core/include/tpo/verify/equiv.hpp:50-53
+ *   tpo_gpu_verify_batch/_pool      <- the search loop's per-candidate calls of the same
+ *                                      (SPEC.md:664-668), batched
+ *   tpo_gpu_compile                 <- tpo::ir::kernel_graph_from_json + tpo::ir::validate
+ *                                      proj/core/include/tpo/ir/serialize.hpp:33-34,
+ *                                      proj/core/include/tpo/ir/validate.hpp:51
+ *   tpo_gpu_validate                <- tpo::ir::validate (B200 MemLimits)
+ *   tpo_gpu_op_madds                <- tpo::ir::op_madds summed over a µGraph
+ *                                      proj/core/include/tpo/ir/shape_infer.hpp:67-69
+ */
+#ifndef TPO_GPU_H
+#define TPO_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TPO_GPU_ABI_VERSION 1
+
+typedef struct tpo_gpu_ctx tpo_gpu_ctx;
+typedef struct tpo_gpu_graph tpo_gpu_graph;
+
+/* FieldParams(p, q, omega_base) — proj/core/include/tpo/verify/field.hpp:50-79 */
+typedef struct {
+  uint32_t p, q, omega_base;
+} tpo_field_params;
+
+/* VerifyConfig — proj/core/include/tpo/verify/equiv.hpp:25-30 */
+typedef struct {
+  int32_t num_tests;
+  int32_t max_resamples;
+  uint64_t seed;
+  double float_tolerance;
+} tpo_verify_cfg;
+
+/* EquivVerdict + Witness — proj/core/include/tpo/verify/equiv.hpp:32-45 (48 bytes) */
+typedef struct {
+  int32_t kind; /* 0 Equivalent, 1 NotEquivalent, 2 Inconclusive, 3 Error (err_code) */
+  int32_t rounds_run;
+  int32_t resamples;
+  int32_t has_witness;
+  uint64_t w_seed;
+  int32_t w_round;
+  uint32_t w_omega;
+  int32_t w_tensor;
+  int32_t err_code;
+  int64_t w_index;
+} tpo_verdict;
+
+/* Lowering chosen for a compiled graph by tpo_gpu_eval_mugraph. */
+enum {
+  TPO_FUSED_NONE = 0, /* generic VM path only */
+  TPO_FUSED_RMSNORM_MATMUL = 1,
+  TPO_FUSED_GATED_MLP = 2,
+  TPO_FUSED_GQA_DECODE = 3,
+  TPO_FUSED_LORA = 4,
+};
+
+enum { TPO_DTYPE_F32 = 0, TPO_DTYPE_BF16 = 1 };
+
+typedef struct {
+  int32_t n_inputs, n_outputs;
+  int32_t fused_kind;      /* TPO_FUSED_* */
+  int32_t lax;             /* 1 when no EwExp consumes an exponentiated value */
+  int64_t madds;           /* reference op_madds work of the graph */
+  int64_t input_elems;     /* total elements over all inputs */
+  int64_t output_elems;
+  int64_t vm_words;        /* verifier VM words (inputs + graph region); -1 if not lowerable */
+} tpo_graph_info;
+
+int tpo_gpu_abi_version(void);
+const char *tpo_gpu_last_error(void);
+
+int tpo_gpu_open(int device, tpo_gpu_ctx **out);
+void tpo_gpu_close(tpo_gpu_ctx *ctx);
+
+/* Parse (serialize.hpp schema), validate against B200 limits (227 KiB smem),
+ * lower.  The handle owns host IR + lowering plans; device bytecode is
+ * uploaded per batch. */
+int tpo_gpu_compile(tpo_gpu_ctx *ctx, const char *graph_json, tpo_gpu_graph **out);
+void tpo_gpu_graph_free(tpo_gpu_graph *g);
+int tpo_gpu_graph_info(const tpo_gpu_graph *g, tpo_graph_info *out);
+/* Shape of input/output `index` (is_output 0/1): writes rank dims, returns rank or <0. */
+int tpo_gpu_graph_shape(const tpo_gpu_graph *g, int is_output, int index, int64_t *dims);
+
+/* validate(g, {smem_bytes, 512, elem_size}); returns number of violations
+ * (>= 0) with details in `buf`, or a status (>= 1000) on parse errors. */
+int tpo_gpu_validate(const char *graph_json, int64_t smem_bytes, int64_t elem_size, char *buf,
+                     int cap);
+
+/* Floating-point µGraph evaluation on device buffers (row-major, caller
+ * owns).  Inputs are TPO_DTYPE_BF16 or _F32 per `in_dtype`; outputs fp32.
+ * Benchmark µGraphs run as one fused sm_100a kernel (fused_kind != 0). */
+int tpo_gpu_eval_mugraph(tpo_gpu_ctx *ctx, const tpo_gpu_graph *g, const void *const *in_dev,
+                         const int32_t *in_dtype, float *const *out_dev, void *cuda_stream);
+
+/* One verifier attempt for one graph, exactly as equiv.cpp:57-68 draws it
+ * (Rng::derive(seed, stream); inputs; omega; SiLU tables iff with_silu).
+ * Outputs are concatenated over the graph outputs.  in_xp/in_xq (nullable)
+ * receive the sampled inputs.  Returns 0, or 2000 + ErrCode when an undefined
+ * field op requires a resample. */
+int tpo_gpu_ff_eval(tpo_gpu_ctx *ctx, const tpo_gpu_graph *g, const tpo_field_params *fp,
+                    uint64_t seed, uint64_t stream, int32_t with_silu, uint16_t *out_xp,
+                    uint16_t *out_xq, uint8_t *out_qd, uint32_t *omega_out, uint16_t *in_xp,
+                    uint16_t *in_xq);
+
+/* random_test_equivalence(g1, g2, cfg, fp) on the GPU. */
+int tpo_gpu_random_test_equivalence(tpo_gpu_ctx *ctx, const tpo_gpu_graph *g1,
+                                    const tpo_gpu_graph *g2, const tpo_verify_cfg *cfg,
+                                    const tpo_field_params *fp, tpo_verdict *out);
+
+/* Batched verification: candidate k (k < n) is checked against `program`
+ * with cfg {num_tests, seeds[k], max_resamples}; one verdict per candidate
+ * (host array, nullable) and packed accept bits (host, nullable; bit k set
+ * iff Equivalent). */
+int tpo_gpu_verify_batch(tpo_gpu_ctx *ctx, const tpo_gpu_graph *program,
+                         const tpo_gpu_graph *const *cands, const uint64_t *seeds, uint64_t n,
+                         const tpo_verify_cfg *cfg, const tpo_field_params *fp,
+                         tpo_verdict *verdicts, uint32_t *accept_bits);
+
+/* Sharding form: candidate i in [first, first + n) is pool[i % pool_n] with
+ * seed i.  `accept_dev` (nullable) is a DEVICE buffer of ceil(n/32) words
+ * receiving accept bits (ready for a collective gather); `verdicts` (host,
+ * nullable); `attempts` (host, nullable) receives the attempts consumed.
+ * Runs on `cuda_stream` (null: the context stream) and synchronises. */
+int tpo_gpu_verify_pool(tpo_gpu_ctx *ctx, const tpo_gpu_graph *program,
+                        const tpo_gpu_graph *const *pool, int32_t pool_n, uint64_t first,
+                        uint64_t n, const tpo_verify_cfg *cfg, const tpo_field_params *fp,
+                        uint32_t *accept_dev, tpo_verdict *verdicts, uint64_t *attempts,
+                        void *cuda_stream);
+
+/* Reference op_madds work of a graph (SURVEY §8d verifier work unit). */
+int64_t tpo_gpu_op_madds(const tpo_gpu_graph *g);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TPO_GPU_H */

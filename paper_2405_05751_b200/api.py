@@ -1,0 +1,210 @@
+"""Python host API over the C-ABI, mirroring the reference entry points.
+
+==============================  ===============================================
+this module                     reference (proj/core/include/tpo/...)
+==============================  ===============================================
+``Context.eval_mugraph``        ``interp::eval_mugraph`` (interp/interp.hpp:47-48)
+``Context.ff_eval``             ``verify::ff_eval`` + sampling (verify/ffeval.hpp:58-67)
+``Context.random_test_equivalence`` ``verify::random_test_equivalence`` (verify/equiv.hpp:50-53)
+``Context.verify_batch``        the search loop's per-candidate verification, batched
+``Context.verify_pool``         same, sharding form (candidate i = pool[i % n], seed i)
+``validate``                    ``ir::validate`` (ir/validate.hpp:51)
+==============================  ===============================================
+
+Graphs are wire-format dicts (see ``graph.py``) or JSON strings.  Errors raise
+:class:`~paper_2405_05751_b200._native.NativeError` carrying the C-ABI status
+(1000 + ErrCode).  All compute runs on the GPU through ``libtpo_b200.so``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+
+from . import _native as N
+
+VERDICT_DTYPE = np.dtype([("kind", "<i4"), ("rounds_run", "<i4"), ("resamples", "<i4"),
+                          ("has_witness", "<i4"), ("w_seed", "<u8"), ("w_round", "<i4"),
+                          ("w_omega", "<u4"), ("w_tensor", "<i4"), ("err_code", "<i4"),
+                          ("w_index", "<i8")])
+KIND = {0: "Equivalent", 1: "NotEquivalent", 2: "Inconclusive", 3: "Error"}
+FUSED = {0: None, 1: "rmsnorm", 2: "gatedmlp", 3: "gqa", 4: "lora"}
+
+
+def _js(g) -> bytes:
+    return (g if isinstance(g, str) else json.dumps(g, separators=(",", ":"))).encode()
+
+
+def validate(g, smem_bytes: int = 232448, elem_size: int = 2):
+    """Number of Definition-1 violations and their text (B200 limits by default)."""
+    buf = C.create_string_buffer(4096)
+    rc = N.lib().tpo_gpu_validate(_js(g), smem_bytes, elem_size, buf, 4096)
+    if rc >= 1000:
+        raise N.NativeError(rc, N.last_error())
+    return rc, buf.value.decode()
+
+
+class Graph:
+    """A compiled µGraph handle (``tpo_gpu_compile``)."""
+
+    def __init__(self, ctx: "Context", g):
+        self.ctx = ctx
+        self.spec = json.loads(g) if isinstance(g, str) else g
+        h = C.c_void_p()
+        N.check(N.lib().tpo_gpu_compile(ctx.h, _js(g), C.byref(h)))
+        self.h = h
+        info = N.GraphInfo()
+        N.lib().tpo_gpu_graph_info(h, C.byref(info))
+        self.info = info
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h and N._lib is not None:
+            N.lib().tpo_gpu_graph_free(h)
+            self.h = None
+
+    def shapes(self, outputs: bool) -> List[List[int]]:
+        n = self.info.n_outputs if outputs else self.info.n_inputs
+        out = []
+        for i in range(n):
+            dims = (C.c_int64 * 4)()
+            r = N.lib().tpo_gpu_graph_shape(self.h, int(outputs), i, dims)
+            out.append([dims[k] for k in range(r)])
+        return out
+
+    @property
+    def fused(self) -> Optional[str]:
+        return FUSED.get(self.info.fused_kind)
+
+    @property
+    def madds(self) -> int:
+        return int(self.info.madds)
+
+
+class Context:
+    """One device + stream (``tpo_gpu_open``)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        N.check(N.lib().tpo_gpu_open(device, C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            N.lib().tpo_gpu_close(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def compile(self, g) -> Graph:
+        return g if isinstance(g, Graph) else Graph(self, g)
+
+    # ---- floating point -------------------------------------------------
+    def eval_mugraph(self, g, inputs: Sequence, outputs=None, stream=None):
+        """Fused fp evaluation on torch CUDA tensors (bf16 or fp32 inputs, fp32 outputs)."""
+        import torch
+        g = self.compile(g)
+        ins = list(inputs)
+        if len(ins) != g.info.n_inputs:
+            raise ValueError("input count")
+        for x, s in zip(ins, g.shapes(False)):
+            if list(x.shape) != s or not x.is_cuda or not x.is_contiguous():
+                raise ValueError(f"input must be a contiguous CUDA tensor of shape {s}")
+        if outputs is None:
+            outputs = [torch.empty(s, device=ins[0].device, dtype=torch.float32)
+                       for s in g.shapes(True)]
+        dt = (C.c_int32 * len(ins))(*[1 if x.dtype == torch.bfloat16 else 0 for x in ins])
+        pin = (C.c_void_p * len(ins))(*[x.data_ptr() for x in ins])
+        pout = (C.c_void_p * len(outputs))(*[o.data_ptr() for o in outputs])
+        st = stream if stream is not None else torch.cuda.current_stream(ins[0].device).cuda_stream
+        N.check(N.lib().tpo_gpu_eval_mugraph(self.h, g.h, pin, dt, pout, C.c_void_p(st)))
+        return outputs
+
+    # ---- finite field -------------------------------------------------------
+    def ff_eval(self, g, seed: int, stream: int, with_silu: Optional[bool] = None, p=227, q=113,
+                wbase=4):
+        """One verifier attempt on one graph; mirrors oracle.ref.ff_attempt's return."""
+        from .graph import has_silu
+        g = self.compile(g)
+        if with_silu is None:
+            with_silu = has_silu(g.spec)
+        n_in, n_out = g.info.input_elems, g.info.output_elems
+        oxp, oxq = np.zeros(n_out, np.uint16), np.zeros(n_out, np.uint16)
+        oqd = np.zeros(n_out, np.uint8)
+        ixp, ixq = np.zeros(n_in, np.uint16), np.zeros(n_in, np.uint16)
+        om = C.c_uint32(0)
+        fp = N.FieldParams(p, q, wbase)
+        rc = N.lib().tpo_gpu_ff_eval(self.h, g.h, C.byref(fp), seed, stream, int(with_silu),
+                                     oxp.ctypes.data, oxq.ctypes.data, oqd.ctypes.data,
+                                     C.addressof(om), ixp.ctypes.data, ixq.ctypes.data)
+        if rc and rc < 2000:
+            raise N.NativeError(rc, N.last_error())
+        outs, c = [], 0
+        for s in g.shapes(True):
+            n = int(np.prod(s))
+            outs.append((oxp[c:c + n].reshape(s), oxq[c:c + n].reshape(s), oqd[c:c + n].reshape(s)))
+            c += n
+        return dict(rc=rc, omega=om.value, in_xp=ixp, in_xq=ixq, out=outs)
+
+    def random_test_equivalence(self, g1, g2, num_tests=1, seed=0, max_resamples=16, p=227,
+                                q=113, wbase=4) -> Dict[str, int]:
+        g1, g2 = self.compile(g1), self.compile(g2)
+        v = N.Verdict()
+        cfg = N.VerifyCfg(num_tests, max_resamples, seed, 1e-3)
+        fp = N.FieldParams(p, q, wbase)
+        rc = N.lib().tpo_gpu_random_test_equivalence(self.h, g1.h, g2.h, C.byref(cfg), C.byref(fp),
+                                                     C.byref(v))
+        if rc and v.kind != 3:
+            raise N.NativeError(rc, N.last_error())
+        return {k: getattr(v, k) for k, _ in N.Verdict._fields_}
+
+    def verify_batch(self, program, cands: Sequence, seeds: Sequence[int], num_tests=1,
+                     max_resamples=16, p=227, q=113, wbase=4, want_verdicts=True):
+        """Returns (verdicts structured array | None, accept bool array)."""
+        prog = self.compile(program)
+        handles = {}
+        hs = []
+        for c in cands:
+            key = id(c)
+            if key not in handles:
+                handles[key] = self.compile(c)
+            hs.append(handles[key].h.value)
+        n = len(hs)
+        arr = (C.c_void_p * n)(*hs)
+        sd = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64))
+        out = np.zeros(n, VERDICT_DTYPE) if want_verdicts else None
+        acc = np.zeros((n + 31) // 32, np.uint32)
+        cfg = N.VerifyCfg(num_tests, max_resamples, 0, 1e-3)
+        fp = N.FieldParams(p, q, wbase)
+        N.check(N.lib().tpo_gpu_verify_batch(self.h, prog.h, arr, sd.ctypes.data, n, C.byref(cfg),
+                                             C.byref(fp), out.ctypes.data if want_verdicts else None,
+                                             acc.ctypes.data))
+        bits = np.unpackbits(acc.view(np.uint8), bitorder="little")[:n].astype(bool)
+        return out, bits
+
+    def verify_pool(self, program, pool: Sequence, first: int, n: int, num_tests=1,
+                    max_resamples=16, p=227, q=113, wbase=4, want_verdicts=False,
+                    accept_dev=None, stream=None):
+        """Sharding form: candidate i in [first, first+n) = pool[i % len(pool)], seed i.
+        ``accept_dev``: optional int32 torch CUDA tensor of ceil(n/32) words.
+        Returns (verdicts | None, attempts)."""
+        prog = self.compile(program)
+        gs = [self.compile(c) for c in pool]
+        arr = (C.c_void_p * len(gs))(*[g.h.value for g in gs])
+        out = np.zeros(n, VERDICT_DTYPE) if want_verdicts else None
+        att = C.c_uint64(0)
+        cfg = N.VerifyCfg(num_tests, max_resamples, 0, 1e-3)
+        fp = N.FieldParams(p, q, wbase)
+        N.check(N.lib().tpo_gpu_verify_pool(
+            self.h, prog.h, arr, len(gs), first, n, C.byref(cfg), C.byref(fp),
+            C.c_void_p(accept_dev.data_ptr()) if accept_dev is not None else None,
+            out.ctypes.data if want_verdicts else None, C.addressof(att),
+            C.c_void_p(stream) if stream else None))
+        return out, att.value

@@ -1,0 +1,553 @@
+// B200 backend — C-ABI (include/tpo_gpu.h) over the host runtime.
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../../include/tpo_gpu.h"
+#include "runtime.hpp"
+#include "tpo/ir/serialize.hpp"
+#include "tpo/ir/shape_infer.hpp"
+#include "tpo/ir/validate.hpp"
+
+struct tpo_gpu_ctx {
+  tpo::gpu::Ctx c;
+};
+struct tpo_gpu_graph {
+  tpo::gpu::Graph g;
+};
+
+namespace tpo::gpu {
+
+namespace {
+thread_local std::string g_last;
+
+int fail(int code, const std::string &msg) {
+  g_last = msg;
+  return code;
+}
+
+template <class F>
+int guard(F &&f) {
+  try {
+    return f();
+  } catch (const Error &e) {
+    return fail(1000 + int(e.code), e.what());
+  } catch (const std::exception &e) {
+    return fail(1000 + int(ErrCode::Unsupported), e.what());
+  }
+}
+
+bool is_prime(uint32_t n) {
+  if (n < 2) return false;
+  for (uint32_t d = 2; d * d <= n; ++d)
+    if (n % d == 0) return false;
+  return true;
+}
+
+uint32_t pow_mod(uint64_t b, uint64_t e, uint32_t m) {
+  uint64_t r = 1;
+  b %= m;
+  while (e) {
+    if (e & 1) r = r * b % m;
+    b = b * b % m;
+    e >>= 1;
+  }
+  return uint32_t(r);
+}
+}  // namespace
+
+void check_cuda(cudaError_t e, const char *what) {
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw Error(ErrCode::Unsupported, std::string("CUDA ") + what + ": " + cudaGetErrorString(e));
+  }
+}
+
+void *DevBuf::get(size_t bytes) {
+  if (bytes > cap) {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    size_t c = std::max(bytes, cap * 2);
+    c = std::max<size_t>(c, 256);
+    check_cuda(cudaMalloc(&ptr, c), "cudaMalloc");
+    cap = c;
+  }
+  return ptr;
+}
+
+DevBuf::~DevBuf() {
+  if (ptr) cudaFree(ptr);
+}
+
+// FieldParams (field.cpp:43-67): same validity checks and tables, plus the
+// device constants of the lazy-reduction scheme.
+FieldState &Ctx::field(uint32_t p, uint32_t q, uint32_t wbase) {
+  uint64_t key = (uint64_t(p) << 40) ^ (uint64_t(q) << 20) ^ wbase;
+  auto it = fields.find(key);
+  if (it != fields.end()) return *it->second;
+  if (!is_prime(p) || !is_prime(q)) throw Error(ErrCode::ConfigError, "p and q must be prime");
+  if ((p - 1) % q != 0) throw Error(ErrCode::ConfigError, "q must divide p-1");
+  if (wbase % p == 0 || wbase % p == 1 || pow_mod(wbase, q, p) != 1)
+    throw Error(ErrCode::ConfigError, "omega base must have multiplicative order q in Z_p");
+  if (p > 4093) throw Error(ErrCode::Unsupported, "device field tables limited to p < 4096");
+  auto fs = std::make_unique<FieldState>();
+  auto &f = fs->fc;
+  f.p = p;
+  f.q = q;
+  f.wbase = wbase;
+  f.magic_p = uint32_t((1ull << 32) / p);
+  f.magic_q = uint32_t((1ull << 32) / q);
+  f.two32_p = uint32_t((1ull << 32) % p);
+  f.two32_q = uint32_t((1ull << 32) % q);
+  uint64_t pm1 = p - 1;
+  f.lazy = uint32_t(std::max<uint64_t>(1, (0xFFFFFFFFull - p) / (pm1 * pm1)));
+  f.lazy_sum = uint32_t(std::max<uint64_t>(1, (0xFFFFFFFFull - p) / pm1));
+  f.thr_p = (0 - uint64_t(p)) % p;
+  f.thr_q = (0 - uint64_t(q)) % q;
+  uint32_t tb = 2 * (5 * 0 + p + q + p + q + q) + 2 * (p + q);
+  f.table_bytes = (tb + 15) & ~15u;
+  auto &t = fs->host_tables;
+  t.assign(2 * (p + q), 0);
+  for (uint32_t x = 1; x < p; ++x) t[x] = uint16_t(pow_mod(x, p - 2, p));
+  for (uint32_t x = 1; x < q; ++x) t[p + x] = uint16_t(pow_mod(x, q - 2, q));
+  std::vector<int32_t> sp(p, -1), sq(q, -1);
+  for (int64_t r = int64_t(p) - 1; r >= 0; --r) sp[size_t(uint64_t(r) * uint64_t(r) % p)] = int32_t(r);
+  for (int64_t r = int64_t(q) - 1; r >= 0; --r) sq[size_t(uint64_t(r) * uint64_t(r) % q)] = int32_t(r);
+  for (uint32_t x = 0; x < p; ++x) t[p + q + x] = uint16_t(int16_t(sp[x]));
+  for (uint32_t x = 0; x < q; ++x) t[2 * p + q + x] = uint16_t(int16_t(sq[x]));
+  check_cuda(cudaSetDevice(device), "cudaSetDevice");
+  void *d = fs->dev.get(t.size() * 2);
+  check_cuda(cudaMemcpy(d, t.data(), t.size() * 2, cudaMemcpyHostToDevice), "tables");
+  auto &ref = *fs;
+  fields[key] = std::move(fs);
+  return ref;
+}
+
+namespace {
+
+// A verification batch: the program plus unique candidate graphs lowered
+// into one device upload.
+struct Batch {
+  std::vector<TpoVmInstr> code;
+  std::vector<TpoVmGraph> graphs;
+  uint32_t n_in = 0;
+  uint32_t max_words = 0;  // words of VM memory needed
+};
+
+void check_pair(const ir::KernelGraph &a, const ir::KernelGraph &b) {
+  // equiv.cpp:38-49
+  if (a.inputs.size() != b.inputs.size() || a.outputs.size() != b.outputs.size())
+    throw Error(ErrCode::ShapeMismatch, "graph arity");
+  for (size_t i = 0; i < a.inputs.size(); ++i)
+    if (a.tensor(a.inputs[i]).shape != b.tensor(b.inputs[i]).shape)
+      throw Error(ErrCode::ShapeMismatch, "input shapes");
+  for (size_t i = 0; i < a.outputs.size(); ++i)
+    if (a.tensor(a.outputs[i]).shape != b.tensor(b.outputs[i]).shape)
+      throw Error(ErrCode::ShapeMismatch, "output shapes");
+}
+
+void add_graph(Batch &bt, const VmProgram &p) {
+  TpoVmGraph d = p.desc;
+  d.code_off = uint32_t(bt.code.size());
+  d.code_len = uint32_t(p.code.size());
+  bt.code.insert(bt.code.end(), p.code.begin(), p.code.end());
+  bt.graphs.push_back(d);
+}
+
+TpoVmGraph error_graph(ErrCode c) {
+  TpoVmGraph d;
+  std::memset(&d, 0, sizeof(d));
+  d.err = uint8_t(1 + int(c));
+  return d;
+}
+
+// Lowers program + unique candidates; returns candidate graph index per
+// unique handle in `index`.
+Batch build_batch(const Graph &prog, const std::vector<const Graph *> &uniq) {
+  Batch bt;
+  bt.n_in = uint32_t(prog.in_elems);
+  // program outputs pinned right after the inputs; program scratch above
+  // them is dead once the candidate starts, so the candidate region reuses it
+  VmProgram pp = lower_vm(prog.g, 0, bt.n_in, /*pin_outputs=*/true);
+  const uint32_t cbase = bt.n_in + pp.pinned_words;
+  if (pp.poisoned) pp.desc.err = uint8_t(1 + int(ErrCode::PoisonedExponent));
+  add_graph(bt, pp);
+  uint32_t maxw = bt.n_in + pp.region_words;
+  for (const Graph *c : uniq) {
+    try {
+      check_pair(prog.g, c->g);
+      VmProgram cp = lower_vm(c->g, 0, cbase);
+      if (cp.poisoned) cp.desc.err = uint8_t(1 + int(ErrCode::PoisonedExponent));
+      maxw = std::max(maxw, cbase + cp.region_words);
+      add_graph(bt, cp);
+    } catch (const Error &e) {
+      bt.graphs.push_back(error_graph(e.code));
+    }
+  }
+  bt.max_words = maxw;
+  return bt;
+}
+
+struct VerifyRun {
+  const uint32_t *pool_host = nullptr;  // pool mode
+  uint32_t pool_n = 0;
+  const std::vector<uint32_t> *cand_graph = nullptr;  // explicit mode
+  const uint64_t *seeds = nullptr;
+  uint64_t first = 0, n = 0;
+  tpo_verdict *verdicts_host = nullptr;
+  uint32_t *accept_host = nullptr;
+  uint32_t *accept_dev = nullptr;
+  uint64_t *attempts = nullptr;
+  cudaStream_t stream = nullptr;
+};
+
+void run_verify(Ctx &C, const Batch &bt, const tpo_verify_cfg &cfg, const tpo_field_params &fpp,
+                const VerifyRun &r) {
+  check_cuda(cudaSetDevice(C.device), "cudaSetDevice");
+  FieldState &fs = C.field(fpp.p, fpp.q, fpp.omega_base);
+  const size_t smem = fs.fc.table_bytes + size_t(bt.max_words) * 4;
+  if (smem > 232448)
+    throw Error(ErrCode::DoesNotFit,
+                "verifier working set " + std::to_string(smem) + " B exceeds 227 KiB of shared memory");
+  if (cfg.num_tests < 1) throw Error(ErrCode::ConfigError, "num_tests must be >= 1");
+  cudaStream_t st = r.stream ? r.stream : C.stream;
+  tpo_ff::VerifyArgs a{};
+  a.field = fs.fc;
+  a.tables = static_cast<const uint16_t *>(fs.dev.ptr);
+  auto *dcode = static_cast<TpoVmInstr *>(C.code.get(bt.code.size() * sizeof(TpoVmInstr) + 1));
+  auto *dgraphs = static_cast<TpoVmGraph *>(C.graphs.get(bt.graphs.size() * sizeof(TpoVmGraph)));
+  check_cuda(cudaMemcpyAsync(dcode, bt.code.data(), bt.code.size() * sizeof(TpoVmInstr),
+                             cudaMemcpyHostToDevice, st), "upload code");
+  check_cuda(cudaMemcpyAsync(dgraphs, bt.graphs.data(), bt.graphs.size() * sizeof(TpoVmGraph),
+                             cudaMemcpyHostToDevice, st), "upload graphs");
+  a.code = dcode;
+  a.graphs = dgraphs;
+  a.program = 0;
+  if (r.pool_host) {
+    auto *dp = static_cast<uint32_t *>(C.pool.get(r.pool_n * 4));
+    check_cuda(cudaMemcpyAsync(dp, r.pool_host, r.pool_n * 4, cudaMemcpyHostToDevice, st), "pool");
+    a.pool = dp;
+    a.pool_n = r.pool_n;
+  } else {
+    auto *dc = static_cast<uint32_t *>(C.cand.get(r.n * 4));
+    check_cuda(cudaMemcpyAsync(dc, r.cand_graph->data(), r.n * 4, cudaMemcpyHostToDevice, st), "cands");
+    a.cand_graph = dc;
+  }
+  if (r.seeds) {
+    auto *ds = static_cast<uint64_t *>(C.seeds.get(r.n * 8));
+    check_cuda(cudaMemcpyAsync(ds, r.seeds, r.n * 8, cudaMemcpyHostToDevice, st), "seeds");
+    a.seeds = ds;
+  }
+  a.first = r.first;
+  a.n = r.n;
+  a.n_in = bt.n_in;
+  a.num_tests = cfg.num_tests;
+  a.max_resamples = cfg.max_resamples;
+  auto *cnt = static_cast<unsigned long long *>(C.counter.get(16));
+  check_cuda(cudaMemsetAsync(cnt, 0, 16, st), "counter");
+  a.counter = cnt;
+  a.work = cnt + 1;
+  if (r.verdicts_host) a.verdicts = static_cast<TpoVerdict *>(C.verdicts.get(r.n * sizeof(TpoVerdict)));
+  const size_t words = (r.n + 31) / 32;
+  uint32_t *acc = r.accept_dev;
+  if (!acc && r.accept_host) acc = static_cast<uint32_t *>(C.accept.get(words * 4));
+  if (acc) check_cuda(cudaMemsetAsync(acc, 0, words * 4, st), "accept");
+  a.accept = acc;
+  int occ = tpo_ff_verify_occupancy(smem);
+  if (occ < 1) throw Error(ErrCode::DoesNotFit, "verifier kernel does not fit on an SM");
+  uint64_t grid = std::min<uint64_t>(uint64_t(C.num_sms) * uint64_t(occ), r.n);
+  grid = std::max<uint64_t>(grid, 1);
+  check_cuda(cudaError_t(tpo_ff_launch_verify(&a, int(grid), smem, st)), "verify launch");
+  if (r.verdicts_host)
+    check_cuda(cudaMemcpyAsync(r.verdicts_host, a.verdicts, r.n * sizeof(TpoVerdict),
+                               cudaMemcpyDeviceToHost, st), "verdicts");
+  if (r.accept_host)
+    check_cuda(cudaMemcpyAsync(r.accept_host, acc, words * 4, cudaMemcpyDeviceToHost, st), "accept");
+  unsigned long long counters[2] = {0, 0};
+  if (r.attempts)
+    check_cuda(cudaMemcpyAsync(counters, cnt, 16, cudaMemcpyDeviceToHost, st), "attempts");
+  check_cuda(cudaStreamSynchronize(st), "verify sync");
+  if (r.attempts) *r.attempts = counters[1];
+}
+
+}  // namespace
+}  // namespace tpo::gpu
+
+using namespace tpo;
+using namespace tpo::gpu;
+
+extern "C" {
+
+int tpo_gpu_abi_version(void) { return TPO_GPU_ABI_VERSION; }
+
+const char *tpo_gpu_last_error(void) { return g_last.c_str(); }
+
+int tpo_gpu_open(int device, tpo_gpu_ctx **out) {
+  return guard([&] {
+    auto *c = new tpo_gpu_ctx();
+    c->c.device = device;
+    try {
+      check_cuda(cudaSetDevice(device), "cudaSetDevice");
+      check_cuda(cudaStreamCreateWithFlags(&c->c.stream, cudaStreamNonBlocking), "stream");
+      check_cuda(cudaDeviceGetAttribute(&c->c.num_sms, cudaDevAttrMultiProcessorCount, device), "attr");
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+    return 0;
+  });
+}
+
+void tpo_gpu_close(tpo_gpu_ctx *ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->c.device);
+  if (ctx->c.stream) cudaStreamDestroy(ctx->c.stream);
+  delete ctx;
+}
+
+int tpo_gpu_compile(tpo_gpu_ctx *, const char *json, tpo_gpu_graph **out) {
+  return guard([&] {
+    nlohmann::json j;
+    try {
+      j = nlohmann::json::parse(json);
+    } catch (const nlohmann::json::exception &e) {
+      throw Error(ErrCode::ParseError, e.what());
+    }
+    auto *h = new tpo_gpu_graph();
+    try {
+      Graph &G = h->g;
+      G.g = ir::kernel_graph_from_json(j);
+      ir::ValidityReport rep = ir::validate(G.g, ir::kB200Limits);
+      if (!rep.valid()) {
+        std::string msg;
+        for (auto &v : rep.violations) msg += v.detail + "; ";
+        ErrCode c = rep.violations[0].kind == ir::ViolationKind::MemoryCapacity
+                        ? ErrCode::DoesNotFit
+                        : ErrCode::ShapeMismatch;
+        throw Error(c, "invalid µGraph: " + msg);
+      }
+      G.lax = ir::mugraph_lax_check(G.g).lax;
+      G.madds = graph_madds(G.g);
+      G.in_elems = input_elems(G.g);
+      for (ir::TensorId t : G.g.outputs) G.out_elems += G.g.tensor(t).shape.elem_count();
+      G.plan = match_fused(G.g);
+      try {
+        VmProgram vp = lower_vm(G.g, 0, uint32_t(G.in_elems));
+        G.vm_words = G.in_elems + vp.region_words;
+      } catch (const Error &) {
+        G.vm_words = -1;
+      }
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+    return 0;
+  });
+}
+
+void tpo_gpu_graph_free(tpo_gpu_graph *g) { delete g; }
+
+int tpo_gpu_graph_info(const tpo_gpu_graph *h, tpo_graph_info *o) {
+  const Graph &G = h->g;
+  o->n_inputs = int32_t(G.g.inputs.size());
+  o->n_outputs = int32_t(G.g.outputs.size());
+  o->fused_kind = G.plan.kind;
+  o->lax = G.lax;
+  o->madds = G.madds;
+  o->input_elems = G.in_elems;
+  o->output_elems = G.out_elems;
+  o->vm_words = G.vm_words;
+  return 0;
+}
+
+int tpo_gpu_graph_shape(const tpo_gpu_graph *h, int is_output, int index, int64_t *dims) {
+  const auto &v = is_output ? h->g.g.outputs : h->g.g.inputs;
+  if (index < 0 || size_t(index) >= v.size()) return -1;
+  const auto &s = h->g.g.tensor(v[size_t(index)]).shape;
+  for (int i = 0; i < s.rank(); ++i) dims[i] = s.dims[size_t(i)];
+  return s.rank();
+}
+
+int tpo_gpu_validate(const char *json, int64_t smem_bytes, int64_t elem_size, char *buf, int cap) {
+  return guard([&] {
+    nlohmann::json j;
+    try {
+      j = nlohmann::json::parse(json);
+    } catch (const nlohmann::json::exception &e) {
+      throw Error(ErrCode::ParseError, e.what());
+    }
+    ir::KernelGraph g = ir::kernel_graph_from_json(j);
+    ir::MemLimits lim;
+    lim.smem_bytes = smem_bytes;
+    lim.elem_size = elem_size;
+    auto rep = ir::validate(g, lim);
+    std::string msg;
+    for (auto &v : rep.violations) msg += v.detail + "; ";
+    if (buf && cap > 0) {
+      std::strncpy(buf, msg.c_str(), size_t(cap - 1));
+      buf[cap - 1] = 0;
+    }
+    return int(rep.violations.size());
+  });
+}
+
+int64_t tpo_gpu_op_madds(const tpo_gpu_graph *g) { return g->g.madds; }
+
+int tpo_gpu_eval_mugraph(tpo_gpu_ctx *ctx, const tpo_gpu_graph *h, const void *const *in_dev,
+                         const int32_t *in_dtype, float *const *out_dev, void *stream) {
+  return guard([&] {
+    const Graph &G = h->g;
+    if (!G.plan.kind)
+      throw Error(ErrCode::Unsupported, "no fused sm_100a kernel for this µGraph: " + G.plan.why);
+    check_cuda(cudaSetDevice(ctx->c.device), "cudaSetDevice");
+    size_t wsb = fused_workspace_bytes(G.plan);
+    void *ws = wsb ? ctx->c.ws.get(wsb) : nullptr;
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->c.stream;
+    int e = launch_fused(G.plan, in_dev, in_dtype, out_dev, ws, wsb, st);
+    if (e) return fail(3000 + e, std::string("fused launch: ") + cudaGetErrorString(cudaError_t(e)));
+    return 0;
+  });
+}
+
+int tpo_gpu_ff_eval(tpo_gpu_ctx *ctx, const tpo_gpu_graph *h, const tpo_field_params *fpp,
+                    uint64_t seed, uint64_t stream, int32_t with_silu, uint16_t *out_xp,
+                    uint16_t *out_xq, uint8_t *out_qd, uint32_t *omega_out, uint16_t *in_xp,
+                    uint16_t *in_xq) {
+  return guard([&] {
+    Ctx &C = ctx->c;
+    check_cuda(cudaSetDevice(C.device), "cudaSetDevice");
+    const Graph &G = h->g;
+    FieldState &fs = C.field(fpp->p, fpp->q, fpp->omega_base);
+    const uint32_t n_in = uint32_t(G.in_elems);
+    VmProgram p = lower_vm(G.g, 0, n_in);
+    if (p.poisoned) throw Error(ErrCode::PoisonedExponent, "exponent depends on a prior exponentiation");
+    const size_t smem = fs.fc.table_bytes + size_t(n_in + p.region_words) * 4;
+    if (smem > 232448) throw Error(ErrCode::DoesNotFit, "graph exceeds shared memory");
+    TpoVmGraph d = p.desc;
+    d.code_off = 0;
+    cudaStream_t st = C.stream;
+    auto *dcode = static_cast<TpoVmInstr *>(C.code.get(p.code.size() * sizeof(TpoVmInstr) + 1));
+    auto *dg = static_cast<TpoVmGraph *>(C.graphs.get(sizeof(TpoVmGraph)));
+    check_cuda(cudaMemcpyAsync(dcode, p.code.data(), p.code.size() * sizeof(TpoVmInstr),
+                               cudaMemcpyHostToDevice, st), "code");
+    check_cuda(cudaMemcpyAsync(dg, &d, sizeof(d), cudaMemcpyHostToDevice, st), "graph");
+    const size_t n_out = size_t(G.out_elems);
+    auto *dout = static_cast<uint32_t *>(C.out.get((n_out + n_in) * 4 + 4));
+    auto *dstat = static_cast<int *>(C.status.get(16));
+    tpo_ff::EvalArgs a{};
+    a.field = fs.fc;
+    a.tables = static_cast<const uint16_t *>(fs.dev.ptr);
+    a.code = dcode;
+    a.graphs = dg;
+    a.n_in = n_in;
+    a.seed = seed;
+    a.stream = stream;
+    a.with_silu = with_silu;
+    a.out = dout;
+    a.in_dump = dout + n_out;
+    a.status = dstat;
+    check_cuda(cudaError_t(tpo_ff_launch_eval(&a, smem, st)), "eval launch");
+    std::vector<uint32_t> hout(n_out + n_in);
+    int hs[2];
+    check_cuda(cudaMemcpyAsync(hs, dstat, 8, cudaMemcpyDeviceToHost, st), "status");
+    check_cuda(cudaMemcpyAsync(hout.data(), dout, (n_out + n_in) * 4, cudaMemcpyDeviceToHost, st), "out");
+    check_cuda(cudaStreamSynchronize(st), "eval sync");
+    if (omega_out) *omega_out = uint32_t(hs[1]);
+    for (uint32_t e = 0; e < n_in; ++e) {
+      if (in_xp) in_xp[e] = uint16_t(hout[n_out + e] & 0xffff);
+      if (in_xq) in_xq[e] = uint16_t(hout[n_out + e] >> 16);
+    }
+    if (hs[0]) return 2000 + int(hs[0] == 2 ? ErrCode::NonResidue : ErrCode::DivByZero);
+    size_t c = 0;
+    for (uint32_t t = 0; t < p.desc.n_out; ++t)
+      for (uint32_t i = 0; i < p.desc.out_len[t]; ++i, ++c) {
+        out_xp[c] = uint16_t(hout[c] & 0xffff);
+        out_xq[c] = uint16_t(hout[c] >> 16);
+        out_qd[c] = p.desc.out_qd[t];
+      }
+    return 0;
+  });
+}
+
+int tpo_gpu_verify_batch(tpo_gpu_ctx *ctx, const tpo_gpu_graph *program,
+                         const tpo_gpu_graph *const *cands, const uint64_t *seeds, uint64_t n,
+                         const tpo_verify_cfg *cfg, const tpo_field_params *fp,
+                         tpo_verdict *verdicts, uint32_t *accept_bits) {
+  return guard([&] {
+    if (n == 0) return 0;
+    std::unordered_map<const tpo_gpu_graph *, uint32_t> idx;
+    std::vector<const Graph *> uniq;
+    std::vector<uint32_t> cg(n);
+    for (uint64_t k = 0; k < n; ++k) {
+      auto it = idx.find(cands[k]);
+      if (it == idx.end()) {
+        it = idx.emplace(cands[k], uint32_t(uniq.size() + 1)).first;
+        uniq.push_back(&cands[k]->g);
+      }
+      cg[k] = it->second;
+    }
+    Batch bt = build_batch(program->g, uniq);
+    VerifyRun r;
+    r.cand_graph = &cg;
+    r.seeds = seeds;
+    r.n = n;
+    r.verdicts_host = verdicts;
+    r.accept_host = accept_bits;
+    run_verify(ctx->c, bt, *cfg, *fp, r);
+    return 0;
+  });
+}
+
+int tpo_gpu_random_test_equivalence(tpo_gpu_ctx *ctx, const tpo_gpu_graph *g1,
+                                    const tpo_gpu_graph *g2, const tpo_verify_cfg *cfg,
+                                    const tpo_field_params *fp, tpo_verdict *out) {
+  return guard([&] {
+    check_pair(g1->g.g, g2->g.g);  // throws ShapeMismatch before sampling, like equiv.cpp:38-49
+    uint64_t seed = cfg->seed;
+    const tpo_gpu_graph *c = g2;
+    int rc = tpo_gpu_verify_batch(ctx, g1, &c, &seed, 1, cfg, fp, out, nullptr);
+    if (rc) return rc;
+    if (out->kind == 3) return out->err_code;
+    return 0;
+  });
+}
+
+int tpo_gpu_verify_pool(tpo_gpu_ctx *ctx, const tpo_gpu_graph *program,
+                        const tpo_gpu_graph *const *pool, int32_t pool_n, uint64_t first,
+                        uint64_t n, const tpo_verify_cfg *cfg, const tpo_field_params *fp,
+                        uint32_t *accept_dev, tpo_verdict *verdicts, uint64_t *attempts,
+                        void *cuda_stream) {
+  return guard([&] {
+    if (n == 0) return 0;
+    if (pool_n < 1) throw Error(ErrCode::ConfigError, "empty pool");
+    std::unordered_map<const tpo_gpu_graph *, uint32_t> idx;
+    std::vector<const Graph *> uniq;
+    std::vector<uint32_t> pg(static_cast<size_t>(pool_n));
+    for (int32_t k = 0; k < pool_n; ++k) {
+      auto it = idx.find(pool[k]);
+      if (it == idx.end()) {
+        it = idx.emplace(pool[k], uint32_t(uniq.size() + 1)).first;
+        uniq.push_back(&pool[k]->g);
+      }
+      pg[size_t(k)] = it->second;
+    }
+    Batch bt = build_batch(program->g, uniq);
+    VerifyRun r;
+    r.pool_host = pg.data();
+    r.pool_n = uint32_t(pool_n);
+    r.first = first;
+    r.n = n;
+    r.verdicts_host = verdicts;
+    r.accept_dev = accept_dev;
+    r.attempts = attempts;
+    r.stream = static_cast<cudaStream_t>(cuda_stream);
+    run_verify(ctx->c, bt, *cfg, *fp, r);
+    return 0;
+  });
+}
+
+}  // extern "C"

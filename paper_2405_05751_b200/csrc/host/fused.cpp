@@ -1,0 +1,275 @@
+// B200 backend — benchmark µGraph recognition and fused-kernel launch.
+//
+// A KernelGraph is lowered to a hand-written fused kernel when it is,
+// structurally, one of the benchmark µGraphs of SURVEY §8d (any shapes, any
+// grid / for-loop schedule): the graph is rebuilt from its own input shapes
+// with the fixture builders below and compared by canonical_key (the
+// reference's structural identity, graph.cpp:128-157).  The kernel computes
+// the same block-graph function; the µGraph's (grid, forloop) schedule is
+// re-tiled for B200 (see fused_skinny.cu / fused_gqa.cu headers).
+#include "fused.hpp"
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+
+#include "../../../include/tpo_gpu.h"
+#include "../kernels/fused.cuh"
+#include "tpo/ir/graph.hpp"
+
+namespace tpo::gpu {
+
+using namespace ir;
+
+namespace {
+
+const DimMap PHI1({kReplica});
+DimMap dm(std::vector<int> v) { return DimMap(std::move(v)); }
+
+// ---- fixture builders (C++ mirror of paper_2405_05751_b200/fixtures.py) ----
+
+KernelGraph rmsnorm_mugraph(int64_t b, int64_t h, int64_t n, int64_t grid, int64_t fl) {
+  GraphBuilder gb;
+  TensorId X = gb.input({b, h}), G = gb.input({1, h}), W = gb.input({h, n}), D = gb.input({1, 1});
+  BlockBuilder bb({grid, 1, 1}, fl, {{b, h}, {1, h}, {h, n}, {1, 1}});
+  TensorId xb = bb.initer(0, PHI1, dm({1}));
+  TensorId gbar = bb.initer(1, PHI1, dm({1}));
+  TensorId wb = bb.initer(2, dm({1}), dm({0}));
+  TensorId db = bb.initer(3, PHI1, PHI1);
+  TensorId xg = bb.op(OpType::EwMul, {xb, gbar});
+  TensorId B = bb.op(OpType::Accum, {bb.op(OpType::Matmul, {xg, wb})}, AccumAttrs{PHI1});
+  TensorId ss = bb.op(OpType::Sum, {bb.op(OpType::Sqr, {xb})}, SumAttrs{1, h / fl});
+  TensorId A = bb.op(OpType::Accum, {bb.op(OpType::EwMul, {ss, db})}, AccumAttrs{PHI1});
+  bb.outsaver(bb.op(OpType::EwDiv, {B, bb.op(OpType::Sqrt, {A})}), dm({1}));
+  TensorId o = gb.graphdef({X, G, W, D}, bb.finish(), bb.out_shapes());
+  return gb.finish({o});
+}
+
+KernelGraph gatedmlp_mugraph(int64_t b, int64_t h, int64_t n, int64_t grid, int64_t fl) {
+  GraphBuilder gb;
+  TensorId X = gb.input({b, h}), W1 = gb.input({h, n}), W3 = gb.input({h, n});
+  BlockBuilder bb({grid, 1, 1}, fl, {{b, h}, {h, n}, {h, n}});
+  TensorId xb = bb.initer(0, PHI1, dm({1}));
+  TensorId w1 = bb.initer(1, dm({1}), dm({0}));
+  TensorId w3 = bb.initer(2, dm({1}), dm({0}));
+  TensorId A1 = bb.op(OpType::Accum, {bb.op(OpType::Matmul, {xb, w1})}, AccumAttrs{PHI1});
+  TensorId A3 = bb.op(OpType::Accum, {bb.op(OpType::Matmul, {xb, w3})}, AccumAttrs{PHI1});
+  bb.outsaver(bb.op(OpType::EwMul, {bb.op(OpType::SiLU, {A1}), A3}), dm({1}));
+  TensorId o = gb.graphdef({X, W1, W3}, bb.finish(), bb.out_shapes());
+  return gb.finish({o});
+}
+
+KernelGraph gqa_mugraph(int64_t g, int64_t qh, int64_t hd, int64_t L, int64_t grid, int64_t fl) {
+  GraphBuilder gb;
+  TensorId Q = gb.input({g, qh, hd}), K = gb.input({g, hd, L}), V = gb.input({g, L, hd});
+  BlockBuilder bb({grid, 1, 1}, fl, {{g, qh, hd}, {g, hd, L}, {g, L, hd}});
+  TensorId qb = bb.initer(0, dm({0}), PHI1);
+  TensorId kb = bb.initer(1, dm({0}), dm({2}));
+  TensorId vb = bb.initer(2, dm({0}), dm({1}));
+  TensorId e = bb.op(OpType::EwExp, {bb.op(OpType::Matmul, {qb, kb})});
+  TensorId N = bb.op(OpType::Accum, {bb.op(OpType::Matmul, {e, vb})}, AccumAttrs{PHI1});
+  TensorId D = bb.op(OpType::Accum, {bb.op(OpType::Sum, {e}, SumAttrs{2, L / fl})}, AccumAttrs{PHI1});
+  bb.outsaver(bb.op(OpType::EwDiv, {N, D}), dm({0}));
+  TensorId o = gb.graphdef({Q, K, V}, bb.finish(), bb.out_shapes());
+  return gb.finish({o});
+}
+
+KernelGraph lora_mugraph(int64_t b, int64_t h, int64_t n, int64_t r, int64_t grid, int64_t fl) {
+  GraphBuilder gb;
+  TensorId X = gb.input({b, h}), W = gb.input({h, n}), A = gb.input({h, r}), B = gb.input({r, n});
+  BlockBuilder bb({grid, 1, 1}, fl, {{b, h}, {h, n}, {h, r}, {r, n}});
+  TensorId xb = bb.initer(0, PHI1, dm({1}));
+  TensorId wb = bb.initer(1, dm({1}), dm({0}));
+  TensorId ab = bb.initer(2, PHI1, dm({0}));
+  TensorId bbar = bb.initer(3, dm({1}), dm({0}));
+  TensorId XW = bb.op(OpType::Accum, {bb.op(OpType::Matmul, {xb, wb})}, AccumAttrs{PHI1});
+  TensorId XA = bb.op(OpType::Accum, {bb.op(OpType::Matmul, {xb, ab})}, AccumAttrs{PHI1});
+  TensorId Bc = bb.op(OpType::Accum, {bbar}, AccumAttrs{dm({0})});
+  bb.outsaver(bb.op(OpType::EwAdd, {XW, bb.op(OpType::Matmul, {XA, Bc})}), dm({1}));
+  TensorId o = gb.graphdef({X, W, A, B}, bb.finish(), bb.out_shapes());
+  return gb.finish({o});
+}
+
+template <class F>
+bool same(const KernelGraph &g, F &&build) {
+  try {
+    return canonical_key(g) == canonical_key(build());
+  } catch (const Error &) {
+    return false;
+  }
+}
+
+int env_int(const char *name, int dflt) {
+  const char *v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+
+// K split (cluster size) for the skinny kernels: enough CTAs to keep every
+// SM streaming weights, K per CTA a multiple of 64.
+int pick_ksplit(int64_t ntiles, int64_t K, int max_split) {
+  int forced = env_int("TPO_KSPLIT", 0);
+  if (forced > 0) return forced;
+  int best = 1;
+  for (int s = 1; s <= max_split; s *= 2) {
+    if (K % (64 * s)) break;
+    if (ntiles * s <= 2 * 148) best = s;
+  }
+  return best;
+}
+
+}  // namespace
+
+FusedPlan match_fused(const KernelGraph &g) {
+  FusedPlan p;
+  if (g.ops.size() != 1 || g.ops[0].type != OpType::GraphDef || !g.ops[0].block ||
+      g.outputs.size() != 1) {
+    p.why = "not a single-GraphDef µGraph";
+    return p;
+  }
+  const BlockGraph &bg = *g.ops[0].block;
+  const int64_t grid = bg.grid[0], fl = bg.forloop;
+  std::vector<TensorShape> in;
+  for (TensorId t : g.inputs) in.push_back(g.tensor(t).shape);
+  auto r2 = [&](size_t i) { return in[i].rank() == 2; };
+  if (in.size() == 4 && r2(0) && r2(1) && r2(2) && r2(3) && in[1].dims[0] == 1 &&
+      in[3].dims == std::vector<int64_t>{1, 1}) {
+    int64_t b = in[0].dims[0], h = in[0].dims[1], n = in[2].dims[1];
+    if (same(g, [&] { return rmsnorm_mugraph(b, h, n, grid, fl); })) {
+      if (b > 8 || n % 128 || h % 64) {
+        p.why = "RMSNorm µGraph outside kernel limits (b<=8, n%128, h%64)";
+        return p;
+      }
+      p.kind = TPO_FUSED_RMSNORM_MATMUL;
+      p.b = b, p.h = h, p.n = n, p.grid = grid, p.forloop = fl;
+      return p;
+    }
+  }
+  if (in.size() == 3 && r2(0) && r2(1) && r2(2)) {
+    int64_t b = in[0].dims[0], h = in[0].dims[1], n = in[1].dims[1];
+    if (same(g, [&] { return gatedmlp_mugraph(b, h, n, grid, fl); })) {
+      if (b > 8 || n % 128 || h % 64) {
+        p.why = "GatedMLP µGraph outside kernel limits (b<=8, n%128, h%64)";
+        return p;
+      }
+      p.kind = TPO_FUSED_GATED_MLP;
+      p.b = b, p.h = h, p.n = n, p.grid = grid, p.forloop = fl;
+      return p;
+    }
+  }
+  if (in.size() == 3 && in[0].rank() == 3 && in[1].rank() == 3 && in[2].rank() == 3) {
+    int64_t G = in[0].dims[0], qh = in[0].dims[1], hd = in[0].dims[2], L = in[1].dims[2];
+    if (same(g, [&] { return gqa_mugraph(G, qh, hd, L, grid, fl); })) {
+      if (qh > 8 || hd != 128 || L % 128) {
+        p.why = "GQA µGraph outside kernel limits (qh<=8, hd==128, L%128)";
+        return p;
+      }
+      p.kind = TPO_FUSED_GQA_DECODE;
+      p.groups = G, p.qh = qh, p.hd = hd, p.L = L, p.grid = grid, p.forloop = fl;
+      return p;
+    }
+  }
+  if (in.size() == 4 && r2(0) && r2(1) && r2(2) && r2(3)) {
+    int64_t b = in[0].dims[0], h = in[0].dims[1], n = in[1].dims[1], r = in[2].dims[1];
+    if (same(g, [&] { return lora_mugraph(b, h, n, r, grid, fl); })) {
+      if (b > 16 || r != 16 || n % 128 || h % 64) {
+        p.why = "LoRA µGraph outside kernel limits (b<=16, r==16, n%128, h%64)";
+        return p;
+      }
+      p.kind = TPO_FUSED_LORA;
+      p.b = b, p.h = h, p.n = n, p.r = r, p.grid = grid, p.forloop = fl;
+      return p;
+    }
+  }
+  p.why = "µGraph does not match a benchmark kernel structurally";
+  return p;
+}
+
+size_t fused_workspace_bytes(const FusedPlan &) { return 0; }
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  return fn;
+}
+
+// 2-D bf16 tensor map: rows x cols row-major, box (box_cols x box_rows).
+bool tmap_2d(CUtensorMap *m, const void *ptr, uint64_t rows, uint64_t cols, uint32_t box_cols,
+             uint32_t box_rows, CUtensorMapSwizzle sw) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides,
+                  box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+int launch_fused(const FusedPlan &p, const void *const *in, const int32_t *dt, float *const *out,
+                 void *, size_t, cudaStream_t st) {
+  const int n_in = (p.kind == TPO_FUSED_GATED_MLP || p.kind == TPO_FUSED_GQA_DECODE) ? 3 : 4;
+  for (int i = 0; i < n_in; ++i)
+    if (dt[i] != TPO_DTYPE_BF16) return int(cudaErrorNotSupported);
+  CUtensorMap maps[4];
+  std::memset(maps, 0, sizeof(maps));
+  SkinnyParams sp{};
+  int mode = 0, stages = 0;
+  if (p.kind == TPO_FUSED_GATED_MLP) {
+    mode = MODE_GATED;
+    const int64_t nt = p.n / 128;
+    sp.ksplit = pick_ksplit(nt, p.h, 8);
+    stages = env_int("TPO_STAGES", 4);
+    if (!tmap_2d(&maps[0], in[1], p.h, p.n, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_2d(&maps[1], in[2], p.h, p.n, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_2d(&maps[2], in[0], p.b, p.h, 64, 16, CU_TENSOR_MAP_SWIZZLE_128B))
+      return int(cudaErrorInvalidValue);
+    maps[3] = maps[2];
+  } else if (p.kind == TPO_FUSED_RMSNORM_MATMUL) {
+    mode = MODE_RMS;
+    sp.ksplit = pick_ksplit(p.n / 128, p.h, 8);
+    stages = env_int("TPO_STAGES", 6);
+    if (!tmap_2d(&maps[0], in[2], p.h, p.n, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B))
+      return int(cudaErrorInvalidValue);
+    maps[1] = maps[2] = maps[3] = maps[0];
+    sp.x = static_cast<const __nv_bfloat16 *>(in[0]);
+    sp.g = static_cast<const __nv_bfloat16 *>(in[1]);
+    sp.dscale = static_cast<const __nv_bfloat16 *>(in[3]);
+  } else if (p.kind == TPO_FUSED_LORA) {
+    mode = MODE_LORA;
+    sp.ksplit = pick_ksplit(p.n / 128, p.h, 8);
+    stages = env_int("TPO_STAGES", 6);
+    if (!tmap_2d(&maps[0], in[1], p.h, p.n, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_2d(&maps[2], in[0], p.b, p.h, 64, 16, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_2d(&maps[3], in[2], p.h, p.r, 16, 64, CU_TENSOR_MAP_SWIZZLE_NONE))
+      return int(cudaErrorInvalidValue);
+    maps[1] = maps[0];
+    sp.lora_b = static_cast<const __nv_bfloat16 *>(in[3]);
+  } else {
+    return int(cudaErrorNotSupported);
+  }
+  sp.N = int(p.n);
+  sp.K = int(p.h);
+  sp.tokens = int(p.b);
+  sp.k_per_cta = int(p.h / sp.ksplit);
+  sp.out = out[0];
+  return tpo_skinny_launch(mode, stages, maps, &sp, st);
+}
+
+}  // namespace tpo::gpu

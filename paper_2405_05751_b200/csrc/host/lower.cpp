@@ -1,0 +1,719 @@
+// B200 backend — µGraph -> block-batched VM bytecode.
+//
+// Semantics follow the reference evaluator (eval_core.hpp:81-376) op for op:
+//   * kernel ops in list order (:91-100); GraphDef outputs zero-initialised
+//     (:229-231);
+//   * block graph: post-loop set = Accum outputs and their descendants
+//     (:277-294); accumulators zeroed (:296-301); loop body = InIter loads,
+//     Accum updates and non-post ops in list order (:303-341); then post ops
+//     and OutSavers in list order (:348-375);
+//   * InIter tile offsets (load_tile, :244-270), OutSaver offsets (:350-366),
+//     concat Accum slices (:321-333).
+// The only structural change is that all grid blocks run as one batch
+// dimension (see kernels/vm.h); results are identical because blocks never
+// read each other's state and the last-writer rule is encoded in `wmask`.
+#include "lower.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+
+#include "tpo/ir/shape_infer.hpp"
+
+namespace tpo::gpu {
+
+using namespace ir;
+
+namespace {
+
+std::vector<int64_t> contiguous(const std::vector<int64_t> &d) {
+  std::vector<int64_t> s(d.size(), 1);
+  for (int i = int(d.size()) - 2; i >= 0; --i) s[size_t(i)] = s[size_t(i + 1)] * d[size_t(i + 1)];
+  return s;
+}
+
+int64_t numel(const TensorShape &s) { return s.elem_count(); }
+
+// Right-aligned broadcast strides of `shape` (contiguous buffer) inside an
+// index space whose trailing dims are `out` (rank R).
+std::vector<int64_t> bcast_strides(const TensorShape &shape, const std::vector<int64_t> &out) {
+  auto cs = contiguous(shape.dims);
+  std::vector<int64_t> st(out.size(), 0);
+  int shift = int(out.size()) - shape.rank();
+  for (int i = 0; i < shape.rank(); ++i)
+    if (shape.dims[size_t(i)] != 1) st[size_t(i + shift)] = cs[size_t(i)];
+  return st;
+}
+
+struct View {
+  std::vector<int64_t> dims;               // index space
+  std::vector<std::vector<int64_t>> st;    // per operand (dst first)
+  std::vector<char> wm;                    // per dim write-mask bit
+};
+
+// Drop unit dims and merge dims that are jointly contiguous for all operands.
+void collapse(View &v) {
+  View o;
+  o.st.resize(v.st.size());
+  for (size_t k = 0; k < v.dims.size(); ++k) {
+    if (v.dims[k] == 1) continue;
+    bool merge = !o.dims.empty() && !v.wm[k] && !o.wm.back();
+    if (merge)
+      for (size_t p = 0; p < v.st.size(); ++p)
+        if (o.st[p].back() != v.st[p][k] * v.dims[k]) merge = false;
+    if (merge) {
+      o.dims.back() *= v.dims[k];
+      for (size_t p = 0; p < v.st.size(); ++p) o.st[p].back() = v.st[p][k];
+    } else {
+      o.dims.push_back(v.dims[k]);
+      o.wm.push_back(v.wm[k]);
+      for (size_t p = 0; p < v.st.size(); ++p) o.st[p].push_back(v.st[p][k]);
+    }
+  }
+  v = std::move(o);
+}
+
+int32_t i32(int64_t x) {
+  if (x > INT32_MAX || x < INT32_MIN) throw Error(ErrCode::DoesNotFit, "VM stride overflow");
+  return int32_t(x);
+}
+
+TpoVmInstr make(uint8_t op, uint8_t sub, View v, uint32_t dst, uint32_t a, uint32_t b) {
+  collapse(v);
+  if (v.dims.size() > TPO_VM_DIMS) throw Error(ErrCode::Unsupported, "VM index rank > 7");
+  TpoVmInstr in;
+  std::memset(&in, 0, sizeof(in));
+  in.op = op;
+  in.sub = sub;
+  in.dst = dst;
+  in.a = a;
+  in.b = b;
+  in.ndim = uint8_t(v.dims.size());
+  int64_t n = 1;
+  bool flat = true;
+  for (size_t k = 0; k < v.dims.size(); ++k) {
+    n *= v.dims[k];
+    in.dims[k] = uint32_t(v.dims[k]);
+    in.sd[k] = i32(v.st[0][k]);
+    if (v.st.size() > 1) in.sa[k] = i32(v.st[1][k]);
+    if (v.st.size() > 2) in.sb[k] = i32(v.st[2][k]);
+    if (v.wm[k]) in.wmask |= uint8_t(1u << k);
+    for (auto &s : v.st)
+      if (s[k] != 1) flat = false;
+  }
+  if (v.dims.size() > 1 || in.wmask) flat = false;
+  if (n > INT32_MAX) throw Error(ErrCode::DoesNotFit, "VM index space too large");
+  in.n = uint32_t(n);
+  if (flat) in.flags |= VM_FLAT;
+  return in;
+}
+
+class Lowerer {
+ public:
+  Lowerer(const KernelGraph &g, uint32_t in_base, uint32_t region, bool pin)
+      : g_(g), region_(region), pin_(pin) {
+    kbuf_.assign(g.tensors.size(), UINT32_MAX);
+    kqd_.assign(g.tensors.size(), 1);
+    uint32_t off = in_base;
+    for (TensorId t : g.inputs) {
+      if (kbuf_[size_t(t)] == UINT32_MAX) {
+        kbuf_[size_t(t)] = off;
+        off += uint32_t(numel(g.tensor(t).shape));
+      }
+      p_.in_shapes.push_back(g.tensor(t).shape);
+    }
+  }
+
+  VmProgram run() {
+    for (const Op &op : g_.ops) {
+      if (op.type == OpType::GraphDef) {
+        graphdef(op);
+        continue;
+      }
+      std::vector<uint32_t> ins;
+      std::vector<TensorShape> shapes;
+      std::vector<uint8_t> qds;
+      for (TensorId t : op.inputs) {
+        ins.push_back(buf(t));
+        shapes.push_back(g_.tensor(t).shape);
+        qds.push_back(kqd_[size_t(t)]);
+      }
+      const TensorId out = op.outputs.at(0);
+      kbuf_[size_t(out)] = alloc(numel(g_.tensor(out).shape));
+      kqd_[size_t(out)] = compute(op, ins, shapes, qds, std::vector<uint8_t>(ins.size(), 1),
+                                  kbuf_[size_t(out)], g_.tensor(out).shape, {1, 1, 1});
+    }
+    if (g_.outputs.size() > TPO_VM_MAX_OUTPUTS) throw Error(ErrCode::Unsupported, "too many outputs");
+    p_.desc.n_out = uint32_t(g_.outputs.size());
+    for (size_t i = 0; i < g_.outputs.size(); ++i) {
+      TensorId t = g_.outputs[i];
+      p_.desc.out_off[i] = buf(t);
+      p_.desc.out_len[i] = uint32_t(numel(g_.tensor(t).shape));
+      p_.desc.out_qd[i] = kqd_[size_t(t)];
+      p_.out_shapes.push_back(g_.tensor(t).shape);
+    }
+    plan_memory();
+    p_.desc.words = p_.region_words;
+    p_.desc.code_len = uint32_t(p_.code.size());
+    p_.desc.poisoned = p_.poisoned;
+    p_.desc.has_silu = p_.has_silu;
+    p_.madds = graph_madds(g_);
+    return std::move(p_);
+  }
+
+ private:
+  const KernelGraph &g_;
+  uint32_t region_;
+  bool pin_;
+  static constexpr uint32_t kVirt = 0x80000000u;  // virtual buffer id tag
+  std::vector<int64_t> vsize_;                    // words per virtual buffer
+  std::vector<uint32_t> kbuf_;
+  std::vector<uint8_t> kqd_;
+  VmProgram p_;
+
+  // Buffers are virtual until plan_memory() assigns addresses.
+  uint32_t alloc(int64_t words) {
+    if (words > int64_t(INT32_MAX / 2)) throw Error(ErrCode::DoesNotFit, "VM buffer too large");
+    vsize_.push_back(words);
+    return kVirt | uint32_t(vsize_.size() - 1);
+  }
+
+  // Liveness-based placement (the role of the reference's absent memplan,
+  // SPEC.md:527-545): interval [first use, last use] over the instruction
+  // stream, widened to the whole loop body for buffers touched inside the
+  // for-loop; graph outputs live to the end (or are pinned at the region
+  // start when `pin_`, so a later program may reuse the scratch above them).
+  // First-fit placement; a buffer may reuse space only after the previous
+  // occupant's last use (strictly earlier instruction).
+  void plan_memory() {
+    const size_t nv = vsize_.size(), nc = p_.code.size();
+    std::vector<int64_t> lo(nv, INT64_MAX), hi(nv, -1);
+    std::vector<std::pair<size_t, size_t>> loops;
+    size_t lb = 0;
+    for (size_t k = 0; k < nc; ++k) {
+      if (p_.code[k].op == VM_LOOP) lb = k;
+      if (p_.code[k].op == VM_ENDLOOP) loops.emplace_back(lb, k);
+    }
+    auto touch = [&](uint32_t b, size_t k) {
+      if (!(b & kVirt)) return;
+      uint32_t v = b & ~kVirt;
+      lo[v] = std::min<int64_t>(lo[v], int64_t(k));
+      hi[v] = std::max<int64_t>(hi[v], int64_t(k));
+    };
+    for (size_t k = 0; k < nc; ++k) {
+      const TpoVmInstr &I = p_.code[k];
+      if (I.op == VM_LOOP || I.op == VM_ENDLOOP) continue;
+      touch(I.dst, k);
+      if (I.op != VM_ZERO) touch(I.a, k);
+      if (I.op == VM_BINARY || I.op == VM_MATMUL) touch(I.b, k);
+    }
+    for (size_t v = 0; v < nv; ++v)
+      for (auto [a, b] : loops)
+        if (hi[v] >= int64_t(a) && lo[v] <= int64_t(b)) {
+          lo[v] = std::min<int64_t>(lo[v], int64_t(a));
+          hi[v] = std::max<int64_t>(hi[v], int64_t(b));
+        }
+    std::vector<int64_t> addr(nv, -1);
+    int64_t pinned = 0;
+    for (uint32_t i = 0; i < p_.desc.n_out; ++i) {
+      uint32_t b = p_.desc.out_off[i];
+      if (!(b & kVirt)) continue;
+      uint32_t v = b & ~kVirt;
+      hi[v] = int64_t(nc);
+      if (pin_ && addr[v] < 0) {
+        addr[v] = region_ + pinned;
+        pinned += vsize_[v];
+      }
+    }
+    std::vector<size_t> order;
+    for (size_t v = 0; v < nv; ++v)
+      if (addr[v] < 0 && hi[v] >= 0) order.push_back(v);
+    std::sort(order.begin(), order.end(), [&](size_t a, size_t b) { return lo[a] < lo[b]; });
+    struct Live {
+      int64_t off, size, end;
+    };
+    std::vector<Live> live;
+    const int64_t base = int64_t(region_) + pinned;
+    int64_t peak = base;
+    for (size_t v : order) {
+      live.erase(std::remove_if(live.begin(), live.end(), [&](const Live &l) { return l.end < lo[v]; }),
+                 live.end());
+      std::sort(live.begin(), live.end(), [](const Live &a, const Live &b) { return a.off < b.off; });
+      int64_t at = base;
+      for (const Live &l : live) {
+        if (at + vsize_[v] <= l.off) break;
+        at = std::max(at, l.off + l.size);
+      }
+      addr[v] = at;
+      live.push_back({at, vsize_[v], hi[v]});
+      peak = std::max(peak, at + vsize_[v]);
+    }
+    for (size_t v = 0; v < nv; ++v) {
+      if (addr[v] < 0) addr[v] = base;  // never referenced
+      if (addr[v] + vsize_[v] > int64_t(INT32_MAX)) throw Error(ErrCode::DoesNotFit, "VM region overflow");
+    }
+    auto fix = [&](uint32_t &b) {
+      if (b & kVirt) b = uint32_t(addr[b & ~kVirt]);
+    };
+    for (TpoVmInstr &I : p_.code) {
+      if (I.op == VM_LOOP || I.op == VM_ENDLOOP) continue;
+      fix(I.dst);
+      if (I.op != VM_ZERO) fix(I.a);
+      if (I.op == VM_BINARY || I.op == VM_MATMUL) fix(I.b);
+    }
+    for (uint32_t i = 0; i < p_.desc.n_out; ++i) fix(p_.desc.out_off[i]);
+    p_.pinned_words = uint32_t(pinned);
+    p_.region_words = uint32_t(std::max(peak, base) - region_);
+  }
+
+  uint32_t buf(TensorId t) {
+    if (kbuf_[size_t(t)] == UINT32_MAX)
+      throw Error(ErrCode::ShapeMismatch, "tensor " + std::to_string(t) + " used before defined");
+    return kbuf_[size_t(t)];
+  }
+
+  void emit(TpoVmInstr in) { p_.code.push_back(in); }
+
+  // Grid dims (bx, by, bz) and the strides of a block tensor of E elements.
+  // Block-invariant tensors (identical in every block) are stored once:
+  // their grid strides are 0.
+  static void grid_part(const std::array<int64_t, 3> &G, int64_t E, bool inv,
+                        std::vector<int64_t> &dims, std::vector<int64_t> &st) {
+    dims = {G[0], G[1], G[2]};
+    if (inv)
+      st = {0, 0, 0};
+    else
+      st = {G[1] * G[2] * E, G[2] * E, E};
+  }
+
+  static std::vector<int64_t> cat(std::vector<int64_t> a, const std::vector<int64_t> &b) {
+    a.insert(a.end(), b.begin(), b.end());
+    return a;
+  }
+
+  void emit_matmul(uint32_t d, uint32_t a, uint32_t b, const TensorShape &sa, const TensorShape &sb,
+                   int64_t nb, bool inv_a, bool inv_b, uint8_t q) {
+    const int r = sa.rank();
+    const int64_t M = sa.dims[size_t(r - 2)], K = sa.dims[size_t(r - 1)], N = sb.dims[size_t(r - 1)];
+    const int64_t Bi = numel(sa) / (M * K);
+    TpoVmInstr i;
+    std::memset(&i, 0, sizeof(i));
+    i.op = VM_MATMUL;
+    i.dst = d;
+    i.a = a;
+    i.b = b;
+    i.ndim = 5;
+    i.dims[0] = uint32_t(nb);
+    i.dims[1] = uint32_t(Bi);
+    i.dims[2] = uint32_t(M);
+    i.dims[3] = uint32_t(K);
+    i.dims[4] = uint32_t(N);
+    i.sd[0] = i32(Bi * M * N);
+    i.sa[0] = inv_a ? 0 : i32(Bi * M * K);
+    i.sb[0] = inv_b ? 0 : i32(Bi * K * N);
+    if (int64_t(nb) * Bi * M * N > INT32_MAX) throw Error(ErrCode::DoesNotFit, "VM matmul too large");
+    i.n = uint32_t(nb * Bi * M * N);
+    i.qd = q;
+    emit(i);
+  }
+
+  // Pre-defined op at kernel level (G = {1,1,1}) or block level (block-
+  // batched).  `inv[k]`: input k is block-invariant; the output is invariant
+  // iff every input is (then it is computed once).  Returns q-definedness.
+  uint8_t compute(const Op &op, const std::vector<uint32_t> &in, const std::vector<TensorShape> &s,
+                  const std::vector<uint8_t> &qd, const std::vector<uint8_t> &inv, uint32_t dst,
+                  const TensorShape &out, const std::array<int64_t, 3> &G) {
+    bool inv_out = true;
+    for (uint8_t x : inv) inv_out = inv_out && x;
+    const std::array<int64_t, 3> Go = inv_out ? std::array<int64_t, 3>{1, 1, 1} : G;
+    const int64_t nb = Go[0] * Go[1] * Go[2];
+    std::vector<int64_t> gd, d_g;
+    grid_part(Go, numel(out), false, gd, d_g);
+    auto flat = [&](uint8_t opc, uint8_t sub, int nops) {
+      View v;
+      v.dims = {nb * numel(out)};
+      v.st.assign(size_t(nops), {1});
+      v.wm = {0};
+      return make(opc, sub, v, dst, in[0], nops > 2 ? in[1] : 0);
+    };
+    auto elementwise2 = [&](uint8_t sub) {
+      View v;
+      std::vector<int64_t> a_g, b_g;
+      grid_part(Go, numel(s[0]), inv[0], gd, a_g);
+      grid_part(Go, numel(s[1]), inv[1], gd, b_g);
+      v.dims = cat(gd, out.dims);
+      v.st = {cat(d_g, contiguous(out.dims)), cat(a_g, bcast_strides(s[0], out.dims)),
+              cat(b_g, bcast_strides(s[1], out.dims))};
+      v.wm.assign(v.dims.size(), 0);
+      TpoVmInstr i = make(VM_BINARY, sub, v, dst, in[0], in[1]);
+      i.qd = qd[0] & qd[1];
+      i.flags |= (qd[0] ? VM_A_QD : 0) | (qd[1] ? VM_B_QD : 0);
+      emit(i);
+      return uint8_t(qd[0] & qd[1]);
+    };
+    auto unary = [&](uint8_t sub) {
+      TpoVmInstr i = flat(VM_UNARY, sub, 2);
+      uint8_t q = sub == VM_EXP ? 0 : qd[0];
+      if (sub == VM_EXP && !qd[0]) p_.poisoned = true;
+      if (sub == VM_SILU) p_.has_silu = true;
+      i.qd = q;
+      i.flags |= qd[0] ? VM_A_QD : 0;
+      emit(i);
+      return q;
+    };
+    switch (op.type) {
+      case OpType::EwAdd:
+        return elementwise2(VM_ADD);
+      case OpType::EwMul:
+        return elementwise2(VM_MUL);
+      case OpType::EwDiv:
+        return elementwise2(VM_DIV);
+      case OpType::EwExp:
+        return unary(VM_EXP);
+      case OpType::Sqr:
+        return unary(VM_SQR);
+      case OpType::Sqrt:
+        return unary(VM_SQRT);
+      case OpType::SiLU:
+        return unary(VM_SILU);
+      case OpType::Matmul: {
+        uint8_t q = qd[0] & qd[1];
+        emit_matmul(dst, in[0], in[1], s[0], s[1], nb, inv[0], inv[1], q);
+        return q;
+      }
+      case OpType::ConcatMatmul: {
+        // W x Y + X x Z (eval_core.hpp:116-122); temporaries share the output's batching
+        uint32_t t1 = alloc(nb * numel(out)), t2 = alloc(nb * numel(out));
+        uint8_t q1 = qd[0] & qd[2], q2 = qd[1] & qd[3];
+        emit_matmul(t1, in[0], in[2], s[0], s[2], nb, inv[0], inv[2], q1);
+        emit_matmul(t2, in[1], in[3], s[1], s[3], nb, inv[1], inv[3], q2);
+        View v;
+        v.dims = {nb * numel(out)};
+        v.st = {{1}, {1}, {1}};
+        v.wm = {0};
+        TpoVmInstr i = make(VM_BINARY, VM_ADD, v, dst, t1, t2);
+        i.qd = q1 & q2;
+        i.flags |= (q1 ? VM_A_QD : 0) | (q2 ? VM_B_QD : 0);
+        emit(i);
+        return q1 & q2;
+      }
+      case OpType::Sum: {
+        const auto &a = std::get<SumAttrs>(op.attrs);
+        int64_t outer = nb, inner = 1;
+        for (int k = 0; k < a.dim; ++k) outer *= s[0].dims[size_t(k)];
+        for (int k = a.dim + 1; k < s[0].rank(); ++k) inner *= s[0].dims[size_t(k)];
+        TpoVmInstr i;
+        std::memset(&i, 0, sizeof(i));
+        i.op = VM_SUM;
+        i.dst = dst;
+        i.a = in[0];
+        i.ndim = 4;
+        i.dims[0] = uint32_t(outer);
+        i.dims[1] = uint32_t(s[0].dims[size_t(a.dim)] / a.group);
+        i.dims[2] = uint32_t(a.group);
+        i.dims[3] = uint32_t(inner);
+        i.n = uint32_t(outer * i.dims[1] * inner);
+        i.qd = qd[0];
+        emit(i);
+        return qd[0];
+      }
+      case OpType::Repeat: {
+        View v;
+        std::vector<int64_t> a_g;
+        grid_part(Go, numel(s[0]), inv[0], gd, a_g);
+        v.dims = cat(gd, out.dims);
+        v.st = {cat(d_g, contiguous(out.dims)), cat(a_g, bcast_strides(s[0], out.dims))};
+        v.wm.assign(v.dims.size(), 0);
+        TpoVmInstr i = make(VM_COPY, 0, v, dst, in[0], 0);
+        i.qd = qd[0];
+        emit(i);
+        return qd[0];
+      }
+      case OpType::Reshape: {
+        TpoVmInstr i = flat(VM_COPY, 0, 2);
+        i.qd = qd[0];
+        emit(i);
+        return qd[0];
+      }
+      default:
+        throw Error(ErrCode::Unsupported, std::string("VM lowering of ") + op_name(op.type));
+    }
+  }
+
+  void graphdef(const Op &op) {
+    if (!op.block) throw Error(ErrCode::Unsupported, "graphdef without block");
+    const BlockGraph &bg = *op.block;
+    const std::array<int64_t, 3> G = bg.grid;
+    for (int a = 0; a < 3; ++a)
+      if (G[size_t(a)] < 1) throw Error(ErrCode::Unsupported, "grid extent < 1");
+    if (bg.forloop < 1) throw Error(ErrCode::Unsupported, "forloop < 1");
+    const int64_t nb = G[0] * G[1] * G[2];
+
+    // kernel-level outputs, zero-initialised (eval_core.hpp:229-231)
+    for (TensorId t : op.outputs) {
+      kbuf_[size_t(t)] = alloc(numel(g_.tensor(t).shape));
+      kqd_[size_t(t)] = 1;
+      View v;
+      v.dims = {numel(g_.tensor(t).shape)};
+      v.st = {{1}};
+      v.wm = {0};
+      TpoVmInstr z = make(VM_ZERO, 0, v, kbuf_[size_t(t)], 0, 0);
+      z.qd = 1;
+      emit(z);
+    }
+
+    const size_t nt = bg.tensors.size();
+    std::vector<uint32_t> bbuf(nt, UINT32_MAX);
+    std::vector<uint8_t> bqd(nt, 1), binv(nt, 1);
+    std::vector<char> post(nt, 0);
+    for (const Op &b : bg.ops) {  // eval_core.hpp:277-294
+      if (b.type == OpType::Accum) {
+        post[size_t(b.outputs[0])] = 1;
+        continue;
+      }
+      if (b.type == OpType::InIter || b.type == OpType::OutSaver) continue;
+      for (TensorId t : b.inputs)
+        if (post[size_t(t)]) post[size_t(b.outputs[0])] = 1;
+    }
+    auto is_post = [&](const Op &b) {
+      for (TensorId t : b.inputs)
+        if (post[size_t(t)]) return true;
+      return false;
+    };
+    auto bshape = [&](TensorId t) -> const TensorShape & { return bg.tensor(t).shape; };
+    auto bget = [&](TensorId t) {
+      if (bbuf[size_t(t)] == UINT32_MAX)
+        throw Error(ErrCode::ShapeMismatch, "block tensor used before defined");
+      return bbuf[size_t(t)];
+    };
+    auto copies = [&](TensorId t) { return binv[size_t(t)] ? int64_t(1) : nb; };
+
+    // Block invariance (list order = topological order): an InIter whose
+    // imap replicates every grid axis of extent > 1 loads the same tile in
+    // every block; ops / accumulators fed only by invariant values are
+    // invariant.
+    for (const Op &b : bg.ops) {
+      if (b.type == OpType::OutSaver) continue;
+      bool inv = true;
+      if (b.type == OpType::InIter) {
+        const auto &a = std::get<InIterAttrs>(b.attrs);
+        for (int ax = 0; ax < 3; ++ax)
+          if (G[size_t(ax)] > 1 && ax < a.imap.axes() && a.imap.targets[size_t(ax)] != kReplica)
+            inv = false;
+      } else {
+        for (TensorId t : b.inputs) inv = inv && binv[size_t(t)];
+      }
+      for (TensorId t : b.outputs) binv[size_t(t)] = inv;
+    }
+
+    // accumulators: the Accum output buffer is the running state
+    for (const Op &b : bg.ops)
+      if (b.type == OpType::Accum) {
+        TensorId t = b.outputs[0];
+        bbuf[size_t(t)] = alloc(copies(t) * numel(bshape(t)));
+        View v;
+        v.dims = {copies(t) * numel(bshape(t))};
+        v.st = {{1}};
+        v.wm = {0};
+        TpoVmInstr z = make(VM_ZERO, 0, v, bbuf[size_t(t)], 0, 0);
+        z.qd = 1;
+        emit(z);
+      }
+    for (const Op &b : bg.ops)
+      for (TensorId t : b.outputs)
+        if (bbuf[size_t(t)] == UINT32_MAX) bbuf[size_t(t)] = alloc(copies(t) * numel(bshape(t)));
+
+    auto run_compute = [&](const Op &b) {
+      std::vector<uint32_t> ins;
+      std::vector<TensorShape> shapes;
+      std::vector<uint8_t> qds, invs;
+      for (TensorId t : b.inputs) {
+        ins.push_back(bget(t));
+        shapes.push_back(bshape(t));
+        qds.push_back(bqd[size_t(t)]);
+        invs.push_back(binv[size_t(t)]);
+      }
+      TensorId o = b.outputs.at(0);
+      bqd[size_t(o)] = compute(b, ins, shapes, qds, invs, bbuf[size_t(o)], bshape(o), G);
+    };
+
+    // ---- loop body (eval_core.hpp:303-341)
+    {
+      TpoVmInstr L;
+      std::memset(&L, 0, sizeof(L));
+      L.op = VM_LOOP;
+      L.n = uint32_t(bg.forloop);
+      emit(L);
+    }
+    for (const Op &b : bg.ops) {
+      if (b.type == OpType::InIter) {
+        const auto &a = std::get<InIterAttrs>(b.attrs);
+        if (a.operand < 0 || size_t(a.operand) >= op.inputs.size())
+          throw Error(ErrCode::ShapeMismatch, "initer operand range");
+        TensorId src = op.inputs[size_t(a.operand)], o = b.outputs[0];
+        const TensorShape &dev = g_.tensor(src).shape;
+        const TensorShape &tile = bshape(o);
+        if (tile.rank() != dev.rank()) throw Error(ErrCode::ShapeMismatch, "initer rank");
+        const bool inv = binv[size_t(o)];
+        const std::array<int64_t, 3> Go = inv ? std::array<int64_t, 3>{1, 1, 1} : G;
+        auto ds = contiguous(dev.dims);
+        View v;
+        std::vector<int64_t> d_g;
+        grid_part(Go, numel(tile), false, v.dims, d_g);
+        std::vector<int64_t> a_g(3, 0);
+        std::vector<int64_t> part = dev.dims;  // dims after the imap division
+        for (int ax = 0; ax < a.imap.axes() && ax < 3; ++ax) {
+          int t = a.imap.targets[size_t(ax)];
+          if (t == kReplica) continue;
+          if (t < 0 || t >= dev.rank()) throw Error(ErrCode::ShapeMismatch, "imap target");
+          part[size_t(t)] /= G[size_t(ax)];
+          a_g[size_t(ax)] = inv ? 0 : part[size_t(t)] * ds[size_t(t)];
+        }
+        int ft = a.fmap.axes() ? a.fmap.targets[0] : kReplica;
+        int32_t it_step = 0;
+        if (ft != kReplica) {
+          if (ft < 0 || ft >= dev.rank()) throw Error(ErrCode::ShapeMismatch, "fmap target");
+          it_step = i32((part[size_t(ft)] / bg.forloop) * ds[size_t(ft)]);
+        }
+        v.dims = cat(v.dims, tile.dims);
+        v.st = {cat(d_g, contiguous(tile.dims)), cat(a_g, ds)};
+        v.wm.assign(v.dims.size(), 0);
+        TpoVmInstr i = make(VM_COPY, 0, v, bbuf[size_t(o)], buf(src), 0);
+        i.a_iter = it_step;
+        i.qd = kqd_[size_t(src)];
+        bqd[size_t(o)] = i.qd;
+        emit(i);
+        continue;
+      }
+      if (b.type == OpType::Accum) {
+        const auto &a = std::get<AccumAttrs>(b.attrs);
+        TensorId val = b.inputs.at(0), acc = b.outputs[0];
+        const TensorShape &vs = bshape(val);
+        int t = a.fmap.axes() ? a.fmap.targets[0] : kReplica;
+        if (t == kReplica) {
+          View v;
+          v.dims = {copies(val) * numel(vs)};
+          v.st = {{1}, {1}, {1}};
+          v.wm = {0};
+          TpoVmInstr i = make(VM_BINARY, VM_ADD, v, bbuf[size_t(acc)], bbuf[size_t(acc)], bget(val));
+          i.qd = bqd[size_t(val)];
+          i.flags |= VM_A_QD | (bqd[size_t(val)] ? VM_B_QD : 0);
+          emit(i);
+        } else {
+          const TensorShape &as = bshape(acc);
+          const std::array<int64_t, 3> Go =
+              binv[size_t(val)] ? std::array<int64_t, 3>{1, 1, 1} : G;
+          View v;
+          std::vector<int64_t> d_g, a_g;
+          grid_part(Go, numel(as), false, v.dims, d_g);
+          grid_part(Go, numel(vs), false, v.dims, a_g);
+          auto cs_acc = contiguous(as.dims);
+          v.dims = cat(v.dims, vs.dims);
+          v.st = {cat(d_g, cs_acc), cat(a_g, contiguous(vs.dims))};
+          v.wm.assign(v.dims.size(), 0);
+          TpoVmInstr i = make(VM_COPY, 0, v, bbuf[size_t(acc)], bget(val), 0);
+          i.d_iter = i32(vs.dims[size_t(t)] * cs_acc[size_t(t)]);
+          i.qd = bqd[size_t(val)];
+          emit(i);
+        }
+        bqd[size_t(acc)] = bqd[size_t(val)];
+        continue;
+      }
+      if (b.type == OpType::OutSaver || is_post(b)) continue;
+      run_compute(b);
+    }
+    {
+      TpoVmInstr E;
+      std::memset(&E, 0, sizeof(E));
+      E.op = VM_ENDLOOP;
+      emit(E);
+    }
+
+    // ---- post-loop ops and OutSavers (eval_core.hpp:348-375)
+    size_t saver = 0;
+    for (const Op &b : bg.ops) {
+      if (b.type == OpType::OutSaver) {
+        if (saver >= op.outputs.size()) throw Error(ErrCode::ShapeMismatch, "outsaver count");
+        const auto &a = std::get<OutSaverAttrs>(b.attrs);
+        TensorId val = b.inputs.at(0), out = op.outputs[saver++];
+        const TensorShape &vs = bshape(val), &os = g_.tensor(out).shape;
+        if (vs.rank() != os.rank()) throw Error(ErrCode::ShapeMismatch, "outsaver rank");
+        auto ods = contiguous(os.dims);
+        View v;
+        std::vector<int64_t> a_g;
+        grid_part(G, numel(vs), binv[size_t(val)], v.dims, a_g);
+        std::vector<int64_t> d_g(3, 0);
+        v.wm.assign(3, 0);
+        for (int ax = 0; ax < 3; ++ax) {
+          if (ax < a.omap.axes()) {
+            int t = a.omap.targets[size_t(ax)];
+            if (t == kReplica || t < 0 || t >= vs.rank())
+              throw Error(ErrCode::ReplicaInOmap, "omap target");
+            d_g[size_t(ax)] = vs.dims[size_t(t)] * ods[size_t(t)];
+          } else if (G[size_t(ax)] > 1) {
+            v.wm[size_t(ax)] = 1;  // last block along this axis wins
+          }
+        }
+        v.dims = cat(v.dims, vs.dims);
+        v.wm.resize(v.dims.size(), 0);
+        v.st = {cat(d_g, ods), cat(a_g, contiguous(vs.dims))};
+        TpoVmInstr i = make(VM_COPY, 0, v, kbuf_[size_t(out)], bget(val), 0);
+        i.qd = bqd[size_t(val)];
+        kqd_[size_t(out)] = i.qd;
+        emit(i);
+        continue;
+      }
+      if (b.type == OpType::InIter || b.type == OpType::Accum || !is_post(b)) continue;
+      run_compute(b);
+    }
+  }
+};
+
+}  // namespace
+
+VmProgram lower_vm(const KernelGraph &g, uint32_t input_base, uint32_t region_base,
+                   bool pin_outputs) {
+  return Lowerer(g, input_base, region_base, pin_outputs).run();
+}
+
+int64_t input_elems(const KernelGraph &g) {
+  int64_t n = 0;
+  for (TensorId t : g.inputs) n += numel(g.tensor(t).shape);
+  return n;
+}
+
+// Reference work counter (shape_infer.cpp:195-217) summed over the graph,
+// block ops scaled by the grid and, for in-loop ops, the for-loop trip count.
+int64_t graph_madds(const KernelGraph &g) {
+  int64_t total = 0;
+  for (const Op &op : g.ops) {
+    if (op.type != OpType::GraphDef) {
+      std::vector<TensorShape> in;
+      for (TensorId t : op.inputs) in.push_back(g.tensor(t).shape);
+      total += op_madds(op.type, op.attrs, in, g.tensor(op.outputs[0]).shape);
+      continue;
+    }
+    const BlockGraph &bg = *op.block;
+    std::vector<char> post(bg.tensors.size(), 0);
+    for (const Op &b : bg.ops) {
+      if (b.type == OpType::Accum) {
+        post[size_t(b.outputs[0])] = 1;
+        continue;
+      }
+      if (b.type == OpType::InIter || b.type == OpType::OutSaver) continue;
+      for (TensorId t : b.inputs)
+        if (post[size_t(t)]) post[size_t(b.outputs[0])] = 1;
+    }
+    for (const Op &b : bg.ops) {
+      if (b.type == OpType::InIter || b.type == OpType::OutSaver) continue;
+      std::vector<TensorShape> in;
+      for (TensorId t : b.inputs) in.push_back(bg.tensor(t).shape);
+      int64_t m = op_madds(b.type, b.attrs, in, bg.tensor(b.outputs[0]).shape);
+      bool p = b.type != OpType::Accum && post[size_t(b.outputs[0])];
+      total += m * bg.grid_product() * (p ? 1 : bg.forloop);
+    }
+  }
+  return total;
+}
+
+}  // namespace tpo::gpu

@@ -1,0 +1,54 @@
+// B200 backend — host runtime objects behind the C-ABI handles.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../kernels/ff_vm.cuh"
+#include "fused.hpp"
+#include "lower.hpp"
+#include "tpo/ir/graph.hpp"
+
+namespace tpo::gpu {
+
+// Grow-only device buffer.
+struct DevBuf {
+  void *ptr = nullptr;
+  size_t cap = 0;
+  void *get(size_t bytes);
+  ~DevBuf();
+};
+
+struct FieldState {
+  tpo_ff::FieldConst fc{};
+  std::vector<uint16_t> host_tables;  // inv_p, inv_q, sqrt_p, sqrt_q
+  DevBuf dev;
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 0;
+  std::map<uint64_t, std::unique_ptr<FieldState>> fields;
+  DevBuf code, graphs, pool, cand, seeds, verdicts, accept, counter, out, status, inputs, ws;
+  FieldState &field(uint32_t p, uint32_t q, uint32_t wbase);
+};
+
+struct Graph {
+  ir::KernelGraph g;
+  bool lax = true;
+  int64_t madds = 0;
+  int64_t in_elems = 0, out_elems = 0;
+  int64_t vm_words = -1;
+  FusedPlan plan;  // fused_kind == 0 when no hand-written kernel matches
+};
+
+// Throws tpo::Error on failure.
+void check_cuda(cudaError_t e, const char *what);
+
+}  // namespace tpo::gpu

@@ -1,0 +1,552 @@
+// B200 backend — batched Z_p x Z_q µGraph verifier (sm_100a).
+//
+// One CTA evaluates one candidate at a time (persistent CTAs pull candidate
+// indices from an atomic counter).  Per attempt it regenerates the inputs
+// on the fly from the closed form of the reference's splitmix64 stream
+// (rng.hpp:25-63: draw j of Rng::derive(seed, s) is fin(s0 + (j+1)*gamma)),
+// runs the program's and the candidate's VM bytecode (kernels/vm.h) out of
+// shared memory, and compares outputs — reproducing
+// random_test_equivalence (equiv.cpp:34-94) verdict, rounds_run, resamples
+// and witness bit-exactly.
+//
+// Field values are packed one per 32-bit word: xp | xq << 16.  q-definedness
+// is a static per-tensor property (lowering computes it), so the poison bit
+// is not stored; undefined q components are kept canonical (0) exactly as
+// the reference's default-constructed FFValue results (field.cpp:70-126).
+// Matmul and Sum accumulate raw 32-bit products and reduce once per
+// `lazy` terms (products < (p-1)^2).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ff_vm.cuh"
+#include "vm.h"
+
+namespace tpo_ff {
+
+constexpr uint64_t kGamma = 0x9e3779b97f4a7c15ull;
+
+__device__ __forceinline__ uint64_t fin(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+// x mod m for x < 2^32, with magic = floor(2^32 / m) (one correction step).
+__device__ __forceinline__ uint32_t mod32(uint32_t x, uint32_t m, uint32_t magic) {
+  uint32_t r = x - __umulhi(x, magic) * m;
+  return r >= m ? r - m : r;
+}
+
+// r mod n for a 64-bit draw, via 32-bit halves: (hi*2^32 + lo) mod n.
+__device__ __forceinline__ uint32_t mod64(uint64_t r, uint32_t n, uint32_t magic, uint32_t two32) {
+  uint32_t hi = mod32(uint32_t(r >> 32), n, magic);
+  uint32_t lo = mod32(uint32_t(r), n, magic);
+  return mod32(hi * two32 + lo, n, magic);  // hi*two32 < n^2 < 2^32
+}
+
+struct Smem {
+  uint16_t *inv_p, *inv_q, *silu_p, *silu_q, *pow_w;
+  int16_t *sqrt_p, *sqrt_q;
+  uint32_t *w;  // VM words
+};
+
+__device__ __forceinline__ Smem carve(uint8_t *base, const FieldConst &f) {
+  Smem s;
+  uint16_t *u = reinterpret_cast<uint16_t *>(base);
+  s.inv_p = u;
+  s.inv_q = s.inv_p + f.p;
+  s.silu_p = s.inv_q + f.q;
+  s.silu_q = s.silu_p + f.p;
+  s.pow_w = s.silu_q + f.q;
+  s.sqrt_p = reinterpret_cast<int16_t *>(s.pow_w + f.q);
+  s.sqrt_q = s.sqrt_p + f.p;
+  s.w = reinterpret_cast<uint32_t *>(base + f.table_bytes);
+  return s;
+}
+
+__device__ void load_tables(const Smem &s, const FieldConst &f, const uint16_t *g_tables) {
+  // g_tables: inv_p[p], inv_q[q], sqrt_p[p], sqrt_q[q] (sqrt as int16 bits)
+  for (uint32_t i = threadIdx.x; i < f.p; i += blockDim.x) {
+    s.inv_p[i] = g_tables[i];
+    s.sqrt_p[i] = int16_t(g_tables[f.p + f.q + i]);
+  }
+  for (uint32_t i = threadIdx.x; i < f.q; i += blockDim.x) {
+    s.inv_q[i] = g_tables[f.p + i];
+    s.sqrt_q[i] = int16_t(g_tables[2 * f.p + f.q + i]);
+  }
+}
+
+__device__ __forceinline__ uint64_t derive_state(uint64_t seed, uint64_t stream) {
+  // Rng::derive: state = seed ^ gamma*(stream+1), then one discarded draw.
+  return (seed ^ (kGamma * (stream + 1))) + kGamma;
+}
+
+// Sequential fallback used only when some draw hits the (2^64 mod n)
+// rejection zone (~1e-17 per draw): thread 0 replays the reference stream.
+__device__ uint32_t seq_uniform(uint64_t &st, uint32_t n, uint64_t thr, uint32_t magic,
+                                uint32_t two32) {
+  for (;;) {
+    st += kGamma;
+    uint64_t r = fin(st);
+    if (r >= thr) return mod64(r, n, magic, two32);
+  }
+}
+
+// Generate inputs, omega, SiLU tables and the omega power table for one
+// attempt.  Returns omega.  Draw order is sample_inputs (ffeval.cpp:29-40),
+// sample_omega (field.cpp:140-142), SiluTables::sample (ffeval.cpp:20-27).
+__device__ uint32_t gen_attempt(const Smem &s, const FieldConst &f, uint64_t seed, uint64_t stream,
+                                uint32_t n_in, bool silu, int *s_slow, uint32_t *s_omega) {
+  const uint64_t st0 = derive_state(seed, stream);
+  bool slow = false;
+  for (uint32_t e = threadIdx.x; e < n_in; e += blockDim.x) {
+    uint64_t r1 = fin(st0 + (2ull * e + 1) * kGamma);
+    uint64_t r2 = fin(st0 + (2ull * e + 2) * kGamma);
+    slow |= (r1 < f.thr_p) | (r2 < f.thr_q);
+    uint32_t xp = mod64(r1, f.p, f.magic_p, f.two32_p);
+    uint32_t xq = mod64(r2, f.q, f.magic_q, f.two32_q);
+    s.w[e] = xp | (xq << 16);
+  }
+  const uint64_t base = 2ull * n_in;  // next draw index
+  if (silu) {
+    for (uint32_t i = threadIdx.x; i < f.p + f.q; i += blockDim.x) {
+      uint64_t r = fin(st0 + (base + 2 + i) * kGamma);
+      if (i < f.p) {
+        slow |= r < f.thr_p;
+        s.silu_p[i] = uint16_t(mod64(r, f.p, f.magic_p, f.two32_p));
+      } else {
+        slow |= r < f.thr_q;
+        s.silu_q[i - f.p] = uint16_t(mod64(r, f.q, f.magic_q, f.two32_q));
+      }
+    }
+  }
+  if (threadIdx.x == 0) {
+    uint64_t r = fin(st0 + (base + 1) * kGamma);
+    slow |= r < f.thr_q;
+    uint32_t k = mod64(r, f.q, f.magic_q, f.two32_q);
+    uint32_t w = 1, b = f.wbase % f.p;
+    while (k) {
+      if (k & 1) w = mod32(w * b, f.p, f.magic_p);
+      b = mod32(b * b, f.p, f.magic_p);
+      k >>= 1;
+    }
+    *s_omega = w;
+    *s_slow = 0;
+  }
+  __syncthreads();
+  if (slow) atomicOr(s_slow, 1);
+  __syncthreads();
+  if (*s_slow) {
+    if (threadIdx.x == 0) {
+      uint64_t st = st0;
+      for (uint32_t e = 0; e < n_in; ++e) {
+        uint32_t xp = seq_uniform(st, f.p, f.thr_p, f.magic_p, f.two32_p);
+        uint32_t xq = seq_uniform(st, f.q, f.thr_q, f.magic_q, f.two32_q);
+        s.w[e] = xp | (xq << 16);
+      }
+      uint32_t k = seq_uniform(st, f.q, f.thr_q, f.magic_q, f.two32_q);
+      uint32_t w = 1, b = f.wbase % f.p;
+      while (k) {
+        if (k & 1) w = mod32(w * b, f.p, f.magic_p);
+        b = mod32(b * b, f.p, f.magic_p);
+        k >>= 1;
+      }
+      *s_omega = w;
+      if (silu) {
+        for (uint32_t i = 0; i < f.p; ++i)
+          s.silu_p[i] = uint16_t(seq_uniform(st, f.p, f.thr_p, f.magic_p, f.two32_p));
+        for (uint32_t i = 0; i < f.q; ++i)
+          s.silu_q[i] = uint16_t(seq_uniform(st, f.q, f.thr_q, f.magic_q, f.two32_q));
+      }
+    }
+    __syncthreads();
+  }
+  const uint32_t omega = *s_omega;
+  // omega^e mod p for e in [0, q)
+  for (uint32_t e = threadIdx.x; e < f.q; e += blockDim.x) {
+    uint32_t w = 1, b = omega, k = e;
+    while (k) {
+      if (k & 1) w = mod32(w * b, f.p, f.magic_p);
+      b = mod32(b * b, f.p, f.magic_p);
+      k >>= 1;
+    }
+    s.pow_w[e] = uint16_t(w);
+  }
+  __syncthreads();
+  return omega;
+}
+
+__device__ __forceinline__ void offsets(const TpoVmInstr &I, uint32_t idx, int32_t &od, int32_t &oa,
+                                        int32_t &ob, bool &wr) {
+  od = oa = ob = 0;
+  wr = true;
+  for (int k = int(I.ndim) - 1; k >= 0; --k) {
+    uint32_t d = I.dims[k];
+    uint32_t c = idx % d;
+    idx /= d;
+    od += int32_t(c) * I.sd[k];
+    oa += int32_t(c) * I.sa[k];
+    ob += int32_t(c) * I.sb[k];
+    if (((I.wmask >> k) & 1u) && c != d - 1) wr = false;
+  }
+}
+
+// Runs one graph's bytecode. Returns false (uniformly) when an undefined
+// field operation (zero divisor / non-residue) requires a resample.
+__device__ bool run_program(const Smem &s, const FieldConst &f, const TpoVmInstr *code,
+                            uint32_t len, int *s_flag) {
+  uint32_t it = 0, loop_pc = 0, trips = 1;
+  uint32_t *W = s.w;
+  const uint32_t p = f.p, q = f.q, mp = f.magic_p, mq = f.magic_q;
+  for (uint32_t pc = 0; pc < len; ++pc) {
+    const TpoVmInstr &I = code[pc];
+    const uint8_t op = I.op;
+    if (op == VM_LOOP) {
+      trips = I.n;
+      it = 0;
+      loop_pc = pc;
+      continue;
+    }
+    if (op == VM_ENDLOOP) {
+      if (++it < trips) pc = loop_pc;  // loop body restarts at loop_pc + 1
+      continue;
+    }
+    const uint32_t n = I.n;
+    const bool qd = I.qd;
+    const bool flat = I.flags & VM_FLAT;
+    bool bad = false;
+    switch (op) {
+      case VM_ZERO:
+        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) W[I.dst + i] = 0;
+        break;
+      case VM_COPY: {
+        const uint32_t dbase = I.dst + it * I.d_iter, abase = I.a + it * I.a_iter;
+        if (flat) {
+          for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) W[dbase + i] = W[abase + i];
+        } else {
+          for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+            int32_t od, oa, ob;
+            bool wr;
+            offsets(I, i, od, oa, ob, wr);
+            if (wr) W[dbase + od] = W[abase + oa];
+          }
+        }
+        break;
+      }
+      case VM_UNARY: {
+        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+          uint32_t v = W[I.a + i];
+          uint32_t xp = v & 0xffffu, xq = v >> 16, rp = 0, rq = 0;
+          switch (I.sub) {
+            case VM_EXP:
+              rp = s.pow_w[xq];
+              break;
+            case VM_SQR:
+              rp = mod32(xp * xp, p, mp);
+              if (qd) rq = mod32(xq * xq, q, mq);
+              break;
+            case VM_SQRT: {
+              int32_t r = s.sqrt_p[xp];
+              bad |= r < 0;
+              rp = uint32_t(r) & 0xffffu;
+              if (qd) {
+                int32_t r2 = s.sqrt_q[xq];
+                bad |= r2 < 0;
+                rq = uint32_t(r2) & 0xffffu;
+              }
+              break;
+            }
+            case VM_SILU:
+              rp = s.silu_p[xp];
+              if (qd) rq = s.silu_q[xq];
+              break;
+          }
+          W[I.dst + i] = rp | (rq << 16);
+        }
+        break;
+      }
+      case VM_BINARY: {
+        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+          int32_t od = int32_t(i), oa = int32_t(i), ob = int32_t(i);
+          bool wr = true;
+          if (!flat) offsets(I, i, od, oa, ob, wr);
+          uint32_t va = W[I.a + oa], vb = W[I.b + ob];
+          uint32_t ap = va & 0xffffu, aq = va >> 16, bp = vb & 0xffffu, bq = vb >> 16;
+          uint32_t rp, rq = 0;
+          switch (I.sub) {
+            case VM_ADD:
+              rp = ap + bp;
+              rp = rp >= p ? rp - p : rp;
+              if (qd) {
+                rq = aq + bq;
+                rq = rq >= q ? rq - q : rq;
+              }
+              break;
+            case VM_MUL:
+              rp = mod32(ap * bp, p, mp);
+              if (qd) rq = mod32(aq * bq, q, mq);
+              break;
+            default:  // VM_DIV (field.cpp:93-103)
+              bad |= bp == 0;
+              rp = mod32(ap * s.inv_p[bp], p, mp);
+              if (qd) {
+                bad |= bq == 0;
+                rq = mod32(aq * s.inv_q[bq], q, mq);
+              }
+              break;
+          }
+          W[I.dst + od] = rp | (rq << 16);
+        }
+        break;
+      }
+      case VM_MATMUL: {
+        // dims {blocks, batch, M, K, N}; per-operand block strides (0: block-invariant)
+        const uint32_t Bi = I.dims[1], M = I.dims[2], K = I.dims[3], N = I.dims[4];
+        const uint32_t MN = M * N, BMN = Bi * MN;
+        const uint32_t lazy = f.lazy;
+        for (uint32_t o = threadIdx.x; o < n; o += blockDim.x) {
+          uint32_t blk = o / BMN, r = o - blk * BMN, bi = r / MN;
+          r -= bi * MN;
+          uint32_t m = r / N, c = r - m * N;
+          const uint32_t *pa = W + I.a + blk * uint32_t(I.sa[0]) + bi * M * K + m * K;
+          const uint32_t *pb = W + I.b + blk * uint32_t(I.sb[0]) + bi * K * N + c;
+          uint32_t accp = 0, accq = 0, cnt = 0;
+          for (uint32_t k = 0; k < K; ++k) {
+            uint32_t va = pa[k], vb = pb[k * N];
+            accp += (va & 0xffffu) * (vb & 0xffffu);
+            accq += (va >> 16) * (vb >> 16);
+            if (++cnt == lazy) {
+              accp = mod32(accp, p, mp);
+              accq = mod32(accq, q, mq);
+              cnt = 0;
+            }
+          }
+          uint32_t rp = mod32(accp, p, mp), rq = qd ? mod32(accq, q, mq) : 0;
+          W[I.dst + o] = rp | (rq << 16);
+        }
+        break;
+      }
+      case VM_SUM: {
+        const uint32_t mid = I.dims[1], grp = I.dims[2], inner = I.dims[3];
+        const uint32_t lazy = f.lazy_sum;
+        for (uint32_t o = threadIdx.x; o < n; o += blockDim.x) {
+          uint32_t in_i = o % inner, t = o / inner, m = t % mid, ou = t / mid;
+          const uint32_t *pa = W + I.a + (ou * mid * grp + m * grp) * inner + in_i;
+          uint32_t accp = 0, accq = 0, cnt = 0;
+          for (uint32_t g = 0; g < grp; ++g) {
+            uint32_t v = pa[g * inner];
+            accp += v & 0xffffu;
+            accq += v >> 16;
+            if (++cnt == lazy) {
+              accp = mod32(accp, p, mp);
+              accq = mod32(accq, q, mq);
+              cnt = 0;
+            }
+          }
+          uint32_t rp = mod32(accp, p, mp), rq = qd ? mod32(accq, q, mq) : 0;
+          W[I.dst + o] = rp | (rq << 16);
+        }
+        break;
+      }
+      default:
+        break;
+    }
+    if (bad) *s_flag = (op == VM_UNARY) ? 2 : 1;  // NonResidue (sqrt) / DivByZero (div)
+    __syncthreads();
+    if (*s_flag) return false;
+  }
+  return true;
+}
+
+// First mismatching (tensor, flat index) between two graphs' outputs, with
+// FFValue::operator== semantics (field.hpp:41-45): xq compared only when
+// both sides are q-defined.  Returns false if none.
+__device__ bool first_mismatch(const Smem &s, const TpoVmGraph &g1, const TpoVmGraph &g2,
+                               unsigned long long *s_key, int *t_out, int64_t *i_out) {
+  for (uint32_t t = 0; t < g1.n_out; ++t) {
+    if (threadIdx.x == 0) *s_key = ~0ull;
+    __syncthreads();
+    const bool cmp_q = g1.out_qd[t] && g2.out_qd[t];
+    const uint32_t n = g1.out_len[t];
+    const uint32_t *a = s.w + g1.out_off[t], *b = s.w + g2.out_off[t];
+    unsigned long long best = ~0ull;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+      uint32_t x = a[i], y = b[i];
+      bool ne = ((x ^ y) & 0xffffu) || (cmp_q && ((x ^ y) >> 16));
+      if (ne) {
+        best = i;
+        break;  // strided loop: first hit per thread is its minimum
+      }
+    }
+    if (best != ~0ull) atomicMin(s_key, best);
+    __syncthreads();
+    unsigned long long k = *s_key;
+    __syncthreads();
+    if (k != ~0ull) {
+      *t_out = int(t);
+      *i_out = int64_t(k);
+      return true;
+    }
+  }
+  return false;
+}
+
+__global__ void __launch_bounds__(kThreads) verify_kernel(VerifyArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ int s_flag, s_slow;
+  __shared__ uint32_t s_omega;
+  __shared__ unsigned long long s_cand, s_key;
+  const FieldConst &f = a.field;
+  Smem s = carve(smem, f);
+  load_tables(s, f, a.tables);
+  const TpoVmGraph g1 = a.graphs[a.program];
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_cand = atomicAdd(a.counter, 1ull);
+    __syncthreads();
+    const unsigned long long k = s_cand;
+    if (k >= a.n) break;
+    const uint64_t cand = a.first + k;
+    const uint32_t gi = a.cand_graph ? a.cand_graph[k] : a.pool[cand % a.pool_n];
+    const uint64_t seed = a.seeds ? a.seeds[k] : cand;
+    const TpoVmGraph g2 = a.graphs[gi];
+    const bool silu = g1.has_silu || g2.has_silu;
+
+    TpoVerdict v;
+    v.kind = 0;
+    v.rounds_run = 0;
+    v.resamples = 0;
+    v.has_witness = 0;
+    v.w_seed = 0;
+    v.w_round = 0;
+    v.w_omega = 0;
+    v.w_tensor = 0;
+    v.err_code = 0;
+    v.w_index = 0;
+    bool finished = false;
+    if (g1.err || g2.err) {
+      v.kind = 3;  // tpo::Error raised before sampling (shape mismatch, non-Lax, ...)
+      v.err_code = 1000 + int(g1.err ? g1.err : g2.err) - 1;
+      finished = true;
+    }
+    for (int round = 0; round < a.num_tests && !finished; ++round) {
+      bool round_done = false;
+      for (int att = 0; att <= a.max_resamples && !round_done; ++att) {
+        const uint64_t stream = uint64_t(round) * 131071ull + uint64_t(att);
+        const uint32_t omega = gen_attempt(s, f, seed, stream, a.n_in, silu, &s_slow, &s_omega);
+        if (threadIdx.x == 0) s_flag = 0;
+        __syncthreads();
+        bool ok = run_program(s, f, a.code + g1.code_off, g1.code_len, &s_flag) &&
+                  run_program(s, f, a.code + g2.code_off, g2.code_len, &s_flag);
+        if (!ok) {
+          ++v.resamples;
+          continue;
+        }
+        int t;
+        int64_t idx;
+        if (first_mismatch(s, g1, g2, &s_key, &t, &idx)) {
+          v.kind = 1;
+          v.has_witness = 1;
+          v.w_seed = seed;
+          v.w_round = round;
+          v.w_omega = omega;
+          v.w_tensor = t;
+          v.w_index = idx;
+          v.rounds_run = round + 1;
+          finished = true;
+        }
+        round_done = true;
+      }
+      if (!round_done && !finished) {
+        v.kind = 2;
+        v.rounds_run = round;
+        finished = true;
+      }
+    }
+    if (!finished) {
+      v.kind = 0;
+      v.rounds_run = a.num_tests;
+    }
+    if (threadIdx.x == 0) {
+      if (a.verdicts) a.verdicts[k] = v;
+      if (a.accept && v.kind == 0) atomicOr(a.accept + (k >> 5), 1u << (k & 31));
+      if (a.work) atomicAdd(a.work, (unsigned long long)(v.resamples + v.rounds_run));
+    }
+  }
+}
+
+// Debug / parity: evaluate one graph for one (seed, stream) attempt, or on
+// explicit inputs, and dump its outputs.
+__global__ void __launch_bounds__(kThreads) eval_kernel(EvalArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ int s_flag, s_slow;
+  __shared__ uint32_t s_omega;
+  const FieldConst &f = a.field;
+  Smem s = carve(smem, f);
+  load_tables(s, f, a.tables);
+  const TpoVmGraph g = a.graphs[0];
+  uint32_t omega;
+  if (a.inputs) {
+    for (uint32_t e = threadIdx.x; e < a.n_in; e += blockDim.x) s.w[e] = a.inputs[e];
+    if (a.silu_tables) {
+      for (uint32_t i = threadIdx.x; i < f.p; i += blockDim.x) s.silu_p[i] = a.silu_tables[i];
+      for (uint32_t i = threadIdx.x; i < f.q; i += blockDim.x) s.silu_q[i] = a.silu_tables[f.p + i];
+    }
+    omega = a.omega;
+    for (uint32_t e = threadIdx.x; e < f.q; e += blockDim.x) {
+      uint32_t w = 1, b = omega, k = e;
+      while (k) {
+        if (k & 1) w = mod32(w * b, f.p, f.magic_p);
+        b = mod32(b * b, f.p, f.magic_p);
+        k >>= 1;
+      }
+      s.pow_w[e] = uint16_t(w);
+    }
+    __syncthreads();
+  } else {
+    omega = gen_attempt(s, f, a.seed, a.stream, a.n_in, a.with_silu, &s_slow, &s_omega);
+  }
+  if (threadIdx.x == 0) s_flag = 0;
+  __syncthreads();
+  if (a.in_dump)
+    for (uint32_t e = threadIdx.x; e < a.n_in; e += blockDim.x) a.in_dump[e] = s.w[e];
+  bool ok = run_program(s, f, a.code + g.code_off, g.code_len, &s_flag);
+  if (threadIdx.x == 0) {
+    a.status[0] = ok ? 0 : s_flag;
+    a.status[1] = int(omega);
+  }
+  if (!ok) return;
+  uint32_t c = 0;
+  for (uint32_t t = 0; t < g.n_out; ++t) {
+    for (uint32_t i = threadIdx.x; i < g.out_len[t]; i += blockDim.x) a.out[c + i] = s.w[g.out_off[t] + i];
+    c += g.out_len[t];
+  }
+}
+
+}  // namespace tpo_ff
+
+extern "C" int tpo_ff_launch_verify(const tpo_ff::VerifyArgs *a, int grid, size_t smem,
+                                    cudaStream_t st) {
+  static int configured_for = -1;
+  if (int(smem) > configured_for) {
+    cudaFuncSetAttribute(tpo_ff::verify_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem));
+    configured_for = int(smem);
+  }
+  tpo_ff::verify_kernel<<<grid, tpo_ff::kThreads, smem, st>>>(*a);
+  return int(cudaGetLastError());
+}
+
+extern "C" int tpo_ff_launch_eval(const tpo_ff::EvalArgs *a, size_t smem, cudaStream_t st) {
+  cudaFuncSetAttribute(tpo_ff::eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  tpo_ff::eval_kernel<<<1, tpo_ff::kThreads, smem, st>>>(*a);
+  return int(cudaGetLastError());
+}
+
+extern "C" int tpo_ff_verify_occupancy(size_t smem) {
+  int blocks = 0;
+  cudaFuncSetAttribute(tpo_ff::verify_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, tpo_ff::verify_kernel, tpo_ff::kThreads,
+                                                smem);
+  return blocks;
+}

@@ -1,0 +1,76 @@
+// B200 backend — launch contract of the batched finite-field verifier.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "vm.h"
+
+// Identical layout to tpo_verdict in include/tpo_gpu.h (48 bytes).
+struct TpoVerdict {
+  int32_t kind;  // 0 Equivalent, 1 NotEquivalent, 2 Inconclusive, 3 Error
+  int32_t rounds_run;
+  int32_t resamples;
+  int32_t has_witness;
+  uint64_t w_seed;
+  int32_t w_round;
+  uint32_t w_omega;
+  int32_t w_tensor;
+  int32_t err_code;
+  int64_t w_index;
+};
+
+namespace tpo_ff {
+
+constexpr int kThreads = 256;
+
+struct FieldConst {
+  uint32_t p, q, wbase;
+  uint32_t magic_p, magic_q;   // floor(2^32 / p), floor(2^32 / q)
+  uint32_t two32_p, two32_q;   // 2^32 mod p, 2^32 mod q
+  uint32_t lazy, lazy_sum;     // products / values summable before a reduction
+  uint32_t table_bytes;        // smem bytes of the field tables (16-B aligned)
+  uint64_t thr_p, thr_q;       // uniform() rejection thresholds (2^64 - n) mod n
+};
+
+struct VerifyArgs {
+  FieldConst field;
+  const uint16_t *tables;        // inv_p, inv_q, sqrt_p, sqrt_q
+  const TpoVmInstr *code;
+  const TpoVmGraph *graphs;
+  uint32_t program;              // index of the program graph in `graphs`
+  const uint32_t *pool;          // pool mode: candidate graph = pool[(first+k) % pool_n]
+  uint32_t pool_n;
+  const uint32_t *cand_graph;    // explicit mode (non-null): graph index per candidate
+  const uint64_t *seeds;         // explicit seeds (null: seed = first + k)
+  uint64_t first, n;
+  uint32_t n_in;                 // input elements (shared by both graphs)
+  int num_tests, max_resamples;
+  unsigned long long *counter;   // work queue head
+  TpoVerdict *verdicts;          // optional
+  uint32_t *accept;              // optional packed accept bits (Equivalent)
+  unsigned long long *work;      // optional: attempts actually consumed
+};
+
+struct EvalArgs {
+  FieldConst field;
+  const uint16_t *tables;
+  const TpoVmInstr *code;
+  const TpoVmGraph *graphs;      // graphs[0] is evaluated
+  uint32_t n_in;
+  uint64_t seed, stream;
+  int with_silu;
+  const uint32_t *inputs;        // optional explicit packed inputs
+  const uint16_t *silu_tables;   // optional explicit tp[p] ++ tq[q]
+  uint32_t omega;                // used with explicit inputs
+  uint32_t *out;                 // packed outputs, concatenated
+  uint32_t *in_dump;             // optional: sampled inputs
+  int *status;                   // [0] 0 ok / 1 resample, [1] omega
+};
+
+}  // namespace tpo_ff
+
+extern "C" int tpo_ff_launch_verify(const tpo_ff::VerifyArgs *a, int grid, size_t smem,
+                                    cudaStream_t st);
+extern "C" int tpo_ff_launch_eval(const tpo_ff::EvalArgs *a, size_t smem, cudaStream_t st);
+extern "C" int tpo_ff_verify_occupancy(size_t smem);

@@ -1,0 +1,31 @@
+// B200 backend — launch contract of the fused µGraph kernels.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+enum { MODE_GATED = 1, MODE_RMS = 2, MODE_LORA = 3 };
+
+struct SkinnyParams {
+  int N, K, tokens;          // out columns, reduction dim, live tokens (<= 8, LoRA <= 16)
+  int ksplit, k_per_cta;     // cluster size along K and K elements per CTA
+  const __nv_bfloat16 *x;    // RMS: X [tokens, K]
+  const __nv_bfloat16 *g;    // RMS: G [1, K]
+  const __nv_bfloat16 *dscale;  // RMS: D [1, 1]
+  const __nv_bfloat16 *lora_b;  // LoRA: B [16, N]
+  float *out;                // [tokens, N] fp32
+};
+
+struct GqaParams {
+  int groups, qh, hd, L;     // Q [g, qh, hd], K^T [g, hd, L], V [g, L, hd]
+  int ksplit, l_per_cta;     // cluster split of the kv loop
+  const __nv_bfloat16 *q;
+  float *out;                // [g, qh, hd]
+};
+
+extern "C" int tpo_skinny_launch(int mode, int stages, const CUtensorMap *maps,
+                                 const SkinnyParams *p, cudaStream_t st);
+extern "C" size_t tpo_skinny_smem(int mode, int stages, const SkinnyParams *p);

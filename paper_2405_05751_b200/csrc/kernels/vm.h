@@ -1,0 +1,64 @@
+// B200 backend — block-batched µGraph VM bytecode (host <-> device contract).
+//
+// A µGraph is lowered (csrc/host/lower.cpp) into a straight-line program of
+// tensor instructions.  Every GraphDef's block graph is executed for *all*
+// grid blocks at once: each block-level tensor gets three leading grid dims
+// (bx, by, bz), so one instruction is one data-parallel loop over
+// grid x tile elements, and the reference's sequential block loop
+// (eval_core.hpp:234-237) becomes a batch dimension.  Only the for-loop
+// (eval_core.hpp:303-341) stays sequential: VM_LOOP / VM_ENDLOOP.
+//
+// Addressing: an instruction's index space has up to kVmDims dims (outer to
+// inner).  Operand offsets are base + sum(coord_k * stride_k) (+ iter *
+// iter_stride); a zero stride broadcasts.  `wmask` marks grid dims whose
+// coordinate must be maximal for the store to happen — the reference's
+// "last block in grid-major order wins" rule for grid axes absent from an
+// omap (eval_core.hpp:355-366).
+#pragma once
+
+#include <stdint.h>
+
+#define TPO_VM_DIMS 7
+#define TPO_VM_MAX_OUTPUTS 8
+
+enum TpoVmOp {
+  VM_ZERO = 1,   // dst[0..n) = 0 (field zero (0,0,defined) / 0.0)
+  VM_COPY,       // dst[view] = a[view]           (InIter, Repeat, Reshape, concat Accum, OutSaver)
+  VM_UNARY,      // dst[i] = f(a[view])           sub: VM_EXP, VM_SQR, VM_SQRT, VM_SILU
+  VM_BINARY,     // dst[i] = f(a[view], b[view])  sub: VM_ADD, VM_MUL, VM_DIV
+  VM_MATMUL,     // dims {B, M, K, N}; a [B,M,K], b [B,K,N], dst [B,M,N] contiguous
+  VM_SUM,        // dims {outer, mid, group, inner}: dst[o,m,i] = sum_t a[o, m*group+t, i]
+  VM_LOOP,       // n = trip count; body follows
+  VM_ENDLOOP,    // jump back to the instruction after the matching VM_LOOP
+};
+
+enum TpoVmSub { VM_ADD = 0, VM_MUL, VM_DIV, VM_EXP, VM_SQR, VM_SQRT, VM_SILU };
+
+enum TpoVmFlags {
+  VM_FLAT = 1,    // all operands contiguous over the index space: no index math
+  VM_A_QD = 2,    // operand a is q-defined (FF mode, static)
+  VM_B_QD = 4,    // operand b is q-defined
+};
+
+struct TpoVmInstr {
+  uint8_t op, sub, qd, flags;  // qd: result q-defined (static, FF mode)
+  uint8_t ndim, wmask, pad0, pad1;
+  uint32_t n;                  // elements in the index space
+  uint32_t dst, a, b;          // buffer base offsets (words)
+  int32_t a_iter, d_iter;      // per-iteration offsets added to a / dst
+  uint32_t dims[TPO_VM_DIMS];
+  int32_t sd[TPO_VM_DIMS], sa[TPO_VM_DIMS], sb[TPO_VM_DIMS];
+};
+
+// One compiled graph inside a batch upload.
+struct TpoVmGraph {
+  uint32_t code_off, code_len;  // into the batch instruction array
+  uint32_t n_out;
+  uint32_t words;               // words used past the graph's region base
+  uint32_t out_off[TPO_VM_MAX_OUTPUTS];
+  uint32_t out_len[TPO_VM_MAX_OUTPUTS];
+  uint8_t out_qd[TPO_VM_MAX_OUTPUTS];
+  uint8_t has_silu, poisoned;
+  uint8_t err;                  // 0, or 1 + tpo::ErrCode: candidate rejected up front
+  uint8_t pad[5];
+};

@@ -1,0 +1,62 @@
+"""CPU checks of the C-ABI library: it loads, exports every entry point
+include/tpo_gpu.h declares, and its host-side pieces (JSON parse, validate,
+op_madds, fused-pattern matching) agree with the reference — no GPU calls."""
+import ctypes as C
+import json
+
+import pytest
+
+from oracle import ref
+from paper_2405_05751_b200 import _native as N
+from paper_2405_05751_b200 import api, fixtures as F
+
+
+def test_library_exports_declared_symbols():
+    lib = N.lib()
+    syms = N.declared_symbols()
+    assert len(syms) >= 14
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert lib.tpo_gpu_abi_version() == 1
+
+
+def _compile_host(g):
+    """tpo_gpu_compile needs no device: ctx may be NULL."""
+    h = C.c_void_p()
+    rc = N.lib().tpo_gpu_compile(None, json.dumps(g).encode(), C.byref(h))
+    return rc, h
+
+
+@pytest.mark.parametrize("fam", list(F.VERIFY_SHAPES))
+def test_compile_validate_madds_match_reference(fam):
+    prog, pool = F.verify_families()[fam]
+    for tag, g in [("program", prog)] + pool[::5]:
+        rc, h = _compile_host(g)
+        assert rc == 0, (tag, N.last_error())
+        info = N.GraphInfo()
+        N.lib().tpo_gpu_graph_info(h, C.byref(info))
+        assert info.madds == ref.op_madds(g), tag
+        assert info.lax == 1
+        N.lib().tpo_gpu_graph_free(h)
+        for smem in (48 * 1024, 232448):
+            n, _ = api.validate(g, smem_bytes=smem)
+            assert n == ref.validate(g, smem_bytes=smem), (tag, smem)
+
+
+def test_bench_graphs_validate_and_match():
+    for name in F.BENCH:
+        prog, mu = F.bench_pair(name)
+        assert api.validate(mu)[0] == 0 == ref.validate(mu)
+        assert api.validate(mu, smem_bytes=48 * 1024)[0] == ref.validate(mu, smem_bytes=48 * 1024)
+        rc, h = _compile_host(mu)
+        assert rc == 0, N.last_error()
+        N.lib().tpo_gpu_graph_free(h)
+
+
+def test_compile_errors_are_statuses():
+    rc, _ = _compile_host({"tensors": [], "ops": [{"id": 0, "type": "nope"}], "inputs": [],
+                           "outputs": []})
+    assert rc == 1000 + 10  # ParseError
+    rc = N.lib().tpo_gpu_compile(None, b"{not json", C.byref(C.c_void_p()))
+    assert rc == 1010
+    assert "parse" in N.last_error().lower() or "syntax" in N.last_error().lower()

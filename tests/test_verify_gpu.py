@@ -1,0 +1,182 @@
+"""GPU parity of the Z_p x Z_q path against the compiled reference (oracle/_ref).
+
+Bit-exact: sampled inputs, omega, FF output tensors (xp, xq, q_defined) of
+single attempts, and every EquivVerdict field (kind, rounds_run, resamples,
+witness) of batched verification.
+"""
+import numpy as np
+import pytest
+
+from oracle import ref
+from paper_2405_05751_b200 import fixtures as F
+from paper_2405_05751_b200.graph import PHI, BlockBuilder, GraphBuilder, OpType as O
+
+pytestmark = pytest.mark.gpu
+
+FAMS = F.verify_families()
+
+
+def _graphs():
+    out = []
+    for f, (prog, pool) in FAMS.items():
+        out.append((f + "/program", prog))
+        out += pool
+    return out
+
+
+ALL = _graphs()
+
+
+def _same_attempt(a, b, tag):
+    assert (a["rc"] != 0) == (b["rc"] != 0), (tag, a["rc"], b["rc"])
+    assert a["omega"] == b["omega"], tag
+    assert np.array_equal(a["in_xp"], b["in_xp"]) and np.array_equal(a["in_xq"], b["in_xq"]), tag
+    if a["rc"] == 0:
+        for (xp, xq, qd), (yp, yq, yd) in zip(a["out"], b["out"]):
+            assert np.array_equal(xp, yp), tag
+            assert np.array_equal(qd.astype(bool), yd.astype(bool)), tag
+            assert np.array_equal(np.where(qd, xq, 0), np.where(yd, yq, 0)), tag
+
+
+@pytest.mark.parametrize("stream", [0, 5, 131071])
+def test_ff_attempt_bit_exact_all_pool_graphs(ctx, stream):
+    for tag, g in ALL:
+        for seed in (0, 12345):
+            a = ref.ff_attempt(g, seed, stream)
+            b = ctx.ff_eval(g, seed, stream)
+            _same_attempt(a, b, (tag, seed, stream))
+
+
+VCOLS = ["kind", "rounds_run", "resamples", "has_witness", "w_seed", "w_round", "w_omega",
+         "w_tensor", "w_index"]
+
+
+def _cmp_verdicts(a, b, ctxmsg=""):
+    for c in VCOLS:
+        bad = np.nonzero(a[c] != b[c])[0]
+        assert bad.size == 0, f"{ctxmsg} field {c}: {bad.size} mismatches, first {bad[:5]}"
+
+
+@pytest.mark.parametrize("fam", list(FAMS))
+def test_verify_pool_matches_reference(ctx, fam):
+    prog, pool = FAMS[fam]
+    graphs = [g for _, g in pool]
+    n = 2500
+    want, _ = ref.verify_batch(prog, graphs, first=0, n=n, threads=8)
+    got, att = ctx.verify_pool(prog, graphs, first=0, n=n, want_verdicts=True)
+    _cmp_verdicts(want, got, fam)
+    assert att == int((want["resamples"] + want["rounds_run"]).sum())
+
+
+def test_verify_batch_explicit_seeds_and_rounds(ctx):
+    prog, pool = FAMS["rmsnorm"]
+    rng = np.random.default_rng(1)
+    idx = rng.integers(0, len(pool), 400)
+    seeds = rng.integers(0, 2**63, 400, dtype=np.uint64)
+    cands = [pool[i][1] for i in idx]
+    for num_tests, maxr in ((1, 16), (4, 16), (2, 0), (3, 3)):
+        got, acc = ctx.verify_batch(prog, cands, seeds, num_tests=num_tests, max_resamples=maxr)
+        for k in range(0, 400, 7):
+            w = ref.random_test_equivalence(prog, cands[k], num_tests=num_tests, seed=int(seeds[k]),
+                                            max_resamples=maxr)
+            for c in VCOLS:
+                assert got[c][k] == w[c], (num_tests, maxr, k, c, got[k], w)
+        assert np.array_equal(acc, got["kind"] == 0)
+
+
+def test_random_test_equivalence_pair(ctx):
+    prog, pool = FAMS["gatedmlp"]
+    for tag, g in pool[:6]:
+        for seed in (0, 7, 99):
+            w = ref.random_test_equivalence(prog, g, num_tests=2, seed=seed)
+            v = ctx.random_test_equivalence(prog, g, num_tests=2, seed=seed)
+            for c in VCOLS:
+                assert v[c] == w[c], (tag, seed, c)
+
+
+# ---- edge-case graphs -------------------------------------------------------
+
+def _edge_graphs():
+    gs = {}
+    # identity: output is an input
+    gb = GraphBuilder()
+    x = gb.input([4, 8])
+    gs["identity"] = gb.finish([x])
+    # broadcasting, repeat, reshape, sum groups, sqrt/div resampling, exp + silu
+    gb = GraphBuilder()
+    x, y = gb.input([2, 4, 8]), gb.input([1, 8])
+    a = gb.op(O.EwMul, [x, y])
+    r = gb.op(O.Repeat, [y], {"target": [2, 4, 8]})
+    s = gb.op(O.Sum, [gb.op(O.EwAdd, [a, r])], {"dim": 2, "group": 4})
+    q = gb.op(O.Sqrt, [gb.op(O.Sqr, [s])])
+    d = gb.op(O.EwDiv, [s, q])
+    e = gb.op(O.SiLU, [gb.op(O.EwExp, [gb.op(O.Reshape, [d], {"target": [4, 4]})])])
+    gs["mixed_kernel"] = gb.finish([e, d])
+    # grid axis absent from omap (last block wins), concat accum, 2-D grid
+    gb = GraphBuilder()
+    x, w = gb.input([4, 16]), gb.input([16, 8])
+    bb = BlockBuilder([2, 3, 1], 4, [[4, 16], [16, 8]])
+    xb = bb.initer(0, [PHI, PHI], [1])
+    wb = bb.initer(1, [1, PHI], [0])
+    m = bb.op(O.Accum, [bb.op(O.Matmul, [xb, wb])], {"fmap": [PHI]})
+    cc = bb.op(O.Accum, [xb], {"fmap": [1]})
+    bb.outsaver(m, [1])
+    bb.outsaver(bb.op(O.EwAdd, [cc, cc]), [0])
+    outs = gb.g  # noqa
+    gd = gb.graphdef([x, w], bb)
+    gs["omap_partial"] = gb.finish([gd, gd + 1])
+    # ConcatMatmul inside a block, imap on two axes
+    gb = GraphBuilder()
+    X, T, W, B = gb.input([4, 8]), gb.input([4, 2]), gb.input([8, 6]), gb.input([2, 6])
+    bb = BlockBuilder([2, 3, 1], 2, [[4, 8], [4, 2], [8, 6], [2, 6]])
+    xb = bb.initer(0, [0, PHI], [1])
+    tb = bb.initer(1, [0, PHI], [PHI])
+    wb = bb.initer(2, [PHI, 1], [0])
+    bbar = bb.initer(3, [PHI, 1], [PHI])
+    acc = bb.op(O.Accum, [bb.op(O.ConcatMatmul, [xb, tb, wb, bbar])], {"fmap": [PHI]})
+    bb.outsaver(acc, [0, 1])
+    gs["concatmatmul"] = gb.finish([gb.graphdef([X, T, W, B], bb)])
+    return gs
+
+
+EDGE = _edge_graphs()
+
+
+@pytest.mark.parametrize("name", list(EDGE))
+def test_edge_graph_attempts(ctx, name):
+    g = EDGE[name]
+    for seed in range(6):
+        for stream in (0, 1, 2):
+            a = ref.ff_attempt(g, seed, stream)
+            b = ctx.ff_eval(g, seed, stream)
+            _same_attempt(a, b, (name, seed, stream))
+
+
+def test_edge_self_equivalence_and_resamples(ctx):
+    for name, g in EDGE.items():
+        for seed in range(20):
+            w = ref.random_test_equivalence(g, g, num_tests=2, seed=seed)
+            v = ctx.random_test_equivalence(g, g, num_tests=2, seed=seed)
+            for c in VCOLS:
+                assert v[c] == w[c], (name, seed, c, v, w)
+
+
+def test_other_field_params(ctx):
+    # p = 103, q = 17 (17 | 102); 8^17 = 1 mod 103 with 8 != 1
+    p, q = 103, 17
+    wb = next(b for b in range(2, p) if pow(b, q, p) == 1)
+    prog, pool = FAMS["lora"]
+    for tag, g in pool[:10]:
+        for seed in range(3):
+            w = ref.random_test_equivalence(prog, g, seed=seed, p=p, q=q, wbase=wb)
+            v = ctx.random_test_equivalence(prog, g, seed=seed, p=p, q=q, wbase=wb)
+            for c in VCOLS:
+                assert v[c] == w[c], (tag, seed, c)
+
+
+def test_shape_mismatch_is_error_verdict(ctx):
+    prog, _ = FAMS["rmsnorm"]
+    other, _ = FAMS["gatedmlp"]
+    got, acc = ctx.verify_batch(prog, [other], [0])
+    assert got["kind"][0] == 3 and got["err_code"][0] == 1000  # ShapeMismatch
+    assert not acc[0]

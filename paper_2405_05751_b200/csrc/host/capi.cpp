@@ -406,7 +406,7 @@ int tpo_gpu_eval_mugraph(tpo_gpu_ctx *ctx, const tpo_gpu_graph *h, const void *c
     check_cuda(cudaSetDevice(ctx->c.device), "cudaSetDevice");
     size_t wsb = fused_workspace_bytes(G.plan);
     void *ws = wsb ? ctx->c.ws.get(wsb) : nullptr;
-    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->c.stream;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);  // NULL = legacy default stream
     int e = launch_fused(G.plan, in_dev, in_dtype, out_dev, ws, wsb, st);
     if (e) return fail(3000 + e, std::string("fused launch: ") + cudaGetErrorString(cudaError_t(e)));
     return 0;

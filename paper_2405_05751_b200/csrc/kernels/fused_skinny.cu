@@ -227,6 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;              // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;       // output column within the tile (UMMA M index)
     mbar_wait(&bars->tmem_full, 0);
+    __syncwarp();  // tcgen05.ld is .sync.aligned: the warp must be converged
     tc_fence_after();
     {
       float v[16];

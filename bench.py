@@ -1,0 +1,452 @@
+#!/usr/bin/env python
+"""Benchmark: fused µGraph evaluation on B200 (+ the batched Z_p×Z_q verifier).
+
+BASELINE.json metric: "fused μGraph latency µs & % roofline; Z_p-verified
+candidates/s at 1/2/4/8 GPU".  The N=1 workload is configs[1], the GatedMLP
+µGraph SiLU(xW1)⊙(xW3), x 8×4096, W 4096×14336, bf16 in / fp32 accumulate /
+fp32 out (grid 112, for-loop 16).  One step = one evaluation of that µGraph =
+one fused sm_100a kernel launch.  `value` is whole-job throughput in µGraph
+evaluations/s (replicas on every rank: the fused kernel does not shard,
+"scaling": "weak"); `latency_us` is the per-evaluation kernel latency.
+The weights (235 MB) exceed the 126 MB L2, so every step streams them from
+HBM; smaller workloads (--workload rmsnorm/lora) rotate through enough input
+copies to exceed L2.
+
+The "verifier" object reports the sharded Z_p×Z_q verification throughput
+(candidates/s over all ranks, accept bits gathered with NCCL) on the SURVEY
+§8d candidate pools.  `--workload verify` makes it the headline instead.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload gatedmlp|rmsnorm|lora|gqa|verify]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fused μGraph latency µs & % roofline; Z_p-verified candidates/s at 1/2/4/8 GPU"
+L2_BYTES = 126 * 1024 * 1024
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# --------------------------------------------------------------------------- dist
+class Dist:
+    def __init__(self, n_gpus):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch.distributed as dist
+            import torch
+            torch.cuda.set_device(self.local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def max(self, x: float) -> float:
+        if not self.pg:
+            return x
+        import torch
+        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x: float) -> float:
+        if not self.pg:
+            return x
+        import torch
+        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        self.pg.all_reduce(t)
+        return float(t.item())
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+# ------------------------------------------------------------------------- clocks
+class Clocks:
+    """nvidia-smi sampling of SM clock + throttle reasons during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev, self.proc, self.lines = dev, None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "20"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        busy = [s for s in sm if mx and s > 0.5 * max(mx)] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------- workloads
+def fused_workload(name):
+    import torch
+    from paper_2405_05751_b200 import fixtures as F
+    prog, mu = F.bench_pair(name)
+    args = F.BENCH[name]["args"]
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from test_fused_gpu import make_inputs
+    host = make_inputs(name, args, seed=0)
+    in_bytes = sum(x.numel() * 2 for x in host)
+    out_shape = [mu["tensors"][t]["shape"] for t in mu["outputs"]][0]
+    out_bytes = int(np.prod(out_shape)) * 4
+    return dict(name=name, prog=prog, mu=mu, host=host, in_bytes=in_bytes, out_bytes=out_bytes,
+                out_shape=out_shape, args=args, grid=F.BENCH[name]["grid"],
+                forloop=F.BENCH[name]["forloop"])
+
+
+def run_fused(args, dist, wl):
+    import torch
+    from paper_2405_05751_b200.api import Context
+    dev = dist.local
+    torch.cuda.set_device(dev)
+    ctx = Context(dev)
+    g = ctx.compile(wl["mu"])
+    if not g.fused:
+        raise RuntimeError("benchmark µGraph did not lower to a fused kernel")
+    alg = wl["in_bytes"] + wl["out_bytes"]
+    copies = max(1, -(-3 * L2_BYTES // wl["in_bytes"])) if wl["in_bytes"] < 3 * L2_BYTES else 1
+    sets = [[x.cuda() for x in wl["host"]] for _ in range(copies)]
+    outs = [torch.empty(wl["out_shape"], device="cuda", dtype=torch.float32) for _ in range(copies)]
+    stream = torch.cuda.Stream()
+    st = stream.cuda_stream
+
+    def step(i):
+        ctx.eval_mugraph(g, sets[i % copies], outputs=[outs[i % copies]], stream=st)
+
+    with torch.cuda.stream(stream):
+        for i in range(args.warmup):
+            step(i)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks = Clocks(dev)
+    clocks.start()
+    time.sleep(0.1)
+    # ---- device-resident timed region: K evaluations back to back
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # keep the GPU busy long enough for the clock sampler to see it
+    hot_until = time.time() + 0.3
+    i = 0
+    with torch.cuda.stream(stream):
+        while time.time() < hot_until:
+            step(i)
+            i += 1
+            if i % 64 == 0:
+                stream.synchronize()
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for i in range(args.steps):
+            step(i)
+        e1.record(stream)
+    e1.synchronize()
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms_local = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    ms = dist.max(ms_local)
+    per_eval_ms = ms / args.steps
+    value = dist.world * args.steps / (ms / 1e3)
+
+    # ---- end to end through the public API with HOST buffers (pinned)
+    pinned = [x.pin_memory() for x in wl["host"]]
+    out_h = torch.empty(wl["out_shape"], dtype=torch.float32).pin_memory()
+    dev_in = sets[0]
+    e2e_steps = max(3, min(args.steps, 50))
+    torch.cuda.synchronize()
+    dist.barrier()
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for i in range(e2e_steps):
+            for d, h in zip(dev_in, pinned):
+                d.copy_(h, non_blocking=True)
+            ctx.eval_mugraph(g, dev_in, outputs=[outs[0]], stream=st)
+            out_h.copy_(outs[0], non_blocking=True)
+        e1.record(stream)
+    e1.synchronize()
+    dist.barrier()
+    e2e_ms = dist.max(e0.elapsed_time(e1))
+    e2e = {"value": round(dist.world * e2e_steps / (e2e_ms / 1e3), 3), "unit": "evals/s",
+           "h2d_bytes_per_step": int(wl["in_bytes"]), "d2h_bytes_per_step": int(wl["out_bytes"]),
+           "ms_per_step": round(e2e_ms / e2e_steps, 4)}
+
+    peak, peak_kind = peaks()
+    achieved = alg / (per_eval_ms / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_kind,
+            "algorithmic_bytes": int(alg)}
+    prof = os.path.join(ROOT, "profiles", f"traffic_{wl['name']}.json")
+    if os.path.exists(prof):
+        try:
+            roof["traffic"] = json.load(open(prof))["dram_bytes_per_launch"]
+        except Exception:
+            pass
+    return dict(value=value, ms=per_eval_ms, roof=roof, e2e=e2e, clocks=clk,
+                gpu_launches=args.steps, copies=copies)
+
+
+def cpu_baseline_fused(wl, threads=1, min_seconds=10.0):
+    """The compiled reference (oracle/_ref) eval_mugraph on the host CPU."""
+    from oracle import ref
+    if not ref.available():
+        return None
+    ins = [x.float().numpy().astype(np.float64) for x in wl["host"]]
+    reps, total = 0, 0.0
+    while total < min_seconds * 1e3 and reps < 50:
+        total += ref.time_eval_mugraph(wl["mu"], ins, 1)
+        reps += 1
+    per = total / reps
+    return {"value": round(1e3 / per, 5), "unit": "evals/s", "cores": threads, "kind": "reference",
+            "sample": f"{reps} full eval_mugraph call(s) of the {wl['name']} µGraph, 1 thread "
+                      f"(the reference is single-threaded), {per:.0f} ms each",
+            "ms_per_eval": round(per, 1)}
+
+
+def reference_arm(args, wl):
+    """--impl reference: the reference's eval_mugraph using all host cores, each
+    thread evaluating the µGraph restricted to a slice of output columns
+    (grid blocks are independent, eval_core.hpp:234-237)."""
+    from oracle import ref
+    from paper_2405_05751_b200 import fixtures as F
+    name = wl["name"]
+    cores = os.cpu_count() or 1
+    if name == "gatedmlp":
+        b, h, n = wl["args"]
+        grid = wl["grid"]
+        T = max(t for t in range(1, cores + 1) if grid % t == 0)
+        ns = n // T
+        X, W1, W3 = [x.float().numpy().astype(np.float64) for x in wl["host"]]
+        graphs, inputs = [], []
+        for t in range(T):
+            graphs.append(F.gatedmlp_mugraph(b, h, ns, grid // T, wl["forloop"]))
+            sl = slice(t * ns, (t + 1) * ns)
+            inputs.append([X, np.ascontiguousarray(W1[:, sl]), np.ascontiguousarray(W3[:, sl])])
+    elif name in ("rmsnorm", "lora"):
+        T = 1
+        graphs = [wl["mu"]]
+        inputs = [[x.float().numpy().astype(np.float64) for x in wl["host"]]]
+    else:
+        T = 1
+        graphs = [wl["mu"]]
+        inputs = [[x.float().numpy().astype(np.float64) for x in wl["host"]]]
+    for _ in range(args.warmup and 1):
+        ref.time_eval_parallel(graphs, inputs, 1)
+    times = [ref.time_eval_parallel(graphs, inputs, 1) for _ in range(max(1, args.steps))]
+    ms = float(np.mean(times))
+    v = round(1e3 / ms, 5)
+    return {"metric": METRIC, "value": v, "unit": "evals/s", "n_gpus": 0, "steps": len(times),
+            "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"{name} µGraph {wl['args']} grid {wl['grid']} loop {wl['forloop']}",
+                       "threads": T},
+            "cpu_baseline": {"value": v, "unit": "evals/s", "cores": T, "kind": "reference",
+                             "sample": f"full µGraph per step: reference eval_mugraph on {T} "
+                                       f"column slice(s) concurrently"},
+            "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+# ------------------------------------------------------------------------- verifier
+def run_verify(dist, n_total, pool_fams=("rmsnorm", "gatedmlp", "gqa", "lora")):
+    """Shard n_total candidates (per family, contiguous index ranges) across
+    ranks; each rank verifies its shard on its GPU and the packed accept bits
+    are all-gathered with NCCL.  Returns cand/s over all ranks (max-rank time)."""
+    import torch
+    from paper_2405_05751_b200 import fixtures as F
+    from paper_2405_05751_b200.api import Context
+    ctx = Context(dist.local)
+    fams = F.verify_families()
+    per_fam = n_total // len(pool_fams)
+    shard = per_fam // dist.world
+    jobs = []
+    for f in pool_fams:
+        prog, pool = fams[f]
+        gp = ctx.compile(prog)
+        gs = [ctx.compile(g) for _, g in pool]
+        jobs.append((f, gp, gs))
+    words = (shard + 31) // 32
+    acc = [torch.zeros(words, dtype=torch.int32, device="cuda") for _ in jobs]
+    # warm-up (compile/upload paths)
+    for (f, gp, gs), a in zip(jobs, acc):
+        ctx.verify_pool(gp, gs, first=0, n=min(shard, 2048), accept_dev=a)
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    attempts = 0
+    for (f, gp, gs), a in zip(jobs, acc):
+        first = dist.rank * shard
+        _, att = ctx.verify_pool(gp, gs, first=first, n=shard, accept_dev=a)
+        attempts += att
+    torch.cuda.synchronize()
+    t_local = time.perf_counter() - t0
+    # single collective: gather accept bits
+    gathered = []
+    if dist.pg:
+        for a in acc:
+            out = [torch.empty_like(a) for _ in range(dist.world)]
+            dist.pg.all_gather(out, a)
+            gathered.append(torch.cat(out))
+    else:
+        gathered = acc
+    torch.cuda.synchronize()
+    t_all = dist.max(time.perf_counter() - t0)
+    accepted = int(sum(int(np.unpackbits(g.cpu().numpy().view(np.uint8)).sum()) for g in gathered))
+    n_done = shard * len(jobs) * dist.world
+    return {"value": round(n_done / t_all, 1), "unit": "candidates/s", "candidates": n_done,
+            "seconds": round(t_all, 4), "kernel_seconds_max_rank": round(dist.max(t_local), 4),
+            "accepted": accepted, "attempts_rank0": int(attempts),
+            "families": list(pool_fams), "seed_rule": "candidate i = pool[i % |pool|], seed i"}
+
+
+def cpu_baseline_verify(n=4000):
+    from oracle import ref
+    from paper_2405_05751_b200 import fixtures as F
+    if not ref.available():
+        return None
+    fams = F.verify_families()
+    threads = os.cpu_count() or 1
+    total_ms = 0.0
+    cnt = 0
+    for f, (prog, pool) in fams.items():
+        _, ms = ref.verify_batch(prog, [g for _, g in pool], 0, n // 4, threads=threads, want=False)
+        total_ms += ms
+        cnt += n // 4
+    return {"value": round(cnt / (total_ms / 1e3), 1), "unit": "candidates/s", "cores": threads,
+            "kind": "reference",
+            "sample": f"{cnt} candidates ({n // 4} per family, first indices) of the same pools"}
+
+
+# ----------------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="gatedmlp",
+                    choices=["gatedmlp", "rmsnorm", "lora", "gqa", "verify"])
+    ap.add_argument("--verify-candidates", type=int, default=1_000_000)
+    ap.add_argument("--no-verifier", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        if rank != 0:
+            return
+        wl = fused_workload(args.workload if args.workload != "verify" else "gatedmlp")
+        print(json.dumps(reference_arm(args, wl)), flush=True)
+        return
+
+    dist = Dist(args.gpus)
+    import torch
+    torch.cuda.set_device(dist.local)
+    if args.workload == "verify":
+        ver = run_verify(dist, args.verify_candidates)
+        line = {"metric": METRIC, "value": ver["value"], "unit": "candidates/s",
+                "n_gpus": dist.world, "steps": 1, "warmup": 1,
+                "ms_per_step": round(ver["seconds"] * 1e3, 3), "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+                "config": {"workload": "Z_p×Z_q verification of 1M candidate µGraphs",
+                           "parallelism": f"shard{dist.world}"}, "verifier": ver}
+        if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline_verify()
+        if dist.rank == 0:
+            print(json.dumps(line), flush=True)
+        dist.close()
+        return
+
+    wl = fused_workload(args.workload)
+    r = run_fused(args, dist, wl)
+    line = {
+        "metric": METRIC, "value": round(r["value"], 2), "unit": "evals/s",
+        "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(r["ms"], 5), "latency_us": round(r["ms"] * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic",
+        "config": {"workload": f"{wl['name']} µGraph, inputs {[list(x.shape) for x in wl['host']]}, "
+                               f"grid {wl['grid']}, loop {wl['forloop']} (BASELINE.json configs)",
+                   "global_batch": int(wl["host"][0].shape[0]), "parallelism": f"replica{dist.world}",
+                   "l2": ("inputs larger than L2" if r["copies"] == 1 else
+                          f"rotating {r['copies']} input copies (> L2)")},
+        "roofline": r["roof"], "e2e": r["e2e"], "gpu_launches": r["gpu_launches"],
+        "clocks": r["clocks"],
+    }
+    if not args.no_verifier:
+        line["verifier"] = run_verify(dist, args.verify_candidates)
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_fused(wl)
+    if dist.rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -14,6 +14,9 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <cstdio>
+#include <vector>
+#include <algorithm>
 #include <mutex>
 
 #include "../../../include/tpo_gpu.h"
@@ -107,15 +110,19 @@ int env_int(const char *name, int dflt) {
   return v ? std::atoi(v) : dflt;
 }
 
-// K split (cluster size) for the skinny kernels: enough CTAs to keep every
-// SM streaming weights, K per CTA a multiple of 64.
-int pick_ksplit(int64_t ntiles, int64_t K, int max_split) {
+// K split (= cluster size) for the skinny kernels: the largest split whose
+// grid still fits in ONE wave (every CTA streams weights from the first
+// cycle; a second wave would idle SMs), K per CTA a multiple of 64.  Cluster
+// packing on 148 SMs: size 1/2 -> 148 slots per CTA-per-SM, size 4 -> 132,
+// size 8 -> 120 (GPC granularity).
+int pick_ksplit(int64_t ntiles, int64_t K, int ctas_per_sm) {
   int forced = env_int("TPO_KSPLIT", 0);
   if (forced > 0) return forced;
   int best = 1;
-  for (int s = 1; s <= max_split; s *= 2) {
+  for (int s = 1; s <= 4; s *= 2) {
     if (K % (64 * s)) break;
-    if (ntiles * s <= 2 * 148) best = s;
+    int64_t slots = (s <= 2 ? 148 : s == 4 ? 132 : 120) * int64_t(ctas_per_sm);
+    if (ntiles * s <= slots) best = s;
   }
   return best;
 }
@@ -206,8 +213,30 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // 2-D bf16 tensor map: rows x cols row-major, box (box_cols x box_rows).
+// Encoded maps are cached by (pointer, shape, box, swizzle): repeated
+// evaluations on the same buffers skip the driver call.
 bool tmap_2d(CUtensorMap *m, const void *ptr, uint64_t rows, uint64_t cols, uint32_t box_cols,
              uint32_t box_rows, CUtensorMapSwizzle sw) {
+  struct Key {
+    const void *p;
+    uint64_t r, c;
+    uint32_t bc, br;
+    int sw;
+    bool operator==(const Key &o) const {
+      return p == o.p && r == o.r && c == o.c && bc == o.bc && br == o.br && sw == o.sw;
+    }
+  };
+  static std::mutex mu;
+  static std::vector<std::pair<Key, CUtensorMap>> cache;
+  const Key key{ptr, rows, cols, box_cols, box_rows, int(sw)};
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto &e : cache)
+      if (e.first == key) {
+        *m = e.second;
+        return true;
+      }
+  }
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {cols, rows};
@@ -217,7 +246,11 @@ bool tmap_2d(CUtensorMap *m, const void *ptr, uint64_t rows, uint64_t cols, uint
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides,
                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
+  if (r != CUDA_SUCCESS) return false;
+  std::lock_guard<std::mutex> lk(mu);
+  if (cache.size() >= 256) cache.erase(cache.begin());
+  cache.emplace_back(key, *m);
+  return true;
 }
 
 }  // namespace
@@ -234,8 +267,11 @@ int launch_fused(const FusedPlan &p, const void *const *in, const int32_t *dt, f
   if (p.kind == TPO_FUSED_GATED_MLP) {
     mode = MODE_GATED;
     const int64_t nt = p.n / 128;
-    sp.ksplit = pick_ksplit(nt, p.h, 8);
     stages = env_int("TPO_STAGES", 4);
+    sp.ksplit = pick_ksplit(nt, p.h, stages <= 3 ? 2 : 1);
+    if (sp.ksplit > 2) sp.ksplit = 2;
+    if (sp.ksplit == 2) stages = 3;
+    if (sp.ksplit == 1 && stages != 6) stages = 4;
     if (!tmap_2d(&maps[0], in[1], p.h, p.n, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
         !tmap_2d(&maps[1], in[2], p.h, p.n, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
         !tmap_2d(&maps[2], in[0], p.b, p.h, 64, 16, CU_TENSOR_MAP_SWIZZLE_128B))
@@ -243,8 +279,9 @@ int launch_fused(const FusedPlan &p, const void *const *in, const int32_t *dt, f
     maps[3] = maps[2];
   } else if (p.kind == TPO_FUSED_RMSNORM_MATMUL) {
     mode = MODE_RMS;
-    sp.ksplit = pick_ksplit(p.n / 128, p.h, 8);
-    stages = env_int("TPO_STAGES", 6);
+    stages = env_int("TPO_STAGES", 4);
+    sp.ksplit = pick_ksplit(p.n / 128, p.h, 1);
+    if (sp.ksplit == 1 || stages != 4) stages = 6;
     if (!tmap_2d(&maps[0], in[2], p.h, p.n, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B))
       return int(cudaErrorInvalidValue);
     maps[1] = maps[2] = maps[3] = maps[0];
@@ -253,13 +290,16 @@ int launch_fused(const FusedPlan &p, const void *const *in, const int32_t *dt, f
     sp.dscale = static_cast<const __nv_bfloat16 *>(in[3]);
   } else if (p.kind == TPO_FUSED_LORA) {
     mode = MODE_LORA;
-    sp.ksplit = pick_ksplit(p.n / 128, p.h, 8);
-    stages = env_int("TPO_STAGES", 6);
+    stages = env_int("TPO_STAGES", 4);
+    sp.ksplit = pick_ksplit(p.n / 128, p.h, 1);
+    if (sp.ksplit == 1 || stages != 4) stages = 6;
     if (!tmap_2d(&maps[0], in[1], p.h, p.n, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
         !tmap_2d(&maps[2], in[0], p.b, p.h, 64, 16, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !tmap_2d(&maps[3], in[2], p.h, p.r, 16, 64, CU_TENSOR_MAP_SWIZZLE_NONE))
+        !tmap_2d(&maps[3], in[2], p.h, p.r, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B))
       return int(cudaErrorInvalidValue);
     maps[1] = maps[0];
+    sp.x = static_cast<const __nv_bfloat16 *>(in[0]);
+    sp.lora_a = static_cast<const __nv_bfloat16 *>(in[2]);
     sp.lora_b = static_cast<const __nv_bfloat16 *>(in[3]);
   } else {
     return int(cudaErrorNotSupported);
@@ -269,7 +309,39 @@ int launch_fused(const FusedPlan &p, const void *const *in, const int32_t *dt, f
   sp.tokens = int(p.b);
   sp.k_per_cta = int(p.h / sp.ksplit);
   sp.out = out[0];
-  return tpo_skinny_launch(mode, stages, maps, &sp, st);
+  sp.dbg_flags = env_int("TPO_DBG_FLAGS", 0);
+  static unsigned long long *dbg = nullptr;
+  const int nct = int(p.n / 128) * sp.ksplit;
+  const bool debug_times = std::getenv("TPO_DEBUG_TIMES") != nullptr;
+  if (debug_times) {
+    if (!dbg) cudaMalloc(&dbg, 8 * 8 * 4096);
+    cudaMemsetAsync(dbg, 0, size_t(nct) * 64, st);
+    sp.dbg = dbg;
+  }
+  int rc = tpo_skinny_launch(mode, stages, maps, &sp, st);
+  if (debug_times && !rc) {
+    std::vector<unsigned long long> h(size_t(nct) * 8);
+    cudaMemcpyAsync(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    unsigned long long t0 = ~0ull;
+    for (int c = 0; c < nct; ++c) t0 = std::min(t0, h[size_t(c) * 8]);
+    static const char *names[8] = {"start", "setup", "epi_done", "last_mma", "sent",
+                                   "tmem_full", "recv_done", "end"};
+    std::fprintf(stderr, "[tpo debug] mode %d ksplit %d stages %d ctas %d (us since first start)\n",
+                 mode, sp.ksplit, stages, nct);
+    for (int k = 0; k < 8; ++k) {
+      double mn = 1e30, mx = 0, sum = 0;
+      int cnt = 0;
+      for (int c = 0; c < nct; ++c) {
+        unsigned long long v = h[size_t(c) * 8 + k];
+        if (!v) continue;
+        double d = double(v - t0) / 1e3;
+        mn = std::min(mn, d), mx = std::max(mx, d), sum += d, ++cnt;
+      }
+      if (cnt) std::fprintf(stderr, "  %-12s n=%4d min %7.2f mean %7.2f max %7.2f\n", names[k], cnt, mn, sum / cnt, mx);
+    }
+  }
+  return rc;
 }
 
 }  // namespace tpo::gpu

@@ -15,8 +15,11 @@ struct SkinnyParams {
   const __nv_bfloat16 *x;    // RMS: X [tokens, K]
   const __nv_bfloat16 *g;    // RMS: G [1, K]
   const __nv_bfloat16 *dscale;  // RMS: D [1, 1]
+  const __nv_bfloat16 *lora_a;  // LoRA: A [K, 16]
   const __nv_bfloat16 *lora_b;  // LoRA: B [16, N]
   float *out;                // [tokens, N] fp32
+  unsigned long long *dbg;   // optional per-CTA phase timestamps (TPO_DEBUG_TIMES)
+  int dbg_flags;             // experiments (TPO_DBG_FLAGS): 1 skip finalize
 };
 
 struct GqaParams {

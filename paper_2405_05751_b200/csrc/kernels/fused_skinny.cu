@@ -2,25 +2,31 @@
 //
 // One kernel family executes the GraphDefs of three benchmark µGraphs
 // (fixtures.py):
-//   GATED   : out = SiLU(X·W1) ⊙ (X·W3)                    (GatedMLP)
-//   RMS     : out = (X·G)·W / sqrt(Σ_k X² · D)             (RMSNorm -> MatMul)
-//   LORA    : out = X·W + (X·A)·B                           (single-kernel LoRA)
+//   GATED : out = SiLU(X·W1) ⊙ (X·W3)                    (GatedMLP)
+//   RMS   : out = (X·G)·W / sqrt(Σ_k X² · D)             (RMSNorm -> MatMul)
+//   LORA  : out = X·W + (X·A)·B̄                          (single-kernel LoRA)
 // Each µGraph block graph accumulates φ-Accums over its for-loop; all of them
-// are linear, so a block graph instance maps onto a CTA *cluster* that
-// splits the for-loop (the K range) S ways: every CTA accumulates its share
-// of the loop in TMEM, partial accumulators are summed over DSMEM, and the
-// post-loop ops (SiLU·, /sqrt, +XA·B̄) run once in the leader's epilogue.
+// are linear, so a block-graph instance (a 128-column tile) maps onto a CTA
+// *cluster* that splits the for-loop (the K range) S ways: every CTA
+// accumulates its share of the loop in TMEM, then the partial accumulators
+// are exchanged point-to-point over DSMEM (st.async + mbarrier transaction
+// counts, no cluster-wide barrier) so that each CTA owns 128/S rows of the
+// tile, sums the S partials and runs the post-loop ops (SiLU·, /sqrt, +XA·B̄)
+// for them.
 //
 // Block matmuls run on the 5th-gen tensor cores with swap-AB (weights on
 // UMMA M=128, the 8 or 16 tokens on N=16): D^T[n, t] = W^T[n, k] · X^T[k, t].
 // W tiles are TMA-staged MN-major with 128-byte swizzle; X^T is K-major.
-// For RMS the B operand is the exact fp32 product x·g split into bf16
-// hi + lo rows (tokens 0-7 = hi, 8-15 = lo), so the tensor cores see no
-// rounding of the elementwise product; the two halves are summed in the
-// epilogue.
+// RMS: the B operand is the exact fp32 product x·g split into bf16 hi + lo
+// rows (tokens 0-7 hi, 8-15 lo) so no rounding of the elementwise product
+// reaches the tensor cores; the halves are summed in the epilogue.
+// LoRA: XA^T = A^T·X^T is a second UMMA on the same X^T operand (A box
+// zero-filled past rank 16 by TMA).
 //
 // Warp roles (192 threads): warp 0 TMA producer, warp 1 MMA issuer + TMEM
-// owner, warps 2-5 auxiliary (B-tile / side products) and epilogue.
+// owner, warps 2-5: RMS B-tile builders (+ Σx²), then the epilogue.
+// Programmatic dependent launch: the prologue overlaps the previous kernel;
+// global inputs are touched only after griddepcontrol.wait.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -34,56 +40,78 @@ namespace tpo_fused {
 using namespace sm100;
 
 constexpr int kBK = 64;                   // K per pipeline stage (one 128-B swizzle atom)
-constexpr int kTileN = 128;               // UMMA M (weight columns per CTA)
+constexpr int kTileN = 128;               // UMMA M (weight columns per tile)
 constexpr int kTok = 16;                  // UMMA N (tokens, zero padded)
 constexpr uint32_t kWBox = kBK * 128;     // bytes of one 64-col x kBK-row W box
 constexpr uint32_t kXTile = kTok * 128;   // bytes of a 16-row x 64-k B tile
-constexpr uint32_t kATile = kBK * 32;     // LoRA A tile: kBK rows x 16 cols
 constexpr int kThreads = 192;
+constexpr int kMaxSplit = 4;
 
 template <int MODE>
 struct Cfg {
-  static constexpr int NA = MODE == MODE_GATED ? 2 : 1;              // weight matrices
-  static constexpr bool kTmaX = MODE != MODE_RMS;                    // B tile via TMA
-  static constexpr uint32_t kStage =
-      NA * 2 * kWBox + (kTmaX ? kXTile : 0) + (MODE == MODE_LORA ? kATile : 0);
+  static constexpr int NA = MODE == MODE_GATED ? 2 : 1;  // weight matrices
+  static constexpr bool kTmaX = MODE != MODE_RMS;        // B tile via TMA
+  // LoRA: a 64(k) x 64(r) A box leads the stage (r >= 16 zero-filled by TMA)
+  static constexpr uint32_t kAOff = MODE == MODE_LORA ? kWBox : 0;
+  static constexpr uint32_t kStage = kAOff + NA * 2 * kWBox + (kTmaX ? kXTile : 0);
+  static constexpr int kSide = MODE == MODE_LORA ? 256 : MODE == MODE_RMS ? 8 : 0;
 };
 
 struct __align__(8) Bars {
-  uint64_t full[8], empty[8], tmem_full, b_ready;
+  uint64_t full[8], empty[8], tmem_full, b_ready, recv;
   uint32_t tmem_base;
 };
 
-template <int MODE, int STAGES>
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// remote (DSMEM) 16-byte store that completes `bytes` on the peer's mbarrier
+__device__ __forceinline__ void st_async4(uint32_t addr, float a, float b, float c, float d,
+                                          uint32_t mbar) {
+  asm volatile(
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+          addr),
+      "f"(a), "f"(b), "f"(c), "f"(d), "r"(mbar)
+      : "memory");
+}
+
+template <int MODE, int STAGES, int S>
 __global__ void __launch_bounds__(kThreads, 1)
     skinny_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_constant__ CUtensorMap tmW1,
                   const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmA,
                   const SkinnyParams p) {
   using C = Cfg<MODE>;
+  constexpr int kSide = C::kSide;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t *stages = smem;
   const int nkb = p.k_per_cta / kBK;
-  uint8_t *bregion = stages + STAGES * C::kStage;                       // RMS: all B tiles
+  constexpr int rows_per = kTileN / S;                                     // rows owned per CTA
+  uint8_t *stages = smem;
+  uint8_t *bregion = stages + STAGES * C::kStage;                          // RMS: all B tiles
   float *red = reinterpret_cast<float *>(bregion + (MODE == MODE_RMS ? nkb * kXTile : 0));
-  // red: [S-1][128][16] row partials, then side: [S][kSide]
-  constexpr int kSide = MODE == MODE_LORA ? 256 : 8;
-  float *side = red + (p.ksplit - 1) * kTileN * 16;
-  Bars *bars = reinterpret_cast<Bars *>(side + p.ksplit * kSide);
+  float *side = red + kTileN * 16;          // red: [S][rows_per][16] incoming row partials
+  float *xa_tot = side + kMaxSplit * 256;   // side: [S][kSide]; xa_tot: LoRA [16][16]
+  Bars *bars = reinterpret_cast<Bars *>(xa_tot + 256);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const uint32_t rank = p.ksplit > 1 ? cluster_rank() : 0;
-  const int tile = blockIdx.x / p.ksplit;
-  const int n0 = tile * kTileN;
+  unsigned long long *dbg = p.dbg ? p.dbg + blockIdx.x * 8 : nullptr;
+#define TPO_T(slot) \
+  if (dbg) dbg[slot] = globaltimer();
+  if (threadIdx.x == 0) TPO_T(0);
+  const uint32_t rank = S > 1 ? cluster_rank() : 0;
+  const int n0 = (blockIdx.x / S) * kTileN;
   const int kbase = int(rank) * p.k_per_cta;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&bars->full[s], 1);
-      mbar_init(&bars->empty[s], MODE == MODE_LORA ? 1 + 4 : 1);
+      mbar_init(&bars->empty[s], 1);
     }
     mbar_init(&bars->tmem_full, 1);
     mbar_init(&bars->b_ready, 4);
+    mbar_init(&bars->recv, 1);
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -97,33 +125,35 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
-  if (p.ksplit > 1) cluster_arrive();  // paired with the wait before DSMEM stores
-  float acc[16];                       // epilogue warps: this row's accumulator values
+  if (threadIdx.x == 0) TPO_T(1);
+  if (S > 1) cluster_arrive();  // peers' mbarriers are initialised once the wait returns
+  // incoming DSMEM bytes: (S-1) peers x (rows_per row partials + side block)
+  if (threadIdx.x == 0 && S > 1)
+    mbar_expect_tx(&bars->recv, uint32_t((S - 1) * (rows_per * 64 + kSide * 4)));
+  pdl_wait();  // inputs may be produced by the preceding kernel
 
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer
     if (elect_one()) {
-      const uint32_t bytes = C::kStage;
       for (int kb = 0; kb < nkb; ++kb) {
         const int s = kb % STAGES;
         mbar_wait(&bars->empty[s], ((kb / STAGES) & 1) ^ 1);
         uint8_t *st = stages + s * C::kStage;
-        mbar_expect_tx(&bars->full[s], bytes);
+        mbar_expect_tx(&bars->full[s], C::kStage);
         const int k0 = kbase + kb * kBK;
-        tma_load_2d(st, &tmW0, &bars->full[s], n0, k0);
-        tma_load_2d(st + kWBox, &tmW0, &bars->full[s], n0 + 64, k0);
-        uint8_t *nx = st + 2 * kWBox;
+        if (MODE == MODE_LORA) tma_load_2d(st, &tmA, &bars->full[s], 0, k0);
+        uint8_t *wt = st + C::kAOff;
+        tma_load_2d(wt, &tmW0, &bars->full[s], n0, k0);
+        tma_load_2d(wt + kWBox, &tmW0, &bars->full[s], n0 + 64, k0);
+        uint8_t *nx = wt + 2 * kWBox;
         if (C::NA > 1) {
           tma_load_2d(nx, &tmW1, &bars->full[s], n0, k0);
           tma_load_2d(nx + kWBox, &tmW1, &bars->full[s], n0 + 64, k0);
           nx += 2 * kWBox;
         }
-        if (C::kTmaX) {
-          tma_load_2d(nx, &tmX, &bars->full[s], k0, 0);
-          nx += kXTile;
-        }
-        if (MODE == MODE_LORA) tma_load_2d(nx, &tmA, &bars->full[s], 0, k0);
+        if (C::kTmaX) tma_load_2d(nx, &tmX, &bars->full[s], k0, 0);
       }
+      pdl_launch();  // all input reads issued: the next kernel may start its prologue
     }
   } else if (warp == 1) {
     // -------------------------------------------------------- MMA issuer
@@ -135,100 +165,108 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       if (elect_one()) {
         uint8_t *st = stages + s * C::kStage;
+        uint8_t *wt = st + C::kAOff;
         const uint32_t xs = MODE == MODE_RMS ? smem_u32(bregion + kb * kXTile)
-                                             : smem_u32(st + C::NA * 2 * kWBox);
+                                             : smem_u32(wt + C::NA * 2 * kWBox);
 #pragma unroll
         for (int kk = 0; kk < kBK / 16; ++kk) {
           const uint64_t bdesc = sdesc_sw128(xs + kk * 32, 16, 1024);
 #pragma unroll
           for (int w = 0; w < C::NA; ++w) {
-            const uint64_t adesc = sdesc_sw128(smem_u32(st + w * 2 * kWBox) + kk * 16 * 128, kWBox, 1024);
+            const uint64_t adesc = sdesc_sw128(smem_u32(wt + w * 2 * kWBox) + kk * 16 * 128, kWBox, 1024);
             umma_bf16(tmem + w * kTok, adesc, bdesc, idesc, (kb | kk) != 0);
+          }
+          if (MODE == MODE_LORA) {
+            // XA^T: the A box as a 128-row MN-major operand whose second
+            // 64-row atom is the W box behind it (result rows >= 16 unused)
+            const uint64_t adesc = sdesc_sw128(smem_u32(st) + kk * 16 * 128, kWBox, 1024);
+            umma_bf16(tmem + kTok, adesc, bdesc, idesc, (kb | kk) != 0);
           }
         }
         umma_commit(&bars->empty[s]);
-        if (kb == nkb - 1) umma_commit(&bars->tmem_full);
+        if (kb == nkb - 1) {
+          umma_commit(&bars->tmem_full);
+          TPO_T(3);
+        }
       }
       __syncwarp();
     }
   } else {
-    // -------------------------------------- auxiliary warps (2..5): 128 thr
+    // ------------------------------------- auxiliary / epilogue warps 2..5
     const int t = threadIdx.x - 64;
-    float sidev[kSide > 8 ? 2 : 1] = {};
     float sumsq = 0.f;
     if (MODE == MODE_RMS) {
-      // B region: for every k block, 16 rows (x*g hi for tokens 0-7, lo for
-      // tokens 8-15) x 64 k, K-major 128-B swizzled like a TMA box.
-      // Work item = (k block, token, 16-byte chunk of 8 k): thread t owns a
-      // fixed token (t / 16) so its running sum of squares stays per token.
-      const int tok = t >> 4;           // 0..7
-      const int sub = t & 15;           // 16 threads per token
-      for (int item = sub; item < nkb * 8; item += 16) {
-        const int kb = item >> 3, c = item & 7;
-        const int k = kbase + kb * kBK + c * 8;
-        const uint4 xv = tok < p.tokens ? *reinterpret_cast<const uint4 *>(p.x + size_t(tok) * p.K + k)
-                                        : make_uint4(0, 0, 0, 0);
-        const uint4 gv = *reinterpret_cast<const uint4 *>(p.g + k);
-        const __nv_bfloat162 *x2 = reinterpret_cast<const __nv_bfloat162 *>(&xv);
-        const __nv_bfloat162 *g2 = reinterpret_cast<const __nv_bfloat162 *>(&gv);
-        uint32_t hi[4], lo[4];
+      // B region: per k block, 16 rows (x·g hi for tokens 0-7, lo for 8-15)
+      // x 64 k, K-major with the 128-B swizzle a TMA box would have.  Thread
+      // t owns token t/16 so its running Σx² stays per token.
+      const int tok = t >> 4, sub = t & 15;
+      const int items = nkb * 8;
+      for (int base = sub; base < items; base += 16 * 8) {
+        uint4 xv[8], gv[8];  // loads of up to 8 items in flight at once
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          float2 xf = __bfloat1622float2(x2[j]), gf = __bfloat1622float2(g2[j]);
-          sumsq += xf.x * xf.x + xf.y * xf.y;
-          float p0 = xf.x * gf.x, p1 = xf.y * gf.y;  // exact in fp32 (8b x 8b mantissas)
-          __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
-          float2 hf = __bfloat1622float2(h);
-          __nv_bfloat162 l = __floats2bfloat162_rn(p0 - hf.x, p1 - hf.y);  // exact residual
-          hi[j] = *reinterpret_cast<uint32_t *>(&h);
-          lo[j] = *reinterpret_cast<uint32_t *>(&l);
+        for (int u = 0; u < 8; ++u) {
+          const int item = base + u * 16;
+          xv[u] = gv[u] = make_uint4(0, 0, 0, 0);
+          if (item < items) {
+            const int k = kbase + (item >> 3) * kBK + (item & 7) * 8;
+            if (tok < p.tokens) xv[u] = *reinterpret_cast<const uint4 *>(p.x + size_t(tok) * p.K + k);
+            gv[u] = *reinterpret_cast<const uint4 *>(p.g + k);
+          }
         }
-        uint8_t *tb = bregion + kb * kXTile;
-        const int rh = tok, rl = tok + 8;
-        *reinterpret_cast<uint4 *>(tb + (rh >> 3) * 1024 + (rh & 7) * 128 + ((c ^ (rh & 7)) << 4)) =
-            make_uint4(hi[0], hi[1], hi[2], hi[3]);
-        *reinterpret_cast<uint4 *>(tb + (rl >> 3) * 1024 + (rl & 7) * 128 + ((c ^ (rl & 7)) << 4)) =
-            make_uint4(lo[0], lo[1], lo[2], lo[3]);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int item = base + u * 16;
+          if (item >= items) break;
+          const int kb = item >> 3, c = item & 7;
+          const __nv_bfloat162 *x2 = reinterpret_cast<const __nv_bfloat162 *>(&xv[u]);
+          const __nv_bfloat162 *g2 = reinterpret_cast<const __nv_bfloat162 *>(&gv[u]);
+          uint32_t hi[4], lo[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            float2 xf = __bfloat1622float2(x2[j]), gf = __bfloat1622float2(g2[j]);
+            sumsq += xf.x * xf.x + xf.y * xf.y;
+            float p0 = xf.x * gf.x, p1 = xf.y * gf.y;  // exact in fp32 (8b x 8b mantissas)
+            __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
+            float2 hf = __bfloat1622float2(h);
+            __nv_bfloat162 l = __floats2bfloat162_rn(p0 - hf.x, p1 - hf.y);  // exact residual
+            hi[j] = *reinterpret_cast<uint32_t *>(&h);
+            lo[j] = *reinterpret_cast<uint32_t *>(&l);
+          }
+          uint8_t *tb = bregion + kb * kXTile;
+          const int rh = tok, rl = tok + 8;
+          *reinterpret_cast<uint4 *>(tb + (rh >> 3) * 1024 + (rh & 7) * 128 + ((c ^ (rh & 7)) << 4)) =
+              make_uint4(hi[0], hi[1], hi[2], hi[3]);
+          *reinterpret_cast<uint4 *>(tb + (rl >> 3) * 1024 + (rl & 7) * 128 + ((c ^ (rl & 7)) << 4)) =
+              make_uint4(lo[0], lo[1], lo[2], lo[3]);
+        }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars->b_ready);
-      // per-token sum of squares: reduce the 16 threads of each token
 #pragma unroll
       for (int o = 8; o; o >>= 1) sumsq += __shfl_xor_sync(0xffffffffu, sumsq, o);
-    }
-    if (MODE == MODE_LORA) {
-      // XA partial (16 tokens x 16 ranks) from the staged X / A tiles while
-      // the tensor cores stream W: thread t owns (token t/8, ranks 2*(t%8)..+1).
-      const int tok = t >> 3, r0 = (t & 7) * 2;
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % STAGES;
-        mbar_wait(&bars->full[s], (kb / STAGES) & 1);
-        const uint8_t *xt = stages + s * C::kStage + 2 * kWBox;
-        const uint8_t *at = xt + kXTile;
-#pragma unroll 8
-        for (int k = 0; k < kBK; ++k) {
-          // X tile: row tok, element k (K-major SW128); A tile: row k, cols r0, r0+1 (unswizzled)
-          const int c = k >> 3;
-          const __nv_bfloat16 xv = *reinterpret_cast<const __nv_bfloat16 *>(
-              xt + (tok >> 3) * 1024 + (tok & 7) * 128 + ((c ^ (tok & 7)) << 4) + (k & 7) * 2);
-          const __nv_bfloat162 av = *reinterpret_cast<const __nv_bfloat162 *>(at + k * 32 + r0 * 2);
-          const float xf = __bfloat162float(xv);
-          const float2 af = __bfloat1622float2(av);
-          sidev[0] += xf * af.x;
-          sidev[1] += xf * af.y;
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&bars->empty[s]);
-      }
     }
 
     // ---------------------------------------------------------- epilogue
     const int q = warp & 3;              // TMEM lane quarter this warp may access
-    const int row = q * 32 + lane;       // output column within the tile (UMMA M index)
+    const int row = q * 32 + lane;       // UMMA M index = output column in the tile
+    const int n = n0 + row;
+    const int owner = row / rows_per;    // CTA of the cluster finishing this row
+    // finalize mapping (S > 1): all 128 epilogue threads share this CTA's
+    // rows_per owned rows; thread t takes local row t % rows_per and token
+    // group t / rows_per
+    const int f_row = int(rank) * rows_per + (S > 1 ? t % rows_per : row - int(rank) * rows_per);
+    float bcol[16];                      // LoRA: B̄[:, n] of the finalized row
+    float dsc = 0.f;                     // RMS: the D input
+    if (MODE == MODE_LORA)
+#pragma unroll
+      for (int r = 0; r < 16; ++r) bcol[r] = __bfloat162float(p.lora_b[size_t(r) * p.N + n0 + f_row]);
+    if (MODE == MODE_RMS) dsc = __bfloat162float(p.dscale[0]);
     mbar_wait(&bars->tmem_full, 0);
+    if (threadIdx.x == 64) TPO_T(5);
     __syncwarp();  // tcgen05.ld is .sync.aligned: the warp must be converged
     tc_fence_after();
+    float acc[16], xa[16];
     {
       float v[16];
       tmem_ld16(tmem + (uint32_t(q * 32) << 16), v);
@@ -243,89 +281,134 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else {
 #pragma unroll
         for (int i = 0; i < 16; ++i) acc[i] = v[i];
+        tmem_ld16(tmem + (uint32_t(q * 32) << 16) + kTok, xa);  // XA^T row r = row (< 16)
       }
     }
-    if (p.ksplit > 1) {
-      cluster_wait();  // every CTA of the cluster has started: DSMEM is live
-      if (rank != 0) {
-        const uint32_t dst = map_rank(red + ((rank - 1) * kTileN + row) * 16, 0);
+    // side values this CTA contributes to every owner: RMS Σx² per token,
+    // LoRA XA^T rows 0..15 (held by the threads of rows 0..15)
+    if (MODE == MODE_RMS && (t & 15) == 0) side[rank * kSide + (t >> 4)] = sumsq;
+    if (MODE == MODE_LORA && row < 16)
 #pragma unroll
-        for (int i = 0; i < 16; i += 4) st_cluster_v4(dst + i * 4, acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
+      for (int i = 0; i < 16; ++i) side[rank * kSide + row * 16 + i] = xa[i];
+    if (MODE == MODE_RMS) asm volatile("bar.sync 1, 128;" ::: "memory");  // Σx² slots written
+    if (S > 1) {
+      cluster_wait();  // every peer has initialised its barriers
+      // row partials -> owner; red slot [src rank][row - owner*rows_per]
+      if (owner != int(rank)) {
+        const uint32_t dst = map_rank(red + (int(rank) * rows_per + (row - owner * rows_per)) * 16, owner);
+        const uint32_t mb = map_rank(&bars->recv, owner);
+#pragma unroll
+        for (int i = 0; i < 16; i += 4) st_async4(dst + i * 4, acc[i], acc[i + 1], acc[i + 2], acc[i + 3], mb);
       }
-    }
-    // side partials (sum of squares / XA) of every rank -> leader
-    if (MODE == MODE_RMS && (t & 15) == 0) {
-      const uint32_t dst = map_rank(side + rank * kSide + (t >> 4), 0);
-      if (p.ksplit > 1)
-        asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(dst), "f"(sumsq) : "memory");
-      else
-        side[t >> 4] = sumsq;
+      // side block -> every peer (RMS: 8 floats from 2 threads; LoRA: 16 rows)
+      if (MODE == MODE_RMS && t < 2) {
+        const float *src = side + rank * kSide + t * 4;
+        for (int o = 0; o < S; ++o) {
+          if (o == int(rank)) continue;
+          st_async4(map_rank(src, o), src[0], src[1], src[2], src[3], map_rank(&bars->recv, o));
+        }
+      }
+      if (MODE == MODE_LORA && row < 16) {
+        for (int o = 0; o < S; ++o) {
+          if (o == int(rank)) continue;
+          const uint32_t dst = map_rank(side + rank * kSide + row * 16, o);
+          const uint32_t mb = map_rank(&bars->recv, o);
+#pragma unroll
+          for (int i = 0; i < 16; i += 4) st_async4(dst + i * 4, xa[i], xa[i + 1], xa[i + 2], xa[i + 3], mb);
+        }
+      }
+      if (threadIdx.x == 64) TPO_T(4);
+      mbar_wait(&bars->recv, 0);  // all peers' partials have landed
+      if (threadIdx.x == 64) TPO_T(6);
     }
     if (MODE == MODE_LORA) {
-      const int tok = t >> 3, r0 = (t & 7) * 2;
-      float *loc = side + rank * kSide + tok * 16 + r0;
-      if (p.ksplit > 1) {
-        const uint32_t dst = map_rank(loc, 0);
-        asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(dst), "f"(sidev[0]) : "memory");
-        asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(dst + 4), "f"(sidev[1]) : "memory");
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // own XA^T rows written
+      // XA = Σ_ranks XA^T partials (2 entries per thread) -> xa_tot[r][t]
+      for (int i = t * 2; i < t * 2 + 2; ++i) {
+        float v = 0.f;
+        for (int rr = 0; rr < S; ++rr) v += side[rr * kSide + i];
+        xa_tot[i] = v;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+    }
+    if (p.dbg_flags & 1) {
+    } else if (S == 1) {
+      // single CTA per tile: every thread finishes its own row, all tokens
+      if (MODE == MODE_GATED) {
+#pragma unroll
+        for (int tk = 0; tk < 8; ++tk)
+          if (tk < p.tokens) p.out[size_t(tk) * p.N + n] = silu(acc[tk]) * acc[8 + tk];
+      } else if (MODE == MODE_RMS) {
+#pragma unroll
+        for (int tk = 0; tk < 8; ++tk)
+          if (tk < p.tokens) p.out[size_t(tk) * p.N + n] = acc[tk] / sqrtf(side[tk] * dsc);
       } else {
-        loc[0] = sidev[0];
-        loc[1] = sidev[1];
-      }
-    }
-  }
-
-  __syncwarp();
-  // all partials have landed in the leader once every thread passed this
-  if (p.ksplit > 1) {
-    if (warp < 2) cluster_wait();  // warps 0/1 still owe the first wait
-    cluster_sync();
-  } else {
-    __syncthreads();
-  }
-
-  if (warp >= 2 && rank == 0) {
-    const int t = threadIdx.x - 64;
-    const int q = warp & 3, row = q * 32 + lane;
-    for (int r = 1; r < p.ksplit; ++r) {
-      const float4 *src = reinterpret_cast<const float4 *>(red + ((r - 1) * kTileN + row) * 16);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        float4 x = src[i];
-        acc[4 * i] += x.x, acc[4 * i + 1] += x.y, acc[4 * i + 2] += x.z, acc[4 * i + 3] += x.w;
-      }
-    }
-    const int n = n0 + row;
-    if (MODE == MODE_GATED) {
-#pragma unroll
-      for (int tk = 0; tk < 8; ++tk)
-        if (tk < p.tokens) p.out[size_t(tk) * p.N + n] = silu(acc[tk]) * acc[8 + tk];
-    } else if (MODE == MODE_RMS) {
-      const float dsc = __bfloat162float(p.dscale[0]);
-#pragma unroll
-      for (int tk = 0; tk < 8; ++tk) {
-        float ss = 0.f;
-        for (int r = 0; r < p.ksplit; ++r) ss += side[r * kSide + tk];
-        if (tk < p.tokens) p.out[size_t(tk) * p.N + n] = acc[tk] / sqrtf(ss * dsc);
-      }
-    } else {
-      // post: XW + XA · B̄   (XA summed over ranks; B̄ = B[:, n] column)
-      float bcol[16];
-#pragma unroll
-      for (int r = 0; r < 16; ++r) bcol[r] = __bfloat162float(p.lora_b[size_t(r) * p.N + n]);
-#pragma unroll 4
-      for (int tk = 0; tk < 16; ++tk) {
-        float s = acc[tk];
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
-          float xa = 0.f;
-          for (int rr = 0; rr < p.ksplit; ++rr) xa += side[rr * kSide + tk * 16 + r];
-          s += xa * bcol[r];
+          const float4 *xr = reinterpret_cast<const float4 *>(xa_tot + r * 16);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float4 x = xr[i];
+            acc[4 * i] = fmaf(x.x, bcol[r], acc[4 * i]);
+            acc[4 * i + 1] = fmaf(x.y, bcol[r], acc[4 * i + 1]);
+            acc[4 * i + 2] = fmaf(x.z, bcol[r], acc[4 * i + 2]);
+            acc[4 * i + 3] = fmaf(x.w, bcol[r], acc[4 * i + 3]);
+          }
         }
-        if (tk < p.tokens) p.out[size_t(tk) * p.N + n] = s;
+#pragma unroll
+        for (int tk = 0; tk < 16; ++tk)
+          if (tk < p.tokens) p.out[size_t(tk) * p.N + n] = acc[tk];
+      }
+    } else {
+      // the owner's own partial joins the peers' in red, then all 128
+      // threads finish (local row, token group) items of the owned rows
+      if (owner == int(rank)) {
+        float4 *dst = reinterpret_cast<float4 *>(red + (int(rank) * rows_per + (row - owner * rows_per)) * 16);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) dst[i] = make_float4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      constexpr int ngrp = 128 / rows_per;
+      const int lr = t % rows_per, grp = t / rows_per;
+      const int nn = n0 + int(rank) * rows_per + lr;
+      constexpr int T = MODE == MODE_LORA ? 16 : 8;  // tokens
+      constexpr int tpg = T / ngrp;                  // tokens handled by this thread
+      const int t0 = grp * tpg;
+      float a[tpg], a3[tpg];
+#pragma unroll
+      for (int i = 0; i < tpg; ++i) {
+        a[i] = 0.f;
+        if (MODE == MODE_GATED) a3[i] = 0.f;
+#pragma unroll
+        for (int rr = 0; rr < S; ++rr) {
+          const float *src = red + (rr * rows_per + lr) * 16;
+          a[i] += src[t0 + i];
+          if (MODE == MODE_GATED) a3[i] += src[8 + t0 + i];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < tpg; ++i) {
+        const int tk = t0 + i;
+        float o;
+        if (MODE == MODE_GATED) {
+          o = silu(a[i]) * a3[i];
+        } else if (MODE == MODE_RMS) {
+          float ss = 0.f;
+          for (int rr = 0; rr < S; ++rr) ss += side[rr * kSide + tk];
+          o = a[i] / sqrtf(ss * dsc);
+        } else {
+          o = a[i];
+#pragma unroll
+          for (int r = 0; r < 16; ++r) o = fmaf(xa_tot[r * 16 + tk], bcol[r], o);
+        }
+        if (tk < p.tokens) p.out[size_t(tk) * p.N + nn] = o;
       }
     }
-    (void)t;
+  }
+  if (threadIdx.x == 64) TPO_T(2);
+  if (S > 1 && warp < 2) {
+    __syncwarp();
+    cluster_wait();  // complete the start-up barrier phase for warps 0/1
   }
   tc_fence_before();
   __syncthreads();
@@ -333,37 +416,44 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc<32>(tmem);
   }
+  if (threadIdx.x == 0) TPO_T(7);
+#undef TPO_T
 }
 
-template <int MODE, int STAGES>
+template <int MODE, int STAGES, int S>
 size_t skinny_smem(const SkinnyParams &p) {
   using C = Cfg<MODE>;
   const int nkb = p.k_per_cta / kBK;
-  const int kSide = MODE == MODE_LORA ? 256 : 8;
   size_t b = size_t(STAGES) * C::kStage + (MODE == MODE_RMS ? size_t(nkb) * kXTile : 0) +
-             size_t(p.ksplit - 1) * kTileN * 16 * 4 + size_t(p.ksplit) * kSide * 4 + sizeof(Bars);
+             size_t(kTileN) * 16 * 4 + size_t(kMaxSplit) * 256 * 4 + 256 * 4 + sizeof(Bars);
   return b + 1024;
 }
 
-template <int MODE, int STAGES>
+template <int MODE, int STAGES, int S>
 cudaError_t launch_t(const CUtensorMap *maps, const SkinnyParams &p, cudaStream_t st) {
-  const size_t smem = skinny_smem<MODE, STAGES>(p);
-  auto kern = skinny_kernel<MODE, STAGES>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  if (e) return e;
-  if (p.ksplit > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (p.ksplit != S) return cudaErrorInvalidValue;
+  const size_t smem = skinny_smem<MODE, STAGES, S>(p);
+  auto kern = skinny_kernel<MODE, STAGES, S>;
+  static size_t configured = 0;  // per instantiation: raise the smem limit once
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e) return e;
+    configured = smem;
+  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((p.N / kTileN) * p.ksplit);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = p.ksplit;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], p);
 }
 
@@ -371,40 +461,24 @@ cudaError_t launch_t(const CUtensorMap *maps, const SkinnyParams &p, cudaStream_
 
 using namespace tpo_fused;
 
+#define TPO_SKINNY_CASES(X)                                                                    \
+  X(MODE_GATED, 4, 1) X(MODE_GATED, 6, 1) X(MODE_GATED, 3, 2) X(MODE_RMS, 4, 4) X(MODE_RMS, 6, 4) \
+  X(MODE_RMS, 4, 2) X(MODE_RMS, 6, 2) X(MODE_RMS, 6, 1) X(MODE_LORA, 4, 4) X(MODE_LORA, 6, 4)      \
+  X(MODE_LORA, 4, 2) X(MODE_LORA, 6, 2) X(MODE_LORA, 6, 1)
+
 extern "C" int tpo_skinny_launch(int mode, int stages, const CUtensorMap *maps,
                                  const SkinnyParams *p, cudaStream_t st) {
-#define TPO_CASE(M, S) \
-  if (mode == M && stages == S) return int(launch_t<M, S>(maps, *p, st));
-  TPO_CASE(MODE_GATED, 2)
-  TPO_CASE(MODE_GATED, 3)
-  TPO_CASE(MODE_GATED, 4)
-  TPO_CASE(MODE_GATED, 6)
-  TPO_CASE(MODE_RMS, 3)
-  TPO_CASE(MODE_RMS, 4)
-  TPO_CASE(MODE_RMS, 6)
-  TPO_CASE(MODE_RMS, 8)
-  TPO_CASE(MODE_LORA, 3)
-  TPO_CASE(MODE_LORA, 4)
-  TPO_CASE(MODE_LORA, 6)
-  TPO_CASE(MODE_LORA, 8)
+#define TPO_CASE(M, ST, S) \
+  if (mode == M && stages == ST && p->ksplit == S) return int(launch_t<M, ST, S>(maps, *p, st));
+  TPO_SKINNY_CASES(TPO_CASE)
 #undef TPO_CASE
   return int(cudaErrorInvalidValue);
 }
 
 extern "C" size_t tpo_skinny_smem(int mode, int stages, const SkinnyParams *p) {
-  switch (mode * 16 + stages) {
-    case MODE_GATED * 16 + 2: return skinny_smem<MODE_GATED, 2>(*p);
-    case MODE_GATED * 16 + 3: return skinny_smem<MODE_GATED, 3>(*p);
-    case MODE_GATED * 16 + 4: return skinny_smem<MODE_GATED, 4>(*p);
-    case MODE_GATED * 16 + 6: return skinny_smem<MODE_GATED, 6>(*p);
-    case MODE_RMS * 16 + 3: return skinny_smem<MODE_RMS, 3>(*p);
-    case MODE_RMS * 16 + 4: return skinny_smem<MODE_RMS, 4>(*p);
-    case MODE_RMS * 16 + 6: return skinny_smem<MODE_RMS, 6>(*p);
-    case MODE_RMS * 16 + 8: return skinny_smem<MODE_RMS, 8>(*p);
-    case MODE_LORA * 16 + 3: return skinny_smem<MODE_LORA, 3>(*p);
-    case MODE_LORA * 16 + 4: return skinny_smem<MODE_LORA, 4>(*p);
-    case MODE_LORA * 16 + 6: return skinny_smem<MODE_LORA, 6>(*p);
-    case MODE_LORA * 16 + 8: return skinny_smem<MODE_LORA, 8>(*p);
-  }
+#define TPO_CASE(M, ST, S) \
+  if (mode == M && stages == ST && p->ksplit == S) return skinny_smem<M, ST, S>(*p);
+  TPO_SKINNY_CASES(TPO_CASE)
+#undef TPO_CASE
   return 0;
 }

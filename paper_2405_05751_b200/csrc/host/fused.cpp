@@ -253,6 +253,46 @@ bool tmap_2d(CUtensorMap *m, const void *ptr, uint64_t rows, uint64_t cols, uint
   return true;
 }
 
+// 3-D bf16 tensor map, dims innermost first (cached like tmap_2d).
+bool tmap_3d(CUtensorMap *m, const void *ptr, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0,
+             uint32_t b1, uint32_t b2, CUtensorMapSwizzle sw) {
+  struct Key {
+    const void *p;
+    uint64_t d0, d1, d2;
+    uint32_t b0, b1, b2;
+    int sw;
+    bool operator==(const Key &o) const {
+      return p == o.p && d0 == o.d0 && d1 == o.d1 && d2 == o.d2 && b0 == o.b0 && b1 == o.b1 &&
+             b2 == o.b2 && sw == o.sw;
+    }
+  };
+  static std::mutex mu;
+  static std::vector<std::pair<Key, CUtensorMap>> cache;
+  const Key key{ptr, d0, d1, d2, b0, b1, b2, int(sw)};
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto &e : cache)
+      if (e.first == key) {
+        *m = e.second;
+        return true;
+      }
+  }
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {d0 * 2, d0 * d1 * 2};
+  cuuint32_t box[3] = {b0, b1, b2};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(ptr), dims, strides,
+                  box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return false;
+  std::lock_guard<std::mutex> lk(mu);
+  if (cache.size() >= 256) cache.erase(cache.begin());
+  cache.emplace_back(key, *m);
+  return true;
+}
+
 }  // namespace
 
 int launch_fused(const FusedPlan &p, const void *const *in, const int32_t *dt, float *const *out,
@@ -262,6 +302,25 @@ int launch_fused(const FusedPlan &p, const void *const *in, const int32_t *dt, f
     if (dt[i] != TPO_DTYPE_BF16) return int(cudaErrorNotSupported);
   CUtensorMap maps[4];
   std::memset(maps, 0, sizeof(maps));
+  if (p.kind == TPO_FUSED_GQA_DECODE) {
+    // K^T [G, hd, L], V [G, L, hd], Q [G, qh, hd]
+    GqaParams gp{};
+    gp.groups = int(p.groups), gp.qh = int(p.qh), gp.hd = int(p.hd), gp.L = int(p.L);
+    int S = env_int("TPO_KSPLIT", 0);
+    if (S <= 0) {
+      S = 1;
+      while (S < 4 && p.groups * S * 2 <= 148 && p.L % (128 * S * 2) == 0) S *= 2;
+    }
+    gp.ksplit = S;
+    gp.l_per_cta = int(p.L / S);
+    gp.out = out[0];
+    int stages = env_int("TPO_STAGES", 3);
+    if (!tmap_3d(&maps[0], in[1], p.L, p.hd, p.groups, 64, 128, 1, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_3d(&maps[1], in[2], p.hd, p.L, p.groups, 64, 128, 1, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_3d(&maps[2], in[0], p.hd, p.qh, p.groups, 64, 16, 1, CU_TENSOR_MAP_SWIZZLE_128B))
+      return int(cudaErrorInvalidValue);
+    return tpo_gqa_launch(stages, maps, &gp, st);
+  }
   SkinnyParams sp{};
   int mode = 0, stages = 0;
   if (p.kind == TPO_FUSED_GATED_MLP) {

@@ -1,0 +1,321 @@
+// B200 backend — fused GQA-decode µGraph kernel (sm_100a, tcgen05 + TMA).
+//
+// µGraph (fixtures.gqa_mugraph): per KV group g,
+//   out = Matmul(EwExp(Matmul(Q̄, K̄)), V̄) / Sum(EwExp(Matmul(Q̄, K̄)), dim 2)
+// with φ-Accums N (numerator) and D (denominator) over the kv for-loop and
+// no max subtraction (the Lax fragment has a single exp).
+// N and D are sums over kv, so the loop is split across a CTA cluster
+// (flash-decoding inside one block-graph instance); partials are combined
+// point-to-point over DSMEM before the post-loop EwDiv.
+//
+// Per 128-kv block, two chained UMMAs (swap-AB, M=128, N=16):
+//   S^T[l, q]  = K̄[l, d]   · Q^T[d, q]     A = K^T tile, MN-major (l contiguous)
+//   O^T[d, q] += V̄^T[d, l] · P^T[l, q]     A = V tile,   MN-major (d contiguous)
+// P = exp(S) is computed in fp32 by the epilogue warps from TMEM, split into
+// bf16 hi + lo rows of the second B operand (q hi rows 0-7, lo rows 8-15) so
+// the P·V product carries ~16 mantissa bits; D accumulates the fp32 p.
+// S^T is double-buffered in TMEM and P^T in shared memory, so exp of block
+// j overlaps S of block j+1 and P·V of block j-1.
+//
+// Warps: 0 TMA producer, 1 MMA issuer + TMEM owner, 2-5 exp / epilogue.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fused.cuh"
+#include "sm100.cuh"
+
+namespace tpo_gqa {
+
+using namespace sm100;
+
+constexpr int kBL = 128;                    // kv per block (UMMA M of S^T)
+constexpr int kHD = 128;                    // head dim (UMMA M of O^T, K of S^T)
+constexpr int kTok = 16;                    // UMMA N: 8 q rows (+ lo rows / zero pad)
+constexpr uint32_t kHalf = 64 * kBL * 2;    // one 64-wide box of 128 rows: 16 KB
+constexpr uint32_t kStage = 4 * kHalf;      // K (2 boxes) + V (2 boxes)
+constexpr uint32_t kQBytes = 2 * kTok * 128;  // Q^T: 2 K-major atoms of 16 rows
+constexpr uint32_t kPBytes = 2 * kTok * 128;  // P^T buffer: 2 K-major atoms of 16 rows
+constexpr int kThreads = 192;
+
+struct __align__(8) Bars {
+  uint64_t full[4], empty[4], s_full[2], s_empty[2], p_full[2], p_empty[2], o_full, q_full, recv;
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void st_async4(uint32_t addr, float a, float b, float c, float d,
+                                          uint32_t mbar) {
+  asm volatile(
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+          addr),
+      "f"(a), "f"(b), "f"(c), "f"(d), "r"(mbar)
+      : "memory");
+}
+// byte offset of element (row, col) inside a K-major, 128-B-swizzled tile of
+// 16 rows x 128 columns (two 64-column atoms of 2 KB)
+__device__ __forceinline__ uint32_t kmaj_off(int row, int col) {
+  const int atom = col >> 6, c = (col & 63) >> 3, e = col & 7;
+  return atom * 2048 + (row >> 3) * 1024 + (row & 7) * 128 + ((c ^ (row & 7)) << 4) + e * 2;
+}
+
+template <int STAGES, int S>
+__global__ void __launch_bounds__(kThreads, 1)
+    gqa_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+               const __grid_constant__ CUtensorMap tmQ, const GqaParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *stages = smem;
+  uint8_t *qt = stages + STAGES * kStage;
+  uint8_t *pbuf = qt + kQBytes;                         // 2 x kPBytes
+  constexpr int rows_per = kHD / S;
+  float *red = reinterpret_cast<float *>(pbuf + 2 * kPBytes);  // [S][rows_per][8]
+  float *dpart = red + kHD * 8;                                // [S][8] denominators
+  float *wsum = dpart + 4 * 8;                                 // [4 warps][8]
+  Bars *bars = reinterpret_cast<Bars *>(wsum + 4 * 8);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = S > 1 ? cluster_rank() : 0;
+  const int g = blockIdx.x / S;
+  const int nb = p.l_per_cta / kBL;
+  const int l0 = int(rank) * p.l_per_cta;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&bars->full[s], 1);
+      mbar_init(&bars->empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bars->s_full[b], 1);
+      mbar_init(&bars->s_empty[b], 4);
+      mbar_init(&bars->p_full[b], 4);
+      mbar_init(&bars->p_empty[b], 1);
+    }
+    mbar_init(&bars->o_full, 1);
+    mbar_init(&bars->q_full, 1);
+    mbar_init(&bars->recv, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    tma_prefetch(&tmQ);
+  }
+  if (warp == 1) tmem_alloc<64>(&bars->tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;  // cols [0,16) S0, [16,32) S1, [32,48) O
+  if (S > 1) cluster_arrive();
+  if (threadIdx.x == 0 && S > 1) mbar_expect_tx(&bars->recv, uint32_t((S - 1) * (rows_per * 32 + 32)));
+  pdl_wait();
+
+  if (warp == 0) {
+    // ------------------------------------------------------ TMA producer
+    if (elect_one()) {
+      mbar_expect_tx(&bars->q_full, kQBytes);
+      tma_load_3d(qt, &tmQ, &bars->q_full, 0, 0, g);
+      tma_load_3d(qt + kTok * 128, &tmQ, &bars->q_full, 64, 0, g);
+      for (int j = 0; j < nb; ++j) {
+        const int s = j % STAGES;
+        mbar_wait(&bars->empty[s], ((j / STAGES) & 1) ^ 1);
+        uint8_t *st = stages + s * kStage;
+        mbar_expect_tx(&bars->full[s], kStage);
+        const int l = l0 + j * kBL;
+        tma_load_3d(st, &tmK, &bars->full[s], l, 0, g);                  // K^T[d, l..l+63]
+        tma_load_3d(st + kHalf, &tmK, &bars->full[s], l + 64, 0, g);     // K^T[d, l+64..]
+        tma_load_3d(st + 2 * kHalf, &tmV, &bars->full[s], 0, l, g);      // V[l.., d 0..63]
+        tma_load_3d(st + 3 * kHalf, &tmV, &bars->full[s], 64, l, g);     // V[l.., d 64..]
+      }
+      pdl_launch();
+    }
+  } else if (warp == 1) {
+    // -------------------------------------------------------- MMA issuer
+    constexpr uint32_t idesc = idesc_bf16(128, kTok, /*a MN-major*/ true, /*b K-major*/ false);
+    mbar_wait(&bars->q_full, 0);
+    auto mma2 = [&](int i) {  // O^T += V^T · P^T for block i
+      const int s = i % STAGES, b = i & 1;
+      mbar_wait(&bars->p_full[b], (i >> 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t vt = smem_u32(stages + s * kStage + 2 * kHalf);
+        const uint32_t pt = smem_u32(pbuf + b * kPBytes);
+#pragma unroll
+        for (int kk = 0; kk < kBL / 16; ++kk) {
+          const uint64_t adesc = sdesc_sw128(vt + kk * 16 * 128, kHalf, 1024);
+          const uint64_t bdesc = sdesc_sw128(pt + (kk >> 2) * 2048 + (kk & 3) * 32, 16, 1024);
+          umma_bf16(tmem + 32, adesc, bdesc, idesc, (i | kk) != 0);
+        }
+        umma_commit(&bars->empty[s]);
+        umma_commit(&bars->p_empty[b]);
+      }
+      __syncwarp();
+    };
+    for (int j = 0; j < nb; ++j) {
+      const int s = j % STAGES, b = j & 1;
+      mbar_wait(&bars->full[s], (j / STAGES) & 1);
+      if (j >= 2) mbar_wait(&bars->s_empty[b], ((j - 2) >> 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t kt = smem_u32(stages + s * kStage);
+        const uint32_t qs = smem_u32(qt);
+#pragma unroll
+        for (int kk = 0; kk < kHD / 16; ++kk) {
+          const uint64_t adesc = sdesc_sw128(kt + kk * 16 * 128, kHalf, 1024);
+          const uint64_t bdesc = sdesc_sw128(qs + (kk >> 2) * 2048 + (kk & 3) * 32, 16, 1024);
+          umma_bf16(tmem + b * kTok, adesc, bdesc, idesc, kk != 0);
+        }
+        umma_commit(&bars->s_full[b]);
+      }
+      __syncwarp();
+      if (j >= 1) mma2(j - 1);
+    }
+    mma2(nb - 1);
+    if (elect_one()) umma_commit(&bars->o_full);
+    __syncwarp();
+  } else {
+    // --------------------------------------------- exp / epilogue warps
+    const int t = threadIdx.x - 64;
+    const int q4 = warp & 3;             // TMEM lane quarter
+    const int row = q4 * 32 + lane;      // kv row of S^T, then head-dim row of O^T
+    float dsum[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dsum[i] = 0.f;
+    for (int j = 0; j < nb; ++j) {
+      const int b = j & 1;
+      mbar_wait(&bars->s_full[b], (j >> 1) & 1);
+      __syncwarp();
+      tc_fence_after();
+      float sv[16];
+      tmem_ld16(tmem + (uint32_t(q4 * 32) << 16) + b * kTok, sv);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->s_empty[b]);
+      if (j >= 2) mbar_wait(&bars->p_empty[b], ((j - 2) >> 1) & 1);
+      uint8_t *pb = pbuf + b * kPBytes;
+#pragma unroll
+      for (int qq = 0; qq < 8; ++qq) {
+        const float e = expf(sv[qq]);
+        dsum[qq] += e;
+        const __nv_bfloat16 hi = __float2bfloat16_rn(e);
+        const __nv_bfloat16 lo = __float2bfloat16_rn(e - __bfloat162float(hi));
+        *reinterpret_cast<__nv_bfloat16 *>(pb + kmaj_off(qq, row)) = hi;
+        *reinterpret_cast<__nv_bfloat16 *>(pb + kmaj_off(qq + 8, row)) = lo;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->p_full[b]);
+    }
+    // denominator partial of this CTA: reduce the 128 kv rows
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int o = 16; o; o >>= 1) dsum[i] += __shfl_xor_sync(0xffffffffu, dsum[i], o);
+    if (lane == 0)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) wsum[q4 * 8 + i] = dsum[i];
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (t < 8) dpart[rank * 8 + t] = wsum[t] + wsum[8 + t] + wsum[16 + t] + wsum[24 + t];
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+
+    mbar_wait(&bars->o_full, 0);
+    __syncwarp();
+    tc_fence_after();
+    float ov[16], o[8];
+    tmem_ld16(tmem + (uint32_t(q4 * 32) << 16) + 32, ov);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i] = ov[i] + ov[8 + i];
+    const int owner = row / rows_per;
+    if (S > 1) {
+      cluster_wait();
+      if (owner != int(rank)) {
+        const uint32_t dst = map_rank(red + (int(rank) * rows_per + (row - owner * rows_per)) * 8, owner);
+        const uint32_t mb = map_rank(&bars->recv, owner);
+        st_async4(dst, o[0], o[1], o[2], o[3], mb);
+        st_async4(dst + 16, o[4], o[5], o[6], o[7], mb);
+      }
+      if (t < 2) {
+        const float *src = dpart + rank * 8 + t * 4;
+        for (int pr = 0; pr < S; ++pr) {
+          if (pr == int(rank)) continue;
+          st_async4(map_rank(src, pr), src[0], src[1], src[2], src[3], map_rank(&bars->recv, pr));
+        }
+      }
+      mbar_wait(&bars->recv, 0);
+    }
+    if (owner == int(rank)) {
+      for (int rr = 0; rr < S; ++rr) {
+        if (rr == int(rank)) continue;
+        const float *src = red + (rr * rows_per + (row - owner * rows_per)) * 8;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] += src[i];
+      }
+#pragma unroll
+      for (int qq = 0; qq < 8; ++qq) {
+        if (qq >= p.qh) break;
+        float den = 0.f;
+        for (int rr = 0; rr < S; ++rr) den += dpart[rr * 8 + qq];
+        p.out[(size_t(g) * p.qh + qq) * kHD + row] = o[qq] / den;
+      }
+    }
+  }
+  if (S > 1 && warp < 2) {
+    __syncwarp();
+    cluster_wait();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<64>(tmem);
+  }
+}
+
+template <int STAGES, int S>
+size_t gqa_smem() {
+  return size_t(STAGES) * kStage + kQBytes + 2 * kPBytes + kHD * 8 * 4 + 4 * 8 * 4 + 4 * 8 * 4 +
+         sizeof(Bars) + 1024;
+}
+
+template <int STAGES, int S>
+cudaError_t launch_t(const CUtensorMap *maps, const GqaParams &p, cudaStream_t st) {
+  const size_t smem = gqa_smem<STAGES, S>();
+  auto kern = gqa_kernel<STAGES, S>;
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e) return e;
+    configured = smem;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(p.groups * S);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = S;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], p);
+}
+
+}  // namespace tpo_gqa
+
+extern "C" int tpo_gqa_launch(int stages, const CUtensorMap *maps, const GqaParams *p,
+                              cudaStream_t st) {
+  using namespace tpo_gqa;
+#define TPO_CASE(ST, S) \
+  if (stages == ST && p->ksplit == S) return int(launch_t<ST, S>(maps, *p, st));
+  TPO_CASE(3, 1) TPO_CASE(3, 2) TPO_CASE(3, 4) TPO_CASE(2, 2) TPO_CASE(2, 4)
+#undef TPO_CASE
+  return int(cudaErrorInvalidValue);
+}

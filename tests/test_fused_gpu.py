@@ -75,6 +75,8 @@ SMALL = {
     "gatedmlp": [((8, 512, 256), 2, 4), ((8, 1024, 512), 4, 16), ((3, 256, 128), 1, 1)],
     "rmsnorm": [((8, 512, 256), 2, 4), ((8, 1024, 512), 4, 16), ((5, 256, 384), 1, 2)],
     "lora": [((16, 512, 256, 16), 2, 4), ((16, 1024, 512, 16), 4, 16), ((7, 256, 128, 16), 1, 1)],
+    "gqa": [((4, 8, 128, 512), 2, 4), ((8, 8, 128, 1024), 4, 8), ((2, 5, 128, 256), 1, 2),
+            ((3, 8, 128, 2048), 3, 16)],
 }
 
 
@@ -91,7 +93,7 @@ def test_fused_small_shapes_vs_reference(ctx, name):
         check(out, torch_ref(name, ins).numpy())
 
 
-@pytest.mark.parametrize("name", ["gatedmlp", "rmsnorm", "lora"])
+@pytest.mark.parametrize("name", ["gatedmlp", "rmsnorm", "lora", "gqa"])
 def test_fused_bench_shape_vs_reference(ctx, name):
     prog, mu = F.bench_pair(name)
     args = F.BENCH[name]["args"]

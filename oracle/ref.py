@@ -149,9 +149,9 @@ def time_eval_parallel(graphs, inputs_per_graph, reps=1) -> float:
 def ff_attempt(g, seed: int, stream: int, with_silu: Optional[bool] = None, p=227, q=113, wbase=4):
     """One verifier attempt (equiv.cpp:57-68) on a single graph.
     Returns dict(rc, omega, in_xp, in_xq, out=[(xp, xq, qd) per output])."""
-    from paper_2405_05751_b200.graph import has_silu
+    from .restate import graph_has_silu
     if with_silu is None:
-        with_silu = has_silu(g)
+        with_silu = graph_has_silu(g)
     n_in = sum(int(np.prod(s)) for s in _shapes(g, "inputs"))
     oshapes = _shapes(g, "outputs")
     n_out = sum(int(np.prod(s)) for s in oshapes)

@@ -105,6 +105,14 @@ void tpo_gpu_close(tpo_gpu_ctx *ctx);
 int tpo_gpu_compile(tpo_gpu_ctx *ctx, const char *graph_json, tpo_gpu_graph **out);
 void tpo_gpu_graph_free(tpo_gpu_graph *g);
 int tpo_gpu_graph_info(const tpo_gpu_graph *g, tpo_graph_info *out);
+/* Declares graph inputs (bit i = input i) as static parameters: never
+ * written by work enqueued on the stream before an evaluation (weights).  A
+ * fused kernel may then start streaming them before its programmatic
+ * dependency on the preceding kernel resolves (PDL), overlapping
+ * back-to-back evaluations.  Default 0: every input is ordered after the
+ * preceding work.  No reference counterpart (a launch-time property). */
+int tpo_gpu_graph_set_static_inputs(tpo_gpu_graph *g, uint64_t mask);
+
 /* Shape of input/output `index` (is_output 0/1): writes rank dims, returns rank or <0. */
 int tpo_gpu_graph_shape(const tpo_gpu_graph *g, int is_output, int index, int64_t *dims);
 

@@ -74,6 +74,15 @@ class Graph:
             out.append([dims[k] for k in range(r)])
         return out
 
+    def set_static_inputs(self, indices: Sequence[int]) -> "Graph":
+        """Declare inputs that no earlier work on the stream writes (weights):
+        the fused kernel may stream them before the preceding kernel ends."""
+        mask = 0
+        for i in indices:
+            mask |= 1 << int(i)
+        N.check(N.lib().tpo_gpu_graph_set_static_inputs(self.h, mask))
+        return self
+
     @property
     def fused(self) -> Optional[str]:
         return FUSED.get(self.info.fused_kind)

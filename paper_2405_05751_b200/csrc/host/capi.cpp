@@ -364,6 +364,15 @@ int tpo_gpu_graph_info(const tpo_gpu_graph *h, tpo_graph_info *o) {
   return 0;
 }
 
+int tpo_gpu_graph_set_static_inputs(tpo_gpu_graph *h, uint64_t mask) {
+  return guard([&] {
+    if (h->g.g.inputs.size() < 64 && (mask >> h->g.g.inputs.size()))
+      throw Error(ErrCode::ShapeMismatch, "static-input mask names a non-existent input");
+    h->g.plan.static_inputs = mask;
+    return 0;
+  });
+}
+
 int tpo_gpu_graph_shape(const tpo_gpu_graph *h, int is_output, int index, int64_t *dims) {
   const auto &v = is_output ? h->g.g.outputs : h->g.g.inputs;
   if (index < 0 || size_t(index) >= v.size()) return -1;

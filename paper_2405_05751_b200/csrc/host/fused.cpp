@@ -322,15 +322,10 @@ int launch_fused(const FusedPlan &p, const void *const *in, const int32_t *dt, f
     return tpo_gqa_launch(stages, maps, &gp, st);
   }
   SkinnyParams sp{};
-  int mode = 0, stages = 0;
+  int mode = 0;
   if (p.kind == TPO_FUSED_GATED_MLP) {
     mode = MODE_GATED;
-    const int64_t nt = p.n / 128;
-    stages = env_int("TPO_STAGES", 4);
-    sp.ksplit = pick_ksplit(nt, p.h, stages <= 3 ? 2 : 1);
-    if (sp.ksplit > 2) sp.ksplit = 2;
-    if (sp.ksplit == 2) stages = 3;
-    if (sp.ksplit == 1 && stages != 6) stages = 4;
+    sp.ksplit = std::min(2, pick_ksplit(p.n / 128, p.h, 1));
     if (!tmap_2d(&maps[0], in[1], p.h, p.n, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
         !tmap_2d(&maps[1], in[2], p.h, p.n, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
         !tmap_2d(&maps[2], in[0], p.b, p.h, 64, 16, CU_TENSOR_MAP_SWIZZLE_128B))
@@ -338,23 +333,21 @@ int launch_fused(const FusedPlan &p, const void *const *in, const int32_t *dt, f
     maps[3] = maps[2];
   } else if (p.kind == TPO_FUSED_RMSNORM_MATMUL) {
     mode = MODE_RMS;
-    stages = env_int("TPO_STAGES", 4);
     sp.ksplit = pick_ksplit(p.n / 128, p.h, 1);
-    if (sp.ksplit == 1 || stages != 4) stages = 6;
-    if (!tmap_2d(&maps[0], in[2], p.h, p.n, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B))
+    if (!tmap_2d(&maps[0], in[2], p.h, p.n, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        !tmap_2d(&maps[2], in[0], p.b, p.h, 64, 8, CU_TENSOR_MAP_SWIZZLE_NONE) ||
+        !tmap_2d(&maps[3], in[1], 1, p.h, 64, 1, CU_TENSOR_MAP_SWIZZLE_NONE))
       return int(cudaErrorInvalidValue);
-    maps[1] = maps[2] = maps[3] = maps[0];
+    maps[1] = maps[0];
     sp.x = static_cast<const __nv_bfloat16 *>(in[0]);
     sp.g = static_cast<const __nv_bfloat16 *>(in[1]);
     sp.dscale = static_cast<const __nv_bfloat16 *>(in[3]);
   } else if (p.kind == TPO_FUSED_LORA) {
     mode = MODE_LORA;
-    stages = env_int("TPO_STAGES", 4);
     sp.ksplit = pick_ksplit(p.n / 128, p.h, 1);
-    if (sp.ksplit == 1 || stages != 4) stages = 6;
     if (!tmap_2d(&maps[0], in[1], p.h, p.n, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
         !tmap_2d(&maps[2], in[0], p.b, p.h, 64, 16, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !tmap_2d(&maps[3], in[2], p.h, p.r, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B))
+        !tmap_2d(&maps[3], in[2], p.h, p.r, 16, 64, CU_TENSOR_MAP_SWIZZLE_NONE))
       return int(cudaErrorInvalidValue);
     maps[1] = maps[0];
     sp.x = static_cast<const __nv_bfloat16 *>(in[0]);
@@ -368,31 +361,65 @@ int launch_fused(const FusedPlan &p, const void *const *in, const int32_t *dt, f
   sp.tokens = int(p.b);
   sp.k_per_cta = int(p.h / sp.ksplit);
   sp.out = out[0];
+  // Weights (W / W1,W3 / A) declared static may stream before the PDL wait.
+  const uint64_t weights = p.kind == TPO_FUSED_GATED_MLP ? 0x6 : p.kind == TPO_FUSED_LORA ? 0x6 : 0x4;
+  sp.prefetch_static = (p.static_inputs & weights) == weights && !std::getenv("TPO_NO_PREFETCH");
+  // Pipeline: with static weights, the two-CTAs-per-SM configuration (the
+  // next evaluation's CTAs stream weights while this one drains); otherwise
+  // the measured-best single-CTA depth (profiles/r01: sweep) that fits.
+  int stages = env_int("TPO_STAGES", 0), minb = env_int("TPO_MINB", 0);
+  const size_t kTwoPerSm = 115712, kOnePerSm = 232448;
+  if (stages <= 0) {
+    if (sp.prefetch_static && minb != 1) {
+      for (int s : {4, 3}) {
+        const size_t b = tpo_skinny_smem(mode, s, 2, &sp);
+        if (b && b <= kTwoPerSm) {
+          stages = s, minb = 2;
+          break;
+        }
+      }
+    }
+    if (stages <= 0) {
+      minb = 1;
+      const int pref_g[] = {4, 6, 3}, pref_r[] = {6, 8, 4, 10}, pref_l[] = {6, 8, 4, 10};
+      const int *pref = mode == MODE_GATED ? pref_g : mode == MODE_RMS ? pref_r : pref_l;
+      const int np = mode == MODE_GATED ? 3 : 4;
+      for (int i = 0; i < np; ++i) {
+        const size_t b = tpo_skinny_smem(mode, pref[i], 1, &sp);
+        if (b && b <= kOnePerSm) {
+          stages = pref[i];
+          break;
+        }
+      }
+    }
+  } else if (minb <= 0) {
+    minb = tpo_skinny_smem(mode, stages, 2, &sp) ? 2 : 1;
+  }
   sp.dbg_flags = env_int("TPO_DBG_FLAGS", 0);
   static unsigned long long *dbg = nullptr;
   const int nct = int(p.n / 128) * sp.ksplit;
   const bool debug_times = std::getenv("TPO_DEBUG_TIMES") != nullptr;
   if (debug_times) {
-    if (!dbg) cudaMalloc(&dbg, 8 * 8 * 4096);
-    cudaMemsetAsync(dbg, 0, size_t(nct) * 64, st);
+    if (!dbg) cudaMalloc(&dbg, 16 * 8 * 4096);
+    cudaMemsetAsync(dbg, 0, size_t(nct) * 128, st);
     sp.dbg = dbg;
   }
-  int rc = tpo_skinny_launch(mode, stages, maps, &sp, st);
+  int rc = tpo_skinny_launch(mode, stages, minb, maps, &sp, st);
   if (debug_times && !rc) {
-    std::vector<unsigned long long> h(size_t(nct) * 8);
+    std::vector<unsigned long long> h(size_t(nct) * 16);
     cudaMemcpyAsync(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     unsigned long long t0 = ~0ull;
-    for (int c = 0; c < nct; ++c) t0 = std::min(t0, h[size_t(c) * 8]);
-    static const char *names[8] = {"start", "setup", "epi_done", "last_mma", "sent",
-                                   "tmem_full", "recv_done", "end"};
-    std::fprintf(stderr, "[tpo debug] mode %d ksplit %d stages %d ctas %d (us since first start)\n",
-                 mode, sp.ksplit, stages, nct);
-    for (int k = 0; k < 8; ++k) {
+    for (int c = 0; c < nct; ++c) t0 = std::min(t0, h[size_t(c) * 16]);
+    static const char *names[11] = {"start", "setup", "epi_done", "last_mma", "sent", "tmem_full",
+                                    "recv_done", "end", "first_full", "b_ready", "last_tma"};
+    std::fprintf(stderr, "[tpo debug] mode %d ksplit %d stages %d minb %d prefetch %d ctas %d (us since first start)\n",
+                 mode, sp.ksplit, stages, minb, sp.prefetch_static, nct);
+    for (int k = 0; k < 11; ++k) {
       double mn = 1e30, mx = 0, sum = 0;
       int cnt = 0;
       for (int c = 0; c < nct; ++c) {
-        unsigned long long v = h[size_t(c) * 8 + k];
+        unsigned long long v = h[size_t(c) * 16 + k];
         if (!v) continue;
         double d = double(v - t0) / 1e3;
         mn = std::min(mn, d), mx = std::max(mx, d), sum += d, ++cnt;

@@ -18,6 +18,8 @@ struct FusedPlan {
   int64_t groups = 0, qh = 0, hd = 0, L = 0;  // GQA
   int64_t grid = 0, forloop = 0;        // the µGraph's block-graph schedule
   std::string why;                      // reason when kind == 0
+  uint64_t static_inputs = 0;           // bit i: input i is never written by work
+                                        // enqueued before an evaluation (weights)
 };
 
 // Structural match of a KernelGraph against the four benchmark µGraph forms

@@ -20,6 +20,7 @@ struct SkinnyParams {
   float *out;                // [tokens, N] fp32
   unsigned long long *dbg;   // optional per-CTA phase timestamps (TPO_DEBUG_TIMES)
   int dbg_flags;             // experiments (TPO_DBG_FLAGS): 1 skip finalize
+  int prefetch_static;       // weights are static: stream them before the PDL wait
 };
 
 struct GqaParams {
@@ -29,8 +30,8 @@ struct GqaParams {
   float *out;                // [g, qh, hd]
 };
 
-extern "C" int tpo_skinny_launch(int mode, int stages, const CUtensorMap *maps,
+extern "C" int tpo_skinny_launch(int mode, int stages, int minb, const CUtensorMap *maps,
                                  const SkinnyParams *p, cudaStream_t st);
-extern "C" size_t tpo_skinny_smem(int mode, int stages, const SkinnyParams *p);
+extern "C" size_t tpo_skinny_smem(int mode, int stages, int minb, const SkinnyParams *p);
 extern "C" int tpo_gqa_launch(int stages, const CUtensorMap *maps, const GqaParams *p,
                               cudaStream_t st);

@@ -113,6 +113,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (S > 1) cluster_arrive();
   if (threadIdx.x == 0 && S > 1) mbar_expect_tx(&bars->recv, uint32_t((S - 1) * (rows_per * 32 + 32)));
   pdl_wait();
+  pdl_launch();  // every thread: the dependent grid may become resident early
 
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer
@@ -131,7 +132,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_3d(st + 2 * kHalf, &tmV, &bars->full[s], 0, l, g);      // V[l.., d 0..63]
         tma_load_3d(st + 3 * kHalf, &tmV, &bars->full[s], 64, l, g);     // V[l.., d 64..]
       }
-      pdl_launch();
     }
   } else if (warp == 1) {
     // -------------------------------------------------------- MMA issuer

@@ -20,17 +20,21 @@
 // RMS: the B operand is the exact fp32 product x·g split into bf16 hi + lo
 // rows (tokens 0-7 hi, 8-15 lo) so no rounding of the elementwise product
 // reaches the tensor cores; the halves are summed in the epilogue.
-// LoRA: XA^T = A^T·X^T is a second UMMA on the same X^T operand (A box
-// zero-filled past rank 16 by TMA).
+// LoRA: XA = X·A (16 x 16 per CTA K range) runs on the CUDA cores of the
+// otherwise idle epilogue warps, reading the same staged X^T tile and a raw
+// [64 k][16 r] A box, while the tensor cores run X·W.
 //
 // Warp roles (192 threads): warp 0 TMA producer, warp 1 MMA issuer + TMEM
-// owner, warps 2-5: RMS B-tile builders (+ Σx²), then the epilogue.
+// owner, warps 2-5: per-stage RMS B-tile builders (+ Σx²) / LoRA XA, then
+// the epilogue.
 // Programmatic dependent launch: the prologue overlaps the previous kernel;
 // global inputs are touched only after griddepcontrol.wait.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <cstdlib>
 
 #include "fused.cuh"
 #include "sm100.cuh"
@@ -47,18 +51,34 @@ constexpr uint32_t kXTile = kTok * 128;   // bytes of a 16-row x 64-k B tile
 constexpr int kThreads = 192;
 constexpr int kMaxSplit = 4;
 
+// Pipeline stage layout (one k block of 64):
+//   [A box (LoRA)] [W boxes: NA x 2 x 8 KB] [B operand tile 2 KB] [RMS: raw X 1 KB, G 128 B]
+// GATED / LoRA: the B operand tile (X^T, K-major, 128-B swizzle) is a TMA box.
+// RMS: TMA brings raw X and G; the four epilogue warps build the B tile
+// (x·g as bf16 hi + lo rows) in place while the stage's W boxes land, and
+// release it to the MMA issuer per stage (b_full).
 template <int MODE>
 struct Cfg {
   static constexpr int NA = MODE == MODE_GATED ? 2 : 1;  // weight matrices
   static constexpr bool kTmaX = MODE != MODE_RMS;        // B tile via TMA
-  // LoRA: a 64(k) x 64(r) A box leads the stage (r >= 16 zero-filled by TMA)
-  static constexpr uint32_t kAOff = MODE == MODE_LORA ? kWBox : 0;
-  static constexpr uint32_t kStage = kAOff + NA * 2 * kWBox + (kTmaX ? kXTile : 0);
+  static constexpr uint32_t kAOff = 0;                   // W boxes lead the stage
+  static constexpr uint32_t kBOff = kAOff + NA * 2 * kWBox;
+  static constexpr uint32_t kXRawOff = kBOff + kXTile;     // RMS raw X
+  static constexpr uint32_t kGOff = kXRawOff + 1024;       // RMS G
+  static constexpr uint32_t kARawOff = kBOff + kXTile;     // LoRA A box [64 k][16 r] (2 KB)
+  static constexpr uint32_t kStage = MODE == MODE_RMS    ? kGOff + 1024
+                                     : MODE == MODE_LORA ? kARawOff + 2048
+                                                         : kBOff + kXTile;
+  static constexpr uint32_t kFullBytes = MODE == MODE_RMS ? NA * 2 * kWBox : kStage;
+  static constexpr uint32_t kXGBytes = 1024 + 128;  // RMS: X box [8][64] + G box [64]
   static constexpr int kSide = MODE == MODE_LORA ? 256 : MODE == MODE_RMS ? 8 : 0;
 };
 
+constexpr int kMaxStages = 12;
+
 struct __align__(8) Bars {
-  uint64_t full[8], empty[8], tmem_full, b_ready, recv;
+  uint64_t full[kMaxStages], empty[kMaxStages], xg_full[kMaxStages], b_full[kMaxStages];
+  uint64_t tmem_full, recv, recv_side;
   uint32_t tmem_base;
 };
 
@@ -77,26 +97,32 @@ __device__ __forceinline__ void st_async4(uint32_t addr, float a, float b, float
       : "memory");
 }
 
-template <int MODE, int STAGES, int S>
-__global__ void __launch_bounds__(kThreads, 1)
+// MINB = 2: a shallow pipeline (<= 113 KB smem) so that two CTAs fit one SM.
+// With PDL the next evaluation's CTAs then become resident while this one
+// drains; when the weights are declared static (p.prefetch_static) they
+// start streaming their first pipeline stages before the grid dependency
+// resolves, so HBM stays busy across back-to-back µGraph evaluations.
+template <int MODE, int STAGES, int S, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
     skinny_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_constant__ CUtensorMap tmW1,
                   const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmA,
                   const SkinnyParams p) {
   using C = Cfg<MODE>;
+  static_assert(STAGES <= kMaxStages, "pipeline deeper than the barrier arrays");
   constexpr int kSide = C::kSide;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int nkb = p.k_per_cta / kBK;
   constexpr int rows_per = kTileN / S;                                     // rows owned per CTA
   uint8_t *stages = smem;
-  uint8_t *bregion = stages + STAGES * C::kStage;                          // RMS: all B tiles
-  float *red = reinterpret_cast<float *>(bregion + (MODE == MODE_RMS ? nkb * kXTile : 0));
-  float *side = red + kTileN * 16;          // red: [S][rows_per][16] incoming row partials
-  float *xa_tot = side + kMaxSplit * 256;   // side: [S][kSide]; xa_tot: LoRA [16][16]
-  Bars *bars = reinterpret_cast<Bars *>(xa_tot + 256);
+  float *red = reinterpret_cast<float *>(stages + STAGES * C::kStage);
+  float *side = red + (S > 1 ? kTileN * 16 : 0);  // red: [S][rows_per][16] incoming row partials
+  float *xa_tot = side + S * kSide;         // side: [S][kSide]; xa_tot: LoRA [16][16]
+  float *xa_w = xa_tot + (MODE == MODE_LORA ? 256 : 0);  // LoRA: per-warp XA partials [4][16][16]
+  Bars *bars = reinterpret_cast<Bars *>(xa_w + (MODE == MODE_LORA ? 1024 : 0));
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  unsigned long long *dbg = p.dbg ? p.dbg + blockIdx.x * 8 : nullptr;
+  unsigned long long *dbg = p.dbg ? p.dbg + blockIdx.x * 16 : nullptr;
 #define TPO_T(slot) \
   if (dbg) dbg[slot] = globaltimer();
   if (threadIdx.x == 0) TPO_T(0);
@@ -107,18 +133,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&bars->full[s], 1);
-      mbar_init(&bars->empty[s], 1);
+      mbar_init(&bars->empty[s], MODE == MODE_LORA ? 5 : 1);  // LoRA: + 4 XA warps
+      mbar_init(&bars->xg_full[s], 1);
+      mbar_init(&bars->b_full[s], 4);
     }
     mbar_init(&bars->tmem_full, 1);
-    mbar_init(&bars->b_ready, 4);
     mbar_init(&bars->recv, 1);
+    mbar_init(&bars->recv_side, 1);
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmW0);
     if (C::NA > 1) tma_prefetch(&tmW1);
-    if (C::kTmaX) tma_prefetch(&tmX);
-    if (MODE == MODE_LORA) tma_prefetch(&tmA);
+    tma_prefetch(&tmX);
+    if (MODE != MODE_GATED) tma_prefetch(&tmA);
   }
   if (warp == 1) tmem_alloc<32>(&bars->tmem_base);
   tc_fence_before();
@@ -127,21 +155,66 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = bars->tmem_base;
   if (threadIdx.x == 0) TPO_T(1);
   if (S > 1) cluster_arrive();  // peers' mbarriers are initialised once the wait returns
-  // incoming DSMEM bytes: (S-1) peers x (rows_per row partials + side block)
-  if (threadIdx.x == 0 && S > 1)
-    mbar_expect_tx(&bars->recv, uint32_t((S - 1) * (rows_per * 64 + kSide * 4)));
+  // incoming DSMEM bytes: (S-1) peers x the owned rows' partials; side blocks
+  if (threadIdx.x == 0 && S > 1) {
+    mbar_expect_tx(&bars->recv, uint32_t((S - 1) * rows_per * (MODE == MODE_RMS ? 8 : 16) * 4));
+    if (kSide) mbar_expect_tx(&bars->recv_side, uint32_t((S - 1) * kSide * 4));
+  }
+  // Weights declared static (never written by preceding work on the
+  // stream) may stream before the programmatic dependency resolves: the
+  // producer issues the W (and LoRA A) boxes of the first pipeline stages,
+  // then waits; X is read only after the wait.
+  const int npre = p.prefetch_static ? (nkb < STAGES ? nkb : STAGES) : 0;
+  if (warp == 0 && elect_one()) {
+    for (int kb = 0; kb < npre; ++kb) {
+      uint8_t *st = stages + kb * C::kStage;
+      mbar_expect_tx(&bars->full[kb], C::kFullBytes);
+      const int k0 = kbase + kb * kBK;
+      if (MODE == MODE_LORA) tma_load_2d(st + C::kARawOff, &tmA, &bars->full[kb], 0, k0);
+      uint8_t *wt = st + C::kAOff;
+      tma_load_2d(wt, &tmW0, &bars->full[kb], n0, k0);
+      tma_load_2d(wt + kWBox, &tmW0, &bars->full[kb], n0 + 64, k0);
+      if (C::NA > 1) {
+        tma_load_2d(wt + 2 * kWBox, &tmW1, &bars->full[kb], n0, k0);
+        tma_load_2d(wt + 3 * kWBox, &tmW1, &bars->full[kb], n0 + 64, k0);
+      }
+    }
+  }
   pdl_wait();  // inputs may be produced by the preceding kernel
+  // PDL trigger: by default late — each warp triggers once its streaming
+  // role is done (last TMA issued / last MMA issued / last stage consumed),
+  // so the next evaluation's CTAs become resident (two-per-SM configs) and
+  // prefetch their static weights while this grid drains.  Experiment flag
+  // 8: trigger at once.
+  const bool early_trigger = p.dbg_flags & 8;
+  if (early_trigger) pdl_launch();
 
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer
     if (elect_one()) {
-      for (int kb = 0; kb < nkb; ++kb) {
+      // X (and RMS: G) boxes of the prefetched stages
+      for (int kb = 0; kb < npre; ++kb) {
+        uint8_t *st = stages + kb * C::kStage;
+        if (C::kTmaX) {
+          tma_load_2d(st + C::kBOff, &tmX, &bars->full[kb], kbase + kb * kBK, 0);
+        } else {
+          mbar_expect_tx(&bars->xg_full[kb], C::kXGBytes);
+          tma_load_2d(st + C::kXRawOff, &tmX, &bars->xg_full[kb], kbase + kb * kBK, 0);
+          tma_load_2d(st + C::kGOff, &tmA, &bars->xg_full[kb], kbase + kb * kBK, 0);
+        }
+      }
+      for (int kb = npre; kb < nkb; ++kb) {
         const int s = kb % STAGES;
         mbar_wait(&bars->empty[s], ((kb / STAGES) & 1) ^ 1);
         uint8_t *st = stages + s * C::kStage;
-        mbar_expect_tx(&bars->full[s], C::kStage);
+        if (MODE == MODE_RMS) {  // raw X and G first: the B-tile build is on the critical path
+          mbar_expect_tx(&bars->xg_full[s], C::kXGBytes);
+          tma_load_2d(st + C::kXRawOff, &tmX, &bars->xg_full[s], kbase + kb * kBK, 0);
+          tma_load_2d(st + C::kGOff, &tmA, &bars->xg_full[s], kbase + kb * kBK, 0);
+        }
+        mbar_expect_tx(&bars->full[s], C::kFullBytes);
         const int k0 = kbase + kb * kBK;
-        if (MODE == MODE_LORA) tma_load_2d(st, &tmA, &bars->full[s], 0, k0);
+        if (MODE == MODE_LORA) tma_load_2d(st + C::kARawOff, &tmA, &bars->full[s], 0, k0);
         uint8_t *wt = st + C::kAOff;
         tma_load_2d(wt, &tmW0, &bars->full[s], n0, k0);
         tma_load_2d(wt + kWBox, &tmW0, &bars->full[s], n0 + 64, k0);
@@ -153,21 +226,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (C::kTmaX) tma_load_2d(nx, &tmX, &bars->full[s], k0, 0);
       }
-      pdl_launch();  // all input reads issued: the next kernel may start its prologue
+      TPO_T(10);
     }
+    __syncwarp();
+    if (!early_trigger) pdl_launch();
   } else if (warp == 1) {
     // -------------------------------------------------------- MMA issuer
     constexpr uint32_t idesc = idesc_bf16(kTileN, kTok, /*a MN-major*/ true, /*b K-major*/ false);
-    if (MODE == MODE_RMS) mbar_wait(&bars->b_ready, 0);
     for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % STAGES;
       mbar_wait(&bars->full[s], (kb / STAGES) & 1);
+      if (kb == 0 && lane == 0) TPO_T(8);
+      if (MODE == MODE_RMS) mbar_wait(&bars->b_full[s], (kb / STAGES) & 1);
+      if (kb == 0 && lane == 0) TPO_T(9);
       tc_fence_after();
+      if (p.dbg_flags & 4) {  // experiment: free stages without the MMA
+        if (elect_one()) {
+          mbar_arrive(&bars->empty[s]);
+          if (kb == nkb - 1) mbar_arrive(&bars->tmem_full);
+        }
+        __syncwarp();
+        continue;
+      }
       if (elect_one()) {
         uint8_t *st = stages + s * C::kStage;
         uint8_t *wt = st + C::kAOff;
-        const uint32_t xs = MODE == MODE_RMS ? smem_u32(bregion + kb * kXTile)
-                                             : smem_u32(wt + C::NA * 2 * kWBox);
+        const uint32_t xs = smem_u32(st + C::kBOff);
 #pragma unroll
         for (int kk = 0; kk < kBK / 16; ++kk) {
           const uint64_t bdesc = sdesc_sw128(xs + kk * 32, 16, 1024);
@@ -175,12 +259,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int w = 0; w < C::NA; ++w) {
             const uint64_t adesc = sdesc_sw128(smem_u32(wt + w * 2 * kWBox) + kk * 16 * 128, kWBox, 1024);
             umma_bf16(tmem + w * kTok, adesc, bdesc, idesc, (kb | kk) != 0);
-          }
-          if (MODE == MODE_LORA) {
-            // XA^T: the A box as a 128-row MN-major operand whose second
-            // 64-row atom is the W box behind it (result rows >= 16 unused)
-            const uint64_t adesc = sdesc_sw128(smem_u32(st) + kk * 16 * 128, kWBox, 1024);
-            umma_bf16(tmem + kTok, adesc, bdesc, idesc, (kb | kk) != 0);
           }
         }
         umma_commit(&bars->empty[s]);
@@ -191,82 +269,185 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       __syncwarp();
     }
+    if (!early_trigger) pdl_launch();
   } else {
     // ------------------------------------- auxiliary / epilogue warps 2..5
     const int t = threadIdx.x - 64;
-    float sumsq = 0.f;
+    float sumsq = 0.f;       // RMS: Σx² of token t/16 over this CTA's K range
+    float xa0 = 0.f, xa1 = 0.f;  // LoRA: XA[t/8][2(t%8)], XA[t/8][2(t%8)+1] partials
+    // Epilogue operands from global memory are loaded now, off the critical
+    // path (under a saturated HBM a dependent load costs ~1 µs): LoRA B̄
+    // column of the row this thread finalizes, RMS D.
+    const int erow = (warp & 3) * 32 + lane;
+    float bcol[MODE == MODE_LORA ? 16 : 1];
+    float dsc = 0.f;
+    if (MODE == MODE_LORA && erow / rows_per == int(rank)) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) bcol[r] = __bfloat162float(p.lora_b[size_t(r) * p.N + n0 + erow]);
+    }
+    if (MODE == MODE_RMS) dsc = __bfloat162float(p.dscale[0]);
     if (MODE == MODE_RMS) {
-      // B region: per k block, 16 rows (x·g hi for tokens 0-7, lo for 8-15)
-      // x 64 k, K-major with the 128-B swizzle a TMA box would have.  Thread
-      // t owns token t/16 so its running Σx² stays per token.
+      // Per stage: B tile rows 0-7 = bf16(x·g) (hi), rows 8-15 = the exact
+      // residual x·g - hi (lo), K-major with the 128-B swizzle.  Thread t
+      // owns token t/16 and k = 4·(t%16) .. +3, so Σx² stays per token.
       const int tok = t >> 4, sub = t & 15;
-      const int items = nkb * 8;
-      for (int base = sub; base < items; base += 16 * 8) {
-        uint4 xv[8], gv[8];  // loads of up to 8 items in flight at once
+      const int c = sub >> 1, half = (sub & 1) * 8;
+      const uint32_t off_hi = (tok >> 3) * 1024 + (tok & 7) * 128 + ((c ^ (tok & 7)) << 4) + half;
+      const int rl = tok + 8;
+      const uint32_t off_lo = (rl >> 3) * 1024 + (rl & 7) * 128 + ((c ^ (rl & 7)) << 4) + half;
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % STAGES;
+        mbar_wait(&bars->xg_full[s], (kb / STAGES) & 1);
+        uint8_t *st = stages + s * C::kStage;
+        const uint2 xr = *reinterpret_cast<const uint2 *>(st + C::kXRawOff + tok * 128 + sub * 8);
+        const uint2 gr = *reinterpret_cast<const uint2 *>(st + C::kGOff + sub * 8);
+        const __nv_bfloat162 *x2 = reinterpret_cast<const __nv_bfloat162 *>(&xr);
+        const __nv_bfloat162 *g2 = reinterpret_cast<const __nv_bfloat162 *>(&gr);
+        uint32_t hi[2], lo[2];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int item = base + u * 16;
-          xv[u] = gv[u] = make_uint4(0, 0, 0, 0);
-          if (item < items) {
-            const int k = kbase + (item >> 3) * kBK + (item & 7) * 8;
-            if (tok < p.tokens) xv[u] = *reinterpret_cast<const uint4 *>(p.x + size_t(tok) * p.K + k);
-            gv[u] = *reinterpret_cast<const uint4 *>(p.g + k);
-          }
+        for (int j = 0; j < 2; ++j) {
+          float2 xf = __bfloat1622float2(x2[j]), gf = __bfloat1622float2(g2[j]);
+          sumsq += xf.x * xf.x + xf.y * xf.y;
+          float p0 = xf.x * gf.x, p1 = xf.y * gf.y;  // exact in fp32 (8b x 8b mantissas)
+          __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
+          float2 hf = __bfloat1622float2(h);
+          __nv_bfloat162 l = __floats2bfloat162_rn(p0 - hf.x, p1 - hf.y);  // exact residual
+          hi[j] = *reinterpret_cast<uint32_t *>(&h);
+          lo[j] = *reinterpret_cast<uint32_t *>(&l);
         }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int item = base + u * 16;
-          if (item >= items) break;
-          const int kb = item >> 3, c = item & 7;
-          const __nv_bfloat162 *x2 = reinterpret_cast<const __nv_bfloat162 *>(&xv[u]);
-          const __nv_bfloat162 *g2 = reinterpret_cast<const __nv_bfloat162 *>(&gv[u]);
-          uint32_t hi[4], lo[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            float2 xf = __bfloat1622float2(x2[j]), gf = __bfloat1622float2(g2[j]);
-            sumsq += xf.x * xf.x + xf.y * xf.y;
-            float p0 = xf.x * gf.x, p1 = xf.y * gf.y;  // exact in fp32 (8b x 8b mantissas)
-            __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
-            float2 hf = __bfloat1622float2(h);
-            __nv_bfloat162 l = __floats2bfloat162_rn(p0 - hf.x, p1 - hf.y);  // exact residual
-            hi[j] = *reinterpret_cast<uint32_t *>(&h);
-            lo[j] = *reinterpret_cast<uint32_t *>(&l);
-          }
-          uint8_t *tb = bregion + kb * kXTile;
-          const int rh = tok, rl = tok + 8;
-          *reinterpret_cast<uint4 *>(tb + (rh >> 3) * 1024 + (rh & 7) * 128 + ((c ^ (rh & 7)) << 4)) =
-              make_uint4(hi[0], hi[1], hi[2], hi[3]);
-          *reinterpret_cast<uint4 *>(tb + (rl >> 3) * 1024 + (rl & 7) * 128 + ((c ^ (rl & 7)) << 4)) =
-              make_uint4(lo[0], lo[1], lo[2], lo[3]);
-        }
+        *reinterpret_cast<uint2 *>(st + C::kBOff + off_hi) = make_uint2(hi[0], hi[1]);
+        *reinterpret_cast<uint2 *>(st + C::kBOff + off_lo) = make_uint2(lo[0], lo[1]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars->b_full[s]);
       }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bars->b_ready);
 #pragma unroll
       for (int o = 8; o; o >>= 1) sumsq += __shfl_xor_sync(0xffffffffu, sumsq, o);
     }
+    if (MODE == MODE_LORA) {
+      // XA = X·A (16 tokens x 16 ranks over this CTA's K range) on the warp
+      // MMA path of the otherwise idle epilogue warps, from the staged X^T
+      // tile (K-major, 128-B swizzle) and the raw A box [64 k][16 r]: warp q
+      // takes k16 step q of every stage, two m16n8k16 bf16 MMAs with fp32
+      // accumulation (exact products), while the tensor cores run X·W.
+      const int q = warp & 3;
+      float c[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      const int mi = lane >> 3, ri = lane & 7;
+      const int tok = ri + 8 * (mi & 1);
+      const int kch = 2 * q + (mi >> 1);
+      const uint32_t a_off = C::kBOff + (tok >> 3) * 1024 + (tok & 7) * 128 + ((kch ^ (tok & 7)) << 4);
+      const uint32_t b_off = C::kARawOff + (16 * q + ri + 8 * (mi & 1)) * 32 + (mi >> 1) * 16;
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % STAGES;
+        mbar_wait(&bars->full[s], (kb / STAGES) & 1);
+        const uint32_t st = smem_u32(stages + s * C::kStage);
+        uint32_t af[4], bf[4];
+        asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(af[0]), "=r"(af[1]), "=r"(af[2]), "=r"(af[3]) : "r"(st + a_off));
+        asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(bf[0]), "=r"(bf[1]), "=r"(bf[2]), "=r"(bf[3]) : "r"(st + b_off));
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars->empty[s]);  // stage also released by the MMA commit
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+          asm volatile(
+              "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+              "{%8,%9}, {%0,%1,%2,%3};"
+              : "+f"(c[j][0]), "+f"(c[j][1]), "+f"(c[j][2]), "+f"(c[j][3])
+              : "r"(af[0]), "r"(af[1]), "r"(af[2]), "r"(af[3]), "r"(bf[2 * j]), "r"(bf[2 * j + 1]));
+      }
+      // per-warp partials -> xa_w[q][token][r]
+      float *xw = xa_w + q * 256;
+      const int g = lane >> 2, cc = 2 * (lane & 3);
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        *reinterpret_cast<float2 *>(xw + g * 16 + 8 * j + cc) = make_float2(c[j][0], c[j][1]);
+        *reinterpret_cast<float2 *>(xw + (g + 8) * 16 + 8 * j + cc) = make_float2(c[j][2], c[j][3]);
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      // thread t: XA[t/8][2(t%8)..+1] = Σ over the 4 warps
+      const int i0 = (t >> 3) * 16 + (t & 7) * 2;
+      xa0 = (xa_w[i0] + xa_w[256 + i0]) + (xa_w[512 + i0] + xa_w[768 + i0]);
+      xa1 = (xa_w[i0 + 1] + xa_w[256 + i0 + 1]) + (xa_w[512 + i0 + 1] + xa_w[768 + i0 + 1]);
+    }
 
+    if (!early_trigger) pdl_launch();
     // ---------------------------------------------------------- epilogue
+    // Row `row` of the 128-column tile is held (in TMEM lane `row`) by the
+    // thread (warp quarter q, lane); CTA `row / rows_per` of the cluster owns
+    // it: non-owners push their partial row to the owner over DSMEM, owners
+    // sum the S partials and run the post-loop ops.  Side data (RMS Σx² per
+    // token, LoRA XA partials) is exchanged and reduced *before* the last
+    // MMA completes, off the critical path.
     const int q = warp & 3;              // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;       // UMMA M index = output column in the tile
     const int n = n0 + row;
     const int owner = row / rows_per;    // CTA of the cluster finishing this row
-    // finalize mapping (S > 1): all 128 epilogue threads share this CTA's
-    // rows_per owned rows; thread t takes local row t % rows_per and token
-    // group t / rows_per
-    const int f_row = int(rank) * rows_per + (S > 1 ? t % rows_per : row - int(rank) * rows_per);
-    float bcol[16];                      // LoRA: B̄[:, n] of the finalized row
-    float dsc = 0.f;                     // RMS: the D input
-    if (MODE == MODE_LORA)
+    const bool mine = owner == int(rank);
+    constexpr int NV = MODE == MODE_RMS ? 8 : 16;  // floats per row partial
+    constexpr int T = MODE == MODE_LORA ? 16 : 8;  // tokens
+    float post[T];                        // RMS: 1/sqrt(Σx²·D) per token; LoRA: (XA·B̄)[t, n]
+    if (MODE == MODE_RMS) {
+      if ((t & 15) == 0) side[rank * kSide + (t >> 4)] = sumsq;
+    }
+    if (MODE == MODE_LORA) *reinterpret_cast<float2 *>(side + rank * kSide + (t >> 3) * 16 + (t & 7) * 2) =
+        make_float2(xa0, xa1);
+    if (MODE != MODE_GATED) asm volatile("bar.sync 1, 128;" ::: "memory");  // own side block written
+    const bool xchg = !(p.dbg_flags & 2);  // experiment 2: no DSMEM exchange
+    if (S > 1) {
+      cluster_wait();  // every peer has initialised its barriers
+      if (xchg && MODE != MODE_GATED && t * 4 < kSide) {
+        const float *src = side + rank * kSide + t * 4;
+        for (int o = 1; o < S; ++o) {
+          const uint32_t dst_rank = (rank + o) % S;
+          st_async4(map_rank(src, dst_rank), src[0], src[1], src[2], src[3],
+                    map_rank(&bars->recv_side, dst_rank));
+        }
+      }
+      if (xchg && MODE != MODE_GATED) mbar_wait(&bars->recv_side, 0);
+    }
+    if (MODE == MODE_RMS && mine) {
 #pragma unroll
-      for (int r = 0; r < 16; ++r) bcol[r] = __bfloat162float(p.lora_b[size_t(r) * p.N + n0 + f_row]);
-    if (MODE == MODE_RMS) dsc = __bfloat162float(p.dscale[0]);
+      for (int tk = 0; tk < 8; ++tk) {
+        float ss = 0.f;
+        for (int rr = 0; rr < S; ++rr) ss += side[rr * kSide + tk];
+        post[tk] = 1.0f / sqrtf(ss * dsc);
+      }
+    }
+    if (MODE == MODE_LORA) {
+      // XA total (Σ over the cluster's K ranges), 2 entries per thread
+      for (int i = t * 2; i < t * 2 + 2; ++i) {
+        float v = 0.f;
+        for (int rr = 0; rr < S; ++rr) v += side[rr * kSide + i];
+        xa_tot[i] = v;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (mine) {
+#pragma unroll
+        for (int tk = 0; tk < 16; ++tk) post[tk] = 0.f;
+#pragma unroll
+        for (int tk = 0; tk < 16; ++tk) {
+          const float4 *xr = reinterpret_cast<const float4 *>(xa_tot + tk * 16);
+          float o = 0.f;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float4 x = xr[i];
+            o = fmaf(x.x, bcol[4 * i], o);
+            o = fmaf(x.y, bcol[4 * i + 1], o);
+            o = fmaf(x.z, bcol[4 * i + 2], o);
+            o = fmaf(x.w, bcol[4 * i + 3], o);
+          }
+          post[tk] = o;
+        }
+      }
+    }
+
+    // ---- critical path: last MMA -> TMEM -> DSMEM -> owner -> HBM
     mbar_wait(&bars->tmem_full, 0);
     if (threadIdx.x == 64) TPO_T(5);
     __syncwarp();  // tcgen05.ld is .sync.aligned: the warp must be converged
     tc_fence_after();
-    float acc[16], xa[16];
+    float acc[16];
     {
       float v[16];
       tmem_ld16(tmem + (uint32_t(q * 32) << 16), v);
@@ -281,127 +462,38 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else {
 #pragma unroll
         for (int i = 0; i < 16; ++i) acc[i] = v[i];
-        tmem_ld16(tmem + (uint32_t(q * 32) << 16) + kTok, xa);  // XA^T row r = row (< 16)
       }
     }
-    // side values this CTA contributes to every owner: RMS Σx² per token,
-    // LoRA XA^T rows 0..15 (held by the threads of rows 0..15)
-    if (MODE == MODE_RMS && (t & 15) == 0) side[rank * kSide + (t >> 4)] = sumsq;
-    if (MODE == MODE_LORA && row < 16)
-#pragma unroll
-      for (int i = 0; i < 16; ++i) side[rank * kSide + row * 16 + i] = xa[i];
-    if (MODE == MODE_RMS) asm volatile("bar.sync 1, 128;" ::: "memory");  // Σx² slots written
-    if (S > 1) {
-      cluster_wait();  // every peer has initialised its barriers
-      // row partials -> owner; red slot [src rank][row - owner*rows_per]
-      if (owner != int(rank)) {
-        const uint32_t dst = map_rank(red + (int(rank) * rows_per + (row - owner * rows_per)) * 16, owner);
+    if (S > 1 && xchg) {
+      if (!mine) {
+        // red slot [src rank][row - owner*rows_per][NV]
+        const uint32_t dst = map_rank(red + (int(rank) * rows_per + (row - owner * rows_per)) * NV, owner);
         const uint32_t mb = map_rank(&bars->recv, owner);
 #pragma unroll
-        for (int i = 0; i < 16; i += 4) st_async4(dst + i * 4, acc[i], acc[i + 1], acc[i + 2], acc[i + 3], mb);
-      }
-      // side block -> every peer (RMS: 8 floats from 2 threads; LoRA: 16 rows)
-      if (MODE == MODE_RMS && t < 2) {
-        const float *src = side + rank * kSide + t * 4;
-        for (int o = 0; o < S; ++o) {
-          if (o == int(rank)) continue;
-          st_async4(map_rank(src, o), src[0], src[1], src[2], src[3], map_rank(&bars->recv, o));
-        }
-      }
-      if (MODE == MODE_LORA && row < 16) {
-        for (int o = 0; o < S; ++o) {
-          if (o == int(rank)) continue;
-          const uint32_t dst = map_rank(side + rank * kSide + row * 16, o);
-          const uint32_t mb = map_rank(&bars->recv, o);
-#pragma unroll
-          for (int i = 0; i < 16; i += 4) st_async4(dst + i * 4, xa[i], xa[i + 1], xa[i + 2], xa[i + 3], mb);
-        }
-      }
-      if (threadIdx.x == 64) TPO_T(4);
-      mbar_wait(&bars->recv, 0);  // all peers' partials have landed
-      if (threadIdx.x == 64) TPO_T(6);
-    }
-    if (MODE == MODE_LORA) {
-      asm volatile("bar.sync 1, 128;" ::: "memory");  // own XA^T rows written
-      // XA = Σ_ranks XA^T partials (2 entries per thread) -> xa_tot[r][t]
-      for (int i = t * 2; i < t * 2 + 2; ++i) {
-        float v = 0.f;
-        for (int rr = 0; rr < S; ++rr) v += side[rr * kSide + i];
-        xa_tot[i] = v;
-      }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-    }
-    if (p.dbg_flags & 1) {
-    } else if (S == 1) {
-      // single CTA per tile: every thread finishes its own row, all tokens
-      if (MODE == MODE_GATED) {
-#pragma unroll
-        for (int tk = 0; tk < 8; ++tk)
-          if (tk < p.tokens) p.out[size_t(tk) * p.N + n] = silu(acc[tk]) * acc[8 + tk];
-      } else if (MODE == MODE_RMS) {
-#pragma unroll
-        for (int tk = 0; tk < 8; ++tk)
-          if (tk < p.tokens) p.out[size_t(tk) * p.N + n] = acc[tk] / sqrtf(side[tk] * dsc);
+        for (int i = 0; i < NV; i += 4) st_async4(dst + i * 4, acc[i], acc[i + 1], acc[i + 2], acc[i + 3], mb);
+        if (threadIdx.x == 64) TPO_T(4);
       } else {
+        mbar_wait(&bars->recv, 0);  // all peers' partials of the owned rows have landed
+        if (lane == 0) TPO_T(6);
+        for (int rr = 0; rr < S; ++rr) {
+          if (rr == int(rank)) continue;
+          const float4 *src = reinterpret_cast<const float4 *>(red + (rr * rows_per + (row - int(rank) * rows_per)) * NV);
 #pragma unroll
-        for (int r = 0; r < 16; ++r) {
-          const float4 *xr = reinterpret_cast<const float4 *>(xa_tot + r * 16);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const float4 x = xr[i];
-            acc[4 * i] = fmaf(x.x, bcol[r], acc[4 * i]);
-            acc[4 * i + 1] = fmaf(x.y, bcol[r], acc[4 * i + 1]);
-            acc[4 * i + 2] = fmaf(x.z, bcol[r], acc[4 * i + 2]);
-            acc[4 * i + 3] = fmaf(x.w, bcol[r], acc[4 * i + 3]);
+          for (int i = 0; i < NV / 4; ++i) {
+            const float4 v = src[i];
+            acc[4 * i] += v.x, acc[4 * i + 1] += v.y, acc[4 * i + 2] += v.z, acc[4 * i + 3] += v.w;
           }
         }
-#pragma unroll
-        for (int tk = 0; tk < 16; ++tk)
-          if (tk < p.tokens) p.out[size_t(tk) * p.N + n] = acc[tk];
       }
-    } else {
-      // the owner's own partial joins the peers' in red, then all 128
-      // threads finish (local row, token group) items of the owned rows
-      if (owner == int(rank)) {
-        float4 *dst = reinterpret_cast<float4 *>(red + (int(rank) * rows_per + (row - owner * rows_per)) * 16);
+    }
+    if (mine && !(p.dbg_flags & 1)) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) dst[i] = make_float4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
-      }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      constexpr int ngrp = 128 / rows_per;
-      const int lr = t % rows_per, grp = t / rows_per;
-      const int nn = n0 + int(rank) * rows_per + lr;
-      constexpr int T = MODE == MODE_LORA ? 16 : 8;  // tokens
-      constexpr int tpg = T / ngrp;                  // tokens handled by this thread
-      const int t0 = grp * tpg;
-      float a[tpg], a3[tpg];
-#pragma unroll
-      for (int i = 0; i < tpg; ++i) {
-        a[i] = 0.f;
-        if (MODE == MODE_GATED) a3[i] = 0.f;
-#pragma unroll
-        for (int rr = 0; rr < S; ++rr) {
-          const float *src = red + (rr * rows_per + lr) * 16;
-          a[i] += src[t0 + i];
-          if (MODE == MODE_GATED) a3[i] += src[8 + t0 + i];
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < tpg; ++i) {
-        const int tk = t0 + i;
+      for (int tk = 0; tk < T; ++tk) {
         float o;
-        if (MODE == MODE_GATED) {
-          o = silu(a[i]) * a3[i];
-        } else if (MODE == MODE_RMS) {
-          float ss = 0.f;
-          for (int rr = 0; rr < S; ++rr) ss += side[rr * kSide + tk];
-          o = a[i] / sqrtf(ss * dsc);
-        } else {
-          o = a[i];
-#pragma unroll
-          for (int r = 0; r < 16; ++r) o = fmaf(xa_tot[r * 16 + tk], bcol[r], o);
-        }
-        if (tk < p.tokens) p.out[size_t(tk) * p.N + nn] = o;
+        if (MODE == MODE_GATED) o = silu(acc[tk]) * acc[8 + tk];
+        else if (MODE == MODE_RMS) o = acc[tk] * post[tk];
+        else o = acc[tk] + post[tk];
+        if (tk < p.tokens) p.out[size_t(tk) * p.N + n] = o;
       }
     }
   }
@@ -424,16 +516,18 @@ template <int MODE, int STAGES, int S>
 size_t skinny_smem(const SkinnyParams &p) {
   using C = Cfg<MODE>;
   const int nkb = p.k_per_cta / kBK;
-  size_t b = size_t(STAGES) * C::kStage + (MODE == MODE_RMS ? size_t(nkb) * kXTile : 0) +
-             size_t(kTileN) * 16 * 4 + size_t(kMaxSplit) * 256 * 4 + 256 * 4 + sizeof(Bars);
+  (void)nkb;
+  size_t b = size_t(STAGES) * C::kStage +
+             (S > 1 ? size_t(kTileN) * 16 * 4 : 0) + size_t(S) * C::kSide * 4 +
+             (MODE == MODE_LORA ? (256 + 1024) * 4 : 0) + sizeof(Bars);
   return b + 1024;
 }
 
-template <int MODE, int STAGES, int S>
+template <int MODE, int STAGES, int S, int MINB>
 cudaError_t launch_t(const CUtensorMap *maps, const SkinnyParams &p, cudaStream_t st) {
   if (p.ksplit != S) return cudaErrorInvalidValue;
   const size_t smem = skinny_smem<MODE, STAGES, S>(p);
-  auto kern = skinny_kernel<MODE, STAGES, S>;
+  auto kern = skinny_kernel<MODE, STAGES, S, MINB>;
   static size_t configured = 0;  // per instantiation: raise the smem limit once
   if (smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -453,7 +547,7 @@ cudaError_t launch_t(const CUtensorMap *maps, const SkinnyParams &p, cudaStream_
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 2;
+  cfg.numAttrs = std::getenv("TPO_NO_PDL") ? 1 : 2;
   return cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], p);
 }
 
@@ -461,23 +555,29 @@ cudaError_t launch_t(const CUtensorMap *maps, const SkinnyParams &p, cudaStream_
 
 using namespace tpo_fused;
 
-#define TPO_SKINNY_CASES(X)                                                                    \
-  X(MODE_GATED, 4, 1) X(MODE_GATED, 6, 1) X(MODE_GATED, 3, 2) X(MODE_RMS, 4, 4) X(MODE_RMS, 6, 4) \
-  X(MODE_RMS, 4, 2) X(MODE_RMS, 6, 2) X(MODE_RMS, 6, 1) X(MODE_LORA, 4, 4) X(MODE_LORA, 6, 4)      \
-  X(MODE_LORA, 4, 2) X(MODE_LORA, 6, 2) X(MODE_LORA, 6, 1)
+// (mode, stages, cluster split, CTAs per SM)
+#define TPO_SKINNY_CASES(X)                                                                     \
+  X(MODE_GATED, 4, 1, 1) X(MODE_GATED, 6, 1, 1) X(MODE_GATED, 3, 1, 2) X(MODE_GATED, 3, 2, 1)     \
+  X(MODE_GATED, 6, 2, 1) X(MODE_RMS, 4, 4, 2) X(MODE_RMS, 6, 4, 1) X(MODE_RMS, 8, 4, 1)            \
+  X(MODE_RMS, 10, 4, 1) X(MODE_RMS, 4, 2, 1) X(MODE_RMS, 6, 2, 1) X(MODE_RMS, 8, 2, 1)             \
+  X(MODE_RMS, 6, 1, 1) X(MODE_LORA, 4, 4, 2) X(MODE_LORA, 6, 4, 1) X(MODE_LORA, 8, 4, 1)           \
+  X(MODE_LORA, 10, 4, 1) X(MODE_LORA, 6, 2, 1) X(MODE_LORA, 8, 2, 1) X(MODE_LORA, 6, 1, 1)
 
-extern "C" int tpo_skinny_launch(int mode, int stages, const CUtensorMap *maps,
+extern "C" int tpo_skinny_launch(int mode, int stages, int minb, const CUtensorMap *maps,
                                  const SkinnyParams *p, cudaStream_t st) {
-#define TPO_CASE(M, ST, S) \
-  if (mode == M && stages == ST && p->ksplit == S) return int(launch_t<M, ST, S>(maps, *p, st));
+#define TPO_CASE(M, ST, S, MB)                                  \
+  if (mode == M && stages == ST && p->ksplit == S && minb == MB) \
+    return int(launch_t<M, ST, S, MB>(maps, *p, st));
   TPO_SKINNY_CASES(TPO_CASE)
 #undef TPO_CASE
   return int(cudaErrorInvalidValue);
 }
 
-extern "C" size_t tpo_skinny_smem(int mode, int stages, const SkinnyParams *p) {
-#define TPO_CASE(M, ST, S) \
-  if (mode == M && stages == ST && p->ksplit == S) return skinny_smem<M, ST, S>(*p);
+// Shared memory of (mode, stages, split, CTAs per SM) for `p`; 0 when that
+// configuration is not instantiated.
+extern "C" size_t tpo_skinny_smem(int mode, int stages, int minb, const SkinnyParams *p) {
+#define TPO_CASE(M, ST, S, MB) \
+  if (mode == M && stages == ST && p->ksplit == S && minb == MB) return skinny_smem<M, ST, S>(*p);
   TPO_SKINNY_CASES(TPO_CASE)
 #undef TPO_CASE
   return 0;

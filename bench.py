@@ -220,27 +220,27 @@ def run_fused(args, dist, wl):
     per_eval_ms = ms / args.steps
     value = dist.world * args.steps / (ms / 1e3)
 
-    # ---- end to end through the public API with HOST buffers (pinned)
+    # ---- end to end through the C-ABI with HOST buffers: every step copies
+    # that step's inputs host->device (pinned), runs the fused kernel and
+    # copies the output back (tpo_gpu_eval_mugraph_host, synchronous)
     pinned = [x.pin_memory() for x in wl["host"]]
     out_h = torch.empty(wl["out_shape"], dtype=torch.float32).pin_memory()
-    dev_in = sets[0]
     e2e_steps = 0 if args.profile else max(3, min(args.steps, 50))
+    ctx.eval_mugraph_host(g, pinned, outputs=[out_h], stream=st)  # warm the staging buffers
     torch.cuda.synchronize()
     dist.barrier()
     with torch.cuda.stream(stream):
         e0.record(stream)
         for i in range(e2e_steps):
-            for d, h in zip(dev_in, pinned):
-                d.copy_(h, non_blocking=True)
-            ctx.eval_mugraph(g, dev_in, outputs=[outs[0]], stream=st)
-            out_h.copy_(outs[0], non_blocking=True)
+            ctx.eval_mugraph_host(g, pinned, outputs=[out_h], stream=st)
         e1.record(stream)
     e1.synchronize()
     dist.barrier()
     e2e_ms = max(dist.max(e0.elapsed_time(e1)), 1e-9)
     e2e = {"value": round(dist.world * e2e_steps / (e2e_ms / 1e3), 3), "unit": "evals/s",
            "h2d_bytes_per_step": int(wl["in_bytes"]), "d2h_bytes_per_step": int(wl["out_bytes"]),
-           "ms_per_step": round(e2e_ms / max(e2e_steps, 1), 4)}
+           "ms_per_step": round(e2e_ms / max(e2e_steps, 1), 4),
+           "path": "tpo_gpu_eval_mugraph_host (C-ABI, pinned host buffers, copies in the timed region)"}
 
     peak, peak_kind = peaks()
     achieved = alg / (per_eval_ms / 1e3) / 1e9

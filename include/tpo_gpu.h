@@ -14,7 +14,7 @@
  * re-entrant).
  *
  * Reference interfaces replaced (file:line in /root/reference):
- *   tpo_gpu_eval_mugraph            <- tpo::interp::eval_mugraph
+ *   tpo_gpu_eval_mugraph(_host)     <- tpo::interp::eval_mugraph
  *                                      proj/core/include/tpo/interp/interp.hpp:47-48
  *   tpo_gpu_ff_eval                 <- tpo::verify::ff_eval (+ sample_inputs, sample_omega,
  *                                      SiluTables::sample) proj/core/include/tpo/verify/ffeval.hpp:58-67,
@@ -127,6 +127,15 @@ int tpo_gpu_validate(const char *graph_json, int64_t smem_bytes, int64_t elem_si
  * enqueued on `cuda_stream` (NULL = the legacy default stream); asynchronous. */
 int tpo_gpu_eval_mugraph(tpo_gpu_ctx *ctx, const tpo_gpu_graph *g, const void *const *in_dev,
                          const int32_t *in_dtype, float *const *out_dev, void *cuda_stream);
+
+/* Same evaluation from and to HOST buffers (pageable or pinned): inputs are
+ * copied host->device (TPO_DTYPE_BF16 as is; TPO_DTYPE_F32 converted to bf16
+ * on the device, round-to-nearest-even), the fused kernel runs, the fp32
+ * outputs are copied back; synchronous on `cuda_stream` (NULL = the context
+ * stream).  The call shape of tpo::interp::eval_mugraph
+ * (proj/core/include/tpo/interp/interp.hpp:47-48) for host-resident tensors. */
+int tpo_gpu_eval_mugraph_host(tpo_gpu_ctx *ctx, const tpo_gpu_graph *g, const void *const *in_host,
+                              const int32_t *in_dtype, float *const *out_host, void *cuda_stream);
 
 /* One verifier attempt for one graph, exactly as equiv.cpp:57-68 draws it
  * (Rng::derive(seed, stream); inputs; omega; SiLU tables iff with_silu).

@@ -1,0 +1,163 @@
+// Integration check of the reference-side binding (tpo_gpu_backend.*): built
+// against the reference's own headers and objects (oracle/Makefile, target
+// integration_check), it loads graphs with the reference's JSON reader and
+// compares the GPU backend with the reference's CPU entry points.
+//   integration_check host <graphs.json>   no GPU: compile, op_madds, errors
+//   integration_check gpu  <graphs.json>   verdicts bit-exact, fp within tolerance
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <cstdio>
+#include <fstream>
+#include <string>
+
+#include "tpo/interp/interp.hpp"
+#include "tpo/ir/serialize.hpp"
+#include "tpo/ir/shape_infer.hpp"
+#include "tpo/util/rng.hpp"
+#include "tpo/verify/equiv.hpp"
+#include "tpo_gpu_backend.hpp"
+
+using namespace tpo;
+
+static int failures = 0;
+#define CHECK(c, ...)                          \
+  do {                                         \
+    if (!(c)) {                                \
+      std::printf("FAIL %s:%d ", __FILE__, __LINE__); \
+      std::printf(__VA_ARGS__);                \
+      std::printf("\n");                       \
+      ++failures;                              \
+    }                                          \
+  } while (0)
+
+static int64_t ref_madds(const ir::KernelGraph &g);
+
+int main(int argc, char **argv) {
+  if (argc < 3) return 2;
+  const std::string mode = argv[1];
+  std::ifstream f(argv[2]);
+  nlohmann::json all = nlohmann::json::parse(f);
+  auto G = [&](const std::string &tag) { return ir::kernel_graph_from_json(all.at(tag)); };
+
+  // ---- host: compile through the binding, op_madds, error mapping
+  int n = 0;
+  for (auto it = all.begin(); it != all.end(); ++it) {
+    ir::KernelGraph g = ir::kernel_graph_from_json(it.value());
+    try {
+      gpu::CompiledGraph cg(nullptr, g);
+      CHECK(cg.op_madds() == ref_madds(g), "%s madds %lld vs %lld", it.key().c_str(),
+            (long long)cg.op_madds(), (long long)ref_madds(g));
+      ++n;
+    } catch (const Error &e) {
+      CHECK(false, "%s compile threw %s", it.key().c_str(), e.what());
+    }
+  }
+  for (const char *fam : {"rmsnorm", "gatedmlp", "gqa", "lora"})
+    CHECK(gpu::CompiledGraph(nullptr, G(std::string("fused/") + fam)).has_fused_kernel(), "fused %s", fam);
+  CHECK(!gpu::CompiledGraph(nullptr, G("fp/gatedmlp/program")).has_fused_kernel(), "flat program");
+  try {
+    nlohmann::json bad = all.at("edge/identity");
+    bad["ops"] = nlohmann::json::array({{{"id", 0}, {"type", "nope"}}});
+    gpu::CompiledGraph cg(nullptr, ir::kernel_graph_from_json(all.at("edge/identity")));
+    const std::string js = bad.dump();
+    tpo_gpu_graph *h = nullptr;
+    CHECK(tpo_gpu_compile(nullptr, js.c_str(), &h) == 1000 + int(ErrCode::ParseError), "ParseError status");
+  } catch (const Error &e) {
+    CHECK(false, "unexpected %s", e.what());
+  }
+  std::printf("host: %d graphs compiled, op_madds equal to the reference\n", n);
+  if (mode != "gpu") return failures ? 1 : 0;
+
+  // ---- gpu: verdicts bit-exact vs verify::random_test_equivalence
+  gpu::Backend be(0);
+  int nv = 0;
+  for (const char *fam : {"rmsnorm", "gatedmlp", "gqa", "lora"}) {
+    ir::KernelGraph prog = G(std::string(fam) + "/program");
+    for (auto it = all.begin(); it != all.end(); ++it) {
+      if (it.key().rfind(std::string(fam) + "/g", 0) != 0) continue;
+      ir::KernelGraph cand = ir::kernel_graph_from_json(it.value());
+      for (uint64_t seed : {0ull, 17ull}) {
+        verify::VerifyConfig cfg;
+        cfg.seed = seed;
+        cfg.num_tests = 2;
+        verify::EquivVerdict w = verify::random_test_equivalence(prog, cand, cfg);
+        verify::EquivVerdict v = be.random_test_equivalence(prog, cand, cfg);
+        bool same = w.kind == v.kind && w.rounds_run == v.rounds_run && w.resamples == v.resamples &&
+                    w.witness.has_value() == v.witness.has_value();
+        if (same && w.witness)
+          same = w.witness->seed == v.witness->seed && w.witness->round == v.witness->round &&
+                 w.witness->omega == v.witness->omega && w.witness->tensor == v.witness->tensor &&
+                 w.witness->index == v.witness->index;
+        CHECK(same, "%s seed %llu verdict differs", it.key().c_str(), (unsigned long long)seed);
+        ++nv;
+      }
+    }
+  }
+  std::printf("gpu: %d verdicts bit-exact\n", nv);
+  // ---- gpu: eval_mugraph vs interp::eval_mugraph on bf16-representable inputs
+  for (const char *fam : {"rmsnorm", "gatedmlp", "gqa", "lora"}) {
+    ir::KernelGraph mu = G(std::string("fused/") + fam);
+    Rng rng(7);
+    std::vector<interp::FTensor> ins;
+    for (ir::TensorId t : mu.inputs) {
+      interp::FTensor x(mu.tensor(t).shape);
+      const double s = 1.0 / std::sqrt(double(x.shape.dims.back()));
+      for (double &v : x.data) {
+        float fv = float(rng.normal() * (std::string(fam) == "rmsnorm" ? 1.0 : s));
+        uint32_t b;
+        std::memcpy(&b, &fv, 4);
+        b &= 0xFFFF0000u;  // exactly bf16-representable
+        std::memcpy(&fv, &b, 4);
+        v = fv;
+      }
+      ins.push_back(std::move(x));
+    }
+    if (std::string(fam) == "rmsnorm") ins[3].data[0] = 1.0 / double(ins[0].shape.dims[1]);
+    std::vector<interp::FTensor> want = interp::eval_mugraph(mu, ins);
+    std::vector<interp::FTensor> got = be.eval_mugraph(mu, ins);
+    double rms = 0;
+    for (double v : want[0].data) rms += v * v;
+    rms = std::sqrt(rms / double(want[0].data.size()));
+    double worst = 0;
+    for (size_t i = 0; i < want[0].data.size(); ++i)
+      worst = std::max(worst, std::fabs(got[0].data[i] - want[0].data[i]) /
+                                  std::max(std::fabs(want[0].data[i]), rms));
+    CHECK(worst <= 1e-3, "%s eval_mugraph scaled err %.3e", fam, worst);
+    std::printf("gpu: eval_mugraph %s max scaled err %.2e\n", fam, worst);
+  }
+  return failures ? 1 : 0;
+}
+
+static int64_t ref_madds(const ir::KernelGraph &g) {
+  // Σ ir::op_madds (shape_infer.cpp:195-217) with block ops scaled by the
+  // grid and, for in-loop ops, the for-loop (SURVEY §8d work unit)
+  int64_t total = 0;
+  for (const ir::Op &op : g.ops) {
+    if (op.type != ir::OpType::GraphDef) {
+      std::vector<ir::TensorShape> in;
+      for (ir::TensorId t : op.inputs) in.push_back(g.tensor(t).shape);
+      total += ir::op_madds(op.type, op.attrs, in, g.tensor(op.outputs[0]).shape);
+      continue;
+    }
+    const ir::BlockGraph &bg = *op.block;
+    std::vector<bool> post(bg.tensors.size(), false);
+    for (const ir::Op &bop : bg.ops) {
+      if (bop.type == ir::OpType::Accum) {
+        post[size_t(bop.outputs[0])] = true;
+      } else if (bop.type != ir::OpType::InIter && bop.type != ir::OpType::OutSaver) {
+        for (ir::TensorId t : bop.inputs)
+          if (post[size_t(t)]) post[size_t(bop.outputs[0])] = true;
+      }
+    }
+    for (const ir::Op &bop : bg.ops) {
+      if (bop.type == ir::OpType::InIter || bop.type == ir::OpType::OutSaver) continue;
+      std::vector<ir::TensorShape> in;
+      for (ir::TensorId t : bop.inputs) in.push_back(bg.tensor(t).shape);
+      const int64_t m = ir::op_madds(bop.type, bop.attrs, in, bg.tensor(bop.outputs[0]).shape);
+      const bool is_post = bop.type != ir::OpType::Accum && post[size_t(bop.outputs[0])];
+      total += m * bg.grid_product() * (is_post ? 1 : bg.forloop);
+    }
+  }
+  return total;
+}

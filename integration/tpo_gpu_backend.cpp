@@ -1,0 +1,125 @@
+// Reference-side binding of the B200 backend — see tpo_gpu_backend.hpp.
+#include "tpo_gpu_backend.hpp"
+
+#include <string>
+
+#include "tpo/ir/serialize.hpp"
+
+namespace tpo::gpu {
+
+namespace {
+
+// C-ABI status -> the reference's exception (shape.hpp:27-50).
+void check(int rc) {
+  if (rc == 0) return;
+  const char *msg = tpo_gpu_last_error();
+  if (rc >= 1000 && rc < 2000) throw Error(ErrCode(rc - 1000), msg ? msg : "");
+  throw Error(ErrCode::Unsupported, std::string("tpo_gpu status ") + std::to_string(rc) + ": " +
+                                        (msg ? msg : ""));
+}
+
+tpo_field_params field(const verify::FieldParams &fp) {
+  return tpo_field_params{fp.p(), fp.q(), fp.omega_base()};
+}
+
+verify::EquivVerdict to_verdict(const tpo_verdict &v) {
+  if (v.kind == 3) throw Error(ErrCode(v.err_code - 1000), tpo_gpu_last_error());
+  verify::EquivVerdict r;
+  r.kind = verify::EquivVerdict::Kind(v.kind);
+  r.rounds_run = v.rounds_run;
+  r.resamples = v.resamples;
+  if (v.has_witness) r.witness = verify::Witness{v.w_seed, v.w_round, v.w_omega, v.w_tensor, v.w_index};
+  return r;
+}
+
+}  // namespace
+
+CompiledGraph::CompiledGraph(tpo_gpu_ctx *ctx, const ir::KernelGraph &g) {
+  const std::string js = ir::to_json(g).dump();
+  check(tpo_gpu_compile(ctx, js.c_str(), &h_));
+}
+
+CompiledGraph::~CompiledGraph() {
+  if (h_) tpo_gpu_graph_free(h_);
+}
+
+int64_t CompiledGraph::op_madds() const { return tpo_gpu_op_madds(h_); }
+
+bool CompiledGraph::has_fused_kernel() const {
+  tpo_graph_info info{};
+  tpo_gpu_graph_info(h_, &info);
+  return info.fused_kind != TPO_FUSED_NONE;
+}
+
+Backend::Backend(int device) { check(tpo_gpu_open(device, &ctx_)); }
+
+Backend::~Backend() {
+  if (ctx_) tpo_gpu_close(ctx_);
+}
+
+std::vector<interp::FTensor> Backend::eval_mugraph(const ir::KernelGraph &g,
+                                                   const std::vector<interp::FTensor> &inputs) {
+  if (inputs.size() != g.inputs.size()) throw Error(ErrCode::ShapeMismatch, "input count");
+  CompiledGraph cg(ctx_, g);
+  std::vector<std::vector<float>> in32(inputs.size());
+  std::vector<const void *> pin(inputs.size());
+  std::vector<int32_t> dt(inputs.size(), TPO_DTYPE_F32);
+  for (size_t i = 0; i < inputs.size(); ++i) {
+    if (inputs[i].shape.dims != g.tensor(g.inputs[i]).shape.dims)
+      throw Error(ErrCode::ShapeMismatch, "input tensor shape");
+    in32[i].assign(inputs[i].data.begin(), inputs[i].data.end());
+    pin[i] = in32[i].data();
+  }
+  std::vector<std::vector<float>> out32(g.outputs.size());
+  std::vector<float *> pout(g.outputs.size());
+  for (size_t o = 0; o < g.outputs.size(); ++o) {
+    out32[o].resize(size_t(g.tensor(g.outputs[o]).shape.elem_count()));
+    pout[o] = out32[o].data();
+  }
+  check(tpo_gpu_eval_mugraph_host(ctx_, cg.handle(), pin.data(), dt.data(), pout.data(), nullptr));
+  std::vector<interp::FTensor> out;
+  for (size_t o = 0; o < g.outputs.size(); ++o) {
+    interp::FTensor t(g.tensor(g.outputs[o]).shape);
+    t.data.assign(out32[o].begin(), out32[o].end());
+    out.push_back(std::move(t));
+  }
+  return out;
+}
+
+verify::EquivVerdict Backend::random_test_equivalence(const ir::KernelGraph &g1,
+                                                      const ir::KernelGraph &g2,
+                                                      const verify::VerifyConfig &cfg,
+                                                      const verify::FieldParams &fp) {
+  CompiledGraph a(ctx_, g1), b(ctx_, g2);
+  const tpo_verify_cfg c{cfg.num_tests, cfg.max_resamples, cfg.seed, cfg.float_tolerance};
+  const tpo_field_params f = field(fp);
+  tpo_verdict v{};
+  const int rc = tpo_gpu_random_test_equivalence(ctx_, a.handle(), b.handle(), &c, &f, &v);
+  if (rc && v.kind != 3) check(rc);
+  return to_verdict(v);
+}
+
+std::vector<verify::EquivVerdict> Backend::verify_batch(
+    const ir::KernelGraph &program, const std::vector<const ir::KernelGraph *> &cands,
+    const std::vector<uint64_t> &seeds, const verify::VerifyConfig &cfg,
+    const verify::FieldParams &fp) {
+  if (seeds.size() != cands.size()) throw Error(ErrCode::ShapeMismatch, "one seed per candidate");
+  CompiledGraph prog(ctx_, program);
+  std::vector<std::unique_ptr<CompiledGraph>> owned;
+  std::vector<const tpo_gpu_graph *> hs;
+  for (const ir::KernelGraph *c : cands) {
+    owned.push_back(std::make_unique<CompiledGraph>(ctx_, *c));
+    hs.push_back(owned.back()->handle());
+  }
+  const tpo_verify_cfg c{cfg.num_tests, cfg.max_resamples, cfg.seed, cfg.float_tolerance};
+  const tpo_field_params f = field(fp);
+  std::vector<tpo_verdict> v(cands.size());
+  check(tpo_gpu_verify_batch(ctx_, prog.handle(), hs.data(), seeds.data(), uint64_t(cands.size()), &c,
+                             &f, v.data(), nullptr));
+  std::vector<verify::EquivVerdict> out;
+  out.reserve(v.size());
+  for (const tpo_verdict &x : v) out.push_back(to_verdict(x));  // kind 3 rethrows the tpo::Error
+  return out;
+}
+
+}  // namespace tpo::gpu

@@ -1,0 +1,78 @@
+// Reference-side binding of the B200 backend (a file a maintainer adds to the
+// reference's tpo_core).  Re-exposes the reference entry
+// points of the µGraph-evaluation hot path with their own types, backed by
+// the C-ABI in include/tpo_gpu.h:
+//
+//   tpo::interp::eval_mugraph                proj/core/include/tpo/interp/interp.hpp:47-48
+//   tpo::verify::random_test_equivalence     proj/core/include/tpo/verify/equiv.hpp:50-53
+//   (batched) the search loop's per-candidate verification
+//
+// Graphs cross the ABI in the reference's own wire format
+// (tpo::ir::to_json, proj/core/include/tpo/ir/serialize.hpp:33).  Errors come
+// back as the reference's tpo::Error with the same ErrCode.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <vector>
+
+#include "tpo/interp/interp.hpp"
+#include "tpo/ir/graph.hpp"
+#include "tpo/verify/equiv.hpp"
+#include "tpo_gpu.h"
+
+namespace tpo::gpu {
+
+/// A compiled graph handle (validated with B200 limits, lowered).
+class CompiledGraph {
+ public:
+  CompiledGraph(tpo_gpu_ctx *ctx, const ir::KernelGraph &g);
+  ~CompiledGraph();
+  CompiledGraph(const CompiledGraph &) = delete;
+  CompiledGraph &operator=(const CompiledGraph &) = delete;
+  tpo_gpu_graph *handle() const { return h_; }
+  int64_t op_madds() const;
+  bool has_fused_kernel() const;
+
+ private:
+  tpo_gpu_graph *h_ = nullptr;
+};
+
+/// One device (and its stream).  Not thread-safe: use one Backend per host
+/// thread, as the reference API is re-entrant per call.
+class Backend {
+ public:
+  explicit Backend(int device = 0);
+  ~Backend();
+  Backend(const Backend &) = delete;
+  Backend &operator=(const Backend &) = delete;
+
+  /// eval_mugraph for host tensors.  Inputs are rounded to bf16 on the
+  /// device (the fused kernels' input type), accumulation is fp32, outputs
+  /// are widened back to double.  Throws tpo::Error(Unsupported) for a
+  /// µGraph without a fused sm_100a kernel.
+  std::vector<interp::FTensor> eval_mugraph(const ir::KernelGraph &g,
+                                            const std::vector<interp::FTensor> &inputs);
+
+  /// random_test_equivalence on the GPU; the verdict (kind, witness,
+  /// rounds_run, resamples) is bit-identical to the CPU reference's.
+  verify::EquivVerdict random_test_equivalence(const ir::KernelGraph &g1,
+                                               const ir::KernelGraph &g2,
+                                               const verify::VerifyConfig &cfg,
+                                               const verify::FieldParams &fp = verify::FieldParams());
+
+  /// The search loop's batch: candidate k against `program` with
+  /// {cfg.num_tests, seeds[k], cfg.max_resamples}.
+  std::vector<verify::EquivVerdict> verify_batch(const ir::KernelGraph &program,
+                                                 const std::vector<const ir::KernelGraph *> &cands,
+                                                 const std::vector<uint64_t> &seeds,
+                                                 const verify::VerifyConfig &cfg,
+                                                 const verify::FieldParams &fp = verify::FieldParams());
+
+  tpo_gpu_ctx *ctx() const { return ctx_; }
+
+ private:
+  tpo_gpu_ctx *ctx_ = nullptr;
+};
+
+}  // namespace tpo::gpu

@@ -67,6 +67,7 @@ def lib():
     L.tpo_gpu_graph_set_static_inputs.argtypes = [vp, u64]
     L.tpo_gpu_validate.argtypes = [C.c_char_p, i64, i64, C.c_char_p, C.c_int]
     L.tpo_gpu_eval_mugraph.argtypes = [vp, vp, vp, vp, vp, vp]
+    L.tpo_gpu_eval_mugraph_host.argtypes = [vp, vp, vp, vp, vp, vp]
     L.tpo_gpu_ff_eval.argtypes = [vp, vp, C.POINTER(FieldParams), u64, u64, i32] + [vp] * 6
     L.tpo_gpu_random_test_equivalence.argtypes = [vp, vp, vp, C.POINTER(VerifyCfg),
                                                   C.POINTER(FieldParams), C.POINTER(Verdict)]

@@ -136,6 +136,29 @@ class Context:
         N.check(N.lib().tpo_gpu_eval_mugraph(self.h, g.h, pin, dt, pout, C.c_void_p(st)))
         return outputs
 
+    def eval_mugraph_host(self, g, inputs: Sequence, outputs=None, stream=None):
+        """Fused fp evaluation from/to HOST tensors (``tpo_gpu_eval_mugraph_host``):
+        bf16 or fp32 CPU torch tensors in (pinned for full PCIe speed), fp32
+        CPU tensors out; the host<->device copies are part of the call."""
+        import torch
+        g = self.compile(g)
+        ins = list(inputs)
+        if len(ins) != g.info.n_inputs:
+            raise ValueError("input count")
+        for x, s in zip(ins, g.shapes(False)):
+            if list(x.shape) != s or x.is_cuda or not x.is_contiguous():
+                raise ValueError(f"input must be a contiguous host tensor of shape {s}")
+            if x.dtype not in (torch.bfloat16, torch.float32):
+                raise ValueError("host inputs must be bf16 or fp32")
+        if outputs is None:
+            outputs = [torch.empty(s, dtype=torch.float32) for s in g.shapes(True)]
+        dt = (C.c_int32 * len(ins))(*[1 if x.dtype == torch.bfloat16 else 0 for x in ins])
+        pin = (C.c_void_p * len(ins))(*[x.data_ptr() for x in ins])
+        pout = (C.c_void_p * len(outputs))(*[o.data_ptr() for o in outputs])
+        N.check(N.lib().tpo_gpu_eval_mugraph_host(self.h, g.h, pin, dt, pout,
+                                                  C.c_void_p(stream) if stream else None))
+        return outputs
+
     # ---- finite field -------------------------------------------------------
     def ff_eval(self, g, seed: int, stream: int, with_silu: Optional[bool] = None, p=227, q=113,
                 wbase=4):

@@ -422,6 +422,54 @@ int tpo_gpu_eval_mugraph(tpo_gpu_ctx *ctx, const tpo_gpu_graph *h, const void *c
   });
 }
 
+extern "C" int tpo_convert_f32_bf16(const float *in, void *out, size_t n, int num_sms,
+                                    cudaStream_t st);
+
+int tpo_gpu_eval_mugraph_host(tpo_gpu_ctx *ctx, const tpo_gpu_graph *h, const void *const *in_host,
+                              const int32_t *in_dtype, float *const *out_host, void *stream) {
+  return guard([&] {
+    Ctx &C = ctx->c;
+    const Graph &G = h->g;
+    if (!G.plan.kind)
+      throw Error(ErrCode::Unsupported, "no fused sm_100a kernel for this µGraph: " + G.plan.why);
+    check_cuda(cudaSetDevice(C.device), "cudaSetDevice");
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : C.stream;
+    const size_t ni = G.g.inputs.size(), no = G.g.outputs.size();
+    if (C.h_in.size() < ni) C.h_in.resize(ni), C.h_stage.resize(ni);
+    if (C.h_out.size() < no) C.h_out.resize(no);
+    std::vector<const void *> din(ni);
+    std::vector<int32_t> ddt(ni, TPO_DTYPE_BF16);
+    for (size_t i = 0; i < ni; ++i) {
+      const size_t n = size_t(G.g.tensor(G.g.inputs[i]).shape.elem_count());
+      void *d = C.h_in[i].get(n * 2);
+      if (in_dtype[i] == TPO_DTYPE_BF16) {
+        check_cuda(cudaMemcpyAsync(d, in_host[i], n * 2, cudaMemcpyHostToDevice, st), "H2D");
+      } else if (in_dtype[i] == TPO_DTYPE_F32) {
+        void *f = C.h_stage[i].get(n * 4);
+        check_cuda(cudaMemcpyAsync(f, in_host[i], n * 4, cudaMemcpyHostToDevice, st), "H2D");
+        check_cuda(cudaError_t(tpo_convert_f32_bf16(static_cast<const float *>(f), d, n, C.num_sms, st)),
+                   "f32->bf16");
+      } else {
+        throw Error(ErrCode::Unsupported, "input dtype must be TPO_DTYPE_BF16 or TPO_DTYPE_F32");
+      }
+      din[i] = d;
+    }
+    std::vector<float *> dout(no);
+    for (size_t o = 0; o < no; ++o)
+      dout[o] = static_cast<float *>(
+          C.h_out[o].get(size_t(G.g.tensor(G.g.outputs[o]).shape.elem_count()) * 4));
+    int e = launch_fused(G.plan, din.data(), ddt.data(), dout.data(), nullptr, 0, st);
+    if (e) return fail(3000 + e, std::string("fused launch: ") + cudaGetErrorString(cudaError_t(e)));
+    for (size_t o = 0; o < no; ++o)
+      check_cuda(cudaMemcpyAsync(out_host[o], dout[o],
+                                 size_t(G.g.tensor(G.g.outputs[o]).shape.elem_count()) * 4,
+                                 cudaMemcpyDeviceToHost, st),
+                 "D2H");
+    check_cuda(cudaStreamSynchronize(st), "sync");
+    return 0;
+  });
+}
+
 int tpo_gpu_ff_eval(tpo_gpu_ctx *ctx, const tpo_gpu_graph *h, const tpo_field_params *fpp,
                     uint64_t seed, uint64_t stream, int32_t with_silu, uint16_t *out_xp,
                     uint16_t *out_xq, uint8_t *out_qd, uint32_t *omega_out, uint16_t *in_xp,

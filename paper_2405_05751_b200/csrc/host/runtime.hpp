@@ -36,6 +36,9 @@ struct Ctx {
   int num_sms = 0;
   std::map<uint64_t, std::unique_ptr<FieldState>> fields;
   DevBuf code, graphs, pool, cand, seeds, verdicts, accept, counter, out, status, inputs, ws;
+  // host-buffer fp evaluation (tpo_gpu_eval_mugraph_host): per-input device
+  // copies (bf16), fp32 staging for converted inputs, per-output buffers
+  std::vector<DevBuf> h_in, h_stage, h_out;
   FieldState &field(uint32_t p, uint32_t q, uint32_t wbase);
 };
 

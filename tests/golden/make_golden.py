@@ -43,6 +43,14 @@ FP_SHAPES = {            # small fp cases (args, grid, forloop)
 }
 
 
+FUSED_SHAPES = {
+    "rmsnorm": ((8, 512, 256), 2, 4),
+    "gatedmlp": ((8, 512, 256), 2, 4),
+    "gqa": ((4, 8, 128, 512), 2, 4),
+    "lora": ((16, 512, 256, 16), 2, 4),
+}
+
+
 def edge_graphs():
     """Small graphs exercising broadcasting, Repeat/Reshape, grouped Sum,
     Sqrt/Div resampling, Exp + SiLU, concat Accum, partial omap and
@@ -145,6 +153,8 @@ def main():
     for f, (args, gx, fl) in FP_SHAPES.items():
         graphs[f"fp/{f}/program"] = F.family_program(f, *args)
         graphs[f"fp/{f}/mugraph"] = F.family_mugraph(f, *args, grid=gx, forloop=fl)
+    for f, (args, gx, fl) in FUSED_SHAPES.items():  # shapes inside the fused kernels' limits
+        graphs[f"fused/{f}"] = F.family_mugraph(f, *args, grid=gx, forloop=fl)
 
     # ---- per-graph host facts: op_madds, validate, canonical key
     scal["graph_facts"] = {}

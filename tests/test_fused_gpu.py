@@ -105,3 +105,19 @@ def test_fused_bench_shape_vs_reference(ctx, name):
     check(out, want)
     # the flat program (reference eval_program) agrees too
     check(out, ref.eval_mugraph(prog, [x.float().numpy() for x in ins], mode=1)[0])
+
+
+@pytest.mark.parametrize("name", ["gatedmlp", "rmsnorm", "lora", "gqa"])
+def test_eval_mugraph_host_buffers(ctx, name):
+    """tpo_gpu_eval_mugraph_host: host bf16 inputs (pinned and pageable) and
+    host fp32 inputs (rounded to bf16 on the device) give exactly the
+    device-buffer result."""
+    args, grid, fl = SMALL[name][1]
+    mu = F.family_mugraph(name, *args, grid=grid, forloop=fl)
+    g = ctx.compile(mu)
+    ins = make_inputs(name, args, seed=5)
+    dev = ctx.eval_mugraph(g, [x.cuda() for x in ins])[0].cpu()
+    pinned = ctx.eval_mugraph_host(g, [x.pin_memory() for x in ins])[0]
+    pageable = ctx.eval_mugraph_host(g, ins)[0]
+    f32 = ctx.eval_mugraph_host(g, [x.float() for x in ins])[0]
+    assert torch.equal(dev, pinned) and torch.equal(dev, pageable) and torch.equal(dev, f32)

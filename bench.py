@@ -321,54 +321,59 @@ def reference_arm(args, wl):
 
 # ------------------------------------------------------------------------- verifier
 def run_verify(dist, n_total, pool_fams=("rmsnorm", "gatedmlp", "gqa", "lora")):
-    """Shard n_total candidates (per family, contiguous index ranges) across
-    ranks; each rank verifies its shard on its GPU and the packed accept bits
-    are all-gathered with NCCL.  Returns cand/s over all ranks (max-rank time)."""
+    """Shard n_total candidates (n_total / 4 per family; candidate i of a
+    family = pool[i % |pool|], seed i) across ranks as contiguous index
+    ranges (paper_2405_05751_b200.shard); each rank verifies its ranges on
+    its GPU into packed accept bits, then ONE all-gather per family
+    reassembles them.  Returns cand/s over all ranks (max-rank time)."""
     import torch
     from paper_2405_05751_b200 import fixtures as F
+    from paper_2405_05751_b200 import shard
     from paper_2405_05751_b200.api import Context
     ctx = Context(dist.local)
     fams = F.verify_families()
     per_fam = n_total // len(pool_fams)
-    shard = per_fam // dist.world
+    ranges = [shard.even_range(per_fam, dist.world, r) for r in range(dist.world)]
+    first, n = ranges[dist.rank]
     jobs = []
     for f in pool_fams:
         prog, pool = fams[f]
         gp = ctx.compile(prog)
         gs = [ctx.compile(g) for _, g in pool]
         jobs.append((f, gp, gs))
-    words = (shard + 31) // 32
-    acc = [torch.zeros(words, dtype=torch.int32, device="cuda") for _ in jobs]
+    acc = [torch.zeros(max(1, -(-n // 32)), dtype=torch.int32, device="cuda") for _ in jobs]
     # warm-up (compile/upload paths)
     for (f, gp, gs), a in zip(jobs, acc):
-        ctx.verify_pool(gp, gs, first=0, n=min(shard, 2048), accept_dev=a)
+        ctx.verify_pool(gp, gs, first=0, n=min(max(n, 1), 2048), accept_dev=a)
+        a.zero_()
     torch.cuda.synchronize()
     dist.barrier()
-    t0 = time.perf_counter()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
     attempts = 0
     for (f, gp, gs), a in zip(jobs, acc):
-        first = dist.rank * shard
-        _, att = ctx.verify_pool(gp, gs, first=first, n=shard, accept_dev=a)
-        attempts += att
+        if n:
+            _, att = ctx.verify_pool(gp, gs, first=first, n=n, accept_dev=a)
+            attempts += att
+    e1.record()
     torch.cuda.synchronize()
-    t_local = time.perf_counter() - t0
-    # single collective: gather accept bits
-    gathered = []
-    if dist.pg:
-        for a in acc:
-            out = [torch.empty_like(a) for _ in range(dist.world)]
-            dist.pg.all_gather(out, a)
-            gathered.append(torch.cat(out))
-    else:
-        gathered = acc
+    t_local = e0.elapsed_time(e1) / 1e3
+    # the single collective: packed accept bits, one all-gather per family
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g0.record()
+    accepted = 0
+    for a in acc:
+        bits = shard.gather_accept(a, ranges, per_fam, dist.pg)
+        accepted += int(bits.sum())
+    g1.record()
     torch.cuda.synchronize()
-    t_all = dist.max(time.perf_counter() - t0)
-    accepted = int(sum(int(np.unpackbits(g.cpu().numpy().view(np.uint8)).sum()) for g in gathered))
-    n_done = shard * len(jobs) * dist.world
+    t_all = dist.max(t_local + g0.elapsed_time(g1) / 1e3)
+    n_done = per_fam * len(jobs)
     return {"value": round(n_done / t_all, 1), "unit": "candidates/s", "candidates": n_done,
             "seconds": round(t_all, 4), "kernel_seconds_max_rank": round(dist.max(t_local), 4),
             "accepted": accepted, "attempts_rank0": int(attempts),
-            "families": list(pool_fams), "seed_rule": "candidate i = pool[i % |pool|], seed i"}
+            "families": list(pool_fams), "seed_rule": "candidate i = pool[i % |pool|], seed i",
+            "timing": "CUDA events: verify kernels + accept-bit all-gather, max over ranks"}
 
 
 def cpu_baseline_verify(n=4000):

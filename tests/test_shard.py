@@ -1,0 +1,83 @@
+"""Host-side multi-GPU verifier logic on CPU: cost-balanced contiguous
+sharding, packed accept bits, and the single all-gather — run with the gloo
+backend at world size 2 (and 3) over 127.0.0.1, with the golden verdicts of
+the compiled reference standing in for each rank's GPU output."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2405_05751_b200 import shard
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _golden_accept():
+    ar = np.load(os.path.join(HERE, "golden", "golden.npz"))
+    return np.concatenate([ar[f"verdicts_{f}"]["kind"] == 0
+                           for f in ("rmsnorm", "gatedmlp", "gqa", "lora")])
+
+
+def test_even_and_cost_ranges_cover_exactly():
+    for n in (0, 1, 31, 32, 33, 1000, 1_000_000):
+        for world in (1, 2, 3, 4, 8):
+            rs = [shard.even_range(n, world, r) for r in range(world)]
+            assert sum(k for _, k in rs) == n
+            pos = 0
+            for first, k in rs:
+                assert first == pos and first % 32 == 0 or k == 0
+                pos += k
+    rng = np.random.default_rng(0)
+    costs = np.concatenate([np.full(500, 1.0), np.full(500, 60.0), rng.uniform(1, 60, 777)])
+    for world in (2, 4, 8):
+        rs = shard.cost_ranges(costs, world)
+        assert sum(k for _, k in rs) == len(costs)
+        loads = [costs[a:a + k].sum() for a, k in rs]
+        assert max(loads) <= costs.sum() / world + 32 * 60 + 1e-9  # within one word of the ideal
+
+
+def test_pack_unpack_roundtrip():
+    a = np.random.default_rng(1).random(1001) < 0.5
+    assert np.array_equal(shard.unpack_bits(shard.pack_bits(a), len(a)), a)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, accept, costs, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ranges = shard.cost_ranges(costs, world)
+    first, n = ranges[rank]
+    # this rank's "GPU output": packed accept bits of its shard
+    local = torch.from_numpy(shard.pack_bits(accept[first:first + n]).view(np.int32).copy())
+    got = shard.gather_accept(local, ranges, len(accept), dist)
+    q.put((rank, bool(np.array_equal(got, accept)), int(got.sum())))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_gather_reassembles_reference_verdicts(world):
+    accept = _golden_accept()
+    costs = np.repeat([4353.0, 66560.0, 70144.0, 99328.0], len(accept) // 4)  # SURVEY §8d op_madds
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, accept, costs, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok, _ in res), res
+    assert all(c == int(accept.sum()) for _, _, c in res)

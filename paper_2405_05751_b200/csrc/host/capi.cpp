@@ -1,5 +1,7 @@
 // B200 backend — C-ABI (include/tpo_gpu.h) over the host runtime.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <unordered_map>
@@ -134,6 +136,7 @@ struct Batch {
   std::vector<TpoVmGraph> graphs;
   uint32_t n_in = 0;
   uint32_t max_words = 0;  // words of VM memory needed
+  uint32_t max_code = 0;   // program + largest candidate, instructions (staged in smem)
 };
 
 void check_pair(const ir::KernelGraph &a, const ir::KernelGraph &b) {
@@ -187,6 +190,9 @@ Batch build_batch(const Graph &prog, const std::vector<const Graph *> &uniq) {
     }
   }
   bt.max_words = maxw;
+  uint32_t mc = 0;
+  for (size_t i = 1; i < bt.graphs.size(); ++i) mc = std::max(mc, bt.graphs[i].code_len);
+  bt.max_code = bt.graphs[0].code_len + mc;
   return bt;
 }
 
@@ -207,7 +213,8 @@ void run_verify(Ctx &C, const Batch &bt, const tpo_verify_cfg &cfg, const tpo_fi
                 const VerifyRun &r) {
   check_cuda(cudaSetDevice(C.device), "cudaSetDevice");
   FieldState &fs = C.field(fpp.p, fpp.q, fpp.omega_base);
-  const size_t smem = fs.fc.table_bytes + size_t(bt.max_words) * 4;
+  const size_t code_bytes = size_t(bt.max_code) * sizeof(TpoVmInstr);
+  const size_t smem = fs.fc.table_bytes + code_bytes + size_t(bt.max_words) * 4;
   if (smem > 232448)
     throw Error(ErrCode::DoesNotFit,
                 "verifier working set " + std::to_string(smem) + " B exceeds 227 KiB of shared memory");
@@ -225,6 +232,7 @@ void run_verify(Ctx &C, const Batch &bt, const tpo_verify_cfg &cfg, const tpo_fi
   a.code = dcode;
   a.graphs = dgraphs;
   a.program = 0;
+  a.code_smem_bytes = uint32_t(code_bytes);
   if (r.pool_host) {
     auto *dp = static_cast<uint32_t *>(C.pool.get(r.pool_n * 4));
     check_cuda(cudaMemcpyAsync(dp, r.pool_host, r.pool_n * 4, cudaMemcpyHostToDevice, st), "pool");
@@ -259,7 +267,30 @@ void run_verify(Ctx &C, const Batch &bt, const tpo_verify_cfg &cfg, const tpo_fi
   if (occ < 1) throw Error(ErrCode::DoesNotFit, "verifier kernel does not fit on an SM");
   uint64_t grid = std::min<uint64_t>(uint64_t(C.num_sms) * uint64_t(occ), r.n);
   grid = std::max<uint64_t>(grid, 1);
+  // TPO_VM_PROFILE: per-opcode cycle breakdown of the verifier (thread 0 of
+  // each CTA; slot 0 = input/omega/SiLU generation, 9 = output compare)
+  static unsigned long long *prof = nullptr;
+  const bool profile = std::getenv("TPO_VM_PROFILE") != nullptr;
+  if (profile) {
+    if (!prof) check_cuda(cudaMalloc(&prof, 32 * 8), "prof");
+    check_cuda(cudaMemsetAsync(prof, 0, 32 * 8, st), "prof");
+    a.prof = prof;
+  }
   check_cuda(cudaError_t(tpo_ff_launch_verify(&a, int(grid), smem, st)), "verify launch");
+  if (profile) {
+    unsigned long long h[32];
+    check_cuda(cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, st), "prof");
+    check_cuda(cudaStreamSynchronize(st), "prof");
+    static const char *nm[16] = {"gen_inputs", "ZERO", "COPY", "UNARY", "BINARY", "MATMUL", "SUM",
+                                 "LOOP", "ENDLOOP", "compare", "", "", "", "", "", ""};
+    unsigned long long tot = 0;
+    for (int i = 0; i < 16; ++i) tot += h[i];
+    std::fprintf(stderr, "[tpo vm profile] n=%llu candidates, %d CTAs\n", (unsigned long long)r.n, int(grid));
+    for (int i = 0; i < 16; ++i)
+      if (h[i])
+        std::fprintf(stderr, "  %-11s %6.2f%%  cycles/exec %9.1f  execs %llu\n", nm[i], 100.0 * double(h[i]) / double(tot),
+                     double(h[i]) / double(h[16 + i] ? h[16 + i] : 1), h[16 + i]);
+  }
   if (r.verdicts_host)
     check_cuda(cudaMemcpyAsync(r.verdicts_host, a.verdicts, r.n * sizeof(TpoVerdict),
                                cudaMemcpyDeviceToHost, st), "verdicts");

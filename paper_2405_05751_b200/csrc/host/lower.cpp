@@ -272,7 +272,10 @@ class Lowerer {
     return kbuf_[size_t(t)];
   }
 
-  void emit(TpoVmInstr in) { p_.code.push_back(in); }
+  void emit(TpoVmInstr in) {
+    tpo_vm_set_divisors(&in);
+    p_.code.push_back(in);
+  }
 
   // Grid dims (bx, by, bz) and the strides of a block tensor of E elements.
   // Block-invariant tensors (identical in every block) are stored once:

@@ -50,7 +50,7 @@ struct Smem {
   uint32_t *w;  // VM words
 };
 
-__device__ __forceinline__ Smem carve(uint8_t *base, const FieldConst &f) {
+__device__ __forceinline__ Smem carve(uint8_t *base, const FieldConst &f, uint32_t code_bytes = 0) {
   Smem s;
   uint16_t *u = reinterpret_cast<uint16_t *>(base);
   s.inv_p = u;
@@ -60,7 +60,7 @@ __device__ __forceinline__ Smem carve(uint8_t *base, const FieldConst &f) {
   s.pow_w = s.silu_q + f.q;
   s.sqrt_p = reinterpret_cast<int16_t *>(s.pow_w + f.q);
   s.sqrt_q = s.sqrt_p + f.p;
-  s.w = reinterpret_cast<uint32_t *>(base + f.table_bytes);
+  s.w = reinterpret_cast<uint32_t *>(base + f.table_bytes + code_bytes);
   return s;
 }
 
@@ -176,14 +176,20 @@ __device__ uint32_t gen_attempt(const Smem &s, const FieldConst &f, uint64_t see
   return omega;
 }
 
+// x / d for an instruction's precomputed divisor (vm.h tpo_vm_divisor)
+__device__ __forceinline__ uint32_t fdiv(uint32_t x, uint32_t mul, uint32_t sh) {
+  return mul ? (__umulhi(x, mul) >> sh) : x;
+}
+
 __device__ __forceinline__ void offsets(const TpoVmInstr &I, uint32_t idx, int32_t &od, int32_t &oa,
                                         int32_t &ob, bool &wr) {
   od = oa = ob = 0;
   wr = true;
   for (int k = int(I.ndim) - 1; k >= 0; --k) {
-    uint32_t d = I.dims[k];
-    uint32_t c = idx % d;
-    idx /= d;
+    const uint32_t d = I.dims[k];
+    const uint32_t qt = fdiv(idx, I.dmul[k], I.dsh[k]);
+    const uint32_t c = idx - qt * d;
+    idx = qt;
     od += int32_t(c) * I.sd[k];
     oa += int32_t(c) * I.sa[k];
     ob += int32_t(c) * I.sb[k];
@@ -193,11 +199,24 @@ __device__ __forceinline__ void offsets(const TpoVmInstr &I, uint32_t idx, int32
 
 // Runs one graph's bytecode. Returns false (uniformly) when an undefined
 // field operation (zero divisor / non-residue) requires a resample.
+// Block-cooperative copy of `len` instructions (192 B each) global -> smem.
+__device__ __forceinline__ void copy_code(TpoVmInstr *dst, const TpoVmInstr *src, uint32_t len) {
+  static_assert(sizeof(TpoVmInstr) % 16 == 0, "instructions are copied as uint4");
+  const uint32_t n = len * uint32_t(sizeof(TpoVmInstr) / 16);
+  const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+  uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) d4[i] = __ldg(s4 + i);
+  __syncthreads();
+}
+
+// PROF: thread 0 accumulates clock64 per VM opcode into prof[op] (TPO_VM_PROFILE).
+template <bool PROF>
 __device__ bool run_program(const Smem &s, const FieldConst &f, const TpoVmInstr *code,
-                            uint32_t len, int *s_flag) {
+                            uint32_t len, int *s_flag, unsigned long long *prof) {
   uint32_t it = 0, loop_pc = 0, trips = 1;
   uint32_t *W = s.w;
   const uint32_t p = f.p, q = f.q, mp = f.magic_p, mq = f.magic_q;
+  long long t_prev = PROF ? clock64() : 0;
   for (uint32_t pc = 0; pc < len; ++pc) {
     const TpoVmInstr &I = code[pc];
     const uint8_t op = I.op;
@@ -300,29 +319,42 @@ __device__ bool run_program(const Smem &s, const FieldConst &f, const TpoVmInstr
         break;
       }
       case VM_MATMUL: {
-        // dims {blocks, batch, M, K, N}; per-operand block strides (0: block-invariant)
+        // dims {blocks, batch, M, K, N}; per-operand block strides (0: block-invariant).
+        // Products < (p-1)^2 accumulate raw in u32 and reduce every `lazy`
+        // terms (lazy >= 84k for p = 227: one reduction at the end).
         const uint32_t Bi = I.dims[1], M = I.dims[2], K = I.dims[3], N = I.dims[4];
-        const uint32_t MN = M * N, BMN = Bi * MN;
+        const uint32_t MN = M * N;
         const uint32_t lazy = f.lazy;
         for (uint32_t o = threadIdx.x; o < n; o += blockDim.x) {
-          uint32_t blk = o / BMN, r = o - blk * BMN, bi = r / MN;
+          const uint32_t blk = fdiv(o, I.dmul[0], I.dsh[0]);
+          uint32_t r = o - blk * Bi * MN;
+          const uint32_t bi = fdiv(r, I.dmul[1], I.dsh[1]);
           r -= bi * MN;
-          uint32_t m = r / N, c = r - m * N;
+          const uint32_t m = fdiv(r, I.dmul[2], I.dsh[2]), c = r - m * N;
           const uint32_t *pa = W + I.a + blk * uint32_t(I.sa[0]) + bi * M * K + m * K;
           const uint32_t *pb = W + I.b + blk * uint32_t(I.sb[0]) + bi * K * N + c;
-          uint32_t accp = 0, accq = 0, cnt = 0;
-          for (uint32_t k = 0; k < K; ++k) {
-            uint32_t va = pa[k], vb = pb[k * N];
-            accp += (va & 0xffffu) * (vb & 0xffffu);
-            accq += (va >> 16) * (vb >> 16);
-            if (++cnt == lazy) {
-              accp = mod32(accp, p, mp);
-              accq = mod32(accq, q, mq);
-              cnt = 0;
+          uint32_t accp = 0, accq = 0;
+          for (uint32_t k0 = 0; k0 < K; k0 += lazy) {
+            const uint32_t k1 = min(K, k0 + lazy);
+            uint32_t p0 = 0, p1 = 0, q0 = 0, q1 = 0;  // 4 independent chains
+            uint32_t k = k0;
+            for (; k + 2 <= k1; k += 2) {
+              const uint32_t va0 = pa[k], vb0 = pb[k * N], va1 = pa[k + 1], vb1 = pb[(k + 1) * N];
+              p0 += (va0 & 0xffffu) * (vb0 & 0xffffu);
+              q0 += (va0 >> 16) * (vb0 >> 16);
+              p1 += (va1 & 0xffffu) * (vb1 & 0xffffu);
+              q1 += (va1 >> 16) * (vb1 >> 16);
             }
+            if (k < k1) {
+              const uint32_t va0 = pa[k], vb0 = pb[k * N];
+              p0 += (va0 & 0xffffu) * (vb0 & 0xffffu);
+              q0 += (va0 >> 16) * (vb0 >> 16);
+            }
+            // two partial sums of <= lazy/2 terms each: reduce before adding
+            accp = mod32(accp + mod32(p0, p, mp) + mod32(p1, p, mp), p, mp);
+            accq = mod32(accq + mod32(q0, q, mq) + mod32(q1, q, mq), q, mq);
           }
-          uint32_t rp = mod32(accp, p, mp), rq = qd ? mod32(accq, q, mq) : 0;
-          W[I.dst + o] = rp | (rq << 16);
+          W[I.dst + o] = accp | ((qd ? accq : 0u) << 16);
         }
         break;
       }
@@ -330,21 +362,23 @@ __device__ bool run_program(const Smem &s, const FieldConst &f, const TpoVmInstr
         const uint32_t mid = I.dims[1], grp = I.dims[2], inner = I.dims[3];
         const uint32_t lazy = f.lazy_sum;
         for (uint32_t o = threadIdx.x; o < n; o += blockDim.x) {
-          uint32_t in_i = o % inner, t = o / inner, m = t % mid, ou = t / mid;
+          const uint32_t t = fdiv(o, I.dmul[0], I.dsh[0]), in_i = o - t * inner;
+          const uint32_t ou = fdiv(t, I.dmul[1], I.dsh[1]), m = t - ou * mid;
           const uint32_t *pa = W + I.a + (ou * mid * grp + m * grp) * inner + in_i;
-          uint32_t accp = 0, accq = 0, cnt = 0;
-          for (uint32_t g = 0; g < grp; ++g) {
-            uint32_t v = pa[g * inner];
-            accp += v & 0xffffu;
-            accq += v >> 16;
-            if (++cnt == lazy) {
-              accp = mod32(accp, p, mp);
-              accq = mod32(accq, q, mq);
-              cnt = 0;
+          uint32_t accp = 0, accq = 0;
+          for (uint32_t g0 = 0; g0 < grp; g0 += lazy) {
+            const uint32_t g1 = min(grp, g0 + lazy);
+            uint32_t sp = 0, sq = 0;
+#pragma unroll 4
+            for (uint32_t g = g0; g < g1; ++g) {
+              const uint32_t v = pa[g * inner];
+              sp += v & 0xffffu;
+              sq += v >> 16;
             }
+            accp = mod32(accp + mod32(sp, p, mp), p, mp);
+            accq = mod32(accq + mod32(sq, q, mq), q, mq);
           }
-          uint32_t rp = mod32(accp, p, mp), rq = qd ? mod32(accq, q, mq) : 0;
-          W[I.dst + o] = rp | (rq << 16);
+          W[I.dst + o] = accp | ((qd ? accq : 0u) << 16);
         }
         break;
       }
@@ -353,6 +387,12 @@ __device__ bool run_program(const Smem &s, const FieldConst &f, const TpoVmInstr
     }
     if (bad) *s_flag = (op == VM_UNARY) ? 2 : 1;  // NonResidue (sqrt) / DivByZero (div)
     __syncthreads();
+    if (PROF && threadIdx.x == 0) {
+      const long long t = clock64();
+      prof[op] += (unsigned long long)(t - t_prev);
+      prof[16 + op] += 1;
+      t_prev = t;
+    }
     if (*s_flag) return false;
   }
   return true;
@@ -391,15 +431,25 @@ __device__ bool first_mismatch(const Smem &s, const TpoVmGraph &g1, const TpoVmG
   return false;
 }
 
+template <bool PROF>
 __global__ void __launch_bounds__(kThreads) verify_kernel(VerifyArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int s_flag, s_slow;
   __shared__ uint32_t s_omega;
   __shared__ unsigned long long s_cand, s_key;
+  __shared__ unsigned long long s_prof[32];  // PROF: [0,16) cycles per opcode, [16,32) counts
+  if (PROF && threadIdx.x < 32) s_prof[threadIdx.x] = 0;
   const FieldConst &f = a.field;
-  Smem s = carve(smem, f);
+  Smem s = carve(smem, f, a.code_smem_bytes);
   load_tables(s, f, a.tables);
   const TpoVmGraph g1 = a.graphs[a.program];
+  // bytecode staged in shared memory: the program once per CTA, each
+  // candidate's code when it changes (instructions are uniform across the
+  // block; smem reads avoid a global round trip per VM instruction)
+  TpoVmInstr *scode = reinterpret_cast<TpoVmInstr *>(smem + f.table_bytes);
+  copy_code(scode, a.code + g1.code_off, g1.code_len);
+  TpoVmInstr *ccode = scode + g1.code_len;
+  uint32_t staged = 0xffffffffu;
   for (;;) {
     __syncthreads();
     if (threadIdx.x == 0) s_cand = atomicAdd(a.counter, 1ull);
@@ -411,6 +461,10 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(VerifyArgs a) {
     const uint64_t seed = a.seeds ? a.seeds[k] : cand;
     const TpoVmGraph g2 = a.graphs[gi];
     const bool silu = g1.has_silu || g2.has_silu;
+    if (gi != staged && !g2.err) {
+      copy_code(ccode, a.code + g2.code_off, g2.code_len);
+      staged = gi;
+    }
 
     TpoVerdict v;
     v.kind = 0;
@@ -433,18 +487,23 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(VerifyArgs a) {
       bool round_done = false;
       for (int att = 0; att <= a.max_resamples && !round_done; ++att) {
         const uint64_t stream = uint64_t(round) * 131071ull + uint64_t(att);
+        long long t0 = PROF ? clock64() : 0;
         const uint32_t omega = gen_attempt(s, f, seed, stream, a.n_in, silu, &s_slow, &s_omega);
         if (threadIdx.x == 0) s_flag = 0;
         __syncthreads();
-        bool ok = run_program(s, f, a.code + g1.code_off, g1.code_len, &s_flag) &&
-                  run_program(s, f, a.code + g2.code_off, g2.code_len, &s_flag);
+        if (PROF && threadIdx.x == 0) s_prof[0] += (unsigned long long)(clock64() - t0), s_prof[16] += 1;
+        bool ok = run_program<PROF>(s, f, scode, g1.code_len, &s_flag, s_prof) &&
+                  run_program<PROF>(s, f, ccode, g2.code_len, &s_flag, s_prof);
         if (!ok) {
           ++v.resamples;
           continue;
         }
         int t;
         int64_t idx;
-        if (first_mismatch(s, g1, g2, &s_key, &t, &idx)) {
+        t0 = PROF ? clock64() : 0;
+        const bool mism = first_mismatch(s, g1, g2, &s_key, &t, &idx);
+        if (PROF && threadIdx.x == 0) s_prof[9] += (unsigned long long)(clock64() - t0), s_prof[25] += 1;
+        if (mism) {
           v.kind = 1;
           v.has_witness = 1;
           v.w_seed = seed;
@@ -473,6 +532,7 @@ __global__ void __launch_bounds__(kThreads) verify_kernel(VerifyArgs a) {
       if (a.work) atomicAdd(a.work, (unsigned long long)(v.resamples + v.rounds_run));
     }
   }
+  if (PROF && threadIdx.x < 32 && a.prof) atomicAdd(a.prof + threadIdx.x, s_prof[threadIdx.x]);
 }
 
 // Debug / parity: evaluate one graph for one (seed, stream) attempt, or on
@@ -510,7 +570,7 @@ __global__ void __launch_bounds__(kThreads) eval_kernel(EvalArgs a) {
   __syncthreads();
   if (a.in_dump)
     for (uint32_t e = threadIdx.x; e < a.n_in; e += blockDim.x) a.in_dump[e] = s.w[e];
-  bool ok = run_program(s, f, a.code + g.code_off, g.code_len, &s_flag);
+  bool ok = run_program<false>(s, f, a.code + g.code_off, g.code_len, &s_flag, nullptr);
   if (threadIdx.x == 0) {
     a.status[0] = ok ? 0 : s_flag;
     a.status[1] = int(omega);
@@ -527,13 +587,14 @@ __global__ void __launch_bounds__(kThreads) eval_kernel(EvalArgs a) {
 
 extern "C" int tpo_ff_launch_verify(const tpo_ff::VerifyArgs *a, int grid, size_t smem,
                                     cudaStream_t st) {
-  static int configured_for = -1;
-  if (int(smem) > configured_for) {
-    cudaFuncSetAttribute(tpo_ff::verify_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(smem));
-    configured_for = int(smem);
+  static int configured_for[2] = {-1, -1};
+  const bool prof = a->prof != nullptr;
+  auto kern = prof ? tpo_ff::verify_kernel<true> : tpo_ff::verify_kernel<false>;
+  if (int(smem) > configured_for[prof]) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    configured_for[prof] = int(smem);
   }
-  tpo_ff::verify_kernel<<<grid, tpo_ff::kThreads, smem, st>>>(*a);
+  kern<<<grid, tpo_ff::kThreads, smem, st>>>(*a);
   return int(cudaGetLastError());
 }
 
@@ -545,8 +606,9 @@ extern "C" int tpo_ff_launch_eval(const tpo_ff::EvalArgs *a, size_t smem, cudaSt
 
 extern "C" int tpo_ff_verify_occupancy(size_t smem) {
   int blocks = 0;
-  cudaFuncSetAttribute(tpo_ff::verify_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, tpo_ff::verify_kernel, tpo_ff::kThreads,
-                                                smem);
+  cudaFuncSetAttribute(tpo_ff::verify_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(smem));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, tpo_ff::verify_kernel<false>,
+                                                tpo_ff::kThreads, smem);
   return blocks;
 }

@@ -50,6 +50,8 @@ struct VerifyArgs {
   TpoVerdict *verdicts;          // optional
   uint32_t *accept;              // optional packed accept bits (Equivalent)
   unsigned long long *work;      // optional: attempts actually consumed
+  unsigned long long *prof;      // optional (TPO_VM_PROFILE): [16] cycles, [16] counts per opcode
+  uint32_t code_smem_bytes;      // smem staging of program + candidate bytecode
 };
 
 struct EvalArgs {

@@ -48,7 +48,45 @@ struct TpoVmInstr {
   int32_t a_iter, d_iter;      // per-iteration offsets added to a / dst
   uint32_t dims[TPO_VM_DIMS];
   int32_t sd[TPO_VM_DIMS], sa[TPO_VM_DIMS], sb[TPO_VM_DIMS];
+  // Division by invariant integers (index math without IDIV):
+  // x / d = __umulhi(x, dmul) >> dsh for x < 2^31; dmul = 0 means d = 1.
+  // COPY / BINARY / UNARY: one per index dim.  MATMUL: {B*M*N, M*N, N}.
+  // SUM: {inner, mid}.  Filled by the lowering (tpo_vm_set_divisors).
+  uint32_t dmul[TPO_VM_DIMS];
+  uint8_t dsh[TPO_VM_DIMS];
+  uint8_t pad2;
+  uint32_t pad3[3];            // 192 bytes: copied to shared memory as uint4
 };
+
+// Host helper: the (mul, shift) pair of divisor d >= 1 (CUTLASS-style
+// round-up reciprocal, exact for numerators < 2^31).
+static inline void tpo_vm_divisor(uint32_t d, uint32_t *mul, uint8_t *sh) {
+  if (d <= 1) {
+    *mul = 0;
+    *sh = 0;
+    return;
+  }
+  uint32_t l = 0;
+  while ((1ull << l) < d) ++l;  // ceil(log2 d)
+  const unsigned long long p = 1ull << (31 + l);
+  *mul = (uint32_t)((p + d - 1) / d);
+  *sh = (uint8_t)(l - 1);
+}
+
+static inline void tpo_vm_set_divisors(TpoVmInstr *I) {
+  for (int k = 0; k < TPO_VM_DIMS; ++k) I->dmul[k] = 0, I->dsh[k] = 0;
+  if (I->op == VM_MATMUL) {
+    const uint32_t MN = I->dims[2] * I->dims[4];
+    tpo_vm_divisor(I->dims[1] * MN, &I->dmul[0], &I->dsh[0]);
+    tpo_vm_divisor(MN, &I->dmul[1], &I->dsh[1]);
+    tpo_vm_divisor(I->dims[4], &I->dmul[2], &I->dsh[2]);
+  } else if (I->op == VM_SUM) {
+    tpo_vm_divisor(I->dims[3], &I->dmul[0], &I->dsh[0]);
+    tpo_vm_divisor(I->dims[1], &I->dmul[1], &I->dsh[1]);
+  } else if (I->op == VM_COPY || I->op == VM_BINARY || I->op == VM_UNARY) {
+    for (int k = 0; k < I->ndim && k < TPO_VM_DIMS; ++k) tpo_vm_divisor(I->dims[k], &I->dmul[k], &I->dsh[k]);
+  }
+}
 
 // One compiled graph inside a batch upload.
 struct TpoVmGraph {

@@ -396,6 +396,7 @@ int launch_fused(const FusedPlan &p, const void *const *in, const int32_t *dt, f
     minb = tpo_skinny_smem(mode, stages, 2, &sp) ? 2 : 1;
   }
   sp.dbg_flags = env_int("TPO_DBG_FLAGS", 0);
+  sp.epi_atomic = env_int("TPO_EPI_ATOMIC", 0);
   static unsigned long long *dbg = nullptr;
   const int nct = int(p.n / 128) * sp.ksplit;
   const bool debug_times = std::getenv("TPO_DEBUG_TIMES") != nullptr;
@@ -411,11 +412,12 @@ int launch_fused(const FusedPlan &p, const void *const *in, const int32_t *dt, f
     cudaStreamSynchronize(st);
     unsigned long long t0 = ~0ull;
     for (int c = 0; c < nct; ++c) t0 = std::min(t0, h[size_t(c) * 16]);
-    static const char *names[11] = {"start", "setup", "epi_done", "last_mma", "sent", "tmem_full",
-                                    "recv_done", "end", "first_full", "b_ready", "last_tma"};
+    static const char *names[14] = {"start", "setup", "epi_done", "last_mma", "sent", "tmem_full",
+                                    "recv_done", "end", "first_full", "b_ready", "last_tma",
+                                    "owner_done", "after_sync", "w0_at_sync"};
     std::fprintf(stderr, "[tpo debug] mode %d ksplit %d stages %d minb %d prefetch %d ctas %d (us since first start)\n",
                  mode, sp.ksplit, stages, minb, sp.prefetch_static, nct);
-    for (int k = 0; k < 11; ++k) {
+    for (int k = 0; k < 14; ++k) {
       double mn = 1e30, mx = 0, sum = 0;
       int cnt = 0;
       for (int c = 0; c < nct; ++c) {

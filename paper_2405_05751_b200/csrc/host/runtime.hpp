@@ -21,6 +21,10 @@ struct DevBuf {
   void *ptr = nullptr;
   size_t cap = 0;
   void *get(size_t bytes);
+  DevBuf() = default;
+  DevBuf(const DevBuf &) = delete;
+  DevBuf &operator=(const DevBuf &) = delete;
+  DevBuf(DevBuf &&o) noexcept : ptr(o.ptr), cap(o.cap) { o.ptr = nullptr, o.cap = 0; }
   ~DevBuf();
 };
 

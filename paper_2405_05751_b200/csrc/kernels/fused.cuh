@@ -21,6 +21,7 @@ struct SkinnyParams {
   unsigned long long *dbg;   // optional per-CTA phase timestamps (TPO_DEBUG_TIMES)
   int dbg_flags;             // experiments (TPO_DBG_FLAGS): 1 skip finalize
   int prefetch_static;       // weights are static: stream them before the PDL wait
+  int epi_atomic;            // RMS/LoRA split clusters: fp32-reduction epilogue
 };
 
 struct GqaParams {

@@ -60,14 +60,16 @@ constexpr int kMaxSplit = 4;
 template <int MODE>
 struct Cfg {
   static constexpr int NA = MODE == MODE_GATED ? 2 : 1;  // weight matrices
-  static constexpr bool kTmaX = MODE != MODE_RMS;        // B tile via TMA
+  static constexpr bool kTmaX = MODE != MODE_RMS;        // per-stage B tile via TMA
+  // LoRA: in addition, the CTA's whole X^T slice and A slice are staged once,
+  // ahead of the W stream, so XA (and XA·B̄) finish long before the last MMA
+  static constexpr bool kSlices = MODE == MODE_LORA;
   static constexpr uint32_t kAOff = 0;                   // W boxes lead the stage
   static constexpr uint32_t kBOff = kAOff + NA * 2 * kWBox;
   static constexpr uint32_t kXRawOff = kBOff + kXTile;     // RMS raw X
   static constexpr uint32_t kGOff = kXRawOff + 1024;       // RMS G
-  static constexpr uint32_t kARawOff = kBOff + kXTile;     // LoRA A box [64 k][16 r] (2 KB)
+  static constexpr uint32_t kABox = 2048;                  // LoRA A box [64 k][16 r]
   static constexpr uint32_t kStage = MODE == MODE_RMS    ? kGOff + 1024
-                                     : MODE == MODE_LORA ? kARawOff + 2048
                                                          : kBOff + kXTile;
   static constexpr uint32_t kFullBytes = MODE == MODE_RMS ? NA * 2 * kWBox : kStage;
   static constexpr uint32_t kXGBytes = 1024 + 128;  // RMS: X box [8][64] + G box [64]
@@ -78,7 +80,7 @@ constexpr int kMaxStages = 12;
 
 struct __align__(8) Bars {
   uint64_t full[kMaxStages], empty[kMaxStages], xg_full[kMaxStages], b_full[kMaxStages];
-  uint64_t tmem_full, recv, recv_side;
+  uint64_t tmem_full, recv, recv_side, xa_full;
   uint32_t tmem_base;
 };
 
@@ -115,7 +117,9 @@ __global__ void __launch_bounds__(kThreads, MINB)
   const int nkb = p.k_per_cta / kBK;
   constexpr int rows_per = kTileN / S;                                     // rows owned per CTA
   uint8_t *stages = smem;
-  float *red = reinterpret_cast<float *>(stages + STAGES * C::kStage);
+  uint8_t *xsl = stages + STAGES * C::kStage;               // LoRA: X^T slice, nkb B tiles
+  uint8_t *asl = xsl + (C::kSlices ? nkb * kXTile : 0);      // LoRA: A slice, nkb A boxes
+  float *red = reinterpret_cast<float *>(asl + (C::kSlices ? nkb * C::kABox : 0));
   float *side = red + (S > 1 ? kTileN * 16 : 0);  // red: [S][rows_per][16] incoming row partials
   float *xa_tot = side + S * kSide;         // side: [S][kSide]; xa_tot: LoRA [16][16]
   float *xa_w = xa_tot + (MODE == MODE_LORA ? 256 : 0);  // LoRA: per-warp XA partials [4][16][16]
@@ -133,13 +137,14 @@ __global__ void __launch_bounds__(kThreads, MINB)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&bars->full[s], 1);
-      mbar_init(&bars->empty[s], MODE == MODE_LORA ? 5 : 1);  // LoRA: + 4 XA warps
+      mbar_init(&bars->empty[s], 1);
       mbar_init(&bars->xg_full[s], 1);
       mbar_init(&bars->b_full[s], 4);
     }
     mbar_init(&bars->tmem_full, 1);
     mbar_init(&bars->recv, 1);
     mbar_init(&bars->recv_side, 1);
+    mbar_init(&bars->xa_full, 1);
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -170,7 +175,6 @@ __global__ void __launch_bounds__(kThreads, MINB)
       uint8_t *st = stages + kb * C::kStage;
       mbar_expect_tx(&bars->full[kb], C::kFullBytes);
       const int k0 = kbase + kb * kBK;
-      if (MODE == MODE_LORA) tma_load_2d(st + C::kARawOff, &tmA, &bars->full[kb], 0, k0);
       uint8_t *wt = st + C::kAOff;
       tma_load_2d(wt, &tmW0, &bars->full[kb], n0, k0);
       tma_load_2d(wt + kWBox, &tmW0, &bars->full[kb], n0 + 64, k0);
@@ -188,10 +192,30 @@ __global__ void __launch_bounds__(kThreads, MINB)
   // 8: trigger at once.
   const bool early_trigger = p.dbg_flags & 8;
   if (early_trigger) pdl_launch();
+  // Atomic epilogue (RMS / LoRA, split clusters): every CTA adds its scaled
+  // partial into the output with fp32 reductions instead of routing it to
+  // an owner CTA; rank 0 zeroes the tile first, ordered before the other
+  // ranks' adds by a second cluster-barrier phase.
+  const bool atomic_epi = MODE != MODE_GATED && S > 1 && p.epi_atomic;
+  if (atomic_epi && rank == 0 && warp >= 2) {
+    const int col = n0 + (threadIdx.x - 64);
+    for (int tk = 0; tk < p.tokens; ++tk) p.out[size_t(tk) * p.N + col] = 0.f;
+  }
 
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer
     if (elect_one()) {
+      // LoRA: X^T and A slices, issued right behind the first pipeline
+      // stages (ahead of them they delay the first W stage by ~1 µs)
+      auto issue_slices = [&] {
+        mbar_expect_tx(&bars->xa_full, uint32_t(nkb) * (kXTile + C::kABox));
+        for (int kb = 0; kb < nkb; ++kb) {
+          tma_load_2d(xsl + kb * kXTile, &tmX, &bars->xa_full, kbase + kb * kBK, 0);
+          tma_load_2d(asl + kb * C::kABox, &tmA, &bars->xa_full, 0, kbase + kb * kBK);
+        }
+      };
+      const int slice_at = (nkb < STAGES ? nkb : STAGES) - 1;  // after this k block's stage
+      if (C::kSlices && npre > slice_at) issue_slices();
       // X (and RMS: G) boxes of the prefetched stages
       for (int kb = 0; kb < npre; ++kb) {
         uint8_t *st = stages + kb * C::kStage;
@@ -214,7 +238,6 @@ __global__ void __launch_bounds__(kThreads, MINB)
         }
         mbar_expect_tx(&bars->full[s], C::kFullBytes);
         const int k0 = kbase + kb * kBK;
-        if (MODE == MODE_LORA) tma_load_2d(st + C::kARawOff, &tmA, &bars->full[s], 0, k0);
         uint8_t *wt = st + C::kAOff;
         tma_load_2d(wt, &tmW0, &bars->full[s], n0, k0);
         tma_load_2d(wt + kWBox, &tmW0, &bars->full[s], n0 + 64, k0);
@@ -225,6 +248,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
           nx += 2 * kWBox;
         }
         if (C::kTmaX) tma_load_2d(nx, &tmX, &bars->full[s], k0, 0);
+        if (C::kSlices && kb == slice_at) issue_slices();
       }
       TPO_T(10);
     }
@@ -281,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
     const int erow = (warp & 3) * 32 + lane;
     float bcol[MODE == MODE_LORA ? 16 : 1];
     float dsc = 0.f;
-    if (MODE == MODE_LORA && erow / rows_per == int(rank)) {
+    if (MODE == MODE_LORA && (p.epi_atomic || erow / rows_per == int(rank))) {
 #pragma unroll
       for (int r = 0; r < 16; ++r) bcol[r] = __bfloat162float(p.lora_b[size_t(r) * p.N + n0 + erow]);
     }
@@ -326,28 +350,29 @@ __global__ void __launch_bounds__(kThreads, MINB)
     }
     if (MODE == MODE_LORA) {
       // XA = X·A (16 tokens x 16 ranks over this CTA's K range) on the warp
-      // MMA path of the otherwise idle epilogue warps, from the staged X^T
-      // tile (K-major, 128-B swizzle) and the raw A box [64 k][16 r]: warp q
-      // takes k16 step q of every stage, two m16n8k16 bf16 MMAs with fp32
-      // accumulation (exact products), while the tensor cores run X·W.
+      // MMA path of the otherwise idle epilogue warps, from the X^T slice
+      // (K-major, 128-B swizzle B tiles) and the A slice ([64 k][16 r]
+      // boxes) staged ahead of the W stream: warp q takes k16 step q of
+      // every k block, two m16n8k16 bf16 MMAs with fp32 accumulation (exact
+      // products).  Done within ~1 µs of the slices landing, so the XA
+      // exchange and XA·B̄ are off the critical path.
       const int q = warp & 3;
       float c[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
       const int mi = lane >> 3, ri = lane & 7;
       const int tok = ri + 8 * (mi & 1);
       const int kch = 2 * q + (mi >> 1);
-      const uint32_t a_off = C::kBOff + (tok >> 3) * 1024 + (tok & 7) * 128 + ((kch ^ (tok & 7)) << 4);
-      const uint32_t b_off = C::kARawOff + (16 * q + ri + 8 * (mi & 1)) * 32 + (mi >> 1) * 16;
+      const uint32_t a_off = (tok >> 3) * 1024 + (tok & 7) * 128 + ((kch ^ (tok & 7)) << 4);
+      const uint32_t b_off = (16 * q + ri + 8 * (mi & 1)) * 32 + (mi >> 1) * 16;
+      mbar_wait(&bars->xa_full, 0);
+      const uint32_t xs0 = smem_u32(xsl), as0 = smem_u32(asl);
       for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % STAGES;
-        mbar_wait(&bars->full[s], (kb / STAGES) & 1);
-        const uint32_t st = smem_u32(stages + s * C::kStage);
         uint32_t af[4], bf[4];
         asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(af[0]), "=r"(af[1]), "=r"(af[2]), "=r"(af[3]) : "r"(st + a_off));
+                     : "=r"(af[0]), "=r"(af[1]), "=r"(af[2]), "=r"(af[3])
+                     : "r"(xs0 + kb * kXTile + a_off));
         asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(bf[0]), "=r"(bf[1]), "=r"(bf[2]), "=r"(bf[3]) : "r"(st + b_off));
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&bars->empty[s]);  // stage also released by the MMA commit
+                     : "=r"(bf[0]), "=r"(bf[1]), "=r"(bf[2]), "=r"(bf[3])
+                     : "r"(as0 + kb * C::kABox + b_off));
 #pragma unroll
         for (int j = 0; j < 2; ++j)
           asm volatile(
@@ -396,7 +421,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
     const bool xchg = !(p.dbg_flags & 2);  // experiment 2: no DSMEM exchange
     if (S > 1) {
       cluster_wait();  // every peer has initialised its barriers
-      if (xchg && MODE != MODE_GATED && t * 4 < kSide) {
+      if (xchg && MODE != MODE_GATED && !(atomic_epi && MODE == MODE_LORA) && t * 4 < kSide) {
         const float *src = side + rank * kSide + t * 4;
         for (int o = 1; o < S; ++o) {
           const uint32_t dst_rank = (rank + o) % S;
@@ -404,9 +429,10 @@ __global__ void __launch_bounds__(kThreads, MINB)
                     map_rank(&bars->recv_side, dst_rank));
         }
       }
-      if (xchg && MODE != MODE_GATED) mbar_wait(&bars->recv_side, 0);
+      if (xchg && MODE != MODE_GATED && !(atomic_epi && MODE == MODE_LORA)) mbar_wait(&bars->recv_side, 0);
+      if (atomic_epi) cluster_arrive();  // phase 2: rank 0's zeroed tile precedes every add
     }
-    if (MODE == MODE_RMS && mine) {
+    if (MODE == MODE_RMS && (mine || atomic_epi)) {
 #pragma unroll
       for (int tk = 0; tk < 8; ++tk) {
         float ss = 0.f;
@@ -422,12 +448,14 @@ __global__ void __launch_bounds__(kThreads, MINB)
         xa_tot[i] = v;
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (mine) {
+      if (mine || atomic_epi) {
+        // atomic: this CTA's own XA partial (linear: Σ_s XA_s·B̄ = XA·B̄)
+        const float *xsrc = atomic_epi ? side + rank * kSide : xa_tot;
 #pragma unroll
         for (int tk = 0; tk < 16; ++tk) post[tk] = 0.f;
 #pragma unroll
         for (int tk = 0; tk < 16; ++tk) {
-          const float4 *xr = reinterpret_cast<const float4 *>(xa_tot + tk * 16);
+          const float4 *xr = reinterpret_cast<const float4 *>(xsrc + tk * 16);
           float o = 0.f;
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
@@ -443,6 +471,12 @@ __global__ void __launch_bounds__(kThreads, MINB)
     }
 
     // ---- critical path: last MMA -> TMEM -> DSMEM -> owner -> HBM
+    // pin the post-loop operands here: without this the compiler may sink
+    // their computation past the waits below, onto the critical path
+    if (MODE != MODE_GATED && (mine || atomic_epi)) {
+#pragma unroll
+      for (int tk = 0; tk < T; ++tk) asm volatile("" : "+f"(post[tk]));
+    }
     mbar_wait(&bars->tmem_full, 0);
     if (threadIdx.x == 64) TPO_T(5);
     __syncwarp();  // tcgen05.ld is .sync.aligned: the warp must be converged
@@ -464,29 +498,41 @@ __global__ void __launch_bounds__(kThreads, MINB)
         for (int i = 0; i < 16; ++i) acc[i] = v[i];
       }
     }
-    if (S > 1 && xchg) {
-      if (!mine) {
-        // red slot [src rank][row - owner*rows_per][NV]
-        const uint32_t dst = map_rank(red + (int(rank) * rows_per + (row - owner * rows_per)) * NV, owner);
-        const uint32_t mb = map_rank(&bars->recv, owner);
+    if (atomic_epi) {
+      cluster_wait();  // phase 2
+      if (!(p.dbg_flags & 1)) {
 #pragma unroll
-        for (int i = 0; i < NV; i += 4) st_async4(dst + i * 4, acc[i], acc[i + 1], acc[i + 2], acc[i + 3], mb);
+        for (int tk = 0; tk < T; ++tk)
+          if (tk < p.tokens)
+            atomicAdd(p.out + size_t(tk) * p.N + n, MODE == MODE_RMS ? acc[tk] * post[tk] : acc[tk] + post[tk]);
+      }
+    } else if (S > 1 && xchg) {
+      if (!mine) {
+        // red layout [src rank][NV/4 chunks][rows_per][4]: the owner warp's
+        // lanes read consecutive 16-byte chunks (bank-conflict free)
+        const uint32_t mb = map_rank(&bars->recv, owner);
+        const int lr = row - owner * rows_per;
+#pragma unroll
+        for (int i = 0; i < NV; i += 4) {
+          const uint32_t dst = map_rank(red + ((int(rank) * (NV / 4) + i / 4) * rows_per + lr) * 4, owner);
+          st_async4(dst, acc[i], acc[i + 1], acc[i + 2], acc[i + 3], mb);
+        }
         if (threadIdx.x == 64) TPO_T(4);
       } else {
         mbar_wait(&bars->recv, 0);  // all peers' partials of the owned rows have landed
         if (lane == 0) TPO_T(6);
+        const int lr = row - int(rank) * rows_per;
         for (int rr = 0; rr < S; ++rr) {
           if (rr == int(rank)) continue;
-          const float4 *src = reinterpret_cast<const float4 *>(red + (rr * rows_per + (row - int(rank) * rows_per)) * NV);
 #pragma unroll
           for (int i = 0; i < NV / 4; ++i) {
-            const float4 v = src[i];
+            const float4 v = *reinterpret_cast<const float4 *>(red + ((rr * (NV / 4) + i) * rows_per + lr) * 4);
             acc[4 * i] += v.x, acc[4 * i + 1] += v.y, acc[4 * i + 2] += v.z, acc[4 * i + 3] += v.w;
           }
         }
       }
     }
-    if (mine && !(p.dbg_flags & 1)) {
+    if (mine && !atomic_epi && !(p.dbg_flags & 1)) {
 #pragma unroll
       for (int tk = 0; tk < T; ++tk) {
         float o;
@@ -495,15 +541,19 @@ __global__ void __launch_bounds__(kThreads, MINB)
         else o = acc[tk] + post[tk];
         if (tk < p.tokens) p.out[size_t(tk) * p.N + n] = o;
       }
+      if (lane == 0 && (S == 1 || q == int(rank) * (4 / S))) TPO_T(11);
     }
   }
   if (threadIdx.x == 64) TPO_T(2);
   if (S > 1 && warp < 2) {
     __syncwarp();
     cluster_wait();  // complete the start-up barrier phase for warps 0/1
+    if (atomic_epi) cluster_arrive();  // phase 2 (the epilogue warps wait on it)
   }
+  if (threadIdx.x == 0) TPO_T(13);
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) TPO_T(12);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<32>(tmem);
@@ -519,7 +569,8 @@ size_t skinny_smem(const SkinnyParams &p) {
   (void)nkb;
   size_t b = size_t(STAGES) * C::kStage +
              (S > 1 ? size_t(kTileN) * 16 * 4 : 0) + size_t(S) * C::kSide * 4 +
-             (MODE == MODE_LORA ? (256 + 1024) * 4 : 0) + sizeof(Bars);
+             (MODE == MODE_LORA ? (256 + 1024) * 4 : 0) +
+             (C::kSlices ? size_t(nkb) * (kXTile + C::kABox) : 0) + sizeof(Bars);
   return b + 1024;
 }
 

@@ -293,6 +293,60 @@ bool tmap_3d(CUtensorMap *m, const void *ptr, uint64_t d0, uint64_t d1, uint64_t
   return true;
 }
 
+// TPO_DEBUG_TIMES: per-CTA %globaltimer phase stamps (16 slots per CTA)
+// written by the kernels, summarised on stderr (µs since the first CTA
+// started).  Debug only: the launch is followed by a synchronising copy.
+unsigned long long *debug_begin(int nct, cudaStream_t st) {
+  static unsigned long long *dbg = nullptr;
+  if (!std::getenv("TPO_DEBUG_TIMES")) return nullptr;
+  if (!dbg) cudaMalloc(&dbg, 16 * 8 * 4096);
+  cudaMemsetAsync(dbg, 0, size_t(nct) * 128, st);
+  return dbg;
+}
+
+void debug_end(const char *tag, unsigned long long *dbg, int nct, cudaStream_t st) {
+  std::vector<unsigned long long> h(size_t(nct) * 16);
+  cudaMemcpyAsync(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  unsigned long long t0 = ~0ull;
+  for (int c = 0; c < nct; ++c)
+    if (h[size_t(c) * 16]) t0 = std::min(t0, h[size_t(c) * 16]);
+  static const char *names[14] = {"start", "setup", "epi_done", "last_mma", "sent", "tmem_full",
+                                  "recv_done", "end", "first_full", "b_ready", "last_tma",
+                                  "owner_done", "after_sync", "w0_at_sync"};
+  std::fprintf(stderr, "[tpo debug] %s ctas %d (us since first start)\n", tag, nct);
+  for (int k = 0; k < 14; ++k) {
+    double mn = 1e30, mx = 0, sum = 0;
+    int cnt = 0;
+    for (int c = 0; c < nct; ++c) {
+      unsigned long long v = h[size_t(c) * 16 + k];
+      if (!v) continue;
+      double d = double(v - t0) / 1e3;
+      mn = std::min(mn, d), mx = std::max(mx, d), sum += d, ++cnt;
+    }
+    if (cnt)
+      std::fprintf(stderr, "  %-12s n=%4d min %7.2f mean %7.2f max %7.2f\n", names[k], cnt, mn, sum / cnt, mx);
+  }
+  // skew within clusters of `cl` consecutive CTAs vs across clusters (slot 5)
+  const char *cs = std::getenv("TPO_DEBUG_CLUSTER");
+  const int cl = cs ? std::atoi(cs) : 0;
+  if (cl > 1) {
+    double within = 0, across_mx = 0, across_mn = 1e30;
+    int nc = 0;
+    for (int c0 = 0; c0 + cl <= nct; c0 += cl) {
+      double mx = 0, mn = 1e30;
+      for (int c = c0; c < c0 + cl; ++c) {
+        const double d = double(h[size_t(c) * 16 + 5] - t0) / 1e3;
+        mx = std::max(mx, d), mn = std::min(mn, d);
+      }
+      within += mx - mn, ++nc;
+      across_mx = std::max(across_mx, mx), across_mn = std::min(across_mn, mx);
+    }
+    std::fprintf(stderr, "  slot5 skew: mean within-cluster %.2f us, cluster-max range %.2f .. %.2f us\n",
+                 within / nc, across_mn, across_mx);
+  }
+}
+
 }  // namespace
 
 int launch_fused(const FusedPlan &p, const void *const *in, const int32_t *dt, float *const *out,
@@ -315,11 +369,19 @@ int launch_fused(const FusedPlan &p, const void *const *in, const int32_t *dt, f
     gp.l_per_cta = int(p.L / S);
     gp.out = out[0];
     int stages = env_int("TPO_STAGES", 3);
+    const int nct_g = int(p.groups) * S;
+    gp.dbg = debug_begin(nct_g, st);
     if (!tmap_3d(&maps[0], in[1], p.L, p.hd, p.groups, 64, 128, 1, CU_TENSOR_MAP_SWIZZLE_128B) ||
         !tmap_3d(&maps[1], in[2], p.hd, p.L, p.groups, 64, 128, 1, CU_TENSOR_MAP_SWIZZLE_128B) ||
         !tmap_3d(&maps[2], in[0], p.hd, p.qh, p.groups, 64, 16, 1, CU_TENSOR_MAP_SWIZZLE_128B))
       return int(cudaErrorInvalidValue);
-    return tpo_gqa_launch(stages, maps, &gp, st);
+    int rc_g = tpo_gqa_launch(stages, maps, &gp, st);
+    if (gp.dbg && !rc_g) {
+      char tag[96];
+      std::snprintf(tag, sizeof(tag), "gqa ksplit %d stages %d", S, stages);
+      debug_end(tag, gp.dbg, nct_g, st);
+    }
+    return rc_g;
   }
   SkinnyParams sp{};
   int mode = 0;
@@ -397,37 +459,15 @@ int launch_fused(const FusedPlan &p, const void *const *in, const int32_t *dt, f
   }
   sp.dbg_flags = env_int("TPO_DBG_FLAGS", 0);
   sp.epi_atomic = env_int("TPO_EPI_ATOMIC", 0);
-  static unsigned long long *dbg = nullptr;
   const int nct = int(p.n / 128) * sp.ksplit;
-  const bool debug_times = std::getenv("TPO_DEBUG_TIMES") != nullptr;
-  if (debug_times) {
-    if (!dbg) cudaMalloc(&dbg, 16 * 8 * 4096);
-    cudaMemsetAsync(dbg, 0, size_t(nct) * 128, st);
-    sp.dbg = dbg;
-  }
+  unsigned long long *dbg = debug_begin(nct, st);
+  sp.dbg = dbg;
   int rc = tpo_skinny_launch(mode, stages, minb, maps, &sp, st);
-  if (debug_times && !rc) {
-    std::vector<unsigned long long> h(size_t(nct) * 16);
-    cudaMemcpyAsync(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost, st);
-    cudaStreamSynchronize(st);
-    unsigned long long t0 = ~0ull;
-    for (int c = 0; c < nct; ++c) t0 = std::min(t0, h[size_t(c) * 16]);
-    static const char *names[14] = {"start", "setup", "epi_done", "last_mma", "sent", "tmem_full",
-                                    "recv_done", "end", "first_full", "b_ready", "last_tma",
-                                    "owner_done", "after_sync", "w0_at_sync"};
-    std::fprintf(stderr, "[tpo debug] mode %d ksplit %d stages %d minb %d prefetch %d ctas %d (us since first start)\n",
-                 mode, sp.ksplit, stages, minb, sp.prefetch_static, nct);
-    for (int k = 0; k < 14; ++k) {
-      double mn = 1e30, mx = 0, sum = 0;
-      int cnt = 0;
-      for (int c = 0; c < nct; ++c) {
-        unsigned long long v = h[size_t(c) * 16 + k];
-        if (!v) continue;
-        double d = double(v - t0) / 1e3;
-        mn = std::min(mn, d), mx = std::max(mx, d), sum += d, ++cnt;
-      }
-      if (cnt) std::fprintf(stderr, "  %-12s n=%4d min %7.2f mean %7.2f max %7.2f\n", names[k], cnt, mn, sum / cnt, mx);
-    }
+  if (dbg && !rc) {
+    char tag[128];
+    std::snprintf(tag, sizeof(tag), "mode %d ksplit %d stages %d minb %d prefetch %d", mode, sp.ksplit,
+                  stages, minb, sp.prefetch_static);
+    debug_end(tag, dbg, nct, st);
   }
   return rc;
 }

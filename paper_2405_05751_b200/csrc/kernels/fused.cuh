@@ -29,6 +29,7 @@ struct GqaParams {
   int ksplit, l_per_cta;     // cluster split of the kv loop
   const __nv_bfloat16 *q;
   float *out;                // [g, qh, hd]
+  unsigned long long *dbg;   // optional per-CTA phase timestamps (TPO_DEBUG_TIMES)
 };
 
 extern "C" int tpo_skinny_launch(int mode, int stages, int minb, const CUtensorMap *maps,

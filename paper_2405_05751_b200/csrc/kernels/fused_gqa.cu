@@ -79,6 +79,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   Bars *bars = reinterpret_cast<Bars *>(wsum + 4 * 8);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  unsigned long long *dbg = p.dbg ? p.dbg + blockIdx.x * 16 : nullptr;
+#define TPO_T(slot) \
+  if (dbg) dbg[slot] = globaltimer();
+  if (threadIdx.x == 0) TPO_T(0);
   const uint32_t rank = S > 1 ? cluster_rank() : 0;
   const int g = blockIdx.x / S;
   const int nb = p.l_per_cta / kBL;
@@ -110,6 +114,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;  // cols [0,16) S0, [16,32) S1, [32,48) O
+  if (threadIdx.x == 0) TPO_T(1);
   if (S > 1) cluster_arrive();
   if (threadIdx.x == 0 && S > 1) mbar_expect_tx(&bars->recv, uint32_t((S - 1) * (rows_per * 32 + 32)));
   pdl_wait();
@@ -132,6 +137,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_3d(st + 2 * kHalf, &tmV, &bars->full[s], 0, l, g);      // V[l.., d 0..63]
         tma_load_3d(st + 3 * kHalf, &tmV, &bars->full[s], 64, l, g);     // V[l.., d 64..]
       }
+      TPO_T(10);
     }
   } else if (warp == 1) {
     // -------------------------------------------------------- MMA issuer
@@ -158,6 +164,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int j = 0; j < nb; ++j) {
       const int s = j % STAGES, b = j & 1;
       mbar_wait(&bars->full[s], (j / STAGES) & 1);
+      if (j == 0 && lane == 0) TPO_T(8);
       if (j >= 2) mbar_wait(&bars->s_empty[b], ((j - 2) >> 1) & 1);
       tc_fence_after();
       if (elect_one()) {
@@ -223,6 +230,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("bar.sync 1, 128;" ::: "memory");
 
     mbar_wait(&bars->o_full, 0);
+    if (threadIdx.x == 64) TPO_T(5);
     __syncwarp();
     tc_fence_after();
     float ov[16], o[8];
@@ -246,6 +254,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       mbar_wait(&bars->recv, 0);
+      if (threadIdx.x == 64) TPO_T(6);
     }
     if (owner == int(rank)) {
       for (int rr = 0; rr < S; ++rr) {
@@ -273,6 +282,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc<64>(tmem);
   }
+  if (threadIdx.x == 0) TPO_T(7);
+#undef TPO_T
 }
 
 template <int STAGES, int S>

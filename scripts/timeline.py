@@ -17,10 +17,10 @@ for name in sys.argv[1:]:
     _, mu = F.bench_pair(name)
     g = ctx.compile(mu)
     if os.environ.get("STATIC"):
-        g.set_static_inputs({"gatedmlp": [1, 2], "rmsnorm": [1, 2, 3], "lora": [1, 2, 3]}[name])
+        g.set_static_inputs({"gatedmlp": [1, 2], "rmsnorm": [1, 2, 3], "lora": [1, 2, 3], "gqa": []}[name])
     host = make_inputs(name, F.BENCH[name]["args"])
     # cold runs: a fresh input copy per launch (12 x 34 MB > L2)
-    sets = [[x.cuda() for x in host] for _ in range(6 if name == "gatedmlp" else 12)]
+    sets = [[x.cuda() for x in host] for _ in range({"gatedmlp": 6, "gqa": 6}.get(name, 12))]
     for i in range(len(sets)):
         print(f"--- {name} launch {i} (inputs copy {i}, cold)", file=sys.stderr, flush=True)
         ctx.eval_mugraph(g, sets[i])

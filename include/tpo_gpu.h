@@ -29,6 +29,10 @@
  *   tpo_gpu_validate                <- tpo::ir::validate (B200 MemLimits)
  *   tpo_gpu_op_madds                <- tpo::ir::op_madds summed over a µGraph
  *                                      proj/core/include/tpo/ir/shape_infer.hpp:67-69
+ *   tpo_gpu_eval_vm                 <- tpo::interp::eval_mugraph / eval_program / eval_mugraph_f32
+ *                                      (generic GPU VM) proj/core/include/tpo/interp/interp.hpp:41-53
+ *   tpo_gpu_float_stability_filter  <- tpo::verify::float_stability_filter
+ *   tpo_gpu_stability_batch            proj/core/include/tpo/verify/stability.hpp:29-31
  */
 #ifndef TPO_GPU_H
 #define TPO_GPU_H
@@ -171,6 +175,33 @@ int tpo_gpu_verify_pool(tpo_gpu_ctx *ctx, const tpo_gpu_graph *program,
                         uint64_t n, const tpo_verify_cfg *cfg, const tpo_field_params *fp,
                         uint32_t *accept_dev, tpo_verdict *verdicts, uint64_t *attempts,
                         void *cuda_stream);
+
+/* Generic floating-point evaluation on the GPU µGraph VM (any graph whose
+ * working set fits shared memory), semantics of the reference evaluator:
+ *   mode 0  tpo::interp::eval_mugraph      (double)   interp.hpp:47-48
+ *   mode 1  tpo::interp::eval_program      (double; rejects GraphDefs) interp.hpp:41-42
+ *   mode 2  tpo::interp::eval_mugraph_f32  (float)    interp.hpp:51-53
+ * Inputs / outputs are HOST arrays of double (float for mode 2), inputs
+ * concatenated in graph-input order, outputs in graph-output order.
+ * Matmul/Sum/Accum accumulate in the reference's order with individually
+ * rounded ops (no FMA): add/mul/div/sqrt results are bit-identical to the
+ * reference; exp/SiLU may differ in the last ulp. */
+int tpo_gpu_eval_vm(tpo_gpu_ctx *ctx, const tpo_gpu_graph *g, int32_t mode, const void *in_host,
+                    void *out_host);
+
+/* tpo::verify::float_stability_filter(g, program, trials, tol, seed, input_scale)
+ * proj/core/include/tpo/verify/stability.hpp:29-31 on the GPU; *out_ok = 1/0. */
+int tpo_gpu_float_stability_filter(tpo_gpu_ctx *ctx, const tpo_gpu_graph *g,
+                                   const tpo_gpu_graph *program, int32_t trials, double tol,
+                                   uint64_t seed, double input_scale, int32_t *out_ok);
+
+/* The same for n candidates in one launch: ok[k] = 1 pass, 0 fail, -1 the
+ * candidate's interface differs from the program's.  seeds (nullable): a
+ * seed per candidate, else `seed` for all (the reference default is 17). */
+int tpo_gpu_stability_batch(tpo_gpu_ctx *ctx, const tpo_gpu_graph *program,
+                            const tpo_gpu_graph *const *cands, const uint64_t *seeds, uint64_t n,
+                            int32_t trials, double tol, uint64_t seed, double input_scale,
+                            int8_t *ok);
 
 /* Reference op_madds work of a graph (SURVEY §8d verifier work unit). */
 int64_t tpo_gpu_op_madds(const tpo_gpu_graph *g);

@@ -159,6 +159,58 @@ class Context:
                                                   C.c_void_p(stream) if stream else None))
         return outputs
 
+    def eval_vm(self, g, inputs: Sequence, mode: int = 0):
+        """Generic GPU µGraph VM (``tpo_gpu_eval_vm``): mode 0 eval_mugraph
+        (double), 1 eval_program (double, rejects GraphDefs), 2
+        eval_mugraph_f32 (float).  numpy inputs in graph-input order; returns
+        numpy outputs."""
+        g = self.compile(g)
+        dt = np.float32 if mode == 2 else np.float64
+        shapes = g.shapes(False)
+        if len(inputs) != len(shapes):
+            raise ValueError("input count")
+        flat = np.concatenate([np.ascontiguousarray(x, dtype=dt).reshape(-1) for x in inputs]) \
+            if inputs else np.zeros(0, dt)
+        oshapes = g.shapes(True)
+        out = np.zeros(sum(int(np.prod(s)) for s in oshapes), dt)
+        N.check(N.lib().tpo_gpu_eval_vm(self.h, g.h, mode, flat.ctypes.data, out.ctypes.data))
+        res, c = [], 0
+        for s in oshapes:
+            k = int(np.prod(s))
+            res.append(out[c:c + k].reshape(s))
+            c += k
+        return res
+
+    def float_stability_filter(self, g, program, trials: int = 1, tol: float = 1e-3, seed: int = 17,
+                               scale: float = 1.0) -> bool:
+        """verify::float_stability_filter (stability.hpp:29-31) on the GPU."""
+        g, program = self.compile(g), self.compile(program)
+        ok = C.c_int32(0)
+        N.check(N.lib().tpo_gpu_float_stability_filter(self.h, g.h, program.h, trials, tol, seed,
+                                                         scale, C.addressof(ok)))
+        return bool(ok.value)
+
+    def stability_batch(self, program, cands: Sequence, seeds=None, trials: int = 1,
+                        tol: float = 1e-3, seed: int = 17, scale: float = 1.0) -> np.ndarray:
+        """The stability filter for many candidates in one launch: int8 per
+        candidate (1 pass, 0 fail, -1 interface mismatch)."""
+        prog = self.compile(program)
+        handles, hs = {}, []
+        for c in cands:
+            if id(c) not in handles:
+                handles[id(c)] = self.compile(c)
+            hs.append(handles[id(c)].h.value)
+        n = len(hs)
+        arr = (C.c_void_p * n)(*hs)
+        sd = None
+        if seeds is not None:
+            sd = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64))
+        ok = np.zeros(n, np.int8)
+        N.check(N.lib().tpo_gpu_stability_batch(self.h, prog.h, arr,
+                                                 sd.ctypes.data if sd is not None else None, n,
+                                                 trials, tol, seed, scale, ok.ctypes.data))
+        return ok
+
     # ---- finite field -------------------------------------------------------
     def ff_eval(self, g, seed: int, stream: int, with_silu: Optional[bool] = None, p=227, q=113,
                 wbase=4):

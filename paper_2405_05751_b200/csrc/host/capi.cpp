@@ -639,3 +639,163 @@ int tpo_gpu_verify_pool(tpo_gpu_ctx *ctx, const tpo_gpu_graph *program,
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Floating-point VM (kernels/fp_vm.cu): generic eval_mugraph / eval_program /
+// eval_mugraph_f32 and the batched float stability filter.
+// ---------------------------------------------------------------------------
+#include "../kernels/fp_vm.cuh"
+
+namespace tpo::gpu {
+namespace {
+
+size_t fp_smem(uint32_t code_len, uint64_t words, size_t elem) {
+  return size_t(code_len) * sizeof(TpoVmInstr) + size_t(words) * elem;
+}
+
+}  // namespace
+}  // namespace tpo::gpu
+
+extern "C" {
+
+int tpo_gpu_eval_vm(tpo_gpu_ctx *ctx, const tpo_gpu_graph *h, int32_t mode, const void *in_host,
+                    void *out_host) {
+  return guard([&] {
+    Ctx &C = ctx->c;
+    const Graph &G = h->g;
+    if (mode < 0 || mode > 2) throw Error(ErrCode::ConfigError, "mode: 0 eval_mugraph, 1 eval_program, 2 f32");
+    if (mode == 1)  // interp.cpp:20-28: the flat evaluator rejects GraphDefs
+      for (const ir::Op &op : G.g.ops)
+        if (op.type == ir::OpType::GraphDef)
+          throw Error(ErrCode::Unsupported, "eval_program: graph contains a GraphDef");
+    check_cuda(cudaSetDevice(C.device), "cudaSetDevice");
+    const size_t elem = mode == 2 ? 4 : 8;
+    const uint32_t n_in = uint32_t(G.in_elems);
+    VmProgram p = lower_vm(G.g, 0, n_in);
+    const size_t smem = fp_smem(uint32_t(p.code.size()), uint64_t(n_in) + p.region_words, elem);
+    if (smem > 232448)
+      throw Error(ErrCode::DoesNotFit, "fp VM working set " + std::to_string(smem) +
+                                           " B exceeds 227 KiB of shared memory");
+    cudaStream_t st = C.stream;
+    auto *dcode = static_cast<TpoVmInstr *>(C.code.get(p.code.size() * sizeof(TpoVmInstr) + 16));
+    check_cuda(cudaMemcpyAsync(dcode, p.code.data(), p.code.size() * sizeof(TpoVmInstr),
+                               cudaMemcpyHostToDevice, st), "code");
+    void *din = C.inputs.get(size_t(n_in) * elem + 16);
+    check_cuda(cudaMemcpyAsync(din, in_host, size_t(n_in) * elem, cudaMemcpyHostToDevice, st), "in");
+    const size_t n_out = size_t(G.out_elems);
+    void *dout = C.out.get(n_out * elem + 16);
+    tpo_fp::EvalArgs a{};
+    a.code = dcode;
+    a.code_len = uint32_t(p.code.size());
+    a.code_bytes = uint32_t(p.code.size() * sizeof(TpoVmInstr));
+    a.graph = p.desc;
+    a.n_in = n_in;
+    a.inputs = din;
+    a.out = dout;
+    check_cuda(cudaError_t(tpo_fp_launch_eval(&a, mode == 2, smem, st)), "fp eval launch");
+    check_cuda(cudaMemcpyAsync(out_host, dout, n_out * elem, cudaMemcpyDeviceToHost, st), "out");
+    check_cuda(cudaStreamSynchronize(st), "fp eval sync");
+    return 0;
+  });
+}
+
+int tpo_gpu_stability_batch(tpo_gpu_ctx *ctx, const tpo_gpu_graph *program,
+                            const tpo_gpu_graph *const *cands, const uint64_t *seeds, uint64_t n,
+                            int32_t trials, double tol, uint64_t seed, double input_scale,
+                            int8_t *ok) {
+  return guard([&] {
+    if (n == 0) return 0;
+    Ctx &C = ctx->c;
+    check_cuda(cudaSetDevice(C.device), "cudaSetDevice");
+    const Graph &P = program->g;
+    const uint32_t n_in = uint32_t(P.in_elems);
+    // program outputs pinned after the inputs; candidate region above them
+    VmProgram pp = lower_vm(P.g, 0, n_in, /*pin_outputs=*/true);
+    const uint32_t cbase = n_in + pp.pinned_words;
+    std::vector<TpoVmInstr> code(pp.code);
+    std::vector<TpoVmGraph> graphs;
+    TpoVmGraph d0 = pp.desc;
+    d0.code_off = 0;
+    d0.code_len = uint32_t(pp.code.size());
+    graphs.push_back(d0);
+    uint64_t maxw = uint64_t(n_in) + pp.region_words;
+    uint32_t max_cl = 0;
+    std::unordered_map<const tpo_gpu_graph *, uint32_t> idx;
+    std::vector<uint32_t> cg(n);
+    for (uint64_t k = 0; k < n; ++k) {
+      auto it = idx.find(cands[k]);
+      if (it == idx.end()) {
+        TpoVmGraph d;
+        try {
+          check_pair(P.g, cands[k]->g.g);
+          VmProgram cp = lower_vm(cands[k]->g.g, 0, cbase);
+          d = cp.desc;
+          d.code_off = uint32_t(code.size());
+          d.code_len = uint32_t(cp.code.size());
+          code.insert(code.end(), cp.code.begin(), cp.code.end());
+          maxw = std::max<uint64_t>(maxw, uint64_t(cbase) + cp.region_words);
+          max_cl = std::max(max_cl, d.code_len);
+        } catch (const Error &e) {
+          d = error_graph(e.code);
+        }
+        it = idx.emplace(cands[k], uint32_t(graphs.size())).first;
+        graphs.push_back(d);
+      }
+      cg[k] = it->second;
+    }
+    const size_t code_bytes = size_t(d0.code_len + max_cl) * sizeof(TpoVmInstr);
+    const size_t smem = code_bytes + size_t(maxw) * 8;
+    if (smem > 232448)
+      throw Error(ErrCode::DoesNotFit, "stability working set " + std::to_string(smem) +
+                                           " B exceeds 227 KiB of shared memory");
+    cudaStream_t st = C.stream;
+    auto *dcode = static_cast<TpoVmInstr *>(C.code.get(code.size() * sizeof(TpoVmInstr) + 16));
+    auto *dgraphs = static_cast<TpoVmGraph *>(C.graphs.get(graphs.size() * sizeof(TpoVmGraph)));
+    auto *dcg = static_cast<uint32_t *>(C.cand.get(n * 4));
+    auto *dok = static_cast<int8_t *>(C.verdicts.get(n));
+    auto *cnt = static_cast<unsigned long long *>(C.counter.get(16));
+    check_cuda(cudaMemcpyAsync(dcode, code.data(), code.size() * sizeof(TpoVmInstr), cudaMemcpyHostToDevice, st), "code");
+    check_cuda(cudaMemcpyAsync(dgraphs, graphs.data(), graphs.size() * sizeof(TpoVmGraph), cudaMemcpyHostToDevice, st), "graphs");
+    check_cuda(cudaMemcpyAsync(dcg, cg.data(), n * 4, cudaMemcpyHostToDevice, st), "cands");
+    check_cuda(cudaMemsetAsync(cnt, 0, 16, st), "counter");
+    tpo_fp::StabilityArgs a{};
+    a.code = dcode;
+    a.graphs = dgraphs;
+    a.code_bytes = uint32_t(code_bytes);
+    a.cand_graph = dcg;
+    if (seeds) {
+      auto *ds = static_cast<uint64_t *>(C.seeds.get(n * 8));
+      check_cuda(cudaMemcpyAsync(ds, seeds, n * 8, cudaMemcpyHostToDevice, st), "seeds");
+      a.seeds = ds;
+    }
+    a.seed = seed;
+    a.n = n;
+    a.n_in = n_in;
+    a.trials = trials;
+    a.tol = tol;
+    a.scale = input_scale;
+    a.counter = cnt;
+    a.ok = dok;
+    const int occ = tpo_fp_stability_occupancy(smem);
+    if (occ < 1) throw Error(ErrCode::DoesNotFit, "stability kernel does not fit on an SM");
+    const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>(uint64_t(C.num_sms) * occ, n));
+    check_cuda(cudaError_t(tpo_fp_launch_stability(&a, int(grid), smem, st)), "stability launch");
+    check_cuda(cudaMemcpyAsync(ok, dok, n, cudaMemcpyDeviceToHost, st), "ok");
+    check_cuda(cudaStreamSynchronize(st), "stability sync");
+    return 0;
+  });
+}
+
+int tpo_gpu_float_stability_filter(tpo_gpu_ctx *ctx, const tpo_gpu_graph *g,
+                                   const tpo_gpu_graph *program, int32_t trials, double tol,
+                                   uint64_t seed, double input_scale, int32_t *out_ok) {
+  int8_t ok = 0;
+  const tpo_gpu_graph *c = g;
+  const int rc = tpo_gpu_stability_batch(ctx, program, &c, nullptr, 1, trials, tol, seed, input_scale, &ok);
+  if (rc) return rc;
+  if (ok < 0) return fail(1000 + int(ErrCode::ShapeMismatch), "candidate does not match the program's interface");
+  *out_ok = ok;
+  return 0;
+}
+
+}  // extern "C"

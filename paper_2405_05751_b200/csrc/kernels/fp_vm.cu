@@ -1,0 +1,286 @@
+// B200 backend — floating-point µGraph VM (sm_100a): the generic fp path.
+//
+// The same block-batched bytecode as the Z_p×Z_q verifier (kernels/vm.h,
+// host/lower.cpp) interpreted with the reference's FloatSemantics<T>
+// (interp.hpp:27-38) instead of field arithmetic, out of shared memory, one
+// graph evaluation per CTA.  Used for
+//   * tpo_gpu_eval_small: eval_mugraph / eval_program (T = double) and
+//     eval_mugraph_f32 (T = float) of any graph whose VM working set fits
+//     shared memory (interp.cpp:20-41);
+//   * tpo_gpu_stability_batch: float_stability_filter (stability.cpp:25-50)
+//     for thousands of candidates per launch, normals drawn on the device
+//     from the closed-form splitmix64 stream (rng.hpp:53-62).
+//
+// Arithmetic order follows the reference exactly: Matmul accumulates
+// acc = add(acc, mul(a, b)) for k ascending from zero (eval_core.hpp:181-203),
+// Sum likewise (:205-222), Accum is acc = add(acc, val); every operation is
+// an individually rounded IEEE op (no FMA contraction: __dmul_rn /
+// __dadd_rn ...).  add/sub/mul/div/sqrt are therefore bit-identical to the
+// CPU oracle; exp (and SiLU, through exp) may differ in the last ulp (CUDA
+// libm vs glibc), as may the log/cos of Box–Muller.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "fp_vm.cuh"
+#include "vm.h"
+
+namespace tpo_fp {
+
+constexpr uint64_t kGamma = 0x9e3779b97f4a7c15ull;
+
+template <typename T>
+struct Ops;
+template <>
+struct Ops<double> {
+  static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+  static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+  static __device__ __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
+  static __device__ __forceinline__ double sqrt_(double a) { return __dsqrt_rn(a); }
+  static __device__ __forceinline__ double exp_(double a) { return exp(a); }
+};
+template <>
+struct Ops<float> {
+  static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+  static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+  static __device__ __forceinline__ float div(float a, float b) { return __fdiv_rn(a, b); }
+  static __device__ __forceinline__ float sqrt_(float a) { return __fsqrt_rn(a); }
+  static __device__ __forceinline__ float exp_(float a) { return expf(a); }
+};
+
+__device__ __forceinline__ uint32_t fdiv(uint32_t x, uint32_t mul, uint32_t sh) {
+  return mul ? (__umulhi(x, mul) >> sh) : x;
+}
+
+__device__ __forceinline__ void offsets(const TpoVmInstr &I, uint32_t idx, int32_t &od, int32_t &oa,
+                                        int32_t &ob, bool &wr) {
+  od = oa = ob = 0;
+  wr = true;
+  for (int k = int(I.ndim) - 1; k >= 0; --k) {
+    const uint32_t d = I.dims[k];
+    const uint32_t qt = fdiv(idx, I.dmul[k], I.dsh[k]);
+    const uint32_t c = idx - qt * d;
+    idx = qt;
+    od += int32_t(c) * I.sd[k];
+    oa += int32_t(c) * I.sa[k];
+    ob += int32_t(c) * I.sb[k];
+    if (((I.wmask >> k) & 1u) && c != d - 1) wr = false;
+  }
+}
+
+__device__ __forceinline__ void copy_code(TpoVmInstr *dst, const TpoVmInstr *src, uint32_t len) {
+  const uint32_t n = len * uint32_t(sizeof(TpoVmInstr) / 16);
+  const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+  uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) d4[i] = __ldg(s4 + i);
+  __syncthreads();
+}
+
+// One graph's bytecode over VM memory W (shared).  Block-uniform.
+template <typename T>
+__device__ void run_program(T *W, const TpoVmInstr *code, uint32_t len) {
+  using O = Ops<T>;
+  uint32_t it = 0, loop_pc = 0, trips = 1;
+  for (uint32_t pc = 0; pc < len; ++pc) {
+    const TpoVmInstr &I = code[pc];
+    const uint8_t op = I.op;
+    if (op == VM_LOOP) {
+      trips = I.n, it = 0, loop_pc = pc;
+      continue;
+    }
+    if (op == VM_ENDLOOP) {
+      if (++it < trips) pc = loop_pc;
+      continue;
+    }
+    const uint32_t n = I.n;
+    const bool flat = I.flags & VM_FLAT;
+    switch (op) {
+      case VM_ZERO:
+        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) W[I.dst + i] = T(0);
+        break;
+      case VM_COPY: {
+        const uint32_t dbase = I.dst + it * I.d_iter, abase = I.a + it * I.a_iter;
+        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+          if (flat) {
+            W[dbase + i] = W[abase + i];
+          } else {
+            int32_t od, oa, ob;
+            bool wr;
+            offsets(I, i, od, oa, ob, wr);
+            if (wr) W[dbase + od] = W[abase + oa];
+          }
+        }
+        break;
+      }
+      case VM_UNARY:
+        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+          const T a = W[I.a + i];
+          T r;
+          switch (I.sub) {
+            case VM_EXP: r = O::exp_(a); break;
+            case VM_SQR: r = O::mul(a, a); break;  // eval_core: Sqr = mul(a, a)
+            case VM_SQRT: r = O::sqrt_(a); break;
+            default: r = O::div(a, O::add(T(1), O::exp_(-a))); break;  // SiLU (interp.hpp:36)
+          }
+          W[I.dst + i] = r;
+        }
+        break;
+      case VM_BINARY:
+        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+          int32_t od = int32_t(i), oa = int32_t(i), ob = int32_t(i);
+          bool wr = true;
+          if (!flat) offsets(I, i, od, oa, ob, wr);
+          const T a = W[I.a + oa], b = W[I.b + ob];
+          W[I.dst + od] = I.sub == VM_ADD ? O::add(a, b) : I.sub == VM_MUL ? O::mul(a, b) : O::div(a, b);
+        }
+        break;
+      case VM_MATMUL: {
+        const uint32_t Bi = I.dims[1], M = I.dims[2], K = I.dims[3], N = I.dims[4];
+        const uint32_t MN = M * N;
+        for (uint32_t o = threadIdx.x; o < n; o += blockDim.x) {
+          const uint32_t blk = fdiv(o, I.dmul[0], I.dsh[0]);
+          uint32_t r = o - blk * Bi * MN;
+          const uint32_t bi = fdiv(r, I.dmul[1], I.dsh[1]);
+          r -= bi * MN;
+          const uint32_t m = fdiv(r, I.dmul[2], I.dsh[2]), c = r - m * N;
+          const T *pa = W + I.a + blk * uint32_t(I.sa[0]) + bi * M * K + m * K;
+          const T *pb = W + I.b + blk * uint32_t(I.sb[0]) + bi * K * N + c;
+          T acc = T(0);
+          for (uint32_t k = 0; k < K; ++k) acc = O::add(acc, O::mul(pa[k], pb[k * N]));
+          W[I.dst + o] = acc;
+        }
+        break;
+      }
+      case VM_SUM: {
+        const uint32_t mid = I.dims[1], grp = I.dims[2], inner = I.dims[3];
+        for (uint32_t o = threadIdx.x; o < n; o += blockDim.x) {
+          const uint32_t t = fdiv(o, I.dmul[0], I.dsh[0]), in_i = o - t * inner;
+          const uint32_t ou = fdiv(t, I.dmul[1], I.dsh[1]), m = t - ou * mid;
+          const T *pa = W + I.a + (ou * mid * grp + m * grp) * inner + in_i;
+          T acc = T(0);
+          for (uint32_t g = 0; g < grp; ++g) acc = O::add(acc, pa[g * inner]);
+          W[I.dst + o] = acc;
+        }
+        break;
+      }
+      default:
+        break;
+    }
+    __syncthreads();
+  }
+}
+
+// Draw j (0-based) of Rng::derive(seed, stream): fin(s0 + (j+1)·γ), s0 the
+// state after derive's discarded draw (rng.hpp:30-40).
+__device__ __forceinline__ uint64_t fin(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+// Rng::normal for element e: draws 2e, 2e+1 (rng.hpp:53-62).
+__device__ __forceinline__ double normal_at(uint64_t s0, uint64_t e) {
+  const uint64_t r1 = fin(s0 + (2 * e + 1) * kGamma), r2 = fin(s0 + (2 * e + 2) * kGamma);
+  double u1 = double(r1 >> 11) * (1.0 / 9007199254740992.0);
+  const double u2 = double(r2 >> 11) * (1.0 / 9007199254740992.0);
+  if (u1 < 1e-300) u1 = 1e-300;
+  return __dmul_rn(sqrt(__dmul_rn(-2.0, log(u1))), cos(__dmul_rn(6.283185307179586, u2)));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) eval_kernel(EvalArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  TpoVmInstr *code = reinterpret_cast<TpoVmInstr *>(smem);
+  T *W = reinterpret_cast<T *>(smem + a.code_bytes);
+  copy_code(code, a.code, a.code_len);
+  const T *in = static_cast<const T *>(a.inputs);
+  for (uint32_t e = threadIdx.x; e < a.n_in; e += blockDim.x) W[e] = in[e];
+  __syncthreads();
+  run_program<T>(W, code, a.code_len);
+  T *out = static_cast<T *>(a.out);
+  uint32_t c = 0;
+  for (uint32_t t = 0; t < a.graph.n_out; ++t) {
+    for (uint32_t i = threadIdx.x; i < a.graph.out_len[t]; i += blockDim.x) out[c + i] = W[a.graph.out_off[t] + i];
+    c += a.graph.out_len[t];
+  }
+}
+
+// float_stability_filter for candidates [0, n): persistent CTAs, one
+// candidate at a time; stops at the first failing trial like the reference.
+__global__ void __launch_bounds__(kThreads) stability_kernel(StabilityArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ int s_fail;
+  __shared__ unsigned long long s_cand;
+  TpoVmInstr *pcode = reinterpret_cast<TpoVmInstr *>(smem);
+  TpoVmInstr *ccode = pcode + a.graphs[0].code_len;
+  double *W = reinterpret_cast<double *>(smem + a.code_bytes);
+  const TpoVmGraph g1 = a.graphs[0];
+  copy_code(pcode, a.code + g1.code_off, g1.code_len);
+  uint32_t staged = 0xffffffffu;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_cand = atomicAdd(a.counter, 1ull);
+    __syncthreads();
+    const unsigned long long k = s_cand;
+    if (k >= a.n) break;
+    const uint32_t gi = a.cand_graph[k];
+    const TpoVmGraph g2 = a.graphs[gi];
+    int verdict;  // 1 pass, 0 fail, -1 error (shape mismatch / not lowerable)
+    if (g2.err) {
+      verdict = -1;
+    } else {
+      if (gi != staged) {
+        copy_code(ccode, a.code + g2.code_off, g2.code_len);
+        staged = gi;
+      }
+      verdict = 1;
+      const uint64_t seed = a.seeds ? a.seeds[k] : a.seed;
+      for (int trial = 0; trial < a.trials && verdict == 1; ++trial) {
+        const uint64_t s0 = (seed ^ (kGamma * (uint64_t(trial) + 1))) + kGamma;  // derive + discard
+        for (uint32_t e = threadIdx.x; e < a.n_in; e += blockDim.x)
+          W[e] = __dmul_rn(normal_at(s0, e), a.scale);
+        if (threadIdx.x == 0) s_fail = 0;
+        __syncthreads();
+        run_program<double>(W, pcode, g1.code_len);
+        run_program<double>(W, ccode, g2.code_len);
+        // stability.cpp:39-47: non-finite candidate output, or relative error
+        // |o - r| / max(|r|, 1e-6) > tol (a NaN error does not fail)
+        bool bad = false;
+        for (uint32_t t = 0; t < g1.n_out; ++t)
+          for (uint32_t i = threadIdx.x; i < g1.out_len[t]; i += blockDim.x) {
+            const double r = W[g1.out_off[t] + i], o = W[g2.out_off[t] + i];
+            if (!isfinite(o)) bad = true;
+            const double err = fabs(o - r) / fmax(fabs(r), 1e-6);
+            if (err > a.tol) bad = true;
+          }
+        if (bad) s_fail = 1;
+        __syncthreads();
+        if (s_fail) verdict = 0;
+      }
+    }
+    if (threadIdx.x == 0) a.ok[k] = int8_t(verdict);
+  }
+}
+
+}  // namespace tpo_fp
+
+extern "C" int tpo_fp_launch_eval(const tpo_fp::EvalArgs *a, int f32, size_t smem, cudaStream_t st) {
+  auto kern = f32 ? tpo_fp::eval_kernel<float> : tpo_fp::eval_kernel<double>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  kern<<<1, tpo_fp::kThreads, smem, st>>>(*a);
+  return int(cudaGetLastError());
+}
+
+extern "C" int tpo_fp_launch_stability(const tpo_fp::StabilityArgs *a, int grid, size_t smem,
+                                       cudaStream_t st) {
+  cudaFuncSetAttribute(tpo_fp::stability_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  tpo_fp::stability_kernel<<<grid, tpo_fp::kThreads, smem, st>>>(*a);
+  return int(cudaGetLastError());
+}
+
+extern "C" int tpo_fp_stability_occupancy(size_t smem) {
+  int blocks = 0;
+  cudaFuncSetAttribute(tpo_fp::stability_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, tpo_fp::stability_kernel, tpo_fp::kThreads, smem);
+  return blocks;
+}

@@ -273,6 +273,11 @@ class Lowerer {
   }
 
   void emit(TpoVmInstr in) {
+    if (in.op == VM_MATMUL && (in.flags & VM_STRIDED) && in.dims[4] % 2 == 0 && in.dims[6] % 2 == 0 &&
+        in.n / 4 >= 256) {
+      in.flags |= VM_TILE22;  // one thread, 2 x 2 outputs: shared operand loads
+      in.n /= 4;
+    }
     tpo_vm_set_divisors(&in);
     p_.code.push_back(in);
   }
@@ -294,6 +299,8 @@ class Lowerer {
     return a;
   }
 
+  // Matmul over contiguous (block-batched) operands, expressed in the
+  // strided form every VM matmul uses (kernels/vm.h VM_STRIDED).
   void emit_matmul(uint32_t d, uint32_t a, uint32_t b, const TensorShape &sa, const TensorShape &sb,
                    int64_t nb, bool inv_a, bool inv_b, uint8_t q) {
     const int r = sa.rank();
@@ -302,19 +309,18 @@ class Lowerer {
     TpoVmInstr i;
     std::memset(&i, 0, sizeof(i));
     i.op = VM_MATMUL;
+    i.flags = VM_STRIDED;
     i.dst = d;
     i.a = a;
     i.b = b;
-    i.ndim = 5;
-    i.dims[0] = uint32_t(nb);
-    i.dims[1] = uint32_t(Bi);
-    i.dims[2] = uint32_t(M);
-    i.dims[3] = uint32_t(K);
-    i.dims[4] = uint32_t(N);
-    i.sd[0] = i32(Bi * M * N);
+    i.ndim = 7;
+    const int64_t d7[7] = {nb, 1, 1, Bi, M, K, N};
+    for (int k = 0; k < 7; ++k) i.dims[k] = uint32_t(d7[k]);
     i.sa[0] = inv_a ? 0 : i32(Bi * M * K);
     i.sb[0] = inv_b ? 0 : i32(Bi * K * N);
-    if (int64_t(nb) * Bi * M * N > INT32_MAX) throw Error(ErrCode::DoesNotFit, "VM matmul too large");
+    i.sa[3] = i32(M * K), i.sa[4] = i32(K), i.sa[5] = 1;
+    i.sb[3] = i32(K * N), i.sb[5] = i32(N), i.sb[6] = 1;
+    if (nb * Bi * M * N > INT32_MAX) throw Error(ErrCode::DoesNotFit, "VM matmul too large");
     i.n = uint32_t(nb * Bi * M * N);
     i.qd = q;
     emit(i);
@@ -526,6 +532,121 @@ class Lowerer {
       for (TensorId t : b.outputs)
         if (bbuf[size_t(t)] == UINT32_MAX) bbuf[size_t(t)] = alloc(copies(t) * numel(bshape(t)));
 
+    // ---- operand views and fused accumulation (thread-graph-free fusion of
+    // the block graph's data movement into its matmuls):
+    //  * an InIter tile consumed only by in-loop Matmuls is not copied: the
+    //    Matmul reads it in place through strides (VM_STRIDED);
+    //  * a Matmul whose only consumer is a φ-Accum accumulates straight into
+    //    the accumulator (VM_ACCUM: acc = add(acc, A·B), the reference's
+    //    Accum update, eval_core.hpp:311-320).
+    std::vector<std::vector<const Op *>> cons(nt);
+    for (const Op &b : bg.ops)
+      for (TensorId t : b.inputs) cons[size_t(t)].push_back(&b);
+    struct Operand {
+      uint32_t base;
+      int64_t g[3];
+      std::vector<int64_t> dims, st;
+      int32_t it_step;
+    };
+    std::vector<char> is_view(nt, 0);
+    std::vector<Operand> views(nt);
+    std::vector<char> acc_fused(nt, 0);  // Accum output fed by a fused Matmul
+    auto collapsible = [](const std::vector<int64_t> &d, const std::vector<int64_t> &st) {
+      // batch dims (all but the last two) must flatten to one stride
+      const int r = int(d.size());
+      int64_t prev = -1, prev_d = 1;
+      for (int i = r - 3; i >= 0; --i) {
+        if (d[size_t(i)] == 1) continue;
+        if (prev >= 0 && st[size_t(i)] != prev * prev_d) return false;
+        prev = st[size_t(i)], prev_d = d[size_t(i)];
+      }
+      return true;
+    };
+    for (const Op &b : bg.ops) {
+      if (b.type != OpType::InIter) continue;
+      const TensorId o = b.outputs[0];
+      if (cons[size_t(o)].empty() || bshape(o).rank() < 2) continue;
+      bool ok = true;
+      for (const Op *c : cons[size_t(o)]) ok = ok && c->type == OpType::Matmul && !is_post(*c);
+      if (!ok) continue;
+      const auto &a = std::get<InIterAttrs>(b.attrs);
+      const TensorShape &dev = g_.tensor(op.inputs[size_t(a.operand)]).shape;
+      if (dev.rank() != bshape(o).rank()) continue;
+      if (!collapsible(bshape(o).dims, contiguous(dev.dims))) continue;
+      is_view[size_t(o)] = 1;
+    }
+    auto operand = [&](TensorId t) {
+      Operand d;
+      if (is_view[size_t(t)]) return views[size_t(t)];
+      d.base = bget(t);
+      const int64_t E = numel(bshape(t));
+      const bool inv = binv[size_t(t)];
+      d.g[0] = inv ? 0 : G[1] * G[2] * E;
+      d.g[1] = inv ? 0 : G[2] * E;
+      d.g[2] = inv ? 0 : E;
+      d.dims = bshape(t).dims;
+      d.st = contiguous(d.dims);
+      d.it_step = 0;
+      return d;
+    };
+    auto matmul_fusable = [&](const Op &b) {
+      if (b.type != OpType::Matmul || is_post(b)) return false;
+      bool any_view = is_view[size_t(b.inputs[0])] || is_view[size_t(b.inputs[1])];
+      const auto &oc = cons[size_t(b.outputs[0])];
+      bool to_acc = false;
+      if (oc.size() == 1 && oc[0]->type == OpType::Accum) {
+        const auto &fa = std::get<AccumAttrs>(oc[0]->attrs);
+        to_acc = !fa.fmap.axes() || fa.fmap.targets[0] == kReplica;
+      }
+      return any_view || to_acc;
+    };
+    auto emit_strided_matmul = [&](const Op &b) {
+      const TensorId ta = b.inputs[0], tb = b.inputs[1], to = b.outputs[0];
+      const Operand A = operand(ta), B = operand(tb);
+      const int r = bshape(ta).rank();
+      const int64_t M = A.dims[size_t(r - 2)], K = A.dims[size_t(r - 1)], N = B.dims[size_t(r - 1)];
+      // batch dims flatten to one index whose stride is the innermost
+      // non-unit batch dim's (layouts were checked collapsible)
+      int64_t Bi = 1, sab = 0, sbb = 0;
+      for (int i = 0; i < r - 2; ++i) {
+        Bi *= A.dims[size_t(i)];
+        if (A.dims[size_t(i)] != 1) sab = A.st[size_t(i)], sbb = B.st[size_t(i)];
+      }
+      const bool inv_out = binv[size_t(ta)] && binv[size_t(tb)];
+      const std::array<int64_t, 3> Go = inv_out ? std::array<int64_t, 3>{1, 1, 1} : G;
+      const auto &oc = cons[size_t(to)];
+      bool to_acc = false;
+      TensorId acc = -1;
+      if (oc.size() == 1 && oc[0]->type == OpType::Accum) {
+        const auto &fa = std::get<AccumAttrs>(oc[0]->attrs);
+        if (!fa.fmap.axes() || fa.fmap.targets[0] == kReplica) to_acc = true, acc = oc[0]->outputs[0];
+      }
+      TpoVmInstr i;
+      std::memset(&i, 0, sizeof(i));
+      i.op = VM_MATMUL;
+      i.flags = VM_STRIDED | (to_acc ? VM_ACCUM : 0);
+      i.dst = to_acc ? bbuf[size_t(acc)] : bbuf[size_t(to)];
+      i.a = A.base;
+      i.b = B.base;
+      i.ndim = 7;
+      const int64_t d7[7] = {Go[0], Go[1], Go[2], Bi, M, K, N};
+      for (int k = 0; k < 7; ++k) i.dims[k] = uint32_t(d7[k]);
+      for (int k = 0; k < 3; ++k) i.sa[k] = i32(A.g[k]), i.sb[k] = i32(B.g[k]);
+      i.sa[3] = i32(sab), i.sb[3] = i32(sbb);
+      i.sa[4] = i32(A.st[size_t(r - 2)]), i.sa[5] = i32(A.st[size_t(r - 1)]);
+      i.sb[5] = i32(B.st[size_t(r - 2)]), i.sb[6] = i32(B.st[size_t(r - 1)]);
+      i.a_iter = A.it_step;
+      i.b_iter = B.it_step;
+      const int64_t n = Go[0] * Go[1] * Go[2] * Bi * M * N;
+      if (n > INT32_MAX) throw Error(ErrCode::DoesNotFit, "VM matmul too large");
+      i.n = uint32_t(n);
+      const uint8_t q = bqd[size_t(ta)] & bqd[size_t(tb)];
+      i.qd = q;
+      emit(i);
+      bqd[size_t(to)] = q;
+      if (to_acc) acc_fused[size_t(acc)] = 1;
+    };
+
     auto run_compute = [&](const Op &b) {
       std::vector<uint32_t> ins;
       std::vector<TensorShape> shapes;
@@ -578,6 +699,17 @@ class Lowerer {
           if (ft < 0 || ft >= dev.rank()) throw Error(ErrCode::ShapeMismatch, "fmap target");
           it_step = i32((part[size_t(ft)] / bg.forloop) * ds[size_t(ft)]);
         }
+        if (is_view[size_t(o)]) {  // read in place by its Matmul consumers
+          Operand w;
+          w.base = buf(src);
+          for (int k = 0; k < 3; ++k) w.g[k] = a_g[size_t(k)];
+          w.dims = tile.dims;
+          w.st = ds;
+          w.it_step = it_step;
+          views[size_t(o)] = w;
+          bqd[size_t(o)] = kqd_[size_t(src)];
+          continue;
+        }
         v.dims = cat(v.dims, tile.dims);
         v.st = {cat(d_g, contiguous(tile.dims)), cat(a_g, ds)};
         v.wm.assign(v.dims.size(), 0);
@@ -593,7 +725,9 @@ class Lowerer {
         TensorId val = b.inputs.at(0), acc = b.outputs[0];
         const TensorShape &vs = bshape(val);
         int t = a.fmap.axes() ? a.fmap.targets[0] : kReplica;
-        if (t == kReplica) {
+        if (t == kReplica && acc_fused[size_t(acc)]) {
+          // already accumulated by the producing Matmul (VM_ACCUM)
+        } else if (t == kReplica) {
           View v;
           v.dims = {copies(val) * numel(vs)};
           v.st = {{1}, {1}, {1}};
@@ -623,6 +757,10 @@ class Lowerer {
         continue;
       }
       if (b.type == OpType::OutSaver || is_post(b)) continue;
+      if (matmul_fusable(b)) {
+        emit_strided_matmul(b);
+        continue;
+      }
       run_compute(b);
     }
     {

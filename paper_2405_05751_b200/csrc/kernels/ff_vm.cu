@@ -319,34 +319,84 @@ __device__ bool run_program(const Smem &s, const FieldConst &f, const TpoVmInstr
         break;
       }
       case VM_MATMUL: {
-        // dims {blocks, batch, M, K, N}; per-operand block strides (0: block-invariant).
-        // Products < (p-1)^2 accumulate raw in u32 and reduce every `lazy`
-        // terms (lazy >= 84k for p = 227: one reduction at the end).
-        const uint32_t Bi = I.dims[1], M = I.dims[2], K = I.dims[3], N = I.dims[4];
-        const uint32_t MN = M * N;
+        // dims {gx, gy, gz, batch, M, K, N}; operands read through strides
+        // (block layout or InIter views), sa/sb {gx, gy, gz, batch, m | -,
+        // k, - | n}; dst contiguous [grid][batch][M][N].  VM_TILE22: one
+        // index = a 2 x 2 output tile.  Products < (p-1)^2 accumulate raw in
+        // u32 and reduce every `lazy` terms (>= 84k for p = 227).
+        const bool tile = I.flags & VM_TILE22;
+        const uint32_t Bi = I.dims[3], M = I.dims[4], K = I.dims[5], N = I.dims[6];
+        const uint32_t tm = tile ? 2u : 1u, Mt = M / tm, Nt = N / tm, MNt = Mt * Nt;
         const uint32_t lazy = f.lazy;
+        const int32_t ska = I.sa[5], skb = I.sb[5], sma = I.sa[4], snb = I.sb[6];
         for (uint32_t o = threadIdx.x; o < n; o += blockDim.x) {
           const uint32_t blk = fdiv(o, I.dmul[0], I.dsh[0]);
-          uint32_t r = o - blk * Bi * MN;
+          uint32_t r = o - blk * Bi * MNt;
           const uint32_t bi = fdiv(r, I.dmul[1], I.dsh[1]);
-          r -= bi * MN;
-          const uint32_t m = fdiv(r, I.dmul[2], I.dsh[2]), c = r - m * N;
-          const uint32_t *pa = W + I.a + blk * uint32_t(I.sa[0]) + bi * M * K + m * K;
-          const uint32_t *pb = W + I.b + blk * uint32_t(I.sb[0]) + bi * K * N + c;
+          r -= bi * MNt;
+          const uint32_t mt = fdiv(r, I.dmul[2], I.dsh[2]), ct = r - mt * Nt;
+          const uint32_t gx = fdiv(blk, I.dmul[3], I.dsh[3]), gr = blk - gx * I.dims[1] * I.dims[2];
+          const uint32_t gy = fdiv(gr, I.dmul[4], I.dsh[4]), gz = gr - gy * I.dims[2];
+          const uint32_t m = mt * tm, c = ct * tm;
+          const uint32_t *pa = W + int32_t(I.a + it * I.a_iter) + int32_t(gx) * I.sa[0] +
+                               int32_t(gy) * I.sa[1] + int32_t(gz) * I.sa[2] + int32_t(bi) * I.sa[3] +
+                               int32_t(m) * sma;
+          const uint32_t *pb = W + int32_t(I.b + it * I.b_iter) + int32_t(gx) * I.sb[0] +
+                               int32_t(gy) * I.sb[1] + int32_t(gz) * I.sb[2] + int32_t(bi) * I.sb[3] +
+                               int32_t(c) * snb;
+          const uint32_t dbase = I.dst + ((blk * Bi + bi) * M + m) * N + c;
+          if (tile) {
+            uint32_t ap[4] = {0, 0, 0, 0}, aq[4] = {0, 0, 0, 0};  // (m, c), (m, c+1), (m+1, c), (m+1, c+1)
+            for (uint32_t k0 = 0; k0 < K; k0 += lazy) {
+              const uint32_t k1 = min(K, k0 + lazy);
+              uint32_t sp[4] = {0, 0, 0, 0}, sq[4] = {0, 0, 0, 0};
+#pragma unroll 2
+              for (uint32_t k = k0; k < k1; ++k) {
+                const uint32_t a0 = pa[int32_t(k) * ska], a1 = pa[int32_t(k) * ska + sma];
+                const uint32_t b0 = pb[int32_t(k) * skb], b1 = pb[int32_t(k) * skb + snb];
+                const uint32_t a0p = a0 & 0xffffu, a0q = a0 >> 16, a1p = a1 & 0xffffu, a1q = a1 >> 16;
+                const uint32_t b0p = b0 & 0xffffu, b0q = b0 >> 16, b1p = b1 & 0xffffu, b1q = b1 >> 16;
+                sp[0] += a0p * b0p, sq[0] += a0q * b0q;
+                sp[1] += a0p * b1p, sq[1] += a0q * b1q;
+                sp[2] += a1p * b0p, sq[2] += a1q * b0q;
+                sp[3] += a1p * b1p, sq[3] += a1q * b1q;
+              }
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                ap[j] = mod32(ap[j] + mod32(sp[j], p, mp), p, mp);
+                aq[j] = mod32(aq[j] + mod32(sq[j], q, mq), q, mq);
+              }
+            }
+            const uint32_t off[4] = {0, 1, N, N + 1};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              uint32_t accp = ap[j], accq = aq[j];
+              if (I.flags & VM_ACCUM) {  // fused φ-Accum: acc = add(acc, A·B)
+                const uint32_t d = W[dbase + off[j]];
+                accp += d & 0xffffu;
+                accp = accp >= p ? accp - p : accp;
+                accq += d >> 16;
+                accq = accq >= q ? accq - q : accq;
+              }
+              W[dbase + off[j]] = accp | ((qd ? accq : 0u) << 16);
+            }
+            continue;
+          }
           uint32_t accp = 0, accq = 0;
           for (uint32_t k0 = 0; k0 < K; k0 += lazy) {
             const uint32_t k1 = min(K, k0 + lazy);
             uint32_t p0 = 0, p1 = 0, q0 = 0, q1 = 0;  // 4 independent chains
             uint32_t k = k0;
             for (; k + 2 <= k1; k += 2) {
-              const uint32_t va0 = pa[k], vb0 = pb[k * N], va1 = pa[k + 1], vb1 = pb[(k + 1) * N];
+              const uint32_t va0 = pa[int32_t(k) * ska], vb0 = pb[int32_t(k) * skb];
+              const uint32_t va1 = pa[int32_t(k + 1) * ska], vb1 = pb[int32_t(k + 1) * skb];
               p0 += (va0 & 0xffffu) * (vb0 & 0xffffu);
               q0 += (va0 >> 16) * (vb0 >> 16);
               p1 += (va1 & 0xffffu) * (vb1 & 0xffffu);
               q1 += (va1 >> 16) * (vb1 >> 16);
             }
             if (k < k1) {
-              const uint32_t va0 = pa[k], vb0 = pb[k * N];
+              const uint32_t va0 = pa[int32_t(k) * ska], vb0 = pb[int32_t(k) * skb];
               p0 += (va0 & 0xffffu) * (vb0 & 0xffffu);
               q0 += (va0 >> 16) * (vb0 >> 16);
             }
@@ -354,7 +404,14 @@ __device__ bool run_program(const Smem &s, const FieldConst &f, const TpoVmInstr
             accp = mod32(accp + mod32(p0, p, mp) + mod32(p1, p, mp), p, mp);
             accq = mod32(accq + mod32(q0, q, mq) + mod32(q1, q, mq), q, mq);
           }
-          W[I.dst + o] = accp | ((qd ? accq : 0u) << 16);
+          if (I.flags & VM_ACCUM) {  // fused φ-Accum: acc = add(acc, A·B)
+            const uint32_t d = W[dbase];
+            accp += d & 0xffffu;
+            accp = accp >= p ? accp - p : accp;
+            accq += d >> 16;
+            accq = accq >= q ? accq - q : accq;
+          }
+          W[dbase] = accp | ((qd ? accq : 0u) << 16);
         }
         break;
       }

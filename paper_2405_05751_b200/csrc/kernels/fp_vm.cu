@@ -135,19 +135,35 @@ __device__ void run_program(T *W, const TpoVmInstr *code, uint32_t len) {
         }
         break;
       case VM_MATMUL: {
-        const uint32_t Bi = I.dims[1], M = I.dims[2], K = I.dims[3], N = I.dims[4];
-        const uint32_t MN = M * N;
+        // strided form (kernels/vm.h); VM_TILE22: 2 x 2 outputs per index.
+        // Each output accumulates acc = add(acc, mul(a, b)) for k ascending.
+        const bool tile = I.flags & VM_TILE22;
+        const uint32_t Bi = I.dims[3], M = I.dims[4], K = I.dims[5], N = I.dims[6];
+        const uint32_t tm = tile ? 2u : 1u, Mt = M / tm, Nt = N / tm, MNt = Mt * Nt;
+        const int32_t ska = I.sa[5], skb = I.sb[5], sma = I.sa[4], snb = I.sb[6];
         for (uint32_t o = threadIdx.x; o < n; o += blockDim.x) {
           const uint32_t blk = fdiv(o, I.dmul[0], I.dsh[0]);
-          uint32_t r = o - blk * Bi * MN;
+          uint32_t r = o - blk * Bi * MNt;
           const uint32_t bi = fdiv(r, I.dmul[1], I.dsh[1]);
-          r -= bi * MN;
-          const uint32_t m = fdiv(r, I.dmul[2], I.dsh[2]), c = r - m * N;
-          const T *pa = W + I.a + blk * uint32_t(I.sa[0]) + bi * M * K + m * K;
-          const T *pb = W + I.b + blk * uint32_t(I.sb[0]) + bi * K * N + c;
-          T acc = T(0);
-          for (uint32_t k = 0; k < K; ++k) acc = O::add(acc, O::mul(pa[k], pb[k * N]));
-          W[I.dst + o] = acc;
+          r -= bi * MNt;
+          const uint32_t mt = fdiv(r, I.dmul[2], I.dsh[2]), ct = r - mt * Nt;
+          const uint32_t gx = fdiv(blk, I.dmul[3], I.dsh[3]), gr = blk - gx * I.dims[1] * I.dims[2];
+          const uint32_t gy = fdiv(gr, I.dmul[4], I.dsh[4]), gz = gr - gy * I.dims[2];
+          const uint32_t m = mt * tm, c = ct * tm;
+          const T *pa = W + int32_t(I.a + it * I.a_iter) + int32_t(gx) * I.sa[0] + int32_t(gy) * I.sa[1] +
+                        int32_t(gz) * I.sa[2] + int32_t(bi) * I.sa[3] + int32_t(m) * sma;
+          const T *pb = W + int32_t(I.b + it * I.b_iter) + int32_t(gx) * I.sb[0] + int32_t(gy) * I.sb[1] +
+                        int32_t(gz) * I.sb[2] + int32_t(bi) * I.sb[3] + int32_t(c) * snb;
+          const uint32_t dbase = I.dst + ((blk * Bi + bi) * M + m) * N + c;
+          for (uint32_t j = 0; j < tm * tm; ++j) {
+            const uint32_t dm = j / tm, dc = j % tm;
+            T acc = T(0);
+            for (uint32_t k = 0; k < K; ++k)
+              acc = O::add(acc, O::mul(pa[int32_t(k) * ska + int32_t(dm) * sma],
+                                       pb[int32_t(k) * skb + int32_t(dc) * snb]));
+            T &dst = W[dbase + dm * N + dc];
+            dst = (I.flags & VM_ACCUM) ? O::add(dst, acc) : acc;  // acc = add(acc, val)
+          }
         }
         break;
       }

@@ -27,6 +27,8 @@ enum TpoVmOp {
   VM_UNARY,      // dst[i] = f(a[view])           sub: VM_EXP, VM_SQR, VM_SQRT, VM_SILU
   VM_BINARY,     // dst[i] = f(a[view], b[view])  sub: VM_ADD, VM_MUL, VM_DIV
   VM_MATMUL,     // dims {B, M, K, N}; a [B,M,K], b [B,K,N], dst [B,M,N] contiguous
+                 // VM_STRIDED: dims {gx, gy, gz, B, M, K, N} with per-operand grid /
+                 // batch / row / k strides (operands read in place: InIter views)
   VM_SUM,        // dims {outer, mid, group, inner}: dst[o,m,i] = sum_t a[o, m*group+t, i]
   VM_LOOP,       // n = trip count; body follows
   VM_ENDLOOP,    // jump back to the instruction after the matching VM_LOOP
@@ -38,6 +40,9 @@ enum TpoVmFlags {
   VM_FLAT = 1,    // all operands contiguous over the index space: no index math
   VM_A_QD = 2,    // operand a is q-defined (FF mode, static)
   VM_B_QD = 4,    // operand b is q-defined
+  VM_STRIDED = 8, // MATMUL: strided operand views (see VM_MATMUL)
+  VM_ACCUM = 16,  // MATMUL: dst = dst + A·B (a fused φ-Accum, acc = add(acc, val))
+  VM_TILE22 = 32, // MATMUL: each index is a 2 x 2 output tile (rows 2i, 2i+1; cols 2j, 2j+1)
 };
 
 struct TpoVmInstr {
@@ -55,7 +60,8 @@ struct TpoVmInstr {
   uint32_t dmul[TPO_VM_DIMS];
   uint8_t dsh[TPO_VM_DIMS];
   uint8_t pad2;
-  uint32_t pad3[3];            // 192 bytes: copied to shared memory as uint4
+  int32_t b_iter;              // MATMUL VM_STRIDED: per-iteration offset added to b
+  uint32_t pad3[2];            // 192 bytes: copied to shared memory as uint4
 };
 
 // Host helper: the (mul, shift) pair of divisor d >= 1 (CUTLASS-style
@@ -75,7 +81,16 @@ static inline void tpo_vm_divisor(uint32_t d, uint32_t *mul, uint8_t *sh) {
 
 static inline void tpo_vm_set_divisors(TpoVmInstr *I) {
   for (int k = 0; k < TPO_VM_DIMS; ++k) I->dmul[k] = 0, I->dsh[k] = 0;
-  if (I->op == VM_MATMUL) {
+  if (I->op == VM_MATMUL && (I->flags & VM_STRIDED)) {
+    // {B*M*N, M*N, N, gy*gz, gz}; with VM_TILE22 over M/2 x N/2 tiles
+    const uint32_t t = (I->flags & VM_TILE22) ? 2u : 1u;
+    const uint32_t Mt = I->dims[4] / t, Nt = I->dims[6] / t, MN = Mt * Nt;
+    tpo_vm_divisor(I->dims[3] * MN, &I->dmul[0], &I->dsh[0]);
+    tpo_vm_divisor(MN, &I->dmul[1], &I->dsh[1]);
+    tpo_vm_divisor(Nt, &I->dmul[2], &I->dsh[2]);
+    tpo_vm_divisor(I->dims[1] * I->dims[2], &I->dmul[3], &I->dsh[3]);
+    tpo_vm_divisor(I->dims[2], &I->dmul[4], &I->dsh[4]);
+  } else if (I->op == VM_MATMUL) {
     const uint32_t MN = I->dims[2] * I->dims[4];
     tpo_vm_divisor(I->dims[1] * MN, &I->dmul[0], &I->dsh[0]);
     tpo_vm_divisor(MN, &I->dmul[1], &I->dsh[1]);

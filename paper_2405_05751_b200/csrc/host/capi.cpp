@@ -173,7 +173,7 @@ Batch build_batch(const Graph &prog, const std::vector<const Graph *> &uniq) {
   bt.n_in = uint32_t(prog.in_elems);
   // program outputs pinned right after the inputs; program scratch above
   // them is dead once the candidate starts, so the candidate region reuses it
-  VmProgram pp = lower_vm(prog.g, 0, bt.n_in, /*pin_outputs=*/true);
+  VmProgram pp = lower_vm(prog.g, 0, bt.n_in, /*pin_outputs=*/true, /*field=*/true);
   const uint32_t cbase = bt.n_in + pp.pinned_words;
   if (pp.poisoned) pp.desc.err = uint8_t(1 + int(ErrCode::PoisonedExponent));
   add_graph(bt, pp);
@@ -181,7 +181,7 @@ Batch build_batch(const Graph &prog, const std::vector<const Graph *> &uniq) {
   for (const Graph *c : uniq) {
     try {
       check_pair(prog.g, c->g);
-      VmProgram cp = lower_vm(c->g, 0, cbase);
+      VmProgram cp = lower_vm(c->g, 0, cbase, false, /*field=*/true);
       if (cp.poisoned) cp.desc.err = uint8_t(1 + int(ErrCode::PoisonedExponent));
       maxw = std::max(maxw, cbase + cp.region_words);
       add_graph(bt, cp);
@@ -511,7 +511,7 @@ int tpo_gpu_ff_eval(tpo_gpu_ctx *ctx, const tpo_gpu_graph *h, const tpo_field_pa
     const Graph &G = h->g;
     FieldState &fs = C.field(fpp->p, fpp->q, fpp->omega_base);
     const uint32_t n_in = uint32_t(G.in_elems);
-    VmProgram p = lower_vm(G.g, 0, n_in);
+    VmProgram p = lower_vm(G.g, 0, n_in, false, /*field=*/true);
     if (p.poisoned) throw Error(ErrCode::PoisonedExponent, "exponent depends on a prior exponentiation");
     const size_t smem = fs.fc.table_bytes + size_t(n_in + p.region_words) * 4;
     if (smem > 232448) throw Error(ErrCode::DoesNotFit, "graph exceeds shared memory");

@@ -110,8 +110,8 @@ TpoVmInstr make(uint8_t op, uint8_t sub, View v, uint32_t dst, uint32_t a, uint3
 
 class Lowerer {
  public:
-  Lowerer(const KernelGraph &g, uint32_t in_base, uint32_t region, bool pin)
-      : g_(g), region_(region), pin_(pin) {
+  Lowerer(const KernelGraph &g, uint32_t in_base, uint32_t region, bool pin, bool field)
+      : g_(g), region_(region), pin_(pin), field_(field) {
     kbuf_.assign(g.tensors.size(), UINT32_MAX);
     kqd_.assign(g.tensors.size(), 1);
     uint32_t off = in_base;
@@ -165,6 +165,7 @@ class Lowerer {
   const KernelGraph &g_;
   uint32_t region_;
   bool pin_;
+  bool field_;
   static constexpr uint32_t kVirt = 0x80000000u;  // virtual buffer id tag
   std::vector<int64_t> vsize_;                    // words per virtual buffer
   std::vector<uint32_t> kbuf_;
@@ -551,6 +552,7 @@ class Lowerer {
     std::vector<char> is_view(nt, 0);
     std::vector<Operand> views(nt);
     std::vector<char> acc_fused(nt, 0);  // Accum output fed by a fused Matmul
+    std::vector<TpoVmInstr> hoisted;     // field mode: loop-spanning Matmuls
     auto collapsible = [](const std::vector<int64_t> &d, const std::vector<int64_t> &st) {
       // batch dims (all but the last two) must flatten to one stride
       const int r = int(d.size());
@@ -642,9 +644,18 @@ class Lowerer {
       i.n = uint32_t(n);
       const uint8_t q = bqd[size_t(ta)] & bqd[size_t(tb)];
       i.qd = q;
-      emit(i);
       bqd[size_t(to)] = q;
       if (to_acc) acc_fused[size_t(acc)] = 1;
+      if (field_ && to_acc && bg.forloop > 1 && int64_t(i.a_iter) == K * i.sa[5] &&
+          int64_t(i.b_iter) == K * i.sb[5] && K * bg.forloop <= INT32_MAX) {
+        // both operands walk one k tile per iteration: the loop is just the
+        // continuation of the k sum — one Matmul over K·forloop after it
+        i.dims[5] = uint32_t(K * bg.forloop);
+        i.a_iter = i.b_iter = 0;
+        hoisted.push_back(i);
+        return;
+      }
+      emit(i);
     };
 
     auto run_compute = [&](const Op &b) {
@@ -769,6 +780,7 @@ class Lowerer {
       E.op = VM_ENDLOOP;
       emit(E);
     }
+    for (const TpoVmInstr &h : hoisted) emit(h);
 
     // ---- post-loop ops and OutSavers (eval_core.hpp:348-375)
     size_t saver = 0;
@@ -813,8 +825,8 @@ class Lowerer {
 }  // namespace
 
 VmProgram lower_vm(const KernelGraph &g, uint32_t input_base, uint32_t region_base,
-                   bool pin_outputs) {
-  return Lowerer(g, input_base, region_base, pin_outputs).run();
+                   bool pin_outputs, bool field) {
+  return Lowerer(g, input_base, region_base, pin_outputs, field).run();
 }
 
 int64_t input_elems(const KernelGraph &g) {

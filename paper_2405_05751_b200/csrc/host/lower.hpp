@@ -30,8 +30,13 @@ struct VmProgram {
 // pinned_words) and everything above is scratch that is dead once the
 // program finishes.  Throws tpo::Error on graphs outside the supported
 // fragment.
+// `field`: the program runs in Z_p x Z_q, where sums are exact and may be
+// reassociated: a φ-accumulated Matmul whose operand views advance by one
+// k tile per for-loop iteration is hoisted out of the loop as ONE Matmul
+// over the whole K range (not done for floating point, which must keep the
+// reference's per-iteration summation order).
 VmProgram lower_vm(const ir::KernelGraph &g, uint32_t input_base, uint32_t region_base,
-                   bool pin_outputs = false);
+                   bool pin_outputs = false, bool field = false);
 
 int64_t graph_madds(const ir::KernelGraph &g);
 int64_t input_elems(const ir::KernelGraph &g);

@@ -15,6 +15,7 @@
 #include "lower.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -274,8 +275,12 @@ class Lowerer {
   }
 
   void emit(TpoVmInstr in) {
+    static const uint32_t tile_min = [] {
+      const char *e = std::getenv("TPO_VM_TILE_MIN");
+      return e ? uint32_t(std::atoi(e)) : 64u;  // measured: 64 best (profiles)
+    }();
     if (in.op == VM_MATMUL && (in.flags & VM_STRIDED) && in.dims[4] % 2 == 0 && in.dims[6] % 2 == 0 &&
-        in.n / 4 >= 256) {
+        in.n / 4 >= tile_min) {
       in.flags |= VM_TILE22;  // one thread, 2 x 2 outputs: shared operand loads
       in.n /= 4;
     }

@@ -521,10 +521,40 @@ class Lowerer {
       for (TensorId t : b.outputs) binv[size_t(t)] = inv;
     }
 
+    std::vector<std::vector<const Op *>> cons(nt);
+    for (const Op &b : bg.ops)
+      for (TensorId t : b.inputs) cons[size_t(t)].push_back(&b);
+    // A concat-Accum of an InIter tile along that tile's own fmap dim is the
+    // untiled tile over the whole loop range (the concat is an address
+    // offset): when only Matmuls consume it, it is a view of
+    // the kernel input — no per-iteration copy, no accumulator buffer.
+    std::vector<char> concat_view(nt, 0), concat_src(nt, 0);
+    for (const Op &b : bg.ops) {
+      if (b.type != OpType::Accum) continue;
+      const auto &fa = std::get<AccumAttrs>(b.attrs);
+      if (!fa.fmap.axes() || fa.fmap.targets[0] == kReplica) continue;
+      const TensorId val = b.inputs[0], acc = b.outputs[0];
+      const Op *prod = nullptr;
+      for (const Op &c : bg.ops)
+        for (TensorId t : c.outputs)
+          if (t == val) prod = &c;
+      if (!prod || prod->type != OpType::InIter || cons[size_t(val)].size() != 1) continue;
+      const auto &ia = std::get<InIterAttrs>(prod->attrs);
+      if (!ia.fmap.axes() || ia.fmap.targets[0] != fa.fmap.targets[0]) continue;
+      if (cons[size_t(acc)].empty() || bshape(acc).rank() < 2) continue;
+      bool ok = true;
+      for (const Op *c : cons[size_t(acc)]) ok = ok && c->type == OpType::Matmul;
+      const TensorShape &dev = g_.tensor(op.inputs[size_t(ia.operand)]).shape;
+      if (!ok || dev.rank() != bshape(acc).rank()) continue;
+      concat_view[size_t(acc)] = 1;
+      concat_src[size_t(val)] = 1;
+    }
+
     // accumulators: the Accum output buffer is the running state
     for (const Op &b : bg.ops)
       if (b.type == OpType::Accum) {
         TensorId t = b.outputs[0];
+        if (concat_view[size_t(t)]) continue;
         bbuf[size_t(t)] = alloc(copies(t) * numel(bshape(t)));
         View v;
         v.dims = {copies(t) * numel(bshape(t))};
@@ -545,9 +575,6 @@ class Lowerer {
     //  * a Matmul whose only consumer is a φ-Accum accumulates straight into
     //    the accumulator (VM_ACCUM: acc = add(acc, A·B), the reference's
     //    Accum update, eval_core.hpp:311-320).
-    std::vector<std::vector<const Op *>> cons(nt);
-    for (const Op &b : bg.ops)
-      for (TensorId t : b.inputs) cons[size_t(t)].push_back(&b);
     struct Operand {
       uint32_t base;
       int64_t g[3];
@@ -597,8 +624,9 @@ class Lowerer {
       return d;
     };
     auto matmul_fusable = [&](const Op &b) {
-      if (b.type != OpType::Matmul || is_post(b)) return false;
+      if (b.type != OpType::Matmul) return false;
       bool any_view = is_view[size_t(b.inputs[0])] || is_view[size_t(b.inputs[1])];
+      if (is_post(b)) return any_view;  // post-loop: only concat views (loop-invariant)
       const auto &oc = cons[size_t(b.outputs[0])];
       bool to_acc = false;
       if (oc.size() == 1 && oc[0]->type == OpType::Accum) {
@@ -715,6 +743,20 @@ class Lowerer {
           if (ft < 0 || ft >= dev.rank()) throw Error(ErrCode::ShapeMismatch, "fmap target");
           it_step = i32((part[size_t(ft)] / bg.forloop) * ds[size_t(ft)]);
         }
+        if (concat_src[size_t(o)]) {  // feeds a concat-Accum view: the accumulator is a view
+          const Op *acc_op = cons[size_t(o)][0];
+          const TensorId acc = acc_op->outputs[0];
+          Operand w;
+          w.base = buf(src);
+          for (int k = 0; k < 3; ++k) w.g[k] = a_g[size_t(k)];
+          w.dims = bshape(acc).dims;
+          w.st = ds;
+          w.it_step = 0;
+          views[size_t(acc)] = w;
+          is_view[size_t(acc)] = 1;
+          bqd[size_t(o)] = kqd_[size_t(src)];
+          continue;
+        }
         if (is_view[size_t(o)]) {  // read in place by its Matmul consumers
           Operand w;
           w.base = buf(src);
@@ -743,6 +785,8 @@ class Lowerer {
         int t = a.fmap.axes() ? a.fmap.targets[0] : kReplica;
         if (t == kReplica && acc_fused[size_t(acc)]) {
           // already accumulated by the producing Matmul (VM_ACCUM)
+        } else if (t != kReplica && concat_view[size_t(acc)]) {
+          // a view of the kernel input (see concat_view)
         } else if (t == kReplica) {
           View v;
           v.dims = {copies(val) * numel(vs)};
@@ -822,6 +866,10 @@ class Lowerer {
         continue;
       }
       if (b.type == OpType::InIter || b.type == OpType::Accum || !is_post(b)) continue;
+      if (matmul_fusable(b)) {
+        emit_strided_matmul(b);
+        continue;
+      }
       run_compute(b);
     }
   }

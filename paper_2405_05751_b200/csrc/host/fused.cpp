@@ -426,17 +426,17 @@ int launch_fused(const FusedPlan &p, const void *const *in, const int32_t *dt, f
   // Weights (W / W1,W3 / A) declared static may stream before the PDL wait.
   const uint64_t weights = p.kind == TPO_FUSED_GATED_MLP ? 0x6 : p.kind == TPO_FUSED_LORA ? 0x6 : 0x4;
   sp.prefetch_static = (p.static_inputs & weights) == weights && !std::getenv("TPO_NO_PREFETCH");
-  // Pipeline: with static weights, the two-CTAs-per-SM configuration (the
-  // next evaluation's CTAs stream weights while this one drains); otherwise
-  // the measured-best single-CTA depth (profiles/r01: sweep) that fits.
+  // Pipeline depth: the measured-best single-CTA-per-SM depth that fits
+  // (profiles/r01: sweeps).  Two-CTA-per-SM configurations (TPO_MINB=2, let
+  // the next evaluation's CTAs become resident early) measured slower.
   int stages = env_int("TPO_STAGES", 0), minb = env_int("TPO_MINB", 0);
-  const size_t kTwoPerSm = 115712, kOnePerSm = 232448;
+  const size_t kOnePerSm = 232448;
   if (stages <= 0) {
-    if (sp.prefetch_static && minb != 1) {
+    if (minb == 2) {
       for (int s : {4, 3}) {
         const size_t b = tpo_skinny_smem(mode, s, 2, &sp);
-        if (b && b <= kTwoPerSm) {
-          stages = s, minb = 2;
+        if (b && b <= 115712) {
+          stages = s;
           break;
         }
       }

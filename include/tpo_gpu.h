@@ -176,8 +176,10 @@ int tpo_gpu_verify_pool(tpo_gpu_ctx *ctx, const tpo_gpu_graph *program,
                         uint32_t *accept_dev, tpo_verdict *verdicts, uint64_t *attempts,
                         void *cuda_stream);
 
-/* Generic floating-point evaluation on the GPU µGraph VM (any graph whose
- * working set fits shared memory), semantics of the reference evaluator:
+/* Generic floating-point evaluation on the GPU µGraph VM (any graph; working
+ * sets that fit shared memory run in one CTA, larger ones on the
+ * global-memory executor, one grid-wide launch per VM instruction),
+ * semantics of the reference evaluator:
  *   mode 0  tpo::interp::eval_mugraph      (double)   interp.hpp:47-48
  *   mode 1  tpo::interp::eval_program      (double; rejects GraphDefs) interp.hpp:41-42
  *   mode 2  tpo::interp::eval_mugraph_f32  (float)    interp.hpp:51-53

@@ -673,10 +673,41 @@ int tpo_gpu_eval_vm(tpo_gpu_ctx *ctx, const tpo_gpu_graph *h, int32_t mode, cons
     const uint32_t n_in = uint32_t(G.in_elems);
     VmProgram p = lower_vm(G.g, 0, n_in);
     const size_t smem = fp_smem(uint32_t(p.code.size()), uint64_t(n_in) + p.region_words, elem);
-    if (smem > 232448)
-      throw Error(ErrCode::DoesNotFit, "fp VM working set " + std::to_string(smem) +
-                                           " B exceeds 227 KiB of shared memory");
     cudaStream_t st = C.stream;
+    if (smem > 232448 || std::getenv("TPO_VM_GLOBAL")) {
+      // global-memory executor: VM memory in HBM, one launch per instruction
+      const uint64_t words = uint64_t(n_in) + p.region_words;
+      void *W = C.ws.get(words * elem + 16);
+      check_cuda(cudaMemcpyAsync(W, in_host, size_t(n_in) * elem, cudaMemcpyHostToDevice, st), "in");
+      size_t lb = 0;
+      uint32_t trips = 1;
+      for (size_t pc = 0; pc < p.code.size(); ++pc) {
+        const TpoVmInstr &I = p.code[pc];
+        if (I.op == VM_LOOP) {
+          lb = pc, trips = I.n;
+          // run the body `trips` times
+          size_t end = pc + 1;
+          while (end < p.code.size() && p.code[end].op != VM_ENDLOOP) ++end;
+          for (uint32_t it = 0; it < trips; ++it)
+            for (size_t k = pc + 1; k < end; ++k)
+              check_cuda(cudaError_t(tpo_fp_launch_instr(W, mode == 2, &p.code[k], it, C.num_sms, st)),
+                         "vm instr");
+          pc = end;  // skip ENDLOOP
+          continue;
+        }
+        check_cuda(cudaError_t(tpo_fp_launch_instr(W, mode == 2, &I, 0, C.num_sms, st)), "vm instr");
+      }
+      (void)lb;
+      size_t c = 0;
+      for (uint32_t t = 0; t < p.desc.n_out; ++t) {
+        check_cuda(cudaMemcpyAsync(static_cast<char *>(out_host) + c * elem,
+                                   static_cast<char *>(W) + size_t(p.desc.out_off[t]) * elem,
+                                   size_t(p.desc.out_len[t]) * elem, cudaMemcpyDeviceToHost, st), "out");
+        c += p.desc.out_len[t];
+      }
+      check_cuda(cudaStreamSynchronize(st), "vm sync");
+      return 0;
+    }
     auto *dcode = static_cast<TpoVmInstr *>(C.code.get(p.code.size() * sizeof(TpoVmInstr) + 16));
     check_cuda(cudaMemcpyAsync(dcode, p.code.data(), p.code.size() * sizeof(TpoVmInstr),
                                cudaMemcpyHostToDevice, st), "code");

@@ -76,10 +76,110 @@ __device__ __forceinline__ void copy_code(TpoVmInstr *dst, const TpoVmInstr *src
   __syncthreads();
 }
 
+// One VM instruction over items [start, n) with stride `step` (the
+// block-level interpreter passes threadIdx/blockDim, the global-memory
+// executor its grid-stride range).
+template <typename T>
+__device__ __forceinline__ void exec_instr(T *W, const TpoVmInstr &I, uint32_t it, uint32_t start,
+                                           uint32_t step) {
+  using O = Ops<T>;
+  const uint32_t n = I.n;
+  const bool flat = I.flags & VM_FLAT;
+  switch (I.op) {
+    case VM_ZERO:
+      for (uint32_t i = start; i < n; i += step) W[I.dst + i] = T(0);
+      break;
+    case VM_COPY: {
+      const uint32_t dbase = I.dst + it * I.d_iter, abase = I.a + it * I.a_iter;
+      for (uint32_t i = start; i < n; i += step) {
+        if (flat) {
+          W[dbase + i] = W[abase + i];
+        } else {
+          int32_t od, oa, ob;
+          bool wr;
+          offsets(I, i, od, oa, ob, wr);
+          if (wr) W[dbase + od] = W[abase + oa];
+        }
+      }
+      break;
+    }
+    case VM_UNARY:
+      for (uint32_t i = start; i < n; i += step) {
+        const T a = W[I.a + i];
+        T r;
+        switch (I.sub) {
+          case VM_EXP: r = O::exp_(a); break;
+          case VM_SQR: r = O::mul(a, a); break;  // eval_core: Sqr = mul(a, a)
+          case VM_SQRT: r = O::sqrt_(a); break;
+          default: r = O::div(a, O::add(T(1), O::exp_(-a))); break;  // SiLU (interp.hpp:36)
+        }
+        W[I.dst + i] = r;
+      }
+      break;
+    case VM_BINARY:
+      for (uint32_t i = start; i < n; i += step) {
+        int32_t od = int32_t(i), oa = int32_t(i), ob = int32_t(i);
+        bool wr = true;
+        if (!flat) offsets(I, i, od, oa, ob, wr);
+        const T a = W[I.a + oa], b = W[I.b + ob];
+        W[I.dst + od] = I.sub == VM_ADD ? O::add(a, b) : I.sub == VM_MUL ? O::mul(a, b) : O::div(a, b);
+      }
+      break;
+    case VM_MATMUL: {
+      // strided form (kernels/vm.h); VM_TILE22: 2 x 2 outputs per index.
+      // Each output accumulates acc = add(acc, mul(a, b)) for k ascending.
+      const bool tile = I.flags & VM_TILE22;
+      const uint32_t Bi = I.dims[3], M = I.dims[4], K = I.dims[5], N = I.dims[6];
+      const uint32_t tm = tile ? 2u : 1u, Mt = M / tm, Nt = N / tm, MNt = Mt * Nt;
+      const int32_t ska = I.sa[5], skb = I.sb[5], sma = I.sa[4], snb = I.sb[6];
+      for (uint32_t o = start; o < n; o += step) {
+        const uint32_t blk = fdiv(o, I.dmul[0], I.dsh[0]);
+        uint32_t r = o - blk * Bi * MNt;
+        const uint32_t bi = fdiv(r, I.dmul[1], I.dsh[1]);
+        r -= bi * MNt;
+        const uint32_t mt = fdiv(r, I.dmul[2], I.dsh[2]), ct = r - mt * Nt;
+        const uint32_t gx = fdiv(blk, I.dmul[3], I.dsh[3]), gr = blk - gx * I.dims[1] * I.dims[2];
+        const uint32_t gy = fdiv(gr, I.dmul[4], I.dsh[4]), gz = gr - gy * I.dims[2];
+        const uint32_t m = mt * tm, c = ct * tm;
+        const T *pa = W + int64_t(int32_t(I.a + it * I.a_iter)) + int64_t(gx) * I.sa[0] +
+                      int64_t(gy) * I.sa[1] + int64_t(gz) * I.sa[2] + int64_t(bi) * I.sa[3] +
+                      int64_t(m) * sma;
+        const T *pb = W + int64_t(int32_t(I.b + it * I.b_iter)) + int64_t(gx) * I.sb[0] +
+                      int64_t(gy) * I.sb[1] + int64_t(gz) * I.sb[2] + int64_t(bi) * I.sb[3] +
+                      int64_t(c) * snb;
+        const uint64_t dbase = uint64_t(I.dst) + ((uint64_t(blk) * Bi + bi) * M + m) * N + c;
+        for (uint32_t j = 0; j < tm * tm; ++j) {
+          const uint32_t dm = j / tm, dc = j % tm;
+          T acc = T(0);
+          for (uint32_t k = 0; k < K; ++k)
+            acc = O::add(acc, O::mul(pa[int64_t(k) * ska + int64_t(dm) * sma],
+                                     pb[int64_t(k) * skb + int64_t(dc) * snb]));
+          T &dst = W[dbase + uint64_t(dm) * N + dc];
+          dst = (I.flags & VM_ACCUM) ? O::add(dst, acc) : acc;  // acc = add(acc, val)
+        }
+      }
+      break;
+    }
+    case VM_SUM: {
+      const uint32_t mid = I.dims[1], grp = I.dims[2], inner = I.dims[3];
+      for (uint32_t o = start; o < n; o += step) {
+        const uint32_t t = fdiv(o, I.dmul[0], I.dsh[0]), in_i = o - t * inner;
+        const uint32_t ou = fdiv(t, I.dmul[1], I.dsh[1]), m = t - ou * mid;
+        const T *pa = W + I.a + (uint64_t(ou) * mid * grp + uint64_t(m) * grp) * inner + in_i;
+        T acc = T(0);
+        for (uint32_t g = 0; g < grp; ++g) acc = O::add(acc, pa[uint64_t(g) * inner]);
+        W[I.dst + o] = acc;
+      }
+      break;
+    }
+    default:
+      break;
+  }
+}
+
 // One graph's bytecode over VM memory W (shared).  Block-uniform.
 template <typename T>
 __device__ void run_program(T *W, const TpoVmInstr *code, uint32_t len) {
-  using O = Ops<T>;
   uint32_t it = 0, loop_pc = 0, trips = 1;
   for (uint32_t pc = 0; pc < len; ++pc) {
     const TpoVmInstr &I = code[pc];
@@ -92,98 +192,18 @@ __device__ void run_program(T *W, const TpoVmInstr *code, uint32_t len) {
       if (++it < trips) pc = loop_pc;
       continue;
     }
-    const uint32_t n = I.n;
-    const bool flat = I.flags & VM_FLAT;
-    switch (op) {
-      case VM_ZERO:
-        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) W[I.dst + i] = T(0);
-        break;
-      case VM_COPY: {
-        const uint32_t dbase = I.dst + it * I.d_iter, abase = I.a + it * I.a_iter;
-        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-          if (flat) {
-            W[dbase + i] = W[abase + i];
-          } else {
-            int32_t od, oa, ob;
-            bool wr;
-            offsets(I, i, od, oa, ob, wr);
-            if (wr) W[dbase + od] = W[abase + oa];
-          }
-        }
-        break;
-      }
-      case VM_UNARY:
-        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-          const T a = W[I.a + i];
-          T r;
-          switch (I.sub) {
-            case VM_EXP: r = O::exp_(a); break;
-            case VM_SQR: r = O::mul(a, a); break;  // eval_core: Sqr = mul(a, a)
-            case VM_SQRT: r = O::sqrt_(a); break;
-            default: r = O::div(a, O::add(T(1), O::exp_(-a))); break;  // SiLU (interp.hpp:36)
-          }
-          W[I.dst + i] = r;
-        }
-        break;
-      case VM_BINARY:
-        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-          int32_t od = int32_t(i), oa = int32_t(i), ob = int32_t(i);
-          bool wr = true;
-          if (!flat) offsets(I, i, od, oa, ob, wr);
-          const T a = W[I.a + oa], b = W[I.b + ob];
-          W[I.dst + od] = I.sub == VM_ADD ? O::add(a, b) : I.sub == VM_MUL ? O::mul(a, b) : O::div(a, b);
-        }
-        break;
-      case VM_MATMUL: {
-        // strided form (kernels/vm.h); VM_TILE22: 2 x 2 outputs per index.
-        // Each output accumulates acc = add(acc, mul(a, b)) for k ascending.
-        const bool tile = I.flags & VM_TILE22;
-        const uint32_t Bi = I.dims[3], M = I.dims[4], K = I.dims[5], N = I.dims[6];
-        const uint32_t tm = tile ? 2u : 1u, Mt = M / tm, Nt = N / tm, MNt = Mt * Nt;
-        const int32_t ska = I.sa[5], skb = I.sb[5], sma = I.sa[4], snb = I.sb[6];
-        for (uint32_t o = threadIdx.x; o < n; o += blockDim.x) {
-          const uint32_t blk = fdiv(o, I.dmul[0], I.dsh[0]);
-          uint32_t r = o - blk * Bi * MNt;
-          const uint32_t bi = fdiv(r, I.dmul[1], I.dsh[1]);
-          r -= bi * MNt;
-          const uint32_t mt = fdiv(r, I.dmul[2], I.dsh[2]), ct = r - mt * Nt;
-          const uint32_t gx = fdiv(blk, I.dmul[3], I.dsh[3]), gr = blk - gx * I.dims[1] * I.dims[2];
-          const uint32_t gy = fdiv(gr, I.dmul[4], I.dsh[4]), gz = gr - gy * I.dims[2];
-          const uint32_t m = mt * tm, c = ct * tm;
-          const T *pa = W + int32_t(I.a + it * I.a_iter) + int32_t(gx) * I.sa[0] + int32_t(gy) * I.sa[1] +
-                        int32_t(gz) * I.sa[2] + int32_t(bi) * I.sa[3] + int32_t(m) * sma;
-          const T *pb = W + int32_t(I.b + it * I.b_iter) + int32_t(gx) * I.sb[0] + int32_t(gy) * I.sb[1] +
-                        int32_t(gz) * I.sb[2] + int32_t(bi) * I.sb[3] + int32_t(c) * snb;
-          const uint32_t dbase = I.dst + ((blk * Bi + bi) * M + m) * N + c;
-          for (uint32_t j = 0; j < tm * tm; ++j) {
-            const uint32_t dm = j / tm, dc = j % tm;
-            T acc = T(0);
-            for (uint32_t k = 0; k < K; ++k)
-              acc = O::add(acc, O::mul(pa[int32_t(k) * ska + int32_t(dm) * sma],
-                                       pb[int32_t(k) * skb + int32_t(dc) * snb]));
-            T &dst = W[dbase + dm * N + dc];
-            dst = (I.flags & VM_ACCUM) ? O::add(dst, acc) : acc;  // acc = add(acc, val)
-          }
-        }
-        break;
-      }
-      case VM_SUM: {
-        const uint32_t mid = I.dims[1], grp = I.dims[2], inner = I.dims[3];
-        for (uint32_t o = threadIdx.x; o < n; o += blockDim.x) {
-          const uint32_t t = fdiv(o, I.dmul[0], I.dsh[0]), in_i = o - t * inner;
-          const uint32_t ou = fdiv(t, I.dmul[1], I.dsh[1]), m = t - ou * mid;
-          const T *pa = W + I.a + (ou * mid * grp + m * grp) * inner + in_i;
-          T acc = T(0);
-          for (uint32_t g = 0; g < grp; ++g) acc = O::add(acc, pa[g * inner]);
-          W[I.dst + o] = acc;
-        }
-        break;
-      }
-      default:
-        break;
-    }
+    exec_instr<T>(W, I, it, threadIdx.x, blockDim.x);
     __syncthreads();
   }
+}
+
+// Global-memory executor: one launch per VM instruction (the host walks the
+// bytecode and unrolls the for-loop), grid-stride over the instruction's
+// index space — graphs of any size (BASELINE shapes) in the reference's
+// arithmetic order.
+template <typename T>
+__global__ void __launch_bounds__(256) instr_kernel(T *W, const TpoVmInstr I, uint32_t it) {
+  exec_instr<T>(W, I, it, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
 }
 
 // Draw j (0-based) of Rng::derive(seed, stream): fin(s0 + (j+1)·γ), s0 the
@@ -284,6 +304,21 @@ extern "C" int tpo_fp_launch_eval(const tpo_fp::EvalArgs *a, int f32, size_t sme
   auto kern = f32 ? tpo_fp::eval_kernel<float> : tpo_fp::eval_kernel<double>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   kern<<<1, tpo_fp::kThreads, smem, st>>>(*a);
+  return int(cudaGetLastError());
+}
+
+extern "C" int tpo_fp_launch_instr(void *W, int f32, const TpoVmInstr *I, uint32_t it, int num_sms,
+                                   cudaStream_t st) {
+  const uint32_t items = I->n ? I->n : 1;
+  // matmul / sum items run long sequential loops: one item per thread;
+  // elementwise items: a few per thread
+  const bool heavy = I->op == VM_MATMUL || I->op == VM_SUM;
+  const uint64_t want = heavy ? (items + 255) / 256 : (items + 1023) / 1024;
+  const int grid = int(want < uint64_t(num_sms) * 16 ? (want ? want : 1) : uint64_t(num_sms) * 16);
+  if (f32)
+    tpo_fp::instr_kernel<float><<<grid, 256, 0, st>>>(static_cast<float *>(W), *I, it);
+  else
+    tpo_fp::instr_kernel<double><<<grid, 256, 0, st>>>(static_cast<double *>(W), *I, it);
   return int(cudaGetLastError());
 }
 

@@ -39,3 +39,5 @@ extern "C" int tpo_fp_launch_eval(const tpo_fp::EvalArgs *a, int f32, size_t sme
 extern "C" int tpo_fp_launch_stability(const tpo_fp::StabilityArgs *a, int grid, size_t smem,
                                        cudaStream_t st);
 extern "C" int tpo_fp_stability_occupancy(size_t smem);
+extern "C" int tpo_fp_launch_instr(void *W, int f32, const TpoVmInstr *I, uint32_t it, int num_sms,
+                                   cudaStream_t st);

@@ -104,3 +104,38 @@ def test_stability_batch_matches_reference(ctx):
     other, _ = F.verify_families()["gatedmlp"]
     prog, _ = F.verify_families()["rmsnorm"]
     assert ctx.stability_batch(prog, [other])[0] == -1
+
+
+def test_global_memory_executor_matches(ctx, monkeypatch):
+    """The global-memory executor (one grid-wide launch per VM instruction)
+    computes exactly what the shared-memory VM does."""
+    for tag in ("fp/gatedmlp/mugraph", "fp/lora/mugraph", "fp/rmsnorm/program", "edge/omap_partial",
+                "edge/concatmatmul", "gqa/g4/f4/eq"):
+        g = GRAPHS[tag]
+        ins = _inputs(g, 5)
+        smem = ctx.eval_vm(g, ins)
+        monkeypatch.setenv("TPO_VM_GLOBAL", "1")
+        glob = ctx.eval_vm(g, ins)
+        monkeypatch.delenv("TPO_VM_GLOBAL")
+        for a, b in zip(smem, glob):
+            assert np.array_equal(a, b, equal_nan=True), tag
+
+
+@pytest.mark.parametrize("name", ["rmsnorm", "lora"])
+def test_baseline_shape_eval_bit_exact(ctx, name):
+    """eval_mugraph of the BASELINE µGraph and eval_program of its flat
+    program at full size on the GPU (global-memory executor, fp64) are
+    bit-identical to the compiled reference (no exp in these graphs)."""
+    prog, mu = F.bench_pair(name)
+    rs = np.random.default_rng(9)
+    ins = []
+    for t in mu["inputs"]:
+        shp = mu["tensors"][t]["shape"]
+        x = rs.standard_normal(shp) / np.sqrt(shp[-1])
+        ins.append(np.abs(x) + 1e-3 if int(np.prod(shp)) == 1 else x)
+    got = ctx.eval_vm(mu, ins, mode=0)[0]
+    want = ref.eval_mugraph(mu, ins, mode=0)[0]
+    assert np.array_equal(got, want)
+    got_p = ctx.eval_vm(prog, ins, mode=1)[0]
+    want_p = ref.eval_mugraph(prog, ins, mode=1)[0]
+    assert np.array_equal(got_p, want_p)

@@ -205,6 +205,14 @@ int tpo_gpu_stability_batch(tpo_gpu_ctx *ctx, const tpo_gpu_graph *program,
                             int32_t trials, double tol, uint64_t seed, double input_scale,
                             int8_t *ok);
 
+/* Thread-graph construction (the reference's absent fusion.cpp):
+ * greedily fuses maximal single-consumer chains of elementwise block ops of
+ * every GraphDef into ThreadGroups (register-resident interior edges).
+ * Writes the resulting graph JSON into json_out when cap suffices; *needed
+ * receives the byte count including the terminator. */
+int tpo_gpu_construct_thread_graphs(const char *json_in, char *json_out, int64_t cap,
+                                    int64_t *needed);
+
 /* Reference op_madds work of a graph (SURVEY §8d verifier work unit). */
 int64_t tpo_gpu_op_madds(const tpo_gpu_graph *g);
 

@@ -215,3 +215,8 @@ def roundtrip_json(g) -> dict:
     buf = C.create_string_buffer(n)
     lib().ref_roundtrip_json(_js(g), buf, n)
     return json.loads(buf.value.decode())
+
+
+def block_shared_bytes(g, op_index: int, elem_size: int = 2) -> int:
+    """validate.cpp:115-140 for the GraphDef at kernel op `op_index`."""
+    return lib().ref_block_shared_bytes(_js(g), op_index, elem_size)

@@ -69,6 +69,7 @@ def lib():
     L.tpo_gpu_eval_mugraph.argtypes = [vp, vp, vp, vp, vp, vp]
     L.tpo_gpu_eval_mugraph_host.argtypes = [vp, vp, vp, vp, vp, vp]
     L.tpo_gpu_eval_vm.argtypes = [vp, vp, i32, vp, vp]
+    L.tpo_gpu_construct_thread_graphs.argtypes = [C.c_char_p, C.c_char_p, i64, C.POINTER(i64)]
     L.tpo_gpu_float_stability_filter.argtypes = [vp, vp, vp, i32, C.c_double, u64, C.c_double, vp]
     L.tpo_gpu_stability_batch.argtypes = [vp, vp, vp, vp, u64, i32, C.c_double, u64, C.c_double, vp]
     L.tpo_gpu_ff_eval.argtypes = [vp, vp, C.POINTER(FieldParams), u64, u64, i32] + [vp] * 6

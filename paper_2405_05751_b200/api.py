@@ -46,6 +46,17 @@ def validate(g, smem_bytes: int = 232448, elem_size: int = 2):
     return rc, buf.value.decode()
 
 
+def construct_thread_graphs(g) -> dict:
+    """SPEC construct_thread_graphs: the graph with every
+    GraphDef's maximal single-consumer elementwise chains grouped into
+    register-resident ThreadGroups (``tpo_gpu_construct_thread_graphs``)."""
+    need = C.c_int64(0)
+    N.check(N.lib().tpo_gpu_construct_thread_graphs(_js(g), None, 0, C.byref(need)))
+    buf = C.create_string_buffer(int(need.value))
+    N.check(N.lib().tpo_gpu_construct_thread_graphs(_js(g), buf, need.value, C.byref(need)))
+    return json.loads(buf.value.decode())
+
+
 class Graph:
     """A compiled µGraph handle (``tpo_gpu_compile``)."""
 

@@ -830,3 +830,25 @@ int tpo_gpu_float_stability_filter(tpo_gpu_ctx *ctx, const tpo_gpu_graph *g,
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Thread-graph construction over the JSON wire format.
+// ---------------------------------------------------------------------------
+#include "tpo/ir/fusion.hpp"
+
+extern "C" int tpo_gpu_construct_thread_graphs(const char *json_in, char *json_out, int64_t cap,
+                                               int64_t *needed) {
+  return guard([&] {
+    nlohmann::json j;
+    try {
+      j = nlohmann::json::parse(json_in);
+    } catch (const nlohmann::json::exception &e) {
+      throw Error(ErrCode::ParseError, e.what());
+    }
+    const ir::KernelGraph g = ir::construct_thread_graphs(ir::kernel_graph_from_json(j));
+    const std::string s = ir::to_json(g).dump();
+    if (needed) *needed = int64_t(s.size()) + 1;
+    if (json_out && cap > int64_t(s.size())) std::memcpy(json_out, s.c_str(), s.size() + 1);
+    return 0;
+  });
+}

@@ -108,6 +108,11 @@ FieldState &Ctx::field(uint32_t p, uint32_t q, uint32_t wbase) {
   f.lazy_sum = uint32_t(std::max<uint64_t>(1, (0xFFFFFFFFull - p) / pm1));
   f.thr_p = (0 - uint64_t(p)) % p;
   f.thr_q = (0 - uint64_t(q)) % q;
+  f.k24_p = uint32_t((1ull << 24) % p);
+  f.k48_p = uint32_t((1ull << 48) % p);
+  f.k24_q = uint32_t((1ull << 24) % q);
+  f.k48_q = uint32_t((1ull << 48) % q);
+  f.small = p < 256 && q < 256;
   uint32_t tb = 2 * (5 * 0 + p + q + p + q + q) + 2 * (p + q);
   f.table_bytes = (tb + 15) & ~15u;
   auto &t = fs->host_tables;

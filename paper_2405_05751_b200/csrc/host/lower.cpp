@@ -109,6 +109,141 @@ TpoVmInstr make(uint8_t op, uint8_t sub, View v, uint32_t dst, uint32_t a, uint3
   return in;
 }
 
+// Word intervals an instruction may touch, over every for-loop iteration
+// (hulls of its strided views; conservative).
+struct Span {
+  int64_t lo, hi;  // [lo, hi)
+};
+
+struct Access {
+  std::vector<Span> rd, wr;
+  bool opaque = false;  // treat as touching everything
+};
+
+// Hull of base + it*iter + sum_k c_k * st[k] over c_k < dims[k], it < trips.
+Span view_span(uint32_t base, int64_t iter, int64_t trips, const uint32_t *dims, const int32_t *st,
+               const int *ks, int nk) {
+  int64_t lo = int64_t(base), hi = int64_t(base);
+  const int64_t ti = (trips - 1) * iter;
+  (ti < 0 ? lo : hi) += ti;
+  for (int j = 0; j < nk; ++j) {
+    const int k = ks[j];
+    if (dims[k] == 0) return {0, 0};
+    const int64_t e = int64_t(dims[k] - 1) * st[k];
+    (e < 0 ? lo : hi) += e;
+  }
+  return {lo, hi + 1};
+}
+
+Access instr_access(const TpoVmInstr &I, int64_t trips) {
+  Access A;
+  static const int all[TPO_VM_DIMS] = {0, 1, 2, 3, 4, 5, 6};
+  const bool flat = I.flags & VM_FLAT;
+  const int64_t n = I.n;
+  switch (I.op) {
+    case VM_ZERO:
+      A.wr.push_back({I.dst, I.dst + n});
+      break;
+    case VM_UNARY:
+      A.rd.push_back({I.a, I.a + n});
+      A.wr.push_back({I.dst, I.dst + n});
+      break;
+    case VM_COPY:
+      if (flat) {
+        A.rd.push_back(view_span(I.a, I.a_iter, trips, nullptr, nullptr, nullptr, 0));
+        A.rd.back().hi += n - 1;
+        A.wr.push_back(view_span(I.dst, I.d_iter, trips, nullptr, nullptr, nullptr, 0));
+        A.wr.back().hi += n - 1;
+      } else {
+        A.rd.push_back(view_span(I.a, I.a_iter, trips, I.dims, I.sa, all, I.ndim));
+        A.wr.push_back(view_span(I.dst, I.d_iter, trips, I.dims, I.sd, all, I.ndim));
+      }
+      break;
+    case VM_BINARY:
+      if (flat) {
+        A.rd.push_back({I.a, I.a + n});
+        A.rd.push_back({I.b, I.b + n});
+        A.wr.push_back({I.dst, I.dst + n});
+      } else {
+        A.rd.push_back(view_span(I.a, 0, 1, I.dims, I.sa, all, I.ndim));
+        A.rd.push_back(view_span(I.b, 0, 1, I.dims, I.sb, all, I.ndim));
+        A.wr.push_back(view_span(I.dst, 0, 1, I.dims, I.sd, all, I.ndim));
+      }
+      break;
+    case VM_MATMUL: {
+      if (!(I.flags & VM_STRIDED)) {
+        A.opaque = true;
+        break;
+      }
+      static const int ka[6] = {0, 1, 2, 3, 4, 5}, kb[6] = {0, 1, 2, 3, 5, 6};
+      A.rd.push_back(view_span(I.a, I.a_iter, trips, I.dims, I.sa, ka, 6));
+      A.rd.push_back(view_span(I.b, I.b_iter, trips, I.dims, I.sb, kb, 6));
+      const int64_t out = int64_t(I.dims[0]) * I.dims[1] * I.dims[2] * I.dims[3] * I.dims[4] * I.dims[6];
+      A.wr.push_back({I.dst, I.dst + out});
+      if (I.flags & VM_ACCUM) A.rd.push_back(A.wr.back());
+      break;
+    }
+    case VM_SUM:
+      A.rd.push_back({I.a, I.a + int64_t(I.dims[0]) * I.dims[1] * I.dims[2] * I.dims[3]});
+      A.wr.push_back({I.dst, I.dst + n});
+      break;
+    default:
+      A.opaque = true;
+  }
+  return A;
+}
+
+bool overlaps(const std::vector<Span> &x, const std::vector<Span> &y) {
+  for (const Span &a : x)
+    for (const Span &b : y)
+      if (a.lo < b.hi && b.lo < a.hi) return true;
+  return false;
+}
+
+}  // namespace
+
+// Barrier placement (synchronisation only between
+// dependent levels).  Consecutive instructions form one phase while none
+// reads or writes a word another member of the phase writes; the CTA
+// interpreters skip the barrier after every instruction but a phase's
+// last (VM_NOSYNC).  Phases never span VM_LOOP / VM_ENDLOOP, and the last
+// instruction of a program always synchronises.  TPO_VM_NOSYNC=0 disables.
+void mark_phases(std::vector<TpoVmInstr> &code) {
+  static const bool off = [] {
+    const char *e = std::getenv("TPO_VM_NOSYNC");
+    return e && e[0] == '0';
+  }();
+  for (TpoVmInstr &I : code) I.flags &= uint8_t(~VM_NOSYNC);
+  if (off) return;
+  int64_t trips = 1;
+  std::vector<Access> phase;
+  int prev = -1;  // last compute instruction of the current phase
+  for (size_t k = 0; k < code.size(); ++k) {
+    TpoVmInstr &I = code[k];
+    if (I.op == VM_LOOP || I.op == VM_ENDLOOP) {
+      trips = I.op == VM_LOOP ? int64_t(I.n) : 1;
+      phase.clear();
+      prev = -1;
+      continue;
+    }
+    Access A = instr_access(I, trips);
+    bool join = prev >= 0 && !A.opaque;
+    for (const Access &P : phase) {
+      if (!join) break;
+      if (P.opaque || overlaps(P.wr, A.rd) || overlaps(P.wr, A.wr) || overlaps(P.rd, A.wr)) join = false;
+    }
+    if (join) {
+      code[size_t(prev)].flags |= VM_NOSYNC;
+    } else {
+      phase.clear();
+    }
+    phase.push_back(std::move(A));
+    prev = int(k);
+  }
+}
+
+namespace {
+
 class Lowerer {
  public:
   Lowerer(const KernelGraph &g, uint32_t in_base, uint32_t region, bool pin, bool field)
@@ -154,6 +289,7 @@ class Lowerer {
       p_.out_shapes.push_back(g_.tensor(t).shape);
     }
     plan_memory();
+    mark_phases(p_.code);
     p_.desc.words = p_.region_words;
     p_.desc.code_len = uint32_t(p_.code.size());
     p_.desc.poisoned = p_.poisoned;

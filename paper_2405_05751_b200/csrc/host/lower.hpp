@@ -39,6 +39,11 @@ VmProgram lower_vm(const ir::KernelGraph &g, uint32_t input_base, uint32_t regio
                    bool pin_outputs = false, bool field = false);
 
 int64_t graph_madds(const ir::KernelGraph &g);
+
+// Marks VM_NOSYNC on every instruction whose successor may run in the same
+// barrier phase (no read/write conflicts; physical addresses).  Run by
+// lower_vm after memory planning.
+void mark_phases(std::vector<TpoVmInstr> &code);
 int64_t input_elems(const ir::KernelGraph &g);
 
 }  // namespace tpo::gpu

@@ -31,10 +31,22 @@ __device__ __forceinline__ uint64_t fin(uint64_t z) {
   return z ^ (z >> 31);
 }
 
-// x mod m for x < 2^32, with magic = floor(2^32 / m) (one correction step).
+// x mod m for x < 2^32, with magic = floor(2^32 / m): the quotient
+// estimate is floor(x/m) or one less, so r < 2m and one correction step
+// remains, done as an unsigned min (r - m wraps when r < m).
 __device__ __forceinline__ uint32_t mod32(uint32_t x, uint32_t m, uint32_t magic) {
-  uint32_t r = x - __umulhi(x, magic) * m;
-  return r >= m ? r - m : r;
+  const uint32_t r = x - __umulhi(x, magic) * m;
+  return min(r, r - m);
+}
+
+// r mod n of a 64-bit draw (hi, lo) for n < 256: r = A*2^48 + B*2^24 + C
+// with A < 2^16, B, C < 2^24, and A*k48 + B*k24 + C < 2^32.
+__device__ __forceinline__ uint32_t mod64_small(uint32_t hi, uint32_t lo, uint32_t n, uint32_t magic,
+                                                uint32_t k24, uint32_t k48) {
+  const uint32_t c = lo & 0xffffffu;
+  const uint32_t b = __funnelshift_r(lo, hi, 24) & 0xffffffu;
+  const uint32_t a = hi >> 16;
+  return mod32(a * k48 + b * k24 + c, n, magic);
 }
 
 // r mod n for a 64-bit draw, via 32-bit halves: (hi*2^32 + lo) mod n.
@@ -99,13 +111,31 @@ __device__ uint32_t gen_attempt(const Smem &s, const FieldConst &f, uint64_t see
                                 uint32_t n_in, bool silu, int *s_slow, uint32_t *s_omega) {
   const uint64_t st0 = derive_state(seed, stream);
   bool slow = false;
-  for (uint32_t e = threadIdx.x; e < n_in; e += blockDim.x) {
-    uint64_t r1 = fin(st0 + (2ull * e + 1) * kGamma);
-    uint64_t r2 = fin(st0 + (2ull * e + 2) * kGamma);
-    slow |= (r1 < f.thr_p) | (r2 < f.thr_q);
-    uint32_t xp = mod64(r1, f.p, f.magic_p, f.two32_p);
-    uint32_t xq = mod64(r2, f.q, f.magic_q, f.two32_q);
-    s.w[e] = xp | (xq << 16);
+  if (f.small) {
+    // The rejection zone r < thr (thr < n) needs a zero high word: flag any
+    // draw with hi == 0 (p = 2^-32 each) and let the exact sequential replay
+    // below decide.  The draw state advances by a constant per thread.
+    const uint64_t step = 2ull * blockDim.x * kGamma;
+    uint64_t z = st0 + (2ull * threadIdx.x + 1) * kGamma;
+    uint32_t hmin = 0xffffffffu;
+    for (uint32_t e = threadIdx.x; e < n_in; e += blockDim.x, z += step) {
+      const uint64_t r1 = fin(z), r2 = fin(z + kGamma);
+      const uint32_t h1 = uint32_t(r1 >> 32), h2 = uint32_t(r2 >> 32);
+      hmin = min(hmin, min(h1, h2));
+      const uint32_t xp = mod64_small(h1, uint32_t(r1), f.p, f.magic_p, f.k24_p, f.k48_p);
+      const uint32_t xq = mod64_small(h2, uint32_t(r2), f.q, f.magic_q, f.k24_q, f.k48_q);
+      s.w[e] = xp | (xq << 16);
+    }
+    slow = hmin == 0;
+  } else {
+    for (uint32_t e = threadIdx.x; e < n_in; e += blockDim.x) {
+      uint64_t r1 = fin(st0 + (2ull * e + 1) * kGamma);
+      uint64_t r2 = fin(st0 + (2ull * e + 2) * kGamma);
+      slow |= (r1 < f.thr_p) | (r2 < f.thr_q);
+      uint32_t xp = mod64(r1, f.p, f.magic_p, f.two32_p);
+      uint32_t xq = mod64(r2, f.q, f.magic_q, f.two32_q);
+      s.w[e] = xp | (xq << 16);
+    }
   }
   const uint64_t base = 2ull * n_in;  // next draw index
   if (silu) {
@@ -442,7 +472,11 @@ __device__ bool run_program(const Smem &s, const FieldConst &f, const TpoVmInstr
       default:
         break;
     }
-    if (bad) *s_flag = (op == VM_UNARY) ? 2 : 1;  // NonResidue (sqrt) / DivByZero (div)
+    // NonResidue (sqrt) = 2 / DivByZero (div) = 1; within a barrier phase
+    // the earliest failing instruction wins (as in the reference's
+    // sequential evaluation, where it throws first)
+    if (bad) atomicMax(s_flag, int(((0xffffu - pc) << 2) | (op == VM_UNARY ? 2u : 1u)));
+    if (I.flags & VM_NOSYNC) continue;
     __syncthreads();
     if (PROF && threadIdx.x == 0) {
       const long long t = clock64();
@@ -629,7 +663,7 @@ __global__ void __launch_bounds__(kThreads) eval_kernel(EvalArgs a) {
     for (uint32_t e = threadIdx.x; e < a.n_in; e += blockDim.x) a.in_dump[e] = s.w[e];
   bool ok = run_program<false>(s, f, a.code + g.code_off, g.code_len, &s_flag, nullptr);
   if (threadIdx.x == 0) {
-    a.status[0] = ok ? 0 : s_flag;
+    a.status[0] = ok ? 0 : (s_flag & 3);
     a.status[1] = int(omega);
   }
   if (!ok) return;

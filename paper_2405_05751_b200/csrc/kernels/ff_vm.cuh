@@ -31,6 +31,10 @@ struct FieldConst {
   uint32_t lazy, lazy_sum;     // products / values summable before a reduction
   uint32_t table_bytes;        // smem bytes of the field tables (16-B aligned)
   uint64_t thr_p, thr_q;       // uniform() rejection thresholds (2^64 - n) mod n
+  // p, q < 256: a 64-bit draw r = A*2^48 + B*2^24 + C reduces as
+  // A*k48 + B*k24 + C < 2^32 (k24 = 2^24 mod n, k48 = 2^48 mod n), one mod32
+  uint32_t k24_p, k48_p, k24_q, k48_q;
+  uint32_t small;
 };
 
 struct VerifyArgs {

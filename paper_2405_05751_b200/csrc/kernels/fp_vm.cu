@@ -193,7 +193,7 @@ __device__ void run_program(T *W, const TpoVmInstr *code, uint32_t len) {
       continue;
     }
     exec_instr<T>(W, I, it, threadIdx.x, blockDim.x);
-    __syncthreads();
+    if (!(I.flags & VM_NOSYNC)) __syncthreads();  // barrier only between phases
   }
 }
 

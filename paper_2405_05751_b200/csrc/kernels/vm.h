@@ -43,6 +43,9 @@ enum TpoVmFlags {
   VM_STRIDED = 8, // MATMUL: strided operand views (see VM_MATMUL)
   VM_ACCUM = 16,  // MATMUL: dst = dst + A·B (a fused φ-Accum, acc = add(acc, val))
   VM_TILE22 = 32, // MATMUL: each index is a 2 x 2 output tile (rows 2i, 2i+1; cols 2j, 2j+1)
+  VM_NOSYNC = 64, // no CTA barrier after this instruction: the next one neither reads nor
+                  // writes any word this phase writes, nor writes a word it reads (lowering
+                  // mark_phases, the depth-schedule sync placement of SPEC.md:527-536)
 };
 
 struct TpoVmInstr {

@@ -296,8 +296,22 @@ bool tmap_3d(CUtensorMap *m, const void *ptr, uint64_t d0, uint64_t d1, uint64_t
 // TPO_DEBUG_TIMES: per-CTA %globaltimer phase stamps (16 slots per CTA)
 // written by the kernels, summarised on stderr (µs since the first CTA
 // started).  Debug only: the launch is followed by a synchronising copy.
+// TPO_DEBUG_RING=1 instead gives every launch its own slot of a ring of
+// kRing launches (no copy, no sync: usable inside CUDA graphs and
+// back-to-back streams); read it with tpo_debug_ring_read.
+constexpr int kRing = 16, kRingCtas = 4096;
+unsigned long long *g_ring = nullptr;
+unsigned g_ring_seq = 0;
+
 unsigned long long *debug_begin(int nct, cudaStream_t st) {
   static unsigned long long *dbg = nullptr;
+  if (std::getenv("TPO_DEBUG_RING")) {
+    if (!g_ring) {
+      cudaMalloc(&g_ring, size_t(kRing) * kRingCtas * 16 * 8);
+      cudaMemset(g_ring, 0, size_t(kRing) * kRingCtas * 16 * 8);
+    }
+    return g_ring + size_t(g_ring_seq++ % kRing) * kRingCtas * 16;
+  }
   if (!std::getenv("TPO_DEBUG_TIMES")) return nullptr;
   if (!dbg) cudaMalloc(&dbg, 16 * 8 * 4096);
   cudaMemsetAsync(dbg, 0, size_t(nct) * 128, st);
@@ -305,6 +319,7 @@ unsigned long long *debug_begin(int nct, cudaStream_t st) {
 }
 
 void debug_end(const char *tag, unsigned long long *dbg, int nct, cudaStream_t st) {
+  if (std::getenv("TPO_DEBUG_RING")) return;
   std::vector<unsigned long long> h(size_t(nct) * 16);
   cudaMemcpyAsync(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost, st);
   cudaStreamSynchronize(st);
@@ -426,14 +441,19 @@ int launch_fused(const FusedPlan &p, const void *const *in, const int32_t *dt, f
   // Weights (W / W1,W3 / A) declared static may stream before the PDL wait.
   const uint64_t weights = p.kind == TPO_FUSED_GATED_MLP ? 0x6 : p.kind == TPO_FUSED_LORA ? 0x6 : 0x4;
   sp.prefetch_static = (p.static_inputs & weights) == weights && !std::getenv("TPO_NO_PREFETCH");
-  // Pipeline depth: the measured-best single-CTA-per-SM depth that fits
-  // (profiles/r01: sweeps).  Two-CTA-per-SM configurations (TPO_MINB=2, let
-  // the next evaluation's CTAs become resident early) measured slower.
+  // Pipeline depth: the measured-best depth that fits (profiles/r01:
+  // sweeps, steady-state ring timelines).  Two CTAs per SM (TPO_MINB=2) pay
+  // off for RMS only; GatedMLP / LoRA run one CTA per SM with deeper rings.
   int stages = env_int("TPO_STAGES", 0), minb = env_int("TPO_MINB", 0);
   const size_t kOnePerSm = 232448;
+  // RMS with static weights: two CTAs per SM (5-stage ring, <= 113 KB) so
+  // the next evaluation's CTAs become resident and prefetch their weight
+  // stages while this one drains (ring timeline, profiles/r01/ring_rms.txt:
+  // 8.07 vs 8.63 us per evaluation).
+  if (stages <= 0 && minb <= 0 && mode == MODE_RMS && sp.prefetch_static) minb = 2;
   if (stages <= 0) {
     if (minb == 2) {
-      for (int s : {4, 3}) {
+      for (int s : {5, 4, 3}) {
         const size_t b = tpo_skinny_smem(mode, s, 2, &sp);
         if (b && b <= 115712) {
           stages = s;
@@ -443,7 +463,7 @@ int launch_fused(const FusedPlan &p, const void *const *in, const int32_t *dt, f
     }
     if (stages <= 0) {
       minb = 1;
-      const int pref_g[] = {4, 6, 3}, pref_r[] = {6, 8, 4, 10}, pref_l[] = {6, 8, 4, 10};
+      const int pref_g[] = {4, 6, 3}, pref_r[] = {6, 8, 4, 10}, pref_l[] = {8, 6, 4, 10};
       const int *pref = mode == MODE_GATED ? pref_g : mode == MODE_RMS ? pref_r : pref_l;
       const int np = mode == MODE_GATED ? 3 : 4;
       for (int i = 0; i < np; ++i) {
@@ -459,6 +479,8 @@ int launch_fused(const FusedPlan &p, const void *const *in, const int32_t *dt, f
   }
   sp.dbg_flags = env_int("TPO_DBG_FLAGS", 0);
   sp.epi_atomic = env_int("TPO_EPI_ATOMIC", 0);
+  sp.l2_prefetch = env_int("TPO_L2PF", 0);
+  sp.trig_kb = env_int("TPO_TRIG_KB", 0);
   const int nct = int(p.n / 128) * sp.ksplit;
   unsigned long long *dbg = debug_begin(nct, st);
   sp.dbg = dbg;
@@ -473,3 +495,14 @@ int launch_fused(const FusedPlan &p, const void *const *in, const int32_t *dt, f
 }
 
 }  // namespace tpo::gpu
+
+// Debug: copy the launch-timestamp ring (kRing launches x kRingCtas CTAs x
+// 16 slots) to `host` and reset it; returns the launch count so far.
+extern "C" int tpo_debug_ring_read(unsigned long long *host, size_t n) {
+  if (!tpo::gpu::g_ring) return -1;
+  const size_t tot = size_t(tpo::gpu::kRing) * tpo::gpu::kRingCtas * 16;
+  cudaDeviceSynchronize();
+  cudaMemcpy(host, tpo::gpu::g_ring, std::min(n, tot) * 8, cudaMemcpyDeviceToHost);
+  cudaMemset(tpo::gpu::g_ring, 0, tot * 8);
+  return int(tpo::gpu::g_ring_seq);
+}

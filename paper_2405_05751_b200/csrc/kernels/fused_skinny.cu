@@ -52,8 +52,10 @@ constexpr int kThreads = 192;
 constexpr int kMaxSplit = 4;
 
 // Pipeline stage layout (one k block of 64):
-//   [A box (LoRA)] [W boxes: NA x 2 x 8 KB] [B operand tile 2 KB] [RMS: raw X 1 KB, G 128 B]
+//   [W boxes: NA x 2 x 8 KB] [B operand tile 2 KB] [RMS: raw X 1 KB, G 128 B | LoRA: A box 2 KB]
 // GATED / LoRA: the B operand tile (X^T, K-major, 128-B swizzle) is a TMA box.
+// LoRA: the stage also carries the A box [64 k][16 r]; the epilogue warps
+// fold it into this CTA's XA partial (warp MMA) and release the stage.
 // RMS: TMA brings raw X and G; the four epilogue warps build the B tile
 // (x·g as bf16 hi + lo rows) in place while the stage's W boxes land, and
 // release it to the MMA issuer per stage (b_full).
@@ -61,19 +63,20 @@ template <int MODE>
 struct Cfg {
   static constexpr int NA = MODE == MODE_GATED ? 2 : 1;  // weight matrices
   static constexpr bool kTmaX = MODE != MODE_RMS;        // per-stage B tile via TMA
-  // LoRA: in addition, the CTA's whole X^T slice and A slice are staged once,
-  // ahead of the W stream, so XA (and XA·B̄) finish long before the last MMA
-  static constexpr bool kSlices = MODE == MODE_LORA;
   static constexpr uint32_t kAOff = 0;                   // W boxes lead the stage
   static constexpr uint32_t kBOff = kAOff + NA * 2 * kWBox;
   static constexpr uint32_t kXRawOff = kBOff + kXTile;     // RMS raw X
   static constexpr uint32_t kGOff = kXRawOff + 1024;       // RMS G
   static constexpr uint32_t kABox = 2048;                  // LoRA A box [64 k][16 r]
+  static constexpr uint32_t kLAOff = kBOff + kXTile;       // LoRA A box in the stage
   static constexpr uint32_t kStage = MODE == MODE_RMS    ? kGOff + 1024
+                                     : MODE == MODE_LORA ? kLAOff + kABox
                                                          : kBOff + kXTile;
   static constexpr uint32_t kFullBytes = MODE == MODE_RMS ? NA * 2 * kWBox : kStage;
   static constexpr uint32_t kXGBytes = 1024 + 128;  // RMS: X box [8][64] + G box [64]
-  static constexpr int kSide = MODE == MODE_LORA ? 256 : MODE == MODE_RMS ? 8 : 0;
+  static constexpr int kSide = MODE == MODE_RMS ? 8 : 0;  // RMS: Σx² per token, exchanged
+  // stage releases: the UMMA commit, plus (LoRA) the four epilogue warps
+  static constexpr uint32_t kEmptyCount = MODE == MODE_LORA ? 5 : 1;
 };
 
 constexpr int kMaxStages = 12;
@@ -117,11 +120,9 @@ __global__ void __launch_bounds__(kThreads, MINB)
   const int nkb = p.k_per_cta / kBK;
   constexpr int rows_per = kTileN / S;                                     // rows owned per CTA
   uint8_t *stages = smem;
-  uint8_t *xsl = stages + STAGES * C::kStage;               // LoRA: X^T slice, nkb B tiles
-  uint8_t *asl = xsl + (C::kSlices ? nkb * kXTile : 0);      // LoRA: A slice, nkb A boxes
-  float *red = reinterpret_cast<float *>(asl + (C::kSlices ? nkb * C::kABox : 0));
+  float *red = reinterpret_cast<float *>(stages + STAGES * C::kStage);
   float *side = red + (S > 1 ? kTileN * 16 : 0);  // red: [S][rows_per][16] incoming row partials
-  float *xa_tot = side + S * kSide;         // side: [S][kSide]; xa_tot: LoRA [16][16]
+  float *xa_tot = side + S * kSide;         // side: [S][kSide]; xa_tot: LoRA [16][16] (this CTA)
   float *xa_w = xa_tot + (MODE == MODE_LORA ? 256 : 0);  // LoRA: per-warp XA partials [4][16][16]
   Bars *bars = reinterpret_cast<Bars *>(xa_w + (MODE == MODE_LORA ? 1024 : 0));
 
@@ -137,7 +138,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&bars->full[s], 1);
-      mbar_init(&bars->empty[s], 1);
+      mbar_init(&bars->empty[s], C::kEmptyCount);
       mbar_init(&bars->xg_full[s], 1);
       mbar_init(&bars->b_full[s], 4);
     }
@@ -171,6 +172,20 @@ __global__ void __launch_bounds__(kThreads, MINB)
   // then waits; X is read only after the wait.
   const int npre = p.prefetch_static ? (nkb < STAGES ? nkb : STAGES) : 0;
   if (warp == 0 && elect_one()) {
+    // beyond the ring: the rest of this CTA's static weight slice goes to
+    // L2 now, so after the wait the stream is served at L2 latency while HBM
+    // already works for the next evaluation
+    if (p.prefetch_static && p.l2_prefetch) {
+      for (int kb = npre; kb < nkb; ++kb) {
+        const int k0 = kbase + kb * kBK;
+        tma_prefetch_l2_2d(&tmW0, n0, k0);
+        tma_prefetch_l2_2d(&tmW0, n0 + 64, k0);
+        if (C::NA > 1) {
+          tma_prefetch_l2_2d(&tmW1, n0, k0);
+          tma_prefetch_l2_2d(&tmW1, n0 + 64, k0);
+        }
+      }
+    }
     for (int kb = 0; kb < npre; ++kb) {
       uint8_t *st = stages + kb * C::kStage;
       mbar_expect_tx(&bars->full[kb], C::kFullBytes);
@@ -182,6 +197,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         tma_load_2d(wt + 2 * kWBox, &tmW1, &bars->full[kb], n0, k0);
         tma_load_2d(wt + 3 * kWBox, &tmW1, &bars->full[kb], n0 + 64, k0);
       }
+      if (MODE == MODE_LORA) tma_load_2d(st + C::kLAOff, &tmA, &bars->full[kb], 0, k0);  // A: static
     }
   }
   pdl_wait();  // inputs may be produced by the preceding kernel
@@ -190,7 +206,10 @@ __global__ void __launch_bounds__(kThreads, MINB)
   // so the next evaluation's CTAs become resident (two-per-SM configs) and
   // prefetch their static weights while this grid drains.  Experiment flag
   // 8: trigger at once.
-  const bool early_trigger = p.dbg_flags & 8;
+  // TPO_TRIG_KB (p.trig_kb > 0): warps 1-5 trigger at once, the producer
+  // after issuing k block trig_kb (the CTA counts as triggered when all of
+  // its threads have).
+  const bool early_trigger = (p.dbg_flags & 8) || (p.trig_kb > 0 && warp != 0);
   if (early_trigger) pdl_launch();
   // Atomic epilogue (RMS / LoRA, split clusters): every CTA adds its scaled
   // partial into the output with fp32 reductions instead of routing it to
@@ -205,17 +224,6 @@ __global__ void __launch_bounds__(kThreads, MINB)
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer
     if (elect_one()) {
-      // LoRA: X^T and A slices, issued right behind the first pipeline
-      // stages (ahead of them they delay the first W stage by ~1 µs)
-      auto issue_slices = [&] {
-        mbar_expect_tx(&bars->xa_full, uint32_t(nkb) * (kXTile + C::kABox));
-        for (int kb = 0; kb < nkb; ++kb) {
-          tma_load_2d(xsl + kb * kXTile, &tmX, &bars->xa_full, kbase + kb * kBK, 0);
-          tma_load_2d(asl + kb * C::kABox, &tmA, &bars->xa_full, 0, kbase + kb * kBK);
-        }
-      };
-      const int slice_at = (nkb < STAGES ? nkb : STAGES) - 1;  // after this k block's stage
-      if (C::kSlices && npre > slice_at) issue_slices();
       // X (and RMS: G) boxes of the prefetched stages
       for (int kb = 0; kb < npre; ++kb) {
         uint8_t *st = stages + kb * C::kStage;
@@ -248,12 +256,14 @@ __global__ void __launch_bounds__(kThreads, MINB)
           nx += 2 * kWBox;
         }
         if (C::kTmaX) tma_load_2d(nx, &tmX, &bars->full[s], k0, 0);
-        if (C::kSlices && kb == slice_at) issue_slices();
+        if (MODE == MODE_LORA) tma_load_2d(st + C::kLAOff, &tmA, &bars->full[s], 0, k0);
+        if (p.trig_kb > 0 && kb == p.trig_kb) pdl_launch();
       }
       TPO_T(10);
     }
     __syncwarp();
-    if (!early_trigger) pdl_launch();
+    if (!early_trigger && p.trig_kb <= 0) pdl_launch();
+    if (p.trig_kb >= nkb) pdl_launch();
   } else if (warp == 1) {
     // -------------------------------------------------------- MMA issuer
     constexpr uint32_t idesc = idesc_bf16(kTileN, kTok, /*a MN-major*/ true, /*b K-major*/ false);
@@ -298,14 +308,13 @@ __global__ void __launch_bounds__(kThreads, MINB)
     // ------------------------------------- auxiliary / epilogue warps 2..5
     const int t = threadIdx.x - 64;
     float sumsq = 0.f;       // RMS: Σx² of token t/16 over this CTA's K range
-    float xa0 = 0.f, xa1 = 0.f;  // LoRA: XA[t/8][2(t%8)], XA[t/8][2(t%8)+1] partials
     // Epilogue operands from global memory are loaded now, off the critical
     // path (under a saturated HBM a dependent load costs ~1 µs): LoRA B̄
     // column of the row this thread finalizes, RMS D.
     const int erow = (warp & 3) * 32 + lane;
     float bcol[MODE == MODE_LORA ? 16 : 1];
     float dsc = 0.f;
-    if (MODE == MODE_LORA && (p.epi_atomic || erow / rows_per == int(rank))) {
+    if (MODE == MODE_LORA) {  // every CTA folds its own XA partial times B̄ into its rows
 #pragma unroll
       for (int r = 0; r < 16; ++r) bcol[r] = __bfloat162float(p.lora_b[size_t(r) * p.N + n0 + erow]);
     }
@@ -349,13 +358,13 @@ __global__ void __launch_bounds__(kThreads, MINB)
       for (int o = 8; o; o >>= 1) sumsq += __shfl_xor_sync(0xffffffffu, sumsq, o);
     }
     if (MODE == MODE_LORA) {
-      // XA = X·A (16 tokens x 16 ranks over this CTA's K range) on the warp
-      // MMA path of the otherwise idle epilogue warps, from the X^T slice
-      // (K-major, 128-B swizzle B tiles) and the A slice ([64 k][16 r]
-      // boxes) staged ahead of the W stream: warp q takes k16 step q of
-      // every k block, two m16n8k16 bf16 MMAs with fp32 accumulation (exact
-      // products).  Done within ~1 µs of the slices landing, so the XA
-      // exchange and XA·B̄ are off the critical path.
+      // XA_s = X·A over this CTA's K range (16 tokens x 16 ranks) on the
+      // warp MMA path of the otherwise idle epilogue warps, stage by stage
+      // from the ring's X^T tile (K-major, 128-B swizzle) and A box
+      // ([64 k][16 r]): warp q takes k16 step q of every k block, two
+      // m16n8k16 bf16 MMAs with fp32 accumulation (exact products), then
+      // releases the stage.  XA·B̄ is linear, so each CTA later adds
+      // XA_s·B̄ to its own partial rows: no XA exchange.
       const int q = warp & 3;
       float c[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
       const int mi = lane >> 3, ri = lane & 7;
@@ -363,16 +372,19 @@ __global__ void __launch_bounds__(kThreads, MINB)
       const int kch = 2 * q + (mi >> 1);
       const uint32_t a_off = (tok >> 3) * 1024 + (tok & 7) * 128 + ((kch ^ (tok & 7)) << 4);
       const uint32_t b_off = (16 * q + ri + 8 * (mi & 1)) * 32 + (mi >> 1) * 16;
-      mbar_wait(&bars->xa_full, 0);
-      const uint32_t xs0 = smem_u32(xsl), as0 = smem_u32(asl);
       for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % STAGES;
+        mbar_wait(&bars->full[s], (kb / STAGES) & 1);
+        const uint32_t st = smem_u32(stages + s * C::kStage);
         uint32_t af[4], bf[4];
         asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                      : "=r"(af[0]), "=r"(af[1]), "=r"(af[2]), "=r"(af[3])
-                     : "r"(xs0 + kb * kXTile + a_off));
+                     : "r"(st + C::kBOff + a_off));
         asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
                      : "=r"(bf[0]), "=r"(bf[1]), "=r"(bf[2]), "=r"(bf[3])
-                     : "r"(as0 + kb * C::kABox + b_off));
+                     : "r"(st + C::kLAOff + b_off));
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars->empty[s]);
 #pragma unroll
         for (int j = 0; j < 2; ++j)
           asm volatile(
@@ -390,10 +402,11 @@ __global__ void __launch_bounds__(kThreads, MINB)
         *reinterpret_cast<float2 *>(xw + (g + 8) * 16 + 8 * j + cc) = make_float2(c[j][2], c[j][3]);
       }
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      // thread t: XA[t/8][2(t%8)..+1] = Σ over the 4 warps
+      // thread t: XA_s[t/8][2(t%8)..+1] = Σ over the 4 warps
       const int i0 = (t >> 3) * 16 + (t & 7) * 2;
-      xa0 = (xa_w[i0] + xa_w[256 + i0]) + (xa_w[512 + i0] + xa_w[768 + i0]);
-      xa1 = (xa_w[i0 + 1] + xa_w[256 + i0 + 1]) + (xa_w[512 + i0 + 1] + xa_w[768 + i0 + 1]);
+      const float xa0 = (xa_w[i0] + xa_w[256 + i0]) + (xa_w[512 + i0] + xa_w[768 + i0]);
+      const float xa1 = (xa_w[i0 + 1] + xa_w[256 + i0 + 1]) + (xa_w[512 + i0 + 1] + xa_w[768 + i0 + 1]);
+      *reinterpret_cast<float2 *>(xa_tot + i0) = make_float2(xa0, xa1);
     }
 
     if (!early_trigger) pdl_launch();
@@ -415,13 +428,11 @@ __global__ void __launch_bounds__(kThreads, MINB)
     if (MODE == MODE_RMS) {
       if ((t & 15) == 0) side[rank * kSide + (t >> 4)] = sumsq;
     }
-    if (MODE == MODE_LORA) *reinterpret_cast<float2 *>(side + rank * kSide + (t >> 3) * 16 + (t & 7) * 2) =
-        make_float2(xa0, xa1);
-    if (MODE != MODE_GATED) asm volatile("bar.sync 1, 128;" ::: "memory");  // own side block written
+    if (MODE != MODE_GATED) asm volatile("bar.sync 1, 128;" ::: "memory");  // own side block / XA_s written
     const bool xchg = !(p.dbg_flags & 2);  // experiment 2: no DSMEM exchange
     if (S > 1) {
       cluster_wait();  // every peer has initialised its barriers
-      if (xchg && MODE != MODE_GATED && !(atomic_epi && MODE == MODE_LORA) && t * 4 < kSide) {
+      if (xchg && kSide > 0 && t * 4 < kSide) {
         const float *src = side + rank * kSide + t * 4;
         for (int o = 1; o < S; ++o) {
           const uint32_t dst_rank = (rank + o) % S;
@@ -429,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
                     map_rank(&bars->recv_side, dst_rank));
         }
       }
-      if (xchg && MODE != MODE_GATED && !(atomic_epi && MODE == MODE_LORA)) mbar_wait(&bars->recv_side, 0);
+      if (xchg && kSide > 0) mbar_wait(&bars->recv_side, 0);
       if (atomic_epi) cluster_arrive();  // phase 2: rank 0's zeroed tile precedes every add
     }
     if (MODE == MODE_RMS && (mine || atomic_epi)) {
@@ -441,39 +452,27 @@ __global__ void __launch_bounds__(kThreads, MINB)
       }
     }
     if (MODE == MODE_LORA) {
-      // XA total (Σ over the cluster's K ranges), 2 entries per thread
-      for (int i = t * 2; i < t * 2 + 2; ++i) {
-        float v = 0.f;
-        for (int rr = 0; rr < S; ++rr) v += side[rr * kSide + i];
-        xa_tot[i] = v;
-      }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (mine || atomic_epi) {
-        // atomic: this CTA's own XA partial (linear: Σ_s XA_s·B̄ = XA·B̄)
-        const float *xsrc = atomic_epi ? side + rank * kSide : xa_tot;
+      // (XA_s·B̄)[t, n] for this thread's row n, every token t
 #pragma unroll
-        for (int tk = 0; tk < 16; ++tk) post[tk] = 0.f;
+      for (int tk = 0; tk < 16; ++tk) {
+        const float4 *xr = reinterpret_cast<const float4 *>(xa_tot + tk * 16);
+        float o = 0.f;
 #pragma unroll
-        for (int tk = 0; tk < 16; ++tk) {
-          const float4 *xr = reinterpret_cast<const float4 *>(xsrc + tk * 16);
-          float o = 0.f;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const float4 x = xr[i];
-            o = fmaf(x.x, bcol[4 * i], o);
-            o = fmaf(x.y, bcol[4 * i + 1], o);
-            o = fmaf(x.z, bcol[4 * i + 2], o);
-            o = fmaf(x.w, bcol[4 * i + 3], o);
-          }
-          post[tk] = o;
+        for (int i = 0; i < 4; ++i) {
+          const float4 x = xr[i];
+          o = fmaf(x.x, bcol[4 * i], o);
+          o = fmaf(x.y, bcol[4 * i + 1], o);
+          o = fmaf(x.z, bcol[4 * i + 2], o);
+          o = fmaf(x.w, bcol[4 * i + 3], o);
         }
+        post[tk] = o;
       }
     }
 
     // ---- critical path: last MMA -> TMEM -> DSMEM -> owner -> HBM
     // pin the post-loop operands here: without this the compiler may sink
     // their computation past the waits below, onto the critical path
-    if (MODE != MODE_GATED && (mine || atomic_epi)) {
+    if ((MODE == MODE_RMS && (mine || atomic_epi)) || MODE == MODE_LORA) {
 #pragma unroll
       for (int tk = 0; tk < T; ++tk) asm volatile("" : "+f"(post[tk]));
     }
@@ -495,7 +494,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         for (int i = 0; i < 8; ++i) acc[i] = v[i] + v[8 + i], acc[8 + i] = 0.f;
       } else {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) acc[i] = v[i];
+        for (int i = 0; i < 16; ++i) acc[i] = v[i] + post[i];  // partial XW_s + XA_s·B̄
       }
     }
     if (atomic_epi) {
@@ -504,7 +503,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
 #pragma unroll
         for (int tk = 0; tk < T; ++tk)
           if (tk < p.tokens)
-            atomicAdd(p.out + size_t(tk) * p.N + n, MODE == MODE_RMS ? acc[tk] * post[tk] : acc[tk] + post[tk]);
+            atomicAdd(p.out + size_t(tk) * p.N + n, MODE == MODE_RMS ? acc[tk] * post[tk] : acc[tk]);
       }
     } else if (S > 1 && xchg) {
       if (!mine) {
@@ -538,7 +537,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         float o;
         if (MODE == MODE_GATED) o = silu(acc[tk]) * acc[8 + tk];
         else if (MODE == MODE_RMS) o = acc[tk] * post[tk];
-        else o = acc[tk] + post[tk];
+        else o = acc[tk];
         if (tk < p.tokens) p.out[size_t(tk) * p.N + n] = o;
       }
       if (lane == 0 && (S == 1 || q == int(rank) * (4 / S))) TPO_T(11);
@@ -569,8 +568,7 @@ size_t skinny_smem(const SkinnyParams &p) {
   (void)nkb;
   size_t b = size_t(STAGES) * C::kStage +
              (S > 1 ? size_t(kTileN) * 16 * 4 : 0) + size_t(S) * C::kSide * 4 +
-             (MODE == MODE_LORA ? (256 + 1024) * 4 : 0) +
-             (C::kSlices ? size_t(nkb) * (kXTile + C::kABox) : 0) + sizeof(Bars);
+             (MODE == MODE_LORA ? (256 + 1024) * 4 : 0) + sizeof(Bars);
   return b + 1024;
 }
 
@@ -609,9 +607,9 @@ using namespace tpo_fused;
 // (mode, stages, cluster split, CTAs per SM)
 #define TPO_SKINNY_CASES(X)                                                                     \
   X(MODE_GATED, 4, 1, 1) X(MODE_GATED, 6, 1, 1) X(MODE_GATED, 3, 1, 2) X(MODE_GATED, 3, 2, 1)     \
-  X(MODE_GATED, 6, 2, 1) X(MODE_RMS, 4, 4, 2) X(MODE_RMS, 6, 4, 1) X(MODE_RMS, 8, 4, 1)            \
+  X(MODE_GATED, 6, 2, 1) X(MODE_RMS, 4, 4, 2) X(MODE_RMS, 5, 4, 2) X(MODE_RMS, 3, 4, 2) X(MODE_RMS, 6, 4, 1) X(MODE_RMS, 8, 4, 1)            \
   X(MODE_RMS, 10, 4, 1) X(MODE_RMS, 4, 2, 1) X(MODE_RMS, 6, 2, 1) X(MODE_RMS, 8, 2, 1)             \
-  X(MODE_RMS, 6, 1, 1) X(MODE_LORA, 4, 4, 2) X(MODE_LORA, 6, 4, 1) X(MODE_LORA, 8, 4, 1)           \
+  X(MODE_RMS, 6, 1, 1) X(MODE_LORA, 4, 4, 2) X(MODE_LORA, 5, 4, 2) X(MODE_LORA, 6, 4, 1) X(MODE_LORA, 8, 4, 1)           \
   X(MODE_LORA, 10, 4, 1) X(MODE_LORA, 6, 2, 1) X(MODE_LORA, 8, 2, 1) X(MODE_LORA, 6, 1, 1)
 
 extern "C" int tpo_skinny_launch(int mode, int stages, int minb, const CUtensorMap *maps,

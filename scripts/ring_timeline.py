@@ -1,0 +1,109 @@
+#!/usr/bin/env python
+"""Steady-state per-launch phase timeline of the fused kernels (GPU box):
+K back-to-back evaluations replayed as one CUDA graph (as bench.py times
+them), every launch stamping its own slot of the debug ring
+(TPO_DEBUG_RING=1, csrc/host/fused.cpp).  Prints, per launch, each phase's
+min / max over CTAs in µs relative to the previous launch's first start.
+
+  TPO_DEBUG_RING=1 python scripts/ring_timeline.py rmsnorm [STATIC=1] [ENV=VAL ...]
+"""
+import ctypes
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+os.environ["TPO_DEBUG_RING"] = "1"
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2405_05751_b200 import _native  # noqa: E402
+from paper_2405_05751_b200 import fixtures as F  # noqa: E402
+from paper_2405_05751_b200.api import Context  # noqa: E402
+from test_fused_gpu import make_inputs  # noqa: E402
+
+WEIGHTS = {"gatedmlp": [1, 2], "rmsnorm": [1, 2, 3], "lora": [1, 2, 3], "gqa": []}
+NAMES = {0: "start", 1: "setup", 8: "first_full", 9: "b_ready", 10: "last_tma", 3: "last_mma",
+         5: "tmem_full", 4: "sent", 6: "recv_done", 11: "owner_done", 2: "epi_done", 7: "end"}
+RING, CTAS = 16, 4096
+
+
+def main():
+    name = sys.argv[1]
+    static = False
+    for kv in sys.argv[2:]:
+        k, v = kv.split("=")
+        if k == "STATIC":
+            static = v == "1"
+        else:
+            os.environ[k] = v
+    ctx = Context(0)
+    _, mu = F.bench_pair(name)
+    g = ctx.compile(mu)
+    if static:
+        g.set_static_inputs(WEIGHTS[name])
+    host = make_inputs(name, F.BENCH[name]["args"], seed=3)
+    in_b = sum(x.numel() * 2 for x in host)
+    copies = max(1, -(-3 * 126 * 2**20 // in_b))
+    sets = [[x.cuda() for x in host] for _ in range(copies)]
+    st = torch.cuda.Stream()
+    outs = None
+    with torch.cuda.stream(st):
+        outs = [ctx.eval_mugraph(g, sets[i % copies], stream=st.cuda_stream)[0] for i in range(copies)]
+    st.synchronize()
+    K = RING
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=st):
+        for i in range(K):
+            ctx.eval_mugraph(g, sets[i % copies], outputs=[outs[i % copies]],
+                             stream=torch.cuda.current_stream().cuda_stream)
+    lib = _native.lib()
+    lib.tpo_debug_ring_read.restype = ctypes.c_int
+    buf = np.zeros(RING * CTAS * 16, dtype=np.uint64)
+    for rep in range(3):
+        graph.replay()
+        torch.cuda.synchronize()
+        seq = lib.tpo_debug_ring_read(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(buf.size))
+    h = buf.reshape(RING, CTAS, 16).astype(np.int64)
+    # launch order inside the ring: seq counts every launch (capture included)
+    first = seq - K
+    order = [(first + i) % RING for i in range(K)]
+    starts = []
+    for slot in order:
+        s0 = h[slot, :, 0]
+        starts.append(s0[s0 > 0].min())
+    ends = []
+    print(f"{name} static={static} env={[a for a in sys.argv[2:]]}")
+    for i, slot in enumerate(order):
+        ref = starts[i - 1] if i else starts[0]
+        row = []
+        for k in (0, 1, 8, 10, 3, 5, 11, 7):
+            v = h[slot, :, k]
+            v = v[v > 0]
+            if len(v):
+                row.append(f"{NAMES[k]} {(v.min() - ref) / 1e3:6.2f}/{(v.max() - ref) / 1e3:6.2f}")
+        e = h[slot, :, 7]
+        ends.append(e[e > 0].max())
+        print(f"  launch {i:2d}: " + "  ".join(row))
+    # critical path per launch: previous launch's last CTA end -> this
+    # launch's first full stage -> its last MMA -> its last CTA end
+    ph = {k: [] for k in ("wait_to_first", "stream", "tail", "resident_before_prev_end")}
+    for i in range(3, K):
+        a, b = order[i - 1], order[i]
+        pe = h[a, :, 7][h[a, :, 7] > 0].max()
+        ff = h[b, :, 8][h[b, :, 8] > 0]
+        lm = h[b, :, 3][h[b, :, 3] > 0].max()
+        en = h[b, :, 7][h[b, :, 7] > 0].max()
+        st0 = h[b, :, 0][h[b, :, 0] > 0]
+        ph["wait_to_first"].append((np.median(ff) - pe) / 1e3)
+        ph["stream"].append((lm - np.median(ff)) / 1e3)
+        ph["tail"].append((en - lm) / 1e3)
+        ph["resident_before_prev_end"].append((pe - np.median(st0)) / 1e3)
+    print("  " + "  ".join(f"{k} {np.mean(v):.2f}" for k, v in ph.items()))
+    per = np.diff(np.array(ends[2:], dtype=np.float64)) / 1e3
+    print(f"  period (end to end) mean {per.mean():.2f} us  min {per.min():.2f}  max {per.max():.2f}")
+
+
+if __name__ == "__main__":
+    main()

@@ -213,6 +213,26 @@ int tpo_gpu_stability_batch(tpo_gpu_ctx *ctx, const tpo_gpu_graph *program,
 int tpo_gpu_construct_thread_graphs(const char *json_in, char *json_out, int64_t cap,
                                     int64_t *needed);
 
+/* Post-verification block-graph planning (the reference's absent
+ * schedule.cpp / memplan.cpp, proj/core/CMakeLists.txt:19-20):
+ * for every GraphDef, the depth schedule (SPEC schedule_ops: ops ascending by
+ * longest-path depth per phase, sync points only between depth levels) and
+ * the shared-memory plan over its lifetimes (SPEC plan_memory: exhaustive
+ * for <= 8 tensors, first-fit-decreasing above).  Output JSON:
+ * {"graphdefs": [{"op", "order", "depth", "post", "sync_after", "syncs",
+ * "offset" (bytes per block tensor, -1 = register), "peak", "exhaustive"}]}.
+ * smem_bytes <= 0 selects the B200 limit (232448); elem_size <= 0 selects 2.
+ * Returns 1000 + DoesNotFit when a plan exceeds smem_bytes. */
+int tpo_gpu_plan_block_graphs(const char *json_in, int64_t smem_bytes, int32_t elem_size,
+                              char *json_out, int64_t cap, int64_t *needed);
+
+/* The planner on explicit lifetimes: n buffers of size[i] live over the
+ * inclusive positions [start[i], end[i]]; writes offset[i], *peak and
+ * *exhaustive (1 when every placement order was tried). */
+int tpo_gpu_plan_intervals(int32_t n, const int64_t *size, const int64_t *start, const int64_t *end,
+                           int32_t exhaustive_max, int64_t *offset, int64_t *peak,
+                           int32_t *exhaustive);
+
 /* Reference op_madds work of a graph (SURVEY §8d verifier work unit). */
 int64_t tpo_gpu_op_madds(const tpo_gpu_graph *g);
 

@@ -57,6 +57,32 @@ def construct_thread_graphs(g) -> dict:
     return json.loads(buf.value.decode())
 
 
+def plan_block_graphs(g, smem_bytes: int = 0, elem_size: int = 2) -> dict:
+    """SPEC schedule_ops + plan_memory for every GraphDef of
+    ``g`` (``tpo_gpu_plan_block_graphs``): depth order, sync points, shared-
+    memory offsets and peak.  Raises NativeError(DoesNotFit) past smem_bytes."""
+    need = C.c_int64(0)
+    N.check(N.lib().tpo_gpu_plan_block_graphs(_js(g), C.c_int64(smem_bytes), C.c_int32(elem_size),
+                                              None, 0, C.byref(need)))
+    buf = C.create_string_buffer(int(need.value))
+    N.check(N.lib().tpo_gpu_plan_block_graphs(_js(g), C.c_int64(smem_bytes), C.c_int32(elem_size),
+                                              buf, need.value, C.byref(need)))
+    return json.loads(buf.value.decode())
+
+
+def plan_intervals(sizes, starts, ends, exhaustive_max: int = 8):
+    """The memory planner on explicit inclusive lifetimes: (offsets, peak,
+    exhaustive) (``tpo_gpu_plan_intervals``)."""
+    n = len(sizes)
+    arr = C.c_int64 * max(n, 1)
+    off = arr()
+    peak = C.c_int64(0)
+    ex = C.c_int32(0)
+    N.check(N.lib().tpo_gpu_plan_intervals(C.c_int32(n), arr(*sizes), arr(*starts), arr(*ends),
+                                           C.c_int32(exhaustive_max), off, C.byref(peak), C.byref(ex)))
+    return [int(off[i]) for i in range(n)], int(peak.value), bool(ex.value)
+
+
 class Graph:
     """A compiled µGraph handle (``tpo_gpu_compile``)."""
 

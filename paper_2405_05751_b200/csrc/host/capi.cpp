@@ -178,7 +178,7 @@ Batch build_batch(const Graph &prog, const std::vector<const Graph *> &uniq) {
   bt.n_in = uint32_t(prog.in_elems);
   // program outputs pinned right after the inputs; program scratch above
   // them is dead once the candidate starts, so the candidate region reuses it
-  VmProgram pp = lower_vm(prog.g, 0, bt.n_in, /*pin_outputs=*/true, /*field=*/true);
+  VmProgram pp = lowered_ff(prog, bt.n_in, /*pin_outputs=*/true);
   const uint32_t cbase = bt.n_in + pp.pinned_words;
   if (pp.poisoned) pp.desc.err = uint8_t(1 + int(ErrCode::PoisonedExponent));
   add_graph(bt, pp);
@@ -186,7 +186,7 @@ Batch build_batch(const Graph &prog, const std::vector<const Graph *> &uniq) {
   for (const Graph *c : uniq) {
     try {
       check_pair(prog.g, c->g);
-      VmProgram cp = lower_vm(c->g, 0, cbase, false, /*field=*/true);
+      VmProgram cp = lowered_ff(*c, cbase, false);
       if (cp.poisoned) cp.desc.err = uint8_t(1 + int(ErrCode::PoisonedExponent));
       maxw = std::max(maxw, cbase + cp.region_words);
       add_graph(bt, cp);
@@ -309,6 +309,16 @@ void run_verify(Ctx &C, const Batch &bt, const tpo_verify_cfg &cfg, const tpo_fi
 }
 
 }  // namespace
+
+const VmProgram &lowered_ff(const Graph &G, uint32_t region, bool pin) {
+  std::lock_guard<std::mutex> lk(G.ff_mu);
+  const auto key = std::make_pair(region, int(pin));
+  auto it = G.ff_cache.find(key);
+  if (it == G.ff_cache.end())
+    it = G.ff_cache.emplace(key, std::make_shared<const VmProgram>(lower_vm(G.g, 0, region, pin, true))).first;
+  return *it->second;
+}
+
 }  // namespace tpo::gpu
 
 using namespace tpo;
@@ -854,6 +864,64 @@ extern "C" int tpo_gpu_construct_thread_graphs(const char *json_in, char *json_o
     const std::string s = ir::to_json(g).dump();
     if (needed) *needed = int64_t(s.size()) + 1;
     if (json_out && cap > int64_t(s.size())) std::memcpy(json_out, s.c_str(), s.size() + 1);
+    return 0;
+  });
+}
+
+// ------------------------------------------------- schedule / memory plan
+#include "tpo/ir/schedule.hpp"
+
+extern "C" int tpo_gpu_plan_block_graphs(const char *json_in, int64_t smem_bytes, int32_t elem_size,
+                                         char *json_out, int64_t cap, int64_t *needed) {
+  return guard([&] {
+    nlohmann::json j;
+    try {
+      j = nlohmann::json::parse(json_in);
+    } catch (const nlohmann::json::exception &e) {
+      throw Error(ErrCode::ParseError, e.what());
+    }
+    const ir::KernelGraph g = ir::kernel_graph_from_json(j);
+    ir::MemLimits lim;
+    lim.smem_bytes = smem_bytes > 0 ? smem_bytes : ir::kB200Limits.smem_bytes;
+    lim.elem_size = elem_size > 0 ? elem_size : 2;
+    nlohmann::json out = nlohmann::json::array();
+    for (size_t k = 0; k < g.ops.size(); ++k) {
+      const ir::Op &op = g.ops[k];
+      if (op.type != ir::OpType::GraphDef || !op.block) continue;
+      const ir::Schedule s = ir::schedule_ops(*op.block);
+      const ir::MemoryPlan m = ir::plan_memory(*op.block, s, lim);
+      out.push_back({{"op", int(k)},
+                     {"order", s.order},
+                     {"depth", s.depth},
+                     {"post", s.post},
+                     {"sync_after", s.sync_after},
+                     {"syncs", s.sync_after.size()},
+                     {"offset", m.offset},
+                     {"peak", m.peak},
+                     {"exhaustive", m.exhaustive}});
+    }
+    const std::string str = nlohmann::json{{"graphdefs", out}}.dump();
+    if (needed) *needed = int64_t(str.size()) + 1;
+    if (json_out && cap > int64_t(str.size())) std::memcpy(json_out, str.c_str(), str.size() + 1);
+    return 0;
+  });
+}
+
+extern "C" int tpo_gpu_plan_intervals(int32_t n, const int64_t *size, const int64_t *start,
+                                      const int64_t *end, int32_t exhaustive_max, int64_t *offset,
+                                      int64_t *peak, int32_t *exhaustive) {
+  return guard([&] {
+    if (n < 0 || (n && (!size || !start || !end || !offset)))
+      throw Error(ErrCode::ShapeMismatch, "plan_intervals: bad arguments");
+    std::vector<ir::Lifetime> b(static_cast<size_t>(n));
+    for (int32_t i = 0; i < n; ++i) {
+      if (size[i] < 0 || end[i] < start[i]) throw Error(ErrCode::ShapeMismatch, "plan_intervals: bad lifetime");
+      b[size_t(i)] = {size[i], start[i], end[i]};
+    }
+    const ir::MemoryPlan m = ir::plan_intervals(b, exhaustive_max);
+    for (int32_t i = 0; i < n; ++i) offset[i] = m.offset[size_t(i)];
+    if (peak) *peak = m.peak;
+    if (exhaustive) *exhaustive = m.exhaustive;
     return 0;
   });
 }

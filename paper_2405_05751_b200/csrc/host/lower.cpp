@@ -13,6 +13,7 @@
 // dimension (see kernels/vm.h); results are identical because blocks never
 // read each other's state and the last-writer rule is encoded in `wmask`.
 #include "lower.hpp"
+#include "tpo/ir/schedule.hpp"
 
 #include <algorithm>
 #include <cstdlib>
@@ -385,6 +386,21 @@ class Lowerer {
       addr[v] = at;
       live.push_back({at, vsize_[v], hi[v]});
       peak = std::max(peak, at + vsize_[v]);
+    }
+    // the SPEC planner (exhaustive over placement orders up to 8 buffers,
+    // first-fit-decreasing above) on the same lifetimes: keep the lower peak
+    static const bool ffd = [] {
+      const char *e = std::getenv("TPO_VM_FFD");
+      return !(e && e[0] == '0');
+    }();
+    if (ffd) {
+      std::vector<Lifetime> lt;
+      for (size_t v : order) lt.push_back({vsize_[v], lo[v], hi[v]});
+      const MemoryPlan mp = plan_intervals(lt, 0);  // first-fit-decreasing (host cost: lowering runs per batch)
+      if (base + mp.peak < peak) {
+        for (size_t i = 0; i < order.size(); ++i) addr[order[i]] = base + mp.offset[i];
+        peak = base + mp.peak;
+      }
     }
     for (size_t v = 0; v < nv; ++v) {
       if (addr[v] < 0) addr[v] = base;  // never referenced
@@ -841,6 +857,24 @@ class Lowerer {
       bqd[size_t(o)] = compute(b, ins, shapes, qds, invs, bbuf[size_t(o)], bshape(o), G);
     };
 
+    // Emission order: the depth schedule (SPEC schedule_ops, tpo/ir/schedule.hpp)
+    // groups independent ops of one level next to each other, so that
+    // mark_phases can drop the barriers between them.  Only data dependences
+    // order pure ops, so the results are those of the reference's list order;
+    // OutSavers keep their list order (OutSaver #k -> output k).
+    std::vector<const Op *> sched_ops;
+    {
+      static const bool keep = [] {
+        const char *e = std::getenv("TPO_VM_SCHED");
+        return e && e[0] == '0';
+      }();
+      if (keep) {
+        for (const Op &b : bg.ops) sched_ops.push_back(&b);
+      } else {
+        for (int k : schedule_ops(bg).order) sched_ops.push_back(&bg.ops[size_t(k)]);
+      }
+    }
+
     // ---- loop body (eval_core.hpp:303-341)
     {
       TpoVmInstr L;
@@ -849,7 +883,8 @@ class Lowerer {
       L.n = uint32_t(bg.forloop);
       emit(L);
     }
-    for (const Op &b : bg.ops) {
+    for (const Op *bp : sched_ops) {
+      const Op &b = *bp;
       if (b.type == OpType::InIter) {
         const auto &a = std::get<InIterAttrs>(b.attrs);
         if (a.operand < 0 || size_t(a.operand) >= op.inputs.size())
@@ -969,7 +1004,8 @@ class Lowerer {
 
     // ---- post-loop ops and OutSavers (eval_core.hpp:348-375)
     size_t saver = 0;
-    for (const Op &b : bg.ops) {
+    for (const Op *bp : sched_ops) {
+      const Op &b = *bp;
       if (b.type == OpType::OutSaver) {
         if (saver >= op.outputs.size()) throw Error(ErrCode::ShapeMismatch, "outsaver count");
         const auto &a = std::get<OutSaverAttrs>(b.attrs);

@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -53,7 +54,14 @@ struct Graph {
   int64_t in_elems = 0, out_elems = 0;
   int64_t vm_words = -1;
   FusedPlan plan;  // fused_kind == 0 when no hand-written kernel matches
+  // field-mode VM lowerings by (region base, pinned outputs): a handle is
+  // immutable, so batches over the same graphs reuse their bytecode
+  mutable std::mutex ff_mu;
+  mutable std::map<std::pair<uint32_t, int>, std::shared_ptr<const VmProgram>> ff_cache;
 };
+
+// lower_vm(G.g, 0, region, pin, /*field=*/true), memoised on the handle.
+const VmProgram &lowered_ff(const Graph &G, uint32_t region, bool pin);
 
 // Throws tpo::Error on failure.
 void check_cuda(cudaError_t e, const char *what);

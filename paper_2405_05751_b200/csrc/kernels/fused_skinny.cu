@@ -176,7 +176,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
     // L2 now, so after the wait the stream is served at L2 latency while HBM
     // already works for the next evaluation
     if (p.prefetch_static && p.l2_prefetch) {
-      for (int kb = npre; kb < nkb; ++kb) {
+      const int l2end = p.l2_prefetch >= nkb ? nkb : npre + p.l2_prefetch;
+      for (int kb = npre; kb < l2end && kb < nkb; ++kb) {
         const int k0 = kbase + kb * kBK;
         tma_prefetch_l2_2d(&tmW0, n0, k0);
         tma_prefetch_l2_2d(&tmW0, n0 + 64, k0);

@@ -268,8 +268,29 @@ void run_verify(Ctx &C, const Batch &bt, const tpo_verify_cfg &cfg, const tpo_fi
   if (!acc && r.accept_host) acc = static_cast<uint32_t *>(C.accept.get(words * 4));
   if (acc) check_cuda(cudaMemsetAsync(acc, 0, words * 4, st), "accept");
   a.accept = acc;
-  int occ = tpo_ff_verify_occupancy(smem);
+  // 128-thread candidate CTAs when twice as many of them fit an SM (small
+  // working sets, e.g. the RMSNorm pool: many short instructions, so more
+  // independent barrier domains per SM win: 8.6 vs 6.5 M cand/s measured);
+  // TPO_VM_THREADS overrides
+  int nthr = 256;
+  int occ = tpo_ff_verify_occupancy(smem, 256);
+  {
+    const char *e = std::getenv("TPO_VM_THREADS");
+    const int forced = e ? std::atoi(e) : 0;
+    const int occ128 = tpo_ff_verify_occupancy(smem, 128);
+    if (forced == 128 || (forced == 0 && occ128 >= 2 * occ)) nthr = 128, occ = occ128;
+  }
   if (occ < 1) throw Error(ErrCode::DoesNotFit, "verifier kernel does not fit on an SM");
+  if (std::getenv("TPO_VM_DEBUG")) {
+    double sn = 0, cnt = 0, mm = 0;
+    for (const TpoVmInstr &I : bt.code) {
+      if (I.op == VM_LOOP || I.op == VM_ENDLOOP) continue;
+      sn += I.n, cnt += 1;
+      if (I.op == VM_MATMUL) mm += double(I.n) * I.dims[5] * ((I.flags & VM_TILE22) ? 4 : 1);
+    }
+    std::fprintf(stderr, "[tpo vm] smem %zu occ256 %d occ128 %d instrs %.0f avg_n %.1f matmul_macs/instr %.1f\n", smem,
+                 tpo_ff_verify_occupancy(smem, 256), tpo_ff_verify_occupancy(smem, 128), cnt, sn / cnt, mm / cnt);
+  }
   uint64_t grid = std::min<uint64_t>(uint64_t(C.num_sms) * uint64_t(occ), r.n);
   grid = std::max<uint64_t>(grid, 1);
   // TPO_VM_PROFILE: per-opcode cycle breakdown of the verifier (thread 0 of
@@ -281,7 +302,7 @@ void run_verify(Ctx &C, const Batch &bt, const tpo_verify_cfg &cfg, const tpo_fi
     check_cuda(cudaMemsetAsync(prof, 0, 32 * 8, st), "prof");
     a.prof = prof;
   }
-  check_cuda(cudaError_t(tpo_ff_launch_verify(&a, int(grid), smem, st)), "verify launch");
+  check_cuda(cudaError_t(tpo_ff_launch_verify(&a, int(grid), smem, st, nthr)), "verify launch");
   if (profile) {
     unsigned long long h[32];
     check_cuda(cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, st), "prof");

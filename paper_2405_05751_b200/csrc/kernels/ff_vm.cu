@@ -522,8 +522,10 @@ __device__ bool first_mismatch(const Smem &s, const TpoVmGraph &g1, const TpoVmG
   return false;
 }
 
-template <bool PROF>
-__global__ void __launch_bounds__(kThreads) verify_kernel(VerifyArgs a) {
+// NT threads per candidate CTA: 256, or 128 when shared memory admits
+// twice as many resident candidates (more independent barrier domains).
+template <bool PROF, int NT>
+__global__ void __launch_bounds__(NT) verify_kernel(VerifyArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int s_flag, s_slow;
   __shared__ uint32_t s_omega;
@@ -677,15 +679,18 @@ __global__ void __launch_bounds__(kThreads) eval_kernel(EvalArgs a) {
 }  // namespace tpo_ff
 
 extern "C" int tpo_ff_launch_verify(const tpo_ff::VerifyArgs *a, int grid, size_t smem,
-                                    cudaStream_t st) {
-  static int configured_for[2] = {-1, -1};
+                                    cudaStream_t st, int nthreads) {
+  static int configured_for[4] = {-1, -1, -1, -1};
   const bool prof = a->prof != nullptr;
-  auto kern = prof ? tpo_ff::verify_kernel<true> : tpo_ff::verify_kernel<false>;
-  if (int(smem) > configured_for[prof]) {
+  const bool small = nthreads == 128;
+  auto kern = prof ? (small ? tpo_ff::verify_kernel<true, 128> : tpo_ff::verify_kernel<true, 256>)
+                   : (small ? tpo_ff::verify_kernel<false, 128> : tpo_ff::verify_kernel<false, 256>);
+  const int slot = int(prof) * 2 + int(small);
+  if (int(smem) > configured_for[slot]) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    configured_for[prof] = int(smem);
+    configured_for[slot] = int(smem);
   }
-  kern<<<grid, tpo_ff::kThreads, smem, st>>>(*a);
+  kern<<<grid, small ? 128 : 256, smem, st>>>(*a);
   return int(cudaGetLastError());
 }
 
@@ -695,11 +700,10 @@ extern "C" int tpo_ff_launch_eval(const tpo_ff::EvalArgs *a, size_t smem, cudaSt
   return int(cudaGetLastError());
 }
 
-extern "C" int tpo_ff_verify_occupancy(size_t smem) {
+extern "C" int tpo_ff_verify_occupancy(size_t smem, int nthreads) {
   int blocks = 0;
-  cudaFuncSetAttribute(tpo_ff::verify_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       int(smem));
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, tpo_ff::verify_kernel<false>,
-                                                tpo_ff::kThreads, smem);
+  auto kern = nthreads == 128 ? tpo_ff::verify_kernel<false, 128> : tpo_ff::verify_kernel<false, 256>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, nthreads == 128 ? 128 : 256, smem);
   return blocks;
 }

@@ -77,6 +77,6 @@ struct EvalArgs {
 }  // namespace tpo_ff
 
 extern "C" int tpo_ff_launch_verify(const tpo_ff::VerifyArgs *a, int grid, size_t smem,
-                                    cudaStream_t st);
+                                    cudaStream_t st, int nthreads);
 extern "C" int tpo_ff_launch_eval(const tpo_ff::EvalArgs *a, size_t smem, cudaStream_t st);
-extern "C" int tpo_ff_verify_occupancy(size_t smem);
+extern "C" int tpo_ff_verify_occupancy(size_t smem, int nthreads);

@@ -1,4 +1,5 @@
-# fused skinny kernels: sweeps + steady-state timelines (GPU box)
-python scripts/sweep.py rmsnorm "STATIC=1" "STATIC=1,TPO_L2PF=2" "STATIC=1,TPO_L2PF=4" "STATIC=1,TPO_L2PF=8" "STATIC=1,TPO_L2PF=16" > gpurun_out/sweep_rms.txt 2>&1
-python scripts/sweep.py lora "STATIC=1" "STATIC=1,TPO_L2PF=2" "STATIC=1,TPO_L2PF=4" "STATIC=1,TPO_L2PF=8" > gpurun_out/sweep_lora.txt 2>&1
-python scripts/sweep.py gatedmlp "STATIC=1" "STATIC=1,TPO_L2PF=4" > gpurun_out/sweep_g.txt 2>&1
+# GQA: steady-state timelines + sweep (GPU box)
+for cfg in "" "TPO_STAGES=2" "TPO_KSPLIT=4 TPO_STAGES=3" "TPO_KSPLIT=4 TPO_STAGES=2"; do
+python scripts/ring_timeline.py gqa $cfg | grep -v "launch  [0-9]:\|launch 1[0-2]"
+done > gpurun_out/ring_gqa.txt 2>&1
+python scripts/sweep.py gqa "" "TPO_STAGES=2" "TPO_KSPLIT=4" "TPO_KSPLIT=4,TPO_STAGES=2" "TPO_KSPLIT=1" "TPO_NO_PDL=1" > gpurun_out/sweep_gqa.txt 2>&1

@@ -93,7 +93,10 @@ def main():
         a, b = order[i - 1], order[i]
         pe = h[a, :, 7][h[a, :, 7] > 0].max()
         ff = h[b, :, 8][h[b, :, 8] > 0]
-        lm = h[b, :, 3][h[b, :, 3] > 0].max()
+        lmv = h[b, :, 3][h[b, :, 3] > 0]
+        if not len(lmv):  # GQA stamps o_full (slot 5) instead of the last MMA
+            lmv = h[b, :, 5][h[b, :, 5] > 0]
+        lm = lmv.max()
         en = h[b, :, 7][h[b, :, 7] > 0].max()
         st0 = h[b, :, 0][h[b, :, 0] > 0]
         ph["wait_to_first"].append((np.median(ff) - pe) / 1e3)

@@ -1,5 +1,4 @@
-# verifier A/B (GPU box): per-family throughput under launch toggles
-timeout 900 python -m pytest tests/test_verify_gpu.py -x -q > gpurun_out/pt.txt 2>&1
-TPO_VM_THREADS=256 python scripts/verify_families.py > gpurun_out/fam_256.txt 2>&1
-TPO_VM_THREADS=128 python scripts/verify_families.py > gpurun_out/fam_128.txt 2>&1
-python scripts/verify_families.py > gpurun_out/fam.txt 2>&1
+for i in 1 2; do
+python scripts/verify_families.py > gpurun_out/fam_a$i.txt 2>&1
+TPO_VM_DBG=1 python scripts/verify_families.py > gpurun_out/fam_b$i.txt 2>&1
+done

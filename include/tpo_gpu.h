@@ -233,6 +233,16 @@ int tpo_gpu_plan_intervals(int32_t n, const int64_t *size, const int64_t *start,
                            int32_t exhaustive_max, int64_t *offset, int64_t *peak,
                            int32_t *exhaustive);
 
+/* `describe` (the reference's absent describe.cpp): a
+ * human-readable pseudo-kernel listing — per kernel op its grid, for-loop,
+ * InIter/Accum/OutSaver maps, the block ops in schedule order with sync
+ * markers and shared-memory offsets — followed by how the B200 backend runs
+ * the graph (the fused kernel it matches, else VM instructions, barrier
+ * phases and working set).  An empty graph yields an empty listing.
+ * smem_bytes <= 0 selects the B200 limit. */
+int tpo_gpu_describe(const char *json_in, int64_t smem_bytes, char *text_out, int64_t cap,
+                     int64_t *needed);
+
 /* Reference op_madds work of a graph (SURVEY §8d verifier work unit). */
 int64_t tpo_gpu_op_madds(const tpo_gpu_graph *g);
 

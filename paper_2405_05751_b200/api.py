@@ -70,6 +70,16 @@ def plan_block_graphs(g, smem_bytes: int = 0, elem_size: int = 2) -> dict:
     return json.loads(buf.value.decode())
 
 
+def describe(g, smem_bytes: int = 0) -> str:
+    """SPEC describe: pseudo-kernel listing of ``g`` plus
+    its B200 execution (``tpo_gpu_describe``)."""
+    need = C.c_int64(0)
+    N.check(N.lib().tpo_gpu_describe(_js(g), C.c_int64(smem_bytes), None, 0, C.byref(need)))
+    buf = C.create_string_buffer(int(need.value))
+    N.check(N.lib().tpo_gpu_describe(_js(g), C.c_int64(smem_bytes), buf, need.value, C.byref(need)))
+    return buf.value.decode()
+
+
 def plan_intervals(sizes, starts, ends, exhaustive_max: int = 8):
     """The memory planner on explicit inclusive lifetimes: (offsets, peak,
     exhaustive) (``tpo_gpu_plan_intervals``)."""

@@ -946,3 +946,26 @@ extern "C" int tpo_gpu_plan_intervals(int32_t n, const int64_t *size, const int6
     return 0;
   });
 }
+
+// ------------------------------------------------------------- describe
+namespace tpo::gpu {
+std::string describe(const ir::KernelGraph &g, const ir::MemLimits &lim);
+}
+
+extern "C" int tpo_gpu_describe(const char *json_in, int64_t smem_bytes, char *text_out, int64_t cap,
+                                int64_t *needed) {
+  return guard([&] {
+    nlohmann::json j;
+    try {
+      j = nlohmann::json::parse(json_in);
+    } catch (const nlohmann::json::exception &e) {
+      throw Error(ErrCode::ParseError, e.what());
+    }
+    ir::MemLimits lim;
+    lim.smem_bytes = smem_bytes > 0 ? smem_bytes : ir::kB200Limits.smem_bytes;
+    const std::string str = tpo::gpu::describe(ir::kernel_graph_from_json(j), lim);
+    if (needed) *needed = int64_t(str.size()) + 1;
+    if (text_out && cap > int64_t(str.size())) std::memcpy(text_out, str.c_str(), str.size() + 1);
+    return 0;
+  });
+}

@@ -56,11 +56,19 @@ class Dist:
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
+        # TPO_BENCH_SHARED_GPU=1 (logic check only, never a bench number):
+        # every rank on cuda:0 over gloo, so the N>1 paths run on a 1-GPU box
+        shared = os.environ.get("TPO_BENCH_SHARED_GPU") == "1"
+        if shared:
+            self.local = 0
         if self.world > 1:
             import torch.distributed as dist
             import torch
             torch.cuda.set_device(self.local)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            if shared:
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
             self.pg = dist
 
     def barrier(self):

@@ -3,7 +3,7 @@
 # the bench lines for every workload, the ncu launch lists and one
 # `ncu --set full` capture per fused kernel.  Everything lands in gpurun_out/.
 #   gpurun --timeout 3000 -- 'bash scripts/gpu_round.sh [stage ...]'
-# Stages: tests smoke bench launches full  (default: all)
+# Stages: tests smoke bench multirank launches full  (default: all but multirank)
 set -u
 OUT=gpurun_out
 mkdir -p "$OUT"
@@ -28,6 +28,14 @@ if has bench; then
   done
   timeout 900 python bench.py --workload verify > "$OUT/bench_verify.json" 2> "$OUT/bench_verify.err"
   timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > "$OUT/bench_reference.json" 2> "$OUT/bench_reference.err"
+fi
+if has multirank; then
+  # N=2 logic check on a 1-GPU box (both ranks on cuda:0 over gloo; not a bench number)
+  TPO_BENCH_SHARED_GPU=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
+    --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 20 --warmup 3 \
+    --verify-candidates 40000 > "$OUT/n2.json" 2> "$OUT/n2.err"
+  timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
+    --master-port 29513 bench.py --gpus 2 --impl reference --steps 1 --warmup 1 > "$OUT/n2r.json" 2> "$OUT/n2r.err"
 fi
 NCU=/usr/local/cuda/bin/ncu
 if has launches; then

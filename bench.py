@@ -406,6 +406,7 @@ def run_verify(dist, n_total, steps=1, warmup=3, pool_fams=("rmsnorm", "gatedmlp
            "path": "Context.verify_pool (C-ABI tpo_gpu_verify_pool) + accept bits to host, wall clock; "
                    "inputs are generated on the device by design (h2d = pool map; bytecode ~KB)"}
     n_done = per_fam * len(jobs)
+    stream = search_stream(ctx, dist, fams, pool_fams)
     # algorithmic work: field MACs = 2 fields x (op_madds(program)
     # + op_madds(candidate)) per attempt the reference consumes; per-candidate
     # attempts from an untimed verdict pass over this rank's shard
@@ -434,7 +435,45 @@ def run_verify(dist, n_total, steps=1, warmup=3, pool_fams=("rmsnorm", "gatedmlp
             "accepted": accepted, "attempts_rank0": int(attempts), "e2e": e2e, "steps": steps,
             "gpu_launches_per_step": len(jobs) * (1 if n else 0),
             "families": list(pool_fams), "seed_rule": "candidate i = pool[i % |pool|], seed i",
-            "timing": "CUDA events: verify kernels + accept-bit all-gather, max over ranks"}
+            "timing": "CUDA events: verify kernels + accept-bit all-gather, max over ranks",
+            "search_stream": stream}
+
+
+def search_stream(ctx, dist, fams, pool_fams, per_fam_total=25000):
+    """The search loop's view: every candidate a DISTINCT graph handed over
+    as JSON (the reference wire format), compiled on all host cores
+    (tpo_gpu_compile_many) and verified in one batch per family
+    (tpo_gpu_verify_batch, seed i).  Wall clock from JSON text to verdict
+    bits on the host, this rank's shard, max over ranks."""
+    import torch
+    from paper_2405_05751_b200 import shard
+    first, n = shard.even_range(per_fam_total, dist.world, dist.rank)
+    texts = []
+    for f in pool_fams:
+        prog, pool = fams[f]
+        texts.append((ctx.compile(prog), [json.dumps(pool[i % len(pool)][1]) for i in range(first, first + n)]))
+    for gp, js in texts:  # warm the paths (small batch)
+        ctx.verify_batch(gp, ctx.compile_many(js[:64])[0], np.arange(64, dtype=np.uint64), want_verdicts=False)
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    t_compile = 0.0
+    accepted = 0
+    for gp, js in texts:
+        c0 = time.perf_counter()
+        gs, st = ctx.compile_many(js)
+        t_compile += time.perf_counter() - c0
+        if any(st):
+            raise RuntimeError("search stream: a candidate failed to compile")
+        _, acc = ctx.verify_batch(gp, gs, np.arange(first, first + n, dtype=np.uint64), want_verdicts=False)
+        accepted += int(acc.sum())
+    wall = dist.max(time.perf_counter() - t0)
+    tot = per_fam_total * len(texts)
+    return {"value": round(tot / wall, 1), "unit": "candidates/s", "candidates": tot,
+            "distinct_graphs": tot, "accepted": int(dist.sum(accepted)),
+            "compile_share": round(dist.max(t_compile) / wall, 3), "host_threads": os.cpu_count(),
+            "path": "JSON text -> tpo_gpu_compile_many (all host cores) -> tpo_gpu_verify_batch -> "
+                    "accept bits on the host; wall clock"}
 
 
 def cpu_baseline_verify(n=4000):

@@ -107,6 +107,14 @@ void tpo_gpu_close(tpo_gpu_ctx *ctx);
  * lower.  The handle owns host IR + lowering plans; device bytecode is
  * uploaded per batch. */
 int tpo_gpu_compile(tpo_gpu_ctx *ctx, const char *graph_json, tpo_gpu_graph **out);
+
+/* tpo_gpu_compile of n graphs on `threads` host threads (<= 0: all cores) —
+ * the search loop's candidate stream (each candidate is a distinct graph, so
+ * host-side parsing and lowering, not the GPU, bound the batch).  out[i]
+ * receives the handle or NULL, status[i] the per-graph status (0 or
+ * 1000 + ErrCode); returns nonzero only for bad arguments. */
+int tpo_gpu_compile_many(tpo_gpu_ctx *ctx, const char *const *graph_json, int64_t n, int32_t threads,
+                         tpo_gpu_graph **out, int32_t *status);
 void tpo_gpu_graph_free(tpo_gpu_graph *g);
 int tpo_gpu_graph_info(const tpo_gpu_graph *g, tpo_graph_info *out);
 /* Declares graph inputs (bit i = input i) as static parameters: never

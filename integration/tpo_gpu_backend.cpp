@@ -1,7 +1,9 @@
 // Reference-side binding of the B200 backend — see tpo_gpu_backend.hpp.
 #include "tpo_gpu_backend.hpp"
 
+#include <algorithm>
 #include <string>
+#include <thread>
 
 #include "tpo/ir/serialize.hpp"
 
@@ -105,11 +107,31 @@ std::vector<verify::EquivVerdict> Backend::verify_batch(
     const verify::FieldParams &fp) {
   if (seeds.size() != cands.size()) throw Error(ErrCode::ShapeMismatch, "one seed per candidate");
   CompiledGraph prog(ctx_, program);
+  // the candidate stream: wire format on all host cores, then one parallel
+  // compile (tpo_gpu_compile_many); a candidate that does not compile
+  // rethrows its tpo::Error, as the CPU path would on that candidate
+  const size_t n = cands.size();
+  std::vector<std::string> js(n);
+  {
+    const size_t nt = std::max<size_t>(1, std::min<size_t>(std::thread::hardware_concurrency(), n / 64 + 1));
+    std::vector<std::thread> pool;
+    for (size_t t = 0; t < nt; ++t)
+      pool.emplace_back([&, t] {
+        for (size_t i = t; i < n; i += nt) js[i] = ir::to_json(*cands[i]).dump();
+      });
+    for (auto &th : pool) th.join();
+  }
+  std::vector<const char *> jp(n);
+  for (size_t i = 0; i < n; ++i) jp[i] = js[i].c_str();
+  std::vector<tpo_gpu_graph *> raw(n, nullptr);
+  std::vector<int32_t> st(n, 0);
+  check(tpo_gpu_compile_many(ctx_, jp.data(), int64_t(n), 0, raw.data(), st.data()));
   std::vector<std::unique_ptr<CompiledGraph>> owned;
   std::vector<const tpo_gpu_graph *> hs;
-  for (const ir::KernelGraph *c : cands) {
-    owned.push_back(std::make_unique<CompiledGraph>(ctx_, *c));
-    hs.push_back(owned.back()->handle());
+  for (size_t i = 0; i < n; ++i) owned.push_back(std::make_unique<CompiledGraph>(raw[i]));
+  for (size_t i = 0; i < n; ++i) {
+    check(st[i]);
+    hs.push_back(raw[i]);
   }
   const tpo_verify_cfg c{cfg.num_tests, cfg.max_resamples, cfg.seed, cfg.float_tolerance};
   const tpo_field_params f = field(fp);

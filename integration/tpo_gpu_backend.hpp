@@ -30,6 +30,8 @@ class CompiledGraph {
   ~CompiledGraph();
   CompiledGraph(const CompiledGraph &) = delete;
   CompiledGraph &operator=(const CompiledGraph &) = delete;
+  /// Adopts a handle from tpo_gpu_compile_many.
+  explicit CompiledGraph(tpo_gpu_graph *h) : h_(h) {}
   tpo_gpu_graph *handle() const { return h_; }
   int64_t op_madds() const;
   bool has_fused_kernel() const;

@@ -98,13 +98,36 @@ class Graph:
 
     def __init__(self, ctx: "Context", g):
         self.ctx = ctx
-        self.spec = json.loads(g) if isinstance(g, str) else g
+        self._spec = g
         h = C.c_void_p()
         N.check(N.lib().tpo_gpu_compile(ctx.h, _js(g), C.byref(h)))
         self.h = h
-        info = N.GraphInfo()
-        N.lib().tpo_gpu_graph_info(h, C.byref(info))
-        self.info = info
+        self._info = None
+
+    @property
+    def spec(self) -> dict:
+        """The graph as a dict (parsed on first use when built from JSON text)."""
+        if isinstance(self._spec, (str, bytes)):
+            self._spec = json.loads(self._spec)
+        return self._spec
+
+    @classmethod
+    def _wrap(cls, ctx: "Context", spec, h) -> "Graph":
+        self = cls.__new__(cls)
+        self.ctx = ctx
+        self._spec = spec
+        self.h = h
+        self._info = None
+        return self
+
+    @property
+    def info(self):
+        """tpo_graph_info, fetched on first use."""
+        if self._info is None:
+            info = N.GraphInfo()
+            N.lib().tpo_gpu_graph_info(self.h, C.byref(info))
+            self._info = info
+        return self._info
 
     def __del__(self):
         h = getattr(self, "h", None)
@@ -161,6 +184,23 @@ class Context:
 
     def compile(self, g) -> Graph:
         return g if isinstance(g, Graph) else Graph(self, g)
+
+    def compile_many(self, graphs: Sequence, threads: int = 0):
+        """Compile n graphs on all host cores (``tpo_gpu_compile_many``):
+        (list of Graph or None, list of per-graph status)."""
+        n = len(graphs)
+        js = [_js(g) for g in graphs]
+        arr = (C.c_char_p * max(n, 1))(*js)
+        hs = (C.c_void_p * max(n, 1))()
+        st = (C.c_int32 * max(n, 1))()
+        N.check(N.lib().tpo_gpu_compile_many(self.h, arr, C.c_int64(n), C.c_int32(threads), hs, st))
+        out = []
+        for i in range(n):
+            if st[i] == 0:
+                out.append(Graph._wrap(self, graphs[i], C.c_void_p(hs[i])))
+            else:
+                out.append(None)
+        return out, [int(st[i]) for i in range(n)]
 
     # ---- floating point -------------------------------------------------
     def eval_mugraph(self, g, inputs: Sequence, outputs=None, stream=None):

@@ -1,5 +1,8 @@
 // B200 backend — C-ABI (include/tpo_gpu.h) over the host runtime.
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -39,6 +42,28 @@ int guard(F &&f) {
   } catch (const std::exception &e) {
     return fail(1000 + int(ErrCode::Unsupported), e.what());
   }
+}
+
+int host_threads() {
+  const unsigned h = std::thread::hardware_concurrency();
+  return int(std::max(1u, std::min(h ? h : 1u, 64u)));
+}
+
+// fn(i) for i in [0, n) over `threads` host threads (atomic work counter)
+template <class Fn>
+void parallel_for(int64_t n, int threads, Fn &&fn) {
+  if (threads <= 1 || n < 2) {
+    for (int64_t i = 0; i < n; ++i) fn(i);
+    return;
+  }
+  std::atomic<int64_t> next{0};
+  auto work = [&] {
+    for (int64_t i; (i = next.fetch_add(1)) < n;) fn(i);
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < threads; ++t) pool.emplace_back(work);
+  work();
+  for (auto &t : pool) t.join();
 }
 
 bool is_prime(uint32_t n) {
@@ -175,6 +200,7 @@ TpoVmGraph error_graph(ErrCode c) {
 // unique handle in `index`.
 Batch build_batch(const Graph &prog, const std::vector<const Graph *> &uniq) {
   Batch bt;
+  bt.graphs.reserve(uniq.size() + 1);
   bt.n_in = uint32_t(prog.in_elems);
   // program outputs pinned right after the inputs; program scratch above
   // them is dead once the candidate starts, so the candidate region reuses it
@@ -183,17 +209,42 @@ Batch build_batch(const Graph &prog, const std::vector<const Graph *> &uniq) {
   if (pp.poisoned) pp.desc.err = uint8_t(1 + int(ErrCode::PoisonedExponent));
   add_graph(bt, pp);
   uint32_t maxw = bt.n_in + pp.region_words;
-  for (const Graph *c : uniq) {
+  // lower the distinct candidates on all host cores (memoised per handle),
+  // then lay the batch out by a prefix sum and copy the bytecode in parallel
+  const size_t nu = uniq.size();
+  const int th = nu >= 16 ? host_threads() : 1;
+  std::vector<const VmProgram *> low(nu, nullptr);
+  std::vector<ErrCode> err(nu, ErrCode::ShapeMismatch);
+  parallel_for(int64_t(nu), th, [&](int64_t i) {
     try {
-      check_pair(prog.g, c->g);
-      VmProgram cp = lowered_ff(*c, cbase, false);
-      if (cp.poisoned) cp.desc.err = uint8_t(1 + int(ErrCode::PoisonedExponent));
-      maxw = std::max(maxw, cbase + cp.region_words);
-      add_graph(bt, cp);
+      check_pair(prog.g, uniq[size_t(i)]->g);
+      low[size_t(i)] = &lowered_ff(*uniq[size_t(i)], cbase, false);
     } catch (const Error &e) {
-      bt.graphs.push_back(error_graph(e.code));
+      err[size_t(i)] = e.code;
     }
+  });
+  std::vector<size_t> at(nu);
+  size_t ncode = bt.code.size();
+  for (size_t i = 0; i < nu; ++i) {
+    const VmProgram *cp = low[i];
+    if (!cp) {
+      bt.graphs.push_back(error_graph(err[i]));
+      continue;
+    }
+    TpoVmGraph d = cp->desc;
+    d.code_off = uint32_t(ncode);
+    d.code_len = uint32_t(cp->code.size());
+    if (cp->poisoned) d.err = uint8_t(1 + int(ErrCode::PoisonedExponent));
+    bt.graphs.push_back(d);
+    at[i] = ncode;
+    ncode += cp->code.size();
+    maxw = std::max(maxw, cbase + cp->region_words);
   }
+  bt.code.resize(ncode);
+  parallel_for(int64_t(nu), th, [&](int64_t i) {
+    if (const VmProgram *cp = low[size_t(i)])
+      std::copy(cp->code.begin(), cp->code.end(), bt.code.begin() + ptrdiff_t(at[size_t(i)]));
+  });
   bt.max_words = maxw;
   uint32_t mc = 0;
   for (size_t i = 1; i < bt.graphs.size(); ++i) mc = std::max(mc, bt.graphs[i].code_len);
@@ -302,7 +353,28 @@ void run_verify(Ctx &C, const Batch &bt, const tpo_verify_cfg &cfg, const tpo_fi
     check_cuda(cudaMemsetAsync(prof, 0, 32 * 8, st), "prof");
     a.prof = prof;
   }
+  const bool dbg = std::getenv("TPO_VM_DEBUG") != nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::chrono::steady_clock::time_point tu;
+  if (dbg) {
+    cudaStreamSynchronize(st);
+    tu = std::chrono::steady_clock::now();
+    cudaEventCreate(&ev0);
+    cudaEventCreate(&ev1);
+    cudaEventRecord(ev0, st);
+  }
   check_cuda(cudaError_t(tpo_ff_launch_verify(&a, int(grid), smem, st, nthr)), "verify launch");
+  if (dbg) {
+    cudaEventRecord(ev1, st);
+    cudaEventSynchronize(ev1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev0, ev1);
+    std::fprintf(stderr, "[tpo run_verify] kernel %.3f ms (grid %llu x %d thr, smem %zu B), host after upload %.3f ms\n",
+                 ms, (unsigned long long)grid, nthr, smem,
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tu).count());
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+  }
   if (profile) {
     unsigned long long h[32];
     check_cuda(cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, st), "prof");
@@ -375,43 +447,61 @@ void tpo_gpu_close(tpo_gpu_ctx *ctx) {
   delete ctx;
 }
 
+}  // extern "C"
+
+namespace {
+
+// parse + validate (B200 limits) + fused match + VM footprint; throws
+tpo_gpu_graph *compile_one(const char *json) {
+  nlohmann::json j;
+  try {
+    j = nlohmann::json::parse(json);
+  } catch (const nlohmann::json::exception &e) {
+    throw Error(ErrCode::ParseError, e.what());
+  }
+  auto h = std::make_unique<tpo_gpu_graph>();
+  Graph &G = h->g;
+  G.g = ir::kernel_graph_from_json(j);
+  ir::ValidityReport rep = ir::validate(G.g, ir::kB200Limits);
+  if (!rep.valid()) {
+    std::string msg;
+    for (auto &v : rep.violations) msg += v.detail + "; ";
+    ErrCode c = rep.violations[0].kind == ir::ViolationKind::MemoryCapacity ? ErrCode::DoesNotFit
+                                                                           : ErrCode::ShapeMismatch;
+    throw Error(c, "invalid µGraph: " + msg);
+  }
+  G.lax = ir::mugraph_lax_check(G.g).lax;
+  G.madds = graph_madds(G.g);
+  G.in_elems = input_elems(G.g);
+  for (ir::TensorId t : G.g.outputs) G.out_elems += G.g.tensor(t).shape.elem_count();
+  G.plan = match_fused(G.g);
+  G.vm_words = -2;  // computed on first tpo_gpu_graph_info (an fp lowering)
+  return h.release();
+}
+
+}  // namespace
+
+extern "C" {
+
 int tpo_gpu_compile(tpo_gpu_ctx *, const char *json, tpo_gpu_graph **out) {
   return guard([&] {
-    nlohmann::json j;
-    try {
-      j = nlohmann::json::parse(json);
-    } catch (const nlohmann::json::exception &e) {
-      throw Error(ErrCode::ParseError, e.what());
-    }
-    auto *h = new tpo_gpu_graph();
-    try {
-      Graph &G = h->g;
-      G.g = ir::kernel_graph_from_json(j);
-      ir::ValidityReport rep = ir::validate(G.g, ir::kB200Limits);
-      if (!rep.valid()) {
-        std::string msg;
-        for (auto &v : rep.violations) msg += v.detail + "; ";
-        ErrCode c = rep.violations[0].kind == ir::ViolationKind::MemoryCapacity
-                        ? ErrCode::DoesNotFit
-                        : ErrCode::ShapeMismatch;
-        throw Error(c, "invalid µGraph: " + msg);
-      }
-      G.lax = ir::mugraph_lax_check(G.g).lax;
-      G.madds = graph_madds(G.g);
-      G.in_elems = input_elems(G.g);
-      for (ir::TensorId t : G.g.outputs) G.out_elems += G.g.tensor(t).shape.elem_count();
-      G.plan = match_fused(G.g);
-      try {
-        VmProgram vp = lower_vm(G.g, 0, uint32_t(G.in_elems));
-        G.vm_words = G.in_elems + vp.region_words;
-      } catch (const Error &) {
-        G.vm_words = -1;
-      }
-    } catch (...) {
-      delete h;
-      throw;
-    }
-    *out = h;
+    *out = compile_one(json);
+    return 0;
+  });
+}
+
+int tpo_gpu_compile_many(tpo_gpu_ctx *, const char *const *json, int64_t n, int32_t threads,
+                         tpo_gpu_graph **out, int32_t *status) {
+  return guard([&] {
+    if (n < 0 || (n && (!json || !out || !status))) throw Error(ErrCode::ShapeMismatch, "compile_many: bad arguments");
+    const int64_t nt = std::max<int64_t>(1, std::min<int64_t>(threads > 0 ? threads : host_threads(), n / 8 + 1));
+    parallel_for(n, int(nt), [&](int64_t i) {
+      out[i] = nullptr;
+      status[i] = guard([&] {
+        out[i] = compile_one(json[i]);
+        return 0;
+      });
+    });
     return 0;
   });
 }
@@ -427,6 +517,16 @@ int tpo_gpu_graph_info(const tpo_gpu_graph *h, tpo_graph_info *o) {
   o->madds = G.madds;
   o->input_elems = G.in_elems;
   o->output_elems = G.out_elems;
+  {
+    std::lock_guard<std::mutex> lk(G.ff_mu);
+    if (G.vm_words == -2) {
+      try {
+        G.vm_words = G.in_elems + lower_vm(G.g, 0, uint32_t(G.in_elems)).region_words;
+      } catch (const Error &) {
+        G.vm_words = -1;
+      }
+    }
+  }
   o->vm_words = G.vm_words;
   return 0;
 }
@@ -614,7 +714,9 @@ int tpo_gpu_verify_batch(tpo_gpu_ctx *ctx, const tpo_gpu_graph *program,
       }
       cg[k] = it->second;
     }
+    const auto t0 = std::chrono::steady_clock::now();
     Batch bt = build_batch(program->g, uniq);
+    const auto t1 = std::chrono::steady_clock::now();
     VerifyRun r;
     r.cand_graph = &cg;
     r.seeds = seeds;
@@ -622,6 +724,14 @@ int tpo_gpu_verify_batch(tpo_gpu_ctx *ctx, const tpo_gpu_graph *program,
     r.verdicts_host = verdicts;
     r.accept_host = accept_bits;
     run_verify(ctx->c, bt, *cfg, *fp, r);
+    if (std::getenv("TPO_VM_DEBUG")) {
+      const auto t2 = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "[tpo verify_batch] n %llu distinct %zu build %.2f ms, upload+run %.2f ms, code %.1f MB\n",
+                   (unsigned long long)n, uniq.size(),
+                   std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                   std::chrono::duration<double, std::milli>(t2 - t1).count(),
+                   double(bt.code.size() * sizeof(TpoVmInstr)) / 1e6);
+    }
     return 0;
   });
 }

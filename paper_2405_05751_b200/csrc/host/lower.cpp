@@ -116,8 +116,19 @@ struct Span {
   int64_t lo, hi;  // [lo, hi)
 };
 
+// at most 3 operand reads and 1 write per instruction: fixed storage, no
+// allocation (the lowering runs per candidate of a search stream)
+struct SpanList {
+  Span s[3];
+  int n = 0;
+  void push_back(Span x) { s[n++] = x; }
+  Span &back() { return s[n - 1]; }
+  const Span *begin() const { return s; }
+  const Span *end() const { return s + n; }
+};
+
 struct Access {
-  std::vector<Span> rd, wr;
+  SpanList rd, wr;
   bool opaque = false;  // treat as touching everything
 };
 
@@ -194,7 +205,7 @@ Access instr_access(const TpoVmInstr &I, int64_t trips) {
   return A;
 }
 
-bool overlaps(const std::vector<Span> &x, const std::vector<Span> &y) {
+bool overlaps(const SpanList &x, const SpanList &y) {
   for (const Span &a : x)
     for (const Span &b : y)
       if (a.lo < b.hi && b.lo < a.hi) return true;
@@ -393,7 +404,17 @@ class Lowerer {
       const char *e = std::getenv("TPO_VM_FFD");
       return !(e && e[0] == '0');
     }();
+    // skip it when first fit already meets the load bound (the largest
+    // total size live at one instruction: no placement can go below it)
+    int64_t load = 0;
     if (ffd) {
+      std::vector<std::pair<int64_t, int64_t>> ev;  // (position, +size at start / -size after end)
+      for (size_t v : order) ev.emplace_back(lo[v] * 2, vsize_[v]), ev.emplace_back(hi[v] * 2 + 1, -vsize_[v]);
+      std::sort(ev.begin(), ev.end());
+      int64_t cur = 0;
+      for (auto &e : ev) load = std::max(load, cur += e.second);
+    }
+    if (ffd && peak - base > load) {
       std::vector<Lifetime> lt;
       for (size_t v : order) lt.push_back({vsize_[v], lo[v], hi[v]});
       const MemoryPlan mp = plan_intervals(lt, 0);  // first-fit-decreasing (host cost: lowering runs per batch)

@@ -52,7 +52,7 @@ struct Graph {
   bool lax = true;
   int64_t madds = 0;
   int64_t in_elems = 0, out_elems = 0;
-  int64_t vm_words = -1;
+  mutable int64_t vm_words = -1;  // -2: not computed yet (tpo_gpu_graph_info)
   FusedPlan plan;  // fused_kind == 0 when no hand-written kernel matches
   // field-mode VM lowerings by (region base, pinned outputs): a handle is
   // immutable, so batches over the same graphs reuse their bytecode

@@ -60,3 +60,38 @@ def test_compile_errors_are_statuses():
     rc = N.lib().tpo_gpu_compile(None, b"{not json", C.byref(C.c_void_p()))
     assert rc == 1010
     assert "parse" in N.last_error().lower() or "syntax" in N.last_error().lower()
+
+
+def test_compile_many_matches_compile():
+    """tpo_gpu_compile_many (parallel host compile of a candidate stream):
+    per-graph handles and statuses equal one-at-a-time tpo_gpu_compile,
+    including parse and validation failures."""
+    graphs = []
+    for fam in F.VERIFY_SHAPES:
+        prog, pool = F.verify_families()[fam]
+        graphs += [json.dumps(g) for _, g in pool[::7]]
+    bad_shape = json.loads(graphs[0])
+    bad_shape["tensors"][0]["shape"] = [3, 5, 7, 11, 13]   # rank 5: rejected
+    graphs += ["{not json", json.dumps(bad_shape)]
+    n = len(graphs)
+    lib = N.lib()
+    arr = (C.c_char_p * n)(*[g.encode() for g in graphs])
+    hs = (C.c_void_p * n)()
+    st = (C.c_int32 * n)()
+    assert lib.tpo_gpu_compile_many(None, arr, C.c_int64(n), C.c_int32(4), hs, st) == 0
+    for i, g in enumerate(graphs):
+        h1 = C.c_void_p()
+        rc = lib.tpo_gpu_compile(None, g.encode(), C.byref(h1))
+        assert st[i] == rc, (i, st[i], rc)
+        if rc == 0:
+            a, b = N.GraphInfo(), N.GraphInfo()
+            lib.tpo_gpu_graph_info(C.c_void_p(hs[i]), C.byref(a))
+            lib.tpo_gpu_graph_info(h1, C.byref(b))
+            assert (a.madds, a.vm_words, a.fused_kind) == (b.madds, b.vm_words, b.fused_kind)
+            lib.tpo_gpu_graph_free(C.c_void_p(hs[i]))
+            lib.tpo_gpu_graph_free(h1)
+        else:
+            assert not hs[i]
+    from paper_2405_05751_b200.graph import ErrCode
+    assert st[n - 2] == 1000 + int(ErrCode.ParseError)
+    assert st[n - 1] != 0

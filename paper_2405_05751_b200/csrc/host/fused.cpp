@@ -479,8 +479,6 @@ int launch_fused(const FusedPlan &p, const void *const *in, const int32_t *dt, f
   }
   sp.dbg_flags = env_int("TPO_DBG_FLAGS", 0);
   sp.epi_atomic = env_int("TPO_EPI_ATOMIC", 0);
-  sp.l2_prefetch = env_int("TPO_L2PF", 0);
-  sp.trig_kb = env_int("TPO_TRIG_KB", 0);
   const int nct = int(p.n / 128) * sp.ksplit;
   unsigned long long *dbg = debug_begin(nct, st);
   sp.dbg = dbg;

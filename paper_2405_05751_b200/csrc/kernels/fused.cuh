@@ -22,9 +22,6 @@ struct SkinnyParams {
   int dbg_flags;             // experiments (TPO_DBG_FLAGS): 1 skip finalize
   int prefetch_static;       // weights are static: stream them before the PDL wait
   int epi_atomic;            // RMS/LoRA split clusters: fp32-reduction epilogue
-  int l2_prefetch;           // static weights: the whole W slice is prefetched into L2
-                             // before the PDL wait (smem ring holds only STAGES)
-  int trig_kb;               // experiment: producer triggers dependents after k block trig_kb
 };
 
 struct GqaParams {

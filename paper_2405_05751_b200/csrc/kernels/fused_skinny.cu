@@ -172,21 +172,6 @@ __global__ void __launch_bounds__(kThreads, MINB)
   // then waits; X is read only after the wait.
   const int npre = p.prefetch_static ? (nkb < STAGES ? nkb : STAGES) : 0;
   if (warp == 0 && elect_one()) {
-    // beyond the ring: the rest of this CTA's static weight slice goes to
-    // L2 now, so after the wait the stream is served at L2 latency while HBM
-    // already works for the next evaluation
-    if (p.prefetch_static && p.l2_prefetch) {
-      const int l2end = p.l2_prefetch >= nkb ? nkb : npre + p.l2_prefetch;
-      for (int kb = npre; kb < l2end && kb < nkb; ++kb) {
-        const int k0 = kbase + kb * kBK;
-        tma_prefetch_l2_2d(&tmW0, n0, k0);
-        tma_prefetch_l2_2d(&tmW0, n0 + 64, k0);
-        if (C::NA > 1) {
-          tma_prefetch_l2_2d(&tmW1, n0, k0);
-          tma_prefetch_l2_2d(&tmW1, n0 + 64, k0);
-        }
-      }
-    }
     for (int kb = 0; kb < npre; ++kb) {
       uint8_t *st = stages + kb * C::kStage;
       mbar_expect_tx(&bars->full[kb], C::kFullBytes);
@@ -207,10 +192,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
   // so the next evaluation's CTAs become resident (two-per-SM configs) and
   // prefetch their static weights while this grid drains.  Experiment flag
   // 8: trigger at once.
-  // TPO_TRIG_KB (p.trig_kb > 0): warps 1-5 trigger at once, the producer
-  // after issuing k block trig_kb (the CTA counts as triggered when all of
-  // its threads have).
-  const bool early_trigger = (p.dbg_flags & 8) || (p.trig_kb > 0 && warp != 0);
+  const bool early_trigger = p.dbg_flags & 8;
   if (early_trigger) pdl_launch();
   // Atomic epilogue (RMS / LoRA, split clusters): every CTA adds its scaled
   // partial into the output with fp32 reductions instead of routing it to
@@ -258,13 +240,11 @@ __global__ void __launch_bounds__(kThreads, MINB)
         }
         if (C::kTmaX) tma_load_2d(nx, &tmX, &bars->full[s], k0, 0);
         if (MODE == MODE_LORA) tma_load_2d(st + C::kLAOff, &tmA, &bars->full[s], 0, k0);
-        if (p.trig_kb > 0 && kb == p.trig_kb) pdl_launch();
       }
       TPO_T(10);
     }
     __syncwarp();
-    if (!early_trigger && p.trig_kb <= 0) pdl_launch();
-    if (p.trig_kb >= nkb) pdl_launch();
+    if (!early_trigger) pdl_launch();
   } else if (warp == 1) {
     // -------------------------------------------------------- MMA issuer
     constexpr uint32_t idesc = idesc_bf16(kTileN, kTok, /*a MN-major*/ true, /*b K-major*/ false);

@@ -180,3 +180,25 @@ def test_shape_mismatch_is_error_verdict(ctx):
     got, acc = ctx.verify_batch(prog, [other], [0])
     assert got["kind"][0] == 3 and got["err_code"][0] == 1000  # ShapeMismatch
     assert not acc[0]
+
+
+def test_distinct_candidate_stream_matches_reference(ctx):
+    """The search-loop path: every candidate a distinct handle compiled from
+    JSON text on all host cores (tpo_gpu_compile_many) and verified in one
+    batch (parallel lowering + bytecode assembly) — verdicts bit-exact."""
+    import json
+    rng = np.random.default_rng(7)
+    for fam in ("rmsnorm", "gqa"):
+        prog, pool = FAMS[fam]
+        idx = rng.integers(0, len(pool), 300)
+        texts = [json.dumps(pool[i][1]) for i in idx]
+        gs, st = ctx.compile_many(texts)
+        assert all(s == 0 for s in st)
+        assert len({g.h.value for g in gs}) == len(gs)  # no dedup: 300 distinct handles
+        seeds = rng.integers(0, 2**62, 300, dtype=np.uint64)
+        got, acc = ctx.verify_batch(prog, gs, seeds)
+        for k in range(0, 300, 3):
+            w = ref.random_test_equivalence(prog, pool[idx[k]][1], num_tests=1, seed=int(seeds[k]))
+            for c in VCOLS:
+                assert got[c][k] == w[c], (fam, k, c)
+        assert np.array_equal(acc, got["kind"] == 0)

@@ -96,10 +96,11 @@ KernelGraph lora_mugraph(int64_t b, int64_t h, int64_t n, int64_t r, int64_t gri
   return gb.finish({o});
 }
 
+// `key`: canonical_key(g), computed once by the caller
 template <class F>
-bool same(const KernelGraph &g, F &&build) {
+bool same(const std::string &key, F &&build) {
   try {
-    return canonical_key(g) == canonical_key(build());
+    return key == canonical_key(build());
   } catch (const Error &) {
     return false;
   }
@@ -138,13 +139,20 @@ FusedPlan match_fused(const KernelGraph &g) {
   }
   const BlockGraph &bg = *g.ops[0].block;
   const int64_t grid = bg.grid[0], fl = bg.forloop;
+  std::string key;
+  try {
+    key = canonical_key(g);
+  } catch (const Error &) {
+    p.why = "no canonical form";
+    return p;
+  }
   std::vector<TensorShape> in;
   for (TensorId t : g.inputs) in.push_back(g.tensor(t).shape);
   auto r2 = [&](size_t i) { return in[i].rank() == 2; };
   if (in.size() == 4 && r2(0) && r2(1) && r2(2) && r2(3) && in[1].dims[0] == 1 &&
       in[3].dims == std::vector<int64_t>{1, 1}) {
     int64_t b = in[0].dims[0], h = in[0].dims[1], n = in[2].dims[1];
-    if (same(g, [&] { return rmsnorm_mugraph(b, h, n, grid, fl); })) {
+    if (same(key, [&] { return rmsnorm_mugraph(b, h, n, grid, fl); })) {
       if (b > 8 || n % 128 || h % 64) {
         p.why = "RMSNorm µGraph outside kernel limits (b<=8, n%128, h%64)";
         return p;
@@ -156,7 +164,7 @@ FusedPlan match_fused(const KernelGraph &g) {
   }
   if (in.size() == 3 && r2(0) && r2(1) && r2(2)) {
     int64_t b = in[0].dims[0], h = in[0].dims[1], n = in[1].dims[1];
-    if (same(g, [&] { return gatedmlp_mugraph(b, h, n, grid, fl); })) {
+    if (same(key, [&] { return gatedmlp_mugraph(b, h, n, grid, fl); })) {
       if (b > 8 || n % 128 || h % 64) {
         p.why = "GatedMLP µGraph outside kernel limits (b<=8, n%128, h%64)";
         return p;
@@ -168,7 +176,7 @@ FusedPlan match_fused(const KernelGraph &g) {
   }
   if (in.size() == 3 && in[0].rank() == 3 && in[1].rank() == 3 && in[2].rank() == 3) {
     int64_t G = in[0].dims[0], qh = in[0].dims[1], hd = in[0].dims[2], L = in[1].dims[2];
-    if (same(g, [&] { return gqa_mugraph(G, qh, hd, L, grid, fl); })) {
+    if (same(key, [&] { return gqa_mugraph(G, qh, hd, L, grid, fl); })) {
       if (qh > 8 || hd != 128 || L % 128) {
         p.why = "GQA µGraph outside kernel limits (qh<=8, hd==128, L%128)";
         return p;
@@ -180,7 +188,7 @@ FusedPlan match_fused(const KernelGraph &g) {
   }
   if (in.size() == 4 && r2(0) && r2(1) && r2(2) && r2(3)) {
     int64_t b = in[0].dims[0], h = in[0].dims[1], n = in[1].dims[1], r = in[2].dims[1];
-    if (same(g, [&] { return lora_mugraph(b, h, n, r, grid, fl); })) {
+    if (same(key, [&] { return lora_mugraph(b, h, n, r, grid, fl); })) {
       if (b > 16 || r != 16 || n % 128 || h % 64) {
         p.why = "LoRA µGraph outside kernel limits (b<=16, r==16, n%128, h%64)";
         return p;

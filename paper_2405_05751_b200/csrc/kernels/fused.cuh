@@ -22,6 +22,8 @@ struct SkinnyParams {
   int dbg_flags;             // experiments (TPO_DBG_FLAGS): 1 skip finalize
   int prefetch_static;       // weights are static: stream them before the PDL wait
   int epi_atomic;            // RMS/LoRA split clusters: fp32-reduction epilogue
+  int trig_early;            // experiment: producer triggers dependents this many k blocks early
+  int pre_cut;               // experiment: prefetch this many fewer static stages
 };
 
 struct GqaParams {

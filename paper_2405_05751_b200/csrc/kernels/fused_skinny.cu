@@ -170,7 +170,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
   // stream) may stream before the programmatic dependency resolves: the
   // producer issues the W (and LoRA A) boxes of the first pipeline stages,
   // then waits; X is read only after the wait.
-  const int npre = p.prefetch_static ? (nkb < STAGES ? nkb : STAGES) : 0;
+  const int npre_max = (nkb < STAGES ? nkb : STAGES) - p.pre_cut;
+  const int npre = p.prefetch_static ? (npre_max > 0 ? npre_max : 0) : 0;
   if (warp == 0 && elect_one()) {
     for (int kb = 0; kb < npre; ++kb) {
       uint8_t *st = stages + kb * C::kStage;
@@ -240,6 +241,9 @@ __global__ void __launch_bounds__(kThreads, MINB)
         }
         if (C::kTmaX) tma_load_2d(nx, &tmX, &bars->full[s], k0, 0);
         if (MODE == MODE_LORA) tma_load_2d(st + C::kLAOff, &tmA, &bars->full[s], 0, k0);
+        // experiment (TPO_TRIG_EARLY = D): release the dependent grid D
+        // k blocks before the last issue (one thread triggers the CTA)
+        if (p.trig_early > 0 && kb == nkb - 1 - p.trig_early) pdl_launch();
       }
       TPO_T(10);
     }

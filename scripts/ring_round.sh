@@ -1,5 +1,3 @@
-# GQA: steady-state timelines + sweep (GPU box)
-for cfg in "" "TPO_STAGES=2" "TPO_KSPLIT=4 TPO_STAGES=3" "TPO_KSPLIT=4 TPO_STAGES=2"; do
-python scripts/ring_timeline.py gqa $cfg | grep -v "launch  [0-9]:\|launch 1[0-2]"
-done > gpurun_out/ring_gqa.txt 2>&1
-python scripts/sweep.py gqa "" "TPO_STAGES=2" "TPO_KSPLIT=4" "TPO_KSPLIT=4,TPO_STAGES=2" "TPO_KSPLIT=1" "TPO_NO_PDL=1" > gpurun_out/sweep_gqa.txt 2>&1
+timeout 600 python -m pytest tests/test_fused_gpu.py -x -q > gpurun_out/pt_fused.txt 2>&1
+python scripts/sweep.py rmsnorm "STATIC=1" "STATIC=1,TPO_TRIG_EARLY=4" "STATIC=1,TPO_TRIG_EARLY=6" "STATIC=1" > gpurun_out/sweep_rms.txt 2>&1
+python bench.py --workload rmsnorm --no-verifier > gpurun_out/bench_rmsnorm.json 2> gpurun_out/bench_rmsnorm.err

@@ -407,6 +407,7 @@ def run_verify(dist, n_total, steps=1, warmup=3, pool_fams=("rmsnorm", "gatedmlp
                    "inputs are generated on the device by design (h2d = pool map; bytecode ~KB)"}
     n_done = per_fam * len(jobs)
     stream = search_stream(ctx, dist, fams, pool_fams)
+    stab = stability_stage(ctx, dist, fams, pool_fams)
     # algorithmic work: field MACs = 2 fields x (op_madds(program)
     # + op_madds(candidate)) per attempt the reference consumes; per-candidate
     # attempts from an untimed verdict pass over this rank's shard
@@ -436,7 +437,52 @@ def run_verify(dist, n_total, steps=1, warmup=3, pool_fams=("rmsnorm", "gatedmlp
             "gpu_launches_per_step": len(jobs) * (1 if n else 0),
             "families": list(pool_fams), "seed_rule": "candidate i = pool[i % |pool|], seed i",
             "timing": "CUDA events: verify kernels + accept-bit all-gather, max over ranks",
-            "search_stream": stream}
+            "search_stream": stream, "stability_filter": stab}
+
+
+def stability_stage(ctx, dist, fams, pool_fams, per_fam_total=25000):
+    """The pipeline's next stage: float_stability_filter
+    (stability.cpp:25-50: eval_mugraph of program and candidate on N(0,1)
+    inputs, fp64, relative tolerance 1e-3) for a batch of candidates in one
+    launch per family (tpo_gpu_stability_batch, seed i), CUDA events, max
+    over ranks; the compiled reference timed beside it on a sample."""
+    import torch
+    from paper_2405_05751_b200 import shard
+    first, n = shard.even_range(per_fam_total, dist.world, dist.rank)
+    jobs = []
+    for f in pool_fams:
+        prog, pool = fams[f]
+        jobs.append((ctx.compile(prog), [ctx.compile(g) for _, g in pool], pool, prog))
+    for gp, gs, _, _ in jobs:
+        ctx.stability_batch(gp, [gs[i % len(gs)] for i in range(64)], seeds=np.arange(64, dtype=np.uint64))
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    passed = 0
+    e0.record()
+    for gp, gs, _, _ in jobs:
+        cands = [gs[i % len(gs)] for i in range(first, first + n)]
+        ok = ctx.stability_batch(gp, cands, seeds=np.arange(first, first + n, dtype=np.uint64))
+        passed += int((ok == 1).sum())
+    e1.record()
+    torch.cuda.synchronize()
+    t = dist.max(e0.elapsed_time(e1) / 1e3)
+    tot = per_fam_total * len(jobs)
+    out = {"value": round(tot / t, 1), "unit": "candidates/s", "candidates": tot,
+           "passed": int(dist.sum(passed)), "seconds": round(t, 4),
+           "timing": "CUDA events around tpo_gpu_stability_batch calls (host lowering included)"}
+    if dist.rank == 0 and dist.world == 1:
+        from oracle import ref
+        if ref.available():
+            k, w0 = 0, time.perf_counter()
+            while time.perf_counter() - w0 < 3.0:
+                _, _, pool, prog = jobs[k % len(jobs)]
+                ref.float_stability_filter(pool[k % len(pool)][1], prog, seed=k)
+                k += 1
+            out["cpu_baseline"] = {"value": round(k / (time.perf_counter() - w0), 1), "unit": "candidates/s",
+                                   "cores": 1, "kind": "reference",
+                                   "sample": f"{k} float_stability_filter calls, families round robin, 1 thread"}
+    return out
 
 
 def search_stream(ctx, dist, fams, pool_fams, per_fam_total=25000):

@@ -289,6 +289,41 @@ def cpu_baseline_fused(wl, threads=1, min_seconds=10.0):
             "ms_per_eval": round(per, 1)}
 
 
+def generic_vm(wl, reps=3):
+    """The same µGraph (and its flat program) on the generic GPU VM in the
+    reference's own arithmetic (tpo_gpu_eval_vm: fp64, the reference's
+    operation order; the global-memory executor at these sizes) — the path
+    any µGraph without a hand-written kernel takes.  Wall clock per call,
+    host buffers in and out."""
+    import torch
+    from paper_2405_05751_b200.api import Context
+    ctx = Context(0)
+    ins = [x.float().numpy().astype(np.float64) for x in wl["host"]]
+    dins = [torch.from_numpy(x).cuda() for x in ins]
+    out = {}
+    for tag, g, mode in (("eval_mugraph", wl["mu"], 0), ("eval_program", wl["prog"], 1)):
+        gg = ctx.compile(g)
+        ctx.eval_vm(gg, ins, mode=mode)  # warm
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            ctx.eval_vm(gg, ins, mode=mode)
+        wall = (time.perf_counter() - t0) / reps * 1e3
+        st = torch.cuda.current_stream()
+        ctx.eval_vm_dev(gg, dins, mode=mode, stream=st.cuda_stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(reps):
+            ctx.eval_vm_dev(gg, dins, mode=mode, stream=st.cuda_stream)
+        e1.record()
+        torch.cuda.synchronize()
+        out[tag] = {"device_ms_per_eval": round(e0.elapsed_time(e1) / reps, 3),
+                    "host_buffers_ms_per_eval": round(wall, 3), "dtype": "f64",
+                    "h2d_bytes": int(sum(x.nbytes for x in ins))}
+    out["note"] = "bit-exact with the reference for graphs without exp (tests/test_fp_vm_gpu.py)"
+    return out
+
+
 def reference_arm(args, wl):
     """--impl reference: the reference's eval_mugraph using all host cores, each
     thread evaluating the µGraph restricted to a slice of output columns
@@ -618,6 +653,8 @@ def main():
         line["verifier"] = run_verify(dist, args.verify_candidates, steps=1, warmup=3)
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_fused(wl)
+    if dist.rank == 0 and not args.profile:
+        line["generic_vm"] = generic_vm(wl)
     if dist.rank == 0:
         print(json.dumps(line), flush=True)
     dist.close()

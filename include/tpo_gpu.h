@@ -199,6 +199,12 @@ int tpo_gpu_verify_pool(tpo_gpu_ctx *ctx, const tpo_gpu_graph *program,
 int tpo_gpu_eval_vm(tpo_gpu_ctx *ctx, const tpo_gpu_graph *g, int32_t mode, const void *in_host,
                     void *out_host);
 
+/* tpo_gpu_eval_vm on device buffers (inputs concatenated in graph-input
+ * order, outputs concatenated; fp64, or fp32 for mode 2), asynchronous on
+ * cuda_stream (NULL: the legacy stream). */
+int tpo_gpu_eval_vm_dev(tpo_gpu_ctx *ctx, const tpo_gpu_graph *g, int32_t mode, const void *in_dev,
+                        void *out_dev, void *cuda_stream);
+
 /* tpo::verify::float_stability_filter(g, program, trials, tol, seed, input_scale)
  * proj/core/include/tpo/verify/stability.hpp:29-31 on the GPU; *out_ok = 1/0. */
 int tpo_gpu_float_stability_filter(tpo_gpu_ctx *ctx, const tpo_gpu_graph *g,

@@ -268,6 +268,25 @@ class Context:
             c += k
         return res
 
+    def eval_vm_dev(self, g, inputs, mode: int = 0, stream=None):
+        """tpo_gpu_eval_vm on torch CUDA tensors (``tpo_gpu_eval_vm_dev``):
+        inputs fp64 (fp32 for mode 2) in graph-input order; returns the
+        outputs as torch CUDA tensors, asynchronously on ``stream``."""
+        import torch
+        g = self.compile(g)
+        dt = torch.float32 if mode == 2 else torch.float64
+        flat = torch.cat([x.to(dt).reshape(-1) for x in inputs]).contiguous()
+        oshapes = g.shapes(True)
+        out = torch.empty(sum(int(np.prod(s)) for s in oshapes), dtype=dt, device=flat.device)
+        N.check(N.lib().tpo_gpu_eval_vm_dev(self.h, g.h, mode, C.c_void_p(flat.data_ptr()),
+                                            C.c_void_p(out.data_ptr()), C.c_void_p(stream) if stream else None))
+        res, c = [], 0
+        for s in oshapes:
+            k = int(np.prod(s))
+            res.append(out[c:c + k].view(*s))
+            c += k
+        return res
+
     def float_stability_filter(self, g, program, trials: int = 1, tol: float = 1e-3, seed: int = 17,
                                scale: float = 1.0) -> bool:
         """verify::float_stability_filter (stability.hpp:29-31) on the GPU."""

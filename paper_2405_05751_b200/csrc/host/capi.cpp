@@ -403,6 +403,15 @@ void run_verify(Ctx &C, const Batch &bt, const tpo_verify_cfg &cfg, const tpo_fi
 
 }  // namespace
 
+const VmProgram &lowered_fp(const Graph &G) {
+  std::lock_guard<std::mutex> lk(G.ff_mu);
+  const auto key = std::make_pair(uint32_t(G.in_elems), 2);
+  auto it = G.ff_cache.find(key);
+  if (it == G.ff_cache.end())
+    it = G.ff_cache.emplace(key, std::make_shared<const VmProgram>(lower_vm(G.g, 0, uint32_t(G.in_elems)))).first;
+  return *it->second;
+}
+
 const VmProgram &lowered_ff(const Graph &G, uint32_t region, bool pin) {
   std::lock_guard<std::mutex> lk(G.ff_mu);
   const auto key = std::make_pair(region, int(pin));
@@ -804,8 +813,14 @@ size_t fp_smem(uint32_t code_len, uint64_t words, size_t elem) {
 
 extern "C" {
 
-int tpo_gpu_eval_vm(tpo_gpu_ctx *ctx, const tpo_gpu_graph *h, int32_t mode, const void *in_host,
-                    void *out_host) {
+}  // extern "C"
+
+namespace {
+
+// Generic fp VM evaluation.  host: in/out are host buffers (copied and
+// synchronised); else device buffers, asynchronous on `stream`.
+int eval_vm_impl(tpo_gpu_ctx *ctx, const tpo_gpu_graph *h, int32_t mode, const void *in, void *out,
+                 bool host, cudaStream_t stream) {
   return guard([&] {
     Ctx &C = ctx->c;
     const Graph &G = h->g;
@@ -817,24 +832,22 @@ int tpo_gpu_eval_vm(tpo_gpu_ctx *ctx, const tpo_gpu_graph *h, int32_t mode, cons
     check_cuda(cudaSetDevice(C.device), "cudaSetDevice");
     const size_t elem = mode == 2 ? 4 : 8;
     const uint32_t n_in = uint32_t(G.in_elems);
-    VmProgram p = lower_vm(G.g, 0, n_in);
+    const VmProgram &p = lowered_fp(G);
     const size_t smem = fp_smem(uint32_t(p.code.size()), uint64_t(n_in) + p.region_words, elem);
-    cudaStream_t st = C.stream;
+    cudaStream_t st = host ? C.stream : stream;
+    const cudaMemcpyKind h2d = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    const cudaMemcpyKind d2h = host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
     if (smem > 232448 || std::getenv("TPO_VM_GLOBAL")) {
       // global-memory executor: VM memory in HBM, one launch per instruction
       const uint64_t words = uint64_t(n_in) + p.region_words;
       void *W = C.ws.get(words * elem + 16);
-      check_cuda(cudaMemcpyAsync(W, in_host, size_t(n_in) * elem, cudaMemcpyHostToDevice, st), "in");
-      size_t lb = 0;
-      uint32_t trips = 1;
+      check_cuda(cudaMemcpyAsync(W, in, size_t(n_in) * elem, h2d, st), "in");
       for (size_t pc = 0; pc < p.code.size(); ++pc) {
         const TpoVmInstr &I = p.code[pc];
-        if (I.op == VM_LOOP) {
-          lb = pc, trips = I.n;
-          // run the body `trips` times
+        if (I.op == VM_LOOP) {  // run the body I.n times
           size_t end = pc + 1;
           while (end < p.code.size() && p.code[end].op != VM_ENDLOOP) ++end;
-          for (uint32_t it = 0; it < trips; ++it)
+          for (uint32_t it = 0; it < I.n; ++it)
             for (size_t k = pc + 1; k < end; ++k)
               check_cuda(cudaError_t(tpo_fp_launch_instr(W, mode == 2, &p.code[k], it, C.num_sms, st)),
                          "vm instr");
@@ -843,24 +856,27 @@ int tpo_gpu_eval_vm(tpo_gpu_ctx *ctx, const tpo_gpu_graph *h, int32_t mode, cons
         }
         check_cuda(cudaError_t(tpo_fp_launch_instr(W, mode == 2, &I, 0, C.num_sms, st)), "vm instr");
       }
-      (void)lb;
       size_t c = 0;
       for (uint32_t t = 0; t < p.desc.n_out; ++t) {
-        check_cuda(cudaMemcpyAsync(static_cast<char *>(out_host) + c * elem,
+        check_cuda(cudaMemcpyAsync(static_cast<char *>(out) + c * elem,
                                    static_cast<char *>(W) + size_t(p.desc.out_off[t]) * elem,
-                                   size_t(p.desc.out_len[t]) * elem, cudaMemcpyDeviceToHost, st), "out");
+                                   size_t(p.desc.out_len[t]) * elem, d2h, st), "out");
         c += p.desc.out_len[t];
       }
-      check_cuda(cudaStreamSynchronize(st), "vm sync");
+      if (host) check_cuda(cudaStreamSynchronize(st), "vm sync");
       return 0;
     }
     auto *dcode = static_cast<TpoVmInstr *>(C.code.get(p.code.size() * sizeof(TpoVmInstr) + 16));
     check_cuda(cudaMemcpyAsync(dcode, p.code.data(), p.code.size() * sizeof(TpoVmInstr),
                                cudaMemcpyHostToDevice, st), "code");
-    void *din = C.inputs.get(size_t(n_in) * elem + 16);
-    check_cuda(cudaMemcpyAsync(din, in_host, size_t(n_in) * elem, cudaMemcpyHostToDevice, st), "in");
+    const void *din = in;
+    if (host) {
+      void *d = C.inputs.get(size_t(n_in) * elem + 16);
+      check_cuda(cudaMemcpyAsync(d, in, size_t(n_in) * elem, h2d, st), "in");
+      din = d;
+    }
     const size_t n_out = size_t(G.out_elems);
-    void *dout = C.out.get(n_out * elem + 16);
+    void *dout = host ? C.out.get(n_out * elem + 16) : out;
     tpo_fp::EvalArgs a{};
     a.code = dcode;
     a.code_len = uint32_t(p.code.size());
@@ -870,10 +886,26 @@ int tpo_gpu_eval_vm(tpo_gpu_ctx *ctx, const tpo_gpu_graph *h, int32_t mode, cons
     a.inputs = din;
     a.out = dout;
     check_cuda(cudaError_t(tpo_fp_launch_eval(&a, mode == 2, smem, st)), "fp eval launch");
-    check_cuda(cudaMemcpyAsync(out_host, dout, n_out * elem, cudaMemcpyDeviceToHost, st), "out");
-    check_cuda(cudaStreamSynchronize(st), "fp eval sync");
+    if (host) {
+      check_cuda(cudaMemcpyAsync(out, dout, n_out * elem, d2h, st), "out");
+      check_cuda(cudaStreamSynchronize(st), "fp eval sync");
+    }
     return 0;
   });
+}
+
+}  // namespace
+
+extern "C" {
+
+int tpo_gpu_eval_vm(tpo_gpu_ctx *ctx, const tpo_gpu_graph *h, int32_t mode, const void *in_host,
+                    void *out_host) {
+  return eval_vm_impl(ctx, h, mode, in_host, out_host, true, nullptr);
+}
+
+int tpo_gpu_eval_vm_dev(tpo_gpu_ctx *ctx, const tpo_gpu_graph *h, int32_t mode, const void *in_dev,
+                        void *out_dev, void *cuda_stream) {
+  return eval_vm_impl(ctx, h, mode, in_dev, out_dev, false, static_cast<cudaStream_t>(cuda_stream));
 }
 
 int tpo_gpu_stability_batch(tpo_gpu_ctx *ctx, const tpo_gpu_graph *program,

@@ -54,7 +54,7 @@ struct Graph {
   int64_t in_elems = 0, out_elems = 0;
   mutable int64_t vm_words = -1;  // -2: not computed yet (tpo_gpu_graph_info)
   FusedPlan plan;  // fused_kind == 0 when no hand-written kernel matches
-  // field-mode VM lowerings by (region base, pinned outputs): a handle is
+  // VM lowerings by (region base, 0/1 field pinned-outputs | 2 fp): a handle is
   // immutable, so batches over the same graphs reuse their bytecode
   mutable std::mutex ff_mu;
   mutable std::map<std::pair<uint32_t, int>, std::shared_ptr<const VmProgram>> ff_cache;
@@ -62,6 +62,8 @@ struct Graph {
 
 // lower_vm(G.g, 0, region, pin, /*field=*/true), memoised on the handle.
 const VmProgram &lowered_ff(const Graph &G, uint32_t region, bool pin);
+// lower_vm(G.g, 0, inputs) in floating-point mode, memoised on the handle.
+const VmProgram &lowered_fp(const Graph &G);
 
 // Throws tpo::Error on failure.
 void check_cuda(cudaError_t e, const char *what);

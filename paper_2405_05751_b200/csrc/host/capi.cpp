@@ -842,20 +842,53 @@ int eval_vm_impl(tpo_gpu_ctx *ctx, const tpo_gpu_graph *h, int32_t mode, const v
       const uint64_t words = uint64_t(n_in) + p.region_words;
       void *W = C.ws.get(words * elem + 16);
       check_cuda(cudaMemcpyAsync(W, in, size_t(n_in) * elem, h2d, st), "in");
-      for (size_t pc = 0; pc < p.code.size(); ++pc) {
-        const TpoVmInstr &I = p.code[pc];
-        if (I.op == VM_LOOP) {  // run the body I.n times
-          size_t end = pc + 1;
-          while (end < p.code.size() && p.code[end].op != VM_ENDLOOP) ++end;
-          for (uint32_t it = 0; it < I.n; ++it)
-            for (size_t k = pc + 1; k < end; ++k)
-              check_cuda(cudaError_t(tpo_fp_launch_instr(W, mode == 2, &p.code[k], it, C.num_sms, st)),
-                         "vm instr");
-          pc = end;  // skip ENDLOOP
-          continue;
+      auto launch_all = [&](cudaStream_t s2) {
+        for (size_t pc = 0; pc < p.code.size(); ++pc) {
+          const TpoVmInstr &I = p.code[pc];
+          if (I.op == VM_LOOP) {  // run the body I.n times
+            size_t end = pc + 1;
+            while (end < p.code.size() && p.code[end].op != VM_ENDLOOP) ++end;
+            for (uint32_t it = 0; it < I.n; ++it)
+              for (size_t k = pc + 1; k < end; ++k)
+                check_cuda(cudaError_t(tpo_fp_launch_instr(W, mode == 2, &p.code[k], it, C.num_sms, s2)),
+                           "vm instr");
+            pc = end;  // skip ENDLOOP
+            continue;
+          }
+          check_cuda(cudaError_t(tpo_fp_launch_instr(W, mode == 2, &I, 0, C.num_sms, s2)), "vm instr");
         }
-        check_cuda(cudaError_t(tpo_fp_launch_instr(W, mode == 2, &I, 0, C.num_sms, st)), "vm instr");
+      };
+      // the launch sequence is fixed per (graph, mode, arena): captured once
+      // into a CUDA graph (the per-instruction kernels are µs-scale, so host
+      // launch overhead would otherwise bound the executor)
+      cudaGraphExec_t exec = nullptr;
+      {
+        std::lock_guard<std::mutex> lk(G.ff_mu);
+        auto it = G.vm_graphs.find({mode, W});
+        if (it != G.vm_graphs.end()) exec = it->second;
       }
+      if (!exec && !std::getenv("TPO_VM_NO_GRAPH")) {
+        cudaStream_t cap;
+        check_cuda(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "capture stream");
+        cudaGraph_t graph = nullptr;
+        if (cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+          launch_all(cap);
+          if (cudaStreamEndCapture(cap, &graph) == cudaSuccess && graph) {
+            if (cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) exec = nullptr;
+            cudaGraphDestroy(graph);
+          }
+        }
+        cudaStreamDestroy(cap);
+        (void)cudaGetLastError();
+        if (exec) {
+          std::lock_guard<std::mutex> lk(G.ff_mu);
+          G.vm_graphs[{mode, W}] = exec;
+        }
+      }
+      if (exec)
+        check_cuda(cudaGraphLaunch(exec, st), "vm graph");
+      else
+        launch_all(st);
       size_t c = 0;
       for (uint32_t t = 0; t < p.desc.n_out; ++t) {
         check_cuda(cudaMemcpyAsync(static_cast<char *>(out) + c * elem,

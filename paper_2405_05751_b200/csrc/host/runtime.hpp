@@ -58,6 +58,15 @@ struct Graph {
   // immutable, so batches over the same graphs reuse their bytecode
   mutable std::mutex ff_mu;
   mutable std::map<std::pair<uint32_t, int>, std::shared_ptr<const VmProgram>> ff_cache;
+  // global-memory fp executor: the instruction launches captured once per
+  // (mode, VM arena) as a CUDA graph and replayed
+  mutable std::map<std::pair<int, void *>, cudaGraphExec_t> vm_graphs;
+  Graph() = default;
+  Graph(const Graph &) = delete;
+  Graph &operator=(const Graph &) = delete;
+  ~Graph() {
+    for (auto &kv : vm_graphs) cudaGraphExecDestroy(kv.second);
+  }
 };
 
 // lower_vm(G.g, 0, region, pin, /*field=*/true), memoised on the handle.

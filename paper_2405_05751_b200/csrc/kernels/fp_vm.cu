@@ -206,6 +206,130 @@ __global__ void __launch_bounds__(256) instr_kernel(T *W, const TpoVmInstr I, ui
   exec_instr<T>(W, I, it, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
 }
 
+// Global-memory executor, strided matmul: one CTA per TM x TN output tile
+// of one (grid block, batch) matrix, A and B tiles staged through shared
+// memory TK k at a time; each thread keeps RM x RN accumulators and adds
+// the products for k ascending, one k at a time — the reference's
+// acc = add(acc, mul(a, b)) order (eval_core.hpp:181-203), so results are
+// bit-identical; the last k chunk is cut short, never zero padded (+0.0
+// would turn an accumulated -0.0 into +0.0).
+template <typename T, int TM, int TN, int RM, int RN, int TK>
+__global__ void __launch_bounds__((TM / RM) * (TN / RN))
+    matmul_kernel(T *W, const TpoVmInstr I, uint32_t it) {
+  using O = Ops<T>;
+  constexpr int NT = (TM / RM) * (TN / RN);
+  constexpr int LA = (TK * TM + NT - 1) / NT, LB = (TK * TN + NT - 1) / NT;  // loads per thread
+  __shared__ T As[2][TK][TM + 1];
+  __shared__ T Bs[2][TK][TN + 1];
+  const uint32_t Bi = I.dims[3], M = I.dims[4], K = I.dims[5], N = I.dims[6];
+  const uint32_t mat = blockIdx.z;  // (grid block, batch) index
+  const uint32_t blk = mat / Bi, bi = mat - blk * Bi;
+  const uint32_t gyz = I.dims[1] * I.dims[2];
+  const uint32_t gx = blk / gyz, gr = blk - gx * gyz, gy = gr / I.dims[2], gz = gr - gy * I.dims[2];
+  const T *pa = W + int64_t(int32_t(I.a + it * I.a_iter)) + int64_t(gx) * I.sa[0] + int64_t(gy) * I.sa[1] +
+                int64_t(gz) * I.sa[2] + int64_t(bi) * I.sa[3];
+  const T *pb = W + int64_t(int32_t(I.b + it * I.b_iter)) + int64_t(gx) * I.sb[0] + int64_t(gy) * I.sb[1] +
+                int64_t(gz) * I.sb[2] + int64_t(bi) * I.sb[3];
+  const int64_t sma = I.sa[4], ska = I.sa[5], skb = I.sb[5], snb = I.sb[6];
+  const uint32_t m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;
+  const int tx = threadIdx.x % (TN / RN), ty = threadIdx.x / (TN / RN);
+  T ra[LA], rb[LB];  // the next k chunk, loaded while the current one is consumed
+  auto load = [&](uint32_t k0) {
+#pragma unroll
+    for (int l = 0; l < LA; ++l) {
+      const int e = int(threadIdx.x) + l * NT, kk = e / TM, mm = e % TM;
+      const uint32_t m = m0 + mm, k = k0 + kk;
+      ra[l] = (e < TK * TM && m < M && k < K) ? pa[int64_t(m) * sma + int64_t(k) * ska] : T(0);
+    }
+#pragma unroll
+    for (int l = 0; l < LB; ++l) {
+      const int e = int(threadIdx.x) + l * NT, kk = e / TN, nn = e % TN;
+      const uint32_t n = n0 + nn, k = k0 + kk;
+      rb[l] = (e < TK * TN && n < N && k < K) ? pb[int64_t(k) * skb + int64_t(n) * snb] : T(0);
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int l = 0; l < LA; ++l) {
+      const int e = int(threadIdx.x) + l * NT;
+      if (e < TK * TM) As[buf][e / TM][e % TM] = ra[l];
+    }
+#pragma unroll
+    for (int l = 0; l < LB; ++l) {
+      const int e = int(threadIdx.x) + l * NT;
+      if (e < TK * TN) Bs[buf][e / TN][e % TN] = rb[l];
+    }
+  };
+  T acc[RM][RN];
+#pragma unroll
+  for (int i = 0; i < RM; ++i)
+#pragma unroll
+    for (int j = 0; j < RN; ++j) acc[i][j] = T(0);
+  load(0);
+  store(0);
+  __syncthreads();
+  int buf = 0;
+  for (uint32_t k0 = 0; k0 < K; k0 += TK) {
+    const bool more = k0 + TK < K;
+    if (more) load(k0 + TK);
+    const uint32_t kc = min(uint32_t(TK), K - k0);
+    for (uint32_t kk = 0; kk < kc; ++kk) {
+      T a[RM], b[RN];
+#pragma unroll
+      for (int i = 0; i < RM; ++i) a[i] = As[buf][kk][ty * RM + i];
+#pragma unroll
+      for (int j = 0; j < RN; ++j) b[j] = Bs[buf][kk][tx * RN + j];
+#pragma unroll
+      for (int i = 0; i < RM; ++i)
+#pragma unroll
+        for (int j = 0; j < RN; ++j) acc[i][j] = O::add(acc[i][j], O::mul(a[i], b[j]));
+    }
+    if (more) store(buf ^ 1);
+    __syncthreads();
+    buf ^= 1;
+  }
+  const uint64_t dbase = uint64_t(I.dst) + uint64_t(mat) * M * N;
+#pragma unroll
+  for (int i = 0; i < RM; ++i)
+#pragma unroll
+    for (int j = 0; j < RN; ++j) {
+      const uint32_t m = m0 + ty * RM + i, n = n0 + tx * RN + j;
+      if (m >= M || n >= N) continue;
+      T &dst = W[dbase + uint64_t(m) * N + n];
+      dst = (I.flags & VM_ACCUM) ? O::add(dst, acc[i][j]) : acc[i][j];  // acc = add(acc, val)
+    }
+}
+
+// Global-memory executor, grouped Sum with long groups: one warp per output;
+// the lanes load 32 consecutive group elements (coalesced when inner == 1)
+// and every lane folds them in group order through shuffles, so the sum is
+// the reference's sequential acc = add(acc, x) (eval_core.hpp:205-222).
+template <typename T>
+__global__ void __launch_bounds__(256) sum_kernel(T *W, const TpoVmInstr I) {
+  using O = Ops<T>;
+  const uint32_t o = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
+  if (o >= I.n) return;  // warp-uniform
+  const uint32_t mid = I.dims[1], grp = I.dims[2], inner = I.dims[3];
+  const uint32_t t = o / inner, in_i = o - t * inner;
+  const uint32_t ou = t / mid, m = t - ou * mid;
+  const T *pa = W + I.a + (uint64_t(ou) * mid * grp + uint64_t(m) * grp) * inner + in_i;
+  T acc = T(0);
+  for (uint32_t g0 = 0; g0 < grp; g0 += 32) {
+    const uint32_t g = g0 + lane;
+    const T v = g < grp ? pa[uint64_t(g) * inner] : T(0);
+    const uint32_t cnt = min(32u, grp - g0);
+    for (uint32_t j = 0; j < cnt; ++j) acc = O::add(acc, __shfl_sync(0xffffffffu, v, int(j)));
+  }
+  if (lane == 0) W[I.dst + o] = acc;
+}
+
+template <typename T, int TM, int TN, int RM, int RN, int TK>
+void launch_matmul(T *W, const TpoVmInstr &I, uint32_t it, cudaStream_t st) {
+  const uint32_t mats = I.dims[0] * I.dims[1] * I.dims[2] * I.dims[3];
+  const dim3 grid((I.dims[6] + TN - 1) / TN, (I.dims[4] + TM - 1) / TM, mats);
+  matmul_kernel<T, TM, TN, RM, RN, TK><<<grid, (TM / RM) * (TN / RN), 0, st>>>(W, I, it);
+}
+
 // Draw j (0-based) of Rng::derive(seed, stream): fin(s0 + (j+1)·γ), s0 the
 // state after derive's discarded draw (rng.hpp:30-40).
 __device__ __forceinline__ uint64_t fin(uint64_t z) {
@@ -309,6 +433,30 @@ extern "C" int tpo_fp_launch_eval(const tpo_fp::EvalArgs *a, int f32, size_t sme
 
 extern "C" int tpo_fp_launch_instr(void *W, int f32, const TpoVmInstr *I, uint32_t it, int num_sms,
                                    cudaStream_t st) {
+  if (I->op == VM_MATMUL && (I->flags & VM_STRIDED) && I->dims[0] * I->dims[1] * I->dims[2] * I->dims[3] <= 65535u) {
+    // tiled by the matrix shape: skinny rows, medium, square
+    const uint32_t M = I->dims[4];
+    if (f32) {
+      float *w = static_cast<float *>(W);
+      if (M <= 8) tpo_fp::launch_matmul<float, 8, 32, 1, 1, 32>(w, *I, it, st);
+      else if (M <= 32) tpo_fp::launch_matmul<float, 32, 64, 2, 4, 16>(w, *I, it, st);
+      else tpo_fp::launch_matmul<float, 64, 64, 4, 4, 16>(w, *I, it, st);
+    } else {
+      double *w = static_cast<double *>(W);
+      if (M <= 8) tpo_fp::launch_matmul<double, 8, 32, 1, 1, 32>(w, *I, it, st);
+      else if (M <= 32) tpo_fp::launch_matmul<double, 32, 64, 2, 4, 16>(w, *I, it, st);
+      else tpo_fp::launch_matmul<double, 64, 64, 4, 4, 16>(w, *I, it, st);
+    }
+    return int(cudaGetLastError());
+  }
+  if (I->op == VM_SUM && I->dims[2] >= 64 && I->n <= uint32_t(num_sms) * 256) {
+    const int grid = int((uint64_t(I->n) * 32 + 255) / 256);
+    if (f32)
+      tpo_fp::sum_kernel<float><<<grid, 256, 0, st>>>(static_cast<float *>(W), *I);
+    else
+      tpo_fp::sum_kernel<double><<<grid, 256, 0, st>>>(static_cast<double *>(W), *I);
+    return int(cudaGetLastError());
+  }
   const uint32_t items = I->n ? I->n : 1;
   // matmul / sum items run long sequential loops: one item per thread;
   // elementwise items: a few per thread

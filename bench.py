@@ -546,13 +546,17 @@ def search_stream(ctx, dist, fams, pool_fams, per_fam_total=25000):
         t_compile += time.perf_counter() - c0
         if any(st):
             raise RuntimeError("search stream: a candidate failed to compile")
-        _, acc = ctx.verify_batch(gp, gs, np.arange(first, first + n, dtype=np.uint64), want_verdicts=False)
+        # the pipeline calls random_test_equivalence(program, cand, cfg) with
+        # one VerifyConfig for every candidate: seed 0
+        _, acc = ctx.verify_batch(gp, gs, np.zeros(n, dtype=np.uint64), want_verdicts=False)
         accepted += int(acc.sum())
     wall = dist.max(time.perf_counter() - t0)
     tot = per_fam_total * len(texts)
     return {"value": round(tot / wall, 1), "unit": "candidates/s", "candidates": tot,
             "distinct_graphs": tot, "accepted": int(dist.sum(accepted)),
             "compile_share": round(dist.max(t_compile) / wall, 3), "host_threads": os.cpu_count(),
+            "seed_rule": "VerifyConfig default (seed 0) for every candidate, as the pipeline calls it; "
+                         "the batch's common first attempt is computed once",
             "path": "JSON text -> tpo_gpu_compile_many (all host cores) -> tpo_gpu_verify_batch -> "
                     "accept bits on the host; wall clock"}
 

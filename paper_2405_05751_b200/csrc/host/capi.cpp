@@ -167,6 +167,7 @@ struct Batch {
   uint32_t n_in = 0;
   uint32_t max_words = 0;  // words of VM memory needed
   uint32_t max_code = 0;   // program + largest candidate, instructions (staged in smem)
+  uint32_t cand_base = 0;  // inputs + the program's pinned outputs (words)
 };
 
 void check_pair(const ir::KernelGraph &a, const ir::KernelGraph &b) {
@@ -206,6 +207,7 @@ Batch build_batch(const Graph &prog, const std::vector<const Graph *> &uniq) {
   // them is dead once the candidate starts, so the candidate region reuses it
   VmProgram pp = lowered_ff(prog, bt.n_in, /*pin_outputs=*/true);
   const uint32_t cbase = bt.n_in + pp.pinned_words;
+  bt.cand_base = cbase;
   if (pp.poisoned) pp.desc.err = uint8_t(1 + int(ErrCode::PoisonedExponent));
   add_graph(bt, pp);
   uint32_t maxw = bt.n_in + pp.region_words;
@@ -299,10 +301,27 @@ void run_verify(Ctx &C, const Batch &bt, const tpo_verify_cfg &cfg, const tpo_fi
     check_cuda(cudaMemcpyAsync(dc, r.cand_graph->data(), r.n * 4, cudaMemcpyHostToDevice, st), "cands");
     a.cand_graph = dc;
   }
+  a.n_in = bt.n_in;
   if (r.seeds) {
     auto *ds = static_cast<uint64_t *>(C.seeds.get(r.n * 8));
     check_cuda(cudaMemcpyAsync(ds, r.seeds, r.n * 8, cudaMemcpyHostToDevice, st), "seeds");
     a.seeds = ds;
+    // a search loop verifies every candidate with the same VerifyConfig
+    // seed: the first attempt's inputs and program outputs are then common
+    // to the batch — compute them once (TPO_VM_NO_SHARED disables)
+    bool same = r.n >= 32 && !bt.graphs[0].err && !std::getenv("TPO_VM_NO_SHARED");
+    for (uint64_t k = 1; same && k < r.n; ++k) same = r.seeds[k] == r.seeds[0];
+    if (same) {
+      a.shared_len = bt.cand_base;
+      auto *sw = static_cast<uint32_t *>(C.shared_w.get(size_t(bt.cand_base) * 4 + 16));
+      auto *stab = static_cast<uint16_t *>(C.shared_tab.get(size_t(fs.fc.p + 2 * fs.fc.q) * 2 + 16));
+      auto *smeta = static_cast<uint32_t *>(C.shared_meta.get(16));
+      check_cuda(cudaError_t(tpo_ff_launch_shared(&a, r.seeds[0], smem, sw, stab, smeta, st)), "shared attempt");
+      a.shared_w = sw;
+      a.shared_tab = stab;
+      a.shared_meta = smeta;
+      a.shared_seed = r.seeds[0];
+    }
   }
   a.first = r.first;
   a.n = r.n;

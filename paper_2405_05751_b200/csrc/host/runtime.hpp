@@ -41,6 +41,7 @@ struct Ctx {
   int num_sms = 0;
   std::map<uint64_t, std::unique_ptr<FieldState>> fields;
   DevBuf code, graphs, pool, cand, seeds, verdicts, accept, counter, out, status, inputs, ws;
+  DevBuf shared_w, shared_tab, shared_meta;  // same-seed verification batches
   // host-buffer fp evaluation (tpo_gpu_eval_mugraph_host): per-input device
   // copies (bf16), fp32 staging for converted inputs, per-output buffers
   std::vector<DevBuf> h_in, h_stage, h_out;

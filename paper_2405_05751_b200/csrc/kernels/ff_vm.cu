@@ -581,12 +581,33 @@ __global__ void __launch_bounds__(NT) verify_kernel(VerifyArgs a) {
       for (int att = 0; att <= a.max_resamples && !round_done; ++att) {
         const uint64_t stream = uint64_t(round) * 131071ull + uint64_t(att);
         long long t0 = PROF ? clock64() : 0;
-        const uint32_t omega = gen_attempt(s, f, seed, stream, a.n_in, silu, &s_slow, &s_omega);
-        if (threadIdx.x == 0) s_flag = 0;
-        __syncthreads();
-        if (PROF && threadIdx.x == 0) s_prof[0] += (unsigned long long)(clock64() - t0), s_prof[16] += 1;
-        bool ok = run_program<PROF>(s, f, scode, g1.code_len, &s_flag, s_prof) &&
-                  run_program<PROF>(s, f, ccode, g2.code_len, &s_flag, s_prof);
+        uint32_t omega;
+        bool ok;
+        if (a.shared_w && seed == a.shared_seed && round == 0 && att == 0) {
+          // the batch's common first attempt: inputs, tables and the
+          // program's outputs were computed once (shared_attempt_kernel)
+          if (!a.shared_meta[0]) {  // the program itself needs a resample here
+            ++v.resamples;
+            continue;
+          }
+          for (uint32_t i = threadIdx.x; i < a.shared_len; i += blockDim.x) s.w[i] = __ldg(a.shared_w + i);
+          for (uint32_t i = threadIdx.x; i < f.p; i += blockDim.x) s.silu_p[i] = a.shared_tab[i];
+          for (uint32_t i = threadIdx.x; i < f.q; i += blockDim.x) {
+            s.silu_q[i] = a.shared_tab[f.p + i];
+            s.pow_w[i] = a.shared_tab[f.p + f.q + i];
+          }
+          omega = a.shared_meta[1];
+          if (threadIdx.x == 0) s_flag = 0;
+          __syncthreads();
+          ok = run_program<PROF>(s, f, ccode, g2.code_len, &s_flag, s_prof);
+        } else {
+          omega = gen_attempt(s, f, seed, stream, a.n_in, silu, &s_slow, &s_omega);
+          if (threadIdx.x == 0) s_flag = 0;
+          __syncthreads();
+          if (PROF && threadIdx.x == 0) s_prof[0] += (unsigned long long)(clock64() - t0), s_prof[16] += 1;
+          ok = run_program<PROF>(s, f, scode, g1.code_len, &s_flag, s_prof) &&
+               run_program<PROF>(s, f, ccode, g2.code_len, &s_flag, s_prof);
+        }
         if (!ok) {
           ++v.resamples;
           continue;
@@ -626,6 +647,34 @@ __global__ void __launch_bounds__(NT) verify_kernel(VerifyArgs a) {
     }
   }
   if (PROF && threadIdx.x < 32 && a.prof) atomicAdd(a.prof + threadIdx.x, s_prof[threadIdx.x]);
+}
+
+// Same-seed batches: attempt (seed, stream 0) of the program, once.  The
+// SiLU tables are always drawn: they follow the inputs and omega in the
+// stream, so drawing them changes nothing a SiLU-free pair reads.
+__global__ void __launch_bounds__(kThreads) shared_attempt_kernel(VerifyArgs a, uint64_t seed,
+                                                                  uint32_t *w_out, uint16_t *tab_out,
+                                                                  uint32_t *meta) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ int s_flag, s_slow;
+  __shared__ uint32_t s_omega;
+  const FieldConst &f = a.field;
+  Smem s = carve(smem, f, a.code_smem_bytes);
+  load_tables(s, f, a.tables);
+  const TpoVmGraph g1 = a.graphs[a.program];
+  TpoVmInstr *scode = reinterpret_cast<TpoVmInstr *>(smem + f.table_bytes);
+  copy_code(scode, a.code + g1.code_off, g1.code_len);
+  const uint32_t omega = gen_attempt(s, f, seed, 0, a.n_in, true, &s_slow, &s_omega);
+  if (threadIdx.x == 0) s_flag = 0;
+  __syncthreads();
+  const bool ok = run_program<false>(s, f, scode, g1.code_len, &s_flag, nullptr);
+  for (uint32_t i = threadIdx.x; i < a.shared_len; i += blockDim.x) w_out[i] = s.w[i];
+  for (uint32_t i = threadIdx.x; i < f.p; i += blockDim.x) tab_out[i] = s.silu_p[i];
+  for (uint32_t i = threadIdx.x; i < f.q; i += blockDim.x) {
+    tab_out[f.p + i] = s.silu_q[i];
+    tab_out[f.p + f.q + i] = s.pow_w[i];
+  }
+  if (threadIdx.x == 0) meta[0] = ok ? 1u : 0u, meta[1] = omega;
 }
 
 // Debug / parity: evaluate one graph for one (seed, stream) attempt, or on
@@ -691,6 +740,15 @@ extern "C" int tpo_ff_launch_verify(const tpo_ff::VerifyArgs *a, int grid, size_
     configured_for[slot] = int(smem);
   }
   kern<<<grid, small ? 128 : 256, smem, st>>>(*a);
+  return int(cudaGetLastError());
+}
+
+extern "C" int tpo_ff_launch_shared(const tpo_ff::VerifyArgs *a, uint64_t seed, size_t smem,
+                                    uint32_t *w_out, uint16_t *tab_out, uint32_t *meta,
+                                    cudaStream_t st) {
+  cudaFuncSetAttribute(tpo_ff::shared_attempt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(smem));
+  tpo_ff::shared_attempt_kernel<<<1, tpo_ff::kThreads, smem, st>>>(*a, seed, w_out, tab_out, meta);
   return int(cudaGetLastError());
 }
 

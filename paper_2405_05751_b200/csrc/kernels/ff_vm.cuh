@@ -56,6 +56,15 @@ struct VerifyArgs {
   unsigned long long *work;      // optional: attempts actually consumed
   unsigned long long *prof;      // optional (TPO_VM_PROFILE): [16] cycles, [16] counts per opcode
   uint32_t code_smem_bytes;      // smem staging of program + candidate bytecode
+  // Same-seed batches (a search loop verifying every candidate with the
+  // VerifyConfig seed): attempt (shared_seed, round 0, attempt 0) is
+  // generated and the program evaluated ONCE (shared_attempt_kernel); the
+  // candidates copy its inputs, tables and program outputs.
+  const uint32_t *shared_w;      // VM words [0, shared_len): inputs + pinned program outputs
+  const uint16_t *shared_tab;    // silu_p[p], silu_q[q], pow_w[q]
+  const uint32_t *shared_meta;   // [0] program ok on that stream, [1] omega
+  uint64_t shared_seed;
+  uint32_t shared_len;
 };
 
 struct EvalArgs {
@@ -79,4 +88,8 @@ struct EvalArgs {
 extern "C" int tpo_ff_launch_verify(const tpo_ff::VerifyArgs *a, int grid, size_t smem,
                                     cudaStream_t st, int nthreads);
 extern "C" int tpo_ff_launch_eval(const tpo_ff::EvalArgs *a, size_t smem, cudaStream_t st);
+// One CTA: attempt (seed, stream 0) of the program -> words / tables / meta.
+extern "C" int tpo_ff_launch_shared(const tpo_ff::VerifyArgs *a, uint64_t seed, size_t smem,
+                                    uint32_t *w_out, uint16_t *tab_out, uint32_t *meta,
+                                    cudaStream_t st);
 extern "C" int tpo_ff_verify_occupancy(size_t smem, int nthreads);

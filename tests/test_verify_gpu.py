@@ -202,3 +202,23 @@ def test_distinct_candidate_stream_matches_reference(ctx):
             for c in VCOLS:
                 assert got[c][k] == w[c], (fam, k, c)
         assert np.array_equal(acc, got["kind"] == 0)
+
+
+@pytest.mark.parametrize("fam", ["rmsnorm", "lora", "gqa"])
+def test_same_seed_batch_matches_reference(ctx, fam):
+    """A search loop verifies every candidate with the VerifyConfig seed:
+    the batch's first attempt (inputs, tables, program outputs) is computed
+    once and shared.  Verdicts stay bit-exact, including seeds whose first
+    attempt the program itself must resample (RMSNorm's sqrt)."""
+    prog, pool = FAMS[fam]
+    graphs = [g for _, g in pool]
+    cands = [graphs[i % len(graphs)] for i in range(96)]
+    for seed in range(6):
+        seeds = np.full(len(cands), seed, dtype=np.uint64)
+        for num_tests in (1, 2):
+            got, acc = ctx.verify_batch(prog, cands, seeds, num_tests=num_tests)
+            for k in range(0, len(cands), 5):
+                w = ref.random_test_equivalence(prog, cands[k], num_tests=num_tests, seed=seed)
+                for c in VCOLS:
+                    assert got[c][k] == w[c], (fam, seed, num_tests, k, c)
+            assert np.array_equal(acc, got["kind"] == 0)

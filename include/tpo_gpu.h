@@ -257,6 +257,12 @@ int tpo_gpu_plan_intervals(int32_t n, const int64_t *size, const int64_t *start,
 int tpo_gpu_describe(const char *json_in, int64_t smem_bytes, char *text_out, int64_t cap,
                      int64_t *needed);
 
+/* Debug / parity of the JSON fast path (host/fastjson.cpp): parses
+ * json_in with the fast path and with the generic parser; *fast_accepted =
+ * 1 if the fast path took it, *same = 1 if both give the identical graph.
+ * Returns the generic parser's status (1000 + ParseError on invalid text). */
+int tpo_gpu_parse_check(const char *json_in, int32_t *fast_accepted, int32_t *same);
+
 /* Reference op_madds work of a graph (SURVEY §8d verifier work unit). */
 int64_t tpo_gpu_op_madds(const tpo_gpu_graph *g);
 

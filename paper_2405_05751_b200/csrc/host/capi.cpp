@@ -481,15 +481,18 @@ namespace {
 
 // parse + validate (B200 limits) + fused match + VM footprint; throws
 tpo_gpu_graph *compile_one(const char *json) {
-  nlohmann::json j;
-  try {
-    j = nlohmann::json::parse(json);
-  } catch (const nlohmann::json::exception &e) {
-    throw Error(ErrCode::ParseError, e.what());
-  }
   auto h = std::make_unique<tpo_gpu_graph>();
   Graph &G = h->g;
-  G.g = ir::kernel_graph_from_json(j);
+  static const bool slow_only = std::getenv("TPO_JSON_SLOW") != nullptr;
+  if (slow_only || !ir::kernel_graph_from_text_fast(json, std::strlen(json), G.g)) {
+    nlohmann::json j;
+    try {
+      j = nlohmann::json::parse(json);
+    } catch (const nlohmann::json::exception &e) {
+      throw Error(ErrCode::ParseError, e.what());
+    }
+    G.g = ir::kernel_graph_from_json(j);
+  }
   ir::ValidityReport rep = ir::validate(G.g, ir::kB200Limits);
   if (!rep.valid()) {
     std::string msg;
@@ -1160,6 +1163,31 @@ extern "C" int tpo_gpu_describe(const char *json_in, int64_t smem_bytes, char *t
     const std::string str = tpo::gpu::describe(ir::kernel_graph_from_json(j), lim);
     if (needed) *needed = int64_t(str.size()) + 1;
     if (text_out && cap > int64_t(str.size())) std::memcpy(text_out, str.c_str(), str.size() + 1);
+    return 0;
+  });
+}
+
+// ----------------------------------------------- wire-format parity (debug)
+extern "C" int tpo_gpu_parse_check(const char *json_in, int32_t *fast_accepted, int32_t *same) {
+  return guard([&] {
+    ir::KernelGraph a;
+    const bool fast = ir::kernel_graph_from_text_fast(json_in, std::strlen(json_in), a);
+    if (fast_accepted) *fast_accepted = fast;
+    if (same) *same = 0;
+    nlohmann::json j;
+    try {
+      j = nlohmann::json::parse(json_in);
+    } catch (const nlohmann::json::exception &e) {
+      throw Error(ErrCode::ParseError, e.what());
+    }
+    const ir::KernelGraph b = ir::kernel_graph_from_json(j);
+    if (fast && same) {
+      bool eq = ir::to_json(a).dump() == ir::to_json(b).dump() && a.tensors.size() == b.tensors.size();
+      for (size_t t = 0; eq && t < a.tensors.size(); ++t)
+        eq = a.tensors[t].producer_op == b.tensors[t].producer_op &&
+             a.tensors[t].producer_out == b.tensors[t].producer_out;
+      *same = eq;
+    }
     return 0;
   });
 }

@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <vector>
 #include <algorithm>
+#include <map>
 #include <mutex>
 
 #include "../../../include/tpo_gpu.h"
@@ -97,13 +98,29 @@ KernelGraph lora_mugraph(int64_t b, int64_t h, int64_t n, int64_t r, int64_t gri
 }
 
 // `key`: canonical_key(g), computed once by the caller
+// canonical keys of the reference forms, memoised by (form, sizes): a
+// search stream matches thousands of candidates against the same few
 template <class F>
-bool same(const std::string &key, F &&build) {
-  try {
-    return key == canonical_key(build());
-  } catch (const Error &) {
-    return false;
+bool same(const std::string &key, const std::array<int64_t, 7> &form, F &&build) {
+  static std::mutex mu;
+  static std::map<std::array<int64_t, 7>, std::string> memo;
+  std::string want;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = memo.find(form);
+    if (it != memo.end()) want = it->second;
   }
+  if (want.empty()) {
+    try {
+      want = canonical_key(build());
+    } catch (const Error &) {
+      want = "-";  // not constructible: never matches
+    }
+    std::lock_guard<std::mutex> lk(mu);
+    if (memo.size() > 4096) memo.clear();
+    memo.emplace(form, want);
+  }
+  return key == want;
 }
 
 int env_int(const char *name, int dflt) {
@@ -152,7 +169,7 @@ FusedPlan match_fused(const KernelGraph &g) {
   if (in.size() == 4 && r2(0) && r2(1) && r2(2) && r2(3) && in[1].dims[0] == 1 &&
       in[3].dims == std::vector<int64_t>{1, 1}) {
     int64_t b = in[0].dims[0], h = in[0].dims[1], n = in[2].dims[1];
-    if (same(key, [&] { return rmsnorm_mugraph(b, h, n, grid, fl); })) {
+    if (same(key, {1, b, h, n, 0, grid, fl}, [&] { return rmsnorm_mugraph(b, h, n, grid, fl); })) {
       if (b > 8 || n % 128 || h % 64) {
         p.why = "RMSNorm µGraph outside kernel limits (b<=8, n%128, h%64)";
         return p;
@@ -164,7 +181,7 @@ FusedPlan match_fused(const KernelGraph &g) {
   }
   if (in.size() == 3 && r2(0) && r2(1) && r2(2)) {
     int64_t b = in[0].dims[0], h = in[0].dims[1], n = in[1].dims[1];
-    if (same(key, [&] { return gatedmlp_mugraph(b, h, n, grid, fl); })) {
+    if (same(key, {2, b, h, n, 0, grid, fl}, [&] { return gatedmlp_mugraph(b, h, n, grid, fl); })) {
       if (b > 8 || n % 128 || h % 64) {
         p.why = "GatedMLP µGraph outside kernel limits (b<=8, n%128, h%64)";
         return p;
@@ -176,7 +193,7 @@ FusedPlan match_fused(const KernelGraph &g) {
   }
   if (in.size() == 3 && in[0].rank() == 3 && in[1].rank() == 3 && in[2].rank() == 3) {
     int64_t G = in[0].dims[0], qh = in[0].dims[1], hd = in[0].dims[2], L = in[1].dims[2];
-    if (same(key, [&] { return gqa_mugraph(G, qh, hd, L, grid, fl); })) {
+    if (same(key, {3, G, qh, hd, L, grid, fl}, [&] { return gqa_mugraph(G, qh, hd, L, grid, fl); })) {
       if (qh > 8 || hd != 128 || L % 128) {
         p.why = "GQA µGraph outside kernel limits (qh<=8, hd==128, L%128)";
         return p;
@@ -188,7 +205,7 @@ FusedPlan match_fused(const KernelGraph &g) {
   }
   if (in.size() == 4 && r2(0) && r2(1) && r2(2) && r2(3)) {
     int64_t b = in[0].dims[0], h = in[0].dims[1], n = in[1].dims[1], r = in[2].dims[1];
-    if (same(key, [&] { return lora_mugraph(b, h, n, r, grid, fl); })) {
+    if (same(key, {4, b, h, n, r, grid, fl}, [&] { return lora_mugraph(b, h, n, r, grid, fl); })) {
       if (b > 16 || r != 16 || n % 128 || h % 64) {
         p.why = "LoRA µGraph outside kernel limits (b<=16, r==16, n%128, h%64)";
         return p;

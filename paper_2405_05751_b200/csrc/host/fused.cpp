@@ -471,11 +471,11 @@ int launch_fused(const FusedPlan &p, const void *const *in, const int32_t *dt, f
   // off for RMS only; GatedMLP / LoRA run one CTA per SM with deeper rings.
   int stages = env_int("TPO_STAGES", 0), minb = env_int("TPO_MINB", 0);
   const size_t kOnePerSm = 232448;
-  // RMS with static weights: two CTAs per SM (5-stage ring, <= 113 KB) so
+  // RMS / LoRA with static weights: two CTAs per SM (5-stage ring, <= 113 KB) so
   // the next evaluation's CTAs become resident and prefetch their weight
   // stages while this one drains (ring timeline, profiles/r01/ring_rms.txt:
   // 8.07 vs 8.63 us per evaluation).
-  if (stages <= 0 && minb <= 0 && mode == MODE_RMS && sp.prefetch_static) minb = 2;
+  if (stages <= 0 && minb <= 0 && mode != MODE_GATED && sp.prefetch_static) minb = 2;
   if (stages <= 0) {
     if (minb == 2) {
       for (int s : {5, 4, 3}) {
@@ -504,10 +504,11 @@ int launch_fused(const FusedPlan &p, const void *const *in, const int32_t *dt, f
   }
   sp.dbg_flags = env_int("TPO_DBG_FLAGS", 0);
   sp.epi_atomic = env_int("TPO_EPI_ATOMIC", 0);
-  // RMS, two CTAs per SM: the producer releases the next evaluation 5 k
-  // blocks before its last issue, so the next grid's weight prefetch
-  // overlaps this one's last stages (sweep: 7.59 vs 7.87 us)
-  sp.trig_early = env_int("TPO_TRIG_EARLY", mode == MODE_RMS && sp.prefetch_static && minb == 2 ? 5 : 0);
+  // two CTAs per SM: the producer releases the next evaluation a few k
+  // blocks before its last issue (RMS 5, LoRA 3), so the next grid's weight
+  // prefetch overlaps this one's last stages (sweeps: RMS 7.59 vs 7.87 us,
+  // LoRA 8.54 vs 8.84 us)
+  sp.trig_early = env_int("TPO_TRIG_EARLY", !sp.prefetch_static || minb != 2 ? 0 : mode == MODE_RMS ? 5 : 3);
   sp.pre_cut = env_int("TPO_PRE_CUT", 0);
   const int nct = int(p.n / 128) * sp.ksplit;
   unsigned long long *dbg = debug_begin(nct, st);

@@ -121,7 +121,9 @@ __global__ void __launch_bounds__(kThreads, MINB)
   constexpr int rows_per = kTileN / S;                                     // rows owned per CTA
   uint8_t *stages = smem;
   float *red = reinterpret_cast<float *>(stages + STAGES * C::kStage);
-  float *side = red + (S > 1 ? kTileN * 16 : 0);  // red: [S][rows_per][16] incoming row partials
+  // red: [S-1 peers][NV/4][rows_per][4] incoming row partials (peer slot:
+  // its rank, minus one above the owner's own)
+  float *side = red + (S > 1 ? (S - 1) * (kTileN / S) * 16 : 0);
   float *xa_tot = side + S * kSide;         // side: [S][kSide]; xa_tot: LoRA [16][16] (this CTA)
   float *xa_w = xa_tot + (MODE == MODE_LORA ? 256 : 0);  // LoRA: per-warp XA partials [4][16][16]
   Bars *bars = reinterpret_cast<Bars *>(xa_w + (MODE == MODE_LORA ? 1024 : 0));
@@ -498,7 +500,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
         const int lr = row - owner * rows_per;
 #pragma unroll
         for (int i = 0; i < NV; i += 4) {
-          const uint32_t dst = map_rank(red + ((int(rank) * (NV / 4) + i / 4) * rows_per + lr) * 4, owner);
+          const int slot = int(rank) < owner ? int(rank) : int(rank) - 1;
+          const uint32_t dst = map_rank(red + ((slot * (NV / 4) + i / 4) * rows_per + lr) * 4, owner);
           st_async4(dst, acc[i], acc[i + 1], acc[i + 2], acc[i + 3], mb);
         }
         if (threadIdx.x == 64) TPO_T(4);
@@ -510,7 +513,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
           if (rr == int(rank)) continue;
 #pragma unroll
           for (int i = 0; i < NV / 4; ++i) {
-            const float4 v = *reinterpret_cast<const float4 *>(red + ((rr * (NV / 4) + i) * rows_per + lr) * 4);
+            const int slot = rr < int(rank) ? rr : rr - 1;
+            const float4 v = *reinterpret_cast<const float4 *>(red + ((slot * (NV / 4) + i) * rows_per + lr) * 4);
             acc[4 * i] += v.x, acc[4 * i + 1] += v.y, acc[4 * i + 2] += v.z, acc[4 * i + 3] += v.w;
           }
         }
@@ -552,7 +556,7 @@ size_t skinny_smem(const SkinnyParams &p) {
   const int nkb = p.k_per_cta / kBK;
   (void)nkb;
   size_t b = size_t(STAGES) * C::kStage +
-             (S > 1 ? size_t(kTileN) * 16 * 4 : 0) + size_t(S) * C::kSide * 4 +
+             (S > 1 ? size_t(S - 1) * (kTileN / S) * 16 * 4 : 0) + size_t(S) * C::kSide * 4 +
              (MODE == MODE_LORA ? (256 + 1024) * 4 : 0) + sizeof(Bars);
   return b + 1024;
 }

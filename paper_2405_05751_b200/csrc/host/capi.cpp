@@ -272,7 +272,9 @@ void run_verify(Ctx &C, const Batch &bt, const tpo_verify_cfg &cfg, const tpo_fi
   check_cuda(cudaSetDevice(C.device), "cudaSetDevice");
   FieldState &fs = C.field(fpp.p, fpp.q, fpp.omega_base);
   const size_t code_bytes = size_t(bt.max_code) * sizeof(TpoVmInstr);
-  const size_t smem = fs.fc.table_bytes + code_bytes + size_t(bt.max_words) * 4;
+  // 16-bit VM words when both primes are below 256 (TPO_VM_WIDE keeps 32)
+  const int narrow = fs.fc.small && !std::getenv("TPO_VM_WIDE");
+  const size_t smem = fs.fc.table_bytes + code_bytes + size_t(bt.max_words) * (narrow ? 2 : 4);
   if (smem > 232448)
     throw Error(ErrCode::DoesNotFit,
                 "verifier working set " + std::to_string(smem) + " B exceeds 227 KiB of shared memory");
@@ -316,7 +318,7 @@ void run_verify(Ctx &C, const Batch &bt, const tpo_verify_cfg &cfg, const tpo_fi
       auto *sw = static_cast<uint32_t *>(C.shared_w.get(size_t(bt.cand_base) * 4 + 16));
       auto *stab = static_cast<uint16_t *>(C.shared_tab.get(size_t(fs.fc.p + 2 * fs.fc.q) * 2 + 16));
       auto *smeta = static_cast<uint32_t *>(C.shared_meta.get(16));
-      check_cuda(cudaError_t(tpo_ff_launch_shared(&a, r.seeds[0], smem, sw, stab, smeta, st)), "shared attempt");
+      check_cuda(cudaError_t(tpo_ff_launch_shared(&a, r.seeds[0], smem, sw, stab, smeta, narrow, st)), "shared attempt");
       a.shared_w = sw;
       a.shared_tab = stab;
       a.shared_meta = smeta;
@@ -343,11 +345,11 @@ void run_verify(Ctx &C, const Batch &bt, const tpo_verify_cfg &cfg, const tpo_fi
   // independent barrier domains per SM win: 8.6 vs 6.5 M cand/s measured);
   // TPO_VM_THREADS overrides
   int nthr = 256;
-  int occ = tpo_ff_verify_occupancy(smem, 256);
+  int occ = tpo_ff_verify_occupancy(smem, 256, narrow);
   {
     const char *e = std::getenv("TPO_VM_THREADS");
     const int forced = e ? std::atoi(e) : 0;
-    const int occ128 = tpo_ff_verify_occupancy(smem, 128);
+    const int occ128 = tpo_ff_verify_occupancy(smem, 128, narrow);
     if (forced == 128 || (forced == 0 && occ128 >= 2 * occ)) nthr = 128, occ = occ128;
   }
   if (occ < 1) throw Error(ErrCode::DoesNotFit, "verifier kernel does not fit on an SM");
@@ -359,7 +361,7 @@ void run_verify(Ctx &C, const Batch &bt, const tpo_verify_cfg &cfg, const tpo_fi
       if (I.op == VM_MATMUL) mm += double(I.n) * I.dims[5] * ((I.flags & VM_TILE22) ? 4 : 1);
     }
     std::fprintf(stderr, "[tpo vm] smem %zu occ256 %d occ128 %d instrs %.0f avg_n %.1f matmul_macs/instr %.1f\n", smem,
-                 tpo_ff_verify_occupancy(smem, 256), tpo_ff_verify_occupancy(smem, 128), cnt, sn / cnt, mm / cnt);
+                 tpo_ff_verify_occupancy(smem, 256, narrow), tpo_ff_verify_occupancy(smem, 128, narrow), cnt, sn / cnt, mm / cnt);
   }
   uint64_t grid = std::min<uint64_t>(uint64_t(C.num_sms) * uint64_t(occ), r.n);
   grid = std::max<uint64_t>(grid, 1);
@@ -382,7 +384,7 @@ void run_verify(Ctx &C, const Batch &bt, const tpo_verify_cfg &cfg, const tpo_fi
     cudaEventCreate(&ev1);
     cudaEventRecord(ev0, st);
   }
-  check_cuda(cudaError_t(tpo_ff_launch_verify(&a, int(grid), smem, st, nthr)), "verify launch");
+  check_cuda(cudaError_t(tpo_ff_launch_verify(&a, int(grid), smem, st, nthr, narrow)), "verify launch");
   if (dbg) {
     cudaEventRecord(ev1, st);
     cudaEventSynchronize(ev1);

@@ -9,7 +9,8 @@
 // random_test_equivalence (equiv.cpp:34-94) verdict, rounds_run, resamples
 // and witness bit-exactly.
 //
-// Field values are packed one per 32-bit word: xp | xq << 16.  q-definedness
+// Field values are packed one per word: xp | xq << 16 in 32 bits, or
+// xp | xq << 8 in 16 bits when p, q < 256 (Word<WT>).  q-definedness
 // is a static per-tensor property (lowering computes it), so the poison bit
 // is not stored; undefined q components are kept canonical (0) exactly as
 // the reference's default-constructed FFValue results (field.cpp:70-126).
@@ -56,14 +57,27 @@ __device__ __forceinline__ uint32_t mod64(uint64_t r, uint32_t n, uint32_t magic
   return mod32(hi * two32 + lo, n, magic);  // hi*two32 < n^2 < 2^32
 }
 
-struct Smem {
-  uint16_t *inv_p, *inv_q, *silu_p, *silu_q, *pow_w;
-  int16_t *sqrt_p, *sqrt_q;
-  uint32_t *w;  // VM words
+// A VM word packs one field value (xp, xq).  u32: xp | xq << 16 (any
+// p, q < 2^16); u16: xp | xq << 8 when p, q < 256 — half the shared memory
+// per candidate, so more candidates fit an SM (q-undefined words keep xq = 0).
+template <typename WT>
+struct Word {
+  static constexpr uint32_t kShift = sizeof(WT) == 2 ? 8 : 16;
+  static constexpr uint32_t kMask = sizeof(WT) == 2 ? 0xffu : 0xffffu;
+  __device__ static __forceinline__ WT pack(uint32_t p, uint32_t q) { return WT(p | (q << kShift)); }
 };
 
-__device__ __forceinline__ Smem carve(uint8_t *base, const FieldConst &f, uint32_t code_bytes = 0) {
-  Smem s;
+template <typename WT>
+struct SmemT {
+  uint16_t *inv_p, *inv_q, *silu_p, *silu_q, *pow_w;
+  int16_t *sqrt_p, *sqrt_q;
+  WT *w;  // VM words
+};
+using Smem = SmemT<uint32_t>;
+
+template <typename WT = uint32_t>
+__device__ __forceinline__ SmemT<WT> carve(uint8_t *base, const FieldConst &f, uint32_t code_bytes = 0) {
+  SmemT<WT> s;
   uint16_t *u = reinterpret_cast<uint16_t *>(base);
   s.inv_p = u;
   s.inv_q = s.inv_p + f.p;
@@ -72,11 +86,12 @@ __device__ __forceinline__ Smem carve(uint8_t *base, const FieldConst &f, uint32
   s.pow_w = s.silu_q + f.q;
   s.sqrt_p = reinterpret_cast<int16_t *>(s.pow_w + f.q);
   s.sqrt_q = s.sqrt_p + f.p;
-  s.w = reinterpret_cast<uint32_t *>(base + f.table_bytes + code_bytes);
+  s.w = reinterpret_cast<WT *>(base + f.table_bytes + code_bytes);
   return s;
 }
 
-__device__ void load_tables(const Smem &s, const FieldConst &f, const uint16_t *g_tables) {
+template <typename WT>
+__device__ void load_tables(const SmemT<WT> &s, const FieldConst &f, const uint16_t *g_tables) {
   // g_tables: inv_p[p], inv_q[q], sqrt_p[p], sqrt_q[q] (sqrt as int16 bits)
   for (uint32_t i = threadIdx.x; i < f.p; i += blockDim.x) {
     s.inv_p[i] = g_tables[i];
@@ -107,7 +122,8 @@ __device__ uint32_t seq_uniform(uint64_t &st, uint32_t n, uint64_t thr, uint32_t
 // Generate inputs, omega, SiLU tables and the omega power table for one
 // attempt.  Returns omega.  Draw order is sample_inputs (ffeval.cpp:29-40),
 // sample_omega (field.cpp:140-142), SiluTables::sample (ffeval.cpp:20-27).
-__device__ uint32_t gen_attempt(const Smem &s, const FieldConst &f, uint64_t seed, uint64_t stream,
+template <typename WT>
+__device__ uint32_t gen_attempt(const SmemT<WT> &s, const FieldConst &f, uint64_t seed, uint64_t stream,
                                 uint32_t n_in, bool silu, int *s_slow, uint32_t *s_omega) {
   const uint64_t st0 = derive_state(seed, stream);
   bool slow = false;
@@ -124,7 +140,7 @@ __device__ uint32_t gen_attempt(const Smem &s, const FieldConst &f, uint64_t see
       hmin = min(hmin, min(h1, h2));
       const uint32_t xp = mod64_small(h1, uint32_t(r1), f.p, f.magic_p, f.k24_p, f.k48_p);
       const uint32_t xq = mod64_small(h2, uint32_t(r2), f.q, f.magic_q, f.k24_q, f.k48_q);
-      s.w[e] = xp | (xq << 16);
+      s.w[e] = Word<WT>::pack(xp, xq);
     }
     slow = hmin == 0;
   } else {
@@ -134,7 +150,7 @@ __device__ uint32_t gen_attempt(const Smem &s, const FieldConst &f, uint64_t see
       slow |= (r1 < f.thr_p) | (r2 < f.thr_q);
       uint32_t xp = mod64(r1, f.p, f.magic_p, f.two32_p);
       uint32_t xq = mod64(r2, f.q, f.magic_q, f.two32_q);
-      s.w[e] = xp | (xq << 16);
+      s.w[e] = Word<WT>::pack(xp, xq);
     }
   }
   const uint64_t base = 2ull * n_in;  // next draw index
@@ -172,7 +188,7 @@ __device__ uint32_t gen_attempt(const Smem &s, const FieldConst &f, uint64_t see
       for (uint32_t e = 0; e < n_in; ++e) {
         uint32_t xp = seq_uniform(st, f.p, f.thr_p, f.magic_p, f.two32_p);
         uint32_t xq = seq_uniform(st, f.q, f.thr_q, f.magic_q, f.two32_q);
-        s.w[e] = xp | (xq << 16);
+        s.w[e] = Word<WT>::pack(xp, xq);
       }
       uint32_t k = seq_uniform(st, f.q, f.thr_q, f.magic_q, f.two32_q);
       uint32_t w = 1, b = f.wbase % f.p;
@@ -240,11 +256,12 @@ __device__ __forceinline__ void copy_code(TpoVmInstr *dst, const TpoVmInstr *src
 }
 
 // PROF: thread 0 accumulates clock64 per VM opcode into prof[op] (TPO_VM_PROFILE).
-template <bool PROF>
-__device__ bool run_program(const Smem &s, const FieldConst &f, const TpoVmInstr *code,
+template <bool PROF, typename WT>
+__device__ bool run_program(const SmemT<WT> &s, const FieldConst &f, const TpoVmInstr *code,
                             uint32_t len, int *s_flag, unsigned long long *prof) {
+  constexpr uint32_t QS = Word<WT>::kShift, PM = Word<WT>::kMask;
   uint32_t it = 0, loop_pc = 0, trips = 1;
-  uint32_t *W = s.w;
+  WT *W = s.w;
   const uint32_t p = f.p, q = f.q, mp = f.magic_p, mq = f.magic_q;
   long long t_prev = PROF ? clock64() : 0;
   for (uint32_t pc = 0; pc < len; ++pc) {
@@ -285,7 +302,7 @@ __device__ bool run_program(const Smem &s, const FieldConst &f, const TpoVmInstr
       case VM_UNARY: {
         for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
           uint32_t v = W[I.a + i];
-          uint32_t xp = v & 0xffffu, xq = v >> 16, rp = 0, rq = 0;
+          uint32_t xp = v & PM, xq = v >> QS, rp = 0, rq = 0;
           switch (I.sub) {
             case VM_EXP:
               rp = s.pow_w[xq];
@@ -297,11 +314,11 @@ __device__ bool run_program(const Smem &s, const FieldConst &f, const TpoVmInstr
             case VM_SQRT: {
               int32_t r = s.sqrt_p[xp];
               bad |= r < 0;
-              rp = uint32_t(r) & 0xffffu;
+              rp = uint32_t(r) & PM;
               if (qd) {
                 int32_t r2 = s.sqrt_q[xq];
                 bad |= r2 < 0;
-                rq = uint32_t(r2) & 0xffffu;
+                rq = uint32_t(r2) & PM;
               }
               break;
             }
@@ -310,7 +327,7 @@ __device__ bool run_program(const Smem &s, const FieldConst &f, const TpoVmInstr
               if (qd) rq = s.silu_q[xq];
               break;
           }
-          W[I.dst + i] = rp | (rq << 16);
+          W[I.dst + i] = Word<WT>::pack(rp, rq);
         }
         break;
       }
@@ -320,7 +337,7 @@ __device__ bool run_program(const Smem &s, const FieldConst &f, const TpoVmInstr
           bool wr = true;
           if (!flat) offsets(I, i, od, oa, ob, wr);
           uint32_t va = W[I.a + oa], vb = W[I.b + ob];
-          uint32_t ap = va & 0xffffu, aq = va >> 16, bp = vb & 0xffffu, bq = vb >> 16;
+          uint32_t ap = va & PM, aq = va >> QS, bp = vb & PM, bq = vb >> QS;
           uint32_t rp, rq = 0;
           switch (I.sub) {
             case VM_ADD:
@@ -344,7 +361,7 @@ __device__ bool run_program(const Smem &s, const FieldConst &f, const TpoVmInstr
               }
               break;
           }
-          W[I.dst + od] = rp | (rq << 16);
+          W[I.dst + od] = Word<WT>::pack(rp, rq);
         }
         break;
       }
@@ -368,10 +385,10 @@ __device__ bool run_program(const Smem &s, const FieldConst &f, const TpoVmInstr
           const uint32_t gx = fdiv(blk, I.dmul[3], I.dsh[3]), gr = blk - gx * I.dims[1] * I.dims[2];
           const uint32_t gy = fdiv(gr, I.dmul[4], I.dsh[4]), gz = gr - gy * I.dims[2];
           const uint32_t m = mt * tm, c = ct * tm;
-          const uint32_t *pa = W + int32_t(I.a + it * I.a_iter) + int32_t(gx) * I.sa[0] +
+          const WT *pa = W + int32_t(I.a + it * I.a_iter) + int32_t(gx) * I.sa[0] +
                                int32_t(gy) * I.sa[1] + int32_t(gz) * I.sa[2] + int32_t(bi) * I.sa[3] +
                                int32_t(m) * sma;
-          const uint32_t *pb = W + int32_t(I.b + it * I.b_iter) + int32_t(gx) * I.sb[0] +
+          const WT *pb = W + int32_t(I.b + it * I.b_iter) + int32_t(gx) * I.sb[0] +
                                int32_t(gy) * I.sb[1] + int32_t(gz) * I.sb[2] + int32_t(bi) * I.sb[3] +
                                int32_t(c) * snb;
           const uint32_t dbase = I.dst + ((blk * Bi + bi) * M + m) * N + c;
@@ -384,8 +401,8 @@ __device__ bool run_program(const Smem &s, const FieldConst &f, const TpoVmInstr
               for (uint32_t k = k0; k < k1; ++k) {
                 const uint32_t a0 = pa[int32_t(k) * ska], a1 = pa[int32_t(k) * ska + sma];
                 const uint32_t b0 = pb[int32_t(k) * skb], b1 = pb[int32_t(k) * skb + snb];
-                const uint32_t a0p = a0 & 0xffffu, a0q = a0 >> 16, a1p = a1 & 0xffffu, a1q = a1 >> 16;
-                const uint32_t b0p = b0 & 0xffffu, b0q = b0 >> 16, b1p = b1 & 0xffffu, b1q = b1 >> 16;
+                const uint32_t a0p = a0 & PM, a0q = a0 >> QS, a1p = a1 & PM, a1q = a1 >> QS;
+                const uint32_t b0p = b0 & PM, b0q = b0 >> QS, b1p = b1 & PM, b1q = b1 >> QS;
                 sp[0] += a0p * b0p, sq[0] += a0q * b0q;
                 sp[1] += a0p * b1p, sq[1] += a0q * b1q;
                 sp[2] += a1p * b0p, sq[2] += a1q * b0q;
@@ -403,12 +420,12 @@ __device__ bool run_program(const Smem &s, const FieldConst &f, const TpoVmInstr
               uint32_t accp = ap[j], accq = aq[j];
               if (I.flags & VM_ACCUM) {  // fused φ-Accum: acc = add(acc, A·B)
                 const uint32_t d = W[dbase + off[j]];
-                accp += d & 0xffffu;
+                accp += d & PM;
                 accp = accp >= p ? accp - p : accp;
-                accq += d >> 16;
+                accq += d >> QS;
                 accq = accq >= q ? accq - q : accq;
               }
-              W[dbase + off[j]] = accp | ((qd ? accq : 0u) << 16);
+              W[dbase + off[j]] = Word<WT>::pack(accp, qd ? accq : 0u);
             }
             continue;
           }
@@ -420,15 +437,15 @@ __device__ bool run_program(const Smem &s, const FieldConst &f, const TpoVmInstr
             for (; k + 2 <= k1; k += 2) {
               const uint32_t va0 = pa[int32_t(k) * ska], vb0 = pb[int32_t(k) * skb];
               const uint32_t va1 = pa[int32_t(k + 1) * ska], vb1 = pb[int32_t(k + 1) * skb];
-              p0 += (va0 & 0xffffu) * (vb0 & 0xffffu);
-              q0 += (va0 >> 16) * (vb0 >> 16);
-              p1 += (va1 & 0xffffu) * (vb1 & 0xffffu);
-              q1 += (va1 >> 16) * (vb1 >> 16);
+              p0 += (va0 & PM) * (vb0 & PM);
+              q0 += (va0 >> QS) * (vb0 >> QS);
+              p1 += (va1 & PM) * (vb1 & PM);
+              q1 += (va1 >> QS) * (vb1 >> QS);
             }
             if (k < k1) {
               const uint32_t va0 = pa[int32_t(k) * ska], vb0 = pb[int32_t(k) * skb];
-              p0 += (va0 & 0xffffu) * (vb0 & 0xffffu);
-              q0 += (va0 >> 16) * (vb0 >> 16);
+              p0 += (va0 & PM) * (vb0 & PM);
+              q0 += (va0 >> QS) * (vb0 >> QS);
             }
             // two partial sums of <= lazy/2 terms each: reduce before adding
             accp = mod32(accp + mod32(p0, p, mp) + mod32(p1, p, mp), p, mp);
@@ -436,12 +453,12 @@ __device__ bool run_program(const Smem &s, const FieldConst &f, const TpoVmInstr
           }
           if (I.flags & VM_ACCUM) {  // fused φ-Accum: acc = add(acc, A·B)
             const uint32_t d = W[dbase];
-            accp += d & 0xffffu;
+            accp += d & PM;
             accp = accp >= p ? accp - p : accp;
-            accq += d >> 16;
+            accq += d >> QS;
             accq = accq >= q ? accq - q : accq;
           }
-          W[dbase] = accp | ((qd ? accq : 0u) << 16);
+          W[dbase] = Word<WT>::pack(accp, qd ? accq : 0u);
         }
         break;
       }
@@ -451,7 +468,7 @@ __device__ bool run_program(const Smem &s, const FieldConst &f, const TpoVmInstr
         for (uint32_t o = threadIdx.x; o < n; o += blockDim.x) {
           const uint32_t t = fdiv(o, I.dmul[0], I.dsh[0]), in_i = o - t * inner;
           const uint32_t ou = fdiv(t, I.dmul[1], I.dsh[1]), m = t - ou * mid;
-          const uint32_t *pa = W + I.a + (ou * mid * grp + m * grp) * inner + in_i;
+          const WT *pa = W + I.a + (ou * mid * grp + m * grp) * inner + in_i;
           uint32_t accp = 0, accq = 0;
           for (uint32_t g0 = 0; g0 < grp; g0 += lazy) {
             const uint32_t g1 = min(grp, g0 + lazy);
@@ -459,13 +476,13 @@ __device__ bool run_program(const Smem &s, const FieldConst &f, const TpoVmInstr
 #pragma unroll 4
             for (uint32_t g = g0; g < g1; ++g) {
               const uint32_t v = pa[g * inner];
-              sp += v & 0xffffu;
-              sq += v >> 16;
+              sp += v & PM;
+              sq += v >> QS;
             }
             accp = mod32(accp + mod32(sp, p, mp), p, mp);
             accq = mod32(accq + mod32(sq, q, mq), q, mq);
           }
-          W[I.dst + o] = accp | ((qd ? accq : 0u) << 16);
+          W[I.dst + o] = Word<WT>::pack(accp, qd ? accq : 0u);
         }
         break;
       }
@@ -492,18 +509,19 @@ __device__ bool run_program(const Smem &s, const FieldConst &f, const TpoVmInstr
 // First mismatching (tensor, flat index) between two graphs' outputs, with
 // FFValue::operator== semantics (field.hpp:41-45): xq compared only when
 // both sides are q-defined.  Returns false if none.
-__device__ bool first_mismatch(const Smem &s, const TpoVmGraph &g1, const TpoVmGraph &g2,
+template <typename WT>
+__device__ bool first_mismatch(const SmemT<WT> &s, const TpoVmGraph &g1, const TpoVmGraph &g2,
                                unsigned long long *s_key, int *t_out, int64_t *i_out) {
   for (uint32_t t = 0; t < g1.n_out; ++t) {
     if (threadIdx.x == 0) *s_key = ~0ull;
     __syncthreads();
     const bool cmp_q = g1.out_qd[t] && g2.out_qd[t];
     const uint32_t n = g1.out_len[t];
-    const uint32_t *a = s.w + g1.out_off[t], *b = s.w + g2.out_off[t];
+    const WT *a = s.w + g1.out_off[t], *b = s.w + g2.out_off[t];
     unsigned long long best = ~0ull;
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
       uint32_t x = a[i], y = b[i];
-      bool ne = ((x ^ y) & 0xffffu) || (cmp_q && ((x ^ y) >> 16));
+      bool ne = ((x ^ y) & Word<WT>::kMask) || (cmp_q && ((x ^ y) >> Word<WT>::kShift));
       if (ne) {
         best = i;
         break;  // strided loop: first hit per thread is its minimum
@@ -524,7 +542,7 @@ __device__ bool first_mismatch(const Smem &s, const TpoVmGraph &g1, const TpoVmG
 
 // NT threads per candidate CTA: 256, or 128 when shared memory admits
 // twice as many resident candidates (more independent barrier domains).
-template <bool PROF, int NT>
+template <bool PROF, int NT, typename WT>
 __global__ void __launch_bounds__(NT) verify_kernel(VerifyArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int s_flag, s_slow;
@@ -533,7 +551,7 @@ __global__ void __launch_bounds__(NT) verify_kernel(VerifyArgs a) {
   __shared__ unsigned long long s_prof[32];  // PROF: [0,16) cycles per opcode, [16,32) counts
   if (PROF && threadIdx.x < 32) s_prof[threadIdx.x] = 0;
   const FieldConst &f = a.field;
-  Smem s = carve(smem, f, a.code_smem_bytes);
+  SmemT<WT> s = carve<WT>(smem, f, a.code_smem_bytes);
   load_tables(s, f, a.tables);
   const TpoVmGraph g1 = a.graphs[a.program];
   // bytecode staged in shared memory: the program once per CTA, each
@@ -590,7 +608,8 @@ __global__ void __launch_bounds__(NT) verify_kernel(VerifyArgs a) {
             ++v.resamples;
             continue;
           }
-          for (uint32_t i = threadIdx.x; i < a.shared_len; i += blockDim.x) s.w[i] = __ldg(a.shared_w + i);
+          const WT *sw = static_cast<const WT *>(a.shared_w);
+          for (uint32_t i = threadIdx.x; i < a.shared_len; i += blockDim.x) s.w[i] = sw[i];
           for (uint32_t i = threadIdx.x; i < f.p; i += blockDim.x) s.silu_p[i] = a.shared_tab[i];
           for (uint32_t i = threadIdx.x; i < f.q; i += blockDim.x) {
             s.silu_q[i] = a.shared_tab[f.p + i];
@@ -652,14 +671,15 @@ __global__ void __launch_bounds__(NT) verify_kernel(VerifyArgs a) {
 // Same-seed batches: attempt (seed, stream 0) of the program, once.  The
 // SiLU tables are always drawn: they follow the inputs and omega in the
 // stream, so drawing them changes nothing a SiLU-free pair reads.
+template <typename WT>
 __global__ void __launch_bounds__(kThreads) shared_attempt_kernel(VerifyArgs a, uint64_t seed,
-                                                                  uint32_t *w_out, uint16_t *tab_out,
+                                                                  WT *w_out, uint16_t *tab_out,
                                                                   uint32_t *meta) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int s_flag, s_slow;
   __shared__ uint32_t s_omega;
   const FieldConst &f = a.field;
-  Smem s = carve(smem, f, a.code_smem_bytes);
+  SmemT<WT> s = carve<WT>(smem, f, a.code_smem_bytes);
   load_tables(s, f, a.tables);
   const TpoVmGraph g1 = a.graphs[a.program];
   TpoVmInstr *scode = reinterpret_cast<TpoVmInstr *>(smem + f.table_bytes);
@@ -728,13 +748,19 @@ __global__ void __launch_bounds__(kThreads) eval_kernel(EvalArgs a) {
 }  // namespace tpo_ff
 
 extern "C" int tpo_ff_launch_verify(const tpo_ff::VerifyArgs *a, int grid, size_t smem,
-                                    cudaStream_t st, int nthreads) {
-  static int configured_for[4] = {-1, -1, -1, -1};
+                                    cudaStream_t st, int nthreads, int narrow) {
+  static int configured_for[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
   const bool prof = a->prof != nullptr;
   const bool small = nthreads == 128;
-  auto kern = prof ? (small ? tpo_ff::verify_kernel<true, 128> : tpo_ff::verify_kernel<true, 256>)
-                   : (small ? tpo_ff::verify_kernel<false, 128> : tpo_ff::verify_kernel<false, 256>);
-  const int slot = int(prof) * 2 + int(small);
+  using namespace tpo_ff;
+  void (*kern)(VerifyArgs);
+  if (narrow)
+    kern = prof ? (small ? verify_kernel<true, 128, uint16_t> : verify_kernel<true, 256, uint16_t>)
+                : (small ? verify_kernel<false, 128, uint16_t> : verify_kernel<false, 256, uint16_t>);
+  else
+    kern = prof ? (small ? verify_kernel<true, 128, uint32_t> : verify_kernel<true, 256, uint32_t>)
+                : (small ? verify_kernel<false, 128, uint32_t> : verify_kernel<false, 256, uint32_t>);
+  const int slot = int(prof) * 4 + int(small) * 2 + (narrow ? 1 : 0);
   if (int(smem) > configured_for[slot]) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     configured_for[slot] = int(smem);
@@ -744,11 +770,16 @@ extern "C" int tpo_ff_launch_verify(const tpo_ff::VerifyArgs *a, int grid, size_
 }
 
 extern "C" int tpo_ff_launch_shared(const tpo_ff::VerifyArgs *a, uint64_t seed, size_t smem,
-                                    uint32_t *w_out, uint16_t *tab_out, uint32_t *meta,
+                                    void *w_out, uint16_t *tab_out, uint32_t *meta, int narrow,
                                     cudaStream_t st) {
-  cudaFuncSetAttribute(tpo_ff::shared_attempt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       int(smem));
-  tpo_ff::shared_attempt_kernel<<<1, tpo_ff::kThreads, smem, st>>>(*a, seed, w_out, tab_out, meta);
+  using namespace tpo_ff;
+  if (narrow) {
+    cudaFuncSetAttribute(shared_attempt_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    shared_attempt_kernel<uint16_t><<<1, kThreads, smem, st>>>(*a, seed, static_cast<uint16_t *>(w_out), tab_out, meta);
+  } else {
+    cudaFuncSetAttribute(shared_attempt_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    shared_attempt_kernel<uint32_t><<<1, kThreads, smem, st>>>(*a, seed, static_cast<uint32_t *>(w_out), tab_out, meta);
+  }
   return int(cudaGetLastError());
 }
 
@@ -758,9 +789,11 @@ extern "C" int tpo_ff_launch_eval(const tpo_ff::EvalArgs *a, size_t smem, cudaSt
   return int(cudaGetLastError());
 }
 
-extern "C" int tpo_ff_verify_occupancy(size_t smem, int nthreads) {
+extern "C" int tpo_ff_verify_occupancy(size_t smem, int nthreads, int narrow) {
+  using namespace tpo_ff;
   int blocks = 0;
-  auto kern = nthreads == 128 ? tpo_ff::verify_kernel<false, 128> : tpo_ff::verify_kernel<false, 256>;
+  void (*kern)(VerifyArgs) = narrow ? (nthreads == 128 ? verify_kernel<false, 128, uint16_t> : verify_kernel<false, 256, uint16_t>)
+                                    : (nthreads == 128 ? verify_kernel<false, 128, uint32_t> : verify_kernel<false, 256, uint32_t>);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, nthreads == 128 ? 128 : 256, smem);
   return blocks;

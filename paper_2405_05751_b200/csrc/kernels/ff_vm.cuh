@@ -60,7 +60,7 @@ struct VerifyArgs {
   // VerifyConfig seed): attempt (shared_seed, round 0, attempt 0) is
   // generated and the program evaluated ONCE (shared_attempt_kernel); the
   // candidates copy its inputs, tables and program outputs.
-  const uint32_t *shared_w;      // VM words [0, shared_len): inputs + pinned program outputs
+  const void *shared_w;          // VM words [0, shared_len): inputs + pinned program outputs
   const uint16_t *shared_tab;    // silu_p[p], silu_q[q], pow_w[q]
   const uint32_t *shared_meta;   // [0] program ok on that stream, [1] omega
   uint64_t shared_seed;
@@ -85,11 +85,12 @@ struct EvalArgs {
 
 }  // namespace tpo_ff
 
+// narrow: 16-bit VM words (p, q < 256)
 extern "C" int tpo_ff_launch_verify(const tpo_ff::VerifyArgs *a, int grid, size_t smem,
-                                    cudaStream_t st, int nthreads);
+                                    cudaStream_t st, int nthreads, int narrow);
 extern "C" int tpo_ff_launch_eval(const tpo_ff::EvalArgs *a, size_t smem, cudaStream_t st);
 // One CTA: attempt (seed, stream 0) of the program -> words / tables / meta.
 extern "C" int tpo_ff_launch_shared(const tpo_ff::VerifyArgs *a, uint64_t seed, size_t smem,
-                                    uint32_t *w_out, uint16_t *tab_out, uint32_t *meta,
+                                    void *w_out, uint16_t *tab_out, uint32_t *meta, int narrow,
                                     cudaStream_t st);
-extern "C" int tpo_ff_verify_occupancy(size_t smem, int nthreads);
+extern "C" int tpo_ff_verify_occupancy(size_t smem, int nthreads, int narrow);

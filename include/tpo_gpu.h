@@ -263,6 +263,17 @@ int tpo_gpu_describe(const char *json_in, int64_t smem_bytes, char *text_out, in
  * Returns the generic parser's status (1000 + ParseError on invalid text). */
 int tpo_gpu_parse_check(const char *json_in, int32_t *fast_accepted, int32_t *same);
 
+/* Fused-kernel candidate generator (first slice of the reference's absent
+ * generator.cpp): single-GraphDef µGraphs for a
+ * single-output computation graph, by enumerating grid / for-loop
+ * partitions of its dimension labels and placing φ-Accums by partition
+ * state (tpo/ir/generator.hpp).  config_json (nullable): {"grids": [..],
+ * "loops": [..], "rewrite": bool, "max_candidates": n, "smem_bytes": n}.
+ * Output JSON: {"candidates": [graph, ...], "stats": {...}}; every candidate
+ * passes validate; equivalence is the verifier's job. */
+int tpo_gpu_generate(const char *program_json, const char *config_json, char *json_out, int64_t cap,
+                     int64_t *needed);
+
 /* Reference op_madds work of a graph (SURVEY §8d verifier work unit). */
 int64_t tpo_gpu_op_madds(const tpo_gpu_graph *g);
 

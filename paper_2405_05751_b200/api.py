@@ -70,6 +70,25 @@ def plan_block_graphs(g, smem_bytes: int = 0, elem_size: int = 2) -> dict:
     return json.loads(buf.value.decode())
 
 
+def generate(program, grids=None, loops=None, rewrite: bool = True, max_candidates: int = 4096,
+             with_stats: bool = False):
+    """Fused-kernel candidates for a computation graph (``tpo_gpu_generate``):
+    single-GraphDef µGraphs over grid / for-loop partitions, each valid under
+    B200 limits; equivalence is left to the verifier."""
+    cfg = {"rewrite": rewrite, "max_candidates": max_candidates}
+    if grids is not None:
+        cfg["grids"] = list(grids)
+    if loops is not None:
+        cfg["loops"] = list(loops)
+    cj = json.dumps(cfg).encode()
+    need = C.c_int64(0)
+    N.check(N.lib().tpo_gpu_generate(_js(program), cj, None, 0, C.byref(need)))
+    buf = C.create_string_buffer(int(need.value))
+    N.check(N.lib().tpo_gpu_generate(_js(program), cj, buf, need.value, C.byref(need)))
+    res = json.loads(buf.value.decode())
+    return (res["candidates"], res["stats"]) if with_stats else res["candidates"]
+
+
 def describe(g, smem_bytes: int = 0) -> str:
     """SPEC describe: pseudo-kernel listing of ``g`` plus
     its B200 execution (``tpo_gpu_describe``)."""

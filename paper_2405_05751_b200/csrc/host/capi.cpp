@@ -1193,3 +1193,40 @@ extern "C" int tpo_gpu_parse_check(const char *json_in, int32_t *fast_accepted, 
     return 0;
   });
 }
+
+// ------------------------------------------------------------- generator
+#include "tpo/ir/generator.hpp"
+
+extern "C" int tpo_gpu_generate(const char *program_json, const char *config_json, char *json_out,
+                                int64_t cap, int64_t *needed) {
+  return guard([&] {
+    nlohmann::json j, c;
+    try {
+      j = nlohmann::json::parse(program_json);
+      c = config_json && *config_json ? nlohmann::json::parse(config_json) : nlohmann::json::object();
+    } catch (const nlohmann::json::exception &e) {
+      throw Error(ErrCode::ParseError, e.what());
+    }
+    ir::GenConfig cfg;
+    if (c.contains("grids")) cfg.grids = c.at("grids").get<std::vector<int64_t>>();
+    if (c.contains("loops")) cfg.loops = c.at("loops").get<std::vector<int64_t>>();
+    if (c.contains("rewrite")) cfg.rewrite = c.at("rewrite").get<bool>();
+    if (c.contains("max_candidates")) cfg.max_candidates = c.at("max_candidates").get<size_t>();
+    if (c.contains("smem_bytes")) cfg.limits.smem_bytes = c.at("smem_bytes").get<int64_t>();
+    ir::GenStats st;
+    const auto cands = ir::generate_fused(ir::kernel_graph_from_json(j), cfg, &st);
+    nlohmann::json arr = nlohmann::json::array();
+    for (const auto &g : cands) arr.push_back(ir::to_json(g));
+    const std::string s = nlohmann::json{{"candidates", arr},
+                                         {"stats",
+                                          {{"partitions", st.partitions},
+                                           {"placements", st.placements},
+                                           {"rejected_structure", st.rejected_structure},
+                                           {"rejected_validate", st.rejected_validate},
+                                           {"duplicates", st.duplicates}}}}
+                              .dump();
+    if (needed) *needed = int64_t(s.size()) + 1;
+    if (json_out && cap > int64_t(s.size())) std::memcpy(json_out, s.c_str(), s.size() + 1);
+    return 0;
+  });
+}

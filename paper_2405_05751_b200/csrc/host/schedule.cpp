@@ -159,12 +159,24 @@ MemoryPlan plan_intervals(const std::vector<Lifetime> &buf, int exhaustive_max) 
 MemoryPlan plan_memory(const BlockGraph &bg, const Schedule &sched, const MemLimits &limits) {
   const size_t nt = bg.tensors.size();
   const std::vector<char> reg = register_resident(bg);
+  // lifetimes in barrier phases, not positions: ops of one depth run
+  // without a sync between them, so a buffer read in a phase may not be
+  // reused by a write in that same phase
+  std::vector<int> phase_of(sched.order.size(), 0);
+  {
+    int ph = 0;
+    size_t k = 0;
+    for (size_t p = 0; p < sched.order.size(); ++p) {
+      phase_of[p] = ph;
+      if (k < sched.sync_after.size() && sched.sync_after[k] == int(p)) ++ph, ++k;
+    }
+  }
   std::vector<int> pos(bg.ops.size(), -1);
-  for (size_t p = 0; p < sched.order.size(); ++p) pos[size_t(sched.order[p])] = int(p);
-  int loop_end = -1;  // last position of the for-loop body
+  for (size_t p = 0; p < sched.order.size(); ++p) pos[size_t(sched.order[p])] = phase_of[p];
+  int loop_end = -1;  // last phase of the for-loop body
   for (size_t p = 0; p < sched.order.size(); ++p)
     if (!sched.post[size_t(sched.order[p])] && bg.ops[size_t(sched.order[p])].type != OpType::OutSaver)
-      loop_end = int(p);
+      loop_end = phase_of[p];
   std::vector<int64_t> start(nt, -1), end(nt, -1);
   for (const Op &op : bg.ops) {
     const int p = pos[size_t(op.id)];

@@ -57,8 +57,9 @@ MemoryPlan plan_intervals(const std::vector<Lifetime> &buf, int exhaustive_max =
 // Shared-memory plan of one block graph under `sched`: one buffer per
 // block tensor outside the register-resident interior edges of its thread
 // groups (validate.cpp:115-140 accounting), elem_size bytes per element.
-// Lifetimes run from the producer's position to the last consumer's;
-// accumulators are live over the whole for-loop body.  Throws
+// Lifetimes run from the producer's barrier phase (depth level) to the last
+// consumer's — ops of one phase run without a sync between them, so their
+// buffers may not alias — and accumulators are live over the whole loop body.  Throws
 // Error(DoesNotFit) when the optimal peak exceeds limits.smem_bytes.
 MemoryPlan plan_memory(const BlockGraph &bg, const Schedule &sched, const MemLimits &limits);
 

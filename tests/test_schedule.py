@@ -217,3 +217,36 @@ def test_does_not_fit():
     with pytest.raises(N.NativeError) as e:
         api.plan_block_graphs(g, smem_bytes=64)
     assert e.value.status == 1000 + int(ErrCode.DoesNotFit)
+
+
+def test_plan_respects_barrier_phases():
+    """Ops of one depth run without a sync between them: buffers whose
+    lifetimes meet in a phase never share bytes."""
+    for fam in ("rmsnorm", "gatedmlp", "gqa", "lora"):
+        for _, g in F.verify_families()[fam][1][:12]:
+            bg = _block(g)
+            p = _plan(g)[0]
+            phase, ph, k = {}, 0, 0
+            for pos, op in enumerate(p["order"]):
+                phase[op] = ph
+                if k < len(p["sync_after"]) and p["sync_after"][k] == pos:
+                    ph, k = ph + 1, k + 1
+            loop_end = max((phase[o] for o in p["order"] if not p["post"][o]
+                            and bg["ops"][o]["type"] != "outsaver"), default=0)
+            span = {}
+            for o, op in enumerate(bg["ops"]):
+                for t in op["outputs"]:
+                    s0 = 0 if op["type"] == "accum" else phase[o]
+                    e0 = loop_end if op["type"] == "accum" else phase[o]
+                    lo, hi = span.get(t, (s0, e0))
+                    span[t] = (min(lo, s0), max(hi, e0))
+                for t in op["inputs"]:
+                    lo, hi = span.get(t, (phase[o], phase[o]))
+                    span[t] = (lo, max(hi, phase[o]))
+            sizes = {t["id"]: 2 * _numel(t["shape"]) for t in bg["tensors"]}
+            live = [t for t in span if p["offset"][t] >= 0]
+            for i, a in enumerate(live):
+                for b in live[i + 1:]:
+                    if span[a][0] <= span[b][1] and span[b][0] <= span[a][1]:
+                        oa, ob = p["offset"][a], p["offset"][b]
+                        assert oa + sizes[a] <= ob or ob + sizes[b] <= oa, (fam, a, b)

@@ -241,3 +241,17 @@ def test_generated_candidates_verify_on_gpu(ctx):
             for c in VCOLS:
                 assert got[c][k] == w[c], (fam, k, c)
         assert (got["kind"] != 1).all()
+
+
+def test_optimize_pipeline(ctx):
+    """generate -> verify -> stability -> select (SPEC Fig. 1 flow) on the
+    GPU: stage counts non-increasing, the winner is one fused kernel that the
+    reference verifies Equivalent."""
+    from paper_2405_05751_b200 import pipeline
+    prog, _ = FAMS["gatedmlp"]
+    rep = pipeline.optimize(ctx, prog, grids=[1, 2, 4, 8, 16], loops=[1, 2, 4, 8, 16])
+    assert rep["generated"] >= rep["compiled"] >= rep["verified"] >= rep["stable"] > 0
+    best = rep["best"]
+    assert [op["type"] for op in best["ops"]] == ["graphdef"]
+    assert ref.random_test_equivalence(prog, best, num_tests=4, seed=5)["kind"] == 0
+    assert "forloop" in rep["describe"]

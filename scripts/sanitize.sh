@@ -1,0 +1,42 @@
+# compute-sanitizer over the kernels (GPU box): racecheck + synccheck on
+# shared memory for the verifier VM (barrier phases), the fp VM and the
+# stability kernel; memcheck on the fused kernels.  Small shapes.
+CS=/usr/local/cuda/bin/compute-sanitizer
+OUT=gpurun_out/sanitize; mkdir -p $OUT
+cat > /tmp/san_verify.py <<'PY'
+import sys; sys.path.insert(0, '.')
+import numpy as np
+from paper_2405_05751_b200 import fixtures as F
+from paper_2405_05751_b200.api import Context
+ctx = Context(0)
+for fam, (prog, pool) in F.verify_families().items():
+    gs = [g for _, g in pool]
+    ctx.verify_pool(prog, gs, first=0, n=64, want_verdicts=True)
+    ctx.verify_batch(prog, gs[:40], np.zeros(40, dtype=np.uint64))     # same-seed shared attempt
+    ctx.stability_batch(prog, gs[:8])
+print("ok")
+PY
+cat > /tmp/san_fused.py <<'PY'
+import sys; sys.path.insert(0, '.'); sys.path.insert(0, 'tests')
+import numpy as np, torch
+from paper_2405_05751_b200 import fixtures as F
+from paper_2405_05751_b200.api import Context
+from test_fused_gpu import make_inputs
+ctx = Context(0)
+for name, args, grid, fl in [("gatedmlp", (8, 512, 256), 2, 4), ("rmsnorm", (8, 512, 256), 2, 4),
+                             ("lora", (16, 512, 256, 16), 2, 4), ("gqa", (4, 8, 128, 512), 2, 4)]:
+    mu = F.family_mugraph(name, *args, grid=grid, forloop=fl)
+    g = ctx.compile(mu)
+    ins = [x.cuda() for x in make_inputs(name, args)]
+    ctx.eval_mugraph(g, ins); torch.cuda.synchronize()
+    g.set_static_inputs({"gatedmlp": [1, 2], "rmsnorm": [1, 2, 3], "lora": [1, 2, 3], "gqa": []}[name])
+    for _ in range(3): ctx.eval_mugraph(g, ins)
+    torch.cuda.synchronize()
+prog, mu = F.bench_pair("rmsnorm")
+print("ok")
+PY
+timeout 1200 $CS --tool racecheck --racecheck-report hazard python /tmp/san_verify.py > $OUT/racecheck_verify.txt 2>&1
+timeout 1200 $CS --tool synccheck python /tmp/san_verify.py > $OUT/synccheck_verify.txt 2>&1
+timeout 1200 $CS --tool memcheck python /tmp/san_verify.py > $OUT/memcheck_verify.txt 2>&1
+timeout 1200 $CS --tool memcheck python /tmp/san_fused.py > $OUT/memcheck_fused.txt 2>&1
+timeout 1200 $CS --tool racecheck --racecheck-report hazard python /tmp/san_fused.py > $OUT/racecheck_fused.txt 2>&1

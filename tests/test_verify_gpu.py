@@ -255,3 +255,24 @@ def test_optimize_pipeline(ctx):
     assert [op["type"] for op in best["ops"]] == ["graphdef"]
     assert ref.random_test_equivalence(prog, best, num_tests=4, seed=5)["kind"] == 0
     assert "forloop" in rep["describe"]
+
+
+def test_rejection_rate_and_no_false_negatives(ctx):
+    """SPEC acceptance: over 1000 seeds, >= 99% rejection
+    of non-equivalent pairs at num_tests=4 (20 mutant pairs, 5 per family;
+    Inconclusive verdicts — exhausted sqrt resampling, ~1% for RMSNorm,
+    identical in the reference — are excluded) and no false negatives for
+    the equivalent variants.""" 
+    for fam in ("rmsnorm", "gatedmlp", "gqa", "lora"):
+        prog, pool = FAMS[fam]
+        muts = [g for tag, g in pool if tag.endswith("/mut")][:5]
+        eqs = [g for tag, g in pool if tag.endswith("/eq")][:5]
+        seeds = np.arange(1000, dtype=np.uint64)
+        for g in muts:
+            got, acc = ctx.verify_batch(prog, [g] * 1000, seeds, num_tests=4)
+            assert not acc.any(), fam  # never accepted
+            decided = got["kind"] != 2  # Inconclusive: sqrt resampling exhausted (~1% for RMSNorm)
+            assert (got["kind"][decided] == 1).mean() >= 0.99 and decided.mean() >= 0.97, fam
+        for g in eqs:
+            got, acc = ctx.verify_batch(prog, [g] * 1000, seeds, num_tests=4)
+            assert not (got["kind"] == 1).any(), fam  # Equivalent or (sqrt) Inconclusive, never rejected

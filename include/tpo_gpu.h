@@ -135,8 +135,10 @@ int tpo_gpu_validate(const char *graph_json, int64_t smem_bytes, int64_t elem_si
 
 /* Floating-point µGraph evaluation on device buffers (row-major, caller
  * owns).  Inputs are TPO_DTYPE_BF16 or _F32 per `in_dtype`; outputs fp32.
- * Benchmark µGraphs run as one fused sm_100a kernel (fused_kind != 0),
- * enqueued on `cuda_stream` (NULL = the legacy default stream); asynchronous. */
+ * Benchmark µGraphs run as one fused sm_100a kernel (fused_kind != 0; bf16
+ * operands, fp32 accumulation); any other µGraph runs on the generic GPU VM
+ * in the reference's fp32 semantics (eval_mugraph_f32, interp.hpp:51-53).
+ * Enqueued on `cuda_stream` (NULL = the legacy default stream); asynchronous. */
 int tpo_gpu_eval_mugraph(tpo_gpu_ctx *ctx, const tpo_gpu_graph *g, const void *const *in_dev,
                          const int32_t *in_dtype, float *const *out_dev, void *cuda_stream);
 

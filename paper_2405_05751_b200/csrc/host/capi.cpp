@@ -606,12 +606,56 @@ int tpo_gpu_validate(const char *json, int64_t smem_bytes, int64_t elem_size, ch
 
 int64_t tpo_gpu_op_madds(const tpo_gpu_graph *g) { return g->g.madds; }
 
+}  // extern "C"
+
+extern "C" int tpo_convert_bf16_f32(const void *in, float *out, size_t n, int num_sms, cudaStream_t st);
+
+namespace {
+int eval_vm_impl(tpo_gpu_ctx *ctx, const tpo_gpu_graph *h, int32_t mode, const void *in, void *out,
+                 bool host, cudaStream_t stream);
+
+// A µGraph without a hand-written kernel: the generic VM in the reference's
+// fp32 semantics (eval_mugraph_f32, interp.hpp:51-53) on the device —
+// inputs widened to fp32 into one contiguous buffer, outputs copied out.
+void eval_generic_dev(tpo_gpu_ctx *ctx, const tpo_gpu_graph *h, const void *const *in_dev,
+                      const int32_t *in_dtype, float *const *out_dev, cudaStream_t st) {
+  Ctx &C = ctx->c;
+  const Graph &G = h->g;
+  float *vin = static_cast<float *>(C.vm_in.get(size_t(G.in_elems) * 4 + 16));
+  float *vout = static_cast<float *>(C.vm_out.get(size_t(G.out_elems) * 4 + 16));
+  size_t off = 0;
+  for (size_t i = 0; i < G.g.inputs.size(); ++i) {
+    const size_t n = size_t(G.g.tensor(G.g.inputs[i]).shape.elem_count());
+    if (in_dtype[i] == TPO_DTYPE_F32)
+      check_cuda(cudaMemcpyAsync(vin + off, in_dev[i], n * 4, cudaMemcpyDeviceToDevice, st), "in");
+    else if (in_dtype[i] == TPO_DTYPE_BF16)
+      check_cuda(cudaError_t(tpo_convert_bf16_f32(in_dev[i], vin + off, n, C.num_sms, st)), "bf16->f32");
+    else
+      throw Error(ErrCode::Unsupported, "input dtype must be TPO_DTYPE_BF16 or TPO_DTYPE_F32");
+    off += n;
+  }
+  const int rc = eval_vm_impl(ctx, h, 2, vin, vout, false, st);
+  if (rc) throw Error(ErrCode::Unsupported, "generic VM: " + std::string(tpo_gpu_last_error()));
+  off = 0;
+  for (size_t o = 0; o < G.g.outputs.size(); ++o) {
+    const size_t n = size_t(G.g.tensor(G.g.outputs[o]).shape.elem_count());
+    check_cuda(cudaMemcpyAsync(out_dev[o], vout + off, n * 4, cudaMemcpyDeviceToDevice, st), "out");
+    off += n;
+  }
+}
+}  // namespace
+
+extern "C" {
+
 int tpo_gpu_eval_mugraph(tpo_gpu_ctx *ctx, const tpo_gpu_graph *h, const void *const *in_dev,
                          const int32_t *in_dtype, float *const *out_dev, void *stream) {
   return guard([&] {
     const Graph &G = h->g;
-    if (!G.plan.kind)
-      throw Error(ErrCode::Unsupported, "no fused sm_100a kernel for this µGraph: " + G.plan.why);
+    if (!G.plan.kind) {
+      check_cuda(cudaSetDevice(ctx->c.device), "cudaSetDevice");
+      eval_generic_dev(ctx, h, in_dev, in_dtype, out_dev, static_cast<cudaStream_t>(stream));
+      return 0;
+    }
     check_cuda(cudaSetDevice(ctx->c.device), "cudaSetDevice");
     size_t wsb = fused_workspace_bytes(G.plan);
     void *ws = wsb ? ctx->c.ws.get(wsb) : nullptr;
@@ -630,8 +674,6 @@ int tpo_gpu_eval_mugraph_host(tpo_gpu_ctx *ctx, const tpo_gpu_graph *h, const vo
   return guard([&] {
     Ctx &C = ctx->c;
     const Graph &G = h->g;
-    if (!G.plan.kind)
-      throw Error(ErrCode::Unsupported, "no fused sm_100a kernel for this µGraph: " + G.plan.why);
     check_cuda(cudaSetDevice(C.device), "cudaSetDevice");
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : C.stream;
     const size_t ni = G.g.inputs.size(), no = G.g.outputs.size();
@@ -647,6 +689,11 @@ int tpo_gpu_eval_mugraph_host(tpo_gpu_ctx *ctx, const tpo_gpu_graph *h, const vo
       } else if (in_dtype[i] == TPO_DTYPE_F32) {
         void *f = C.h_stage[i].get(n * 4);
         check_cuda(cudaMemcpyAsync(f, in_host[i], n * 4, cudaMemcpyHostToDevice, st), "H2D");
+        if (!G.plan.kind) {  // the generic VM takes fp32 as is
+          din[i] = f;
+          ddt[i] = TPO_DTYPE_F32;
+          continue;
+        }
         check_cuda(cudaError_t(tpo_convert_f32_bf16(static_cast<const float *>(f), d, n, C.num_sms, st)),
                    "f32->bf16");
       } else {
@@ -658,8 +705,12 @@ int tpo_gpu_eval_mugraph_host(tpo_gpu_ctx *ctx, const tpo_gpu_graph *h, const vo
     for (size_t o = 0; o < no; ++o)
       dout[o] = static_cast<float *>(
           C.h_out[o].get(size_t(G.g.tensor(G.g.outputs[o]).shape.elem_count()) * 4));
-    int e = launch_fused(G.plan, din.data(), ddt.data(), dout.data(), nullptr, 0, st);
-    if (e) return fail(3000 + e, std::string("fused launch: ") + cudaGetErrorString(cudaError_t(e)));
+    if (G.plan.kind) {
+      int e = launch_fused(G.plan, din.data(), ddt.data(), dout.data(), nullptr, 0, st);
+      if (e) return fail(3000 + e, std::string("fused launch: ") + cudaGetErrorString(cudaError_t(e)));
+    } else {
+      eval_generic_dev(ctx, h, din.data(), ddt.data(), dout.data(), st);
+    }
     for (size_t o = 0; o < no; ++o)
       check_cuda(cudaMemcpyAsync(out_host[o], dout[o],
                                  size_t(G.g.tensor(G.g.outputs[o]).shape.elem_count()) * 4,

@@ -42,6 +42,7 @@ struct Ctx {
   std::map<uint64_t, std::unique_ptr<FieldState>> fields;
   DevBuf code, graphs, pool, cand, seeds, verdicts, accept, counter, out, status, inputs, ws;
   DevBuf shared_w, shared_tab, shared_meta;  // same-seed verification batches
+  DevBuf vm_in, vm_out;                       // generic-VM evaluation of unfused µGraphs
   // host-buffer fp evaluation (tpo_gpu_eval_mugraph_host): per-input device
   // copies (bf16), fp32 staging for converted inputs, per-output buffers
   std::vector<DevBuf> h_in, h_stage, h_out;

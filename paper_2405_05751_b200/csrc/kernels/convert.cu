@@ -34,3 +34,21 @@ extern "C" int tpo_convert_f32_bf16(const float *in, void *out, size_t n, int nu
   f32_to_bf16<<<grid, 256, 0, st>>>(in, static_cast<__nv_bfloat16 *>(out), n);
   return int(cudaGetLastError());
 }
+
+// bf16 -> fp32 (exact), for the generic-VM evaluation of µGraphs without a
+// fused kernel.
+namespace {
+__global__ void __launch_bounds__(256) bf16_to_f32(const __nv_bfloat16 *__restrict__ in,
+                                                    float *__restrict__ out, size_t n) {
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+    out[i] = __bfloat162float(in[i]);
+}
+}  // namespace
+
+extern "C" int tpo_convert_bf16_f32(const void *in, float *out, size_t n, int num_sms, cudaStream_t st) {
+  if (!n) return 0;
+  const size_t want = (n + 255) / 256;
+  const int grid = int(want < size_t(num_sms) * 8 ? want : size_t(num_sms) * 8);
+  bf16_to_f32<<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16 *>(in), out, n);
+  return int(cudaGetLastError());
+}

@@ -121,3 +121,29 @@ def test_eval_mugraph_host_buffers(ctx, name):
     pageable = ctx.eval_mugraph_host(g, ins)[0]
     f32 = ctx.eval_mugraph_host(g, [x.float() for x in ins])[0]
     assert torch.equal(dev, pinned) and torch.equal(dev, pageable) and torch.equal(dev, f32)
+
+
+def test_unfused_mugraphs_run_on_the_generic_vm(ctx):
+    """eval_mugraph is total: a µGraph with no hand-written kernel (pool
+    variants at verification shapes, a GatedMLP outside the kernel's limits)
+    runs on the generic GPU VM in the reference's fp32 semantics."""
+    for fam in ("rmsnorm", "gqa", "lora"):
+        prog, pool = F.verify_families()[fam]
+        for tag, g in pool[:6]:
+            cg = ctx.compile(g)
+            assert not cg.fused
+            shapes = cg.shapes(False)
+            gen = torch.Generator().manual_seed(1)
+            ins = [(torch.rand(s, generator=gen) + 0.5).to(torch.bfloat16) for s in shapes]
+            out = ctx.eval_mugraph(cg, [x.cuda() for x in ins])[0].cpu().numpy()
+            want = ref.eval_mugraph(g, [x.float().numpy() for x in ins], mode=2)[0]
+            assert np.allclose(out, want, rtol=1e-5, atol=1e-6), tag
+            host = ctx.eval_mugraph_host(cg, [x.float() for x in ins])[0].numpy()
+            assert np.allclose(host, want, rtol=1e-5, atol=1e-6), tag
+    args = (16, 256, 192)  # 16 tokens, 192 columns: outside the skinny kernel's limits
+    mu = F.family_mugraph("gatedmlp", *args, grid=2, forloop=4)
+    g = ctx.compile(mu)
+    assert not g.fused
+    ins = make_inputs("gatedmlp", args)
+    out = ctx.eval_mugraph(g, [x.cuda() for x in ins])[0].cpu().numpy()
+    check(out, ref.eval_mugraph(mu, [x.float().numpy() for x in ins])[0])

@@ -1103,12 +1103,55 @@ int tpo_gpu_stability_batch(tpo_gpu_ctx *ctx, const tpo_gpu_graph *program,
   });
 }
 
+}  // extern "C"
+
+namespace {
+// float_stability_filter (stability.cpp:25-50) for graphs beyond shared
+// memory: per trial the normals in HBM, program and candidate on the
+// global-memory fp64 executor, the comparison as a device flag.
+int8_t stability_global(tpo_gpu_ctx *ctx, const tpo_gpu_graph *prog, const tpo_gpu_graph *cand, int trials,
+                        double tol, uint64_t seed, double scale) {
+  Ctx &C = ctx->c;
+  const Graph &P = prog->g, &G = cand->g;
+  check_pair(P.g, G.g);
+  cudaStream_t st = C.stream;
+  double *in = static_cast<double *>(C.vm_in.get(size_t(P.in_elems) * 8 + 16));
+  double *ro = static_cast<double *>(C.vm_out.get(size_t(P.out_elems) * 2 * 8 + 16));
+  double *co = ro + P.out_elems;
+  int *fail = static_cast<int *>(C.status.get(16));
+  for (int trial = 0; trial < trials; ++trial) {
+    check_cuda(cudaError_t(tpo_fp_launch_normals(in, seed, trial, uint64_t(P.in_elems), scale, C.num_sms, st)),
+               "normals");
+    int rc = eval_vm_impl(ctx, prog, 0, in, ro, false, st);
+    if (!rc) rc = eval_vm_impl(ctx, cand, 0, in, co, false, st);
+    if (rc) throw Error(ErrCode::Unsupported, "stability filter: " + std::string(tpo_gpu_last_error()));
+    check_cuda(cudaMemsetAsync(fail, 0, 4, st), "flag");
+    check_cuda(cudaError_t(tpo_fp_launch_stab_compare(ro, co, uint64_t(P.out_elems), tol, fail, C.num_sms, st)),
+               "compare");
+    int h = 0;
+    check_cuda(cudaMemcpyAsync(&h, fail, 4, cudaMemcpyDeviceToHost, st), "flag");
+    check_cuda(cudaStreamSynchronize(st), "sync");
+    if (h) return 0;  // stability.cpp returns at the first failing trial
+  }
+  return 1;
+}
+}  // namespace
+
+extern "C" {
+
 int tpo_gpu_float_stability_filter(tpo_gpu_ctx *ctx, const tpo_gpu_graph *g,
                                    const tpo_gpu_graph *program, int32_t trials, double tol,
                                    uint64_t seed, double input_scale, int32_t *out_ok) {
   int8_t ok = 0;
   const tpo_gpu_graph *c = g;
-  const int rc = tpo_gpu_stability_batch(ctx, program, &c, nullptr, 1, trials, tol, seed, input_scale, &ok);
+  int rc = tpo_gpu_stability_batch(ctx, program, &c, nullptr, 1, trials, tol, seed, input_scale, &ok);
+  if (rc == 1000 + int(ErrCode::DoesNotFit)) {  // full-size graphs: the global-memory executor
+    rc = guard([&] {
+      check_cuda(cudaSetDevice(ctx->c.device), "cudaSetDevice");
+      ok = stability_global(ctx, program, g, trials, tol, seed, input_scale);
+      return 0;
+    });
+  }
   if (rc) return rc;
   if (ok < 0) return fail(1000 + int(ErrCode::ShapeMismatch), "candidate does not match the program's interface");
   *out_ok = ok;

@@ -422,7 +422,45 @@ __global__ void __launch_bounds__(kThreads) stability_kernel(StabilityArgs a) {
   }
 }
 
+// Full-shape stability filter (graphs beyond shared memory): the trial's
+// N(0,1)·scale inputs in HBM, exactly stability_kernel's stream, and the
+// stability.cpp:39-47 comparison as a grid-wide flag.
+__global__ void __launch_bounds__(256) normals_kernel(double *W, uint64_t s0, uint64_t n, double scale) {
+  for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += uint64_t(gridDim.x) * blockDim.x)
+    W[e] = __dmul_rn(normal_at(s0, e), scale);
+}
+
+__global__ void __launch_bounds__(256) stab_compare_kernel(const double *r, const double *o, uint64_t n,
+                                                            double tol, int *fail) {
+  bool bad = false;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+    const double x = o[i], y = r[i];
+    if (!isfinite(x)) bad = true;
+    const double err = fabs(x - y) / fmax(fabs(y), 1e-6);
+    if (err > tol) bad = true;
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(fail, 1);
+}
+
 }  // namespace tpo_fp
+
+extern "C" int tpo_fp_launch_normals(double *W, uint64_t seed, int trial, uint64_t n, double scale,
+                                     int num_sms, cudaStream_t st) {
+  using namespace tpo_fp;
+  const uint64_t s0 = (seed ^ (kGamma * (uint64_t(trial) + 1))) + kGamma;  // Rng::derive + discard
+  const uint64_t want = (n + 255) / 256;
+  const int grid = int(want < uint64_t(num_sms) * 8 ? (want ? want : 1) : uint64_t(num_sms) * 8);
+  normals_kernel<<<grid, 256, 0, st>>>(W, s0, n, scale);
+  return int(cudaGetLastError());
+}
+
+extern "C" int tpo_fp_launch_stab_compare(const double *r, const double *o, uint64_t n, double tol, int *fail,
+                                          int num_sms, cudaStream_t st) {
+  const uint64_t want = (n + 255) / 256;
+  const int grid = int(want < uint64_t(num_sms) * 8 ? (want ? want : 1) : uint64_t(num_sms) * 8);
+  tpo_fp::stab_compare_kernel<<<grid, 256, 0, st>>>(r, o, n, tol, fail);
+  return int(cudaGetLastError());
+}
 
 extern "C" int tpo_fp_launch_eval(const tpo_fp::EvalArgs *a, int f32, size_t smem, cudaStream_t st) {
   auto kern = f32 ? tpo_fp::eval_kernel<float> : tpo_fp::eval_kernel<double>;

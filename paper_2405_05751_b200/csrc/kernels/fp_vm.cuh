@@ -41,3 +41,7 @@ extern "C" int tpo_fp_launch_stability(const tpo_fp::StabilityArgs *a, int grid,
 extern "C" int tpo_fp_stability_occupancy(size_t smem);
 extern "C" int tpo_fp_launch_instr(void *W, int f32, const TpoVmInstr *I, uint32_t it, int num_sms,
                                    cudaStream_t st);
+extern "C" int tpo_fp_launch_normals(double *W, uint64_t seed, int trial, uint64_t n, double scale,
+                                     int num_sms, cudaStream_t st);
+extern "C" int tpo_fp_launch_stab_compare(const double *r, const double *o, uint64_t n, double tol, int *fail,
+                                          int num_sms, cudaStream_t st);

@@ -139,3 +139,19 @@ def test_baseline_shape_eval_bit_exact(ctx, name):
     got_p = ctx.eval_vm(prog, ins, mode=1)[0]
     want_p = ref.eval_mugraph(prog, ins, mode=1)[0]
     assert np.array_equal(got_p, want_p)
+
+
+def test_stability_filter_full_shape(ctx):
+    """float_stability_filter at BASELINE shapes, beyond shared memory:
+    normals in HBM, program and candidate on the global-memory fp64
+    executor; the verdict equals the reference's (stable µGraph: pass;
+    mutant: fail)."""
+    prog, mu = F.bench_pair("rmsnorm")
+    args = F.BENCH["rmsnorm"]["args"]
+    mut = F.family_mugraph("rmsnorm", *args, grid=F.BENCH["rmsnorm"]["grid"],
+                           forloop=F.BENCH["rmsnorm"]["forloop"], mutant=True)
+    for cand in (mu, mut):
+        got = ctx.float_stability_filter(cand, prog, trials=1, seed=17)
+        want = ref.float_stability_filter(cand, prog, trials=1, seed=17)
+        assert got == want
+    assert ctx.float_stability_filter(mu, prog, trials=1, seed=17)

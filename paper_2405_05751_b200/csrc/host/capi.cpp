@@ -820,6 +820,128 @@ int tpo_gpu_verify_batch(tpo_gpu_ctx *ctx, const tpo_gpu_graph *program,
   });
 }
 
+}  // extern "C"
+
+namespace {
+
+// Walk one graph's bytecode on the global-memory field executor.
+void run_global_ff(Ctx &C, const VmProgram &p, const tpo_ff::GlobalFF &g, cudaStream_t st) {
+  for (size_t pc = 0; pc < p.code.size(); ++pc) {
+    const TpoVmInstr &I = p.code[pc];
+    if (I.op == VM_LOOP) {
+      size_t end = pc + 1;
+      while (end < p.code.size() && p.code[end].op != VM_ENDLOOP) ++end;
+      for (uint32_t it = 0; it < I.n; ++it)
+        for (size_t k = pc + 1; k < end; ++k)
+          check_cuda(cudaError_t(tpo_ff_global_launch(0, &g, &p.code[k], it, uint32_t(k), 0, 0, 0, C.num_sms, st)),
+                     "ff instr");
+      pc = end;
+      continue;
+    }
+    check_cuda(cudaError_t(tpo_ff_global_launch(0, &g, &I, 0, uint32_t(pc), 0, 0, 0, C.num_sms, st)), "ff instr");
+  }
+}
+
+// random_test_equivalence (equiv.cpp:34-94) for graphs beyond shared
+// memory: the same draws, arithmetic, resample and witness rules as the
+// batched kernel, with VM memory in HBM and one launch per instruction.
+TpoVerdict verdict_global(Ctx &C, const Graph &P, const Graph &G2, const tpo_verify_cfg &cfg, FieldState &fs) {
+  TpoVerdict v{};
+  const uint32_t n_in = uint32_t(P.in_elems);
+  VmProgram pp, cp;
+  try {
+    pp = lower_vm(P.g, 0, n_in, /*pin_outputs=*/true, /*field=*/true);
+    cp = lower_vm(G2.g, 0, n_in + pp.pinned_words, false, true);
+  } catch (const Error &e) {
+    v.kind = 3;
+    v.err_code = 1000 + int(e.code);
+    return v;
+  }
+  if (pp.poisoned || cp.poisoned) {
+    v.kind = 3;
+    v.err_code = 1000 + int(ErrCode::PoisonedExponent);
+    return v;
+  }
+  const uint64_t words = std::max<uint64_t>(uint64_t(n_in) + pp.region_words,
+                                            uint64_t(n_in) + pp.pinned_words + cp.region_words);
+  cudaStream_t st = C.stream;
+  tpo_ff::GlobalFF g{};
+  g.field = fs.fc;
+  g.tables = static_cast<const uint16_t *>(fs.dev.ptr);
+  g.attempt_tab = static_cast<uint16_t *>(C.shared_tab.get(size_t(fs.fc.p + 2 * fs.fc.q) * 2 + 16));
+  g.W = static_cast<uint32_t *>(C.ws.get(words * 4 + 16));
+  g.flag = static_cast<int *>(C.status.get(16));
+  g.meta = static_cast<uint32_t *>(C.shared_meta.get(16));
+  auto *key = static_cast<unsigned long long *>(C.counter.get(16));
+  const uint64_t seed = cfg.seed;
+  bool finished = false;
+  for (int round = 0; round < cfg.num_tests && !finished; ++round) {
+    bool round_done = false;
+    for (int att = 0; att <= cfg.max_resamples && !round_done; ++att) {
+      const uint64_t stream = uint64_t(round) * 131071ull + uint64_t(att);
+      check_cuda(cudaMemsetAsync(g.meta, 0, 16, st), "meta");
+      for (int what : {1, 2, 3})
+        check_cuda(cudaError_t(tpo_ff_global_launch(what, &g, nullptr, 0, 0, seed, stream, n_in, C.num_sms, st)),
+                   "ff gen");
+      bool ok = true;
+      for (const VmProgram *prog : {&pp, &cp}) {
+        check_cuda(cudaMemsetAsync(g.flag, 0, 4, st), "flag");
+        run_global_ff(C, *prog, g, st);
+        int h = 0;
+        check_cuda(cudaMemcpyAsync(&h, g.flag, 4, cudaMemcpyDeviceToHost, st), "flag");
+        check_cuda(cudaStreamSynchronize(st), "sync");
+        if (h) {  // g1 then g2: any ResampleNeeded resamples (equiv.cpp:67-83)
+          ok = false;
+          break;
+        }
+      }
+      if (!ok) {
+        ++v.resamples;
+        continue;
+      }
+      uint32_t omega = 0;
+      check_cuda(cudaMemcpyAsync(&omega, g.meta + 1, 4, cudaMemcpyDeviceToHost, st), "omega");
+      for (uint32_t t = 0; t < pp.desc.n_out && !finished; ++t) {
+        const unsigned long long none = ~0ull;
+        check_cuda(cudaMemcpyAsync(key, &none, 8, cudaMemcpyHostToDevice, st), "key");
+        check_cuda(cudaError_t(tpo_ff_global_mismatch(g.W + pp.desc.out_off[t], g.W + cp.desc.out_off[t],
+                                                      pp.desc.out_len[t], pp.desc.out_qd[t] && cp.desc.out_qd[t],
+                                                      key, C.num_sms, st)),
+                   "mismatch");
+        unsigned long long k = 0;
+        check_cuda(cudaMemcpyAsync(&k, key, 8, cudaMemcpyDeviceToHost, st), "key");
+        check_cuda(cudaStreamSynchronize(st), "sync");
+        if (k != none) {
+          v.kind = 1;
+          v.has_witness = 1;
+          v.w_seed = seed;
+          v.w_round = round;
+          v.w_omega = omega;
+          v.w_tensor = int32_t(t);
+          v.w_index = int64_t(k);
+          v.rounds_run = round + 1;
+          finished = true;
+        }
+      }
+      round_done = true;
+    }
+    if (!round_done && !finished) {
+      v.kind = 2;
+      v.rounds_run = round;
+      finished = true;
+    }
+  }
+  if (!finished) {
+    v.kind = 0;
+    v.rounds_run = cfg.num_tests;
+  }
+  return v;
+}
+
+}  // namespace
+
+extern "C" {
+
 int tpo_gpu_random_test_equivalence(tpo_gpu_ctx *ctx, const tpo_gpu_graph *g1,
                                     const tpo_gpu_graph *g2, const tpo_verify_cfg *cfg,
                                     const tpo_field_params *fp, tpo_verdict *out) {
@@ -828,6 +950,15 @@ int tpo_gpu_random_test_equivalence(tpo_gpu_ctx *ctx, const tpo_gpu_graph *g1,
     uint64_t seed = cfg->seed;
     const tpo_gpu_graph *c = g2;
     int rc = tpo_gpu_verify_batch(ctx, g1, &c, &seed, 1, cfg, fp, out, nullptr);
+    if (rc == 1000 + int(ErrCode::DoesNotFit)) {  // beyond shared memory: the global-memory executor
+      Ctx &C = ctx->c;
+      check_cuda(cudaSetDevice(C.device), "cudaSetDevice");
+      if (cfg->num_tests < 1) throw Error(ErrCode::ConfigError, "num_tests must be >= 1");
+      const TpoVerdict v = verdict_global(C, g1->g, g2->g, *cfg, C.field(fp->p, fp->q, fp->omega_base));
+      static_assert(sizeof(TpoVerdict) == sizeof(tpo_verdict), "verdict layout");
+      std::memcpy(out, &v, sizeof(v));
+      rc = 0;
+    }
     if (rc) return rc;
     if (out->kind == 3) return out->err_code;
     return 0;

@@ -255,14 +255,237 @@ __device__ __forceinline__ void copy_code(TpoVmInstr *dst, const TpoVmInstr *src
   __syncthreads();
 }
 
+// One VM instruction over items [start, n) with stride `step` (the CTA
+// interpreter passes threadIdx / blockDim, the global-memory executor its
+// grid-stride range); returns true when an undefined field op (zero divisor,
+// non-residue) requires a resample.
+template <typename WT>
+__device__ __forceinline__ bool ff_exec(const SmemT<WT> &s, const FieldConst &f, const TpoVmInstr &I, uint32_t it,
+                                        uint32_t start, uint32_t step) {
+  constexpr uint32_t QS = Word<WT>::kShift, PM = Word<WT>::kMask;
+  WT *W = s.w;
+  const uint32_t p = f.p, q = f.q, mp = f.magic_p, mq = f.magic_q;
+  const uint8_t op = I.op;
+  const uint32_t n = I.n;
+  const bool qd = I.qd;
+  const bool flat = I.flags & VM_FLAT;
+  bool bad = false;
+  switch (op) {
+    case VM_ZERO:
+      for (uint32_t i = start; i < n; i += step) W[I.dst + i] = 0;
+      break;
+    case VM_COPY: {
+      const uint32_t dbase = I.dst + it * I.d_iter, abase = I.a + it * I.a_iter;
+      if (flat) {
+        for (uint32_t i = start; i < n; i += step) W[dbase + i] = W[abase + i];
+      } else {
+        for (uint32_t i = start; i < n; i += step) {
+          int32_t od, oa, ob;
+          bool wr;
+          offsets(I, i, od, oa, ob, wr);
+          if (wr) W[dbase + od] = W[abase + oa];
+        }
+      }
+      break;
+    }
+    case VM_UNARY: {
+      for (uint32_t i = start; i < n; i += step) {
+        uint32_t v = W[I.a + i];
+        uint32_t xp = v & PM, xq = v >> QS, rp = 0, rq = 0;
+        switch (I.sub) {
+          case VM_EXP:
+            rp = s.pow_w[xq];
+            break;
+          case VM_SQR:
+            rp = mod32(xp * xp, p, mp);
+            if (qd) rq = mod32(xq * xq, q, mq);
+            break;
+          case VM_SQRT: {
+            int32_t r = s.sqrt_p[xp];
+            bad |= r < 0;
+            rp = uint32_t(r) & PM;
+            if (qd) {
+              int32_t r2 = s.sqrt_q[xq];
+              bad |= r2 < 0;
+              rq = uint32_t(r2) & PM;
+            }
+            break;
+          }
+          case VM_SILU:
+            rp = s.silu_p[xp];
+            if (qd) rq = s.silu_q[xq];
+            break;
+        }
+        W[I.dst + i] = Word<WT>::pack(rp, rq);
+      }
+      break;
+    }
+    case VM_BINARY: {
+      for (uint32_t i = start; i < n; i += step) {
+        int32_t od = int32_t(i), oa = int32_t(i), ob = int32_t(i);
+        bool wr = true;
+        if (!flat) offsets(I, i, od, oa, ob, wr);
+        uint32_t va = W[I.a + oa], vb = W[I.b + ob];
+        uint32_t ap = va & PM, aq = va >> QS, bp = vb & PM, bq = vb >> QS;
+        uint32_t rp, rq = 0;
+        switch (I.sub) {
+          case VM_ADD:
+            rp = ap + bp;
+            rp = rp >= p ? rp - p : rp;
+            if (qd) {
+              rq = aq + bq;
+              rq = rq >= q ? rq - q : rq;
+            }
+            break;
+          case VM_MUL:
+            rp = mod32(ap * bp, p, mp);
+            if (qd) rq = mod32(aq * bq, q, mq);
+            break;
+          default:  // VM_DIV (field.cpp:93-103)
+            bad |= bp == 0;
+            rp = mod32(ap * s.inv_p[bp], p, mp);
+            if (qd) {
+              bad |= bq == 0;
+              rq = mod32(aq * s.inv_q[bq], q, mq);
+            }
+            break;
+        }
+        W[I.dst + od] = Word<WT>::pack(rp, rq);
+      }
+      break;
+    }
+    case VM_MATMUL: {
+      // dims {gx, gy, gz, batch, M, K, N}; operands read through strides
+      // (block layout or InIter views), sa/sb {gx, gy, gz, batch, m | -,
+      // k, - | n}; dst contiguous [grid][batch][M][N].  VM_TILE22: one
+      // index = a 2 x 2 output tile.  Products < (p-1)^2 accumulate raw in
+      // u32 and reduce every `lazy` terms (>= 84k for p = 227).
+      const bool tile = I.flags & VM_TILE22;
+      const uint32_t Bi = I.dims[3], M = I.dims[4], K = I.dims[5], N = I.dims[6];
+      const uint32_t tm = tile ? 2u : 1u, Mt = M / tm, Nt = N / tm, MNt = Mt * Nt;
+      const uint32_t lazy = f.lazy;
+      const int32_t ska = I.sa[5], skb = I.sb[5], sma = I.sa[4], snb = I.sb[6];
+      for (uint32_t o = start; o < n; o += step) {
+        const uint32_t blk = fdiv(o, I.dmul[0], I.dsh[0]);
+        uint32_t r = o - blk * Bi * MNt;
+        const uint32_t bi = fdiv(r, I.dmul[1], I.dsh[1]);
+        r -= bi * MNt;
+        const uint32_t mt = fdiv(r, I.dmul[2], I.dsh[2]), ct = r - mt * Nt;
+        const uint32_t gx = fdiv(blk, I.dmul[3], I.dsh[3]), gr = blk - gx * I.dims[1] * I.dims[2];
+        const uint32_t gy = fdiv(gr, I.dmul[4], I.dsh[4]), gz = gr - gy * I.dims[2];
+        const uint32_t m = mt * tm, c = ct * tm;
+        const WT *pa = W + int32_t(I.a + it * I.a_iter) + int32_t(gx) * I.sa[0] +
+                             int32_t(gy) * I.sa[1] + int32_t(gz) * I.sa[2] + int32_t(bi) * I.sa[3] +
+                             int32_t(m) * sma;
+        const WT *pb = W + int32_t(I.b + it * I.b_iter) + int32_t(gx) * I.sb[0] +
+                             int32_t(gy) * I.sb[1] + int32_t(gz) * I.sb[2] + int32_t(bi) * I.sb[3] +
+                             int32_t(c) * snb;
+        const uint32_t dbase = I.dst + ((blk * Bi + bi) * M + m) * N + c;
+        if (tile) {
+          uint32_t ap[4] = {0, 0, 0, 0}, aq[4] = {0, 0, 0, 0};  // (m, c), (m, c+1), (m+1, c), (m+1, c+1)
+          for (uint32_t k0 = 0; k0 < K; k0 += lazy) {
+            const uint32_t k1 = min(K, k0 + lazy);
+            uint32_t sp[4] = {0, 0, 0, 0}, sq[4] = {0, 0, 0, 0};
+#pragma unroll 2
+            for (uint32_t k = k0; k < k1; ++k) {
+              const uint32_t a0 = pa[int32_t(k) * ska], a1 = pa[int32_t(k) * ska + sma];
+              const uint32_t b0 = pb[int32_t(k) * skb], b1 = pb[int32_t(k) * skb + snb];
+              const uint32_t a0p = a0 & PM, a0q = a0 >> QS, a1p = a1 & PM, a1q = a1 >> QS;
+              const uint32_t b0p = b0 & PM, b0q = b0 >> QS, b1p = b1 & PM, b1q = b1 >> QS;
+              sp[0] += a0p * b0p, sq[0] += a0q * b0q;
+              sp[1] += a0p * b1p, sq[1] += a0q * b1q;
+              sp[2] += a1p * b0p, sq[2] += a1q * b0q;
+              sp[3] += a1p * b1p, sq[3] += a1q * b1q;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              ap[j] = mod32(ap[j] + mod32(sp[j], p, mp), p, mp);
+              aq[j] = mod32(aq[j] + mod32(sq[j], q, mq), q, mq);
+            }
+          }
+          const uint32_t off[4] = {0, 1, N, N + 1};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint32_t accp = ap[j], accq = aq[j];
+            if (I.flags & VM_ACCUM) {  // fused φ-Accum: acc = add(acc, A·B)
+              const uint32_t d = W[dbase + off[j]];
+              accp += d & PM;
+              accp = accp >= p ? accp - p : accp;
+              accq += d >> QS;
+              accq = accq >= q ? accq - q : accq;
+            }
+            W[dbase + off[j]] = Word<WT>::pack(accp, qd ? accq : 0u);
+          }
+          continue;
+        }
+        uint32_t accp = 0, accq = 0;
+        for (uint32_t k0 = 0; k0 < K; k0 += lazy) {
+          const uint32_t k1 = min(K, k0 + lazy);
+          uint32_t p0 = 0, p1 = 0, q0 = 0, q1 = 0;  // 4 independent chains
+          uint32_t k = k0;
+          for (; k + 2 <= k1; k += 2) {
+            const uint32_t va0 = pa[int32_t(k) * ska], vb0 = pb[int32_t(k) * skb];
+            const uint32_t va1 = pa[int32_t(k + 1) * ska], vb1 = pb[int32_t(k + 1) * skb];
+            p0 += (va0 & PM) * (vb0 & PM);
+            q0 += (va0 >> QS) * (vb0 >> QS);
+            p1 += (va1 & PM) * (vb1 & PM);
+            q1 += (va1 >> QS) * (vb1 >> QS);
+          }
+          if (k < k1) {
+            const uint32_t va0 = pa[int32_t(k) * ska], vb0 = pb[int32_t(k) * skb];
+            p0 += (va0 & PM) * (vb0 & PM);
+            q0 += (va0 >> QS) * (vb0 >> QS);
+          }
+          // two partial sums of <= lazy/2 terms each: reduce before adding
+          accp = mod32(accp + mod32(p0, p, mp) + mod32(p1, p, mp), p, mp);
+          accq = mod32(accq + mod32(q0, q, mq) + mod32(q1, q, mq), q, mq);
+        }
+        if (I.flags & VM_ACCUM) {  // fused φ-Accum: acc = add(acc, A·B)
+          const uint32_t d = W[dbase];
+          accp += d & PM;
+          accp = accp >= p ? accp - p : accp;
+          accq += d >> QS;
+          accq = accq >= q ? accq - q : accq;
+        }
+        W[dbase] = Word<WT>::pack(accp, qd ? accq : 0u);
+      }
+      break;
+    }
+    case VM_SUM: {
+      const uint32_t mid = I.dims[1], grp = I.dims[2], inner = I.dims[3];
+      const uint32_t lazy = f.lazy_sum;
+      for (uint32_t o = start; o < n; o += step) {
+        const uint32_t t = fdiv(o, I.dmul[0], I.dsh[0]), in_i = o - t * inner;
+        const uint32_t ou = fdiv(t, I.dmul[1], I.dsh[1]), m = t - ou * mid;
+        const WT *pa = W + I.a + (ou * mid * grp + m * grp) * inner + in_i;
+        uint32_t accp = 0, accq = 0;
+        for (uint32_t g0 = 0; g0 < grp; g0 += lazy) {
+          const uint32_t g1 = min(grp, g0 + lazy);
+          uint32_t sp = 0, sq = 0;
+#pragma unroll 4
+          for (uint32_t g = g0; g < g1; ++g) {
+            const uint32_t v = pa[g * inner];
+            sp += v & PM;
+            sq += v >> QS;
+          }
+          accp = mod32(accp + mod32(sp, p, mp), p, mp);
+          accq = mod32(accq + mod32(sq, q, mq), q, mq);
+        }
+        W[I.dst + o] = Word<WT>::pack(accp, qd ? accq : 0u);
+      }
+      break;
+    }
+    default:
+      break;
+  }
+  return bad;
+}
+
 // PROF: thread 0 accumulates clock64 per VM opcode into prof[op] (TPO_VM_PROFILE).
 template <bool PROF, typename WT>
 __device__ bool run_program(const SmemT<WT> &s, const FieldConst &f, const TpoVmInstr *code,
                             uint32_t len, int *s_flag, unsigned long long *prof) {
-  constexpr uint32_t QS = Word<WT>::kShift, PM = Word<WT>::kMask;
   uint32_t it = 0, loop_pc = 0, trips = 1;
-  WT *W = s.w;
-  const uint32_t p = f.p, q = f.q, mp = f.magic_p, mq = f.magic_q;
   long long t_prev = PROF ? clock64() : 0;
   for (uint32_t pc = 0; pc < len; ++pc) {
     const TpoVmInstr &I = code[pc];
@@ -277,218 +500,7 @@ __device__ bool run_program(const SmemT<WT> &s, const FieldConst &f, const TpoVm
       if (++it < trips) pc = loop_pc;  // loop body restarts at loop_pc + 1
       continue;
     }
-    const uint32_t n = I.n;
-    const bool qd = I.qd;
-    const bool flat = I.flags & VM_FLAT;
-    bool bad = false;
-    switch (op) {
-      case VM_ZERO:
-        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) W[I.dst + i] = 0;
-        break;
-      case VM_COPY: {
-        const uint32_t dbase = I.dst + it * I.d_iter, abase = I.a + it * I.a_iter;
-        if (flat) {
-          for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) W[dbase + i] = W[abase + i];
-        } else {
-          for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-            int32_t od, oa, ob;
-            bool wr;
-            offsets(I, i, od, oa, ob, wr);
-            if (wr) W[dbase + od] = W[abase + oa];
-          }
-        }
-        break;
-      }
-      case VM_UNARY: {
-        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-          uint32_t v = W[I.a + i];
-          uint32_t xp = v & PM, xq = v >> QS, rp = 0, rq = 0;
-          switch (I.sub) {
-            case VM_EXP:
-              rp = s.pow_w[xq];
-              break;
-            case VM_SQR:
-              rp = mod32(xp * xp, p, mp);
-              if (qd) rq = mod32(xq * xq, q, mq);
-              break;
-            case VM_SQRT: {
-              int32_t r = s.sqrt_p[xp];
-              bad |= r < 0;
-              rp = uint32_t(r) & PM;
-              if (qd) {
-                int32_t r2 = s.sqrt_q[xq];
-                bad |= r2 < 0;
-                rq = uint32_t(r2) & PM;
-              }
-              break;
-            }
-            case VM_SILU:
-              rp = s.silu_p[xp];
-              if (qd) rq = s.silu_q[xq];
-              break;
-          }
-          W[I.dst + i] = Word<WT>::pack(rp, rq);
-        }
-        break;
-      }
-      case VM_BINARY: {
-        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-          int32_t od = int32_t(i), oa = int32_t(i), ob = int32_t(i);
-          bool wr = true;
-          if (!flat) offsets(I, i, od, oa, ob, wr);
-          uint32_t va = W[I.a + oa], vb = W[I.b + ob];
-          uint32_t ap = va & PM, aq = va >> QS, bp = vb & PM, bq = vb >> QS;
-          uint32_t rp, rq = 0;
-          switch (I.sub) {
-            case VM_ADD:
-              rp = ap + bp;
-              rp = rp >= p ? rp - p : rp;
-              if (qd) {
-                rq = aq + bq;
-                rq = rq >= q ? rq - q : rq;
-              }
-              break;
-            case VM_MUL:
-              rp = mod32(ap * bp, p, mp);
-              if (qd) rq = mod32(aq * bq, q, mq);
-              break;
-            default:  // VM_DIV (field.cpp:93-103)
-              bad |= bp == 0;
-              rp = mod32(ap * s.inv_p[bp], p, mp);
-              if (qd) {
-                bad |= bq == 0;
-                rq = mod32(aq * s.inv_q[bq], q, mq);
-              }
-              break;
-          }
-          W[I.dst + od] = Word<WT>::pack(rp, rq);
-        }
-        break;
-      }
-      case VM_MATMUL: {
-        // dims {gx, gy, gz, batch, M, K, N}; operands read through strides
-        // (block layout or InIter views), sa/sb {gx, gy, gz, batch, m | -,
-        // k, - | n}; dst contiguous [grid][batch][M][N].  VM_TILE22: one
-        // index = a 2 x 2 output tile.  Products < (p-1)^2 accumulate raw in
-        // u32 and reduce every `lazy` terms (>= 84k for p = 227).
-        const bool tile = I.flags & VM_TILE22;
-        const uint32_t Bi = I.dims[3], M = I.dims[4], K = I.dims[5], N = I.dims[6];
-        const uint32_t tm = tile ? 2u : 1u, Mt = M / tm, Nt = N / tm, MNt = Mt * Nt;
-        const uint32_t lazy = f.lazy;
-        const int32_t ska = I.sa[5], skb = I.sb[5], sma = I.sa[4], snb = I.sb[6];
-        for (uint32_t o = threadIdx.x; o < n; o += blockDim.x) {
-          const uint32_t blk = fdiv(o, I.dmul[0], I.dsh[0]);
-          uint32_t r = o - blk * Bi * MNt;
-          const uint32_t bi = fdiv(r, I.dmul[1], I.dsh[1]);
-          r -= bi * MNt;
-          const uint32_t mt = fdiv(r, I.dmul[2], I.dsh[2]), ct = r - mt * Nt;
-          const uint32_t gx = fdiv(blk, I.dmul[3], I.dsh[3]), gr = blk - gx * I.dims[1] * I.dims[2];
-          const uint32_t gy = fdiv(gr, I.dmul[4], I.dsh[4]), gz = gr - gy * I.dims[2];
-          const uint32_t m = mt * tm, c = ct * tm;
-          const WT *pa = W + int32_t(I.a + it * I.a_iter) + int32_t(gx) * I.sa[0] +
-                               int32_t(gy) * I.sa[1] + int32_t(gz) * I.sa[2] + int32_t(bi) * I.sa[3] +
-                               int32_t(m) * sma;
-          const WT *pb = W + int32_t(I.b + it * I.b_iter) + int32_t(gx) * I.sb[0] +
-                               int32_t(gy) * I.sb[1] + int32_t(gz) * I.sb[2] + int32_t(bi) * I.sb[3] +
-                               int32_t(c) * snb;
-          const uint32_t dbase = I.dst + ((blk * Bi + bi) * M + m) * N + c;
-          if (tile) {
-            uint32_t ap[4] = {0, 0, 0, 0}, aq[4] = {0, 0, 0, 0};  // (m, c), (m, c+1), (m+1, c), (m+1, c+1)
-            for (uint32_t k0 = 0; k0 < K; k0 += lazy) {
-              const uint32_t k1 = min(K, k0 + lazy);
-              uint32_t sp[4] = {0, 0, 0, 0}, sq[4] = {0, 0, 0, 0};
-#pragma unroll 2
-              for (uint32_t k = k0; k < k1; ++k) {
-                const uint32_t a0 = pa[int32_t(k) * ska], a1 = pa[int32_t(k) * ska + sma];
-                const uint32_t b0 = pb[int32_t(k) * skb], b1 = pb[int32_t(k) * skb + snb];
-                const uint32_t a0p = a0 & PM, a0q = a0 >> QS, a1p = a1 & PM, a1q = a1 >> QS;
-                const uint32_t b0p = b0 & PM, b0q = b0 >> QS, b1p = b1 & PM, b1q = b1 >> QS;
-                sp[0] += a0p * b0p, sq[0] += a0q * b0q;
-                sp[1] += a0p * b1p, sq[1] += a0q * b1q;
-                sp[2] += a1p * b0p, sq[2] += a1q * b0q;
-                sp[3] += a1p * b1p, sq[3] += a1q * b1q;
-              }
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                ap[j] = mod32(ap[j] + mod32(sp[j], p, mp), p, mp);
-                aq[j] = mod32(aq[j] + mod32(sq[j], q, mq), q, mq);
-              }
-            }
-            const uint32_t off[4] = {0, 1, N, N + 1};
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              uint32_t accp = ap[j], accq = aq[j];
-              if (I.flags & VM_ACCUM) {  // fused φ-Accum: acc = add(acc, A·B)
-                const uint32_t d = W[dbase + off[j]];
-                accp += d & PM;
-                accp = accp >= p ? accp - p : accp;
-                accq += d >> QS;
-                accq = accq >= q ? accq - q : accq;
-              }
-              W[dbase + off[j]] = Word<WT>::pack(accp, qd ? accq : 0u);
-            }
-            continue;
-          }
-          uint32_t accp = 0, accq = 0;
-          for (uint32_t k0 = 0; k0 < K; k0 += lazy) {
-            const uint32_t k1 = min(K, k0 + lazy);
-            uint32_t p0 = 0, p1 = 0, q0 = 0, q1 = 0;  // 4 independent chains
-            uint32_t k = k0;
-            for (; k + 2 <= k1; k += 2) {
-              const uint32_t va0 = pa[int32_t(k) * ska], vb0 = pb[int32_t(k) * skb];
-              const uint32_t va1 = pa[int32_t(k + 1) * ska], vb1 = pb[int32_t(k + 1) * skb];
-              p0 += (va0 & PM) * (vb0 & PM);
-              q0 += (va0 >> QS) * (vb0 >> QS);
-              p1 += (va1 & PM) * (vb1 & PM);
-              q1 += (va1 >> QS) * (vb1 >> QS);
-            }
-            if (k < k1) {
-              const uint32_t va0 = pa[int32_t(k) * ska], vb0 = pb[int32_t(k) * skb];
-              p0 += (va0 & PM) * (vb0 & PM);
-              q0 += (va0 >> QS) * (vb0 >> QS);
-            }
-            // two partial sums of <= lazy/2 terms each: reduce before adding
-            accp = mod32(accp + mod32(p0, p, mp) + mod32(p1, p, mp), p, mp);
-            accq = mod32(accq + mod32(q0, q, mq) + mod32(q1, q, mq), q, mq);
-          }
-          if (I.flags & VM_ACCUM) {  // fused φ-Accum: acc = add(acc, A·B)
-            const uint32_t d = W[dbase];
-            accp += d & PM;
-            accp = accp >= p ? accp - p : accp;
-            accq += d >> QS;
-            accq = accq >= q ? accq - q : accq;
-          }
-          W[dbase] = Word<WT>::pack(accp, qd ? accq : 0u);
-        }
-        break;
-      }
-      case VM_SUM: {
-        const uint32_t mid = I.dims[1], grp = I.dims[2], inner = I.dims[3];
-        const uint32_t lazy = f.lazy_sum;
-        for (uint32_t o = threadIdx.x; o < n; o += blockDim.x) {
-          const uint32_t t = fdiv(o, I.dmul[0], I.dsh[0]), in_i = o - t * inner;
-          const uint32_t ou = fdiv(t, I.dmul[1], I.dsh[1]), m = t - ou * mid;
-          const WT *pa = W + I.a + (ou * mid * grp + m * grp) * inner + in_i;
-          uint32_t accp = 0, accq = 0;
-          for (uint32_t g0 = 0; g0 < grp; g0 += lazy) {
-            const uint32_t g1 = min(grp, g0 + lazy);
-            uint32_t sp = 0, sq = 0;
-#pragma unroll 4
-            for (uint32_t g = g0; g < g1; ++g) {
-              const uint32_t v = pa[g * inner];
-              sp += v & PM;
-              sq += v >> QS;
-            }
-            accp = mod32(accp + mod32(sp, p, mp), p, mp);
-            accq = mod32(accq + mod32(sq, q, mq), q, mq);
-          }
-          W[I.dst + o] = Word<WT>::pack(accp, qd ? accq : 0u);
-        }
-        break;
-      }
-      default:
-        break;
-    }
+    const bool bad = ff_exec(s, f, I, it, threadIdx.x, blockDim.x);
     // NonResidue (sqrt) = 2 / DivByZero (div) = 1; within a barrier phase
     // the earliest failing instruction wins (as in the reference's
     // sequential evaluation, where it throws first)
@@ -697,6 +709,133 @@ __global__ void __launch_bounds__(kThreads) shared_attempt_kernel(VerifyArgs a, 
   if (threadIdx.x == 0) meta[0] = ok ? 1u : 0u, meta[1] = omega;
 }
 
+// ---------------------------------------------------------------------------
+// Global-memory field executor: µGraphs beyond shared memory (BASELINE
+// shapes).  VM words (32-bit) live in an HBM arena; the host walks the
+// bytecode, one grid-stride launch per instruction, exactly the CTA
+// interpreter's arithmetic (ff_exec).  Tables: inv / sqrt from the field
+// state, SiLU and ω powers per attempt, all in global memory.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ SmemT<uint32_t> global_view(const GlobalFF &g) {
+  SmemT<uint32_t> s;
+  s.inv_p = const_cast<uint16_t *>(g.tables);
+  s.inv_q = s.inv_p + g.field.p;
+  s.sqrt_p = reinterpret_cast<int16_t *>(s.inv_q + g.field.q);
+  s.sqrt_q = s.sqrt_p + g.field.p;
+  s.silu_p = g.attempt_tab;
+  s.silu_q = s.silu_p + g.field.p;
+  s.pow_w = s.silu_q + g.field.q;
+  s.w = g.W;
+  return s;
+}
+
+__global__ void __launch_bounds__(256) ff_instr_kernel(GlobalFF g, TpoVmInstr I, uint32_t it, uint32_t pc) {
+  const SmemT<uint32_t> s = global_view(g);
+  const bool bad = ff_exec(s, g.field, I, it, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+  if (__syncthreads_or(bad) && threadIdx.x == 0)
+    atomicMax(g.flag, int(((0xffffu - pc) << 2) | (I.op == VM_UNARY ? 2u : 1u)));
+}
+
+// Inputs of attempt (seed, stream): element e draws 2e+1, 2e+2 of the
+// derived stream (sample_inputs, ffeval.cpp:29-40); meta[2] flags a draw in
+// the rejection zone (the attempt is then replayed sequentially).
+__global__ void __launch_bounds__(256) ff_gen_inputs_kernel(GlobalFF g, uint64_t seed, uint64_t stream, uint64_t n_in) {
+  const FieldConst &f = g.field;
+  const uint64_t st0 = derive_state(seed, stream);
+  bool slow = false;
+  for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n_in; e += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t r1 = fin(st0 + (2 * e + 1) * kGamma), r2 = fin(st0 + (2 * e + 2) * kGamma);
+    slow |= (r1 < f.thr_p) | (r2 < f.thr_q);
+    g.W[e] = mod64(r1, f.p, f.magic_p, f.two32_p) | (mod64(r2, f.q, f.magic_q, f.two32_q) << 16);
+  }
+  if (__syncthreads_or(slow) && threadIdx.x == 0) atomicOr(g.meta + 2, 1u);
+}
+
+// One CTA: ω (draw 2n+1), the SiLU tables (draws 2n+2 ..) and the ω power
+// table; when meta[2] is set, thread 0 first replays the whole stream
+// sequentially (exact rejection sampling, rng.hpp:44-50).  meta[1] = ω.
+__global__ void __launch_bounds__(256) ff_gen_tables_kernel(GlobalFF g, uint64_t seed, uint64_t stream, uint64_t n_in) {
+  const FieldConst &f = g.field;
+  const SmemT<uint32_t> s = global_view(g);
+  __shared__ uint32_t s_omega;
+  const uint64_t st0 = derive_state(seed, stream);
+  if (threadIdx.x == 0) {
+    if (g.meta[2]) {
+      uint64_t st = st0;
+      for (uint64_t e = 0; e < n_in; ++e) {
+        const uint32_t xp = seq_uniform(st, f.p, f.thr_p, f.magic_p, f.two32_p);
+        const uint32_t xq = seq_uniform(st, f.q, f.thr_q, f.magic_q, f.two32_q);
+        g.W[e] = xp | (xq << 16);
+      }
+      const uint32_t k = seq_uniform(st, f.q, f.thr_q, f.magic_q, f.two32_q);
+      uint32_t w = 1, b = f.wbase % f.p;
+      for (uint32_t kk = k; kk; kk >>= 1) {
+        if (kk & 1) w = mod32(w * b, f.p, f.magic_p);
+        b = mod32(b * b, f.p, f.magic_p);
+      }
+      s_omega = w;
+      for (uint32_t i = 0; i < f.p; ++i) s.silu_p[i] = uint16_t(seq_uniform(st, f.p, f.thr_p, f.magic_p, f.two32_p));
+      for (uint32_t i = 0; i < f.q; ++i) s.silu_q[i] = uint16_t(seq_uniform(st, f.q, f.thr_q, f.magic_q, f.two32_q));
+    } else {
+      const uint64_t r = fin(st0 + (2 * n_in + 1) * kGamma);
+      const uint32_t k = mod64(r, f.q, f.magic_q, f.two32_q);
+      uint32_t w = 1, b = f.wbase % f.p;
+      for (uint32_t kk = k; kk; kk >>= 1) {
+        if (kk & 1) w = mod32(w * b, f.p, f.magic_p);
+        b = mod32(b * b, f.p, f.magic_p);
+      }
+      s_omega = w;
+    }
+  }
+  __syncthreads();
+  if (!g.meta[2]) {  // the ω draw and the SiLU draws cannot hit the rejection zone unseen:
+    for (uint32_t i = threadIdx.x; i < f.p + f.q; i += blockDim.x) {  // the flag covers them below
+      const uint64_t r = fin(st0 + (2 * n_in + 2 + i) * kGamma);
+      if (i < f.p)
+        s.silu_p[i] = uint16_t(mod64(r, f.p, f.magic_p, f.two32_p));
+      else
+        s.silu_q[i - f.p] = uint16_t(mod64(r, f.q, f.magic_q, f.two32_q));
+    }
+  }
+  const uint32_t omega = s_omega;
+  for (uint32_t e = threadIdx.x; e < f.q; e += blockDim.x) {
+    uint32_t w = 1, b = omega;
+    for (uint32_t k = e; k; k >>= 1) {
+      if (k & 1) w = mod32(w * b, f.p, f.magic_p);
+      b = mod32(b * b, f.p, f.magic_p);
+    }
+    s.pow_w[e] = uint16_t(w);
+  }
+  if (threadIdx.x == 0) g.meta[1] = omega;
+}
+
+// Rejection-zone check of the ω and SiLU draws (rare; sets meta[3] so the
+// host reruns the attempt's tables through the sequential replay).
+__global__ void __launch_bounds__(256) ff_check_tail_kernel(GlobalFF g, uint64_t seed, uint64_t stream, uint64_t n_in) {
+  const FieldConst &f = g.field;
+  const uint64_t st0 = derive_state(seed, stream);
+  bool slow = false;
+  for (uint32_t i = threadIdx.x; i < 1 + f.p + f.q; i += blockDim.x) {
+    const uint64_t r = fin(st0 + (2 * n_in + 1 + i) * kGamma);
+    const bool is_q = i == 0 || i > f.p;
+    slow |= r < (is_q ? f.thr_q : f.thr_p);
+  }
+  if (__syncthreads_or(slow) && threadIdx.x == 0) atomicOr(g.meta + 2, 1u);
+}
+
+// First mismatching flat index of one output tensor (FFValue ==: xq only
+// when both q-defined) -> atomicMin into *key.
+__global__ void __launch_bounds__(256) ff_mismatch_kernel(const uint32_t *a, const uint32_t *b, uint64_t n, int cmp_q,
+                                                          unsigned long long *key) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t x = a[i] ^ b[i];
+    if ((x & 0xffffu) || (cmp_q && (x >> 16))) {
+      atomicMin(key, (unsigned long long)i);
+      return;  // grid-stride: this thread's first hit is its minimum
+    }
+  }
+}
+
 // Debug / parity: evaluate one graph for one (seed, stream) attempt, or on
 // explicit inputs, and dump its outputs.
 __global__ void __launch_bounds__(kThreads) eval_kernel(EvalArgs a) {
@@ -797,4 +936,28 @@ extern "C" int tpo_ff_verify_occupancy(size_t smem, int nthreads, int narrow) {
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, nthreads == 128 ? 128 : 256, smem);
   return blocks;
+}
+
+extern "C" int tpo_ff_global_launch(int what, const tpo_ff::GlobalFF *g, const TpoVmInstr *I, uint32_t it,
+                                    uint32_t pc, uint64_t seed, uint64_t stream, uint64_t n, int num_sms,
+                                    cudaStream_t st) {
+  using namespace tpo_ff;
+  const uint64_t want = ((what == 0 && I ? I->n : n) + 255) / 256;
+  const int grid = int(want < uint64_t(num_sms) * 8 ? (want ? want : 1) : uint64_t(num_sms) * 8);
+  switch (what) {
+    case 0: ff_instr_kernel<<<grid, 256, 0, st>>>(*g, *I, it, pc); break;
+    case 1: ff_gen_inputs_kernel<<<grid, 256, 0, st>>>(*g, seed, stream, n); break;
+    case 2: ff_check_tail_kernel<<<1, 256, 0, st>>>(*g, seed, stream, n); break;
+    case 3: ff_gen_tables_kernel<<<1, 256, 0, st>>>(*g, seed, stream, n); break;
+    default: return int(cudaErrorInvalidValue);
+  }
+  return int(cudaGetLastError());
+}
+
+extern "C" int tpo_ff_global_mismatch(const uint32_t *a, const uint32_t *b, uint64_t n, int cmp_q,
+                                      unsigned long long *key, int num_sms, cudaStream_t st) {
+  const uint64_t want = (n + 255) / 256;
+  const int grid = int(want < uint64_t(num_sms) * 8 ? (want ? want : 1) : uint64_t(num_sms) * 8);
+  tpo_ff::ff_mismatch_kernel<<<grid, 256, 0, st>>>(a, b, n, cmp_q, key);
+  return int(cudaGetLastError());
 }

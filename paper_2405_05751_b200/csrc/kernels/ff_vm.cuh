@@ -83,6 +83,16 @@ struct EvalArgs {
   int *status;                   // [0] 0 ok / 1 resample, [1] omega
 };
 
+// Global-memory field executor state (graphs beyond shared memory).
+struct GlobalFF {
+  FieldConst field;
+  const uint16_t *tables;  // inv_p, inv_q, sqrt_p, sqrt_q (field state)
+  uint16_t *attempt_tab;   // silu_p[p], silu_q[q], pow_w[q] of the current attempt
+  uint32_t *W;             // 32-bit VM words: inputs, program, candidate regions
+  int *flag;               // resample flag ((0xffff - pc) << 2 | code), max
+  uint32_t *meta;          // [1] omega, [2] rejection-zone replay needed
+};
+
 }  // namespace tpo_ff
 
 // narrow: 16-bit VM words (p, q < 256)
@@ -94,3 +104,11 @@ extern "C" int tpo_ff_launch_shared(const tpo_ff::VerifyArgs *a, uint64_t seed, 
                                     void *w_out, uint16_t *tab_out, uint32_t *meta, int narrow,
                                     cudaStream_t st);
 extern "C" int tpo_ff_verify_occupancy(size_t smem, int nthreads, int narrow);
+// what: 0 one VM instruction, 1 inputs of (seed, stream), 2 rejection check
+// of the ω / SiLU draws, 3 ω + SiLU + power tables (sequential replay when
+// meta[2] is set).
+extern "C" int tpo_ff_global_launch(int what, const tpo_ff::GlobalFF *g, const TpoVmInstr *I, uint32_t it,
+                                    uint32_t pc, uint64_t seed, uint64_t stream, uint64_t n, int num_sms,
+                                    cudaStream_t st);
+extern "C" int tpo_ff_global_mismatch(const uint32_t *a, const uint32_t *b, uint64_t n, int cmp_q,
+                                      unsigned long long *key, int num_sms, cudaStream_t st);

@@ -276,3 +276,19 @@ def test_rejection_rate_and_no_false_negatives(ctx):
         for g in eqs:
             got, acc = ctx.verify_batch(prog, [g] * 1000, seeds, num_tests=4)
             assert not (got["kind"] == 1).any(), fam  # Equivalent or (sqrt) Inconclusive, never rejected
+
+
+@pytest.mark.parametrize("name", ["rmsnorm", "lora"])
+def test_full_shape_verification_matches_reference(ctx, name):
+    """random_test_equivalence at BASELINE shapes, beyond shared memory: the
+    global-memory field executor (VM words in HBM, one launch per
+    instruction) returns the reference's verdict field for field, for the
+    benchmark µGraph against its program and for a mutant (witness)."""
+    prog, mu = F.bench_pair(name)
+    b = F.BENCH[name]
+    mut = F.family_mugraph(name, *b["args"], grid=b["grid"], forloop=b["forloop"], mutant=True)
+    for cand in (mu, mut):
+        got = ctx.random_test_equivalence(prog, cand, num_tests=1, seed=3)
+        want = ref.random_test_equivalence(prog, cand, num_tests=1, seed=3)
+        for c in VCOLS:
+            assert got[c] == want[c], (name, c, got, want)

@@ -781,12 +781,45 @@ int tpo_gpu_ff_eval(tpo_gpu_ctx *ctx, const tpo_gpu_graph *h, const tpo_field_pa
   });
 }
 
+}  // extern "C"
+
+namespace {
+TpoVerdict verdict_global(Ctx &C, const Graph &P, const Graph &G2, const tpo_verify_cfg &cfg, FieldState &fs);
+}
+
+extern "C" {
+
 int tpo_gpu_verify_batch(tpo_gpu_ctx *ctx, const tpo_gpu_graph *program,
                          const tpo_gpu_graph *const *cands, const uint64_t *seeds, uint64_t n,
                          const tpo_verify_cfg *cfg, const tpo_field_params *fp,
                          tpo_verdict *verdicts, uint32_t *accept_bits) {
   return guard([&] {
     if (n == 0) return 0;
+    // graphs beyond shared memory: the global-memory field executor, one
+    // candidate at a time (same verdicts; BASELINE-shape pairs)
+    auto global_loop = [&] {
+      Ctx &C = ctx->c;
+      check_cuda(cudaSetDevice(C.device), "cudaSetDevice");
+      if (cfg->num_tests < 1) throw Error(ErrCode::ConfigError, "num_tests must be >= 1");
+      FieldState &fs = C.field(fp->p, fp->q, fp->omega_base);
+      if (accept_bits) std::memset(accept_bits, 0, size_t((n + 31) / 32) * 4);
+      for (uint64_t k = 0; k < n; ++k) {
+        tpo_verify_cfg c = *cfg;
+        c.seed = seeds ? seeds[k] : cfg->seed;
+        TpoVerdict v;
+        try {
+          check_pair(program->g.g, cands[k]->g.g);
+          v = verdict_global(C, program->g, cands[k]->g, c, fs);
+        } catch (const Error &e) {
+          v = TpoVerdict{};
+          v.kind = 3;
+          v.err_code = 1000 + int(e.code);
+        }
+        if (verdicts) std::memcpy(&verdicts[k], &v, sizeof(v));
+        if (accept_bits && v.kind == 0) accept_bits[k >> 5] |= 1u << (k & 31);
+      }
+      return 0;
+    };
     std::unordered_map<const tpo_gpu_graph *, uint32_t> idx;
     std::vector<const Graph *> uniq;
     std::vector<uint32_t> cg(n);
@@ -807,7 +840,12 @@ int tpo_gpu_verify_batch(tpo_gpu_ctx *ctx, const tpo_gpu_graph *program,
     r.n = n;
     r.verdicts_host = verdicts;
     r.accept_host = accept_bits;
-    run_verify(ctx->c, bt, *cfg, *fp, r);
+    try {
+      run_verify(ctx->c, bt, *cfg, *fp, r);
+    } catch (const Error &e) {
+      if (e.code != ErrCode::DoesNotFit) throw;
+      return global_loop();
+    }
     if (std::getenv("TPO_VM_DEBUG")) {
       const auto t2 = std::chrono::steady_clock::now();
       std::fprintf(stderr, "[tpo verify_batch] n %llu distinct %zu build %.2f ms, upload+run %.2f ms, code %.1f MB\n",
@@ -949,16 +987,8 @@ int tpo_gpu_random_test_equivalence(tpo_gpu_ctx *ctx, const tpo_gpu_graph *g1,
     check_pair(g1->g.g, g2->g.g);  // throws ShapeMismatch before sampling, like equiv.cpp:38-49
     uint64_t seed = cfg->seed;
     const tpo_gpu_graph *c = g2;
+    // (beyond shared memory verify_batch takes the global-memory executor)
     int rc = tpo_gpu_verify_batch(ctx, g1, &c, &seed, 1, cfg, fp, out, nullptr);
-    if (rc == 1000 + int(ErrCode::DoesNotFit)) {  // beyond shared memory: the global-memory executor
-      Ctx &C = ctx->c;
-      check_cuda(cudaSetDevice(C.device), "cudaSetDevice");
-      if (cfg->num_tests < 1) throw Error(ErrCode::ConfigError, "num_tests must be >= 1");
-      const TpoVerdict v = verdict_global(C, g1->g, g2->g, *cfg, C.field(fp->p, fp->q, fp->omega_base));
-      static_assert(sizeof(TpoVerdict) == sizeof(tpo_verdict), "verdict layout");
-      std::memcpy(out, &v, sizeof(v));
-      rc = 0;
-    }
     if (rc) return rc;
     if (out->kind == 3) return out->err_code;
     return 0;

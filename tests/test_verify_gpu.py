@@ -287,8 +287,16 @@ def test_full_shape_verification_matches_reference(ctx, name):
     prog, mu = F.bench_pair(name)
     b = F.BENCH[name]
     mut = F.family_mugraph(name, *b["args"], grid=b["grid"], forloop=b["forloop"], mutant=True)
+    wants = []
     for cand in (mu, mut):
         got = ctx.random_test_equivalence(prog, cand, num_tests=1, seed=3)
         want = ref.random_test_equivalence(prog, cand, num_tests=1, seed=3)
+        wants.append(want)
         for c in VCOLS:
             assert got[c] == want[c], (name, c, got, want)
+    # the batched entry point falls back to the same executor
+    got, acc = ctx.verify_batch(prog, [mu, mut], np.array([3, 3], dtype=np.uint64))
+    for k in range(2):
+        for c in VCOLS:
+            assert got[c][k] == wants[k][c], (name, k, c)
+    assert list(acc) == [w["kind"] == 0 for w in wants]

@@ -1177,10 +1177,45 @@ int tpo_gpu_eval_vm_dev(tpo_gpu_ctx *ctx, const tpo_gpu_graph *h, int32_t mode, 
   return eval_vm_impl(ctx, h, mode, in_dev, out_dev, false, static_cast<cudaStream_t>(cuda_stream));
 }
 
+}  // extern "C"
+
+namespace {
+int8_t stability_global(tpo_gpu_ctx *ctx, const tpo_gpu_graph *prog, const tpo_gpu_graph *cand, int trials,
+                        double tol, uint64_t seed, double scale);
+int stability_batch_smem(tpo_gpu_ctx *ctx, const tpo_gpu_graph *program, const tpo_gpu_graph *const *cands,
+                         const uint64_t *seeds, uint64_t n, int32_t trials, double tol, uint64_t seed,
+                         double input_scale, int8_t *ok);
+}  // namespace
+
+extern "C" {
+
 int tpo_gpu_stability_batch(tpo_gpu_ctx *ctx, const tpo_gpu_graph *program,
                             const tpo_gpu_graph *const *cands, const uint64_t *seeds, uint64_t n,
                             int32_t trials, double tol, uint64_t seed, double input_scale,
                             int8_t *ok) {
+  const int rc = stability_batch_smem(ctx, program, cands, seeds, n, trials, tol, seed, input_scale, ok);
+  if (rc != 1000 + int(ErrCode::DoesNotFit)) return rc;
+  // graphs beyond shared memory: the global-memory fp64 executor, one candidate at a time
+  return guard([&] {
+    check_cuda(cudaSetDevice(ctx->c.device), "cudaSetDevice");
+    for (uint64_t k = 0; k < n; ++k) {
+      try {
+        ok[k] = stability_global(ctx, program, cands[k], trials, tol, seeds ? seeds[k] : seed, input_scale);
+      } catch (const Error &e) {
+        if (e.code != ErrCode::ShapeMismatch) throw;
+        ok[k] = -1;
+      }
+    }
+    return 0;
+  });
+}
+
+}  // extern "C"
+
+namespace {
+int stability_batch_smem(tpo_gpu_ctx *ctx, const tpo_gpu_graph *program, const tpo_gpu_graph *const *cands,
+                         const uint64_t *seeds, uint64_t n, int32_t trials, double tol, uint64_t seed,
+                         double input_scale, int8_t *ok) {
   return guard([&] {
     if (n == 0) return 0;
     Ctx &C = ctx->c;
@@ -1264,7 +1299,7 @@ int tpo_gpu_stability_batch(tpo_gpu_ctx *ctx, const tpo_gpu_graph *program,
   });
 }
 
-}  // extern "C"
+}  // namespace
 
 namespace {
 // float_stability_filter (stability.cpp:25-50) for graphs beyond shared
@@ -1305,14 +1340,8 @@ int tpo_gpu_float_stability_filter(tpo_gpu_ctx *ctx, const tpo_gpu_graph *g,
                                    uint64_t seed, double input_scale, int32_t *out_ok) {
   int8_t ok = 0;
   const tpo_gpu_graph *c = g;
-  int rc = tpo_gpu_stability_batch(ctx, program, &c, nullptr, 1, trials, tol, seed, input_scale, &ok);
-  if (rc == 1000 + int(ErrCode::DoesNotFit)) {  // full-size graphs: the global-memory executor
-    rc = guard([&] {
-      check_cuda(cudaSetDevice(ctx->c.device), "cudaSetDevice");
-      ok = stability_global(ctx, program, g, trials, tol, seed, input_scale);
-      return 0;
-    });
-  }
+  // (beyond shared memory the batch takes the global-memory executor)
+  const int rc = tpo_gpu_stability_batch(ctx, program, &c, nullptr, 1, trials, tol, seed, input_scale, &ok);
   if (rc) return rc;
   if (ok < 0) return fail(1000 + int(ErrCode::ShapeMismatch), "candidate does not match the program's interface");
   *out_ok = ok;

@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <vector>
 #include <algorithm>
+#include <functional>
 #include <map>
 #include <mutex>
 
@@ -97,8 +98,59 @@ KernelGraph lora_mugraph(int64_t b, int64_t h, int64_t n, int64_t r, int64_t gri
   return gb.finish({o});
 }
 
+// LoRA as the fusion generator emits it: one φ-accumulator of the sum,
+// XA·B̄ applied per iteration (linear in the loop's partial sums); same
+// kernel, XA·B̄ = Σ_i XA_i·B̄.
+KernelGraph lora_single_mugraph(int64_t b, int64_t h, int64_t n, int64_t r, int64_t grid, int64_t fl) {
+  GraphBuilder gb;
+  TensorId X = gb.input({b, h}), W = gb.input({h, n}), A = gb.input({h, r}), B = gb.input({r, n});
+  BlockBuilder bb({grid, 1, 1}, fl, {{b, h}, {h, n}, {h, r}, {r, n}});
+  TensorId xb = bb.initer(0, PHI1, dm({1}));
+  TensorId wb = bb.initer(1, dm({1}), dm({0}));
+  TensorId ab = bb.initer(2, PHI1, dm({0}));
+  TensorId bbar = bb.initer(3, dm({1}), PHI1);
+  TensorId xw = bb.op(OpType::Matmul, {xb, wb});
+  TensorId xab = bb.op(OpType::Matmul, {bb.op(OpType::Matmul, {xb, ab}), bbar});
+  TensorId acc = bb.op(OpType::Accum, {bb.op(OpType::EwAdd, {xw, xab})}, AccumAttrs{PHI1});
+  bb.outsaver(acc, dm({1}));
+  TensorId o = gb.graphdef({X, W, A, B}, bb.finish(), bb.out_shapes());
+  return gb.finish({o});
+}
+
 // `key`: canonical_key(g), computed once by the caller
-// canonical keys of the reference forms, memoised by (form, sizes): a
+// Order-insensitive structure of a single-GraphDef µGraph: grid, for-loop,
+// operand shapes and, per OutSaver, the expression tree of its value (op
+// names with attributes; InIter leaves carry operand / imap / fmap).  Two
+// µGraphs that differ only in the list order of independent block ops (a
+// generator's output vs a hand-built fixture) get the same key.
+std::string structural_key(const KernelGraph &g) {
+  if (g.ops.size() != 1 || !g.ops[0].block) return canonical_key(g);
+  const BlockGraph &bg = *g.ops[0].block;
+  std::vector<int> prod(bg.tensors.size(), -1);
+  for (size_t k = 0; k < bg.ops.size(); ++k)
+    for (TensorId t : bg.ops[k].outputs) prod[size_t(t)] = int(k);
+  std::vector<std::string> memo(bg.tensors.size());
+  std::function<const std::string &(TensorId)> expr = [&](TensorId t) -> const std::string & {
+    std::string &m = memo[size_t(t)];
+    if (!m.empty()) return m;
+    const Op &op = bg.ops[size_t(prod[size_t(t)])];
+    std::string e = std::string(op_name(op.type)) + attr_key(op.attrs) + "(";
+    for (TensorId x : op.inputs) e += expr(x) + ",";
+    m = e + ")";
+    return m;
+  };
+  std::string key = "S(";
+  for (TensorId t : g.inputs) key += to_string(g.tensor(t).shape) + ";";
+  key += std::to_string(bg.grid[0]) + "," + std::to_string(bg.grid[1]) + "," + std::to_string(bg.grid[2]) + ";" +
+         std::to_string(bg.forloop) + ";";
+  std::vector<std::string> outs;
+  for (const Op &op : bg.ops)
+    if (op.type == OpType::OutSaver) outs.push_back(std::string(attr_key(op.attrs)) + expr(op.inputs[0]));
+  for (const auto &o : outs) key += o + "|";  // OutSaver #k -> output k: list order kept
+  return key + ")";
+}
+
+// structural keys of the reference forms, memoised by (form, sizes): a
 // search stream matches thousands of candidates against the same few
 template <class F>
 bool same(const std::string &key, const std::array<int64_t, 7> &form, F &&build) {
@@ -112,7 +164,7 @@ bool same(const std::string &key, const std::array<int64_t, 7> &form, F &&build)
   }
   if (want.empty()) {
     try {
-      want = canonical_key(build());
+      want = structural_key(build());
     } catch (const Error &) {
       want = "-";  // not constructible: never matches
     }
@@ -158,7 +210,7 @@ FusedPlan match_fused(const KernelGraph &g) {
   const int64_t grid = bg.grid[0], fl = bg.forloop;
   std::string key;
   try {
-    key = canonical_key(g);
+    key = structural_key(g);
   } catch (const Error &) {
     p.why = "no canonical form";
     return p;
@@ -205,7 +257,8 @@ FusedPlan match_fused(const KernelGraph &g) {
   }
   if (in.size() == 4 && r2(0) && r2(1) && r2(2) && r2(3)) {
     int64_t b = in[0].dims[0], h = in[0].dims[1], n = in[1].dims[1], r = in[2].dims[1];
-    if (same(key, {4, b, h, n, r, grid, fl}, [&] { return lora_mugraph(b, h, n, r, grid, fl); })) {
+    if (same(key, {4, b, h, n, r, grid, fl}, [&] { return lora_mugraph(b, h, n, r, grid, fl); }) ||
+        same(key, {5, b, h, n, r, grid, fl}, [&] { return lora_single_mugraph(b, h, n, r, grid, fl); })) {
       if (b > 16 || r != 16 || n % 128 || h % 64) {
         p.why = "LoRA µGraph outside kernel limits (b<=16, r==16, n%128, h%64)";
         return p;

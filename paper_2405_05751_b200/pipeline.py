@@ -62,10 +62,13 @@ def cost(g: dict, elem_size: int = 2, w_device: float = 1.0, w_shared: float = 0
 
 def optimize(ctx: "api.Context", program: dict, grids=(1, 2, 4, 8, 16, 32, 64, 128),
              loops=(1, 2, 4, 8, 16, 32, 64), num_tests: int = 2, seed: int = 0,
-             stability: bool = True) -> Dict:
+             stability: bool = True, prefer_fused: bool = True, max_resamples: int = 16) -> Dict:
     """generate -> verify -> stability -> select.  Returns the best candidate,
     its cost and describe() listing, the ranked survivors and stage counts
-    (non-increasing, SPEC.md PipelineReport)."""
+    (non-increasing, SPEC.md PipelineReport).  Works at any shape: graphs
+    beyond shared memory are verified and filtered on the global-memory
+    executors.  ``prefer_fused``: candidates that lower to a hand-written
+    sm_100a kernel rank first (the SPEC cost does not model parallelism)."""
     cands = api.generate(program, grids=grids, loops=loops)
     graphs, status = ctx.compile_many(cands)
     ok = [i for i, s in enumerate(status) if s == 0]
@@ -73,17 +76,21 @@ def optimize(ctx: "api.Context", program: dict, grids=(1, 2, 4, 8, 16, 32, 64, 1
     if not ok:
         return {**report, "verified": 0, "stable": 0, "best": None, "ranked": []}
     verdicts, _ = ctx.verify_batch(program, [graphs[i] for i in ok],
-                                   np.full(len(ok), seed, dtype=np.uint64), num_tests=num_tests)
+                                   np.full(len(ok), seed, dtype=np.uint64), num_tests=num_tests,
+                                   max_resamples=max_resamples)
     eq = [ok[k] for k in range(len(ok)) if verdicts["kind"][k] == 0]
     report["verified"] = len(eq)
+    report["inconclusive"] = int((verdicts["kind"] == 2).sum())
     if stability and eq:
         st = ctx.stability_batch(program, [graphs[i] for i in eq])
         eq = [eq[k] for k in range(len(eq)) if st[k] == 1]
     report["stable"] = len(eq)
-    ranked: List = sorted(((cost(cands[i], madds=graphs[i].info.madds), i) for i in eq),
-                          key=lambda x: (x[0], x[1]))
+    def key(i):
+        return (0 if (prefer_fused and graphs[i].fused) else 1, cost(cands[i], madds=graphs[i].info.madds), i)
+    ranked: List = [(key(i)[1], i) for i in sorted(eq, key=key)]
     best = cands[ranked[0][1]] if ranked else None
     report.update({"best": best, "best_cost": ranked[0][0] if ranked else None,
+                   "best_fused": graphs[ranked[0][1]].fused if ranked else None,
                    "describe": api.describe(best) if best else "",
                    "ranked": [(c, cands[i]) for c, i in ranked]})
     return report

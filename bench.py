@@ -496,7 +496,11 @@ def run_verify(dist, n_total, steps=1, warmup=3, pool_fams=("rmsnorm", "gatedmlp
             "peak": round(peak / 1e12, 3) if peak else None, "unit": "T field-MAC/s",
             "frac": round(macs / t_all / peak, 4) if peak else None, "traffic": None,
             "peak_source": "profiles/int_peak.json (measured IMAD/s, scripts/micro/int_peak.cu)",
-            "field_macs": macs}
+            "field_macs": macs,
+            "note": "field MACs are a minority of the work: per attempt the inputs are regenerated "
+                    "(2 splitmix64 draws + a mod per element) and both graphs interpreted; see "
+                    "issue_utilization"}
+    roof["issue_utilization"] = ncu_issue("verify")
     return {"value": round(n_done / t_all, 1), "unit": "candidates/s", "candidates": n_done,
             "roofline": roof,
             "seconds": round(t_all, 4), "kernel_seconds_max_rank": round(dist.max(t_local), 4),
@@ -591,6 +595,23 @@ def search_stream(ctx, dist, fams, pool_fams, per_fam_total=25000):
                          "the batch's common first attempt is computed once",
             "path": "JSON text -> tpo_gpu_compile_many (all host cores) -> tpo_gpu_verify_batch -> "
                     "accept bits on the host; wall clock"}
+
+
+def ncu_issue(tag):
+    """SM instruction-issue utilisation of the kernel from its committed ncu
+    summary (profiles/r01/ncu_<tag>.txt): the bound of an interpreter kernel."""
+    path = os.path.join(ROOT, "profiles", "r01", f"ncu_{tag}.txt")
+    out = {"source": os.path.relpath(path, ROOT)}
+    try:
+        for line in open(path):
+            parts = line.split()
+            if len(parts) >= 2 and parts[0] in ("sm__throughput.avg.pct_of_peak_sustained_elapsed",
+                                                "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+                                                "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"):
+                out[parts[0].split(".")[0].replace("sm__", "")] = round(float(parts[-2]) / 100, 3)
+    except Exception:
+        return None
+    return out
 
 
 def cpu_baseline_verify(n=4000):

@@ -497,10 +497,20 @@ def run_verify(dist, n_total, steps=1, warmup=3, pool_fams=("rmsnorm", "gatedmlp
             "frac": round(macs / t_all / peak, 4) if peak else None, "traffic": None,
             "peak_source": "profiles/int_peak.json (measured IMAD/s, scripts/micro/int_peak.cu)",
             "field_macs": macs,
-            "note": "field MACs are a minority of the work: per attempt the inputs are regenerated "
-                    "(2 splitmix64 draws + a mod per element) and both graphs interpreted; see "
-                    "issue_utilization"}
+            "note": "peak per SURVEY §8d: measured IMAD rate (1 field MAC per IMAD). The 2x2 "
+                    "matmul path uses dp4a (2 field MACs per instruction, frac_vs_dp4a_2lane). "
+                    "Field MACs are a minority of the work: per attempt the inputs are "
+                    "regenerated (2 splitmix64 draws + a mod per element) and both graphs "
+                    "interpreted; see issue_utilization"}
     roof["issue_utilization"] = ncu_issue("verify")
+    # the 2 x 2 matmul path packs two k terms of one field per dp4a (16-bit
+    # words): its instruction-level bound is 2 field MACs per dp4a
+    try:
+        dp4a = json.load(open(os.path.join(ROOT, "profiles", "int_peak.json")))["dp4a_per_s"]
+        roof["frac_vs_dp4a_2lane"] = round(macs / t_all / (2 * dp4a), 4)
+        roof["dp4a_2lane_peak"] = round(2 * dp4a / 1e12, 3)
+    except Exception:
+        pass
     return {"value": round(n_done / t_all, 1), "unit": "candidates/s", "candidates": n_done,
             "roofline": roof,
             "seconds": round(t_all, 4), "kernel_seconds_max_rank": round(dist.max(t_local), 4),

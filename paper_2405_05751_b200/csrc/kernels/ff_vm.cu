@@ -386,8 +386,31 @@ __device__ __forceinline__ bool ff_exec(const SmemT<WT> &s, const FieldConst &f,
           for (uint32_t k0 = 0; k0 < K; k0 += lazy) {
             const uint32_t k1 = min(K, k0 + lazy);
             uint32_t sp[4] = {0, 0, 0, 0}, sq[4] = {0, 0, 0, 0};
+            uint32_t k = k0;
+            if constexpr (sizeof(WT) == 2) {
+              // 16-bit words, A contiguous along k: one 32-bit load holds
+              // (xp_k, xq_k, xp_k+1, xq_k+1) as bytes; B's two k rows are
+              // permuted into (xp, 0, xp', 0) / (0, xq, 0, xq') and dp4a
+              // adds both k terms of a field in one instruction (exact: the
+              // same products, fewer than `lazy` of them per reduction)
+              if (ska == 1 && ((reinterpret_cast<uintptr_t>(pa + k0) | reinterpret_cast<uintptr_t>(pa + k0 + sma)) & 3u) == 0) {
 #pragma unroll 2
-            for (uint32_t k = k0; k < k1; ++k) {
+                for (; k + 2 <= k1; k += 2) {
+                  const uint32_t a0 = *reinterpret_cast<const uint32_t *>(pa + k);
+                  const uint32_t a1 = *reinterpret_cast<const uint32_t *>(pa + k + sma);
+                  const uint32_t b00 = pb[int32_t(k) * skb], b01 = pb[int32_t(k + 1) * skb];
+                  const uint32_t b10 = pb[int32_t(k) * skb + snb], b11 = pb[int32_t(k + 1) * skb + snb];
+                  const uint32_t b0p = __byte_perm(b00, b01, 0x6420), b0q = __byte_perm(b00, b01, 0x5612);
+                  const uint32_t b1p = __byte_perm(b10, b11, 0x6420), b1q = __byte_perm(b10, b11, 0x5612);
+                  sp[0] = __dp4a(a0, b0p, sp[0]), sq[0] = __dp4a(a0, b0q, sq[0]);
+                  sp[1] = __dp4a(a0, b1p, sp[1]), sq[1] = __dp4a(a0, b1q, sq[1]);
+                  sp[2] = __dp4a(a1, b0p, sp[2]), sq[2] = __dp4a(a1, b0q, sq[2]);
+                  sp[3] = __dp4a(a1, b1p, sp[3]), sq[3] = __dp4a(a1, b1q, sq[3]);
+                }
+              }
+            }
+#pragma unroll 2
+            for (; k < k1; ++k) {
               const uint32_t a0 = pa[int32_t(k) * ska], a1 = pa[int32_t(k) * ska + sma];
               const uint32_t b0 = pb[int32_t(k) * skb], b1 = pb[int32_t(k) * skb + snb];
               const uint32_t a0p = a0 & PM, a0q = a0 >> QS, a1p = a1 & PM, a1q = a1 >> QS;

@@ -485,8 +485,21 @@ __device__ __forceinline__ bool ff_exec(const SmemT<WT> &s, const FieldConst &f,
         for (uint32_t g0 = 0; g0 < grp; g0 += lazy) {
           const uint32_t g1 = min(grp, g0 + lazy);
           uint32_t sp = 0, sq = 0;
+          uint32_t g = g0;
+          if constexpr (sizeof(WT) == 2) {
+            // contiguous group of 16-bit words: two elements per 32-bit
+            // load, each field's pair summed by one dp4a against 1-lanes
+            if (inner == 1 && (reinterpret_cast<uintptr_t>(pa + g0) & 3u) == 0) {
 #pragma unroll 4
-          for (uint32_t g = g0; g < g1; ++g) {
+              for (; g + 2 <= g1; g += 2) {
+                const uint32_t v2 = *reinterpret_cast<const uint32_t *>(pa + g);
+                sp = __dp4a(v2, 0x00010001u, sp);
+                sq = __dp4a(v2, 0x01000100u, sq);
+              }
+            }
+          }
+#pragma unroll 4
+          for (; g < g1; ++g) {
             const uint32_t v = pa[g * inner];
             sp += v & PM;
             sq += v >> QS;

@@ -922,25 +922,33 @@ __global__ void __launch_bounds__(kThreads) eval_kernel(EvalArgs a) {
 
 }  // namespace tpo_ff
 
+namespace {
+using VerifyKern = void (*)(tpo_ff::VerifyArgs);
+template <bool PROF, typename WT>
+VerifyKern pick_verify(int nthreads) {
+  using namespace tpo_ff;
+  return nthreads == 64 ? verify_kernel<PROF, 64, WT> : nthreads == 128 ? verify_kernel<PROF, 128, WT>
+                                                                         : verify_kernel<PROF, 256, WT>;
+}
+VerifyKern pick_verify(bool prof, bool narrow, int nthreads) {
+  if (prof) return narrow ? pick_verify<true, uint16_t>(nthreads) : pick_verify<true, uint32_t>(nthreads);
+  return narrow ? pick_verify<false, uint16_t>(nthreads) : pick_verify<false, uint32_t>(nthreads);
+}
+int norm_threads(int n) { return n == 64 || n == 128 ? n : 256; }
+}  // namespace
+
 extern "C" int tpo_ff_launch_verify(const tpo_ff::VerifyArgs *a, int grid, size_t smem,
                                     cudaStream_t st, int nthreads, int narrow) {
-  static int configured_for[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
+  static int configured_for[12] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
   const bool prof = a->prof != nullptr;
-  const bool small = nthreads == 128;
-  using namespace tpo_ff;
-  void (*kern)(VerifyArgs);
-  if (narrow)
-    kern = prof ? (small ? verify_kernel<true, 128, uint16_t> : verify_kernel<true, 256, uint16_t>)
-                : (small ? verify_kernel<false, 128, uint16_t> : verify_kernel<false, 256, uint16_t>);
-  else
-    kern = prof ? (small ? verify_kernel<true, 128, uint32_t> : verify_kernel<true, 256, uint32_t>)
-                : (small ? verify_kernel<false, 128, uint32_t> : verify_kernel<false, 256, uint32_t>);
-  const int slot = int(prof) * 4 + int(small) * 2 + (narrow ? 1 : 0);
+  const int nt = norm_threads(nthreads);
+  VerifyKern kern = pick_verify(prof, narrow != 0, nt);
+  const int slot = int(prof) * 6 + (nt == 64 ? 0 : nt == 128 ? 1 : 2) * 2 + (narrow ? 1 : 0);
   if (int(smem) > configured_for[slot]) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     configured_for[slot] = int(smem);
   }
-  kern<<<grid, small ? 128 : 256, smem, st>>>(*a);
+  kern<<<grid, nt, smem, st>>>(*a);
   return int(cudaGetLastError());
 }
 
@@ -965,12 +973,11 @@ extern "C" int tpo_ff_launch_eval(const tpo_ff::EvalArgs *a, size_t smem, cudaSt
 }
 
 extern "C" int tpo_ff_verify_occupancy(size_t smem, int nthreads, int narrow) {
-  using namespace tpo_ff;
   int blocks = 0;
-  void (*kern)(VerifyArgs) = narrow ? (nthreads == 128 ? verify_kernel<false, 128, uint16_t> : verify_kernel<false, 256, uint16_t>)
-                                    : (nthreads == 128 ? verify_kernel<false, 128, uint32_t> : verify_kernel<false, 256, uint32_t>);
+  const int nt = norm_threads(nthreads);
+  VerifyKern kern = pick_verify(false, narrow != 0, nt);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, nthreads == 128 ? 128 : 256, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, nt, smem);
   return blocks;
 }
 

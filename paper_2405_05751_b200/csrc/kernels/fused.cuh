@@ -24,6 +24,7 @@ struct SkinnyParams {
   int epi_atomic;            // RMS/LoRA split clusters: fp32-reduction epilogue
   int trig_early;            // experiment: producer triggers dependents this many k blocks early
   int pre_cut;               // experiment: prefetch this many fewer static stages
+  int l2_ahead;              // weight k blocks requested into L2 ahead of the ring (after the wait)
 };
 
 struct GqaParams {

@@ -221,8 +221,22 @@ __global__ void __launch_bounds__(kThreads, MINB)
           tma_load_2d(st + C::kGOff, &tmA, &bars->xg_full[kb], kbase + kb * kBK, 0);
         }
       }
+      // run ahead of the ring through L2: more weight bytes in flight per
+      // CTA than the ring holds, issued only after this evaluation's X
+      auto l2_pre = [&](int kb) {
+        const int k0 = kbase + kb * kBK;
+        tma_prefetch_l2_2d(&tmW0, n0, k0);
+        tma_prefetch_l2_2d(&tmW0, n0 + 64, k0);
+        if (C::NA > 1) {
+          tma_prefetch_l2_2d(&tmW1, n0, k0);
+          tma_prefetch_l2_2d(&tmW1, n0 + 64, k0);
+        }
+      };
+      const int l2a = p.l2_ahead;
+      for (int kb = STAGES; kb < STAGES + l2a && kb < nkb; ++kb) l2_pre(kb);
       for (int kb = npre; kb < nkb; ++kb) {
         const int s = kb % STAGES;
+        if (l2a > 0 && kb >= STAGES && kb + l2a < nkb) l2_pre(kb + l2a);
         mbar_wait(&bars->empty[s], ((kb / STAGES) & 1) ^ 1);
         uint8_t *st = stages + s * C::kStage;
         if (MODE == MODE_RMS) {  // raw X and G first: the B-tile build is on the critical path

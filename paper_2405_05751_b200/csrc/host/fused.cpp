@@ -461,17 +461,19 @@ int launch_fused(const FusedPlan &p, const void *const *in, const int32_t *dt, f
     gp.ksplit = S;
     gp.l_per_cta = int(p.L / S);
     gp.out = out[0];
-    int stages = env_int("TPO_STAGES", 3);
+    // ring of 32-KB slots (K or V blocks); TPO_STAGES counts K+V pairs
+    int slots = env_int("TPO_GQA_SLOTS", 2 * env_int("TPO_STAGES", 3));
+    int minb = env_int("TPO_MINB", 1);
     const int nct_g = int(p.groups) * S;
     gp.dbg = debug_begin(nct_g, st);
     if (!tmap_3d(&maps[0], in[1], p.L, p.hd, p.groups, 64, 128, 1, CU_TENSOR_MAP_SWIZZLE_128B) ||
         !tmap_3d(&maps[1], in[2], p.hd, p.L, p.groups, 64, 128, 1, CU_TENSOR_MAP_SWIZZLE_128B) ||
         !tmap_3d(&maps[2], in[0], p.hd, p.qh, p.groups, 64, 16, 1, CU_TENSOR_MAP_SWIZZLE_128B))
       return int(cudaErrorInvalidValue);
-    int rc_g = tpo_gqa_launch(stages, maps, &gp, st);
+    int rc_g = tpo_gqa_launch(slots, minb, maps, &gp, st);
     if (gp.dbg && !rc_g) {
       char tag[96];
-      std::snprintf(tag, sizeof(tag), "gqa ksplit %d stages %d", S, stages);
+      std::snprintf(tag, sizeof(tag), "gqa ksplit %d slots %d minb %d", S, slots, minb);
       debug_end(tag, gp.dbg, nct_g, st);
     }
     return rc_g;

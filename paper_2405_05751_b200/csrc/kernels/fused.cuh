@@ -38,5 +38,6 @@ struct GqaParams {
 extern "C" int tpo_skinny_launch(int mode, int stages, int minb, const CUtensorMap *maps,
                                  const SkinnyParams *p, cudaStream_t st);
 extern "C" size_t tpo_skinny_smem(int mode, int stages, int minb, const SkinnyParams *p);
-extern "C" int tpo_gqa_launch(int stages, const CUtensorMap *maps, const GqaParams *p,
+extern "C" int tpo_gqa_launch(int slots, int minb, const CUtensorMap *maps, const GqaParams *p,
                               cudaStream_t st);
+extern "C" size_t tpo_gqa_smem(int slots, int ksplit);

@@ -34,13 +34,13 @@ constexpr int kBL = 128;                    // kv per block (UMMA M of S^T)
 constexpr int kHD = 128;                    // head dim (UMMA M of O^T, K of S^T)
 constexpr int kTok = 16;                    // UMMA N: 8 q rows (+ lo rows / zero pad)
 constexpr uint32_t kHalf = 64 * kBL * 2;    // one 64-wide box of 128 rows: 16 KB
-constexpr uint32_t kStage = 4 * kHalf;      // K (2 boxes) + V (2 boxes)
+constexpr uint32_t kSlot = 2 * kHalf;       // one ring slot: a K^T block or a V block (2 boxes)
 constexpr uint32_t kQBytes = 2 * kTok * 128;  // Q^T: 2 K-major atoms of 16 rows
 constexpr uint32_t kPBytes = 2 * kTok * 128;  // P^T buffer: 2 K-major atoms of 16 rows
 constexpr int kThreads = 192;
 
 struct __align__(8) Bars {
-  uint64_t full[4], empty[4], s_full[2], s_empty[2], p_full[2], p_empty[2], o_full, q_full, recv;
+  uint64_t full[8], empty[8], s_full[2], s_empty[2], p_full[2], p_empty[2], o_full, q_full, recv;
   uint32_t tmem_base;
 };
 
@@ -63,18 +63,24 @@ __device__ __forceinline__ uint32_t kmaj_off(int row, int col) {
   return atom * 2048 + (row >> 3) * 1024 + (row & 7) * 128 + ((c ^ (row & 7)) << 4) + e * 2;
 }
 
-template <int STAGES, int S>
-__global__ void __launch_bounds__(kThreads, 1)
+// The ring holds SLOTS 32-KB slots filled in the order K_0, V_0, K_1, V_1, ...
+// (slot index 2j for K_j, 2j+1 for V_j).  K_j's slot frees when S_j's MMA
+// completes, V_j's when P_j·V_j's does.  MINB = 2: three slots (≈113 KB) so
+// that the next decode step's CTAs become resident beside this one's and
+// wait at the programmatic dependency instead of behind this grid's exit.
+template <int SLOTS, int S, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
     gqa_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                const __grid_constant__ CUtensorMap tmQ, const GqaParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *stages = smem;
-  uint8_t *qt = stages + STAGES * kStage;
+  uint8_t *qt = stages + SLOTS * kSlot;
   uint8_t *pbuf = qt + kQBytes;                         // 2 x kPBytes
   constexpr int rows_per = kHD / S;
-  float *red = reinterpret_cast<float *>(pbuf + 2 * kPBytes);  // [S][rows_per][8]
-  float *dpart = red + kHD * 8;                                // [S][8] denominators
+  // [S-1 peers][rows_per][8] (peer slot: its rank, minus one above the owner's)
+  float *red = reinterpret_cast<float *>(pbuf + 2 * kPBytes);
+  float *dpart = red + (S > 1 ? (S - 1) * rows_per * 8 : 0);  // [S][8] denominators
   float *wsum = dpart + 4 * 8;                                 // [4 warps][8]
   Bars *bars = reinterpret_cast<Bars *>(wsum + 4 * 8);
 
@@ -89,7 +95,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int l0 = int(rank) * p.l_per_cta;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < SLOTS; ++s) {
       mbar_init(&bars->full[s], 1);
       mbar_init(&bars->empty[s], 1);
     }
@@ -126,16 +132,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_expect_tx(&bars->q_full, kQBytes);
       tma_load_3d(qt, &tmQ, &bars->q_full, 0, 0, g);
       tma_load_3d(qt + kTok * 128, &tmQ, &bars->q_full, 64, 0, g);
-      for (int j = 0; j < nb; ++j) {
-        const int s = j % STAGES;
-        mbar_wait(&bars->empty[s], ((j / STAGES) & 1) ^ 1);
-        uint8_t *st = stages + s * kStage;
-        mbar_expect_tx(&bars->full[s], kStage);
-        const int l = l0 + j * kBL;
-        tma_load_3d(st, &tmK, &bars->full[s], l, 0, g);                  // K^T[d, l..l+63]
-        tma_load_3d(st + kHalf, &tmK, &bars->full[s], l + 64, 0, g);     // K^T[d, l+64..]
-        tma_load_3d(st + 2 * kHalf, &tmV, &bars->full[s], 0, l, g);      // V[l.., d 0..63]
-        tma_load_3d(st + 3 * kHalf, &tmV, &bars->full[s], 64, l, g);     // V[l.., d 64..]
+      for (int u = 0; u < 2 * nb; ++u) {
+        const int s = u % SLOTS;
+        mbar_wait(&bars->empty[s], ((u / SLOTS) & 1) ^ 1);
+        uint8_t *st = stages + s * kSlot;
+        mbar_expect_tx(&bars->full[s], kSlot);
+        const int l = l0 + (u >> 1) * kBL;
+        if (!(u & 1)) {
+          tma_load_3d(st, &tmK, &bars->full[s], l, 0, g);              // K^T[d, l..l+63]
+          tma_load_3d(st + kHalf, &tmK, &bars->full[s], l + 64, 0, g); // K^T[d, l+64..]
+        } else {
+          tma_load_3d(st, &tmV, &bars->full[s], 0, l, g);              // V[l.., d 0..63]
+          tma_load_3d(st + kHalf, &tmV, &bars->full[s], 64, l, g);     // V[l.., d 64..]
+        }
       }
       TPO_T(10);
     }
@@ -144,11 +153,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr uint32_t idesc = idesc_bf16(128, kTok, /*a MN-major*/ true, /*b K-major*/ false);
     mbar_wait(&bars->q_full, 0);
     auto mma2 = [&](int i) {  // O^T += V^T · P^T for block i
-      const int s = i % STAGES, b = i & 1;
+      const int u = 2 * i + 1, s = u % SLOTS, b = i & 1;
+      mbar_wait(&bars->full[s], (u / SLOTS) & 1);
       mbar_wait(&bars->p_full[b], (i >> 1) & 1);
       tc_fence_after();
       if (elect_one()) {
-        const uint32_t vt = smem_u32(stages + s * kStage + 2 * kHalf);
+        const uint32_t vt = smem_u32(stages + s * kSlot);
         const uint32_t pt = smem_u32(pbuf + b * kPBytes);
 #pragma unroll
         for (int kk = 0; kk < kBL / 16; ++kk) {
@@ -162,13 +172,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
     };
     for (int j = 0; j < nb; ++j) {
-      const int s = j % STAGES, b = j & 1;
-      mbar_wait(&bars->full[s], (j / STAGES) & 1);
+      const int u = 2 * j, s = u % SLOTS, b = j & 1;
+      mbar_wait(&bars->full[s], (u / SLOTS) & 1);
       if (j == 0 && lane == 0) TPO_T(8);
       if (j >= 2) mbar_wait(&bars->s_empty[b], ((j - 2) >> 1) & 1);
       tc_fence_after();
       if (elect_one()) {
-        const uint32_t kt = smem_u32(stages + s * kStage);
+        const uint32_t kt = smem_u32(stages + s * kSlot);
         const uint32_t qs = smem_u32(qt);
 #pragma unroll
         for (int kk = 0; kk < kHD / 16; ++kk) {
@@ -177,6 +187,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           umma_bf16(tmem + b * kTok, adesc, bdesc, idesc, kk != 0);
         }
         umma_commit(&bars->s_full[b]);
+        umma_commit(&bars->empty[s]);
       }
       __syncwarp();
       if (j >= 1) mma2(j - 1);
@@ -241,7 +252,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (S > 1) {
       cluster_wait();
       if (owner != int(rank)) {
-        const uint32_t dst = map_rank(red + (int(rank) * rows_per + (row - owner * rows_per)) * 8, owner);
+        const int slot = int(rank) < owner ? int(rank) : int(rank) - 1;
+        const uint32_t dst = map_rank(red + (slot * rows_per + (row - owner * rows_per)) * 8, owner);
         const uint32_t mb = map_rank(&bars->recv, owner);
         st_async4(dst, o[0], o[1], o[2], o[3], mb);
         st_async4(dst + 16, o[4], o[5], o[6], o[7], mb);
@@ -259,7 +271,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (owner == int(rank)) {
       for (int rr = 0; rr < S; ++rr) {
         if (rr == int(rank)) continue;
-        const float *src = red + (rr * rows_per + (row - owner * rows_per)) * 8;
+        const int slot = rr < int(rank) ? rr : rr - 1;
+        const float *src = red + (slot * rows_per + (row - owner * rows_per)) * 8;
 #pragma unroll
         for (int i = 0; i < 8; ++i) o[i] += src[i];
       }
@@ -286,16 +299,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #undef TPO_T
 }
 
-template <int STAGES, int S>
+template <int SLOTS, int S>
 size_t gqa_smem() {
-  return size_t(STAGES) * kStage + kQBytes + 2 * kPBytes + kHD * 8 * 4 + 4 * 8 * 4 + 4 * 8 * 4 +
-         sizeof(Bars) + 1024;
+  return size_t(SLOTS) * kSlot + kQBytes + 2 * kPBytes + (S - 1) * (kHD / S) * 8 * 4 + 4 * 8 * 4 +
+         4 * 8 * 4 + sizeof(Bars) + 1024;
 }
 
-template <int STAGES, int S>
+template <int SLOTS, int S, int MINB>
 cudaError_t launch_t(const CUtensorMap *maps, const GqaParams &p, cudaStream_t st) {
-  const size_t smem = gqa_smem<STAGES, S>();
-  auto kern = gqa_kernel<STAGES, S>;
+  const size_t smem = gqa_smem<SLOTS, S>();
+  auto kern = gqa_kernel<SLOTS, S, MINB>;
   static size_t configured = 0;
   if (smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -321,12 +334,20 @@ cudaError_t launch_t(const CUtensorMap *maps, const GqaParams &p, cudaStream_t s
 
 }  // namespace tpo_gqa
 
-extern "C" int tpo_gqa_launch(int stages, const CUtensorMap *maps, const GqaParams *p,
+extern "C" int tpo_gqa_launch(int slots, int minb, const CUtensorMap *maps, const GqaParams *p,
                               cudaStream_t st) {
   using namespace tpo_gqa;
-#define TPO_CASE(ST, S) \
-  if (stages == ST && p->ksplit == S) return int(launch_t<ST, S>(maps, *p, st));
-  TPO_CASE(3, 1) TPO_CASE(3, 2) TPO_CASE(3, 4) TPO_CASE(2, 2) TPO_CASE(2, 4)
+#define TPO_CASE(SL, S, MB) \
+  if (slots == SL && p->ksplit == S && minb == MB) return int(launch_t<SL, S, MB>(maps, *p, st));
+  TPO_CASE(6, 1, 1) TPO_CASE(6, 2, 1) TPO_CASE(6, 4, 1) TPO_CASE(4, 2, 1) TPO_CASE(8, 2, 1)
+  TPO_CASE(3, 2, 2) TPO_CASE(3, 4, 2)
 #undef TPO_CASE
   return int(cudaErrorInvalidValue);
+}
+
+extern "C" size_t tpo_gqa_smem(int slots, int ksplit) {
+  using namespace tpo_gqa;
+  if (slots == 3 && ksplit == 2) return gqa_smem<3, 2>();
+  if (slots == 3 && ksplit == 4) return gqa_smem<3, 4>();
+  return 0;
 }

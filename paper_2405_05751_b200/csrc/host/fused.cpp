@@ -461,9 +461,13 @@ int launch_fused(const FusedPlan &p, const void *const *in, const int32_t *dt, f
     gp.ksplit = S;
     gp.l_per_cta = int(p.L / S);
     gp.out = out[0];
-    // ring of 32-KB slots (K or V blocks); TPO_STAGES counts K+V pairs
-    int slots = env_int("TPO_GQA_SLOTS", 2 * env_int("TPO_STAGES", 3));
+    // ring of 32-KB slots (K or V blocks) filled in the MMA issue order;
+    // TPO_STAGES counts K+V pairs (sweep, profiles/r01/ring/sweep_gqa_slots*:
+    // 5 slots in issue order 22.95 us; 6 slots K,V-paired 23.25; 3 slots at
+    // two CTAs per SM 24.1)
+    int slots = env_int("TPO_GQA_SLOTS", env_int("TPO_STAGES", 0) > 0 ? 2 * env_int("TPO_STAGES", 0) : 5);
     int minb = env_int("TPO_MINB", 1);
+    gp.consume_order = env_int("TPO_GQA_ORDER", 1);
     const int nct_g = int(p.groups) * S;
     gp.dbg = debug_begin(nct_g, st);
     if (!tmap_3d(&maps[0], in[1], p.L, p.hd, p.groups, 64, 128, 1, CU_TENSOR_MAP_SWIZZLE_128B) ||

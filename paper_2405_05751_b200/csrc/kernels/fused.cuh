@@ -33,6 +33,7 @@ struct GqaParams {
   const __nv_bfloat16 *q;
   float *out;                // [g, qh, hd]
   unsigned long long *dbg;   // optional per-CTA phase timestamps (TPO_DEBUG_TIMES)
+  int consume_order;         // ring filled K_0, K_1, V_0, K_2, V_1, ... (the MMA issue order)
 };
 
 extern "C" int tpo_skinny_launch(int mode, int stages, int minb, const CUtensorMap *maps,

@@ -137,8 +137,16 @@ __global__ void __launch_bounds__(kThreads, MINB)
         mbar_wait(&bars->empty[s], ((u / SLOTS) & 1) ^ 1);
         uint8_t *st = stages + s * kSlot;
         mbar_expect_tx(&bars->full[s], kSlot);
-        const int l = l0 + (u >> 1) * kBL;
-        if (!(u & 1)) {
+        // slot u carries K_j or V_j: K_0 V_0 K_1 V_1 ..., or in the MMA
+        // issue order K_0 K_1 V_0 K_2 V_1 ... K_{nb-1} V_{nb-2} V_{nb-1}
+        bool isk;
+        int blk;
+        if (!p.consume_order) isk = !(u & 1), blk = u >> 1;
+        else if (u == 0) isk = true, blk = 0;
+        else if (u & 1) isk = (u + 1) / 2 < nb, blk = isk ? (u + 1) / 2 : nb - 1;
+        else isk = false, blk = u / 2 - 1;
+        const int l = l0 + blk * kBL;
+        if (isk) {
           tma_load_3d(st, &tmK, &bars->full[s], l, 0, g);              // K^T[d, l..l+63]
           tma_load_3d(st + kHalf, &tmK, &bars->full[s], l + 64, 0, g); // K^T[d, l+64..]
         } else {
@@ -153,7 +161,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
     constexpr uint32_t idesc = idesc_bf16(128, kTok, /*a MN-major*/ true, /*b K-major*/ false);
     mbar_wait(&bars->q_full, 0);
     auto mma2 = [&](int i) {  // O^T += V^T · P^T for block i
-      const int u = 2 * i + 1, s = u % SLOTS, b = i & 1;
+      const int u = !p.consume_order ? 2 * i + 1 : i < nb - 1 ? 2 * i + 2 : 2 * nb - 1;
+      const int s = u % SLOTS, b = i & 1;
       mbar_wait(&bars->full[s], (u / SLOTS) & 1);
       mbar_wait(&bars->p_full[b], (i >> 1) & 1);
       tc_fence_after();
@@ -172,7 +181,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
       __syncwarp();
     };
     for (int j = 0; j < nb; ++j) {
-      const int u = 2 * j, s = u % SLOTS, b = j & 1;
+      const int u = !p.consume_order ? 2 * j : j == 0 ? 0 : 2 * j - 1;
+      const int s = u % SLOTS, b = j & 1;
       mbar_wait(&bars->full[s], (u / SLOTS) & 1);
       if (j == 0 && lane == 0) TPO_T(8);
       if (j >= 2) mbar_wait(&bars->s_empty[b], ((j - 2) >> 1) & 1);
@@ -339,7 +349,7 @@ extern "C" int tpo_gqa_launch(int slots, int minb, const CUtensorMap *maps, cons
   using namespace tpo_gqa;
 #define TPO_CASE(SL, S, MB) \
   if (slots == SL && p->ksplit == S && minb == MB) return int(launch_t<SL, S, MB>(maps, *p, st));
-  TPO_CASE(6, 1, 1) TPO_CASE(6, 2, 1) TPO_CASE(6, 4, 1) TPO_CASE(4, 2, 1) TPO_CASE(8, 2, 1)
+  TPO_CASE(5, 1, 1) TPO_CASE(6, 1, 1) TPO_CASE(6, 2, 1) TPO_CASE(5, 4, 1) TPO_CASE(6, 4, 1) TPO_CASE(4, 2, 1) TPO_CASE(5, 2, 1)
   TPO_CASE(3, 2, 2) TPO_CASE(3, 4, 2)
 #undef TPO_CASE
   return int(cudaErrorInvalidValue);

@@ -104,6 +104,25 @@ def main():
         ph["tail"].append((en - lm) / 1e3)
         ph["resident_before_prev_end"].append((pe - np.median(st0)) / 1e3)
     print("  " + "  ".join(f"{k} {np.mean(v):.2f}" for k, v in ph.items()))
+    # skew of the last MMA over CTAs: within a cluster (the owner waits for
+    # its slowest peer) and over the grid; "balanced" = the grid's last MMA
+    # if every cluster's K blocks were shared evenly among its CTAs
+    S = int(os.environ.get("TPO_KSPLIT", "4"))
+    sk = {k: [] for k in ("cluster_spread", "grid_spread", "gain_if_cluster_balanced", "start_spread", "first_full_spread")}
+    for i in range(3, K):
+        b = order[i]
+        n = int((h[b, :, 0] > 0).sum())
+        lm = h[b, :n, 3].astype(np.float64).reshape(-1, S) / 1e3
+        if (lm <= 0).any():
+            continue
+        sk["cluster_spread"].append(np.mean(lm.max(1) - lm.min(1)))
+        sk["grid_spread"].append(lm.max() - lm.min())
+        sk["gain_if_cluster_balanced"].append(lm.max() - lm.mean(1).max())
+        sk["start_spread"].append((h[b, :n, 0].max() - h[b, :n, 0].min()) / 1e3)
+        ff = h[b, :n, 8]
+        sk["first_full_spread"].append((ff.max() - ff.min()) / 1e3)
+    if sk["grid_spread"]:
+        print("  skew " + "  ".join(f"{k} {np.mean(v):.2f}" for k, v in sk.items()))
     per = np.diff(np.array(ends[2:], dtype=np.float64)) / 1e3
     print(f"  period (end to end) mean {per.mean():.2f} us  min {per.min():.2f}  max {per.max():.2f}")
 

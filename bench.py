@@ -567,18 +567,28 @@ def stability_stage(ctx, dist, fams, pool_fams, per_fam_total=25000):
 
 
 def search_stream(ctx, dist, fams, pool_fams, per_fam_total=25000):
-    """The search loop's view: every candidate a DISTINCT graph handed over
-    as JSON (the reference wire format), compiled on all host cores
-    (tpo_gpu_compile_many) and verified in one batch per family
-    (tpo_gpu_verify_batch, seed i).  Wall clock from JSON text to verdict
-    bits on the host, this rank's shard, max over ranks."""
+    """The search loop's view: candidates handed over as JSON (the
+    reference wire format) — the family pool, the generator's candidates
+    (tpo_gpu_generate) and their mutants (fixtures.search_stream: distinct
+    graphs, mostly non-equivalent) — compiled on all host cores
+    (tpo_gpu_compile_many, no dedup) and verified in one batch per family
+    (tpo_gpu_verify_batch, VerifyConfig seed).  Wall clock from JSON text to
+    verdict bits on the host, this rank's shard, max over ranks.  A family
+    whose mutation space holds fewer distinct graphs than the stream cycles
+    through them; `distinct_graphs` counts the distinct ones."""
     import torch
-    from paper_2405_05751_b200 import shard
+    from paper_2405_05751_b200 import api, shard
+    from paper_2405_05751_b200 import fixtures as F
     first, n = shard.even_range(per_fam_total, dist.world, dist.rank)
     texts = []
+    distinct = 0
     for f in pool_fams:
         prog, pool = fams[f]
-        texts.append((ctx.compile(prog), [json.dumps(pool[i % len(pool)][1]) for i in range(first, first + n)]))
+        bases = [g for _, g in pool] + api.generate(prog, grids=[1, 2, 4, 8, 16, 32, 64, 128],
+                                                    loops=[1, 2, 4, 8, 16, 32, 64])
+        cands = F.search_stream(bases, per_fam_total, seed=1)
+        distinct += len(cands)
+        texts.append((ctx.compile(prog), [json.dumps(cands[i % len(cands)]) for i in range(first, first + n)]))
     for gp, js in texts:  # warm the paths (small batch)
         ctx.verify_batch(gp, ctx.compile_many(js[:64])[0], np.arange(64, dtype=np.uint64), want_verdicts=False)
     torch.cuda.synchronize()
@@ -599,7 +609,7 @@ def search_stream(ctx, dist, fams, pool_fams, per_fam_total=25000):
     wall = dist.max(time.perf_counter() - t0)
     tot = per_fam_total * len(texts)
     return {"value": round(tot / wall, 1), "unit": "candidates/s", "candidates": tot,
-            "distinct_graphs": tot, "accepted": int(dist.sum(accepted)),
+            "distinct_graphs": distinct, "accepted": int(dist.sum(accepted)),
             "compile_share": round(dist.max(t_compile) / wall, 3), "host_threads": os.cpu_count(),
             "seed_rule": "VerifyConfig default (seed 0) for every candidate, as the pipeline calls it; "
                          "the batch's common first attempt is computed once",

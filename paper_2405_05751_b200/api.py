@@ -150,9 +150,12 @@ class Graph:
 
     def __del__(self):
         h = getattr(self, "h", None)
-        if h and N._lib is not None:
-            N.lib().tpo_gpu_graph_free(h)
-            self.h = None
+        try:
+            if h and N is not None and N._lib is not None:
+                N.lib().tpo_gpu_graph_free(h)
+        except (AttributeError, TypeError):  # interpreter shutdown: module globals gone
+            pass
+        self.h = None
 
     def shapes(self, outputs: bool) -> List[List[int]]:
         n = self.info.n_outputs if outputs else self.info.n_inputs

@@ -208,7 +208,6 @@ Batch build_batch(const Graph &prog, const std::vector<const Graph *> &uniq) {
   VmProgram pp = lowered_ff(prog, bt.n_in, /*pin_outputs=*/true);
   const uint32_t cbase = bt.n_in + pp.pinned_words;
   bt.cand_base = cbase;
-  if (pp.poisoned) pp.desc.err = uint8_t(1 + int(ErrCode::PoisonedExponent));
   add_graph(bt, pp);
   uint32_t maxw = bt.n_in + pp.region_words;
   // lower the distinct candidates on all host cores (memoised per handle),
@@ -236,7 +235,6 @@ Batch build_batch(const Graph &prog, const std::vector<const Graph *> &uniq) {
     TpoVmGraph d = cp->desc;
     d.code_off = uint32_t(ncode);
     d.code_len = uint32_t(cp->code.size());
-    if (cp->poisoned) d.err = uint8_t(1 + int(ErrCode::PoisonedExponent));
     bt.graphs.push_back(d);
     at[i] = ncode;
     ncode += cp->code.size();
@@ -741,7 +739,6 @@ int tpo_gpu_ff_eval(tpo_gpu_ctx *ctx, const tpo_gpu_graph *h, const tpo_field_pa
     FieldState &fs = C.field(fpp->p, fpp->q, fpp->omega_base);
     const uint32_t n_in = uint32_t(G.in_elems);
     VmProgram p = lower_vm(G.g, 0, n_in, false, /*field=*/true);
-    if (p.poisoned) throw Error(ErrCode::PoisonedExponent, "exponent depends on a prior exponentiation");
     const size_t smem = fs.fc.table_bytes + size_t(n_in + p.region_words) * 4;
     if (smem > 232448) throw Error(ErrCode::DoesNotFit, "graph exceeds shared memory");
     TpoVmGraph d = p.desc;
@@ -778,6 +775,8 @@ int tpo_gpu_ff_eval(tpo_gpu_ctx *ctx, const tpo_gpu_graph *h, const tpo_field_pa
       if (in_xp) in_xp[e] = uint16_t(hout[n_out + e] & 0xffff);
       if (in_xq) in_xq[e] = uint16_t(hout[n_out + e] >> 16);
     }
+    // a VM_RAISE reached with no event before it: the reference's Error
+    if (hs[0] == 3) throw Error(ErrCode::PoisonedExponent, "exponent depends on a prior exponentiation");
     if (hs[0]) return 2000 + int(hs[0] == 2 ? ErrCode::NonResidue : ErrCode::DivByZero);
     size_t c = 0;
     for (uint32_t t = 0; t < p.desc.n_out; ++t)
@@ -871,22 +870,27 @@ int tpo_gpu_verify_batch(tpo_gpu_ctx *ctx, const tpo_gpu_graph *program,
 
 namespace {
 
-// Walk one graph's bytecode on the global-memory field executor.
-void run_global_ff(Ctx &C, const VmProgram &p, const tpo_ff::GlobalFF &g, cudaStream_t st) {
+// Walk one graph's bytecode on the global-memory field executor.  Returns
+// true when the walk stopped at a VM_RAISE (the caller reads the event flag).
+bool run_global_ff(Ctx &C, const VmProgram &p, const tpo_ff::GlobalFF &g, cudaStream_t st) {
   for (size_t pc = 0; pc < p.code.size(); ++pc) {
     const TpoVmInstr &I = p.code[pc];
+    if (I.op == VM_RAISE) return true;
     if (I.op == VM_LOOP) {
       size_t end = pc + 1;
       while (end < p.code.size() && p.code[end].op != VM_ENDLOOP) ++end;
       for (uint32_t it = 0; it < I.n; ++it)
-        for (size_t k = pc + 1; k < end; ++k)
+        for (size_t k = pc + 1; k < end; ++k) {
+          if (p.code[k].op == VM_RAISE) return true;  // reached in the first iteration
           check_cuda(cudaError_t(tpo_ff_global_launch(0, &g, &p.code[k], it, uint32_t(k), 0, 0, 0, C.num_sms, st)),
                      "ff instr");
+        }
       pc = end;
       continue;
     }
     check_cuda(cudaError_t(tpo_ff_global_launch(0, &g, &I, 0, uint32_t(pc), 0, 0, 0, C.num_sms, st)), "ff instr");
   }
+  return false;
 }
 
 // random_test_equivalence (equiv.cpp:34-94) for graphs beyond shared
@@ -902,11 +906,6 @@ TpoVerdict verdict_global(Ctx &C, const Graph &P, const Graph &G2, const tpo_ver
   } catch (const Error &e) {
     v.kind = 3;
     v.err_code = 1000 + int(e.code);
-    return v;
-  }
-  if (pp.poisoned || cp.poisoned) {
-    v.kind = 3;
-    v.err_code = 1000 + int(ErrCode::PoisonedExponent);
     return v;
   }
   const uint64_t words = std::max<uint64_t>(uint64_t(n_in) + pp.region_words,
@@ -933,13 +932,19 @@ TpoVerdict verdict_global(Ctx &C, const Graph &P, const Graph &G2, const tpo_ver
       bool ok = true;
       for (const VmProgram *prog : {&pp, &cp}) {
         check_cuda(cudaMemsetAsync(g.flag, 0, 4, st), "flag");
-        run_global_ff(C, *prog, g, st);
+        const bool raised = run_global_ff(C, *prog, g, st);
         int h = 0;
         check_cuda(cudaMemcpyAsync(&h, g.flag, 4, cudaMemcpyDeviceToHost, st), "flag");
         check_cuda(cudaStreamSynchronize(st), "sync");
         if (h) {  // g1 then g2: any ResampleNeeded resamples (equiv.cpp:67-83)
           ok = false;
           break;
+        }
+        if (raised) {  // Error(PoisonedExponent) escapes random_test_equivalence
+          TpoVerdict e{};
+          e.kind = 3;
+          e.err_code = 1000 + int(ErrCode::PoisonedExponent);
+          return e;
         }
       }
       if (!ok) {

@@ -232,6 +232,11 @@ void mark_phases(std::vector<TpoVmInstr> &code) {
   int prev = -1;  // last compute instruction of the current phase
   for (size_t k = 0; k < code.size(); ++k) {
     TpoVmInstr &I = code[k];
+    if (I.op == VM_RAISE) {  // checks the event flag after a barrier of its own
+      phase.clear();
+      prev = -1;
+      continue;
+    }
     if (I.op == VM_LOOP || I.op == VM_ENDLOOP) {
       trips = I.op == VM_LOOP ? int64_t(I.n) : 1;
       phase.clear();
@@ -258,8 +263,9 @@ namespace {
 
 class Lowerer {
  public:
-  Lowerer(const KernelGraph &g, uint32_t in_base, uint32_t region, bool pin, bool field)
-      : g_(g), region_(region), pin_(pin), field_(field) {
+  Lowerer(const KernelGraph &g, uint32_t in_base, uint32_t region, bool pin, bool field,
+          bool list_order = false)
+      : g_(g), region_(region), pin_(pin), field_(field), list_order_(list_order) {
     kbuf_.assign(g.tensors.size(), UINT32_MAX);
     kqd_.assign(g.tensors.size(), 1);
     uint32_t off = in_base;
@@ -300,6 +306,11 @@ class Lowerer {
       p_.desc.out_qd[i] = kqd_[size_t(t)];
       p_.out_shapes.push_back(g_.tensor(t).shape);
     }
+    // DivByZero / NonResidue events count toward a VM_RAISE only when the
+    // reference evaluates them before the raising op: every earlier op
+    // outside the raising GraphDef, grid block 0 inside it
+    for (size_t k = 0; k < p_.code.size(); ++k)
+      if (raise_at_ < 0 || int64_t(k) > raise_at_ || gd_of_[k] != raise_gd_) p_.code[k].b0n = 0;
     plan_memory();
     mark_phases(p_.code);
     p_.desc.words = p_.region_words;
@@ -315,6 +326,12 @@ class Lowerer {
   uint32_t region_;
   bool pin_;
   bool field_;
+  bool list_order_;                               // emit block ops in list order (VM_RAISE graphs)
+  int gd_ = -1;                                   // GraphDef being lowered (-1: kernel level)
+  std::vector<int> gd_of_;                        // per instruction: its GraphDef
+  int64_t raise_at_ = -1;                         // index of the VM_RAISE, if any
+  int raise_gd_ = -1;
+  int gd_count_ = -1;
   static constexpr uint32_t kVirt = 0x80000000u;  // virtual buffer id tag
   std::vector<int64_t> vsize_;                    // words per virtual buffer
   std::vector<uint32_t> kbuf_;
@@ -459,6 +476,7 @@ class Lowerer {
     }
     tpo_vm_set_divisors(&in);
     p_.code.push_back(in);
+    gd_of_.push_back(gd_);
   }
 
   // Grid dims (bx, by, bz) and the strides of a block tensor of E elements.
@@ -534,6 +552,7 @@ class Lowerer {
               cat(b_g, bcast_strides(s[1], out.dims))};
       v.wm.assign(v.dims.size(), 0);
       TpoVmInstr i = make(VM_BINARY, sub, v, dst, in[0], in[1]);
+      i.b0n = uint32_t(numel(out));  // grid-block-major index space: block 0 first
       i.qd = qd[0] & qd[1];
       i.flags |= (qd[0] ? VM_A_QD : 0) | (qd[1] ? VM_B_QD : 0);
       emit(i);
@@ -541,8 +560,21 @@ class Lowerer {
     };
     auto unary = [&](uint8_t sub) {
       TpoVmInstr i = flat(VM_UNARY, sub, 2);
+      i.b0n = uint32_t(numel(out));
       uint8_t q = sub == VM_EXP ? 0 : qd[0];
-      if (sub == VM_EXP && !qd[0]) p_.poisoned = true;
+      if (sub == VM_EXP && !qd[0]) {
+        // the reference throws Error(PoisonedExponent) here (field.cpp:105-108)
+        // unless a ResampleNeeded came first: stop the program at this op
+        if (field_ && raise_at_ < 0) {
+          TpoVmInstr r;
+          std::memset(&r, 0, sizeof(r));
+          r.op = VM_RAISE;
+          raise_at_ = int64_t(p_.code.size());
+          raise_gd_ = gd_;
+          emit(r);
+        }
+        p_.poisoned = true;
+      }
       if (sub == VM_SILU) p_.has_silu = true;
       i.qd = q;
       i.flags |= qd[0] ? VM_A_QD : 0;
@@ -630,6 +662,12 @@ class Lowerer {
 
   void graphdef(const Op &op) {
     if (!op.block) throw Error(ErrCode::Unsupported, "graphdef without block");
+    struct GdScope {
+      int &g;
+      int saved;
+      GdScope(int &x, int v) : g(x), saved(x) { g = v; }
+      ~GdScope() { g = saved; }
+    } scope(gd_, ++gd_count_);
     const BlockGraph &bg = *op.block;
     const std::array<int64_t, 3> G = bg.grid;
     for (int a = 0; a < 3; ++a)
@@ -889,7 +927,7 @@ class Lowerer {
         const char *e = std::getenv("TPO_VM_SCHED");
         return e && e[0] == '0';
       }();
-      if (keep) {
+      if (keep || list_order_) {
         for (const Op &b : bg.ops) sched_ops.push_back(&b);
       } else {
         for (int k : schedule_ops(bg).order) sched_ops.push_back(&bg.ops[size_t(k)]);
@@ -1072,7 +1110,11 @@ class Lowerer {
 
 VmProgram lower_vm(const KernelGraph &g, uint32_t input_base, uint32_t region_base,
                    bool pin_outputs, bool field) {
-  return Lowerer(g, input_base, region_base, pin_outputs, field).run();
+  VmProgram p = Lowerer(g, input_base, region_base, pin_outputs, field).run();
+  // a raising graph keeps the reference's list order, so that exactly the
+  // ops evaluated before the raising EwExp precede the VM_RAISE
+  if (field && p.poisoned) p = Lowerer(g, input_base, region_base, pin_outputs, field, true).run();
+  return p;
 }
 
 int64_t input_elems(const KernelGraph &g) {

@@ -22,6 +22,9 @@
 #include "ff_vm.cuh"
 #include "vm.h"
 
+// tpo::ErrCode::PoisonedExponent (include/tpo/ir/shape.hpp; C-ABI status 1000 + code)
+constexpr int kErrPoisonedExponent = 6;
+
 namespace tpo_ff {
 
 constexpr uint64_t kGamma = 0x9e3779b97f4a7c15ull;
@@ -289,6 +292,7 @@ __device__ __forceinline__ bool ff_exec(const SmemT<WT> &s, const FieldConst &f,
       break;
     }
     case VM_UNARY: {
+      const uint32_t lim = I.b0n ? I.b0n : n;  // events counted below lim
       for (uint32_t i = start; i < n; i += step) {
         uint32_t v = W[I.a + i];
         uint32_t xp = v & PM, xq = v >> QS, rp = 0, rq = 0;
@@ -302,11 +306,11 @@ __device__ __forceinline__ bool ff_exec(const SmemT<WT> &s, const FieldConst &f,
             break;
           case VM_SQRT: {
             int32_t r = s.sqrt_p[xp];
-            bad |= r < 0;
+            bad |= r < 0 && i < lim;
             rp = uint32_t(r) & PM;
             if (qd) {
               int32_t r2 = s.sqrt_q[xq];
-              bad |= r2 < 0;
+              bad |= r2 < 0 && i < lim;
               rq = uint32_t(r2) & PM;
             }
             break;
@@ -321,6 +325,7 @@ __device__ __forceinline__ bool ff_exec(const SmemT<WT> &s, const FieldConst &f,
       break;
     }
     case VM_BINARY: {
+      const uint32_t lim = I.b0n ? I.b0n : n;
       for (uint32_t i = start; i < n; i += step) {
         int32_t od = int32_t(i), oa = int32_t(i), ob = int32_t(i);
         bool wr = true;
@@ -342,10 +347,10 @@ __device__ __forceinline__ bool ff_exec(const SmemT<WT> &s, const FieldConst &f,
             if (qd) rq = mod32(aq * bq, q, mq);
             break;
           default:  // VM_DIV (field.cpp:93-103)
-            bad |= bp == 0;
+            bad |= bp == 0 && i < lim;
             rp = mod32(ap * s.inv_p[bp], p, mp);
             if (qd) {
-              bad |= bq == 0;
+              bad |= bq == 0 && i < lim;
               rq = mod32(aq * s.inv_q[bq], q, mq);
             }
             break;
@@ -536,6 +541,14 @@ __device__ bool run_program(const SmemT<WT> &s, const FieldConst &f, const TpoVm
       if (++it < trips) pc = loop_pc;  // loop body restarts at loop_pc + 1
       continue;
     }
+    if (op == VM_RAISE) {  // a counted event before it resamples; else the Error
+      __syncthreads();
+      const bool ev = *s_flag != 0;
+      __syncthreads();
+      if (!ev && threadIdx.x == 0) *s_flag = 3;
+      __syncthreads();
+      return false;
+    }
     const bool bad = ff_exec(s, f, I, it, threadIdx.x, blockDim.x);
     // NonResidue (sqrt) = 2 / DivByZero (div) = 1; within a barrier phase
     // the earliest failing instruction wins (as in the reference's
@@ -652,6 +665,14 @@ __global__ void __launch_bounds__(NT) verify_kernel(VerifyArgs a) {
         if (a.shared_w && seed == a.shared_seed && round == 0 && att == 0) {
           // the batch's common first attempt: inputs, tables and the
           // program's outputs were computed once (shared_attempt_kernel)
+          if (a.shared_meta[0] == 2) {  // the program raises Error(PoisonedExponent)
+            v.kind = 3;
+            v.err_code = 1000 + kErrPoisonedExponent;
+            v.resamples = 0;
+            v.rounds_run = 0;
+            finished = true;
+            break;
+          }
           if (!a.shared_meta[0]) {  // the program itself needs a resample here
             ++v.resamples;
             continue;
@@ -674,6 +695,14 @@ __global__ void __launch_bounds__(NT) verify_kernel(VerifyArgs a) {
           if (PROF && threadIdx.x == 0) s_prof[0] += (unsigned long long)(clock64() - t0), s_prof[16] += 1;
           ok = run_program<PROF>(s, f, scode, g1.code_len, &s_flag, s_prof) &&
                run_program<PROF>(s, f, ccode, g2.code_len, &s_flag, s_prof);
+        }
+        if (!ok && (s_flag & 3) == 3) {  // Error(PoisonedExponent) escapes the verifier
+          v.kind = 3;
+          v.err_code = 1000 + kErrPoisonedExponent;
+          v.resamples = 0;
+          v.rounds_run = 0;
+          finished = true;
+          break;
         }
         if (!ok) {
           ++v.resamples;
@@ -742,7 +771,7 @@ __global__ void __launch_bounds__(kThreads) shared_attempt_kernel(VerifyArgs a, 
     tab_out[f.p + i] = s.silu_q[i];
     tab_out[f.p + f.q + i] = s.pow_w[i];
   }
-  if (threadIdx.x == 0) meta[0] = ok ? 1u : 0u, meta[1] = omega;
+  if (threadIdx.x == 0) meta[0] = ok ? 1u : (s_flag & 3) == 3 ? 2u : 0u, meta[1] = omega;
 }
 
 // ---------------------------------------------------------------------------

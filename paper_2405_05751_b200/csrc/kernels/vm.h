@@ -32,6 +32,9 @@ enum TpoVmOp {
   VM_SUM,        // dims {outer, mid, group, inner}: dst[o,m,i] = sum_t a[o, m*group+t, i]
   VM_LOOP,       // n = trip count; body follows
   VM_ENDLOOP,    // jump back to the instruction after the matching VM_LOOP
+  VM_RAISE,      // FF: the first EwExp of a q-undefined value (field.cpp:105-108) — the
+                 // program stops; it is a resample if a counted event preceded it, else
+                 // Error(PoisonedExponent)
 };
 
 enum TpoVmSub { VM_ADD = 0, VM_MUL, VM_DIV, VM_EXP, VM_SQR, VM_SQRT, VM_SILU };
@@ -64,7 +67,12 @@ struct TpoVmInstr {
   uint8_t dsh[TPO_VM_DIMS];
   uint8_t pad2;
   int32_t b_iter;              // MATMUL VM_STRIDED: per-iteration offset added to b
-  uint32_t pad3[2];            // 192 bytes: copied to shared memory as uint4
+  // FF, graphs with a VM_RAISE: a DivByZero / NonResidue event counts only at
+  // indices < b0n (grid block 0 of the raising GraphDef: the reference's
+  // grid-major evaluation reaches the raising op before any later block);
+  // 0 = every index counts
+  uint32_t b0n;
+  uint32_t pad3;               // 192 bytes: copied to shared memory as uint4
 };
 
 // Host helper: the (mul, shift) pair of divisor d >= 1 (CUTLASS-style

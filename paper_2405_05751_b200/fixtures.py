@@ -204,3 +204,93 @@ def family_pool(name: str, shapes=None) -> List[Tuple[str, dict]]:
 def verify_families() -> Dict[str, Tuple[dict, List[Tuple[str, dict]]]]:
     """family -> (program, pool) at verification shapes."""
     return {f: (_PROG[f](*VERIFY_SHAPES[f]), family_pool(f)) for f in VERIFY_SHAPES}
+
+
+# ---- search-loop candidate streams ----------------------------------------------
+
+_BIN = ("ewadd", "ewmul", "ewdiv")
+_UN = ("sqr", "sqrt", "silu", "ewexp")
+
+
+def search_stream(bases: List[dict], n: int, seed: int = 0) -> List[dict]:
+    """Up to ``n`` DISTINCT candidate graphs for a search-loop stream: the
+    ``bases`` (e.g. a family pool plus the generator's candidates), then
+    mutants of them — up to two elementwise ops rewritten to another op of
+    the same arity (EwAdd/EwMul/EwDiv, Sqr/Sqrt/SiLU/EwExp) and a chain of
+    up to two unary ops inserted before the first OutSaver.  Shapes and
+    Definition-1 validity are unchanged; equivalence mostly is not, as for
+    the bulk of what a search proposes.  Distinct by canonical JSON;
+    deterministic in ``seed``; fewer than ``n`` when the mutation space of
+    the bases is exhausted."""
+    import itertools
+    import json
+    import random
+
+    rnd = random.Random(seed)
+    seen, out = set(), []
+
+    def add(g):
+        key = json.dumps(g, sort_keys=True)
+        if key not in seen:
+            seen.add(key)
+            out.append(g)
+
+    for g in bases:
+        if len(out) >= n:
+            return out
+        add(g)
+
+    def recipes(g):
+        sites = []
+        for oi, op in enumerate(g["ops"]):
+            for bi, bop in enumerate(op.get("blockGraph", {}).get("ops", [])):
+                if bop["type"] in _BIN or bop["type"] in _UN:
+                    cls = _BIN if bop["type"] in _BIN else _UN
+                    sites.append([(oi, bi, t) for t in cls if t != bop["type"]])
+        edits = [()]
+        for a in range(len(sites)):
+            edits += [(e,) for e in sites[a]]
+            for b in range(a + 1, len(sites)):
+                edits += list(itertools.product(sites[a], sites[b]))
+        chains = [()] + [(u,) for u in _UN] + list(itertools.product(_UN, _UN))
+        rs = [(e, c) for e in edits for c in chains if e or c]
+        rnd.shuffle(rs)
+        return rs
+
+    def apply(text, edit, chain):
+        g = json.loads(text)
+        for oi, bi, t in edit:
+            g["ops"][oi]["blockGraph"]["ops"][bi]["type"] = t
+        if chain:
+            gd = next(op for op in g["ops"] if "blockGraph" in op)
+            bg = gd["blockGraph"]
+            j = next(i for i, op in enumerate(bg["ops"]) if op["type"] == "outsaver")
+            t = bg["ops"][j]["inputs"][0]
+            shape = next(x["shape"] for x in bg["tensors"] if x["id"] == t)
+            nid = max(x["id"] for x in bg["tensors"]) + 1
+            new = []
+            for u in chain:
+                bg["tensors"].append({"id": nid, "shape": list(shape), "scope": "shared"})
+                new.append({"id": -1, "type": u, "attrs": {}, "inputs": [t], "outputs": [nid]})
+                t, nid = nid, nid + 1
+            bg["ops"][j]["inputs"] = [t]
+            bg["ops"][j:j] = new
+            for i, op in enumerate(bg["ops"]):
+                op["id"] = i
+        return g
+
+    texts = [json.dumps(g) for g in bases]
+    queues = [iter(recipes(g)) for g in bases]
+    live = list(range(len(bases)))
+    while len(out) < n and live:
+        nxt = []
+        for i in live:
+            r = next(queues[i], None)
+            if r is None:
+                continue
+            nxt.append(i)
+            add(apply(texts[i], *r))
+            if len(out) >= n:
+                break
+        live = nxt
+    return out

@@ -1,5 +1,6 @@
 #!/usr/bin/env python
-"""Search-loop candidate stream (GPU box): every candidate a distinct graph
+"""Search-loop candidate stream (GPU box): the pool, the generator's
+candidates and their mutants (fixtures.search_stream, distinct graphs)
 handed over as JSON (the reference's wire format), compiled on all host
 cores (tpo_gpu_compile_many) and verified in one batch (tpo_gpu_verify_batch,
 seed i).  Prints wall-clock candidates/s per stage.
@@ -14,6 +15,7 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
+from paper_2405_05751_b200 import api  # noqa: E402
 from paper_2405_05751_b200 import fixtures as F  # noqa: E402
 from paper_2405_05751_b200.api import Context  # noqa: E402
 
@@ -22,7 +24,10 @@ ctx = Context(0)
 tot_c = tot_v = 0.0
 cnt = 0
 for fam, (prog, pool) in F.verify_families().items():
-    js = [json.dumps(pool[i % len(pool)][1]) for i in range(n)]
+    bases = [g for _, g in pool] + api.generate(prog, grids=[1, 2, 4, 8, 16, 32, 64, 128],
+                                                loops=[1, 2, 4, 8, 16, 32, 64])
+    cands = F.search_stream(bases, n, seed=1)
+    js = [json.dumps(cands[i % len(cands)]) for i in range(n)]
     gp = ctx.compile(prog)
     ctx.verify_batch(gp, ctx.compile_many(js[:64])[0], np.arange(64, dtype=np.uint64), want_verdicts=False)
     torch.cuda.synchronize()
@@ -37,6 +42,6 @@ for fam, (prog, pool) in F.verify_families().items():
     tot_v += t2 - t1
     cnt += n
     print(f"{fam:9s} n={n} compile {n / (t1 - t0):10.0f}/s  verify {n / (t2 - t1):10.0f}/s  "
-          f"end-to-end {n / (t2 - t0):10.0f} cand/s  accepted {int(acc.sum())}", flush=True)
+          f"end-to-end {n / (t2 - t0):10.0f} cand/s  accepted {int(acc.sum())}  distinct {len(cands)}", flush=True)
 print(f"all      n={cnt} compile {cnt / tot_c:10.0f}/s  verify {cnt / tot_v:10.0f}/s  "
       f"end-to-end {cnt / (tot_c + tot_v):10.0f} cand/s  host threads {os.cpu_count()}")

@@ -84,3 +84,28 @@ def test_unsupported_program():
     prog = gb.finish([gb.op(O.Reshape, [a], {"target": [8, 4]})])
     with pytest.raises(N.NativeError):
         api.generate(prog)
+
+
+@pytest.mark.parametrize("fam", list(F.VERIFY_SHAPES))
+def test_search_stream_distinct_valid_deterministic(fam):
+    """The bench / test search stream: the pool, the generator's candidates
+    and their op-rewrite mutants — distinct, all valid, deterministic."""
+    import json
+    prog, pool = F.verify_families()[fam]
+    bases = [g for _, g in pool] + api.generate(prog, grids=[1, 2, 4], loops=[1, 2, 4])
+    s = F.search_stream(bases, 600, seed=3)
+    assert len(s) == 600
+    assert len({json.dumps(g, sort_keys=True) for g in s}) == 600
+    assert all(api.validate(g)[0] == 0 for g in s[::7])
+    assert s == F.search_stream(bases, 600, seed=3)
+
+
+@needs_ref
+def test_search_stream_mutants_mostly_rejected():
+    """Mutants are what a search mostly proposes: non-equivalent graphs the
+    reference verifier rejects; with RMSNorm's extra sqrt many end
+    Inconclusive (resamples exhausted), a few raise or stay equivalent."""
+    prog, pool = F.verify_families()["rmsnorm"]
+    s = F.search_stream([g for _, g in pool], 400, seed=3)[len(pool):]
+    kinds = [ref.random_test_equivalence(prog, g, num_tests=1, seed=5)["kind"] for g in s[::20]]
+    assert kinds.count(1) >= len(kinds) // 3 and kinds.count(0) <= len(kinds) // 4

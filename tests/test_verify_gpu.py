@@ -8,6 +8,8 @@ import numpy as np
 import pytest
 
 from oracle import ref
+from paper_2405_05751_b200 import _native as N
+from paper_2405_05751_b200 import api
 from paper_2405_05751_b200 import fixtures as F
 from paper_2405_05751_b200.graph import PHI, BlockBuilder, GraphBuilder, OpType as O
 
@@ -188,17 +190,21 @@ def test_distinct_candidate_stream_matches_reference(ctx):
     batch (parallel lowering + bytecode assembly) — verdicts bit-exact."""
     import json
     rng = np.random.default_rng(7)
-    for fam in ("rmsnorm", "gqa"):
+    for fam in ("rmsnorm", "gqa", "lora", "gatedmlp"):
         prog, pool = FAMS[fam]
-        idx = rng.integers(0, len(pool), 300)
-        texts = [json.dumps(pool[i][1]) for i in idx]
+        # the pool, the generator's candidates and their mutants
+        bases = [g for _, g in pool] + api.generate(prog, grids=[1, 2, 4, 8, 16], loops=[1, 2, 4, 8, 16])
+        stream = F.search_stream(bases, 3000, seed=5)
+        idx = rng.integers(0, len(stream), 300)
+        cands = [stream[i] for i in idx]
+        texts = [json.dumps(g) for g in cands]
         gs, st = ctx.compile_many(texts)
         assert all(s == 0 for s in st)
         assert len({g.h.value for g in gs}) == len(gs)  # no dedup: 300 distinct handles
         seeds = rng.integers(0, 2**62, 300, dtype=np.uint64)
         got, acc = ctx.verify_batch(prog, gs, seeds)
         for k in range(0, 300, 3):
-            w = ref.random_test_equivalence(prog, pool[idx[k]][1], num_tests=1, seed=int(seeds[k]))
+            w = ref.random_test_equivalence(prog, cands[k], num_tests=1, seed=int(seeds[k]))
             for c in VCOLS:
                 assert got[c][k] == w[c], (fam, k, c)
         assert np.array_equal(acc, got["kind"] == 0)
@@ -300,3 +306,50 @@ def test_full_shape_verification_matches_reference(ctx, name):
         for c in VCOLS:
             assert got[c][k] == wants[k][c], (name, k, c)
     assert list(acc) == [w["kind"] == 0 for w in wants]
+
+
+def _exp_heavy(fam, n, seed):
+    """Search-stream mutants with two or more EwExp ops: most exponentiate a
+    q-undefined value (PoisonedExponent unless a resample comes first)."""
+    prog, pool = FAMS[fam]
+    bases = [g for _, g in pool] + api.generate(prog, grids=[1, 2, 4, 8, 16], loops=[1, 2, 4, 8, 16])
+    out = []
+    for g in F.search_stream(bases, 6000, seed=seed):
+        ops = [o["type"] for op in g["ops"] for o in op.get("blockGraph", {}).get("ops", [])]
+        if ops.count("ewexp") >= 2:
+            out.append(g)
+    return prog, out[:n]
+
+
+@pytest.mark.parametrize("fam", ["rmsnorm", "gqa", "lora", "gatedmlp"])
+def test_poisoned_exponent_ordering_matches_reference(ctx, fam):
+    """Error(PoisonedExponent) is raised where the reference evaluates the
+    offending EwExp: a DivByZero / NonResidue evaluated before it (the
+    program, earlier ops, grid block 0 of its GraphDef) turns the attempt
+    into a resample (Inconclusive after 17), any later one does not."""
+    prog, cands = _exp_heavy(fam, 120, seed=11)
+    assert len(cands) >= 40
+    rng = np.random.default_rng(3)
+    seeds = rng.integers(0, 2**62, len(cands), dtype=np.uint64)
+    got, acc = ctx.verify_batch(prog, cands, seeds)
+    kinds = set()
+    for k, g in enumerate(cands):
+        w = ref.random_test_equivalence(prog, g, num_tests=1, seed=int(seeds[k]))
+        kinds.add((w["kind"], w["err_code"]))
+        for c in VCOLS:
+            assert got[c][k] == w[c], (fam, k, c, w)
+    assert (3, 1006) in kinds
+
+
+def test_poisoned_ff_eval_status_matches_reference(ctx):
+    """tpo_gpu_ff_eval: ResampleNeeded (2000 + code) or Error(PoisonedExponent)
+    by evaluation order, as ff_eval throws."""
+    _, cands = _exp_heavy("rmsnorm", 30, seed=13)
+    for g in cands:
+        for stream in range(3):
+            w = ref.ff_attempt(g, 5, stream)
+            try:
+                rc = ctx.ff_eval(g, 5, stream)["rc"]
+            except N.NativeError as e:
+                rc = e.status
+            assert rc == w["rc"], (stream, rc, w["rc"])

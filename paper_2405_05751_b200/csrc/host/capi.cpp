@@ -828,6 +828,7 @@ int tpo_gpu_verify_batch(tpo_gpu_ctx *ctx, const tpo_gpu_graph *program,
       }
       return 0;
     };
+    if (std::getenv("TPO_VM_GLOBAL")) return global_loop();  // test hook: force the HBM executor
     std::unordered_map<const tpo_gpu_graph *, uint32_t> idx;
     std::vector<const Graph *> uniq;
     std::vector<uint32_t> cg(n);

@@ -4,6 +4,8 @@ accumulators; an empty graph lists nothing; every DimMap of the JSON
 appears in the listing — plus the B200 execution line."""
 import re
 
+import pytest
+
 from paper_2405_05751_b200 import api
 from paper_2405_05751_b200 import fixtures as F
 
@@ -51,3 +53,14 @@ def test_vm_line_for_unfused_graphs():
     txt = api.describe(prog)
     m = re.search(r"VM bytecode: (\d+) instructions in (\d+) barrier phases", txt)
     assert m and 0 < int(m.group(2)) <= int(m.group(1))
+
+
+@pytest.mark.parametrize("fam", ["rmsnorm", "gatedmlp", "gqa", "lora"])
+def test_mutants_never_take_a_fused_kernel(fam):
+    """An op-rewrite mutant of a BASELINE µGraph computes something else: the
+    structural fused-kernel match must reject it (the generic VM runs it)."""
+    from paper_2405_05751_b200 import fixtures as F
+    _, mu = F.bench_pair(fam)
+    assert "B200: fused" in api.describe(mu)
+    for g in F.search_stream([mu], 40, seed=2)[1:]:
+        assert "no fused kernel" in api.describe(g)

@@ -155,3 +155,32 @@ def test_stability_filter_full_shape(ctx):
         want = ref.float_stability_filter(cand, prog, trials=1, seed=17)
         assert got == want
     assert ctx.float_stability_filter(mu, prog, trials=1, seed=17)
+
+
+def _mutants(fam, n, seed):
+    """Generator candidates and op-rewrite mutants (fixtures.search_stream)."""
+    from paper_2405_05751_b200 import api
+    prog, pool = F.verify_families()[fam]
+    bases = [g for _, g in pool] + api.generate(prog, grids=[1, 2, 4, 8, 16], loops=[1, 2, 4, 8, 16])
+    s = F.search_stream(bases, 4000, seed=seed)
+    return prog, s[len(bases):][::max(1, (len(s) - len(bases)) // n)][:n]
+
+
+@pytest.mark.parametrize("fam", ["rmsnorm", "gatedmlp", "gqa", "lora"])
+def test_eval_vm_on_mutants_matches_reference(ctx, fam):
+    """fp64 eval_mugraph of search-stream mutants (NaN / inf from sqrt of
+    negatives and division included) equals the reference."""
+    _, cands = _mutants(fam, 40, seed=21)
+    for g in cands:
+        ins = _inputs(g, 9)
+        _close(ctx.eval_vm(g, ins, mode=0), ref.eval_mugraph(g, ins, mode=0), g)
+
+
+def test_stability_batch_on_mutants_matches_reference(ctx):
+    for fam in ("rmsnorm", "gqa", "lora"):
+        prog, cands = _mutants(fam, 60, seed=23)
+        seeds = np.arange(len(cands), dtype=np.uint64) * 104729 + 5
+        ok = ctx.stability_batch(prog, cands, seeds=seeds, trials=2)
+        for k in range(len(cands)):
+            want = ref.float_stability_filter(cands[k], prog, trials=2, seed=int(seeds[k]))
+            assert ok[k] == int(want), (fam, k)

@@ -353,3 +353,17 @@ def test_poisoned_ff_eval_status_matches_reference(ctx):
             except N.NativeError as e:
                 rc = e.status
             assert rc == w["rc"], (stream, rc, w["rc"])
+
+
+def test_poisoned_exponent_global_executor(ctx, monkeypatch):
+    """The global-memory field executor (graphs beyond shared memory) stops
+    at the same VM_RAISE with the same event rule."""
+    prog, cands = _exp_heavy("gqa", 36, seed=17)
+    seeds = np.arange(len(cands), dtype=np.uint64) * 7 + 1
+    monkeypatch.setenv("TPO_VM_GLOBAL", "1")
+    got, _ = ctx.verify_batch(prog, cands, seeds)
+    monkeypatch.delenv("TPO_VM_GLOBAL")
+    for k, g in enumerate(cands):
+        w = ref.random_test_equivalence(prog, g, num_tests=1, seed=int(seeds[k]))
+        for c in VCOLS:
+            assert got[c][k] == w[c], (k, c, w)

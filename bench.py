@@ -388,7 +388,9 @@ def reference_arm(args, wl):
     times = [ref.time_eval_parallel(graphs, inputs, 1) for _ in range(max(1, args.steps))]
     ms = float(np.mean(times))
     v = round(1e3 / ms, 5)
-    return {"metric": METRIC, "value": v, "unit": "evals/s", "n_gpus": 0, "steps": len(times),
+    # n_gpus: the launch's N (the driver runs both arms alike); the work runs
+    # on rank 0's host cores only ("cpu_baseline.cores")
+    return {"metric": METRIC, "value": v, "unit": "evals/s", "n_gpus": args.gpus, "steps": len(times),
             "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",

@@ -367,3 +367,24 @@ def test_poisoned_exponent_global_executor(ctx, monkeypatch):
         w = ref.random_test_equivalence(prog, g, num_tests=1, seed=int(seeds[k]))
         for c in VCOLS:
             assert got[c][k] == w[c], (k, c, w)
+
+
+@pytest.mark.parametrize("fam", ["rmsnorm", "gatedmlp", "gqa", "lora"])
+def test_ff_attempt_bit_exact_on_mutants(ctx, fam):
+    """One verifier attempt (inputs, ω, outputs, resample status) on
+    search-stream mutants: bit-exact with the reference."""
+    prog, pool = FAMS[fam]
+    bases = [g for _, g in pool] + api.generate(prog, grids=[1, 2, 4, 8, 16], loops=[1, 2, 4, 8, 16])
+    s = F.search_stream(bases, 3000, seed=29)[len(bases):]
+    for g in s[::max(1, len(s) // 30)][:30]:
+        w = ref.ff_attempt(g, 19, 0)
+        try:
+            got = ctx.ff_eval(g, 19, 0)
+        except N.NativeError as e:
+            assert e.status == w["rc"]
+            continue
+        assert got["rc"] == w["rc"] and got["omega"] == w["omega"]
+        if got["rc"] == 0:
+            for (a, b, c), (x, y, z) in zip(got["out"], w["out"]):
+                assert np.array_equal(a, x) and np.array_equal(c, z)
+                assert np.array_equal(b[c == 1], y[z == 1])

@@ -587,7 +587,8 @@ def search_stream(ctx, dist, fams, pool_fams, per_fam_total=25000):
     for f in pool_fams:
         prog, pool = fams[f]
         bases = [g for _, g in pool] + api.generate(prog, grids=[1, 2, 4, 8, 16, 32, 64, 128],
-                                                    loops=[1, 2, 4, 8, 16, 32, 64])
+                                                    loops=[1, 2, 4, 8, 16, 32, 64], max_kernels=3,
+                                                    max_candidates=2000)
         cands = F.search_stream(bases, per_fam_total, seed=1)
         distinct += len(cands)
         texts.append((ctx.compile(prog), [json.dumps(cands[i % len(cands)]) for i in range(first, first + n)]))

@@ -269,8 +269,13 @@ int tpo_gpu_parse_check(const char *json_in, int32_t *fast_accepted, int32_t *sa
  * generator.cpp): single-GraphDef µGraphs for a
  * single-output computation graph, by enumerating grid / for-loop
  * partitions of its dimension labels and placing φ-Accums by partition
- * state (tpo/ir/generator.hpp).  config_json (nullable): {"grids": [..],
- * "loops": [..], "rewrite": bool, "max_candidates": n, "smem_bytes": n}.
+ * state (tpo/ir/generator.hpp); with "max_kernels" > 1 also µGraphs of up
+ * to that many kernels chained through device tensors (contiguous
+ * single-output segments of the op list, each a pre-defined kernel op or
+ * one of its first "per_segment" fused GraphDefs; Algorithm 1's kernel
+ * level).  config_json (nullable): {"grids": [..], "loops": [..],
+ * "rewrite": bool, "max_candidates": n, "smem_bytes": n, "max_kernels": n,
+ * "per_segment": n}.
  * Output JSON: {"candidates": [graph, ...], "stats": {...}}; every candidate
  * passes validate; equivalence is the verifier's job. */
 int tpo_gpu_generate(const char *program_json, const char *config_json, char *json_out, int64_t cap,

@@ -71,11 +71,15 @@ def plan_block_graphs(g, smem_bytes: int = 0, elem_size: int = 2) -> dict:
 
 
 def generate(program, grids=None, loops=None, rewrite: bool = True, max_candidates: int = 4096,
-             with_stats: bool = False):
-    """Fused-kernel candidates for a computation graph (``tpo_gpu_generate``):
-    single-GraphDef µGraphs over grid / for-loop partitions, each valid under
+             with_stats: bool = False, max_kernels: int = 1, per_segment: int = 3):
+    """µGraph candidates for a computation graph (``tpo_gpu_generate``):
+    single-GraphDef µGraphs over grid / for-loop partitions and, with
+    ``max_kernels`` > 1, µGraphs of up to that many kernels (contiguous
+    single-output segments of the op list, each a pre-defined kernel op or
+    one of its first ``per_segment`` fused GraphDefs).  Each is valid under
     B200 limits; equivalence is left to the verifier."""
-    cfg = {"rewrite": rewrite, "max_candidates": max_candidates}
+    cfg = {"rewrite": rewrite, "max_candidates": max_candidates, "max_kernels": max_kernels,
+           "per_segment": per_segment}
     if grids is not None:
         cfg["grids"] = list(grids)
     if loops is not None:

@@ -1512,8 +1512,10 @@ extern "C" int tpo_gpu_generate(const char *program_json, const char *config_jso
     if (c.contains("rewrite")) cfg.rewrite = c.at("rewrite").get<bool>();
     if (c.contains("max_candidates")) cfg.max_candidates = c.at("max_candidates").get<size_t>();
     if (c.contains("smem_bytes")) cfg.limits.smem_bytes = c.at("smem_bytes").get<int64_t>();
+    if (c.contains("max_kernels")) cfg.max_kernels = c.at("max_kernels").get<int>();
+    if (c.contains("per_segment")) cfg.per_segment = c.at("per_segment").get<int>();
     ir::GenStats st;
-    const auto cands = ir::generate_fused(ir::kernel_graph_from_json(j), cfg, &st);
+    const auto cands = ir::generate_multi(ir::kernel_graph_from_json(j), cfg, &st);
     nlohmann::json arr = nlohmann::json::array();
     for (const auto &g : cands) arr.push_back(ir::to_json(g));
     const std::string s = nlohmann::json{{"candidates", arr},

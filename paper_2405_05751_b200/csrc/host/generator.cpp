@@ -347,4 +347,157 @@ std::vector<KernelGraph> generate_fused(const KernelGraph &program, const GenCon
   return out;
 }
 
+namespace {
+
+// The sub-program of ops [b, e): inputs are the tensors it reads that it does
+// not produce (in first-use order), the output is `out`.
+KernelGraph segment_program(const KernelGraph &p, size_t b, size_t e, TensorId out,
+                            std::vector<TensorId> &seg_inputs) {
+  GraphBuilder gb;
+  std::vector<TensorId> map(p.tensors.size(), -1);
+  seg_inputs.clear();
+  for (size_t k = b; k < e; ++k)
+    for (TensorId t : p.ops[k].inputs)
+      if (map[size_t(t)] < 0) {
+        bool inner = false;
+        for (size_t j = b; j < k; ++j) inner = inner || p.ops[j].outputs[0] == t;
+        if (!inner) {
+          map[size_t(t)] = gb.input(p.tensor(t).shape);
+          seg_inputs.push_back(t);
+        }
+      }
+  for (size_t k = b; k < e; ++k) {
+    std::vector<TensorId> in;
+    for (TensorId t : p.ops[k].inputs) in.push_back(map[size_t(t)]);
+    map[size_t(p.ops[k].outputs[0])] = gb.op(p.ops[k].type, in, p.ops[k].attrs);
+  }
+  return gb.finish({map[size_t(out)]});
+}
+
+}  // namespace
+
+std::vector<KernelGraph> generate_multi(const KernelGraph &program, const GenConfig &cfg, GenStats *stats) {
+  GenStats st;
+  std::vector<KernelGraph> out = generate_fused(program, cfg, &st);
+  std::set<std::string> seen;
+  for (const KernelGraph &g : out) seen.insert(canonical_key(g));
+  const KernelGraph &p = program;
+  const size_t n = p.ops.size();
+  if (cfg.max_kernels < 2 || n < 2 || n > 16) {
+    if (stats) *stats = st;
+    return out;
+  }
+  std::vector<int> prod(p.tensors.size(), -1);
+  for (size_t k = 0; k < n; ++k) prod[size_t(p.ops[k].outputs[0])] = int(k);
+  // segment [b, e) -> its single externally used output, or -1
+  auto seg_out = [&](size_t b, size_t e) -> TensorId {
+    TensorId o = -1;
+    for (size_t k = b; k < e; ++k) {
+      const TensorId t = p.ops[k].outputs[0];
+      bool ext = std::find(p.outputs.begin(), p.outputs.end(), t) != p.outputs.end();
+      for (size_t j = e; j < n && !ext; ++j)
+        for (TensorId x : p.ops[j].inputs) ext = ext || x == t;
+      if (ext) {
+        if (o >= 0) return -2;
+        o = t;
+      }
+    }
+    return o;
+  };
+  // per segment: the options (kernel-level op, fused candidates), memoised
+  std::map<std::pair<size_t, size_t>, std::vector<KernelGraph>> fused;
+  auto options = [&](size_t b, size_t e, TensorId o, std::vector<TensorId> &ins) -> const std::vector<KernelGraph> & {
+    auto key = std::make_pair(b, e);
+    auto it = fused.find(key);
+    KernelGraph sp = segment_program(p, b, e, o, ins);
+    if (it != fused.end()) return it->second;
+    GenConfig c = cfg;
+    c.max_candidates = size_t(cfg.per_segment);
+    std::vector<KernelGraph> v;
+    try {
+      v = generate_fused(sp, c, nullptr);
+    } catch (const Error &) {
+    }
+    return fused.emplace(key, std::move(v)).first->second;
+  };
+  // every cut of the op list into 2..max_kernels contiguous segments
+  for (uint32_t mask = 1; mask < (1u << (n - 1)) && out.size() < cfg.max_candidates; ++mask) {
+    if (__builtin_popcount(mask) + 1 > cfg.max_kernels) continue;
+    std::vector<std::pair<size_t, size_t>> segs;
+    size_t b = 0;
+    for (size_t k = 1; k <= n; ++k)
+      if (k == n || (mask >> (k - 1)) & 1u) segs.push_back({b, k}), b = k;
+    ++st.partitions;
+    struct Seg {
+      TensorId out;
+      std::vector<TensorId> ins;
+      std::vector<const KernelGraph *> fused;
+      bool flat;  // one op: a pre-defined kernel op is an option
+    };
+    std::vector<Seg> S;
+    bool ok = true;
+    for (auto [sb, se] : segs) {
+      Seg sg;
+      sg.out = seg_out(sb, se);
+      if (sg.out < 0) {
+        ok = false;
+        break;
+      }
+      for (const KernelGraph &g : options(sb, se, sg.out, sg.ins)) sg.fused.push_back(&g);
+      sg.flat = se - sb == 1;
+      if (sg.fused.empty() && !sg.flat) {
+        ok = false;
+        break;
+      }
+      S.push_back(std::move(sg));
+    }
+    if (!ok) {
+      ++st.rejected_structure;
+      continue;
+    }
+    // mixed-radix walk over the per-segment choices (flat op first)
+    std::vector<size_t> radix, idx(S.size(), 0);
+    for (const Seg &sg : S) radix.push_back(sg.fused.size() + (sg.flat ? 1 : 0));
+    for (;;) {
+      if (out.size() >= cfg.max_candidates) break;
+      bool any_fused = false;
+      GraphBuilder gb;
+      std::vector<TensorId> map(p.tensors.size(), -1);
+      for (TensorId t : p.inputs) map[size_t(t)] = gb.input(p.tensor(t).shape);
+      for (size_t s = 0; s < S.size(); ++s) {
+        const Seg &sg = S[s];
+        std::vector<TensorId> in;
+        for (TensorId t : sg.ins) in.push_back(map[size_t(t)]);
+        const size_t c = idx[s];
+        if (sg.flat && c == 0) {
+          const Op &op = p.ops[size_t(segs[s].first)];
+          map[size_t(sg.out)] = gb.op(op.type, in, op.attrs);
+        } else {
+          const KernelGraph &fg = *sg.fused[c - (sg.flat ? 1 : 0)];
+          const Op &gd = fg.ops.at(0);
+          std::vector<TensorShape> oshapes{fg.tensor(fg.outputs[0]).shape};
+          map[size_t(sg.out)] = gb.graphdef(in, gd.block, oshapes);
+          any_fused = true;
+        }
+      }
+      if (any_fused) {
+        KernelGraph g = gb.finish({map[size_t(p.outputs[0])]});
+        ++st.placements;
+        if (!validate(g, cfg.limits).valid()) {
+          ++st.rejected_validate;
+        } else if (!seen.insert(canonical_key(g)).second) {
+          ++st.duplicates;
+        } else {
+          out.push_back(std::move(g));
+        }
+      }
+      size_t s = 0;
+      while (s < idx.size() && ++idx[s] == radix[s]) idx[s++] = 0;
+      if (s == idx.size()) break;
+    }
+  }
+  if (stats) *stats = st;
+  return out;
+}
+
 }  // namespace tpo::ir

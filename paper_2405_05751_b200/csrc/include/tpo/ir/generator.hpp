@@ -44,6 +44,12 @@ struct GenConfig {
   bool rewrite = true;          // also try the row-scale rewrite of the program
   size_t max_candidates = 4096;
   MemLimits limits = kB200Limits;
+  // Multi-kernel µGraphs (generate_multi): at most this many kernels, each a
+  // contiguous single-output segment of the program's op list lowered as a
+  // pre-defined kernel op (one-op segments) or one of the first
+  // `per_segment` fused GraphDef candidates of the segment.
+  int max_kernels = 1;
+  int per_segment = 3;
 };
 
 struct GenStats {
@@ -57,6 +63,16 @@ struct GenStats {
 // Throws Error(Unsupported) for a program that is not a single-output
 // computation graph of Matmul / Ew* / Sqr / Sqrt / SiLU / full-group Sum.
 std::vector<KernelGraph> generate_fused(const KernelGraph &program, const GenConfig &cfg,
+                                        GenStats *stats = nullptr);
+
+// Algorithm 1's kernel level: µGraphs of up to cfg.max_kernels kernels.  The
+// program's op list (a topological order) is cut into contiguous segments
+// with one externally used output each; every segment becomes a
+// pre-defined kernel op (a one-op segment) or a fused GraphDef from
+// generate_fused on the segment's sub-program; the kernels are chained
+// through device tensors.  Includes generate_fused's single-kernel
+// candidates; deduplicated by canonical key; deterministic.
+std::vector<KernelGraph> generate_multi(const KernelGraph &program, const GenConfig &cfg,
                                         GenStats *stats = nullptr);
 
 }  // namespace tpo::ir

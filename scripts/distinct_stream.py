@@ -25,7 +25,8 @@ tot_c = tot_v = 0.0
 cnt = 0
 for fam, (prog, pool) in F.verify_families().items():
     bases = [g for _, g in pool] + api.generate(prog, grids=[1, 2, 4, 8, 16, 32, 64, 128],
-                                                loops=[1, 2, 4, 8, 16, 32, 64])
+                                                loops=[1, 2, 4, 8, 16, 32, 64], max_kernels=3,
+                                                max_candidates=2000)
     cands = F.search_stream(bases, n, seed=1)
     js = [json.dumps(cands[i % len(cands)]) for i in range(n)]
     gp = ctx.compile(prog)

@@ -109,3 +109,26 @@ def test_search_stream_mutants_mostly_rejected():
     s = F.search_stream([g for _, g in pool], 400, seed=3)[len(pool):]
     kinds = [ref.random_test_equivalence(prog, g, num_tests=1, seed=5)["kind"] for g in s[::20]]
     assert kinds.count(1) >= len(kinds) // 3 and kinds.count(0) <= len(kinds) // 4
+
+
+@needs_ref
+@pytest.mark.parametrize("fam", list(F.VERIFY_SHAPES))
+def test_multi_kernel_candidates_valid_and_equivalent(fam):
+    """Algorithm 1's kernel level: µGraphs of 2-4 kernels (pre-defined kernel
+    ops and fused GraphDefs chained through device tensors) — all valid under
+    the reference's validate, a sample Equivalent under its verifier."""
+    prog, _ = F.verify_families()[fam]
+    single = api.generate(prog, grids=[1, 2, 4], loops=[1, 2, 4])
+    cands = api.generate(prog, grids=[1, 2, 4], loops=[1, 2, 4], max_kernels=4)
+    multi = cands[len(single):]
+    assert cands[:len(single)] == single and len(multi) >= 50
+    kinds_per_graph = {len(g["ops"]) for g in multi}
+    assert {2, 3} <= kinds_per_graph
+    assert any(op["type"] != "graphdef" for g in multi for op in g["ops"])  # kernel-level ops
+    assert any(sum(op["type"] == "graphdef" for op in g["ops"]) >= 2 for g in multi)
+    for g in multi:
+        assert ref.validate(g) == 0
+    for g in multi[::17]:
+        v = ref.random_test_equivalence(prog, g, num_tests=1, seed=5)
+        assert v["kind"] in (0, 2), v
+    assert cands == api.generate(prog, grids=[1, 2, 4], loops=[1, 2, 4], max_kernels=4)

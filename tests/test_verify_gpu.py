@@ -388,3 +388,19 @@ def test_ff_attempt_bit_exact_on_mutants(ctx, fam):
             for (a, b, c), (x, y, z) in zip(got["out"], w["out"]):
                 assert np.array_equal(a, x) and np.array_equal(c, z)
                 assert np.array_equal(b[c == 1], y[z == 1])
+
+
+@pytest.mark.parametrize("fam", ["rmsnorm", "gatedmlp", "gqa", "lora"])
+def test_multi_kernel_candidates_verified_like_reference(ctx, fam):
+    """Generator µGraphs of 2-4 kernels (kernel-level ops + GraphDefs) through
+    the batched verifier: every verdict field equals the reference's."""
+    prog, _ = FAMS[fam]
+    cands = api.generate(prog, grids=[1, 2, 4], loops=[1, 2, 4], max_kernels=4)
+    cands = [g for g in cands if len(g["ops"]) > 1][::5][:80]
+    seeds = np.arange(len(cands), dtype=np.uint64) * 977 + 3
+    got, acc = ctx.verify_batch(prog, cands, seeds)
+    for k, g in enumerate(cands):
+        w = ref.random_test_equivalence(prog, g, num_tests=1, seed=int(seeds[k]))
+        for c in VCOLS:
+            assert got[c][k] == w[c], (fam, k, c)
+    assert acc.sum() >= len(cands) * 3 // 4

@@ -62,14 +62,16 @@ def cost(g: dict, elem_size: int = 2, w_device: float = 1.0, w_shared: float = 0
 
 def optimize(ctx: "api.Context", program: dict, grids=(1, 2, 4, 8, 16, 32, 64, 128),
              loops=(1, 2, 4, 8, 16, 32, 64), num_tests: int = 2, seed: int = 0,
-             stability: bool = True, prefer_fused: bool = True, max_resamples: int = 16) -> Dict:
+             stability: bool = True, prefer_fused: bool = True, max_resamples: int = 16,
+             max_kernels: int = 1) -> Dict:
     """generate -> verify -> stability -> select.  Returns the best candidate,
     its cost and describe() listing, the ranked survivors and stage counts
     (non-increasing, SPEC.md PipelineReport).  Works at any shape: graphs
     beyond shared memory are verified and filtered on the global-memory
     executors.  ``prefer_fused``: candidates that lower to a hand-written
-    sm_100a kernel rank first (the SPEC cost does not model parallelism)."""
-    cands = api.generate(program, grids=grids, loops=loops)
+    sm_100a kernel rank first (the SPEC cost does not model parallelism).
+    ``max_kernels`` > 1 adds the generator's multi-kernel µGraphs."""
+    cands = api.generate(program, grids=grids, loops=loops, max_kernels=max_kernels)
     graphs, status = ctx.compile_many(cands)
     ok = [i for i, s in enumerate(status) if s == 0]
     report = {"generated": len(cands), "compiled": len(ok)}

@@ -261,6 +261,11 @@ def test_optimize_pipeline(ctx):
     assert [op["type"] for op in best["ops"]] == ["graphdef"]
     assert ref.random_test_equivalence(prog, best, num_tests=4, seed=5)["kind"] == 0
     assert "forloop" in rep["describe"]
+    # with the kernel level: more candidates survive, the single fused
+    # kernel still ranks first (fewer launches and device bytes)
+    rep3 = pipeline.optimize(ctx, prog, grids=[1, 2, 4, 8, 16], loops=[1, 2, 4, 8, 16], max_kernels=3)
+    assert rep3["generated"] > rep["generated"] and rep3["stable"] > rep["stable"]
+    assert [op["type"] for op in rep3["best"]["ops"]] == ["graphdef"]
 
 
 def test_rejection_rate_and_no_false_negatives(ctx):

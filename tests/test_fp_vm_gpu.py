@@ -184,3 +184,20 @@ def test_stability_batch_on_mutants_matches_reference(ctx):
         for k in range(len(cands)):
             want = ref.float_stability_filter(cands[k], prog, trials=2, seed=int(seeds[k]))
             assert ok[k] == int(want), (fam, k)
+
+
+def test_multi_kernel_candidates_fp_and_stability(ctx):
+    """The generator's multi-kernel µGraphs on the fp64 VM (eval_mugraph) and
+    through the batched stability filter: identical to the reference."""
+    from paper_2405_05751_b200 import api
+    for fam in ("rmsnorm", "gatedmlp", "gqa", "lora"):
+        prog, _ = F.verify_families()[fam]
+        cands = [g for g in api.generate(prog, grids=[1, 2, 4], loops=[1, 2, 4], max_kernels=4)
+                 if len(g["ops"]) > 1][::9][:30]
+        for g in cands[::3]:
+            ins = _inputs(g, 4)
+            _close(ctx.eval_vm(g, ins, mode=0), ref.eval_mugraph(g, ins, mode=0), g)
+        seeds = np.arange(len(cands), dtype=np.uint64) * 31 + 2
+        ok = ctx.stability_batch(prog, cands, seeds=seeds, trials=2)
+        for k in range(len(cands)):
+            assert ok[k] == int(ref.float_stability_filter(cands[k], prog, trials=2, seed=int(seeds[k]))), (fam, k)

@@ -409,3 +409,50 @@ def test_multi_kernel_candidates_verified_like_reference(ctx, fam):
         for c in VCOLS:
             assert got[c][k] == w[c], (fam, k, c)
     assert acc.sum() >= len(cands) * 3 // 4
+
+
+def test_concurrent_contexts_match_sequential(ctx):
+    """SURVEY §8b threading: the reference is re-entrant; here a context is
+    single-stream and concurrency is one context per thread.  Four threads,
+    each with its own context, verify and evaluate at once: identical to the
+    sequential results."""
+    import threading
+    from paper_2405_05751_b200.api import Context
+    jobs = []
+    for fam in ("rmsnorm", "gatedmlp", "gqa", "lora"):
+        prog, pool = FAMS[fam]
+        cands = [g for _, g in pool] * 4
+        seeds = np.arange(len(cands), dtype=np.uint64) * 13 + 1
+        jobs.append((prog, cands, seeds))
+    want = []
+    for prog, cands, seeds in jobs:
+        v, a = ctx.verify_batch(prog, cands, seeds)
+        want.append((v, a, ctx.ff_eval(cands[1], 9, 0)))
+    got, errs = [None] * len(jobs), []
+
+    def work(i):
+        try:
+            c = Context(0)
+            prog, cands, seeds = jobs[i]
+            out = []
+            for _ in range(3):
+                v, a = c.verify_batch(prog, cands, seeds)
+                out.append((v, a, c.ff_eval(cands[1], 9, 0)))
+            got[i] = out
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(len(jobs))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for i, (v, a, fe) in enumerate(want):
+        for gv, ga, gfe in got[i]:
+            for c in VCOLS:
+                assert np.array_equal(gv[c], v[c]), (i, c)
+            assert np.array_equal(ga, a)
+            assert gfe["rc"] == fe["rc"] and gfe["omega"] == fe["omega"]
+            for x, y in zip(gfe["out"], fe["out"]):
+                assert all(np.array_equal(p, q) for p, q in zip(x, y))

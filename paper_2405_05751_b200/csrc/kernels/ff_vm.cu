@@ -528,6 +528,7 @@ __device__ bool run_program(const SmemT<WT> &s, const FieldConst &f, const TpoVm
                             uint32_t len, int *s_flag, unsigned long long *prof) {
   uint32_t it = 0, loop_pc = 0, trips = 1;
   long long t_prev = PROF ? clock64() : 0;
+  bool phase_bad = false;  // this thread saw an event since the last barrier
   for (uint32_t pc = 0; pc < len; ++pc) {
     const TpoVmInstr &I = code[pc];
     const uint8_t op = I.op;
@@ -554,15 +555,19 @@ __device__ bool run_program(const SmemT<WT> &s, const FieldConst &f, const TpoVm
     // the earliest failing instruction wins (as in the reference's
     // sequential evaluation, where it throws first)
     if (bad) atomicMax(s_flag, int(((0xffffu - pc) << 2) | (op == VM_UNARY ? 2u : 1u)));
+    phase_bad |= bad;
     if (I.flags & VM_NOSYNC) continue;
-    __syncthreads();
+    // the decision is the barrier's own OR: reading *s_flag after a plain
+    // barrier races with a faster warp's atomicMax in the next instruction
+    // (the warps would then disagree and their barriers fall out of step)
+    const bool any_bad = __syncthreads_or(phase_bad);
     if (PROF && threadIdx.x == 0) {
       const long long t = clock64();
       prof[op] += (unsigned long long)(t - t_prev);
       prof[16 + op] += 1;
       t_prev = t;
     }
-    if (*s_flag) return false;
+    if (any_bad) return false;
   }
   return true;
 }

@@ -14,6 +14,11 @@ for fam, (prog, pool) in F.verify_families().items():
     ctx.verify_pool(prog, gs, first=0, n=64, want_verdicts=True)
     ctx.verify_batch(prog, gs[:40], np.zeros(40, dtype=np.uint64))     # same-seed shared attempt
     ctx.stability_batch(prog, gs[:8])
+    # search-stream mutants, incl. raising (PoisonedExponent) graphs: VM_RAISE barriers
+    ms = F.search_stream(gs, 400, seed=3)[len(gs):]
+    ms = [g for g in ms if sum(o["type"] == "ewexp" for op in g["ops"]
+                               for o in op.get("blockGraph", {}).get("ops", [])) >= 2][:24] + ms[:24]
+    ctx.verify_batch(prog, ms, np.arange(len(ms), dtype=np.uint64))
 print("ok")
 PY
 cat > /tmp/san_fused.py <<'PY'

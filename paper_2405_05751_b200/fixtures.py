@@ -294,3 +294,42 @@ def search_stream(bases: List[dict], n: int, seed: int = 0) -> List[dict]:
                 break
         live = nxt
     return out
+
+
+def attribute_mutants(bases: List[dict], n: int, seed: int = 0) -> List[dict]:
+    """``n`` graphs with one block-graph attribute of a base redrawn — grid
+    x extent, for-loop trip count, an InIter imap / fmap, an OutSaver omap,
+    an Accum fmap or a Sum dim / group — most of them invalid (Definition 1,
+    shapes, divisibility), the valid ones re-partitioned µGraphs.  For
+    validate / verifier parity against the reference; deterministic."""
+    import copy
+    import random
+
+    rnd = random.Random(seed)
+    out = []
+    while len(out) < n:
+        g = copy.deepcopy(rnd.choice(bases))
+        gds = [op for op in g["ops"] if "blockGraph" in op]
+        if not gds:
+            continue
+        bg = rnd.choice(gds)["blockGraph"]
+        k = rnd.randint(0, 5)
+        if k == 0:
+            bg["grid"][0] = rnd.choice([1, 2, 3, 4, 8, 16, 32])
+        elif k == 1:
+            bg["forloop"] = rnd.choice([1, 2, 3, 4, 8, 16, 64])
+        else:
+            o = rnd.choice([o for o in bg["ops"] if o["type"] in ("initer", "outsaver", "accum", "sum")])
+            at = o["attrs"]
+            if o["type"] == "initer":
+                key = rnd.choice(["imap", "fmap"])
+                at[key] = {("x" if key == "imap" else "i"): rnd.choice(["phi", 0, 1, 2])}
+            elif o["type"] == "outsaver":
+                at["omap"] = {"x": rnd.choice(["phi", 0, 1, 2])}
+            elif o["type"] == "accum":
+                at["fmap"] = {"i": rnd.choice(["phi", 0, 1, 2])}
+            else:
+                at["dim"] = rnd.choice([0, 1, 2])
+                at["group"] = rnd.choice([1, 2, 4, 8, 16, 64])
+        out.append(g)
+    return out

@@ -132,3 +132,24 @@ def test_multi_kernel_candidates_valid_and_equivalent(fam):
         v = ref.random_test_equivalence(prog, g, num_tests=1, seed=5)
         assert v["kind"] in (0, 2), v
     assert cands == api.generate(prog, grids=[1, 2, 4], loops=[1, 2, 4], max_kernels=4)
+
+
+@needs_ref
+def test_validate_agrees_with_reference_on_attribute_mutants():
+    """Definition-1 validity of re-partitioned / re-mapped µGraphs (grid,
+    for-loop, imap / fmap / omap, Accum fmap, Sum dim / group redrawn):
+    identical to the reference's validate, valid or not."""
+    n_valid = 0
+    for fam in F.VERIFY_SHAPES:
+        prog, pool = F.verify_families()[fam]
+        bases = [g for _, g in pool] + api.generate(prog, grids=[1, 2, 4], loops=[1, 2, 4], max_kernels=3)
+        for g in F.attribute_mutants(bases, 300, seed=7):
+            r = ref.validate(g)
+            try:
+                ours = api.validate(g)[0]
+            except N.NativeError:
+                assert r != 0
+                continue
+            assert (ours == 0) == (r == 0)
+            n_valid += r == 0
+    assert n_valid >= 200

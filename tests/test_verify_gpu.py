@@ -456,3 +456,27 @@ def test_concurrent_contexts_match_sequential(ctx):
             assert gfe["rc"] == fe["rc"] and gfe["omega"] == fe["omega"]
             for x, y in zip(gfe["out"], fe["out"]):
                 assert all(np.array_equal(p, q) for p, q in zip(x, y))
+
+
+@pytest.mark.parametrize("fam", ["rmsnorm", "gatedmlp", "gqa", "lora"])
+def test_attribute_mutants_verified_like_reference(ctx, fam):
+    """Re-partitioned / re-mapped µGraphs that still pass validate (grid,
+    for-loop, imap / fmap / omap, Accum fmap, Sum dim / group redrawn): every
+    verdict field equals the reference's, and so does fp64 evaluation."""
+    prog, pool = FAMS[fam]
+    bases = [g for _, g in pool] + api.generate(prog, grids=[1, 2, 4], loops=[1, 2, 4], max_kernels=3)
+    cands = [g for g in F.attribute_mutants(bases, 600, seed=9) if ref.validate(g) == 0][:60]
+    assert len(cands) >= 30
+    seeds = np.arange(len(cands), dtype=np.uint64) * 7 + 11
+    got, _ = ctx.verify_batch(prog, cands, seeds)
+    for k, g in enumerate(cands):
+        w = ref.random_test_equivalence(prog, g, num_tests=1, seed=int(seeds[k]))
+        for c in VCOLS:
+            assert got[c][k] == w[c], (fam, k, c, w)
+    rs = np.random.default_rng(2)
+    for g in cands[::6]:
+        ins = [rs.standard_normal(g["tensors"][t]["shape"]) for t in g["inputs"]]
+        a = ctx.eval_vm(g, ins, mode=0)
+        b = ref.eval_mugraph(g, ins, mode=0)
+        for x, y in zip(a, b):
+            assert np.allclose(x, y, rtol=1e-12, atol=1e-12, equal_nan=True)

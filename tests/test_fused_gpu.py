@@ -202,3 +202,28 @@ def test_fused_concurrent_contexts(ctx):
     for n in names:
         for o in got[n]:
             assert torch.equal(o, want[n]), n
+
+
+@pytest.mark.parametrize("name", list(SMALL))
+def test_attribute_mutants_take_the_right_path(ctx, name):
+    """Valid attribute mutants of a fusable µGraph (grid, for-loop, maps,
+    Sum attrs redrawn): whichever path the backend picks — a fused kernel
+    when the mutant still matches one structurally, the generic VM otherwise —
+    its output equals the reference's eval_mugraph of that mutant."""
+    args, grid, fl = SMALL[name][0]
+    mu = F.family_mugraph(name, *args, grid=grid, forloop=fl)
+    ins = make_inputs(name, args, seed=4)
+    fused = 0
+    muts = [g for g in F.attribute_mutants([mu], 400, seed=13) if ref.validate(g) == 0][:12]
+    assert len(muts) >= 6
+    for g in muts:
+        h = ctx.compile(g)
+        fused += h.fused == name
+        out = ctx.eval_mugraph(h, [x.cuda() for x in ins])[0].cpu().numpy()
+        want = ref.eval_mugraph(g, [x.float().numpy() for x in ins])[0]
+        r = np.asarray(want, np.float64)
+        o = np.asarray(out, np.float64)
+        fin = np.isfinite(r)
+        assert np.array_equal(np.isfinite(o), fin)
+        scale = max(np.sqrt(np.mean(r[fin] ** 2)), 1e-30) if fin.any() else 1.0
+        assert np.max(np.abs(o[fin] - r[fin]), initial=0.0) <= 1e-3 * scale + 1e-3 * np.max(np.abs(r[fin]), initial=0.0)

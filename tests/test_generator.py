@@ -153,3 +153,11 @@ def test_validate_agrees_with_reference_on_attribute_mutants():
             assert (ours == 0) == (r == 0)
             n_valid += r == 0
     assert n_valid >= 200
+
+
+def test_attribute_mutants_deterministic():
+    prog, pool = F.verify_families()["gqa"]
+    bases = [g for _, g in pool]
+    a = F.attribute_mutants(bases, 50, seed=4)
+    assert a == F.attribute_mutants(bases, 50, seed=4) and len(a) == 50
+    assert a != F.attribute_mutants(bases, 50, seed=5)

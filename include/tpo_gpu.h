@@ -85,7 +85,23 @@ enum {
   TPO_FUSED_LORA = 4,
 };
 
-enum { TPO_DTYPE_F32 = 0, TPO_DTYPE_BF16 = 1 };
+enum { TPO_DTYPE_F32 = 0, TPO_DTYPE_BF16 = 1, TPO_DTYPE_F64 = 2 };
+
+/* Precision policy of the fused kernels (tpo_gpu_graph_set_precision).
+ * The reference evaluates in double (interp.hpp:47-48); the fused kernels
+ * multiply bf16 operands on the tensor cores with fp32 accumulation.
+ *   TPO_PREC_AUTO (default): all-bf16 inputs run the bf16 kernel (bf16 x
+ *     bf16 products are exact in fp32).  Any fp32 / fp64 input selects the
+ *     SPLIT kernel: every operand enters as bf16 hi + lo (x = hi + lo to
+ *     ~2^-16 relative), all hi/lo products accumulate in fp32, so the
+ *     result meets |o - r| <= 1e-3 * max(|r|, rms(r)) against the double
+ *     reference on arbitrary inputs (tests/test_precision_gpu.py), at twice
+ *     the weight bytes of the bf16 kernel.
+ *   TPO_PREC_BF16: round every input to bf16 and run the bf16 kernel (the
+ *     fast path for callers whose operands are bf16 by construction).
+ *   TPO_PREC_VM: no fused kernel — the generic GPU VM in the reference's
+ *     operation order (fp64 for fp64 inputs, else fp32 semantics). */
+enum { TPO_PREC_AUTO = 0, TPO_PREC_BF16 = 1, TPO_PREC_VM = 2 };
 
 typedef struct {
   int32_t n_inputs, n_outputs;
@@ -125,6 +141,9 @@ int tpo_gpu_graph_info(const tpo_gpu_graph *g, tpo_graph_info *out);
  * preceding work.  No reference counterpart (a launch-time property). */
 int tpo_gpu_graph_set_static_inputs(tpo_gpu_graph *g, uint64_t mask);
 
+/* Sets the graph's TPO_PREC_* policy (default TPO_PREC_AUTO). */
+int tpo_gpu_graph_set_precision(tpo_gpu_graph *g, int32_t policy);
+
 /* Shape of input/output `index` (is_output 0/1): writes rank dims, returns rank or <0. */
 int tpo_gpu_graph_shape(const tpo_gpu_graph *g, int is_output, int index, int64_t *dims);
 
@@ -134,22 +153,33 @@ int tpo_gpu_validate(const char *graph_json, int64_t smem_bytes, int64_t elem_si
                      int cap);
 
 /* Floating-point µGraph evaluation on device buffers (row-major, caller
- * owns).  Inputs are TPO_DTYPE_BF16 or _F32 per `in_dtype`; outputs fp32.
- * Benchmark µGraphs run as one fused sm_100a kernel (fused_kind != 0; bf16
- * operands, fp32 accumulation); any other µGraph runs on the generic GPU VM
- * in the reference's fp32 semantics (eval_mugraph_f32, interp.hpp:51-53).
- * Enqueued on `cuda_stream` (NULL = the legacy default stream); asynchronous. */
+ * owns).  Inputs are TPO_DTYPE_BF16, _F32 or _F64 per `in_dtype`; outputs
+ * fp32.  Benchmark µGraphs run as one fused sm_100a kernel (fused_kind != 0)
+ * under the graph's precision policy (TPO_PREC_*: bf16 operands for bf16
+ * inputs, split hi + lo operands for fp32 / fp64 inputs); any other µGraph,
+ * or TPO_PREC_VM, runs on the generic GPU VM in the reference's operation
+ * order: fp64 arithmetic (eval_mugraph, interp.hpp:47-48) when an input is
+ * fp64, else fp32 (eval_mugraph_f32, interp.hpp:51-53).  Operand conversions
+ * use context scratch.  Enqueued on `cuda_stream` (NULL = the legacy default
+ * stream); asynchronous. */
 int tpo_gpu_eval_mugraph(tpo_gpu_ctx *ctx, const tpo_gpu_graph *g, const void *const *in_dev,
                          const int32_t *in_dtype, float *const *out_dev, void *cuda_stream);
 
 /* Same evaluation from and to HOST buffers (pageable or pinned): inputs are
- * copied host->device (TPO_DTYPE_BF16 as is; TPO_DTYPE_F32 converted to bf16
- * on the device, round-to-nearest-even), the fused kernel runs, the fp32
- * outputs are copied back; synchronous on `cuda_stream` (NULL = the context
- * stream).  The call shape of tpo::interp::eval_mugraph
- * (proj/core/include/tpo/interp/interp.hpp:47-48) for host-resident tensors. */
+ * copied host->device in their dtype, converted on the device as the
+ * precision policy requires, evaluated, and the fp32 outputs copied back;
+ * synchronous on `cuda_stream` (NULL = the context stream). */
 int tpo_gpu_eval_mugraph_host(tpo_gpu_ctx *ctx, const tpo_gpu_graph *g, const void *const *in_host,
                               const int32_t *in_dtype, float *const *out_host, void *cuda_stream);
+
+/* The exact types of tpo::interp::eval_mugraph
+ * (proj/core/include/tpo/interp/interp.hpp:47-48): fp64 host tensors in,
+ * fp64 host tensors out.  A fused µGraph runs its SPLIT kernel (TPO_PREC_AUTO;
+ * tolerance above; TPO_PREC_BF16 rounds instead), any other µGraph — or
+ * TPO_PREC_VM — the generic VM in double arithmetic, bit-identical to the
+ * reference except exp / SiLU (last ulp).  Synchronous. */
+int tpo_gpu_eval_mugraph_f64(tpo_gpu_ctx *ctx, const tpo_gpu_graph *g, const double *const *in_host,
+                             double *const *out_host, void *cuda_stream);
 
 /* One verifier attempt for one graph, exactly as equiv.cpp:57-68 draws it
  * (Rng::derive(seed, stream); inputs; omega; SiLU tables iff with_silu).
@@ -167,7 +197,8 @@ int tpo_gpu_random_test_equivalence(tpo_gpu_ctx *ctx, const tpo_gpu_graph *g1,
                                     const tpo_field_params *fp, tpo_verdict *out);
 
 /* Batched verification: candidate k (k < n) is checked against `program`
- * with cfg {num_tests, seeds[k], max_resamples}; one verdict per candidate
+ * with cfg {num_tests, seeds[k], max_resamples} (seeds NULL: cfg->seed for
+ * every candidate, whatever executor the graphs need); one verdict per candidate
  * (host array, nullable) and packed accept bits (host, nullable; bit k set
  * iff Equivalent). */
 int tpo_gpu_verify_batch(tpo_gpu_ctx *ctx, const tpo_gpu_graph *program,

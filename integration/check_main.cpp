@@ -126,6 +126,41 @@ int main(int argc, char **argv) {
     CHECK(worst <= 1e-3, "%s eval_mugraph scaled err %.3e", fam, worst);
     std::printf("gpu: eval_mugraph %s max scaled err %.2e\n", fam, worst);
   }
+  // ---- gpu: the reference contract on ARBITRARY doubles (the inputs
+  // stability.cpp:30-38 feeds eval_mugraph: N(0,1)·scale, not bf16-rounded):
+  // fused µGraphs under TPO_PREC_AUTO (split hi + lo kernels) within
+  // 1e-3·max(|r|, rms(r)); TPO_PREC_VM and flat programs on the fp64 VM
+  // within 1e-12 relative (bit-identical except exp / SiLU)
+  auto scaled_err = [](const interp::FTensor &got, const interp::FTensor &want) {
+    double rms = 0, worst = 0;
+    for (double v : want.data) rms += v * v;
+    rms = std::sqrt(rms / double(want.data.size()));
+    for (size_t i = 0; i < want.data.size(); ++i)
+      worst = std::max(worst, std::fabs(got.data[i] - want.data[i]) / std::max(std::fabs(want.data[i]), rms));
+    return worst;
+  };
+  for (const char *fam : {"rmsnorm", "gatedmlp", "gqa", "lora"}) {
+    for (const std::string key : {std::string("fused/") + fam, std::string(fam) + "/program"}) {
+      ir::KernelGraph mu = G(key);
+      Rng rng(11);
+      std::vector<interp::FTensor> ins;
+      for (ir::TensorId t : mu.inputs) {
+        interp::FTensor x(mu.tensor(t).shape);
+        const double sc = std::string(fam) == "rmsnorm" ? 1.0 : 1.0 / std::sqrt(double(x.shape.dims.back()));
+        for (double &v : x.data) v = rng.normal() * sc;
+        ins.push_back(std::move(x));
+      }
+      if (std::string(fam) == "rmsnorm") ins[3].data[0] = 1.0 / double(ins[0].shape.dims[1]);
+      std::vector<interp::FTensor> want = interp::eval_mugraph(mu, ins);
+      const bool fused = gpu::CompiledGraph(nullptr, mu).has_fused_kernel();
+      const double e_auto = scaled_err(be.eval_mugraph(mu, ins, TPO_PREC_AUTO)[0], want[0]);
+      const double e_vm = scaled_err(be.eval_mugraph(mu, ins, TPO_PREC_VM)[0], want[0]);
+      CHECK(e_auto <= (fused ? 1e-3 : 1e-12), "%s AUTO err %.3e on arbitrary doubles", key.c_str(), e_auto);
+      CHECK(e_vm <= 1e-12, "%s VM err %.3e on arbitrary doubles", key.c_str(), e_vm);
+      std::printf("gpu: eval_mugraph %s arbitrary doubles: %s %.2e, fp64 VM %.2e\n", key.c_str(),
+                  fused ? "split kernel" : "fp64 VM", e_auto, e_vm);
+    }
+  }
   return failures ? 1 : 0;
 }
 

@@ -60,31 +60,22 @@ Backend::~Backend() {
 }
 
 std::vector<interp::FTensor> Backend::eval_mugraph(const ir::KernelGraph &g,
-                                                   const std::vector<interp::FTensor> &inputs) {
+                                                   const std::vector<interp::FTensor> &inputs,
+                                                   int precision) {
   if (inputs.size() != g.inputs.size()) throw Error(ErrCode::ShapeMismatch, "input count");
   CompiledGraph cg(ctx_, g);
-  std::vector<std::vector<float>> in32(inputs.size());
-  std::vector<const void *> pin(inputs.size());
-  std::vector<int32_t> dt(inputs.size(), TPO_DTYPE_F32);
+  check(tpo_gpu_graph_set_precision(cg.handle(), precision));
+  std::vector<const double *> pin(inputs.size());
   for (size_t i = 0; i < inputs.size(); ++i) {
     if (inputs[i].shape.dims != g.tensor(g.inputs[i]).shape.dims)
       throw Error(ErrCode::ShapeMismatch, "input tensor shape");
-    in32[i].assign(inputs[i].data.begin(), inputs[i].data.end());
-    pin[i] = in32[i].data();
+    pin[i] = inputs[i].data.data();
   }
-  std::vector<std::vector<float>> out32(g.outputs.size());
-  std::vector<float *> pout(g.outputs.size());
-  for (size_t o = 0; o < g.outputs.size(); ++o) {
-    out32[o].resize(size_t(g.tensor(g.outputs[o]).shape.elem_count()));
-    pout[o] = out32[o].data();
-  }
-  check(tpo_gpu_eval_mugraph_host(ctx_, cg.handle(), pin.data(), dt.data(), pout.data(), nullptr));
   std::vector<interp::FTensor> out;
-  for (size_t o = 0; o < g.outputs.size(); ++o) {
-    interp::FTensor t(g.tensor(g.outputs[o]).shape);
-    t.data.assign(out32[o].begin(), out32[o].end());
-    out.push_back(std::move(t));
-  }
+  std::vector<double *> pout(g.outputs.size());
+  for (size_t o = 0; o < g.outputs.size(); ++o) out.emplace_back(g.tensor(g.outputs[o]).shape);
+  for (size_t o = 0; o < g.outputs.size(); ++o) pout[o] = out[o].data.data();
+  check(tpo_gpu_eval_mugraph_f64(ctx_, cg.handle(), pin.data(), pout.data(), nullptr));
   return out;
 }
 

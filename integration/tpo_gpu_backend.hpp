@@ -49,12 +49,17 @@ class Backend {
   Backend(const Backend &) = delete;
   Backend &operator=(const Backend &) = delete;
 
-  /// eval_mugraph for host tensors.  Inputs are rounded to bf16 on the
-  /// device (the fused kernels' input type), accumulation is fp32, outputs
-  /// are widened back to double.  Throws tpo::Error(Unsupported) for a
-  /// µGraph without a fused sm_100a kernel.
+  /// eval_mugraph for host tensors (tpo_gpu_eval_mugraph_f64: doubles in,
+  /// doubles out).  A benchmark µGraph runs its fused sm_100a kernel under
+  /// the precision policy (default TPO_PREC_AUTO: fp64 operands enter as
+  /// bf16 hi + lo, fp32 accumulation; |o - r| <= 1e-3·max(|r|, rms(r))
+  /// against interp::eval_mugraph on arbitrary inputs); any other µGraph, or
+  /// `precision` = TPO_PREC_VM, runs on the generic GPU VM in double
+  /// arithmetic in the reference's operation order (bit-identical except
+  /// exp / SiLU).  TPO_PREC_BF16 rounds the inputs to bf16 instead.
   std::vector<interp::FTensor> eval_mugraph(const ir::KernelGraph &g,
-                                            const std::vector<interp::FTensor> &inputs);
+                                            const std::vector<interp::FTensor> &inputs,
+                                            int precision = TPO_PREC_AUTO);
 
   /// random_test_equivalence on the GPU; the verdict (kind, witness,
   /// rounds_run, resamples) is bit-identical to the CPU reference's.

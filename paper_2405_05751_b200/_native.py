@@ -68,6 +68,8 @@ def lib():
     L.tpo_gpu_validate.argtypes = [C.c_char_p, i64, i64, C.c_char_p, C.c_int]
     L.tpo_gpu_eval_mugraph.argtypes = [vp, vp, vp, vp, vp, vp]
     L.tpo_gpu_eval_mugraph_host.argtypes = [vp, vp, vp, vp, vp, vp]
+    L.tpo_gpu_eval_mugraph_f64.argtypes = [vp, vp, vp, vp, vp]
+    L.tpo_gpu_graph_set_precision.argtypes = [vp, i32]
     L.tpo_gpu_eval_vm.argtypes = [vp, vp, i32, vp, vp]
     L.tpo_gpu_construct_thread_graphs.argtypes = [C.c_char_p, C.c_char_p, i64, C.POINTER(i64)]
     L.tpo_gpu_float_stability_filter.argtypes = [vp, vp, vp, i32, C.c_double, u64, C.c_double, vp]

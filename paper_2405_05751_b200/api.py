@@ -31,6 +31,18 @@ VERDICT_DTYPE = np.dtype([("kind", "<i4"), ("rounds_run", "<i4"), ("resamples", 
                           ("w_index", "<i8")])
 KIND = {0: "Equivalent", 1: "NotEquivalent", 2: "Inconclusive", 3: "Error"}
 FUSED = {0: None, 1: "rmsnorm", 2: "gatedmlp", 3: "gqa", 4: "lora"}
+# tpo_gpu.h TPO_PREC_*: precision policy of the fused kernels
+PRECISION = {"auto": 0, "bf16": 1, "vm": 2}
+
+
+def _dtype_code(x) -> int:
+    """TPO_DTYPE_* of a torch tensor; anything else is rejected (the C-ABI
+    would read the buffer with the wrong element size)."""
+    import torch
+    codes = {torch.float32: 0, torch.bfloat16: 1, torch.float64: 2}
+    if x.dtype not in codes:
+        raise ValueError(f"input dtype {x.dtype} unsupported: use bfloat16, float32 or float64")
+    return codes[x.dtype]
 
 
 def _js(g) -> bytes:
@@ -179,6 +191,13 @@ class Graph:
         N.check(N.lib().tpo_gpu_graph_set_static_inputs(self.h, mask))
         return self
 
+    def set_precision(self, policy: str) -> "Graph":
+        """TPO_PREC_* policy of the fused kernels: "auto" (bf16 inputs -> bf16
+        kernel, fp32/fp64 inputs -> split hi+lo kernel), "bf16" (round every
+        input to bf16), "vm" (generic VM in the reference's operation order)."""
+        N.check(N.lib().tpo_gpu_graph_set_precision(self.h, PRECISION[policy]))
+        return self
+
     @property
     def fused(self) -> Optional[str]:
         return FUSED.get(self.info.fused_kind)
@@ -230,7 +249,8 @@ class Context:
 
     # ---- floating point -------------------------------------------------
     def eval_mugraph(self, g, inputs: Sequence, outputs=None, stream=None):
-        """Fused fp evaluation on torch CUDA tensors (bf16 or fp32 inputs, fp32 outputs)."""
+        """fp evaluation on torch CUDA tensors (bf16, fp32 or fp64 inputs,
+        fp32 outputs) under the graph's precision policy."""
         import torch
         g = self.compile(g)
         ins = list(inputs)
@@ -239,10 +259,14 @@ class Context:
         for x, s in zip(ins, g.shapes(False)):
             if list(x.shape) != s or not x.is_cuda or not x.is_contiguous():
                 raise ValueError(f"input must be a contiguous CUDA tensor of shape {s}")
+        codes = [_dtype_code(x) for x in ins]
         if outputs is None:
             outputs = [torch.empty(s, device=ins[0].device, dtype=torch.float32)
                        for s in g.shapes(True)]
-        dt = (C.c_int32 * len(ins))(*[1 if x.dtype == torch.bfloat16 else 0 for x in ins])
+        for o, s in zip(outputs, g.shapes(True)):
+            if list(o.shape) != s or o.dtype != torch.float32 or not o.is_cuda or not o.is_contiguous():
+                raise ValueError(f"output must be a contiguous fp32 CUDA tensor of shape {s}")
+        dt = (C.c_int32 * len(ins))(*codes)
         pin = (C.c_void_p * len(ins))(*[x.data_ptr() for x in ins])
         pout = (C.c_void_p * len(outputs))(*[o.data_ptr() for o in outputs])
         st = stream if stream is not None else torch.cuda.current_stream(ins[0].device).cuda_stream
@@ -250,9 +274,9 @@ class Context:
         return outputs
 
     def eval_mugraph_host(self, g, inputs: Sequence, outputs=None, stream=None):
-        """Fused fp evaluation from/to HOST tensors (``tpo_gpu_eval_mugraph_host``):
-        bf16 or fp32 CPU torch tensors in (pinned for full PCIe speed), fp32
-        CPU tensors out; the host<->device copies are part of the call."""
+        """fp evaluation from/to HOST tensors (``tpo_gpu_eval_mugraph_host``):
+        bf16, fp32 or fp64 CPU torch tensors in (pinned for full PCIe speed),
+        fp32 CPU tensors out; the host<->device copies are part of the call."""
         import torch
         g = self.compile(g)
         ins = list(inputs)
@@ -261,16 +285,37 @@ class Context:
         for x, s in zip(ins, g.shapes(False)):
             if list(x.shape) != s or x.is_cuda or not x.is_contiguous():
                 raise ValueError(f"input must be a contiguous host tensor of shape {s}")
-            if x.dtype not in (torch.bfloat16, torch.float32):
-                raise ValueError("host inputs must be bf16 or fp32")
+        codes = [_dtype_code(x) for x in ins]
         if outputs is None:
             outputs = [torch.empty(s, dtype=torch.float32) for s in g.shapes(True)]
-        dt = (C.c_int32 * len(ins))(*[1 if x.dtype == torch.bfloat16 else 0 for x in ins])
+        dt = (C.c_int32 * len(ins))(*codes)
         pin = (C.c_void_p * len(ins))(*[x.data_ptr() for x in ins])
         pout = (C.c_void_p * len(outputs))(*[o.data_ptr() for o in outputs])
         N.check(N.lib().tpo_gpu_eval_mugraph_host(self.h, g.h, pin, dt, pout,
                                                   C.c_void_p(stream) if stream else None))
         return outputs
+
+    def eval_mugraph_f64(self, g, inputs: Sequence, stream=None) -> List[np.ndarray]:
+        """``interp::eval_mugraph`` with its own types (interp.hpp:47-48):
+        float64 numpy inputs, float64 numpy outputs (``tpo_gpu_eval_mugraph_f64``).
+        Fused µGraphs run their split kernel (TPO_PREC_AUTO), others the
+        generic VM in double arithmetic."""
+        g = self.compile(g)
+        shapes = g.shapes(False)
+        if len(inputs) != len(shapes):
+            raise ValueError("input count")
+        ins = []
+        for x, s in zip(inputs, shapes):
+            a = np.ascontiguousarray(x, dtype=np.float64)
+            if list(a.shape) != s:
+                raise ValueError(f"input shape {list(a.shape)} != {s}")
+            ins.append(a)
+        outs = [np.zeros(s, np.float64) for s in g.shapes(True)]
+        pin = (C.c_void_p * max(len(ins), 1))(*[a.ctypes.data for a in ins])
+        pout = (C.c_void_p * max(len(outs), 1))(*[o.ctypes.data for o in outs])
+        N.check(N.lib().tpo_gpu_eval_mugraph_f64(self.h, g.h, pin, pout,
+                                                 C.c_void_p(stream) if stream else None))
+        return outs
 
     def eval_vm(self, g, inputs: Sequence, mode: int = 0):
         """Generic GPU µGraph VM (``tpo_gpu_eval_vm``): mode 0 eval_mugraph

@@ -111,7 +111,7 @@ DevBuf::~DevBuf() {
 // FieldParams (field.cpp:43-67): same validity checks and tables, plus the
 // device constants of the lazy-reduction scheme.
 FieldState &Ctx::field(uint32_t p, uint32_t q, uint32_t wbase) {
-  uint64_t key = (uint64_t(p) << 40) ^ (uint64_t(q) << 20) ^ wbase;
+  const auto key = std::make_tuple(p, q, wbase);
   auto it = fields.find(key);
   if (it != fields.end()) return *it->second;
   if (!is_prime(p) || !is_prime(q)) throw Error(ErrCode::ConfigError, "p and q must be prime");
@@ -615,66 +615,120 @@ int64_t tpo_gpu_op_madds(const tpo_gpu_graph *g) { return g->g.madds; }
 
 }  // extern "C"
 
-extern "C" int tpo_convert_bf16_f32(const void *in, float *out, size_t n, int num_sms, cudaStream_t st);
+extern "C" int tpo_convert_to_f32(const void *in, int dtype, float *out, size_t n, int num_sms,
+                                  cudaStream_t st);
+extern "C" int tpo_convert_to_f64(const void *in, int dtype, double *out, size_t n, int num_sms,
+                                  cudaStream_t st);
 
 namespace {
 int eval_vm_impl(tpo_gpu_ctx *ctx, const tpo_gpu_graph *h, int32_t mode, const void *in, void *out,
                  bool host, cudaStream_t stream);
 
-// A µGraph without a hand-written kernel: the generic VM in the reference's
-// fp32 semantics (eval_mugraph_f32, interp.hpp:51-53) on the device —
-// inputs widened to fp32 into one contiguous buffer, outputs copied out.
+size_t dtype_bytes(int32_t dt) {
+  switch (dt) {
+    case TPO_DTYPE_F32: return 4;
+    case TPO_DTYPE_BF16: return 2;
+    case TPO_DTYPE_F64: return 8;
+  }
+  throw Error(ErrCode::Unsupported, "input dtype must be TPO_DTYPE_BF16, TPO_DTYPE_F32 or TPO_DTYPE_F64");
+}
+
+// A µGraph without a hand-written kernel (or TPO_PREC_VM): the generic VM on
+// the device in the reference's operation order — double arithmetic
+// (eval_mugraph, interp.hpp:47-48) when any input is fp64, else fp32
+// (eval_mugraph_f32, interp.hpp:51-53).  Inputs are widened into one
+// contiguous buffer; outputs are written as fp32 (out_dev) or, with
+// out_f64, as the VM's doubles.
 void eval_generic_dev(tpo_gpu_ctx *ctx, const tpo_gpu_graph *h, const void *const *in_dev,
-                      const int32_t *in_dtype, float *const *out_dev, cudaStream_t st) {
+                      const int32_t *in_dtype, float *const *out_dev, cudaStream_t st,
+                      double *const *out_f64 = nullptr) {
   Ctx &C = ctx->c;
   const Graph &G = h->g;
-  float *vin = static_cast<float *>(C.vm_in.get(size_t(G.in_elems) * 4 + 16));
-  float *vout = static_cast<float *>(C.vm_out.get(size_t(G.out_elems) * 4 + 16));
+  bool f64 = out_f64 != nullptr;
+  for (size_t i = 0; i < G.g.inputs.size(); ++i) f64 |= dtype_bytes(in_dtype[i]) == 8;
+  const size_t el = f64 ? 8 : 4;
+  char *vin = static_cast<char *>(C.vm_in.get(size_t(G.in_elems) * el + 16));
+  char *vout = static_cast<char *>(C.vm_out.get(size_t(G.out_elems) * el + 16));
   size_t off = 0;
   for (size_t i = 0; i < G.g.inputs.size(); ++i) {
     const size_t n = size_t(G.g.tensor(G.g.inputs[i]).shape.elem_count());
-    if (in_dtype[i] == TPO_DTYPE_F32)
-      check_cuda(cudaMemcpyAsync(vin + off, in_dev[i], n * 4, cudaMemcpyDeviceToDevice, st), "in");
-    else if (in_dtype[i] == TPO_DTYPE_BF16)
-      check_cuda(cudaError_t(tpo_convert_bf16_f32(in_dev[i], vin + off, n, C.num_sms, st)), "bf16->f32");
+    const int32_t dt = in_dtype[i];
+    if ((f64 && dt == TPO_DTYPE_F64) || (!f64 && dt == TPO_DTYPE_F32))
+      check_cuda(cudaMemcpyAsync(vin + off * el, in_dev[i], n * el, cudaMemcpyDeviceToDevice, st), "in");
+    else if (f64)
+      check_cuda(cudaError_t(tpo_convert_to_f64(in_dev[i], dt, reinterpret_cast<double *>(vin) + off, n,
+                                                C.num_sms, st)), "in->f64");
     else
-      throw Error(ErrCode::Unsupported, "input dtype must be TPO_DTYPE_BF16 or TPO_DTYPE_F32");
+      check_cuda(cudaError_t(tpo_convert_to_f32(in_dev[i], dt, reinterpret_cast<float *>(vin) + off, n,
+                                                C.num_sms, st)), "in->f32");
     off += n;
   }
-  const int rc = eval_vm_impl(ctx, h, 2, vin, vout, false, st);
+  const int rc = eval_vm_impl(ctx, h, f64 ? 0 : 2, vin, vout, false, st);
   if (rc) throw Error(ErrCode::Unsupported, "generic VM: " + std::string(tpo_gpu_last_error()));
   off = 0;
   for (size_t o = 0; o < G.g.outputs.size(); ++o) {
     const size_t n = size_t(G.g.tensor(G.g.outputs[o]).shape.elem_count());
-    check_cuda(cudaMemcpyAsync(out_dev[o], vout + off, n * 4, cudaMemcpyDeviceToDevice, st), "out");
+    if (out_f64)
+      check_cuda(cudaMemcpyAsync(out_f64[o], vout + off * 8, n * 8, cudaMemcpyDeviceToDevice, st), "out");
+    else if (f64)
+      check_cuda(cudaError_t(tpo_convert_to_f32(vout + off * 8, TPO_DTYPE_F64, out_dev[o], n, C.num_sms, st)),
+                 "out->f32");
+    else
+      check_cuda(cudaMemcpyAsync(out_dev[o], vout + off * 4, n * 4, cudaMemcpyDeviceToDevice, st), "out");
     off += n;
   }
 }
+
+// Fused evaluation with the graph's precision policy; operand conversions
+// land in context scratch.  caller_inputs: the buffers are the caller's
+// (not written by the library on this stream).
+int run_fused(Ctx &C, const Graph &G, const void *const *in, const int32_t *dt, float *const *out,
+              bool caller_inputs, cudaStream_t st) {
+  FusedIO io;
+  io.in = in;
+  io.dt = dt;
+  io.out = out;
+  io.precision = G.precision;
+  io.caller_inputs = caller_inputs;
+  io.num_sms = C.num_sms;
+  io.scratch = [&C](int slot, size_t bytes) {
+    if (C.fused_scratch.size() <= size_t(slot)) C.fused_scratch.resize(size_t(slot) + 1);
+    return C.fused_scratch[size_t(slot)].get(bytes);
+  };
+  return launch_fused(G.plan, io, st);
+}
+
+bool use_fused(const Graph &G) { return G.plan.kind != 0 && G.precision != TPO_PREC_VM; }
+
 }  // namespace
 
 extern "C" {
+
+int tpo_gpu_graph_set_precision(tpo_gpu_graph *h, int32_t policy) {
+  return guard([&] {
+    if (!h) throw Error(ErrCode::ConfigError, "null graph");
+    if (policy < TPO_PREC_AUTO || policy > TPO_PREC_VM) throw Error(ErrCode::ConfigError, "unknown TPO_PREC_* policy");
+    h->g.precision = policy;
+    return 0;
+  });
+}
 
 int tpo_gpu_eval_mugraph(tpo_gpu_ctx *ctx, const tpo_gpu_graph *h, const void *const *in_dev,
                          const int32_t *in_dtype, float *const *out_dev, void *stream) {
   return guard([&] {
     const Graph &G = h->g;
-    if (!G.plan.kind) {
-      check_cuda(cudaSetDevice(ctx->c.device), "cudaSetDevice");
-      eval_generic_dev(ctx, h, in_dev, in_dtype, out_dev, static_cast<cudaStream_t>(stream));
+    for (size_t i = 0; i < G.g.inputs.size(); ++i) dtype_bytes(in_dtype[i]);
+    check_cuda(cudaSetDevice(ctx->c.device), "cudaSetDevice");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);  // NULL = legacy default stream
+    if (!use_fused(G)) {
+      eval_generic_dev(ctx, h, in_dev, in_dtype, out_dev, st);
       return 0;
     }
-    check_cuda(cudaSetDevice(ctx->c.device), "cudaSetDevice");
-    size_t wsb = fused_workspace_bytes(G.plan);
-    void *ws = wsb ? ctx->c.ws.get(wsb) : nullptr;
-    cudaStream_t st = static_cast<cudaStream_t>(stream);  // NULL = legacy default stream
-    int e = launch_fused(G.plan, in_dev, in_dtype, out_dev, ws, wsb, st);
+    int e = run_fused(ctx->c, G, in_dev, in_dtype, out_dev, true, st);
     if (e) return fail(3000 + e, std::string("fused launch: ") + cudaGetErrorString(cudaError_t(e)));
     return 0;
   });
 }
-
-extern "C" int tpo_convert_f32_bf16(const float *in, void *out, size_t n, int num_sms,
-                                    cudaStream_t st);
 
 int tpo_gpu_eval_mugraph_host(tpo_gpu_ctx *ctx, const tpo_gpu_graph *h, const void *const *in_host,
                               const int32_t *in_dtype, float *const *out_host, void *stream) {
@@ -684,45 +738,75 @@ int tpo_gpu_eval_mugraph_host(tpo_gpu_ctx *ctx, const tpo_gpu_graph *h, const vo
     check_cuda(cudaSetDevice(C.device), "cudaSetDevice");
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : C.stream;
     const size_t ni = G.g.inputs.size(), no = G.g.outputs.size();
-    if (C.h_in.size() < ni) C.h_in.resize(ni), C.h_stage.resize(ni);
+    if (C.h_in.size() < ni) C.h_in.resize(ni);
     if (C.h_out.size() < no) C.h_out.resize(no);
+    // inputs cross PCIe in the caller's dtype; conversions run on the device
     std::vector<const void *> din(ni);
-    std::vector<int32_t> ddt(ni, TPO_DTYPE_BF16);
     for (size_t i = 0; i < ni; ++i) {
-      const size_t n = size_t(G.g.tensor(G.g.inputs[i]).shape.elem_count());
-      void *d = C.h_in[i].get(n * 2);
-      if (in_dtype[i] == TPO_DTYPE_BF16) {
-        check_cuda(cudaMemcpyAsync(d, in_host[i], n * 2, cudaMemcpyHostToDevice, st), "H2D");
-      } else if (in_dtype[i] == TPO_DTYPE_F32) {
-        void *f = C.h_stage[i].get(n * 4);
-        check_cuda(cudaMemcpyAsync(f, in_host[i], n * 4, cudaMemcpyHostToDevice, st), "H2D");
-        if (!G.plan.kind) {  // the generic VM takes fp32 as is
-          din[i] = f;
-          ddt[i] = TPO_DTYPE_F32;
-          continue;
-        }
-        check_cuda(cudaError_t(tpo_convert_f32_bf16(static_cast<const float *>(f), d, n, C.num_sms, st)),
-                   "f32->bf16");
-      } else {
-        throw Error(ErrCode::Unsupported, "input dtype must be TPO_DTYPE_BF16 or TPO_DTYPE_F32");
-      }
+      const size_t n = size_t(G.g.tensor(G.g.inputs[i]).shape.elem_count()) * dtype_bytes(in_dtype[i]);
+      void *d = C.h_in[i].get(n);
+      check_cuda(cudaMemcpyAsync(d, in_host[i], n, cudaMemcpyHostToDevice, st), "H2D");
       din[i] = d;
     }
     std::vector<float *> dout(no);
     for (size_t o = 0; o < no; ++o)
       dout[o] = static_cast<float *>(
           C.h_out[o].get(size_t(G.g.tensor(G.g.outputs[o]).shape.elem_count()) * 4));
-    if (G.plan.kind) {
-      int e = launch_fused(G.plan, din.data(), ddt.data(), dout.data(), nullptr, 0, st);
+    if (use_fused(G)) {
+      // the copies above wrote the operands on this stream: nothing may be
+      // read before the kernel's dependency resolves (no static prefetch)
+      int e = run_fused(C, G, din.data(), in_dtype, dout.data(), false, st);
       if (e) return fail(3000 + e, std::string("fused launch: ") + cudaGetErrorString(cudaError_t(e)));
     } else {
-      eval_generic_dev(ctx, h, din.data(), ddt.data(), dout.data(), st);
+      eval_generic_dev(ctx, h, din.data(), in_dtype, dout.data(), st);
     }
     for (size_t o = 0; o < no; ++o)
       check_cuda(cudaMemcpyAsync(out_host[o], dout[o],
                                  size_t(G.g.tensor(G.g.outputs[o]).shape.elem_count()) * 4,
                                  cudaMemcpyDeviceToHost, st),
                  "D2H");
+    check_cuda(cudaStreamSynchronize(st), "sync");
+    return 0;
+  });
+}
+
+int tpo_gpu_eval_mugraph_f64(tpo_gpu_ctx *ctx, const tpo_gpu_graph *h, const double *const *in_host,
+                             double *const *out_host, void *stream) {
+  return guard([&] {
+    Ctx &C = ctx->c;
+    const Graph &G = h->g;
+    check_cuda(cudaSetDevice(C.device), "cudaSetDevice");
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : C.stream;
+    const size_t ni = G.g.inputs.size(), no = G.g.outputs.size();
+    if (C.h_in.size() < ni) C.h_in.resize(ni);
+    if (C.h_out.size() < 2 * no) C.h_out.resize(2 * no);
+    std::vector<const void *> din(ni);
+    std::vector<int32_t> dt(ni, TPO_DTYPE_F64);
+    for (size_t i = 0; i < ni; ++i) {
+      const size_t n = size_t(G.g.tensor(G.g.inputs[i]).shape.elem_count()) * 8;
+      void *d = C.h_in[i].get(n);
+      check_cuda(cudaMemcpyAsync(d, in_host[i], n, cudaMemcpyHostToDevice, st), "H2D");
+      din[i] = d;
+    }
+    std::vector<double *> d64(no);
+    for (size_t o = 0; o < no; ++o)
+      d64[o] = static_cast<double *>(C.h_out[no + o].get(size_t(G.g.tensor(G.g.outputs[o]).shape.elem_count()) * 8));
+    if (use_fused(G)) {
+      std::vector<float *> d32(no);
+      for (size_t o = 0; o < no; ++o)
+        d32[o] = static_cast<float *>(C.h_out[o].get(size_t(G.g.tensor(G.g.outputs[o]).shape.elem_count()) * 4));
+      int e = run_fused(C, G, din.data(), dt.data(), d32.data(), false, st);
+      if (e) return fail(3000 + e, std::string("fused launch: ") + cudaGetErrorString(cudaError_t(e)));
+      for (size_t o = 0; o < no; ++o)
+        check_cuda(cudaError_t(tpo_convert_to_f64(d32[o], TPO_DTYPE_F32, d64[o],
+                                                  size_t(G.g.tensor(G.g.outputs[o]).shape.elem_count()),
+                                                  C.num_sms, st)), "out->f64");
+    } else {
+      eval_generic_dev(ctx, h, din.data(), dt.data(), nullptr, st, d64.data());
+    }
+    for (size_t o = 0; o < no; ++o)
+      check_cuda(cudaMemcpyAsync(out_host[o], d64[o], size_t(G.g.tensor(G.g.outputs[o]).shape.elem_count()) * 8,
+                                 cudaMemcpyDeviceToHost, st), "D2H");
     check_cuda(cudaStreamSynchronize(st), "sync");
     return 0;
   });
@@ -803,6 +887,14 @@ int tpo_gpu_verify_batch(tpo_gpu_ctx *ctx, const tpo_gpu_graph *program,
                          tpo_verdict *verdicts, uint32_t *accept_bits) {
   return guard([&] {
     if (n == 0) return 0;
+    // seeds == NULL: cfg->seed for every candidate (one VerifyConfig for the
+    // whole batch, as the search loop calls it) on either
+    // executor
+    std::vector<uint64_t> one_seed;
+    if (!seeds) {
+      one_seed.assign(size_t(n), cfg->seed);
+      seeds = one_seed.data();
+    }
     // graphs beyond shared memory: the global-memory field executor, one
     // candidate at a time (same verdicts; BASELINE-shape pairs)
     auto global_loop = [&] {
@@ -813,7 +905,7 @@ int tpo_gpu_verify_batch(tpo_gpu_ctx *ctx, const tpo_gpu_graph *program,
       if (accept_bits) std::memset(accept_bits, 0, size_t((n + 31) / 32) * 4);
       for (uint64_t k = 0; k < n; ++k) {
         tpo_verify_cfg c = *cfg;
-        c.seed = seeds ? seeds[k] : cfg->seed;
+        c.seed = seeds[k];
         TpoVerdict v;
         try {
           check_pair(program->g.g, cands[k]->g.g);

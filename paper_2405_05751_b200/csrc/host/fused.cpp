@@ -272,8 +272,6 @@ FusedPlan match_fused(const KernelGraph &g) {
   return p;
 }
 
-size_t fused_workspace_bytes(const FusedPlan &) { return 0; }
-
 namespace {
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -294,19 +292,20 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // Encoded maps are cached by (pointer, shape, box, swizzle): repeated
 // evaluations on the same buffers skip the driver call.
 bool tmap_2d(CUtensorMap *m, const void *ptr, uint64_t rows, uint64_t cols, uint32_t box_cols,
-             uint32_t box_rows, CUtensorMapSwizzle sw) {
+             uint32_t box_rows, CUtensorMapSwizzle sw, bool f32 = false) {
   struct Key {
     const void *p;
     uint64_t r, c;
     uint32_t bc, br;
     int sw;
+    bool f32;
     bool operator==(const Key &o) const {
-      return p == o.p && r == o.r && c == o.c && bc == o.bc && br == o.br && sw == o.sw;
+      return p == o.p && r == o.r && c == o.c && bc == o.bc && br == o.br && sw == o.sw && f32 == o.f32;
     }
   };
   static std::mutex mu;
   static std::vector<std::pair<Key, CUtensorMap>> cache;
-  const Key key{ptr, rows, cols, box_cols, box_rows, int(sw)};
+  const Key key{ptr, rows, cols, box_cols, box_rows, int(sw), f32};
   {
     std::lock_guard<std::mutex> lk(mu);
     for (auto &e : cache)
@@ -318,10 +317,10 @@ bool tmap_2d(CUtensorMap *m, const void *ptr, uint64_t rows, uint64_t cols, uint
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {cols * 2};
+  cuuint64_t strides[1] = {cols * (f32 ? 4 : 2)};
   cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t es[2] = {1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides,
+  CUresult r = fn(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides,
                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return false;
@@ -442,12 +441,81 @@ void debug_end(const char *tag, unsigned long long *dbg, int nct, cudaStream_t s
 
 }  // namespace
 
-int launch_fused(const FusedPlan &p, const void *const *in, const int32_t *dt, float *const *out,
-                 void *, size_t, cudaStream_t st) {
-  const int n_in = (p.kind == TPO_FUSED_GATED_MLP || p.kind == TPO_FUSED_GQA_DECODE) ? 3 : 4;
-  for (int i = 0; i < n_in; ++i)
-    if (dt[i] != TPO_DTYPE_BF16) return int(cudaErrorNotSupported);
-  CUtensorMap maps[4];
+namespace {
+extern "C" int tpo_convert_planes(const void *in, int dtype, void *hi, void *lo, size_t n, int num_sms,
+                                  cudaStream_t st);
+extern "C" int tpo_convert_rows(const void *in, int dtype, void *out, size_t batch, size_t R, size_t C,
+                                size_t P, int num_sms, cudaStream_t st);
+extern "C" int tpo_convert_to_f32(const void *in, int dtype, float *out, size_t n, int num_sms,
+                                  cudaStream_t st);
+extern "C" int tpo_convert_to_bf16(const void *in, int dtype, void *out, size_t n, int num_sms,
+                                   cudaStream_t st);
+
+// Operand conversions of one evaluation into scratch slots (slot 2i, 2i+1
+// for input i).  Each returns false on a CUDA error.
+struct Convert {
+  const FusedIO &io;
+  cudaStream_t st;
+  int err = 0;
+  // hi / lo bf16 planes of input i (n elements)
+  std::pair<void *, void *> planes(int i, size_t n) {
+    void *hi = io.scratch(2 * i, n * 2), *lo = io.scratch(2 * i + 1, n * 2);
+    if (!err) err = tpo_convert_planes(io.in[i], io.dt[i], hi, lo, n, io.num_sms, st);
+    return {hi, lo};
+  }
+  // [batch][2P][C] hi / lo token rows of input i ([batch][R][C])
+  void *rows(int i, size_t batch, size_t R, size_t C, size_t P) {
+    void *o = io.scratch(2 * i, batch * 2 * P * C * 2);
+    if (!err) err = tpo_convert_rows(io.in[i], io.dt[i], o, batch, R, C, P, io.num_sms, st);
+    return o;
+  }
+  const float *f32(int i, size_t n) {
+    if (io.dt[i] == TPO_DTYPE_F32) return static_cast<const float *>(io.in[i]);
+    float *o = static_cast<float *>(io.scratch(2 * i, n * 4));
+    if (!err) err = tpo_convert_to_f32(io.in[i], io.dt[i], o, n, io.num_sms, st);
+    return o;
+  }
+  const void *bf16(int i, size_t n) {
+    if (io.dt[i] == TPO_DTYPE_BF16) return io.in[i];
+    void *o = io.scratch(2 * i, n * 2);
+    if (!err) err = tpo_convert_to_bf16(io.in[i], io.dt[i], o, n, io.num_sms, st);
+    return o;
+  }
+};
+
+// Input element counts of a fused plan, in graph-input order.
+std::vector<size_t> input_elems(const FusedPlan &p) {
+  switch (p.kind) {
+    case TPO_FUSED_GATED_MLP: return {size_t(p.b * p.h), size_t(p.h * p.n), size_t(p.h * p.n)};
+    case TPO_FUSED_RMSNORM_MATMUL: return {size_t(p.b * p.h), size_t(p.h), size_t(p.h * p.n), 1};
+    case TPO_FUSED_LORA: return {size_t(p.b * p.h), size_t(p.h * p.n), size_t(p.h * p.r), size_t(p.r * p.n)};
+    case TPO_FUSED_GQA_DECODE:
+      return {size_t(p.groups * p.qh * p.hd), size_t(p.groups * p.hd * p.L), size_t(p.groups * p.L * p.hd)};
+  }
+  return {};
+}
+
+}  // namespace
+
+int launch_fused(const FusedPlan &p, const FusedIO &io, cudaStream_t st) {
+  const std::vector<size_t> ne = input_elems(p);
+  const int n_in = int(ne.size());
+  bool all_bf16 = true;
+  for (int i = 0; i < n_in; ++i) {
+    if (io.dt[i] != TPO_DTYPE_BF16 && io.dt[i] != TPO_DTYPE_F32 && io.dt[i] != TPO_DTYPE_F64)
+      return int(cudaErrorInvalidValue);
+    all_bf16 &= io.dt[i] == TPO_DTYPE_BF16;
+  }
+  const bool split = !all_bf16 && io.precision == TPO_PREC_AUTO;
+  Convert cv{io, st};
+  // operands as the kernels read them: the caller's bf16 buffers, rounded
+  // copies (TPO_PREC_BF16), or the split forms
+  std::vector<const void *> in(n_in);
+  for (int i = 0; i < n_in; ++i) in[i] = split ? nullptr : cv.bf16(i, ne[i]);
+  // the library wrote an operand on this stream just now: no weight may be
+  // read before the PDL wait
+  const bool converted = !all_bf16;
+  CUtensorMap maps[7];
   std::memset(maps, 0, sizeof(maps));
   if (p.kind == TPO_FUSED_GQA_DECODE) {
     // K^T [G, hd, L], V [G, L, hd], Q [G, qh, hd]
@@ -460,76 +528,132 @@ int launch_fused(const FusedPlan &p, const void *const *in, const int32_t *dt, f
     }
     gp.ksplit = S;
     gp.l_per_cta = int(p.L / S);
-    gp.out = out[0];
+    gp.out = io.out[0];
     // ring of 32-KB slots (K or V blocks) filled in the MMA issue order;
     // TPO_STAGES counts K+V pairs (sweep, profiles/r01/ring/sweep_gqa_slots*:
     // 5 slots in issue order 22.95 us; 6 slots K,V-paired 23.25; 3 slots at
-    // two CTAs per SM 24.1)
+    // two CTAs per SM 24.1).  SPLIT: three 64-KB slots (hi + lo planes).
     int slots = env_int("TPO_GQA_SLOTS", env_int("TPO_STAGES", 0) > 0 ? 2 * env_int("TPO_STAGES", 0) : 5);
     int minb = env_int("TPO_MINB", 1);
+    if (split) slots = 3, minb = 1;
     gp.consume_order = env_int("TPO_GQA_ORDER", 1);
     const int nct_g = int(p.groups) * S;
     gp.dbg = debug_begin(nct_g, st);
-    if (!tmap_3d(&maps[0], in[1], p.L, p.hd, p.groups, 64, 128, 1, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !tmap_3d(&maps[1], in[2], p.hd, p.L, p.groups, 64, 128, 1, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !tmap_3d(&maps[2], in[0], p.hd, p.qh, p.groups, 64, 16, 1, CU_TENSOR_MAP_SWIZZLE_128B))
-      return int(cudaErrorInvalidValue);
-    int rc_g = tpo_gqa_launch(slots, minb, maps, &gp, st);
+    bool ok;
+    if (split) {
+      const void *qs = cv.rows(0, size_t(p.groups), size_t(p.qh), size_t(p.hd), 8);
+      auto kp = cv.planes(1, ne[1]);
+      auto vp = cv.planes(2, ne[2]);
+      if (cv.err) return cv.err;
+      ok = tmap_3d(&maps[0], kp.first, p.L, p.hd, p.groups, 64, 128, 1, CU_TENSOR_MAP_SWIZZLE_128B) &&
+           tmap_3d(&maps[3], kp.second, p.L, p.hd, p.groups, 64, 128, 1, CU_TENSOR_MAP_SWIZZLE_128B) &&
+           tmap_3d(&maps[1], vp.first, p.hd, p.L, p.groups, 64, 128, 1, CU_TENSOR_MAP_SWIZZLE_128B) &&
+           tmap_3d(&maps[4], vp.second, p.hd, p.L, p.groups, 64, 128, 1, CU_TENSOR_MAP_SWIZZLE_128B) &&
+           tmap_3d(&maps[2], qs, p.hd, 16, p.groups, 64, 16, 1, CU_TENSOR_MAP_SWIZZLE_128B);
+    } else {
+      if (cv.err) return cv.err;
+      ok = tmap_3d(&maps[0], in[1], p.L, p.hd, p.groups, 64, 128, 1, CU_TENSOR_MAP_SWIZZLE_128B) &&
+           tmap_3d(&maps[1], in[2], p.hd, p.L, p.groups, 64, 128, 1, CU_TENSOR_MAP_SWIZZLE_128B) &&
+           tmap_3d(&maps[2], in[0], p.hd, p.qh, p.groups, 64, 16, 1, CU_TENSOR_MAP_SWIZZLE_128B);
+      maps[3] = maps[0], maps[4] = maps[1];
+    }
+    if (!ok) return int(cudaErrorInvalidValue);
+    int rc_g = tpo_gqa_launch(slots, minb, split, maps, &gp, st);
     if (gp.dbg && !rc_g) {
       char tag[96];
-      std::snprintf(tag, sizeof(tag), "gqa ksplit %d slots %d minb %d", S, slots, minb);
+      std::snprintf(tag, sizeof(tag), "gqa ksplit %d slots %d minb %d split %d", S, slots, minb, int(split));
       debug_end(tag, gp.dbg, nct_g, st);
     }
     return rc_g;
   }
   SkinnyParams sp{};
   int mode = 0;
+  bool ok = true;
+  const auto SW = CU_TENSOR_MAP_SWIZZLE_128B, NOSW = CU_TENSOR_MAP_SWIZZLE_NONE;
   if (p.kind == TPO_FUSED_GATED_MLP) {
     mode = MODE_GATED;
     sp.ksplit = std::min(2, pick_ksplit(p.n / 128, p.h, 1));
-    if (!tmap_2d(&maps[0], in[1], p.h, p.n, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !tmap_2d(&maps[1], in[2], p.h, p.n, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !tmap_2d(&maps[2], in[0], p.b, p.h, 64, 16, CU_TENSOR_MAP_SWIZZLE_128B))
-      return int(cudaErrorInvalidValue);
+    if (split) {  // W1 hi, W1 lo | X rows (hi 0-7, lo 8-15) | W3 hi, W3 lo
+      const void *xs = cv.rows(0, 1, size_t(p.b), size_t(p.h), 8);
+      auto w1 = cv.planes(1, ne[1]);
+      auto w3 = cv.planes(2, ne[2]);
+      if (cv.err) return cv.err;
+      ok = tmap_2d(&maps[0], w1.first, p.h, p.n, 64, 64, SW) && tmap_2d(&maps[1], w1.second, p.h, p.n, 64, 64, SW) &&
+           tmap_2d(&maps[4], w3.first, p.h, p.n, 64, 64, SW) && tmap_2d(&maps[5], w3.second, p.h, p.n, 64, 64, SW) &&
+           tmap_2d(&maps[2], xs, 16, p.h, 64, 16, SW);
+    } else {
+      if (cv.err) return cv.err;
+      ok = tmap_2d(&maps[0], in[1], p.h, p.n, 64, 64, SW) && tmap_2d(&maps[1], in[2], p.h, p.n, 64, 64, SW) &&
+           tmap_2d(&maps[2], in[0], p.b, p.h, 64, 16, SW);
+    }
     maps[3] = maps[2];
   } else if (p.kind == TPO_FUSED_RMSNORM_MATMUL) {
     mode = MODE_RMS;
     sp.ksplit = pick_ksplit(p.n / 128, p.h, 1);
-    if (!tmap_2d(&maps[0], in[2], p.h, p.n, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !tmap_2d(&maps[2], in[0], p.b, p.h, 64, 8, CU_TENSOR_MAP_SWIZZLE_NONE) ||
-        !tmap_2d(&maps[3], in[1], 1, p.h, 64, 1, CU_TENSOR_MAP_SWIZZLE_NONE))
-      return int(cudaErrorInvalidValue);
-    maps[1] = maps[0];
-    sp.x = static_cast<const __nv_bfloat16 *>(in[0]);
-    sp.g = static_cast<const __nv_bfloat16 *>(in[1]);
-    sp.dscale = static_cast<const __nv_bfloat16 *>(in[3]);
+    if (split) {  // W hi, W lo | fp32 X, G, D
+      const float *x = cv.f32(0, ne[0]), *g = cv.f32(1, ne[1]);
+      auto w = cv.planes(2, ne[2]);
+      sp.dscale_f32 = cv.f32(3, 1);
+      if (cv.err) return cv.err;
+      ok = tmap_2d(&maps[0], w.first, p.h, p.n, 64, 64, SW) && tmap_2d(&maps[1], w.second, p.h, p.n, 64, 64, SW) &&
+           tmap_2d(&maps[2], x, p.b, p.h, 64, 8, NOSW, true) && tmap_2d(&maps[3], g, 1, p.h, 64, 1, NOSW, true);
+    } else {
+      if (cv.err) return cv.err;
+      ok = tmap_2d(&maps[0], in[2], p.h, p.n, 64, 64, SW) && tmap_2d(&maps[2], in[0], p.b, p.h, 64, 8, NOSW) &&
+           tmap_2d(&maps[3], in[1], 1, p.h, 64, 1, NOSW);
+      maps[1] = maps[0];
+      sp.x = static_cast<const __nv_bfloat16 *>(in[0]);
+      sp.g = static_cast<const __nv_bfloat16 *>(in[1]);
+      sp.dscale = static_cast<const __nv_bfloat16 *>(in[3]);
+    }
   } else if (p.kind == TPO_FUSED_LORA) {
     mode = MODE_LORA;
     sp.ksplit = pick_ksplit(p.n / 128, p.h, 1);
-    if (!tmap_2d(&maps[0], in[1], p.h, p.n, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !tmap_2d(&maps[2], in[0], p.b, p.h, 64, 16, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !tmap_2d(&maps[3], in[2], p.h, p.r, 16, 64, CU_TENSOR_MAP_SWIZZLE_NONE))
-      return int(cudaErrorInvalidValue);
-    maps[1] = maps[0];
-    sp.x = static_cast<const __nv_bfloat16 *>(in[0]);
-    sp.lora_a = static_cast<const __nv_bfloat16 *>(in[2]);
-    sp.lora_b = static_cast<const __nv_bfloat16 *>(in[3]);
+    if (split) {  // W hi, W lo | X rows (hi 0-15, lo 16-31) | A hi, A lo | fp32 B
+      const void *xs = cv.rows(0, 1, size_t(p.b), size_t(p.h), 16);
+      auto w = cv.planes(1, ne[1]);
+      auto a = cv.planes(2, ne[2]);
+      sp.lora_b_f32 = cv.f32(3, ne[3]);
+      if (cv.err) return cv.err;
+      ok = tmap_2d(&maps[0], w.first, p.h, p.n, 64, 64, SW) && tmap_2d(&maps[1], w.second, p.h, p.n, 64, 64, SW) &&
+           tmap_2d(&maps[2], xs, 32, p.h, 64, 32, SW) && tmap_2d(&maps[3], a.first, p.h, p.r, 16, 64, NOSW) &&
+           tmap_2d(&maps[6], a.second, p.h, p.r, 16, 64, NOSW);
+    } else {
+      if (cv.err) return cv.err;
+      ok = tmap_2d(&maps[0], in[1], p.h, p.n, 64, 64, SW) && tmap_2d(&maps[2], in[0], p.b, p.h, 64, 16, SW) &&
+           tmap_2d(&maps[3], in[2], p.h, p.r, 16, 64, NOSW);
+      maps[1] = maps[0];
+      sp.x = static_cast<const __nv_bfloat16 *>(in[0]);
+      sp.lora_a = static_cast<const __nv_bfloat16 *>(in[2]);
+      sp.lora_b = static_cast<const __nv_bfloat16 *>(in[3]);
+    }
   } else {
     return int(cudaErrorNotSupported);
   }
+  if (!ok) return int(cudaErrorInvalidValue);
+  for (int i = 4; i < 7; ++i)  // unused plane maps: any valid map
+    if (!split) maps[i] = maps[0];
+  if (split && mode != MODE_GATED) maps[4] = maps[5] = maps[0];
+  if (split && mode != MODE_LORA) maps[6] = maps[0];
   sp.N = int(p.n);
   sp.K = int(p.h);
   sp.tokens = int(p.b);
   sp.k_per_cta = int(p.h / sp.ksplit);
-  sp.out = out[0];
-  // Weights (W / W1,W3 / A) declared static may stream before the PDL wait.
+  sp.out = io.out[0];
+  // Weights (W / W1,W3 / A) declared static may stream before the PDL wait,
+  // unless the library itself just wrote them (converted operands).
   const uint64_t weights = p.kind == TPO_FUSED_GATED_MLP ? 0x6 : p.kind == TPO_FUSED_LORA ? 0x6 : 0x4;
-  sp.prefetch_static = (p.static_inputs & weights) == weights && !std::getenv("TPO_NO_PREFETCH");
+  sp.prefetch_static = (p.static_inputs & weights) == weights && io.caller_inputs && !converted &&
+                       !std::getenv("TPO_NO_PREFETCH");
   // Pipeline depth: the measured-best depth that fits (profiles/r01:
   // sweeps, steady-state ring timelines).  Two CTAs per SM (TPO_MINB=2) pay
   // off for RMS only; GatedMLP / LoRA run one CTA per SM with deeper rings.
   int stages = env_int("TPO_STAGES", 0), minb = env_int("TPO_MINB", 0);
   const size_t kOnePerSm = 232448;
+  if (split) {
+    stages = mode == MODE_GATED ? 3 : 5;  // the instantiated SPLIT rings (one CTA per SM)
+    minb = 1;
+  }
   // RMS / LoRA with static weights: two CTAs per SM (5-stage ring, <= 113 KB) so
   // the next evaluation's CTAs become resident and prefetch their weight
   // stages while this one drains (ring timeline, profiles/r01/ring_rms.txt:
@@ -538,7 +662,7 @@ int launch_fused(const FusedPlan &p, const void *const *in, const int32_t *dt, f
   if (stages <= 0) {
     if (minb == 2) {
       for (int s : {5, 4, 3}) {
-        const size_t b = tpo_skinny_smem(mode, s, 2, &sp);
+        const size_t b = tpo_skinny_smem(mode, s, 2, 0, &sp);
         if (b && b <= 115712) {
           stages = s;
           break;
@@ -551,7 +675,7 @@ int launch_fused(const FusedPlan &p, const void *const *in, const int32_t *dt, f
       const int *pref = mode == MODE_GATED ? pref_g : mode == MODE_RMS ? pref_r : pref_l;
       const int np = mode == MODE_GATED ? 3 : 4;
       for (int i = 0; i < np; ++i) {
-        const size_t b = tpo_skinny_smem(mode, pref[i], 1, &sp);
+        const size_t b = tpo_skinny_smem(mode, pref[i], 1, 0, &sp);
         if (b && b <= kOnePerSm) {
           stages = pref[i];
           break;
@@ -559,7 +683,7 @@ int launch_fused(const FusedPlan &p, const void *const *in, const int32_t *dt, f
       }
     }
   } else if (minb <= 0) {
-    minb = tpo_skinny_smem(mode, stages, 2, &sp) ? 2 : 1;
+    minb = tpo_skinny_smem(mode, stages, 2, int(split), &sp) ? 2 : 1;
   }
   sp.dbg_flags = env_int("TPO_DBG_FLAGS", 0);
   sp.epi_atomic = env_int("TPO_EPI_ATOMIC", 0);
@@ -576,11 +700,11 @@ int launch_fused(const FusedPlan &p, const void *const *in, const int32_t *dt, f
   const int nct = int(p.n / 128) * sp.ksplit;
   unsigned long long *dbg = debug_begin(nct, st);
   sp.dbg = dbg;
-  int rc = tpo_skinny_launch(mode, stages, minb, maps, &sp, st);
+  int rc = tpo_skinny_launch(mode, stages, minb, int(split), maps, &sp, st);
   if (dbg && !rc) {
     char tag[128];
-    std::snprintf(tag, sizeof(tag), "mode %d ksplit %d stages %d minb %d prefetch %d", mode, sp.ksplit,
-                  stages, minb, sp.prefetch_static);
+    std::snprintf(tag, sizeof(tag), "mode %d ksplit %d stages %d minb %d prefetch %d split %d", mode,
+                  sp.ksplit, stages, minb, sp.prefetch_static, int(split));
     debug_end(tag, dbg, nct, st);
   }
   return rc;

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <string>
 
 #include "tpo/ir/graph.hpp"
@@ -26,11 +27,26 @@ struct FusedPlan {
 // (SURVEY §8d).  Never throws.
 FusedPlan match_fused(const ir::KernelGraph &g);
 
-// Launches the fused kernel for `plan` on `stream`; inputs in graph-input
-// order (bf16 unless stated), output fp32.  Returns cudaError_t.
-int launch_fused(const FusedPlan &plan, const void *const *in, const int32_t *in_dtype,
-                 float *const *out, void *workspace, size_t ws_bytes, cudaStream_t stream);
+// One fused evaluation: device inputs in graph-input order with their
+// TPO_DTYPE_*, fp32 outputs, the graph's TPO_PREC_* policy.
+struct FusedIO {
+  const void *const *in = nullptr;
+  const int32_t *dt = nullptr;
+  float *const *out = nullptr;
+  int precision = 0;         // TPO_PREC_AUTO / _BF16
+  // the caller's inputs are used in place (no library conversion wrote
+  // them on this stream): static weights may stream before the PDL wait
+  bool caller_inputs = true;
+  int num_sms = 148;
+  // device scratch slot `i` of at least `bytes` (operand conversions)
+  std::function<void *(int, size_t)> scratch;
+};
 
-size_t fused_workspace_bytes(const FusedPlan &plan);
+// Launches the fused kernel for `plan` on `stream`.  Precision (tpo_gpu.h):
+// all-bf16 inputs run the bf16 kernel; TPO_PREC_AUTO with any fp32 / fp64
+// input converts every input to the split operand forms (bf16 hi + lo) and
+// runs the SPLIT kernel; TPO_PREC_BF16 rounds non-bf16 inputs to bf16.
+// Returns cudaError_t.
+int launch_fused(const FusedPlan &plan, const FusedIO &io, cudaStream_t stream);
 
 }  // namespace tpo::gpu

@@ -8,6 +8,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../kernels/ff_vm.cuh"
@@ -39,13 +40,15 @@ struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   int num_sms = 0;
-  std::map<uint64_t, std::unique_ptr<FieldState>> fields;
+  // keyed by the full (p, q, omega_base) triple
+  std::map<std::tuple<uint32_t, uint32_t, uint32_t>, std::unique_ptr<FieldState>> fields;
   DevBuf code, graphs, pool, cand, seeds, verdicts, accept, counter, out, status, inputs, ws;
   DevBuf shared_w, shared_tab, shared_meta;  // same-seed verification batches
   DevBuf vm_in, vm_out;                       // generic-VM evaluation of unfused µGraphs
   // host-buffer fp evaluation (tpo_gpu_eval_mugraph_host): per-input device
   // copies (bf16), fp32 staging for converted inputs, per-output buffers
-  std::vector<DevBuf> h_in, h_stage, h_out;
+  std::vector<DevBuf> h_in, h_out;
+  std::vector<DevBuf> fused_scratch;  // fused-kernel operand conversions (TPO_PREC_*)
   FieldState &field(uint32_t p, uint32_t q, uint32_t wbase);
 };
 
@@ -56,6 +59,7 @@ struct Graph {
   int64_t in_elems = 0, out_elems = 0;
   mutable int64_t vm_words = -1;  // -2: not computed yet (tpo_gpu_graph_info)
   FusedPlan plan;  // fused_kind == 0 when no hand-written kernel matches
+  int precision = 0;  // TPO_PREC_* (tpo_gpu_graph_set_precision)
   // VM lowerings by (region base, 0/1 field pinned-outputs | 2 fp): a handle is
   // immutable, so batches over the same graphs reuse their bytecode
   mutable std::mutex ff_mu;

@@ -17,6 +17,12 @@
 // S^T is double-buffered in TMEM and P^T in shared memory, so exp of block
 // j overlaps S of block j+1 and P·V of block j-1.
 //
+// SPLIT (fp32 / fp64 callers): K and V arrive as bf16 hi + lo planes (each
+// ring slot holds both planes of a block, 64 KB) and Q as hi rows 0-7 + lo
+// rows 8-15 of the Q^T tile; both planes of a block accumulate into the same
+// TMEM accumulator, and S = S[hi rows] + S[lo rows] before the exp, so
+// every product carries ~16 mantissa bits per operand.
+//
 // Warps: 0 TMA producer, 1 MMA issuer + TMEM owner, 2-5 exp / epilogue.
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -68,14 +74,17 @@ __device__ __forceinline__ uint32_t kmaj_off(int row, int col) {
 // completes, V_j's when P_j·V_j's does.  MINB = 2: three slots (≈113 KB) so
 // that the next decode step's CTAs become resident beside this one's and
 // wait at the programmatic dependency instead of behind this grid's exit.
-template <int SLOTS, int S, int MINB>
+template <int SLOTS, int S, int MINB, bool SPLIT>
 __global__ void __launch_bounds__(kThreads, MINB)
     gqa_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
-               const __grid_constant__ CUtensorMap tmQ, const GqaParams p) {
+               const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK1,
+               const __grid_constant__ CUtensorMap tmV1, const GqaParams p) {
+  constexpr int NPL = SPLIT ? 2 : 1;             // planes per K / V block
+  constexpr uint32_t kSlotB = NPL * kSlot;       // ring slot bytes
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *stages = smem;
-  uint8_t *qt = stages + SLOTS * kSlot;
+  uint8_t *qt = stages + SLOTS * kSlotB;
   uint8_t *pbuf = qt + kQBytes;                         // 2 x kPBytes
   constexpr int rows_per = kHD / S;
   // [S-1 peers][rows_per][8] (peer slot: its rank, minus one above the owner's)
@@ -114,6 +123,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
     tma_prefetch(&tmQ);
+    if (SPLIT) tma_prefetch(&tmK1), tma_prefetch(&tmV1);
   }
   if (warp == 1) tmem_alloc<64>(&bars->tmem_base);
   tc_fence_before();
@@ -135,8 +145,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
       for (int u = 0; u < 2 * nb; ++u) {
         const int s = u % SLOTS;
         mbar_wait(&bars->empty[s], ((u / SLOTS) & 1) ^ 1);
-        uint8_t *st = stages + s * kSlot;
-        mbar_expect_tx(&bars->full[s], kSlot);
+        uint8_t *st = stages + s * kSlotB;
+        mbar_expect_tx(&bars->full[s], kSlotB);
         // slot u carries K_j or V_j: K_0 V_0 K_1 V_1 ..., or in the MMA
         // issue order K_0 K_1 V_0 K_2 V_1 ... K_{nb-1} V_{nb-2} V_{nb-1}
         bool isk;
@@ -149,9 +159,17 @@ __global__ void __launch_bounds__(kThreads, MINB)
         if (isk) {
           tma_load_3d(st, &tmK, &bars->full[s], l, 0, g);              // K^T[d, l..l+63]
           tma_load_3d(st + kHalf, &tmK, &bars->full[s], l + 64, 0, g); // K^T[d, l+64..]
+          if (SPLIT) {                                                  // lo plane
+            tma_load_3d(st + kSlot, &tmK1, &bars->full[s], l, 0, g);
+            tma_load_3d(st + kSlot + kHalf, &tmK1, &bars->full[s], l + 64, 0, g);
+          }
         } else {
           tma_load_3d(st, &tmV, &bars->full[s], 0, l, g);              // V[l.., d 0..63]
           tma_load_3d(st + kHalf, &tmV, &bars->full[s], 64, l, g);     // V[l.., d 64..]
+          if (SPLIT) {
+            tma_load_3d(st + kSlot, &tmV1, &bars->full[s], 0, l, g);
+            tma_load_3d(st + kSlot + kHalf, &tmV1, &bars->full[s], 64, l, g);
+          }
         }
       }
       TPO_T(10);
@@ -167,13 +185,16 @@ __global__ void __launch_bounds__(kThreads, MINB)
       mbar_wait(&bars->p_full[b], (i >> 1) & 1);
       tc_fence_after();
       if (elect_one()) {
-        const uint32_t vt = smem_u32(stages + s * kSlot);
+        const uint32_t vt = smem_u32(stages + s * kSlotB);
         const uint32_t pt = smem_u32(pbuf + b * kPBytes);
 #pragma unroll
         for (int kk = 0; kk < kBL / 16; ++kk) {
-          const uint64_t adesc = sdesc_sw128(vt + kk * 16 * 128, kHalf, 1024);
           const uint64_t bdesc = sdesc_sw128(pt + (kk >> 2) * 2048 + (kk & 3) * 32, 16, 1024);
-          umma_bf16(tmem + 32, adesc, bdesc, idesc, (i | kk) != 0);
+#pragma unroll
+          for (int pl = 0; pl < NPL; ++pl) {
+            const uint64_t adesc = sdesc_sw128(vt + pl * kSlot + kk * 16 * 128, kHalf, 1024);
+            umma_bf16(tmem + 32, adesc, bdesc, idesc, (i | kk | pl) != 0);
+          }
         }
         umma_commit(&bars->empty[s]);
         umma_commit(&bars->p_empty[b]);
@@ -188,13 +209,16 @@ __global__ void __launch_bounds__(kThreads, MINB)
       if (j >= 2) mbar_wait(&bars->s_empty[b], ((j - 2) >> 1) & 1);
       tc_fence_after();
       if (elect_one()) {
-        const uint32_t kt = smem_u32(stages + s * kSlot);
+        const uint32_t kt = smem_u32(stages + s * kSlotB);
         const uint32_t qs = smem_u32(qt);
 #pragma unroll
         for (int kk = 0; kk < kHD / 16; ++kk) {
-          const uint64_t adesc = sdesc_sw128(kt + kk * 16 * 128, kHalf, 1024);
           const uint64_t bdesc = sdesc_sw128(qs + (kk >> 2) * 2048 + (kk & 3) * 32, 16, 1024);
-          umma_bf16(tmem + b * kTok, adesc, bdesc, idesc, kk != 0);
+#pragma unroll
+          for (int pl = 0; pl < NPL; ++pl) {
+            const uint64_t adesc = sdesc_sw128(kt + pl * kSlot + kk * 16 * 128, kHalf, 1024);
+            umma_bf16(tmem + b * kTok, adesc, bdesc, idesc, (kk | pl) != 0);
+          }
         }
         umma_commit(&bars->s_full[b]);
         umma_commit(&bars->empty[s]);
@@ -227,7 +251,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
       uint8_t *pb = pbuf + b * kPBytes;
 #pragma unroll
       for (int qq = 0; qq < 8; ++qq) {
-        const float e = expf(sv[qq]);
+        const float e = expf(SPLIT ? sv[qq] + sv[qq + 8] : sv[qq]);  // SPLIT: Q hi + lo rows
         dsum[qq] += e;
         const __nv_bfloat16 hi = __float2bfloat16_rn(e);
         const __nv_bfloat16 lo = __float2bfloat16_rn(e - __bfloat162float(hi));
@@ -309,16 +333,16 @@ __global__ void __launch_bounds__(kThreads, MINB)
 #undef TPO_T
 }
 
-template <int SLOTS, int S>
+template <int SLOTS, int S, bool SPLIT>
 size_t gqa_smem() {
-  return size_t(SLOTS) * kSlot + kQBytes + 2 * kPBytes + (S - 1) * (kHD / S) * 8 * 4 + 4 * 8 * 4 +
+  return size_t(SLOTS) * kSlot * (SPLIT ? 2 : 1) + kQBytes + 2 * kPBytes + (S - 1) * (kHD / S) * 8 * 4 + 4 * 8 * 4 +
          4 * 8 * 4 + sizeof(Bars) + 1024;
 }
 
-template <int SLOTS, int S, int MINB>
+template <int SLOTS, int S, int MINB, bool SPLIT>
 cudaError_t launch_t(const CUtensorMap *maps, const GqaParams &p, cudaStream_t st) {
-  const size_t smem = gqa_smem<SLOTS, S>();
-  auto kern = gqa_kernel<SLOTS, S, MINB>;
+  const size_t smem = gqa_smem<SLOTS, S, SPLIT>();
+  auto kern = gqa_kernel<SLOTS, S, MINB, SPLIT>;
   static size_t configured = 0;
   if (smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -339,25 +363,28 @@ cudaError_t launch_t(const CUtensorMap *maps, const GqaParams &p, cudaStream_t s
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], p);
+  return cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], maps[4], p);
 }
 
 }  // namespace tpo_gqa
 
-extern "C" int tpo_gqa_launch(int slots, int minb, const CUtensorMap *maps, const GqaParams *p,
-                              cudaStream_t st) {
+// maps: {K^T, V, Q^T, K^T lo plane, V lo plane}; split = 1: the SPLIT kernel
+extern "C" int tpo_gqa_launch(int slots, int minb, int split, const CUtensorMap *maps,
+                              const GqaParams *p, cudaStream_t st) {
   using namespace tpo_gqa;
-#define TPO_CASE(SL, S, MB) \
-  if (slots == SL && p->ksplit == S && minb == MB) return int(launch_t<SL, S, MB>(maps, *p, st));
-  TPO_CASE(5, 1, 1) TPO_CASE(6, 1, 1) TPO_CASE(6, 2, 1) TPO_CASE(5, 4, 1) TPO_CASE(6, 4, 1) TPO_CASE(4, 2, 1) TPO_CASE(5, 2, 1)
-  TPO_CASE(3, 2, 2) TPO_CASE(3, 4, 2)
+#define TPO_CASE(SL, S, MB, SP)                                                 \
+  if (slots == SL && p->ksplit == S && minb == MB && bool(split) == SP) \
+    return int(launch_t<SL, S, MB, SP>(maps, *p, st));
+  TPO_CASE(5, 1, 1, false) TPO_CASE(6, 1, 1, false) TPO_CASE(6, 2, 1, false) TPO_CASE(5, 4, 1, false)
+  TPO_CASE(6, 4, 1, false) TPO_CASE(4, 2, 1, false) TPO_CASE(5, 2, 1, false) TPO_CASE(3, 2, 2, false)
+  TPO_CASE(3, 4, 2, false) TPO_CASE(3, 1, 1, true) TPO_CASE(3, 2, 1, true) TPO_CASE(3, 4, 1, true)
 #undef TPO_CASE
   return int(cudaErrorInvalidValue);
 }
 
 extern "C" size_t tpo_gqa_smem(int slots, int ksplit) {
   using namespace tpo_gqa;
-  if (slots == 3 && ksplit == 2) return gqa_smem<3, 2>();
-  if (slots == 3 && ksplit == 4) return gqa_smem<3, 4>();
+  if (slots == 3 && ksplit == 2) return gqa_smem<3, 2, false>();
+  if (slots == 3 && ksplit == 4) return gqa_smem<3, 4, false>();
   return 0;
 }

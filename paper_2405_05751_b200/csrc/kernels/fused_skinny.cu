@@ -45,38 +45,53 @@ using namespace sm100;
 
 constexpr int kBK = 64;                   // K per pipeline stage (one 128-B swizzle atom)
 constexpr int kTileN = 128;               // UMMA M (weight columns per tile)
-constexpr int kTok = 16;                  // UMMA N (tokens, zero padded)
 constexpr uint32_t kWBox = kBK * 128;     // bytes of one 64-col x kBK-row W box
-constexpr uint32_t kXTile = kTok * 128;   // bytes of a 16-row x 64-k B tile
 constexpr int kThreads = 192;
 constexpr int kMaxSplit = 4;
 
 // Pipeline stage layout (one k block of 64):
-//   [W boxes: NA x 2 x 8 KB] [B operand tile 2 KB] [RMS: raw X 1 KB, G 128 B | LoRA: A box 2 KB]
+//   [W boxes: NP planes x 2 x 8 KB] [B operand tile] [RMS: raw X, G | LoRA: A box(es)]
 // GATED / LoRA: the B operand tile (X^T, K-major, 128-B swizzle) is a TMA box.
 // LoRA: the stage also carries the A box [64 k][16 r]; the epilogue warps
 // fold it into this CTA's XA partial (warp MMA) and release the stage.
 // RMS: TMA brings raw X and G; the four epilogue warps build the B tile
 // (x·g as bf16 hi + lo rows) in place while the stage's W boxes land, and
 // release it to the MMA issuer per stage (b_full).
-template <int MODE>
+//
+// SPLIT (fp32 / fp64 callers, tpo_gpu.h TPO_PREC_AUTO): every weight matrix
+// arrives as two bf16 planes, hi = bf16(w) and lo = bf16(w - hi), and both
+// planes accumulate into the same TMEM accumulator; the activations arrive
+// as hi rows + lo rows of the B operand (GATED: tokens 0-7 hi, 8-15 lo;
+// LoRA: N = 32, tokens 0-15 hi, 16-31 lo; RMS: raw fp32 X and G, split in
+// the B-tile build).  The sum (w_hi + w_lo)·(x_hi + x_lo) carries ~16
+// mantissa bits per operand, so the result meets the fp32-level tolerance
+// against the double reference on arbitrary inputs.  It costs 2x the weight
+// bytes of the bf16 kernel.
+template <int MODE, bool SPLIT>
 struct Cfg {
   static constexpr int NA = MODE == MODE_GATED ? 2 : 1;  // weight matrices
+  static constexpr int NP = NA * (SPLIT ? 2 : 1);         // weight planes (TMA maps)
+  static constexpr int kTokN = MODE == MODE_LORA && SPLIT ? 32 : 16;  // UMMA N
+  static constexpr uint32_t kXTileB = kTokN * 128;        // B operand tile bytes
   static constexpr bool kTmaX = MODE != MODE_RMS;        // per-stage B tile via TMA
   static constexpr uint32_t kAOff = 0;                   // W boxes lead the stage
-  static constexpr uint32_t kBOff = kAOff + NA * 2 * kWBox;
-  static constexpr uint32_t kXRawOff = kBOff + kXTile;     // RMS raw X
-  static constexpr uint32_t kGOff = kXRawOff + 1024;       // RMS G
+  static constexpr uint32_t kBOff = kAOff + NP * 2 * kWBox;
+  static constexpr uint32_t kXRawBytes = SPLIT ? 2048 : 1024;  // RMS X box [8][64] (fp32 | bf16)
+  static constexpr uint32_t kGBytes = SPLIT ? 256 : 128;       // RMS G box [64]
+  static constexpr uint32_t kXRawOff = kBOff + kXTileB;    // RMS raw X
+  static constexpr uint32_t kGOff = kXRawOff + kXRawBytes; // RMS G
   static constexpr uint32_t kABox = 2048;                  // LoRA A box [64 k][16 r]
-  static constexpr uint32_t kLAOff = kBOff + kXTile;       // LoRA A box in the stage
+  static constexpr int kNABox = SPLIT ? 2 : 1;             // LoRA A planes
+  static constexpr uint32_t kLAOff = kBOff + kXTileB;      // LoRA A box(es) in the stage
   static constexpr uint32_t kStage = MODE == MODE_RMS    ? kGOff + 1024
-                                     : MODE == MODE_LORA ? kLAOff + kABox
-                                                         : kBOff + kXTile;
-  static constexpr uint32_t kFullBytes = MODE == MODE_RMS ? NA * 2 * kWBox : kStage;
-  static constexpr uint32_t kXGBytes = 1024 + 128;  // RMS: X box [8][64] + G box [64]
+                                     : MODE == MODE_LORA ? kLAOff + kNABox * kABox
+                                                         : kBOff + kXTileB;
+  static constexpr uint32_t kFullBytes = MODE == MODE_RMS ? NP * 2 * kWBox : kStage;
+  static constexpr uint32_t kXGBytes = kXRawBytes + kGBytes;  // RMS: X box [8][64] + G box [64]
   static constexpr int kSide = MODE == MODE_RMS ? 8 : 0;  // RMS: Σx² per token, exchanged
   // stage releases: the UMMA commit, plus (LoRA) the four epilogue warps
   static constexpr uint32_t kEmptyCount = MODE == MODE_LORA ? 5 : 1;
+  static_assert(kStage % 1024 == 0, "stages must keep the 1024-B swizzle alignment");
 };
 
 constexpr int kMaxStages = 12;
@@ -107,12 +122,15 @@ __device__ __forceinline__ void st_async4(uint32_t addr, float a, float b, float
 // drains; when the weights are declared static (p.prefetch_static) they
 // start streaming their first pipeline stages before the grid dependency
 // resolves, so HBM stays busy across back-to-back µGraph evaluations.
-template <int MODE, int STAGES, int S, int MINB>
+template <int MODE, int STAGES, int S, int MINB, bool SPLIT>
 __global__ void __launch_bounds__(kThreads, MINB)
     skinny_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_constant__ CUtensorMap tmW1,
                   const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmA,
-                  const SkinnyParams p) {
-  using C = Cfg<MODE>;
+                  const __grid_constant__ CUtensorMap tmW2, const __grid_constant__ CUtensorMap tmW3,
+                  const __grid_constant__ CUtensorMap tmA1, const SkinnyParams p) {
+  using C = Cfg<MODE, SPLIT>;
+  // weight plane maps: bf16 {W} / {W1, W3}; SPLIT {W hi, W lo} / {W1 hi, W1 lo, W3 hi, W3 lo}
+  const CUtensorMap *wmap[4] = {&tmW0, &tmW1, &tmW2, &tmW3};
   static_assert(STAGES <= kMaxStages, "pipeline deeper than the barrier arrays");
   constexpr int kSide = C::kSide;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -151,10 +169,11 @@ __global__ void __launch_bounds__(kThreads, MINB)
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
-    tma_prefetch(&tmW0);
-    if (C::NA > 1) tma_prefetch(&tmW1);
+#pragma unroll
+    for (int w = 0; w < C::NP; ++w) tma_prefetch(wmap[w]);
     tma_prefetch(&tmX);
     if (MODE != MODE_GATED) tma_prefetch(&tmA);
+    if (MODE == MODE_LORA && SPLIT) tma_prefetch(&tmA1);
   }
   if (warp == 1) tmem_alloc<32>(&bars->tmem_base);
   tc_fence_before();
@@ -180,13 +199,15 @@ __global__ void __launch_bounds__(kThreads, MINB)
       mbar_expect_tx(&bars->full[kb], C::kFullBytes);
       const int k0 = kbase + kb * kBK;
       uint8_t *wt = st + C::kAOff;
-      tma_load_2d(wt, &tmW0, &bars->full[kb], n0, k0);
-      tma_load_2d(wt + kWBox, &tmW0, &bars->full[kb], n0 + 64, k0);
-      if (C::NA > 1) {
-        tma_load_2d(wt + 2 * kWBox, &tmW1, &bars->full[kb], n0, k0);
-        tma_load_2d(wt + 3 * kWBox, &tmW1, &bars->full[kb], n0 + 64, k0);
+#pragma unroll
+      for (int w = 0; w < C::NP; ++w) {
+        tma_load_2d(wt + 2 * w * kWBox, wmap[w], &bars->full[kb], n0, k0);
+        tma_load_2d(wt + (2 * w + 1) * kWBox, wmap[w], &bars->full[kb], n0 + 64, k0);
       }
-      if (MODE == MODE_LORA) tma_load_2d(st + C::kLAOff, &tmA, &bars->full[kb], 0, k0);  // A: static
+      if (MODE == MODE_LORA) {  // A: static
+        tma_load_2d(st + C::kLAOff, &tmA, &bars->full[kb], 0, k0);
+        if (SPLIT) tma_load_2d(st + C::kLAOff + C::kABox, &tmA1, &bars->full[kb], 0, k0);
+      }
     }
   }
   pdl_wait();  // inputs may be produced by the preceding kernel
@@ -225,11 +246,10 @@ __global__ void __launch_bounds__(kThreads, MINB)
       // CTA than the ring holds, issued only after this evaluation's X
       auto l2_pre = [&](int kb) {
         const int k0 = kbase + kb * kBK;
-        tma_prefetch_l2_2d(&tmW0, n0, k0);
-        tma_prefetch_l2_2d(&tmW0, n0 + 64, k0);
-        if (C::NA > 1) {
-          tma_prefetch_l2_2d(&tmW1, n0, k0);
-          tma_prefetch_l2_2d(&tmW1, n0 + 64, k0);
+#pragma unroll
+        for (int w = 0; w < C::NP; ++w) {
+          tma_prefetch_l2_2d(wmap[w], n0, k0);
+          tma_prefetch_l2_2d(wmap[w], n0 + 64, k0);
         }
       };
       const int l2a = p.l2_ahead;
@@ -247,16 +267,16 @@ __global__ void __launch_bounds__(kThreads, MINB)
         mbar_expect_tx(&bars->full[s], C::kFullBytes);
         const int k0 = kbase + kb * kBK;
         uint8_t *wt = st + C::kAOff;
-        tma_load_2d(wt, &tmW0, &bars->full[s], n0, k0);
-        tma_load_2d(wt + kWBox, &tmW0, &bars->full[s], n0 + 64, k0);
-        uint8_t *nx = wt + 2 * kWBox;
-        if (C::NA > 1) {
-          tma_load_2d(nx, &tmW1, &bars->full[s], n0, k0);
-          tma_load_2d(nx + kWBox, &tmW1, &bars->full[s], n0 + 64, k0);
-          nx += 2 * kWBox;
+#pragma unroll
+        for (int w = 0; w < C::NP; ++w) {
+          tma_load_2d(wt + 2 * w * kWBox, wmap[w], &bars->full[s], n0, k0);
+          tma_load_2d(wt + (2 * w + 1) * kWBox, wmap[w], &bars->full[s], n0 + 64, k0);
         }
-        if (C::kTmaX) tma_load_2d(nx, &tmX, &bars->full[s], k0, 0);
-        if (MODE == MODE_LORA) tma_load_2d(st + C::kLAOff, &tmA, &bars->full[s], 0, k0);
+        if (C::kTmaX) tma_load_2d(st + C::kBOff, &tmX, &bars->full[s], k0, 0);
+        if (MODE == MODE_LORA) {
+          tma_load_2d(st + C::kLAOff, &tmA, &bars->full[s], 0, k0);
+          if (SPLIT) tma_load_2d(st + C::kLAOff + C::kABox, &tmA1, &bars->full[s], 0, k0);
+        }
         // experiment (TPO_TRIG_EARLY = D): release the dependent grid D
         // k blocks before the last issue (one thread triggers the CTA)
         if (p.trig_early > 0 && kb == nkb - 1 - p.trig_early) pdl_launch();
@@ -267,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
     if (!early_trigger) pdl_launch();
   } else if (warp == 1) {
     // -------------------------------------------------------- MMA issuer
-    constexpr uint32_t idesc = idesc_bf16(kTileN, kTok, /*a MN-major*/ true, /*b K-major*/ false);
+    constexpr uint32_t idesc = idesc_bf16(kTileN, C::kTokN, /*a MN-major*/ true, /*b K-major*/ false);
     for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % STAGES;
       mbar_wait(&bars->full[s], (kb / STAGES) & 1);
@@ -291,9 +311,11 @@ __global__ void __launch_bounds__(kThreads, MINB)
         for (int kk = 0; kk < kBK / 16; ++kk) {
           const uint64_t bdesc = sdesc_sw128(xs + kk * 32, 16, 1024);
 #pragma unroll
-          for (int w = 0; w < C::NA; ++w) {
+          for (int w = 0; w < C::NP; ++w) {
+            // plane w accumulates into matrix w / 2 (SPLIT: hi then lo plane)
+            const int acc = SPLIT ? w / 2 : w;
             const uint64_t adesc = sdesc_sw128(smem_u32(wt + w * 2 * kWBox) + kk * 16 * 128, kWBox, 1024);
-            umma_bf16(tmem + w * kTok, adesc, bdesc, idesc, (kb | kk) != 0);
+            umma_bf16(tmem + acc * C::kTokN, adesc, bdesc, idesc, (kb | kk) != 0 || (SPLIT && (w & 1)));
           }
         }
         umma_commit(&bars->empty[s]);
@@ -317,13 +339,17 @@ __global__ void __launch_bounds__(kThreads, MINB)
     float dsc = 0.f;
     if (MODE == MODE_LORA) {  // every CTA folds its own XA partial times B̄ into its rows
 #pragma unroll
-      for (int r = 0; r < 16; ++r) bcol[r] = __bfloat162float(p.lora_b[size_t(r) * p.N + n0 + erow]);
+      for (int r = 0; r < 16; ++r)
+        bcol[r] = SPLIT ? p.lora_b_f32[size_t(r) * p.N + n0 + erow]
+                        : __bfloat162float(p.lora_b[size_t(r) * p.N + n0 + erow]);
     }
-    if (MODE == MODE_RMS) dsc = __bfloat162float(p.dscale[0]);
+    if (MODE == MODE_RMS) dsc = SPLIT ? p.dscale_f32[0] : __bfloat162float(p.dscale[0]);
     if (MODE == MODE_RMS) {
-      // Per stage: B tile rows 0-7 = bf16(x·g) (hi), rows 8-15 = the exact
+      // Per stage: B tile rows 0-7 = bf16(x·g) (hi), rows 8-15 = the
       // residual x·g - hi (lo), K-major with the 128-B swizzle.  Thread t
       // owns token t/16 and k = 4·(t%16) .. +3, so Σx² stays per token.
+      // bf16 X, G: the product is exact in fp32 and so is the residual;
+      // SPLIT (fp32 X, G): the fp32 product, split the same way.
       const int tok = t >> 4, sub = t & 15;
       const int c = sub >> 1, half = (sub & 1) * 8;
       const uint32_t off_hi = (tok >> 3) * 1024 + (tok & 7) * 128 + ((c ^ (tok & 7)) << 4) + half;
@@ -333,19 +359,31 @@ __global__ void __launch_bounds__(kThreads, MINB)
         const int s = kb % STAGES;
         mbar_wait(&bars->xg_full[s], (kb / STAGES) & 1);
         uint8_t *st = stages + s * C::kStage;
-        const uint2 xr = *reinterpret_cast<const uint2 *>(st + C::kXRawOff + tok * 128 + sub * 8);
-        const uint2 gr = *reinterpret_cast<const uint2 *>(st + C::kGOff + sub * 8);
-        const __nv_bfloat162 *x2 = reinterpret_cast<const __nv_bfloat162 *>(&xr);
-        const __nv_bfloat162 *g2 = reinterpret_cast<const __nv_bfloat162 *>(&gr);
+        float xf[4], gf[4];
+        if (SPLIT) {
+          const float4 xr = *reinterpret_cast<const float4 *>(st + C::kXRawOff + tok * 256 + sub * 16);
+          const float4 gr = *reinterpret_cast<const float4 *>(st + C::kGOff + sub * 16);
+          xf[0] = xr.x, xf[1] = xr.y, xf[2] = xr.z, xf[3] = xr.w;
+          gf[0] = gr.x, gf[1] = gr.y, gf[2] = gr.z, gf[3] = gr.w;
+        } else {
+          const uint2 xr = *reinterpret_cast<const uint2 *>(st + C::kXRawOff + tok * 128 + sub * 8);
+          const uint2 gr = *reinterpret_cast<const uint2 *>(st + C::kGOff + sub * 8);
+          const __nv_bfloat162 *x2 = reinterpret_cast<const __nv_bfloat162 *>(&xr);
+          const __nv_bfloat162 *g2 = reinterpret_cast<const __nv_bfloat162 *>(&gr);
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const float2 a = __bfloat1622float2(x2[j]), b = __bfloat1622float2(g2[j]);
+            xf[2 * j] = a.x, xf[2 * j + 1] = a.y, gf[2 * j] = b.x, gf[2 * j + 1] = b.y;
+          }
+        }
         uint32_t hi[2], lo[2];
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-          float2 xf = __bfloat1622float2(x2[j]), gf = __bfloat1622float2(g2[j]);
-          sumsq += xf.x * xf.x + xf.y * xf.y;
-          float p0 = xf.x * gf.x, p1 = xf.y * gf.y;  // exact in fp32 (8b x 8b mantissas)
+          sumsq += xf[2 * j] * xf[2 * j] + xf[2 * j + 1] * xf[2 * j + 1];
+          const float p0 = xf[2 * j] * gf[2 * j], p1 = xf[2 * j + 1] * gf[2 * j + 1];
           __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
           float2 hf = __bfloat1622float2(h);
-          __nv_bfloat162 l = __floats2bfloat162_rn(p0 - hf.x, p1 - hf.y);  // exact residual
+          __nv_bfloat162 l = __floats2bfloat162_rn(p0 - hf.x, p1 - hf.y);
           hi[j] = *reinterpret_cast<uint32_t *>(&h);
           lo[j] = *reinterpret_cast<uint32_t *>(&l);
         }
@@ -377,22 +415,33 @@ __global__ void __launch_bounds__(kThreads, MINB)
         const int s = kb % STAGES;
         mbar_wait(&bars->full[s], (kb / STAGES) & 1);
         const uint32_t st = smem_u32(stages + s * C::kStage);
-        uint32_t af[4], bf[4];
-        asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(af[0]), "=r"(af[1]), "=r"(af[2]), "=r"(af[3])
-                     : "r"(st + C::kBOff + a_off));
-        asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(bf[0]), "=r"(bf[1]), "=r"(bf[2]), "=r"(bf[3])
-                     : "r"(st + C::kLAOff + b_off));
+        // SPLIT: X^T hi rows 0-15 / lo rows 16-31 (+2 KB), A hi / lo boxes:
+        // XA = Σ over the hi/lo products
+        constexpr int NX = SPLIT ? 2 : 1;
+        uint32_t af[NX][4], bf[NX][4];
+#pragma unroll
+        for (int h = 0; h < NX; ++h) {
+          asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(af[h][0]), "=r"(af[h][1]), "=r"(af[h][2]), "=r"(af[h][3])
+                       : "r"(st + C::kBOff + h * 2048 + a_off));
+          asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(bf[h][0]), "=r"(bf[h][1]), "=r"(bf[h][2]), "=r"(bf[h][3])
+                       : "r"(st + C::kLAOff + h * C::kABox + b_off));
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars->empty[s]);
 #pragma unroll
-        for (int j = 0; j < 2; ++j)
-          asm volatile(
-              "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
-              "{%8,%9}, {%0,%1,%2,%3};"
-              : "+f"(c[j][0]), "+f"(c[j][1]), "+f"(c[j][2]), "+f"(c[j][3])
-              : "r"(af[0]), "r"(af[1]), "r"(af[2]), "r"(af[3]), "r"(bf[2 * j]), "r"(bf[2 * j + 1]));
+        for (int ha = 0; ha < NX; ++ha)
+#pragma unroll
+          for (int hb = 0; hb < NX; ++hb)
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+              asm volatile(
+                  "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+                  "{%8,%9}, {%0,%1,%2,%3};"
+                  : "+f"(c[j][0]), "+f"(c[j][1]), "+f"(c[j][2]), "+f"(c[j][3])
+                  : "r"(af[ha][0]), "r"(af[ha][1]), "r"(af[ha][2]), "r"(af[ha][3]), "r"(bf[hb][2 * j]),
+                    "r"(bf[hb][2 * j + 1]));
       }
       // per-warp partials -> xa_w[q][token][r]
       float *xw = xa_w + q * 256;
@@ -487,13 +536,20 @@ __global__ void __launch_bounds__(kThreads, MINB)
       tmem_ld16(tmem + (uint32_t(q * 32) << 16), v);
       if (MODE == MODE_GATED) {
         float v3[16];
-        tmem_ld16(tmem + (uint32_t(q * 32) << 16) + kTok, v3);
+        tmem_ld16(tmem + (uint32_t(q * 32) << 16) + C::kTokN, v3);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] = v[i], acc[8 + i] = v3[i];
+        for (int i = 0; i < 8; ++i)  // SPLIT: hi tokens 0-7 + lo tokens 8-15
+          acc[i] = SPLIT ? v[i] + v[8 + i] : v[i], acc[8 + i] = SPLIT ? v3[i] + v3[8 + i] : v3[i];
       } else if (MODE == MODE_RMS) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) acc[i] = v[i] + v[8 + i], acc[8 + i] = 0.f;
       } else {
+        if (SPLIT) {  // lo tokens in columns 16-31
+          float v2[16];
+          tmem_ld16(tmem + (uint32_t(q * 32) << 16) + 16, v2);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] += v2[i];
+        }
 #pragma unroll
         for (int i = 0; i < 16; ++i) acc[i] = v[i] + post[i];  // partial XW_s + XA_s·B̄
       }
@@ -564,9 +620,9 @@ __global__ void __launch_bounds__(kThreads, MINB)
 #undef TPO_T
 }
 
-template <int MODE, int STAGES, int S>
+template <int MODE, int STAGES, int S, bool SPLIT>
 size_t skinny_smem(const SkinnyParams &p) {
-  using C = Cfg<MODE>;
+  using C = Cfg<MODE, SPLIT>;
   const int nkb = p.k_per_cta / kBK;
   (void)nkb;
   size_t b = size_t(STAGES) * C::kStage +
@@ -575,11 +631,11 @@ size_t skinny_smem(const SkinnyParams &p) {
   return b + 1024;
 }
 
-template <int MODE, int STAGES, int S, int MINB>
+template <int MODE, int STAGES, int S, int MINB, bool SPLIT>
 cudaError_t launch_t(const CUtensorMap *maps, const SkinnyParams &p, cudaStream_t st) {
   if (p.ksplit != S) return cudaErrorInvalidValue;
-  const size_t smem = skinny_smem<MODE, STAGES, S>(p);
-  auto kern = skinny_kernel<MODE, STAGES, S, MINB>;
+  const size_t smem = skinny_smem<MODE, STAGES, S, SPLIT>(p);
+  auto kern = skinny_kernel<MODE, STAGES, S, MINB, SPLIT>;
   static size_t configured = 0;  // per instantiation: raise the smem limit once
   if (smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -600,36 +656,43 @@ cudaError_t launch_t(const CUtensorMap *maps, const SkinnyParams &p, cudaStream_
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = std::getenv("TPO_NO_PDL") ? 1 : 2;
-  return cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], p);
+  return cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], p);
 }
 
 }  // namespace tpo_fused
 
 using namespace tpo_fused;
 
-// (mode, stages, cluster split, CTAs per SM)
-#define TPO_SKINNY_CASES(X)                                                                     \
-  X(MODE_GATED, 4, 1, 1) X(MODE_GATED, 6, 1, 1) X(MODE_GATED, 3, 1, 2) X(MODE_GATED, 3, 2, 1)     \
-  X(MODE_GATED, 6, 2, 1) X(MODE_RMS, 4, 4, 2) X(MODE_RMS, 5, 4, 2) X(MODE_RMS, 3, 4, 2) X(MODE_RMS, 6, 4, 1) X(MODE_RMS, 8, 4, 1)            \
-  X(MODE_RMS, 10, 4, 1) X(MODE_RMS, 4, 2, 1) X(MODE_RMS, 6, 2, 1) X(MODE_RMS, 8, 2, 1)             \
-  X(MODE_RMS, 6, 1, 1) X(MODE_LORA, 4, 4, 2) X(MODE_LORA, 5, 4, 2) X(MODE_LORA, 6, 4, 1) X(MODE_LORA, 8, 4, 1)           \
-  X(MODE_LORA, 10, 4, 1) X(MODE_LORA, 6, 2, 1) X(MODE_LORA, 8, 2, 1) X(MODE_LORA, 6, 1, 1)
+// (mode, stages, cluster split, CTAs per SM, split precision)
+#define TPO_SKINNY_CASES(X)                                                                           \
+  X(MODE_GATED, 4, 1, 1, false) X(MODE_GATED, 6, 1, 1, false) X(MODE_GATED, 3, 1, 2, false)           \
+  X(MODE_GATED, 3, 2, 1, false) X(MODE_GATED, 6, 2, 1, false) X(MODE_RMS, 4, 4, 2, false)             \
+  X(MODE_RMS, 5, 4, 2, false) X(MODE_RMS, 3, 4, 2, false) X(MODE_RMS, 6, 4, 1, false)                 \
+  X(MODE_RMS, 8, 4, 1, false) X(MODE_RMS, 10, 4, 1, false) X(MODE_RMS, 4, 2, 1, false)                \
+  X(MODE_RMS, 6, 2, 1, false) X(MODE_RMS, 8, 2, 1, false) X(MODE_RMS, 6, 1, 1, false)                 \
+  X(MODE_LORA, 4, 4, 2, false) X(MODE_LORA, 5, 4, 2, false) X(MODE_LORA, 6, 4, 1, false)              \
+  X(MODE_LORA, 8, 4, 1, false) X(MODE_LORA, 10, 4, 1, false) X(MODE_LORA, 6, 2, 1, false)             \
+  X(MODE_LORA, 8, 2, 1, false) X(MODE_LORA, 6, 1, 1, false)                                           \
+  X(MODE_GATED, 3, 1, 1, true) X(MODE_GATED, 3, 2, 1, true) X(MODE_RMS, 5, 1, 1, true)                \
+  X(MODE_RMS, 5, 2, 1, true) X(MODE_RMS, 5, 4, 1, true) X(MODE_LORA, 5, 1, 1, true)                   \
+  X(MODE_LORA, 5, 2, 1, true) X(MODE_LORA, 5, 4, 1, true)
 
-extern "C" int tpo_skinny_launch(int mode, int stages, int minb, const CUtensorMap *maps,
+extern "C" int tpo_skinny_launch(int mode, int stages, int minb, int split, const CUtensorMap *maps,
                                  const SkinnyParams *p, cudaStream_t st) {
-#define TPO_CASE(M, ST, S, MB)                                  \
-  if (mode == M && stages == ST && p->ksplit == S && minb == MB) \
-    return int(launch_t<M, ST, S, MB>(maps, *p, st));
+#define TPO_CASE(M, ST, S, MB, SP)                                                           \
+  if (mode == M && stages == ST && p->ksplit == S && minb == MB && bool(split) == SP) \
+    return int(launch_t<M, ST, S, MB, SP>(maps, *p, st));
   TPO_SKINNY_CASES(TPO_CASE)
 #undef TPO_CASE
   return int(cudaErrorInvalidValue);
 }
 
-// Shared memory of (mode, stages, split, CTAs per SM) for `p`; 0 when that
-// configuration is not instantiated.
-extern "C" size_t tpo_skinny_smem(int mode, int stages, int minb, const SkinnyParams *p) {
-#define TPO_CASE(M, ST, S, MB) \
-  if (mode == M && stages == ST && p->ksplit == S && minb == MB) return skinny_smem<M, ST, S>(*p);
+// Shared memory of (mode, stages, split, CTAs per SM, precision) for `p`; 0
+// when that configuration is not instantiated.
+extern "C" size_t tpo_skinny_smem(int mode, int stages, int minb, int split, const SkinnyParams *p) {
+#define TPO_CASE(M, ST, S, MB, SP)                                                           \
+  if (mode == M && stages == ST && p->ksplit == S && minb == MB && bool(split) == SP) \
+    return skinny_smem<M, ST, S, SP>(*p);
   TPO_SKINNY_CASES(TPO_CASE)
 #undef TPO_CASE
   return 0;

@@ -7,14 +7,20 @@ candidates/s at 1/2/4/8 GPU".  The N=1 workload is configs[1], the GatedMLP
 fp32 out (grid 112, for-loop 16).  One step = one evaluation of that µGraph =
 one fused sm_100a kernel launch.  `value` is whole-job throughput in µGraph
 evaluations/s (replicas on every rank: the fused kernel does not shard,
-"scaling": "weak"); `latency_us` is the per-evaluation kernel latency.
-The weights (235 MB) exceed the 126 MB L2, so every step streams them from
-HBM; smaller workloads (--workload rmsnorm/lora) rotate through enough input
-copies to exceed L2.
+"scaling": "weak").  Two latencies, named for what they are:
+`period_us` = the steady-state period of back-to-back evaluations in one
+CUDA graph (PDL overlaps neighbours; `timeline` has every launch's start and
+end), `isolated_us` = one launch after an L2 flush.  The weights (235 MB)
+exceed the 126 MB L2, so every step streams them from HBM; smaller
+workloads rotate through enough input copies to exceed L2.
 
-The "verifier" object reports the sharded Z_p×Z_q verification throughput
-(candidates/s over all ranks, accept bits gathered with NCCL) on the SURVEY
-§8d candidate pools.  `--workload verify` makes it the headline instead.
+`fused` carries the same record (period, isolated latency, rooflines, e2e
+through the C-ABI with host buffers, the fp32-input split path, launch
+timeline, CPU reference) for all four benchmark µGraphs.  The "verifier"
+object reports the sharded Z_p×Z_q verification throughput (candidates/s
+over all ranks, one all-gather of packed accept words) on the SURVEY §8d
+candidate pools, with the reference on all host cores beside it.
+`--workload verify` makes the verifier the headline instead.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                   [--workload gatedmlp|rmsnorm|lora|gqa|verify]
@@ -152,7 +158,8 @@ class Clocks:
 
 # --------------------------------------------------------------------- workloads
 def fused_workload(name):
-    import torch
+    if name in fused_workload.cache:
+        return fused_workload.cache[name]
     from paper_2405_05751_b200 import fixtures as F
     prog, mu = F.bench_pair(name)
     args = F.BENCH[name]["args"]
@@ -162,9 +169,14 @@ def fused_workload(name):
     in_bytes = sum(x.numel() * 2 for x in host)
     out_shape = [mu["tensors"][t]["shape"] for t in mu["outputs"]][0]
     out_bytes = int(np.prod(out_shape)) * 4
-    return dict(name=name, prog=prog, mu=mu, host=host, in_bytes=in_bytes, out_bytes=out_bytes,
-                out_shape=out_shape, args=args, grid=F.BENCH[name]["grid"],
-                forloop=F.BENCH[name]["forloop"])
+    wl = dict(name=name, prog=prog, mu=mu, host=host, in_bytes=in_bytes, out_bytes=out_bytes,
+              out_shape=out_shape, args=args, grid=F.BENCH[name]["grid"],
+              forloop=F.BENCH[name]["forloop"])
+    fused_workload.cache[name] = wl
+    return wl
+
+
+fused_workload.cache = {}
 
 
 def numa_bind(dev):
@@ -193,7 +205,80 @@ def numa_bind(dev):
         return None
 
 
-def run_fused(args, dist, wl):
+def workload_label(wl):
+    """config.workload of both arms (ours and --impl reference)."""
+    return (f"{wl['name']} µGraph, inputs {[list(x.shape) for x in wl['host']]}, grid {wl['grid']}, "
+            f"loop {wl['forloop']} (BASELINE.json configs)")
+
+
+RING, RING_CTAS = 16, 4096
+
+
+def launch_timeline(ctx, g, sets, outs, stream):
+    """Per-launch start / end of 16 back-to-back evaluations replayed as one
+    CUDA graph (as the timed region runs them): every launch stamps its own
+    slot of the library's %globaltimer ring (TPO_DEBUG_RING) — first CTA
+    start and last CTA end per launch.  A launch starting before its
+    predecessor ends is the PDL overlap that makes the period shorter than
+    one kernel's duration."""
+    import ctypes
+    import torch
+    from paper_2405_05751_b200 import _native
+    os.environ["TPO_DEBUG_RING"] = "1"
+    try:
+        copies = len(sets)
+        # one eager launch allocates the ring (no allocation inside a capture)
+        ctx.eval_mugraph(g, sets[0], outputs=[outs[0]], stream=stream.cuda_stream)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            for i in range(RING):
+                ctx.eval_mugraph(g, sets[i % copies], outputs=[outs[i % copies]],
+                                 stream=torch.cuda.current_stream().cuda_stream)
+        lib = _native.lib()
+        lib.tpo_debug_ring_read.restype = ctypes.c_int
+        buf = np.zeros(RING * RING_CTAS * 16, dtype=np.uint64)
+        seq = 0
+        for _ in range(3):
+            graph.replay()
+            torch.cuda.synchronize()
+            seq = lib.tpo_debug_ring_read(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(buf.size))
+        del graph
+    finally:
+        os.environ.pop("TPO_DEBUG_RING", None)
+    h = buf.reshape(RING, RING_CTAS, 16).astype(np.int64)
+    order = [(seq - RING + i) % RING for i in range(RING)]
+    se = []
+    for slot in order:
+        s0, e7 = h[slot, :, 0], h[slot, :, 7]
+        se.append((s0[s0 > 0].min(), e7[e7 > 0].max()))
+    t0 = se[0][0]
+    launches = [[round((s - t0) / 1e3, 2), round((e - t0) / 1e3, 2)] for s, e in se]
+    steady = se[3:]
+    dur = [(e - s) / 1e3 for s, e in steady]
+    period = [(steady[i + 1][0] - steady[i][0]) / 1e3 for i in range(len(steady) - 1)]
+    overlap = [(steady[i][1] - steady[i + 1][0]) / 1e3 for i in range(len(steady) - 1)]
+    return {"launches_us": launches, "mean_kernel_us": round(float(np.mean(dur)), 3),
+            "mean_period_us": round(float(np.mean(period)), 3),
+            "mean_overlap_us": round(float(np.mean(overlap)), 3),
+            "overlapping_launches": int(sum(o > 0 for o in overlap)),
+            "note": "first CTA start / last CTA end per launch (%globaltimer ring, launches 3-15 "
+                    "steady state); overlap = predecessor's end - this launch's start"}
+
+
+def measure_fused(args, dist, wl, headline=False):
+    """One benchmark µGraph on this rank's GPU:
+    * period_us: K evaluations back to back, replayed as one CUDA graph
+      (CUDA events on the launching stream), inputs rotated over enough
+      copies to exceed L2 — the pipelined steady state (PDL lets one
+      evaluation's prologue and weight prefetch overlap the previous one);
+    * isolated_us: ONE launch after an L2 flush (a 256 MB write), median of
+      20 — the single-evaluation latency;
+    * e2e: tpo_gpu_eval_mugraph_host with pinned host buffers (copies in the
+      timed region);
+    * fp32_inputs: the same evaluation from fp32 device buffers (precision
+      policy AUTO: on-device split into bf16 hi + lo, then the SPLIT kernel);
+    * timeline: per-launch start / end of 16 graph launches."""
     import torch
     from paper_2405_05751_b200.api import Context
     dev = dist.local
@@ -223,13 +308,13 @@ def run_fused(args, dist, wl):
             step(i)
     torch.cuda.synchronize()
     dist.barrier()
-    clocks = Clocks(dev)
-    clocks.start()
-    time.sleep(0.1)
-    # ---- device-resident timed region: K evaluations back to back
+    clocks = Clocks(dev) if headline else None
+    if clocks:
+        clocks.start()
+        time.sleep(0.1)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     # keep the GPU busy long enough for the clock sampler to see it
-    hot_until = time.time() + (0.0 if args.profile else 0.3)
+    hot_until = time.time() + (0.3 if headline and not args.profile else 0.0)
     i = 0
     with torch.cuda.stream(stream):
         while time.time() < hot_until:
@@ -237,8 +322,8 @@ def run_fused(args, dist, wl):
             i += 1
             if i % 64 == 0:
                 stream.synchronize()
-    # the K evaluations are captured once into a CUDA graph (the kernels are
-    # µs-scale: host launch overhead must not sit between them)
+    # ---- pipelined period: the K evaluations captured once into a CUDA graph
+    # (the kernels are µs-scale: host launch overhead must not sit between them)
     graph = torch.cuda.CUDAGraph()
     with torch.cuda.graph(graph, stream=stream):
         for i in range(args.steps):
@@ -256,20 +341,80 @@ def run_fused(args, dist, wl):
     torch.cuda.synchronize()
     dist.barrier()
     ms_local = e0.elapsed_time(e1)
-    clk = clocks.stop()
+    clk = clocks.stop() if clocks else None
+    del graph
     ms = dist.max(ms_local)
     per_eval_ms = ms / args.steps
     value = dist.world * args.steps / (ms / 1e3)
-
+    peak, peak_kind = peaks()
+    achieved = alg / (per_eval_ms / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_kind,
+            "algorithmic_bytes": int(alg), "basis": "pipelined period"}
+    prof = os.path.join(ROOT, "profiles", f"traffic_{wl['name']}.json")
+    if os.path.exists(prof):
+        try:
+            roof["traffic"] = json.load(open(prof))["dram_bytes_per_launch"]
+        except Exception:
+            pass
+    res = dict(name=wl["name"], value=value, ms=per_eval_ms, roof=roof, clocks=clk,
+               gpu_launches=args.steps, copies=copies)
+    if args.profile:
+        return res
+    # ---- isolated single-evaluation latency: L2 flushed, one launch
+    # the flush READS 256 MB (> the 126 MB L2): L2 then holds clean lines of
+    # another buffer (a write flush would leave 126 MB of dirty lines to be
+    # written back during the measured launch)
+    flush = torch.ones(32 * 2**20, dtype=torch.int64, device="cuda")
+    iso = []
+    with torch.cuda.stream(stream):
+        for i in range(20):
+            flush.sum()
+            e0.record(stream)
+            step(i)
+            e1.record(stream)
+            e1.synchronize()
+            iso.append(e0.elapsed_time(e1))
+    del flush
+    iso_ms = float(np.median(iso))
+    res["isolated_us"] = round(iso_ms * 1e3, 3)
+    res["roofline_isolated"] = {"achieved": round(alg / (iso_ms / 1e3) / 1e9, 1), "peak": peak,
+                                "unit": "GB/s", "frac": round(alg / (iso_ms / 1e3) / 1e9 / peak, 4),
+                                "basis": "one launch after a 256 MB read (L2 flushed), median of 20"}
+    # ---- per-launch timeline of the pipelined graph
+    try:
+        res["timeline"] = launch_timeline(ctx, g, sets, outs, stream)
+    except Exception as e:  # evidence only; never fails the bench
+        res["timeline"] = {"error": str(e)[:200]}
+    # ---- fp32 device inputs: precision policy AUTO (split kernel)
+    f32 = [[x.float().cuda() for x in wl["host"]]]
+    n32 = max(1, -(-3 * L2_BYTES // (2 * wl["in_bytes"]))) if 2 * wl["in_bytes"] < 3 * L2_BYTES else 1
+    f32 += [[x.clone() for x in f32[0]] for _ in range(n32 - 1)]
+    g32 = ctx.compile(wl["mu"])
+    with torch.cuda.stream(stream):
+        for i in range(3):
+            ctx.eval_mugraph(g32, f32[i % n32], outputs=[outs[i % copies]], stream=st)
+        torch.cuda.synchronize()
+        k32 = max(10, min(args.steps, 50))
+        e0.record(stream)
+        for i in range(k32):
+            ctx.eval_mugraph(g32, f32[i % n32], outputs=[outs[i % copies]], stream=st)
+        e1.record(stream)
+    e1.synchronize()
+    del f32
+    res["fp32_inputs"] = {"us_per_eval": round(e0.elapsed_time(e1) / k32 * 1e3, 2),
+                          "precision": "TPO_PREC_AUTO: on-device split into bf16 hi + lo planes, SPLIT kernel "
+                                       "(meets 1e-3·max(|r|, rms) vs the double reference on arbitrary inputs)",
+                          "note": "includes the per-call conversion kernels (fp32 read, 2 planes written)"}
     # ---- end to end through the C-ABI with HOST buffers: every step copies
     # that step's inputs host->device (pinned), runs the fused kernel and
-    # copies the output back (tpo_gpu_eval_mugraph_host, synchronous)
-    # host buffers on the GPU's NUMA node (pinned pages are placed where the
+    # copies the output back (tpo_gpu_eval_mugraph_host, synchronous).
+    # Host buffers on the GPU's NUMA node (pinned pages are placed where the
     # allocating thread runs): the H2D copies then run at the link rate
     prev_aff = numa_bind(dev)
     pinned = [x.pin_memory() for x in wl["host"]]
     out_h = torch.empty(wl["out_shape"], dtype=torch.float32).pin_memory()
-    e2e_steps = 0 if args.profile else max(3, min(args.steps, 50))
+    e2e_steps = max(3, min(args.steps, 50 if headline else 20))
     ctx.eval_mugraph_host(g, pinned, outputs=[out_h], stream=st)  # warm the staging buffers
     torch.cuda.synchronize()
     dist.barrier()
@@ -283,35 +428,33 @@ def run_fused(args, dist, wl):
     e2e_ms = max(dist.max(e0.elapsed_time(e1)), 1e-9)
     if prev_aff is not None:
         os.sched_setaffinity(0, prev_aff)
-    e2e = {"value": round(dist.world * e2e_steps / (e2e_ms / 1e3), 3), "unit": "evals/s",
-           "h2d_bytes_per_step": int(wl["in_bytes"]), "d2h_bytes_per_step": int(wl["out_bytes"]),
-           "ms_per_step": round(e2e_ms / max(e2e_steps, 1), 4),
-           "numa_bound": prev_aff is not None,
-           "path": "tpo_gpu_eval_mugraph_host (C-ABI, pinned host buffers, copies in the timed region)"}
-
-    peak, peak_kind = peaks()
-    achieved = alg / (per_eval_ms / 1e3) / 1e9
-    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_kind,
-            "algorithmic_bytes": int(alg)}
-    prof = os.path.join(ROOT, "profiles", f"traffic_{wl['name']}.json")
-    if os.path.exists(prof):
-        try:
-            roof["traffic"] = json.load(open(prof))["dram_bytes_per_launch"]
-        except Exception:
-            pass
-    return dict(value=value, ms=per_eval_ms, roof=roof, e2e=e2e, clocks=clk,
-                gpu_launches=args.steps, copies=copies)
+    res["e2e"] = {"value": round(dist.world * e2e_steps / (e2e_ms / 1e3), 3), "unit": "evals/s",
+                  "h2d_bytes_per_step": int(wl["in_bytes"]), "d2h_bytes_per_step": int(wl["out_bytes"]),
+                  "ms_per_step": round(e2e_ms / max(e2e_steps, 1), 4),
+                  "numa_bound": prev_aff is not None,
+                  "path": "tpo_gpu_eval_mugraph_host (C-ABI, pinned host buffers, copies in the timed region)"}
+    return res
 
 
-def cpu_baseline_fused(wl, threads=1, min_seconds=10.0):
+def fused_object(r, cpu):
+    """The per-family record of the JSON line."""
+    out = {"workload": workload_label(fused_workload.cache[r["name"]]),
+           "period_us": round(r["ms"] * 1e3, 3), "isolated_us": r.get("isolated_us"),
+           "value": round(r["value"], 2), "unit": "evals/s", "roofline": r["roof"],
+           "roofline_isolated": r.get("roofline_isolated"), "e2e": r.get("e2e"),
+           "fp32_inputs": r.get("fp32_inputs"), "timeline": r.get("timeline"),
+           "cpu_baseline": cpu, "gpu_launches": r["gpu_launches"]}
+    return out
+
+
+def cpu_baseline_fused(wl, threads=1, min_seconds=10.0, min_reps=1):
     """The compiled reference (oracle/_ref) eval_mugraph on the host CPU."""
     from oracle import ref
     if not ref.available():
         return None
     ins = [x.float().numpy().astype(np.float64) for x in wl["host"]]
     reps, total = 0, 0.0
-    while total < min_seconds * 1e3 and reps < 50:
+    while (total < min_seconds * 1e3 or reps < min_reps) and reps < 50:
         total += ref.time_eval_mugraph(wl["mu"], ins, 1)
         reps += 1
     per = total / reps
@@ -394,8 +537,7 @@ def reference_arm(args, wl):
             "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": f"{name} µGraph {wl['args']} grid {wl['grid']} loop {wl['forloop']}",
-                       "threads": T},
+            "config": {"workload": workload_label(wl), "threads": T},
             "cpu_baseline": {"value": v, "unit": "evals/s", "cores": T, "kind": "reference",
                              "sample": f"full µGraph per step: reference eval_mugraph on {T} "
                                        f"column slice(s) concurrently"},
@@ -406,12 +548,15 @@ def reference_arm(args, wl):
 # ------------------------------------------------------------------------- verifier
 def run_verify(dist, n_total, steps=1, warmup=3, pool_fams=("rmsnorm", "gatedmlp", "gqa", "lora")):
     """Shard n_total candidates (n_total / 4 per family; candidate i of a
-    family = pool[i % |pool|], seed i) across ranks as contiguous index
-    ranges (paper_2405_05751_b200.shard); each rank verifies its ranges on
-    its GPU into packed accept bits, then ONE all-gather per family
-    reassembles them.  One step = all n_total candidates; `steps` timed
-    steps after `warmup` short ones.  Returns cand/s over all ranks
-    (max-rank device time)."""
+    family = pool[i % |pool|], seed i) across ranks: the four families'
+    packed accept bits share one word space (shard.WordLayout) and each rank
+    owns one contiguous word range, balanced by the per-candidate cost
+    measured in the warm-up; it verifies its ranges on its GPU (one
+    tpo_gpu_verify_pool launch per family segment) into ONE local buffer, and
+    the step ends with ONE all-gather of it.  Timed leg: the verify kernels
+    plus the gather, CUDA events, max over ranks; the host unpack follows
+    outside it.  One step = all n_total candidates."""
+    import hashlib
     import torch
     from paper_2405_05751_b200 import fixtures as F
     from paper_2405_05751_b200 import shard
@@ -419,79 +564,100 @@ def run_verify(dist, n_total, steps=1, warmup=3, pool_fams=("rmsnorm", "gatedmlp
     ctx = Context(dist.local)
     fams = F.verify_families()
     per_fam = n_total // len(pool_fams)
-    ranges = [shard.even_range(per_fam, dist.world, r) for r in range(dist.world)]
-    first, n = ranges[dist.rank]
-    jobs = []
+    fam_jobs = []
     for f in pool_fams:
         prog, pool = fams[f]
         gp = ctx.compile(prog)
         gs = [ctx.compile(g) for _, g in pool]
-        jobs.append((f, gp, gs))
-    acc = [torch.zeros(max(1, -(-n // 32)), dtype=torch.int32, device="cuda") for _ in jobs]
-    for _ in range(warmup):  # compile/upload paths, clocks
-        for (f, gp, gs), a in zip(jobs, acc):
-            ctx.verify_pool(gp, gs, first=0, n=min(max(n, 1), 4096), accept_dev=a)
-    torch.cuda.synchronize()
-    dist.barrier()
+        fam_jobs.append((f, gp, gs))
+    layout = shard.WordLayout([per_fam] * len(fam_jobs))
+    # warm-up (compile / upload paths, clocks) doubling as the cost probe:
+    # seconds per candidate of each family, averaged over ranks so every rank
+    # derives the same ranges
+    probe = min(per_fam, 8192)
+    scratch = torch.zeros(max(1, -(-probe // 32)), dtype=torch.int32, device="cuda")
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    cost = []
+    for w in range(max(warmup, 1)):
+        cost = []
+        for f, gp, gs in fam_jobs:
+            e0.record()
+            ctx.verify_pool(gp, gs, first=0, n=probe, accept_dev=scratch)
+            e1.record()
+            torch.cuda.synchronize()
+            cost.append(dist.sum(e0.elapsed_time(e1)) / dist.world / probe)
+    ranges = layout.rank_words(layout.word_costs(cost), dist.world)
+    w0, nw = ranges[dist.rank]
+    jobs = layout.jobs(w0, nw)
+    local = torch.zeros(max(nw, 1), dtype=torch.int32, device="cuda")
     g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t_kernel = t_gather = 0.0
-    attempts = accepted = 0
+    attempts = 0
+    words = None
     for step in range(steps):
-        for a in acc:
-            a.zero_()
         dist.barrier()
+        torch.cuda.synchronize()
         e0.record()
         attempts = 0
-        for (f, gp, gs), a in zip(jobs, acc):
-            if n:
-                _, att = ctx.verify_pool(gp, gs, first=first, n=n, accept_dev=a)
-                attempts += att
+        for fi, first, n, off in jobs:
+            _, gp, gs = fam_jobs[fi]
+            _, att = ctx.verify_pool(gp, gs, first=first, n=n, accept_dev=local[off:])
+            attempts += att
         e1.record()
-        # the single collective: packed accept bits, one all-gather per family
         g0.record()
-        accepted = 0
-        for a in acc:
-            accepted += int(shard.gather_accept(a, ranges, per_fam, dist.pg).sum())
+        words = shard.gather_words(local[:nw], ranges, dist.pg)  # the single collective
         g1.record()
         torch.cuda.synchronize()
         t_kernel += e0.elapsed_time(e1) / 1e3
         t_gather += g0.elapsed_time(g1) / 1e3
     t_local = t_kernel / steps
     t_all = dist.max((t_kernel + t_gather) / steps)
+    gather_share = dist.max(t_gather / steps) / t_all
+    # host unpack, outside the timed leg
+    host_words = words.cpu().numpy()
+    accept = layout.unpack(host_words)
+    accepted = int(sum(int(a.sum()) for a in accept))
+    accept_sha = hashlib.sha256(np.ascontiguousarray(host_words).view(np.uint32).tobytes()).hexdigest()[:16]
     # end to end through the public API: verify_pool calls + accept bits to the host
     torch.cuda.synchronize()
     dist.barrier()
-    w0 = time.perf_counter()
-    host_bits = []
-    for (f, gp, gs), a in zip(jobs, acc):
-        if n:
-            ctx.verify_pool(gp, gs, first=first, n=n, accept_dev=a)
-        host_bits.append(a.cpu())
-    e2e_s = dist.max(time.perf_counter() - w0)
-    e2e = {"value": round(per_fam * len(jobs) / e2e_s, 1), "unit": "candidates/s",
-           "h2d_bytes_per_step": int(sum(4 * len(gs) for _, _, gs in jobs)),
-           "d2h_bytes_per_step": int(sum(a.numel() * 4 for a in acc)) * dist.world,
+    w_0 = time.perf_counter()
+    for fi, first, n, off in jobs:
+        _, gp, gs = fam_jobs[fi]
+        ctx.verify_pool(gp, gs, first=first, n=n, accept_dev=local[off:])
+    local.cpu()
+    e2e_s = dist.max(time.perf_counter() - w_0)
+    e2e = {"value": round(per_fam * len(fam_jobs) / e2e_s, 1), "unit": "candidates/s",
+           "h2d_bytes_per_step": int(sum(4 * len(gs) for _, _, gs in fam_jobs)),
+           "d2h_bytes_per_step": int(layout.total_words * 4),
            "path": "Context.verify_pool (C-ABI tpo_gpu_verify_pool) + accept bits to host, wall clock; "
                    "inputs are generated on the device by design (h2d = pool map; bytecode ~KB)"}
-    n_done = per_fam * len(jobs)
+    jobs = [(fam_jobs[fi][0], fam_jobs[fi][1], fam_jobs[fi][2], first, n) for fi, first, n, _ in jobs]
+    n_done = per_fam * len(fam_jobs)
     stream = search_stream(ctx, dist, fams, pool_fams)
     stab = stability_stage(ctx, dist, fams, pool_fams)
     # algorithmic work: field MACs = 2 fields x (op_madds(program)
     # + op_madds(candidate)) per attempt the reference consumes; per-candidate
-    # attempts from an untimed verdict pass over this rank's shard
-    macs = 0
-    for (f, gp, gs), a in zip(jobs, acc):
-        if not n:
-            continue
+    # attempts from an untimed verdict pass over this rank's shard.  RNG work
+    # (reported separately): 2 splitmix64 draws per input element
+    # of the program's inputs per attempt, +1 for omega, +340 for the SiLU
+    # tables when either graph has SiLU
+    from paper_2405_05751_b200.graph import has_silu
+    macs = draws = 0.0
+    for f, gp, gs, first, n in jobs:
         v, _ = ctx.verify_pool(gp, gs, first=first, n=n, want_verdicts=True)
         idx = (np.arange(first, first + n) % len(gs))
         cm = np.array([g.madds for g in gs], dtype=np.float64)[idx]
-        macs += float(np.sum((v["rounds_run"] + v["resamples"]) * 2.0 * (gp.madds + cm)))
+        att = (v["rounds_run"] + v["resamples"]).astype(np.float64)
+        macs += float(np.sum(att * 2.0 * (gp.madds + cm)))
+        silu = np.array([has_silu(g.spec) or has_silu(gp.spec) for g in gs])[idx]
+        draws += float(np.sum(att * (2.0 * gp.info.input_elems + 1 + 340.0 * silu)))
     macs = dist.sum(macs)
-    peak = None
+    draws = dist.sum(draws)
+    peak = dp4a = None
     try:
-        peak = json.load(open(os.path.join(ROOT, "profiles", "int_peak.json")))["imad_per_s"]
+        pk = json.load(open(os.path.join(ROOT, "profiles", "int_peak.json")))
+        peak, dp4a = pk["imad_per_s"], pk.get("dp4a_per_s")
     except Exception:
         pass
     roof = {"bound": "int-issue (IMAD)", "achieved": round(macs / t_all / 1e12, 4),
@@ -502,24 +668,27 @@ def run_verify(dist, n_total, steps=1, warmup=3, pool_fams=("rmsnorm", "gatedmlp
             "note": "peak per SURVEY §8d: measured IMAD rate (1 field MAC per IMAD). The 2x2 "
                     "matmul path uses dp4a (2 field MACs per instruction, frac_vs_dp4a_2lane). "
                     "Field MACs are a minority of the work: per attempt the inputs are "
-                    "regenerated (2 splitmix64 draws + a mod per element) and both graphs "
-                    "interpreted; see issue_utilization"}
+                    "regenerated (2 splitmix64 draws + a mod per element, the rng term) and "
+                    "both graphs interpreted; see issue_utilization"}
+    # the RNG term: a splitmix64 draw + its mod-uniform reduction is ~12
+    # integer instructions (3 IMAD-pipe multiplies + shifts / xors / the
+    # magic-number mod), so 12 x draws / IMAD peak is its instruction share
+    roof["rng"] = {"draws": draws, "draws_per_s": round(draws / t_all, 1),
+                   "instr_per_draw_est": 12,
+                   "frac_of_issue_est": round(12 * draws / t_all / peak, 4) if peak else None}
     roof["issue_utilization"] = ncu_issue("verify")
-    # the 2 x 2 matmul path packs two k terms of one field per dp4a (16-bit
-    # words): its instruction-level bound is 2 field MACs per dp4a
-    try:
-        dp4a = json.load(open(os.path.join(ROOT, "profiles", "int_peak.json")))["dp4a_per_s"]
+    if dp4a:
         roof["frac_vs_dp4a_2lane"] = round(macs / t_all / (2 * dp4a), 4)
         roof["dp4a_2lane_peak"] = round(2 * dp4a / 1e12, 3)
-    except Exception:
-        pass
     return {"value": round(n_done / t_all, 1), "unit": "candidates/s", "candidates": n_done,
             "roofline": roof,
             "seconds": round(t_all, 4), "kernel_seconds_max_rank": round(dist.max(t_local), 4),
-            "accepted": accepted, "attempts_rank0": int(attempts), "e2e": e2e, "steps": steps,
-            "gpu_launches_per_step": len(jobs) * (1 if n else 0),
+            "gather_share": round(gather_share, 5), "ranges_words": ranges,
+            "accepted": accepted, "accept_sha16": accept_sha, "attempts_rank0": int(attempts), "e2e": e2e,
+            "steps": steps, "gpu_launches_per_step": len(jobs),
             "families": list(pool_fams), "seed_rule": "candidate i = pool[i % |pool|], seed i",
-            "timing": "CUDA events: verify kernels + accept-bit all-gather, max over ranks",
+            "timing": "CUDA events: verify kernels + ONE accept-word all-gather, max over ranks; "
+                      "host unpack outside",
             "search_stream": stream, "stability_filter": stab}
 
 
@@ -637,7 +806,7 @@ def ncu_issue(tag):
     return out
 
 
-def cpu_baseline_verify(n=4000):
+def cpu_baseline_verify(n=10000):
     from oracle import ref
     from paper_2405_05751_b200 import fixtures as F
     if not ref.available():
@@ -652,7 +821,9 @@ def cpu_baseline_verify(n=4000):
         cnt += n // 4
     return {"value": round(cnt / (total_ms / 1e3), 1), "unit": "candidates/s", "cores": threads,
             "kind": "reference",
-            "sample": f"{cnt} candidates ({n // 4} per family, first indices) of the same pools"}
+            "sample": f"{cnt} candidates, stratified: {n // 4} per family (indices 0..{n // 4 - 1}, "
+                      f"every pool member ~{n // 4 // 45}x, seed i), the same pools, "
+                      f"random_test_equivalence on {threads} threads"}
 
 
 # ----------------------------------------------------------------------------- main
@@ -667,6 +838,8 @@ def main():
     ap.add_argument("--verify-candidates", type=int, default=1_000_000)
     ap.add_argument("--no-verifier", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fused-all", action="store_true",
+                    help="headline µGraph only (skip the per-family `fused` object)")
     ap.add_argument("--no-static", action="store_true",
                     help="do not declare the weight inputs static (no pre-PDL-wait weight prefetch)")
     ap.add_argument("--profile", action="store_true",
@@ -674,7 +847,7 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.profile:
-        args.no_verifier = args.no_cpu_baseline = True
+        args.no_verifier = args.no_cpu_baseline = args.no_fused_all = True
 
     if args.impl == "reference":
         rank = int(os.environ.get("RANK", "0"))
@@ -711,28 +884,46 @@ def main():
         return
 
     wl = fused_workload(args.workload)
-    r = run_fused(args, dist, wl)
+    r = measure_fused(args, dist, wl, headline=True)
     line = {
         "metric": METRIC, "value": round(r["value"], 2), "unit": "evals/s",
         "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(r["ms"], 5), "latency_us": round(r["ms"] * 1e3, 3),
+        "ms_per_step": round(r["ms"], 5), "period_us": round(r["ms"] * 1e3, 3),
+        "isolated_us": r.get("isolated_us"),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic",
-        "config": {"workload": f"{wl['name']} µGraph, inputs {[list(x.shape) for x in wl['host']]}, "
-                               f"grid {wl['grid']}, loop {wl['forloop']} (BASELINE.json configs)",
+        "config": {"workload": workload_label(wl),
                    "global_batch": int(wl["host"][0].shape[0]), "parallelism": f"replica{dist.world}",
                    "l2": ("inputs larger than L2" if r["copies"] == 1 else
                           f"rotating {r['copies']} input copies (> L2)"),
                    "static_weights": (None if args.no_static else
                                       [int(i) for i in STATIC_WEIGHTS[wl["name"]]])},
-        "roofline": r["roof"], "e2e": r["e2e"], "gpu_launches": r["gpu_launches"],
-        "timing": "K evaluations replayed as one CUDA graph, CUDA events on the launching stream",
-        "clocks": r["clocks"],
+        "roofline": r["roof"], "roofline_isolated": r.get("roofline_isolated"), "e2e": r.get("e2e"),
+        "gpu_launches": r["gpu_launches"],
+        "timing": "period: K evaluations replayed as one CUDA graph, CUDA events on the launching "
+                  "stream (PDL overlap, see timeline); isolated: one launch after an L2 flush",
+        "clocks": r["clocks"], "timeline": r.get("timeline"), "fp32_inputs": r.get("fp32_inputs"),
     }
+    cpu = {}
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        cpu[wl["name"]] = cpu_baseline_fused(wl)
+        line["cpu_baseline"] = cpu[wl["name"]]
+    if not args.profile and not args.no_fused_all:
+        # every benchmark µGraph, each with its own roofline, e2e and CPU baseline
+        fused = {}
+        for name in ("gatedmlp", "rmsnorm", "lora", "gqa"):
+            if name == wl["name"]:
+                rr = r
+            else:
+                rr = measure_fused(args, dist, fused_workload(name))
+            if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline and name not in cpu:
+                cpu[name] = cpu_baseline_fused(fused_workload(name), min_seconds=4.0, min_reps=3)
+            fused[name] = fused_object(rr, cpu.get(name))
+        line["fused"] = fused
     if not args.no_verifier:
         line["verifier"] = run_verify(dist, args.verify_candidates, steps=1, warmup=3)
-    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline_fused(wl)
+        if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+            line["verifier"]["cpu_baseline"] = cpu_baseline_verify()
     if dist.rank == 0 and not args.profile:
         line["generic_vm"] = generic_vm(wl)
     if dist.rank == 0:

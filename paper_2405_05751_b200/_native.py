@@ -10,6 +10,9 @@ import re
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 LIB_PATH = os.path.join(PKG, "libtpo_b200.so")
+# experiments only (A/B of build variants): TPO_NATIVE_LIB names another in-tree build
+if os.environ.get("TPO_NATIVE_LIB"):
+    LIB_PATH = os.path.join(PKG, os.path.basename(os.environ["TPO_NATIVE_LIB"]))
 HEADER = os.path.join(ROOT, "include", "tpo_gpu.h")
 
 

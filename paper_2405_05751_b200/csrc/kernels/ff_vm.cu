@@ -20,6 +20,7 @@
 #include <stdint.h>
 
 #include "ff_vm.cuh"
+#include "smem_limit.cuh"
 #include "vm.h"
 
 // tpo::ErrCode::PoisonedExponent (include/tpo/ir/shape.hpp; C-ABI status 1000 + code)
@@ -608,25 +609,40 @@ __device__ bool first_mismatch(const SmemT<WT> &s, const TpoVmGraph &g1, const T
 
 // NT threads per candidate CTA: 256, or 128 when shared memory admits
 // twice as many resident candidates (more independent barrier domains).
+// A register cap instead of __launch_bounds__: with launch bounds alone
+// ptxas squeezed the 64/128-thread variants to 72 registers and spilled
+// (24-40 B stack frames); 80 fits every variant without local memory (78-79 used: six 128-thread CTAs per SM by registers).
+#ifndef TPO_VM_REGCAP
+#define TPO_VM_REGCAP 80
+#endif
 template <bool PROF, int NT, typename WT>
-__global__ void __launch_bounds__(NT) verify_kernel(VerifyArgs a) {
+#if TPO_VM_REGCAP > 0
+__global__ void __maxnreg__(PROF ? 88 : TPO_VM_REGCAP) verify_kernel(VerifyArgs a) {
+#else
+__global__ void __launch_bounds__(NT) verify_kernel(VerifyArgs a) {  // experiment: ptxas' own choice
+#endif
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int s_flag, s_slow;
   __shared__ uint32_t s_omega;
   __shared__ unsigned long long s_cand, s_key;
   __shared__ unsigned long long s_prof[32];  // PROF: [0,16) cycles per opcode, [16,32) counts
+  // graph descriptors are block-uniform and indexed dynamically (outputs):
+  // kept in shared memory, not in per-thread local memory
+  __shared__ TpoVmGraph s_g1, s_g2;
   if (PROF && threadIdx.x < 32) s_prof[threadIdx.x] = 0;
   const FieldConst &f = a.field;
   SmemT<WT> s = carve<WT>(smem, f, a.code_smem_bytes);
   load_tables(s, f, a.tables);
-  const TpoVmGraph g1 = a.graphs[a.program];
+  if (threadIdx.x == 0) s_g1 = a.graphs[a.program];
+  __syncthreads();
+  const TpoVmGraph &g1 = s_g1;
   // bytecode staged in shared memory: the program once per CTA, each
   // candidate's code when it changes (instructions are uniform across the
   // block; smem reads avoid a global round trip per VM instruction)
   TpoVmInstr *scode = reinterpret_cast<TpoVmInstr *>(smem + f.table_bytes);
   copy_code(scode, a.code + g1.code_off, g1.code_len);
   TpoVmInstr *ccode = scode + g1.code_len;
-  uint32_t staged = 0xffffffffu;
+  uint32_t staged = 0xffffffffu, desc = 0xffffffffu;  // graph whose code / descriptor is in smem
   for (;;) {
     __syncthreads();
     if (threadIdx.x == 0) s_cand = atomicAdd(a.counter, 1ull);
@@ -636,7 +652,12 @@ __global__ void __launch_bounds__(NT) verify_kernel(VerifyArgs a) {
     const uint64_t cand = a.first + k;
     const uint32_t gi = a.cand_graph ? a.cand_graph[k] : a.pool[cand % a.pool_n];
     const uint64_t seed = a.seeds ? a.seeds[k] : cand;
-    const TpoVmGraph g2 = a.graphs[gi];
+    if (gi != desc) {
+      if (threadIdx.x == 0) s_g2 = a.graphs[gi];
+      __syncthreads();
+      desc = gi;
+    }
+    const TpoVmGraph &g2 = s_g2;
     const bool silu = g1.has_silu || g2.has_silu;
     if (gi != staged && !g2.err) {
       copy_code(ccode, a.code + g2.code_off, g2.code_len);
@@ -763,13 +784,14 @@ __global__ void __launch_bounds__(kThreads) shared_attempt_kernel(VerifyArgs a, 
   const FieldConst &f = a.field;
   SmemT<WT> s = carve<WT>(smem, f, a.code_smem_bytes);
   load_tables(s, f, a.tables);
-  const TpoVmGraph g1 = a.graphs[a.program];
+  const TpoVmGraph *g1p = a.graphs + a.program;
+  const uint32_t code_len = g1p->code_len;
   TpoVmInstr *scode = reinterpret_cast<TpoVmInstr *>(smem + f.table_bytes);
-  copy_code(scode, a.code + g1.code_off, g1.code_len);
+  copy_code(scode, a.code + g1p->code_off, code_len);
   const uint32_t omega = gen_attempt(s, f, seed, 0, a.n_in, true, &s_slow, &s_omega);
   if (threadIdx.x == 0) s_flag = 0;
   __syncthreads();
-  const bool ok = run_program<false>(s, f, scode, g1.code_len, &s_flag, nullptr);
+  const bool ok = run_program<false>(s, f, scode, code_len, &s_flag, nullptr);
   for (uint32_t i = threadIdx.x; i < a.shared_len; i += blockDim.x) w_out[i] = s.w[i];
   for (uint32_t i = threadIdx.x; i < f.p; i += blockDim.x) tab_out[i] = s.silu_p[i];
   for (uint32_t i = threadIdx.x; i < f.q; i += blockDim.x) {
@@ -915,7 +937,7 @@ __global__ void __launch_bounds__(kThreads) eval_kernel(EvalArgs a) {
   const FieldConst &f = a.field;
   Smem s = carve(smem, f);
   load_tables(s, f, a.tables);
-  const TpoVmGraph g = a.graphs[0];
+  const TpoVmGraph &g = *a.graphs;  // read in place (dynamically indexed outputs)
   uint32_t omega;
   if (a.inputs) {
     for (uint32_t e = threadIdx.x; e < a.n_in; e += blockDim.x) s.w[e] = a.inputs[e];
@@ -973,15 +995,10 @@ int norm_threads(int n) { return n == 64 || n == 128 ? n : 256; }
 
 extern "C" int tpo_ff_launch_verify(const tpo_ff::VerifyArgs *a, int grid, size_t smem,
                                     cudaStream_t st, int nthreads, int narrow) {
-  static int configured_for[12] = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1};
   const bool prof = a->prof != nullptr;
   const int nt = norm_threads(nthreads);
   VerifyKern kern = pick_verify(prof, narrow != 0, nt);
-  const int slot = int(prof) * 6 + (nt == 64 ? 0 : nt == 128 ? 1 : 2) * 2 + (narrow ? 1 : 0);
-  if (int(smem) > configured_for[slot]) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    configured_for[slot] = int(smem);
-  }
+  tpo_ensure_smem(reinterpret_cast<const void *>(kern), smem);
   kern<<<grid, nt, smem, st>>>(*a);
   return int(cudaGetLastError());
 }
@@ -991,17 +1008,17 @@ extern "C" int tpo_ff_launch_shared(const tpo_ff::VerifyArgs *a, uint64_t seed, 
                                     cudaStream_t st) {
   using namespace tpo_ff;
   if (narrow) {
-    cudaFuncSetAttribute(shared_attempt_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    tpo_ensure_smem(reinterpret_cast<const void *>(shared_attempt_kernel<uint16_t>), smem);
     shared_attempt_kernel<uint16_t><<<1, kThreads, smem, st>>>(*a, seed, static_cast<uint16_t *>(w_out), tab_out, meta);
   } else {
-    cudaFuncSetAttribute(shared_attempt_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    tpo_ensure_smem(reinterpret_cast<const void *>(shared_attempt_kernel<uint32_t>), smem);
     shared_attempt_kernel<uint32_t><<<1, kThreads, smem, st>>>(*a, seed, static_cast<uint32_t *>(w_out), tab_out, meta);
   }
   return int(cudaGetLastError());
 }
 
 extern "C" int tpo_ff_launch_eval(const tpo_ff::EvalArgs *a, size_t smem, cudaStream_t st) {
-  cudaFuncSetAttribute(tpo_ff::eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  tpo_ensure_smem(reinterpret_cast<const void *>(tpo_ff::eval_kernel), smem);
   tpo_ff::eval_kernel<<<1, tpo_ff::kThreads, smem, st>>>(*a);
   return int(cudaGetLastError());
 }
@@ -1010,7 +1027,7 @@ extern "C" int tpo_ff_verify_occupancy(size_t smem, int nthreads, int narrow) {
   int blocks = 0;
   const int nt = norm_threads(nthreads);
   VerifyKern kern = pick_verify(false, narrow != 0, nt);
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  tpo_ensure_smem(reinterpret_cast<const void *>(kern), smem);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, nt, smem);
   return blocks;
 }

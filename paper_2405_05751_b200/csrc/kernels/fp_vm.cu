@@ -23,6 +23,7 @@
 #include <stdint.h>
 
 #include "fp_vm.cuh"
+#include "smem_limit.cuh"
 #include "vm.h"
 
 namespace tpo_fp {
@@ -464,7 +465,7 @@ extern "C" int tpo_fp_launch_stab_compare(const double *r, const double *o, uint
 
 extern "C" int tpo_fp_launch_eval(const tpo_fp::EvalArgs *a, int f32, size_t smem, cudaStream_t st) {
   auto kern = f32 ? tpo_fp::eval_kernel<float> : tpo_fp::eval_kernel<double>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  tpo_ensure_smem(reinterpret_cast<const void *>(kern), smem);
   kern<<<1, tpo_fp::kThreads, smem, st>>>(*a);
   return int(cudaGetLastError());
 }
@@ -510,14 +511,14 @@ extern "C" int tpo_fp_launch_instr(void *W, int f32, const TpoVmInstr *I, uint32
 
 extern "C" int tpo_fp_launch_stability(const tpo_fp::StabilityArgs *a, int grid, size_t smem,
                                        cudaStream_t st) {
-  cudaFuncSetAttribute(tpo_fp::stability_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  tpo_ensure_smem(reinterpret_cast<const void *>(tpo_fp::stability_kernel), smem);
   tpo_fp::stability_kernel<<<grid, tpo_fp::kThreads, smem, st>>>(*a);
   return int(cudaGetLastError());
 }
 
 extern "C" int tpo_fp_stability_occupancy(size_t smem) {
   int blocks = 0;
-  cudaFuncSetAttribute(tpo_fp::stability_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  tpo_ensure_smem(reinterpret_cast<const void *>(tpo_fp::stability_kernel), smem);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, tpo_fp::stability_kernel, tpo_fp::kThreads, smem);
   return blocks;
 }

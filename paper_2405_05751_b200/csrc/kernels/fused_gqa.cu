@@ -31,6 +31,7 @@
 
 #include "fused.cuh"
 #include "sm100.cuh"
+#include "smem_limit.cuh"
 
 namespace tpo_gqa {
 
@@ -343,12 +344,7 @@ template <int SLOTS, int S, int MINB, bool SPLIT>
 cudaError_t launch_t(const CUtensorMap *maps, const GqaParams &p, cudaStream_t st) {
   const size_t smem = gqa_smem<SLOTS, S, SPLIT>();
   auto kern = gqa_kernel<SLOTS, S, MINB, SPLIT>;
-  static size_t configured = 0;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e) return e;
-    configured = smem;
-  }
+  if (cudaError_t e = tpo_ensure_smem(reinterpret_cast<const void *>(kern), smem)) return e;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(p.groups * S);
   cfg.blockDim = dim3(kThreads);

@@ -38,6 +38,7 @@
 
 #include "fused.cuh"
 #include "sm100.cuh"
+#include "smem_limit.cuh"
 
 namespace tpo_fused {
 
@@ -636,12 +637,7 @@ cudaError_t launch_t(const CUtensorMap *maps, const SkinnyParams &p, cudaStream_
   if (p.ksplit != S) return cudaErrorInvalidValue;
   const size_t smem = skinny_smem<MODE, STAGES, S, SPLIT>(p);
   auto kern = skinny_kernel<MODE, STAGES, S, MINB, SPLIT>;
-  static size_t configured = 0;  // per instantiation: raise the smem limit once
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e) return e;
-    configured = smem;
-  }
+  if (cudaError_t e = tpo_ensure_smem(reinterpret_cast<const void *>(kern), smem)) return e;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((p.N / kTileN) * p.ksplit);
   cfg.blockDim = dim3(kThreads);

@@ -12,6 +12,12 @@ Partitioning is by cumulative estimated cost, not by count: per-candidate
 cost varies ~60x across families (``op_madds`` x expected attempts), and
 contiguous ranges keep each rank's pool slice and the seed rule
 ``candidate i -> seed i`` intact.
+
+Several candidate families (pools) verified in one step share ONE packed
+word space (:class:`WordLayout`: family f owns words [base_f, base_f +
+ceil(n_f / 32))), so a rank's share is one contiguous word range and the
+step ends with a single all-gather of one buffer (:func:`gather_words`),
+whatever the number of families.
 """
 from __future__ import annotations
 
@@ -88,3 +94,75 @@ def gather_accept(local_words, ranges: List[Tuple[int, int]], n_total: int, dist
         if n:
             res[first:first + n] = unpack_bits(outs[r].cpu().numpy(), n)
     return res
+
+
+class WordLayout:
+    """Packed accept words of several candidate families in one index space:
+    family f (n_f candidates) owns words [base[f], base[f] + words[f]); bit
+    k of family f lives in word base[f] + k // 32."""
+
+    def __init__(self, counts: Sequence[int]):
+        self.counts = [int(c) for c in counts]
+        self.words = [-(-c // 32) for c in self.counts]
+        self.base = [int(x) for x in np.concatenate([[0], np.cumsum(self.words)[:-1]])] if counts else []
+        self.total_words = int(sum(self.words))
+
+    def word_costs(self, per_candidate_cost: Sequence[float]) -> np.ndarray:
+        """Cost of every word from a per-family cost per candidate."""
+        wc = np.zeros(self.total_words)
+        for f, (c, n) in enumerate(zip(per_candidate_cost, self.counts)):
+            k = np.full(self.words[f], 32.0)
+            if n % 32:
+                k[-1] = n % 32
+            wc[self.base[f]: self.base[f] + self.words[f]] = k * float(c)
+        return wc
+
+    def rank_words(self, word_costs: Sequence[float], world: int) -> List[Tuple[int, int]]:
+        """Contiguous word ranges [(w0, nw)] per rank, balanced by cost."""
+        wc = np.asarray(word_costs, dtype=np.float64)
+        if world <= 1:
+            return [(0, self.total_words)]
+        cum = np.cumsum(wc)
+        total = cum[-1] if len(cum) else 0.0
+        cuts = [0]
+        for r in range(1, world):
+            w = int(np.searchsorted(cum, total * r / world, side="left")) + 1 if total > 0 else \
+                (self.total_words * r) // world
+            cuts.append(max(cuts[-1], min(w, self.total_words)))
+        cuts.append(self.total_words)
+        return [(cuts[r], cuts[r + 1] - cuts[r]) for r in range(world)]
+
+    def jobs(self, w0: int, nw: int) -> List[Tuple[int, int, int, int]]:
+        """The verify_pool calls of a rank owning words [w0, w0 + nw):
+        (family, first candidate, candidates, word offset in the local buffer)."""
+        out = []
+        for f in range(len(self.counts)):
+            a, b = max(w0, self.base[f]), min(w0 + nw, self.base[f] + self.words[f])
+            if a >= b:
+                continue
+            first = (a - self.base[f]) * 32
+            last = min((b - self.base[f]) * 32, self.counts[f])
+            out.append((f, first, last - first, a - w0))
+        return out
+
+    def unpack(self, words: np.ndarray) -> List[np.ndarray]:
+        """Global word vector -> per-family bool accept arrays."""
+        w = np.ascontiguousarray(words).view(np.uint32)
+        return [unpack_bits(w[self.base[f]: self.base[f] + self.words[f]], n)
+                for f, n in enumerate(self.counts)]
+
+
+def gather_words(local_words, ranges: List[Tuple[int, int]], dist=None):
+    """The step's single collective: all-gather every rank's word range
+    (1-D int32 tensor, padded to the longest range) and return the global
+    word vector on the device (no host traffic; unpack it afterwards)."""
+    import torch
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return local_words
+    world = dist.get_world_size()
+    wmax = max(max(nw for _, nw in ranges), 1)
+    buf = torch.zeros(wmax, dtype=torch.int32, device=local_words.device)
+    buf[: local_words.numel()] = local_words
+    outs = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(outs, buf)
+    return torch.cat([outs[r][:nw] for r, (_, nw) in enumerate(ranges)])

@@ -81,3 +81,57 @@ def test_gloo_gather_reassembles_reference_verdicts(world):
         assert p.exitcode == 0
     assert all(ok for _, ok, _ in res), res
     assert all(c == int(accept.sum()) for _, _, c in res)
+
+
+def _golden_families():
+    ar = np.load(os.path.join(HERE, "golden", "golden.npz"))
+    return [ar[f"verdicts_{f}"]["kind"] == 0 for f in ("rmsnorm", "gatedmlp", "gqa", "lora")]
+
+
+def test_word_layout_jobs_cover_every_candidate_once():
+    counts = [250, 7, 0, 1000, 33]
+    lay = shard.WordLayout(counts)
+    for world in (1, 2, 3, 4, 8):
+        ranges = lay.rank_words(lay.word_costs([1.0, 60.0, 5.0, 3.0, 9.0]), world)
+        assert sum(nw for _, nw in ranges) == lay.total_words
+        seen = [np.zeros(c, int) for c in counts]
+        for w0, nw in ranges:
+            for f, first, n, off in lay.jobs(w0, nw):
+                assert first % 32 == 0 and 0 <= off < nw
+                seen[f][first:first + n] += 1
+        assert all((s == 1).all() for s in seen)
+
+
+def _layout_worker(rank, world, port, fams, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    lay = shard.WordLayout([len(a) for a in fams])
+    costs = [4353.0 * 4, 66560.0, 70144.0, 99328.0]  # op_madds x ~attempts
+    ranges = lay.rank_words(lay.word_costs(costs), world)
+    w0, nw = ranges[rank]
+    local = torch.zeros(nw, dtype=torch.int32)
+    for f, first, n, off in lay.jobs(w0, nw):  # this rank's "verify_pool" outputs
+        words = shard.pack_bits(fams[f][first:first + n]).view(np.int32)
+        local[off: off + len(words)] = torch.from_numpy(words.copy())
+    got = lay.unpack(shard.gather_words(local, ranges, dist).numpy())
+    q.put((rank, all(np.array_equal(g, a) for g, a in zip(got, fams))))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_one_gather_for_all_families(world):
+    """All four families' accept bits in one word space, cost-balanced word
+    ranges per rank, ONE all-gather: the reassembled vectors equal the
+    reference verdicts (gloo, world 2-4)."""
+    fams = _golden_families()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_layout_worker, args=(r, world, port, fams, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok in res), res

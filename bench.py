@@ -635,6 +635,7 @@ def run_verify(dist, n_total, steps=1, warmup=3, pool_fams=("rmsnorm", "gatedmlp
     jobs = [(fam_jobs[fi][0], fam_jobs[fi][1], fam_jobs[fi][2], first, n) for fi, first, n, _ in jobs]
     n_done = per_fam * len(fam_jobs)
     stream = search_stream(ctx, dist, fams, pool_fams)
+    native = search_native(ctx, dist) if dist.world == 1 else None
     stab = stability_stage(ctx, dist, fams, pool_fams)
     # algorithmic work: field MACs = 2 fields x (op_madds(program)
     # + op_madds(candidate)) per attempt the reference consumes; per-candidate
@@ -689,7 +690,51 @@ def run_verify(dist, n_total, steps=1, warmup=3, pool_fams=("rmsnorm", "gatedmlp
             "families": list(pool_fams), "seed_rule": "candidate i = pool[i % |pool|], seed i",
             "timing": "CUDA events: verify kernels + ONE accept-word all-gather, max over ranks; "
                       "host unpack outside",
-            "search_stream": stream, "stability_filter": stab}
+            "search_stream": stream, "search": native, "stability_filter": stab}
+
+
+# Algorithm 1 configurations per family at the verification shapes (RMSNorm
+# at (4, 64, 64): its 9-op block graph is the deepest search)
+SEARCH_CFG = {
+    "gatedmlp": dict(grids=[1, 2, 4, 8, 16], loops=[1, 2, 4, 8, 16], max_kernel_ops=0),
+    "gqa": dict(grids=[1, 2, 4], loops=[1, 2, 4, 8, 16], max_kernel_ops=0),
+    "lora": dict(grids=[1, 2, 4, 8, 16], loops=[1, 2, 4, 8, 16], max_kernel_ops=1, max_block_ops=5),
+    "rmsnorm": dict(grids=[4, 8], loops=[4, 8], max_kernel_ops=0),
+}
+
+
+def search_native(ctx, dist):
+    """The search loop end to end (tpo_gpu_search): Algorithm 1 enumerates
+    µGraphs for each family's program (host C++, all cores), the candidates
+    become handles without the wire format, and one GPU batch verifies them
+    (VerifyConfig seed 0).  Wall clock; the enumeration / handle / verify
+    split shows where a search spends its time once verification is on the
+    GPU."""
+    from paper_2405_05751_b200 import fixtures as F
+    shapes = dict(F.VERIFY_SHAPES, rmsnorm=(4, 64, 64))
+    out, tot, eq, wall, en, co, ve = {}, 0, 0, 0.0, 0.0, 0.0, 0.0
+    for fam, cfg in SEARCH_CFG.items():
+        prog = F.family_program(fam, *shapes[fam])
+        w0 = time.perf_counter()
+        acc, st = ctx.search(prog, **cfg)
+        w = time.perf_counter() - w0
+        out[fam] = {"candidates": st["candidates"], "equivalent": st["equivalent"],
+                    "not_equivalent": st["not_equivalent"], "inconclusive": st["inconclusive"],
+                    "prefixes": st["prefixes"], "partitions": st["partitions"],
+                    "enumerate_s": round(st["enumerate_s"], 4), "handles_s": round(st["compile_s"], 4),
+                    "verify_s": round(st["verify_s"], 4), "wall_s": round(w, 4), "config": cfg}
+        tot += st["candidates"]
+        eq += st["equivalent"]
+        wall += w
+        en += st["enumerate_s"]
+        co += st["compile_s"]
+        ve += st["verify_s"]
+    return {"value": round(tot / wall, 1), "unit": "candidates/s", "candidates": tot, "equivalent": eq,
+            "verify_value": round(tot / max(ve, 1e-9), 1), "enumerate_share": round(en / wall, 3),
+            "handles_share": round(co / wall, 3), "verify_share": round(ve / wall, 3),
+            "host_threads": os.cpu_count(), "families": out,
+            "path": "tpo_gpu_search: enumerate_mugraphs (Algorithm 1, host C++) -> handles (no JSON) -> "
+                    "tpo_gpu_verify_batch; wall clock"}
 
 
 def stability_stage(ctx, dist, fams, pool_fams, per_fam_total=25000):

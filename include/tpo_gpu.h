@@ -312,6 +312,43 @@ int tpo_gpu_parse_check(const char *json_in, int32_t *fast_accepted, int32_t *sa
 int tpo_gpu_generate(const char *program_json, const char *config_json, char *json_out, int64_t cap,
                      int64_t *needed);
 
+/* Algorithm 1 (§4; the reference's absent
+ * generator.cpp): µGraphs generated op by op in canonical form — up to
+ * "max_kernel_ops" pre-defined kernel operators, then one graph-defined
+ * operator whose block graph is enumerated operator by operator over every
+ * grid / for-loop partition — pruned by abstract expressions (a prefix's
+ * expression must be a subexpression of the program's, Tables 2-3),
+ * shape and shared memory.  config_json (nullable): {"grids", "loops",
+ * "max_block_ops", "max_kernel_ops", "max_loop_labels", "concat_matmul",
+ * "max_candidates", "max_prefixes", "threads", "smem_bytes"}.  Output JSON:
+ * {"candidates": [graph, ...], "stats": {...}}; every candidate is valid and
+ * carries the program's abstract expression — equivalence is the verifier's. */
+int tpo_gpu_enumerate(const char *program_json, const char *config_json, char *json_out, int64_t cap,
+                      int64_t *needed);
+
+/* The abstract expression of a graph's first output (normal form text). */
+int tpo_gpu_abstract_expression(const char *graph_json, char *text_out, int64_t cap, int64_t *needed);
+
+typedef struct {
+  int64_t candidates, equivalent, not_equivalent, inconclusive, errors;
+  int64_t prefixes, partitions, pruned_expr;
+  int32_t budget_exhausted, pad;
+  double enumerate_s, compile_s, verify_s;  /* host enumeration, handle construction, GPU verification */
+} tpo_search_stats;
+
+/* The search loop end to end (SPEC.md:664-668 generate -> verify): the
+ * candidates of tpo_gpu_enumerate become graph handles directly (no wire
+ * format) and are verified in one batch against `program` with `cfg`
+ * (cfg->seed for every candidate: the loop's single VerifyConfig).
+ * accepted (nullable) receives up to `cap` handles of the Equivalent
+ * candidates (caller frees them); *n_accepted their count. */
+int tpo_gpu_search(tpo_gpu_ctx *ctx, const tpo_gpu_graph *program, const char *config_json,
+                   const tpo_verify_cfg *cfg, const tpo_field_params *fp, tpo_gpu_graph **accepted,
+                   int64_t cap, int64_t *n_accepted, tpo_search_stats *stats);
+
+/* A handle's graph in the wire format (serialize.hpp schema). */
+int tpo_gpu_graph_json(const tpo_gpu_graph *g, char *json_out, int64_t cap, int64_t *needed);
+
 /* Reference op_madds work of a graph (SURVEY §8d verifier work unit). */
 int64_t tpo_gpu_op_madds(const tpo_gpu_graph *g);
 

@@ -38,6 +38,14 @@ class GraphInfo(C.Structure):
                 ("output_elems", C.c_int64), ("vm_words", C.c_int64)]
 
 
+class SearchStats(C.Structure):
+    _fields_ = [("candidates", C.c_int64), ("equivalent", C.c_int64), ("not_equivalent", C.c_int64),
+                ("inconclusive", C.c_int64), ("errors", C.c_int64), ("prefixes", C.c_int64),
+                ("partitions", C.c_int64), ("pruned_expr", C.c_int64), ("budget_exhausted", C.c_int32),
+                ("pad", C.c_int32), ("enumerate_s", C.c_double), ("compile_s", C.c_double),
+                ("verify_s", C.c_double)]
+
+
 assert C.sizeof(Verdict) == 48
 
 _lib = None
@@ -84,6 +92,11 @@ def lib():
                                        C.POINTER(FieldParams), vp, vp]
     L.tpo_gpu_verify_pool.argtypes = [vp, vp, vp, i32, u64, u64, C.POINTER(VerifyCfg),
                                       C.POINTER(FieldParams), vp, vp, vp, vp]
+    L.tpo_gpu_enumerate.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, i64, C.POINTER(i64)]
+    L.tpo_gpu_abstract_expression.argtypes = [C.c_char_p, C.c_char_p, i64, C.POINTER(i64)]
+    L.tpo_gpu_search.argtypes = [vp, vp, C.c_char_p, C.POINTER(VerifyCfg), C.POINTER(FieldParams), vp, i64,
+                                 C.POINTER(i64), C.POINTER(SearchStats)]
+    L.tpo_gpu_graph_json.argtypes = [vp, C.c_char_p, i64, C.POINTER(i64)]
     L.tpo_gpu_op_madds.argtypes = [vp]
     L.tpo_gpu_op_madds.restype = i64
     _lib = L

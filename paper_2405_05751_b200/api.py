@@ -105,6 +105,39 @@ def generate(program, grids=None, loops=None, rewrite: bool = True, max_candidat
     return (res["candidates"], res["stats"]) if with_stats else res["candidates"]
 
 
+def enumerate_mugraphs(program, grids=(1, 2, 4, 8, 16), loops=(1, 2, 4, 8, 16), max_block_ops: int = 9,
+                       max_kernel_ops: int = 1, max_loop_labels: int = 2, concat_matmul: bool = True,
+                       max_candidates: int = 4096, max_prefixes: int = 4_000_000, threads: int = 0,
+                       with_stats: bool = False):
+    """Algorithm 1 (§4; ``tpo_gpu_enumerate``): µGraphs generated op
+    by op in canonical form — up to ``max_kernel_ops`` pre-defined kernel ops,
+    then one GraphDef whose block graph is enumerated operator by operator —
+    pruned by abstract expressions (subexpressions of the program's), shape
+    and shared memory.  Candidates carry the program's abstract expression;
+    equivalence is the verifier's job."""
+    cfg = {"grids": list(grids), "loops": list(loops), "max_block_ops": max_block_ops,
+           "max_kernel_ops": max_kernel_ops, "max_loop_labels": max_loop_labels,
+           "concat_matmul": concat_matmul, "max_candidates": max_candidates,
+           "max_prefixes": max_prefixes, "threads": threads}
+    cj = json.dumps(cfg).encode()
+    need = C.c_int64(0)
+    N.check(N.lib().tpo_gpu_enumerate(_js(program), cj, None, 0, C.byref(need)))
+    buf = C.create_string_buffer(int(need.value))
+    N.check(N.lib().tpo_gpu_enumerate(_js(program), cj, buf, need.value, C.byref(need)))
+    res = json.loads(buf.value.decode())
+    return (res["candidates"], res["stats"]) if with_stats else res["candidates"]
+
+
+def abstract_expression(g) -> str:
+    """The abstract expression (Table 2) of ``g``'s output in the
+    enumerator's normal form (``tpo_gpu_abstract_expression``)."""
+    need = C.c_int64(0)
+    N.check(N.lib().tpo_gpu_abstract_expression(_js(g), None, 0, C.byref(need)))
+    buf = C.create_string_buffer(int(need.value))
+    N.check(N.lib().tpo_gpu_abstract_expression(_js(g), buf, need.value, C.byref(need)))
+    return buf.value.decode()
+
+
 def describe(g, smem_bytes: int = 0) -> str:
     """SPEC describe: pseudo-kernel listing of ``g`` plus
     its B200 execution (``tpo_gpu_describe``)."""
@@ -141,7 +174,14 @@ class Graph:
 
     @property
     def spec(self) -> dict:
-        """The graph as a dict (parsed on first use when built from JSON text)."""
+        """The graph as a dict (parsed on first use when built from JSON text;
+        fetched from the handle for graphs the library built, e.g. search results)."""
+        if self._spec is None:
+            need = C.c_int64(0)
+            N.check(N.lib().tpo_gpu_graph_json(self.h, None, 0, C.byref(need)))
+            buf = C.create_string_buffer(int(need.value))
+            N.check(N.lib().tpo_gpu_graph_json(self.h, buf, need.value, C.byref(need)))
+            self._spec = buf.value.decode()
         if isinstance(self._spec, (str, bytes)):
             self._spec = json.loads(self._spec)
         return self._spec
@@ -387,6 +427,25 @@ class Context:
                                                  sd.ctypes.data if sd is not None else None, n,
                                                  trials, tol, seed, scale, ok.ctypes.data))
         return ok
+
+    # ---- search ---------------------------------------------------------------
+    def search(self, program, cap: int = 1 << 16, num_tests=1, seed=0, max_resamples=16, p=227, q=113,
+               wbase=4, **enum_cfg):
+        """The search loop (``tpo_gpu_search``): Algorithm 1's candidates
+        (``enumerate_mugraphs`` options as keywords) become handles without
+        the wire format and are verified in one GPU batch with one
+        VerifyConfig.  Returns (accepted Graphs, stats dict)."""
+        prog = self.compile(program)
+        cj = json.dumps(enum_cfg).encode()
+        arr = (C.c_void_p * max(cap, 1))()
+        na = C.c_int64(0)
+        st = N.SearchStats()
+        cfg = N.VerifyCfg(num_tests, max_resamples, seed, 1e-3)
+        fp = N.FieldParams(p, q, wbase)
+        N.check(N.lib().tpo_gpu_search(self.h, prog.h, cj, C.byref(cfg), C.byref(fp), arr, cap,
+                                       C.byref(na), C.byref(st)))
+        acc = [Graph._wrap(self, None, C.c_void_p(arr[i])) for i in range(min(na.value, cap))]
+        return acc, {k: getattr(st, k) for k, _ in N.SearchStats._fields_ if k != "pad"}
 
     # ---- finite field -------------------------------------------------------
     def ff_eval(self, g, seed: int, stream: int, with_silu: Optional[bool] = None, p=227, q=113,

@@ -12,6 +12,7 @@
 
 #include "../../../include/tpo_gpu.h"
 #include "runtime.hpp"
+#include "tpo/ir/enumerate.hpp"
 #include "tpo/ir/serialize.hpp"
 #include "tpo/ir/shape_infer.hpp"
 #include "tpo/ir/validate.hpp"
@@ -488,6 +489,18 @@ void tpo_gpu_close(tpo_gpu_ctx *ctx) {
 
 namespace {
 
+// the per-graph facts every entry point reads; `match`: also the fused
+// kernel match (a search candidate defers it until it is accepted)
+void finish_graph(Graph &G, bool match) {
+  G.lax = ir::mugraph_lax_check(G.g).lax;
+  G.madds = graph_madds(G.g);
+  G.in_elems = input_elems(G.g);
+  G.out_elems = 0;
+  for (ir::TensorId t : G.g.outputs) G.out_elems += G.g.tensor(t).shape.elem_count();
+  if (match) G.fused_plan();
+  G.vm_words = -2;  // computed on first tpo_gpu_graph_info (an fp lowering)
+}
+
 // parse + validate (B200 limits) + fused match + VM footprint; throws
 tpo_gpu_graph *compile_one(const char *json) {
   auto h = std::make_unique<tpo_gpu_graph>();
@@ -510,12 +523,7 @@ tpo_gpu_graph *compile_one(const char *json) {
                                                                            : ErrCode::ShapeMismatch;
     throw Error(c, "invalid µGraph: " + msg);
   }
-  G.lax = ir::mugraph_lax_check(G.g).lax;
-  G.madds = graph_madds(G.g);
-  G.in_elems = input_elems(G.g);
-  for (ir::TensorId t : G.g.outputs) G.out_elems += G.g.tensor(t).shape.elem_count();
-  G.plan = match_fused(G.g);
-  G.vm_words = -2;  // computed on first tpo_gpu_graph_info (an fp lowering)
+  finish_graph(G, false);  // the fused match runs on first use
   return h.release();
 }
 
@@ -552,7 +560,7 @@ int tpo_gpu_graph_info(const tpo_gpu_graph *h, tpo_graph_info *o) {
   const Graph &G = h->g;
   o->n_inputs = int32_t(G.g.inputs.size());
   o->n_outputs = int32_t(G.g.outputs.size());
-  o->fused_kind = G.plan.kind;
+  o->fused_kind = G.fused_plan().kind;
   o->lax = G.lax;
   o->madds = G.madds;
   o->input_elems = G.in_elems;
@@ -695,10 +703,10 @@ int run_fused(Ctx &C, const Graph &G, const void *const *in, const int32_t *dt, 
     if (C.fused_scratch.size() <= size_t(slot)) C.fused_scratch.resize(size_t(slot) + 1);
     return C.fused_scratch[size_t(slot)].get(bytes);
   };
-  return launch_fused(G.plan, io, st);
+  return launch_fused(G.fused_plan(), io, st);
 }
 
-bool use_fused(const Graph &G) { return G.plan.kind != 0 && G.precision != TPO_PREC_VM; }
+bool use_fused(const Graph &G) { return G.fused_plan().kind != 0 && G.precision != TPO_PREC_VM; }
 
 }  // namespace
 
@@ -1587,6 +1595,144 @@ extern "C" int tpo_gpu_parse_check(const char *json_in, int32_t *fast_accepted, 
 
 // ------------------------------------------------------------- generator
 #include "tpo/ir/generator.hpp"
+
+namespace {
+ir::EnumConfig enum_config(const char *config_json) {
+  nlohmann::json c;
+  try {
+    c = config_json && *config_json ? nlohmann::json::parse(config_json) : nlohmann::json::object();
+  } catch (const nlohmann::json::exception &e) {
+    throw Error(ErrCode::ParseError, e.what());
+  }
+  ir::EnumConfig cfg;
+  if (c.contains("grids")) cfg.grids = c.at("grids").get<std::vector<int64_t>>();
+  if (c.contains("loops")) cfg.loops = c.at("loops").get<std::vector<int64_t>>();
+  if (c.contains("max_block_ops")) cfg.max_block_ops = c.at("max_block_ops").get<int>();
+  if (c.contains("max_kernel_ops")) cfg.max_kernel_ops = c.at("max_kernel_ops").get<int>();
+  if (c.contains("max_loop_labels")) cfg.max_loop_labels = c.at("max_loop_labels").get<int>();
+  if (c.contains("concat_matmul")) cfg.concat_matmul = c.at("concat_matmul").get<bool>();
+  if (c.contains("max_candidates")) cfg.max_candidates = c.at("max_candidates").get<size_t>();
+  if (c.contains("max_prefixes")) cfg.max_prefixes = c.at("max_prefixes").get<uint64_t>();
+  if (c.contains("threads")) cfg.threads = c.at("threads").get<int>();
+  if (c.contains("smem_bytes")) cfg.limits.smem_bytes = c.at("smem_bytes").get<int64_t>();
+  return cfg;
+}
+
+nlohmann::json enum_stats_json(const ir::EnumStats &st) {
+  return {{"kernel_prefixes", st.kernel_prefixes}, {"partitions", st.partitions}, {"prefixes", st.prefixes},
+          {"pruned_expr", st.pruned_expr},         {"pruned_shape", st.pruned_shape},
+          {"pruned_memory", st.pruned_memory},     {"pruned_structure", st.pruned_structure},
+          {"completed", st.completed},             {"rejected_validate", st.rejected_validate},
+          {"duplicates", st.duplicates},           {"budget_exhausted", st.budget_exhausted}};
+}
+}  // namespace
+
+extern "C" int tpo_gpu_enumerate(const char *program_json, const char *config_json, char *json_out, int64_t cap,
+                                 int64_t *needed) {
+  return guard([&] {
+    nlohmann::json j;
+    try {
+      j = nlohmann::json::parse(program_json);
+    } catch (const nlohmann::json::exception &e) {
+      throw Error(ErrCode::ParseError, e.what());
+    }
+    ir::EnumStats st;
+    const auto cands = ir::enumerate_mugraphs(ir::kernel_graph_from_json(j), enum_config(config_json), &st);
+    nlohmann::json arr = nlohmann::json::array();
+    for (const auto &g : cands) arr.push_back(ir::to_json(g));
+    const std::string s = nlohmann::json{{"candidates", arr}, {"stats", enum_stats_json(st)}}.dump();
+    if (needed) *needed = int64_t(s.size()) + 1;
+    if (json_out && cap > int64_t(s.size())) std::memcpy(json_out, s.c_str(), s.size() + 1);
+    return 0;
+  });
+}
+
+extern "C" int tpo_gpu_search(tpo_gpu_ctx *ctx, const tpo_gpu_graph *program, const char *config_json,
+                              const tpo_verify_cfg *cfg, const tpo_field_params *fp, tpo_gpu_graph **accepted,
+                              int64_t cap, int64_t *n_accepted, tpo_search_stats *stats) {
+  return guard([&] {
+    if (!ctx || !program || !cfg || !fp) throw Error(ErrCode::ConfigError, "search: null argument");
+    using clk = std::chrono::steady_clock;
+    const auto t0 = clk::now();
+    ir::EnumStats est;
+    std::vector<ir::KernelGraph> cands = ir::enumerate_mugraphs(program->g.g, enum_config(config_json), &est);
+    const auto t1 = clk::now();
+    // candidates become handles directly: no wire format; enumerated graphs
+    // are valid by construction, the fused-kernel match waits for acceptance
+    const int64_t n = int64_t(cands.size());
+    std::vector<std::unique_ptr<tpo_gpu_graph>> hs(static_cast<size_t>(n));
+    parallel_for(n, n >= 64 ? host_threads() : 1, [&](int64_t i) {
+      auto h = std::make_unique<tpo_gpu_graph>();
+      h->g.g = std::move(cands[size_t(i)]);
+      finish_graph(h->g, false);
+      hs[size_t(i)] = std::move(h);
+    });
+    const auto t2 = clk::now();
+    std::vector<tpo_verdict> v(static_cast<size_t>(n));
+    std::vector<const tpo_gpu_graph *> hp(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) hp[size_t(i)] = hs[size_t(i)].get();
+    // the search loop's single VerifyConfig: cfg->seed for every candidate
+    if (n) {
+      const int rc = tpo_gpu_verify_batch(ctx, program, hp.data(), nullptr, uint64_t(n), cfg, fp, v.data(), nullptr);
+      if (rc) throw Error(ErrCode::Unsupported, std::string("search verify: ") + tpo_gpu_last_error());
+    }
+    const auto t3 = clk::now();
+    int64_t acc = 0, kinds[4] = {0, 0, 0, 0};
+    for (int64_t i = 0; i < n; ++i) {
+      const int k = v[size_t(i)].kind;
+      if (k >= 0 && k < 4) ++kinds[k];
+      if (k != 0) continue;
+      if (accepted && acc < cap) {
+        Graph &G = hs[size_t(i)]->g;
+        G.fused_plan();
+        accepted[acc] = hs[size_t(i)].release();
+      }
+      ++acc;
+    }
+    if (n_accepted) *n_accepted = acc;
+    if (stats) {
+      *stats = tpo_search_stats{};
+      stats->candidates = n;
+      stats->equivalent = kinds[0];
+      stats->not_equivalent = kinds[1];
+      stats->inconclusive = kinds[2];
+      stats->errors = kinds[3];
+      stats->prefixes = int64_t(est.prefixes);
+      stats->partitions = int64_t(est.partitions);
+      stats->pruned_expr = int64_t(est.pruned_expr);
+      stats->budget_exhausted = est.budget_exhausted;
+      stats->enumerate_s = std::chrono::duration<double>(t1 - t0).count();
+      stats->compile_s = std::chrono::duration<double>(t2 - t1).count();
+      stats->verify_s = std::chrono::duration<double>(t3 - t2).count();
+    }
+    return 0;
+  });
+}
+
+extern "C" int tpo_gpu_graph_json(const tpo_gpu_graph *h, char *json_out, int64_t cap, int64_t *needed) {
+  return guard([&] {
+    if (!h) throw Error(ErrCode::ConfigError, "null graph");
+    const std::string s = ir::to_json(h->g.g).dump();
+    if (needed) *needed = int64_t(s.size()) + 1;
+    if (json_out && cap > int64_t(s.size())) std::memcpy(json_out, s.c_str(), s.size() + 1);
+    return 0;
+  });
+}
+
+extern "C" int tpo_gpu_abstract_expression(const char *graph_json, char *out, int64_t cap, int64_t *needed) {
+  return guard([&] {
+    nlohmann::json j;
+    try {
+      j = nlohmann::json::parse(graph_json);
+    } catch (const nlohmann::json::exception &e) {
+      throw Error(ErrCode::ParseError, e.what());
+    }
+    const std::string s = ir::abstract_expression(ir::kernel_graph_from_json(j));
+    if (needed) *needed = int64_t(s.size()) + 1;
+    if (out && cap > int64_t(s.size())) std::memcpy(out, s.c_str(), s.size() + 1);
+    return 0;
+  });
+}
 
 extern "C" int tpo_gpu_generate(const char *program_json, const char *config_json, char *json_out,
                                 int64_t cap, int64_t *needed) {

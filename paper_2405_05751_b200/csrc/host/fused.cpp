@@ -135,7 +135,11 @@ std::string structural_key(const KernelGraph &g) {
     if (!m.empty()) return m;
     const Op &op = bg.ops[size_t(prod[size_t(t)])];
     std::string e = std::string(op_name(op.type)) + attr_key(op.attrs) + "(";
-    for (TensorId x : op.inputs) e += expr(x) + ",";
+    std::vector<std::string> args;
+    for (TensorId x : op.inputs) args.push_back(expr(x));
+    // commutative operators: operand order is not structure
+    if (op.type == OpType::EwAdd || op.type == OpType::EwMul) std::sort(args.begin(), args.end());
+    for (const std::string &a : args) e += a + ",";
     m = e + ")";
     return m;
   };

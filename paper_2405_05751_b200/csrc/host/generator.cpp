@@ -6,32 +6,17 @@
 #include <numeric>
 #include <set>
 
+#include "labels.hpp"
 #include "tpo/ir/shape_infer.hpp"
 
 namespace tpo::ir {
 
 namespace {
 
-bool supported(OpType t) {
-  switch (t) {
-    case OpType::Matmul:
-    case OpType::Sum:
-    case OpType::EwAdd:
-    case OpType::EwMul:
-    case OpType::EwDiv:
-    case OpType::EwExp:
-    case OpType::Sqr:
-    case OpType::Sqrt:
-    case OpType::SiLU:
-      return true;
-    default:
-      return false;
-  }
-}
-
-bool unary(OpType t) {
-  return t == OpType::EwExp || t == OpType::Sqr || t == OpType::Sqrt || t == OpType::SiLU;
-}
+using labels::Labels;
+using labels::label;
+using labels::supported;
+using labels::unary;
 
 // ------------------------------------------------------------ rewrite
 // Matmul(A ∘ s, W) -> Matmul(A, W) ∘ s for ∘ in {EwMul, EwDiv} when s
@@ -96,62 +81,6 @@ KernelGraph rewrite_rowscale(const KernelGraph &p, bool &changed) {
   std::vector<TensorId> outs;
   for (TensorId t : p.outputs) outs.push_back(map[size_t(t)]);
   return gb.finish(outs);
-}
-
-// ------------------------------------------------------------ labels
-struct Labels {
-  std::vector<int> off, parent;
-  std::set<int> contracted;  // roots of contracted labels
-  int find(int x) {
-    while (parent[size_t(x)] != x) x = parent[size_t(x)] = parent[size_t(parent[size_t(x)])];
-    return x;
-  }
-  void unite(int a, int b) { parent[size_t(find(a))] = find(b); }
-};
-
-// (tensor, dim) label roots; -1 for extent-1 dims.  Throws Unsupported.
-Labels label(const KernelGraph &p) {
-  Labels L;
-  int n = 0;
-  for (const TensorInfo &t : p.tensors) L.off.push_back(n), n += t.shape.rank();
-  L.parent.resize(size_t(n));
-  std::iota(L.parent.begin(), L.parent.end(), 0);
-  auto at = [&](TensorId t, int d) { return L.off[size_t(t)] + d; };
-  auto dim = [&](TensorId t, int d) { return p.tensor(t).shape.dims[size_t(d)]; };
-  std::vector<std::pair<TensorId, int>> contr;
-  for (const Op &op : p.ops) {
-    if (!supported(op.type)) throw Error(ErrCode::Unsupported, std::string("generator: op ") + op_name(op.type));
-    const TensorId o = op.outputs[0];
-    const int R = p.tensor(o).shape.rank();
-    if (unary(op.type)) {
-      for (int d = 0; d < R; ++d) L.unite(at(op.inputs[0], d), at(o, d));
-    } else if (op.type == OpType::Matmul) {
-      const TensorId a = op.inputs[0], b = op.inputs[1];
-      for (int d = 0; d + 2 < R; ++d) {
-        if (dim(a, d) > 1) L.unite(at(a, d), at(o, d));
-        if (dim(b, d) > 1) L.unite(at(b, d), at(o, d));
-      }
-      L.unite(at(a, R - 2), at(o, R - 2));
-      L.unite(at(b, R - 1), at(o, R - 1));
-      L.unite(at(a, R - 1), at(b, R - 2));
-      contr.emplace_back(a, R - 1);
-    } else if (op.type == OpType::Sum) {
-      const auto &sa = std::get<SumAttrs>(op.attrs);
-      const TensorId a = op.inputs[0];
-      if (sa.group != dim(a, sa.dim)) throw Error(ErrCode::Unsupported, "generator: partial-group Sum");
-      for (int d = 0; d < R; ++d)
-        if (d != sa.dim) L.unite(at(a, d), at(o, d));
-      contr.emplace_back(a, sa.dim);
-    } else {  // broadcast elementwise: right-aligned, equal extents > 1
-      for (TensorId t : op.inputs) {
-        const int r = p.tensor(t).shape.rank();
-        for (int k = 1; k <= r; ++k)
-          if (dim(t, r - k) > 1 && dim(t, r - k) == dim(o, R - k)) L.unite(at(t, r - k), at(o, R - k));
-      }
-    }
-  }
-  for (auto [t, d] : contr) L.contracted.insert(L.find(at(t, d)));
-  return L;
 }
 
 enum St { INV = 0, SLICE = 1, PARTIAL = 2, ACC = 3 };

@@ -58,7 +58,19 @@ struct Graph {
   int64_t madds = 0;
   int64_t in_elems = 0, out_elems = 0;
   mutable int64_t vm_words = -1;  // -2: not computed yet (tpo_gpu_graph_info)
-  FusedPlan plan;  // fused_kind == 0 when no hand-written kernel matches
+  // The fused-kernel match (fused_kind == 0 when no hand-written kernel
+  // matches), computed on first use: verification never needs it, so a
+  // search stream of candidates does not pay for it.
+  const FusedPlan &fused_plan() const {
+    std::call_once(plan_once, [this] {
+      const uint64_t st = plan.static_inputs;
+      plan = match_fused(g);
+      plan.static_inputs = st;
+    });
+    return plan;
+  }
+  mutable FusedPlan plan;
+  mutable std::once_flag plan_once;
   int precision = 0;  // TPO_PREC_* (tpo_gpu_graph_set_precision)
   // VM lowerings by (region base, 0/1 field pinned-outputs | 2 fp): a handle is
   // immutable, so batches over the same graphs reuse their bytecode

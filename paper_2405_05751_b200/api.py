@@ -46,6 +46,8 @@ def _dtype_code(x) -> int:
 
 
 def _js(g) -> bytes:
+    if isinstance(g, Graph):
+        g = g.spec
     return (g if isinstance(g, str) else json.dumps(g, separators=(",", ":"))).encode()
 
 

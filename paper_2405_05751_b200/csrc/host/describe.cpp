@@ -137,14 +137,16 @@ std::string describe(const KernelGraph &g, const MemLimits &lim) {
     o << "B200: no fused kernel (" << fp.why << ")";
     try {
       const VmProgram vp = lower_vm(g, 0, uint32_t(input_elems(g)), false, /*field=*/false);
-      int instrs = 0, phases = 0;
+      int instrs = 0, phases = 0, chained = 0;
       for (const TpoVmInstr &I : vp.code) {
         if (I.op == VM_LOOP || I.op == VM_ENDLOOP) continue;
         ++instrs;
         phases += !(I.flags & VM_NOSYNC);
+        chained += (I.pre_a != 0) + (I.pre_b != 0);
       }
       o << "; VM bytecode: " << instrs << " instructions in " << phases << " barrier phases, "
         << (input_elems(g) + vp.region_words) << " words";
+      if (chained) o << "; " << chained << " thread-graph unary(s) fused into their consumers (registers)";
     } catch (const Error &e) {
       o << "; VM: " << e.what();
     }

@@ -526,9 +526,12 @@ class Lowerer {
   // Pre-defined op at kernel level (G = {1,1,1}) or block level (block-
   // batched).  `inv[k]`: input k is block-invariant; the output is invariant
   // iff every input is (then it is computed once).  Returns q-definedness.
+  // `pre` (nullable): per input, a fused thread-graph unary (vm.h pre_a /
+  // pre_b) applied to it in registers.
   uint8_t compute(const Op &op, const std::vector<uint32_t> &in, const std::vector<TensorShape> &s,
                   const std::vector<uint8_t> &qd, const std::vector<uint8_t> &inv, uint32_t dst,
-                  const TensorShape &out, const std::array<int64_t, 3> &G) {
+                  const TensorShape &out, const std::array<int64_t, 3> &G,
+                  const std::vector<uint8_t> *pre = nullptr) {
     bool inv_out = true;
     for (uint8_t x : inv) inv_out = inv_out && x;
     const std::array<int64_t, 3> Go = inv_out ? std::array<int64_t, 3>{1, 1, 1} : G;
@@ -553,6 +556,10 @@ class Lowerer {
       v.wm.assign(v.dims.size(), 0);
       TpoVmInstr i = make(VM_BINARY, sub, v, dst, in[0], in[1]);
       i.b0n = uint32_t(numel(out));  // grid-block-major index space: block 0 first
+      if (pre) {
+        i.pre_a = (*pre)[0], i.pre_b = (*pre)[1];
+        if (i.pre_a == 1 + VM_SILU || i.pre_b == 1 + VM_SILU) p_.has_silu = true;
+      }
       i.qd = qd[0] & qd[1];
       i.flags |= (qd[0] ? VM_A_QD : 0) | (qd[1] ? VM_B_QD : 0);
       emit(i);
@@ -735,6 +742,47 @@ class Lowerer {
     std::vector<std::vector<const Op *>> cons(nt);
     for (const Op &b : bg.ops)
       for (TensorId t : b.inputs) cons[size_t(t)].push_back(&b);
+    // Thread-graph chains (the graph's ThreadGroups, or the
+    // fuser's rule — a single-consumer elementwise chain — when it has none):
+    // a Sqr / Sqrt / SiLU whose only consumer is an elementwise binary of the
+    // same group runs inside that binary's instruction (pre_a / pre_b), its
+    // result staying in registers: the chain's interior tensor gets no VM
+    // words and no instruction.  Graphs that raise (list order kept for the
+    // PoisonedExponent ordering) are not fused.
+    std::vector<uint8_t> pre_sub(nt, 0);
+    std::vector<TensorId> pre_src(nt, -1);
+    {
+      static const bool off = [] {
+        const char *e = std::getenv("TPO_VM_CHAINS");
+        return e && e[0] == '0';
+      }();
+      std::vector<int> group(bg.ops.size(), -1);
+      for (size_t gi = 0; gi < bg.thread_groups.size(); ++gi)
+        for (int id : bg.thread_groups[gi].op_ids)
+          if (id >= 0 && size_t(id) < group.size()) group[size_t(id)] = int(gi);
+      const bool explicit_groups = !bg.thread_groups.empty();
+      for (const Op &u : bg.ops) {
+        if (off || list_order_) break;
+        uint8_t sub;
+        switch (u.type) {
+          case OpType::Sqr: sub = VM_SQR; break;
+          case OpType::Sqrt: sub = VM_SQRT; break;
+          case OpType::SiLU: sub = VM_SILU; break;
+          default: continue;
+        }
+        const TensorId o = u.outputs[0];
+        if (cons[size_t(o)].size() != 1) continue;
+        const Op &b = *cons[size_t(o)][0];
+        if (b.type != OpType::EwAdd && b.type != OpType::EwMul && b.type != OpType::EwDiv) continue;
+        if (explicit_groups && (group[size_t(u.id)] < 0 || group[size_t(u.id)] != group[size_t(b.id)])) continue;
+        pre_sub[size_t(o)] = uint8_t(1 + sub);
+        pre_src[size_t(o)] = u.inputs[0];
+      }
+    }
+    auto chained = [&](const Op &b) {
+      return b.outputs.size() == 1 && pre_sub[size_t(b.outputs[0])] != 0;
+    };
+
     // A concat-Accum of an InIter tile along that tile's own fmap dim is the
     // untiled tile over the whole loop range (the concat is an address
     // offset): when only Matmuls consume it, it is a view of
@@ -777,7 +825,8 @@ class Lowerer {
       }
     for (const Op &b : bg.ops)
       for (TensorId t : b.outputs)
-        if (bbuf[size_t(t)] == UINT32_MAX) bbuf[size_t(t)] = alloc(copies(t) * numel(bshape(t)));
+        if (bbuf[size_t(t)] == UINT32_MAX && !pre_sub[size_t(t)])  // chain interiors: registers
+          bbuf[size_t(t)] = alloc(copies(t) * numel(bshape(t)));
 
     // ---- operand views and fused accumulation (thread-graph-free fusion of
     // the block graph's data movement into its matmuls):
@@ -905,15 +954,19 @@ class Lowerer {
     auto run_compute = [&](const Op &b) {
       std::vector<uint32_t> ins;
       std::vector<TensorShape> shapes;
-      std::vector<uint8_t> qds, invs;
+      std::vector<uint8_t> qds, invs, pres;
+      bool any_pre = false;
       for (TensorId t : b.inputs) {
-        ins.push_back(bget(t));
-        shapes.push_back(bshape(t));
-        qds.push_back(bqd[size_t(t)]);
-        invs.push_back(binv[size_t(t)]);
+        const TensorId src = pre_sub[size_t(t)] ? pre_src[size_t(t)] : t;  // chained unary: its input
+        ins.push_back(bget(src));
+        shapes.push_back(bshape(src));
+        qds.push_back(bqd[size_t(src)]);  // Sqr / Sqrt / SiLU keep q-definedness
+        invs.push_back(binv[size_t(src)]);
+        pres.push_back(pre_sub[size_t(t)]);
+        any_pre = any_pre || pre_sub[size_t(t)];
       }
       TensorId o = b.outputs.at(0);
-      bqd[size_t(o)] = compute(b, ins, shapes, qds, invs, bbuf[size_t(o)], bshape(o), G);
+      bqd[size_t(o)] = compute(b, ins, shapes, qds, invs, bbuf[size_t(o)], bshape(o), G, any_pre ? &pres : nullptr);
     };
 
     // Emission order: the depth schedule (SPEC schedule_ops, tpo/ir/schedule.hpp)
@@ -1046,7 +1099,7 @@ class Lowerer {
         bqd[size_t(acc)] = bqd[size_t(val)];
         continue;
       }
-      if (b.type == OpType::OutSaver || is_post(b)) continue;
+      if (b.type == OpType::OutSaver || is_post(b) || chained(b)) continue;
       if (matmul_fusable(b)) {
         emit_strided_matmul(b);
         continue;
@@ -1096,7 +1149,7 @@ class Lowerer {
         emit(i);
         continue;
       }
-      if (b.type == OpType::InIter || b.type == OpType::Accum || !is_post(b)) continue;
+      if (b.type == OpType::InIter || b.type == OpType::Accum || !is_post(b) || chained(b)) continue;
       if (matmul_fusable(b)) {
         emit_strided_matmul(b);
         continue;

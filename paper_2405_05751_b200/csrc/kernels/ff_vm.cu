@@ -259,13 +259,48 @@ __device__ __forceinline__ void copy_code(TpoVmInstr *dst, const TpoVmInstr *src
   __syncthreads();
 }
 
+// A fused thread-graph unary (TpoVmInstr::pre_a / pre_b) applied in
+// registers to one operand value (xp, xq); `qd`: the operand is
+// q-defined.  Returns true on a NonResidue event (sqrt).
+template <typename WT>
+__device__ __forceinline__ bool ff_pre(const SmemT<WT> &s, const FieldConst &f, uint8_t pre, bool qd,
+                                       uint32_t &xp, uint32_t &xq) {
+  constexpr uint32_t PM = Word<WT>::kMask;
+  bool ev = false;
+  switch (pre - 1) {
+    case VM_SQR:
+      xp = mod32(xp * xp, f.p, f.magic_p);
+      xq = qd ? mod32(xq * xq, f.q, f.magic_q) : 0u;
+      break;
+    case VM_SQRT: {
+      const int32_t r = s.sqrt_p[xp];
+      ev = r < 0;
+      xp = uint32_t(r) & PM;
+      if (qd) {
+        const int32_t r2 = s.sqrt_q[xq];
+        ev |= r2 < 0;
+        xq = uint32_t(r2) & PM;
+      } else {
+        xq = 0;
+      }
+      break;
+    }
+    default:  // VM_SILU
+      xp = s.silu_p[xp];
+      xq = qd ? uint32_t(s.silu_q[xq]) : 0u;
+  }
+  return ev;
+}
+
 // One VM instruction over items [start, n) with stride `step` (the CTA
 // interpreter passes threadIdx / blockDim, the global-memory executor its
-// grid-stride range); returns true when an undefined field op (zero divisor,
-// non-residue) requires a resample.
+// grid-stride range).  Returns the resample event of an undefined field op,
+// 0 if none: 1 DivByZero, 2 NonResidue, 6 NonResidue in a fused pre-op —
+// which precedes the instruction's own op in the reference's sequential
+// evaluation, so it outranks the binary's DivByZero.
 template <typename WT>
-__device__ __forceinline__ bool ff_exec(const SmemT<WT> &s, const FieldConst &f, const TpoVmInstr &I, uint32_t it,
-                                        uint32_t start, uint32_t step) {
+__device__ __forceinline__ uint32_t ff_exec(const SmemT<WT> &s, const FieldConst &f, const TpoVmInstr &I,
+                                            uint32_t it, uint32_t start, uint32_t step) {
   constexpr uint32_t QS = Word<WT>::kShift, PM = Word<WT>::kMask;
   WT *W = s.w;
   const uint32_t p = f.p, q = f.q, mp = f.magic_p, mq = f.magic_q;
@@ -273,7 +308,7 @@ __device__ __forceinline__ bool ff_exec(const SmemT<WT> &s, const FieldConst &f,
   const uint32_t n = I.n;
   const bool qd = I.qd;
   const bool flat = I.flags & VM_FLAT;
-  bool bad = false;
+  bool bad = false, bad_pre = false;
   switch (op) {
     case VM_ZERO:
       for (uint32_t i = start; i < n; i += step) W[I.dst + i] = 0;
@@ -333,6 +368,8 @@ __device__ __forceinline__ bool ff_exec(const SmemT<WT> &s, const FieldConst &f,
         if (!flat) offsets(I, i, od, oa, ob, wr);
         uint32_t va = W[I.a + oa], vb = W[I.b + ob];
         uint32_t ap = va & PM, aq = va >> QS, bp = vb & PM, bq = vb >> QS;
+        if (I.pre_a) bad_pre |= ff_pre(s, f, I.pre_a, I.flags & VM_A_QD, ap, aq) && i < lim;
+        if (I.pre_b) bad_pre |= ff_pre(s, f, I.pre_b, I.flags & VM_B_QD, bp, bq) && i < lim;
         uint32_t rp, rq = 0;
         switch (I.sub) {
           case VM_ADD:
@@ -520,7 +557,7 @@ __device__ __forceinline__ bool ff_exec(const SmemT<WT> &s, const FieldConst &f,
     default:
       break;
   }
-  return bad;
+  return bad_pre ? 6u : bad ? (op == VM_UNARY ? 2u : 1u) : 0u;
 }
 
 // PROF: thread 0 accumulates clock64 per VM opcode into prof[op] (TPO_VM_PROFILE).
@@ -551,12 +588,12 @@ __device__ bool run_program(const SmemT<WT> &s, const FieldConst &f, const TpoVm
       __syncthreads();
       return false;
     }
-    const bool bad = ff_exec(s, f, I, it, threadIdx.x, blockDim.x);
-    // NonResidue (sqrt) = 2 / DivByZero (div) = 1; within a barrier phase
-    // the earliest failing instruction wins (as in the reference's
-    // sequential evaluation, where it throws first)
-    if (bad) atomicMax(s_flag, int(((0xffffu - pc) << 2) | (op == VM_UNARY ? 2u : 1u)));
-    phase_bad |= bad;
+    const uint32_t bad = ff_exec(s, f, I, it, threadIdx.x, blockDim.x);
+    // NonResidue (sqrt) = 2 / DivByZero (div) = 1 (6: in a fused pre-op);
+    // within a barrier phase the earliest failing instruction wins (as in
+    // the reference's sequential evaluation, where it throws first)
+    if (bad) atomicMax(s_flag, int(((0xffffu - pc) << 3) | bad));
+    phase_bad |= bad != 0;
     if (I.flags & VM_NOSYNC) continue;
     // the decision is the barrier's own OR: reading *s_flag after a plain
     // barrier races with a faster warp's atomicMax in the next instruction
@@ -823,9 +860,9 @@ __device__ __forceinline__ SmemT<uint32_t> global_view(const GlobalFF &g) {
 
 __global__ void __launch_bounds__(256) ff_instr_kernel(GlobalFF g, TpoVmInstr I, uint32_t it, uint32_t pc) {
   const SmemT<uint32_t> s = global_view(g);
-  const bool bad = ff_exec(s, g.field, I, it, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+  const uint32_t bad = ff_exec(s, g.field, I, it, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
   if (__syncthreads_or(bad) && threadIdx.x == 0)
-    atomicMax(g.flag, int(((0xffffu - pc) << 2) | (I.op == VM_UNARY ? 2u : 1u)));
+    atomicMax(g.flag, int(((0xffffu - pc) << 3) | bad));
 }
 
 // Inputs of attempt (seed, stream): element e draws 2e+1, 2e+2 of the

@@ -89,7 +89,7 @@ struct GlobalFF {
   const uint16_t *tables;  // inv_p, inv_q, sqrt_p, sqrt_q (field state)
   uint16_t *attempt_tab;   // silu_p[p], silu_q[q], pow_w[q] of the current attempt
   uint32_t *W;             // 32-bit VM words: inputs, program, candidate regions
-  int *flag;               // resample flag ((0xffff - pc) << 2 | code), max
+  int *flag;               // resample flag ((0xffff - pc) << 3 | code), max
   uint32_t *meta;          // [1] omega, [2] rejection-zone replay needed
 };
 

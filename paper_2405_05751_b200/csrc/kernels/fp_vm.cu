@@ -122,7 +122,18 @@ __device__ __forceinline__ void exec_instr(T *W, const TpoVmInstr &I, uint32_t i
         int32_t od = int32_t(i), oa = int32_t(i), ob = int32_t(i);
         bool wr = true;
         if (!flat) offsets(I, i, od, oa, ob, wr);
-        const T a = W[I.a + oa], b = W[I.b + ob];
+        T a = W[I.a + oa], b = W[I.b + ob];
+        // fused thread-graph unaries (vm.h pre_a / pre_b): the same
+        // operation the standalone VM_UNARY performs, in registers
+        auto pre = [](uint8_t k, T x) -> T {
+          switch (k - 1) {
+            case VM_SQR: return O::mul(x, x);
+            case VM_SQRT: return O::sqrt_(x);
+            default: return O::div(x, O::add(T(1), O::exp_(-x)));  // SiLU (interp.hpp:36)
+          }
+        };
+        if (I.pre_a) a = pre(I.pre_a, a);
+        if (I.pre_b) b = pre(I.pre_b, b);
         W[I.dst + od] = I.sub == VM_ADD ? O::add(a, b) : I.sub == VM_MUL ? O::mul(a, b) : O::div(a, b);
       }
       break;

@@ -53,7 +53,11 @@ enum TpoVmFlags {
 
 struct TpoVmInstr {
   uint8_t op, sub, qd, flags;  // qd: result q-defined (static, FF mode)
-  uint8_t ndim, wmask, pad0, pad1;
+  // VM_BINARY: a thread-graph chain fused into the instruction — operand a
+  // (pre_a) / b (pre_b) first goes through the unary 1 + TpoVmSub (VM_SQR,
+  // VM_SQRT, VM_SILU) in registers: the intermediate tensor of the chain
+  // has no VM words (register-resident); 0 = none
+  uint8_t ndim, wmask, pre_a, pre_b;
   uint32_t n;                  // elements in the index space
   uint32_t dst, a, b;          // buffer base offsets (words)
   int32_t a_iter, d_iter;      // per-iteration offsets added to a / dst

@@ -20,7 +20,10 @@ CFG = {
     "lora": dict(grids=[2, 4], loops=[2, 4], max_kernel_ops=1, max_block_ops=4),
     "rmsnorm": dict(grids=[4], loops=[4], max_kernel_ops=0),
 }
-SHAPES = dict(F.VERIFY_SHAPES, rmsnorm=(4, 64, 64))
+# RMSNorm at 2 tokens: at SPEC's b=4 every attempt of the reference verifier
+# meets a non-residue sqrt in some row (p- and q-side residues, 1/4 per row),
+# so even program-vs-program is Inconclusive there (max_resamples 16)
+SHAPES = dict(F.VERIFY_SHAPES, rmsnorm=(2, 64, 64))
 VCOLS = ["kind", "rounds_run", "resamples", "has_witness", "w_round", "w_omega", "w_tensor", "w_index"]
 
 
@@ -49,9 +52,9 @@ def test_search_accepts_the_paper_mugraphs(ctx):
     """Fig. 2(b) and the paper's LoRA form come out of the search as
     accepted handles, and evaluate like the reference."""
     from test_enumerate import struct_key
-    prog = F.family_program("rmsnorm", 4, 64, 64)
+    prog = F.family_program("rmsnorm", *SHAPES["rmsnorm"])
     accepted, _ = ctx.search(prog, **CFG["rmsnorm"])
-    want = struct_key(F.rmsnorm_mugraph(4, 64, 64, 4, 4))
+    want = struct_key(F.rmsnorm_mugraph(*SHAPES["rmsnorm"], 4, 4))
     hit = [g for g in accepted if struct_key(g.spec) == want]
     assert hit
     prog_l = F.family_program("lora", *F.VERIFY_SHAPES["lora"])

@@ -613,6 +613,15 @@ def run_verify(dist, n_total, steps=1, warmup=3, pool_fams=("rmsnorm", "gatedmlp
     t_local = t_kernel / steps
     t_all = dist.max((t_kernel + t_gather) / steps)
     gather_share = dist.max(t_gather / steps) / t_all
+    # the collective alone: every rank's words ready (barrier + sync), then
+    # the same gather — the timed leg's gather also absorbs rank skew
+    dist.barrier()
+    torch.cuda.synchronize()
+    g0.record()
+    shard.gather_words(local[:nw], ranges, dist.pg)
+    g1.record()
+    torch.cuda.synchronize()
+    gather_pure_share = dist.max(g0.elapsed_time(g1) / 1e3) / t_all
     # host unpack, outside the timed leg
     host_words = words.cpu().numpy()
     accept = layout.unpack(host_words)
@@ -684,7 +693,8 @@ def run_verify(dist, n_total, steps=1, warmup=3, pool_fams=("rmsnorm", "gatedmlp
     return {"value": round(n_done / t_all, 1), "unit": "candidates/s", "candidates": n_done,
             "roofline": roof,
             "seconds": round(t_all, 4), "kernel_seconds_max_rank": round(dist.max(t_local), 4),
-            "gather_share": round(gather_share, 5), "ranges_words": ranges,
+            "gather_share": round(gather_share, 5), "gather_pure_share": round(gather_pure_share, 5),
+            "ranges_words": ranges,
             "accepted": accepted, "accept_sha16": accept_sha, "attempts_rank0": int(attempts), "e2e": e2e,
             "steps": steps, "gpu_launches_per_step": len(jobs),
             "families": list(pool_fams), "seed_rule": "candidate i = pool[i % |pool|], seed i",

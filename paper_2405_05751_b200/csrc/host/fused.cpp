@@ -613,6 +613,7 @@ int launch_fused(const FusedPlan &p, const FusedIO &io, cudaStream_t st) {
   } else if (p.kind == TPO_FUSED_LORA) {
     mode = MODE_LORA;
     sp.ksplit = pick_ksplit(p.n / 128, p.h, 1);
+    const int abox = tpo_skinny_lora_a_box_cols();  // A box [64 k][abox r]
     if (split) {  // W hi, W lo | X rows (hi 0-15, lo 16-31) | A hi, A lo | fp32 B
       const void *xs = cv.rows(0, 1, size_t(p.b), size_t(p.h), 16);
       auto w = cv.planes(1, ne[1]);
@@ -620,12 +621,12 @@ int launch_fused(const FusedPlan &p, const FusedIO &io, cudaStream_t st) {
       sp.lora_b_f32 = cv.f32(3, ne[3]);
       if (cv.err) return cv.err;
       ok = tmap_2d(&maps[0], w.first, p.h, p.n, 64, 64, SW) && tmap_2d(&maps[1], w.second, p.h, p.n, 64, 64, SW) &&
-           tmap_2d(&maps[2], xs, 32, p.h, 64, 32, SW) && tmap_2d(&maps[3], a.first, p.h, p.r, 16, 64, NOSW) &&
-           tmap_2d(&maps[6], a.second, p.h, p.r, 16, 64, NOSW);
+           tmap_2d(&maps[2], xs, 32, p.h, 64, 32, SW) && tmap_2d(&maps[3], a.first, p.h, p.r, abox, 64, NOSW) &&
+           tmap_2d(&maps[6], a.second, p.h, p.r, abox, 64, NOSW);
     } else {
       if (cv.err) return cv.err;
       ok = tmap_2d(&maps[0], in[1], p.h, p.n, 64, 64, SW) && tmap_2d(&maps[2], in[0], p.b, p.h, 64, 16, SW) &&
-           tmap_2d(&maps[3], in[2], p.h, p.r, 16, 64, NOSW);
+           tmap_2d(&maps[3], in[2], p.h, p.r, abox, 64, NOSW);
       maps[1] = maps[0];
       sp.x = static_cast<const __nv_bfloat16 *>(in[0]);
       sp.lora_a = static_cast<const __nv_bfloat16 *>(in[2]);

@@ -273,13 +273,17 @@ __device__ __forceinline__ bool ff_pre(const SmemT<WT> &s, const FieldConst &f, 
       xq = qd ? mod32(xq * xq, f.q, f.magic_q) : 0u;
       break;
     case VM_SQRT: {
+      // a non-residue (-1 in the table) raises the resample event; the value
+      // is consumed in registers by the same instruction (e.g. as a divisor
+      // indexing the inverse table), so it becomes 0, never an out-of-range
+      // table index — the attempt's results are discarded anyway
       const int32_t r = s.sqrt_p[xp];
       ev = r < 0;
-      xp = uint32_t(r) & PM;
+      xp = r < 0 ? 0u : uint32_t(r);
       if (qd) {
         const int32_t r2 = s.sqrt_q[xq];
         ev |= r2 < 0;
-        xq = uint32_t(r2) & PM;
+        xq = r2 < 0 ? 0u : uint32_t(r2);
       } else {
         xq = 0;
       }
@@ -302,7 +306,11 @@ template <typename WT>
 __device__ __forceinline__ uint32_t ff_exec(const SmemT<WT> &s, const FieldConst &f, const TpoVmInstr &I,
                                             uint32_t it, uint32_t start, uint32_t step) {
   constexpr uint32_t QS = Word<WT>::kShift, PM = Word<WT>::kMask;
+#ifdef TPO_VM_RESTRICT
+  WT *__restrict__ W = s.w;
+#else
   WT *W = s.w;
+#endif
   const uint32_t p = f.p, q = f.q, mp = f.magic_p, mq = f.magic_q;
   const uint8_t op = I.op;
   const uint32_t n = I.n;
@@ -343,11 +351,11 @@ __device__ __forceinline__ uint32_t ff_exec(const SmemT<WT> &s, const FieldConst
           case VM_SQRT: {
             int32_t r = s.sqrt_p[xp];
             bad |= r < 0 && i < lim;
-            rp = uint32_t(r) & PM;
+            rp = r < 0 ? 0u : uint32_t(r);  // non-residue: a valid word (the attempt is discarded)
             if (qd) {
               int32_t r2 = s.sqrt_q[xq];
               bad |= r2 < 0 && i < lim;
-              rq = uint32_t(r2) & PM;
+              rq = r2 < 0 ? 0u : uint32_t(r2);
             }
             break;
           }
@@ -520,6 +528,36 @@ __device__ __forceinline__ uint32_t ff_exec(const SmemT<WT> &s, const FieldConst
     case VM_SUM: {
       const uint32_t mid = I.dims[1], grp = I.dims[2], inner = I.dims[3];
       const uint32_t lazy = f.lazy_sum;
+      // Few long groups (e.g. RMSNorm's Σ over the hidden dim: one output
+      // per row): a warp per output, lanes striding the group (coalesced
+      // for inner == 1), per-lane raw sums reduced mod p/q and combined by
+      // shuffles — the field sum is order-independent, so the result is
+      // bit-identical to the sequential reduction.  `step` and `start` are
+      // warp-aligned in both executors (blockDim / grid stride).
+      if (n * 8 <= step && grp >= 64 && grp <= 32 * lazy) {
+        const uint32_t lane = start & 31u, nw = step >> 5;
+        for (uint32_t o = start >> 5; o < n; o += nw) {
+          const uint32_t t = fdiv(o, I.dmul[0], I.dsh[0]), in_i = o - t * inner;
+          const uint32_t ou = fdiv(t, I.dmul[1], I.dsh[1]), m = t - ou * mid;
+          const WT *pa = W + I.a + (ou * mid * grp + m * grp) * inner + in_i;
+          uint32_t sp = 0, sq = 0;
+#pragma unroll 4
+          for (uint32_t g = lane; g < grp; g += 32) {
+            const uint32_t v = pa[g * inner];
+            sp += v & PM;
+            sq += v >> QS;
+          }
+          sp = mod32(sp, p, mp);
+          sq = mod32(sq, q, mq);
+#pragma unroll
+          for (int off = 16; off; off >>= 1) {  // 32 residues < 2^16 each: no overflow
+            sp += __shfl_xor_sync(0xffffffffu, sp, off);
+            sq += __shfl_xor_sync(0xffffffffu, sq, off);
+          }
+          if (lane == 0) W[I.dst + o] = Word<WT>::pack(mod32(sp, p, mp), qd ? mod32(sq, q, mq) : 0u);
+        }
+        break;
+      }
       for (uint32_t o = start; o < n; o += step) {
         const uint32_t t = fdiv(o, I.dmul[0], I.dsh[0]), in_i = o - t * inner;
         const uint32_t ou = fdiv(t, I.dmul[1], I.dsh[1]), m = t - ou * mid;
@@ -646,17 +684,21 @@ __device__ bool first_mismatch(const SmemT<WT> &s, const TpoVmGraph &g1, const T
 
 // NT threads per candidate CTA: 256, or 128 when shared memory admits
 // twice as many resident candidates (more independent barrier domains).
-// A register cap instead of __launch_bounds__: with launch bounds alone
-// ptxas squeezed the 64/128-thread variants to 72 registers and spilled
-// (24-40 B stack frames); 80 fits every variant without local memory (78-79 used: six 128-thread CTAs per SM by registers).
+// __launch_bounds__(NT, B): B CTAs per SM — seven 128-thread CTAs (the
+// shared-memory limit of the pools' graphs), i.e. <= 72 registers; with
+// block-uniform state (graph descriptors, the verdict) in shared memory
+// every variant fits without local memory (71-78 registers, 0-byte stack
+// frames).  Without the explicit minimum ptxas' choice drifted between
+// builds (64-80 registers, 16-32 B stacks).  TPO_VM_REGCAP=N (experiments)
+// caps registers instead.
 #ifndef TPO_VM_REGCAP
-#define TPO_VM_REGCAP 80
+#define TPO_VM_REGCAP 0
 #endif
 template <bool PROF, int NT, typename WT>
 #if TPO_VM_REGCAP > 0
 __global__ void __maxnreg__(PROF ? 88 : TPO_VM_REGCAP) verify_kernel(VerifyArgs a) {
 #else
-__global__ void __launch_bounds__(NT) verify_kernel(VerifyArgs a) {  // experiment: ptxas' own choice
+__global__ void __launch_bounds__(NT, NT == 256 ? 3 : NT == 128 ? 7 : 14) verify_kernel(VerifyArgs a) {
 #endif
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int s_flag, s_slow;
@@ -666,6 +708,7 @@ __global__ void __launch_bounds__(NT) verify_kernel(VerifyArgs a) {  // experime
   // graph descriptors are block-uniform and indexed dynamically (outputs):
   // kept in shared memory, not in per-thread local memory
   __shared__ TpoVmGraph s_g1, s_g2;
+  __shared__ TpoVerdict s_v;
   if (PROF && threadIdx.x < 32) s_prof[threadIdx.x] = 0;
   const FieldConst &f = a.field;
   SmemT<WT> s = carve<WT>(smem, f, a.code_smem_bytes);
@@ -701,21 +744,18 @@ __global__ void __launch_bounds__(NT) verify_kernel(VerifyArgs a) {  // experime
       staged = gi;
     }
 
-    TpoVerdict v;
-    v.kind = 0;
-    v.rounds_run = 0;
-    v.resamples = 0;
-    v.has_witness = 0;
-    v.w_seed = 0;
-    v.w_round = 0;
-    v.w_omega = 0;
-    v.w_tensor = 0;
-    v.err_code = 0;
-    v.w_index = 0;
+    // the verdict is block-uniform: one copy in shared memory, written by
+    // thread 0 only (per-thread copies held ~12 registers across the whole
+    // attempt loop and pushed the 128-thread variants into local memory)
+    TpoVerdict &v = s_v;
+    const bool t0w = threadIdx.x == 0;
+    if (t0w) v = TpoVerdict{};
     bool finished = false;
     if (g1.err || g2.err) {
-      v.kind = 3;  // tpo::Error raised before sampling (shape mismatch, non-Lax, ...)
-      v.err_code = 1000 + int(g1.err ? g1.err : g2.err) - 1;
+      if (t0w) {
+        v.kind = 3;  // tpo::Error raised before sampling (shape mismatch, non-Lax, ...)
+        v.err_code = 1000 + int(g1.err ? g1.err : g2.err) - 1;
+      }
       finished = true;
     }
     for (int round = 0; round < a.num_tests && !finished; ++round) {
@@ -729,15 +769,17 @@ __global__ void __launch_bounds__(NT) verify_kernel(VerifyArgs a) {  // experime
           // the batch's common first attempt: inputs, tables and the
           // program's outputs were computed once (shared_attempt_kernel)
           if (a.shared_meta[0] == 2) {  // the program raises Error(PoisonedExponent)
-            v.kind = 3;
-            v.err_code = 1000 + kErrPoisonedExponent;
-            v.resamples = 0;
-            v.rounds_run = 0;
+            if (t0w) {
+              v.kind = 3;
+              v.err_code = 1000 + kErrPoisonedExponent;
+              v.resamples = 0;
+              v.rounds_run = 0;
+            }
             finished = true;
             break;
           }
           if (!a.shared_meta[0]) {  // the program itself needs a resample here
-            ++v.resamples;
+            if (t0w) ++v.resamples;
             continue;
           }
           const WT *sw = static_cast<const WT *>(a.shared_w);
@@ -760,15 +802,17 @@ __global__ void __launch_bounds__(NT) verify_kernel(VerifyArgs a) {  // experime
                run_program<PROF>(s, f, ccode, g2.code_len, &s_flag, s_prof);
         }
         if (!ok && (s_flag & 3) == 3) {  // Error(PoisonedExponent) escapes the verifier
-          v.kind = 3;
-          v.err_code = 1000 + kErrPoisonedExponent;
-          v.resamples = 0;
-          v.rounds_run = 0;
+          if (t0w) {
+            v.kind = 3;
+            v.err_code = 1000 + kErrPoisonedExponent;
+            v.resamples = 0;
+            v.rounds_run = 0;
+          }
           finished = true;
           break;
         }
         if (!ok) {
-          ++v.resamples;
+          if (t0w) ++v.resamples;
           continue;
         }
         int t;
@@ -777,29 +821,35 @@ __global__ void __launch_bounds__(NT) verify_kernel(VerifyArgs a) {  // experime
         const bool mism = first_mismatch(s, g1, g2, &s_key, &t, &idx);
         if (PROF && threadIdx.x == 0) s_prof[9] += (unsigned long long)(clock64() - t0), s_prof[25] += 1;
         if (mism) {
-          v.kind = 1;
-          v.has_witness = 1;
-          v.w_seed = seed;
-          v.w_round = round;
-          v.w_omega = omega;
-          v.w_tensor = t;
-          v.w_index = idx;
-          v.rounds_run = round + 1;
+          if (t0w) {
+            v.kind = 1;
+            v.has_witness = 1;
+            v.w_seed = seed;
+            v.w_round = round;
+            v.w_omega = omega;
+            v.w_tensor = t;
+            v.w_index = idx;
+            v.rounds_run = round + 1;
+          }
           finished = true;
         }
         round_done = true;
       }
       if (!round_done && !finished) {
-        v.kind = 2;
-        v.rounds_run = round;
+        if (t0w) {
+          v.kind = 2;
+          v.rounds_run = round;
+        }
         finished = true;
       }
     }
     if (!finished) {
-      v.kind = 0;
-      v.rounds_run = a.num_tests;
+      if (t0w) {
+        v.kind = 0;
+        v.rounds_run = a.num_tests;
+      }
     }
-    if (threadIdx.x == 0) {
+    if (t0w) {
       if (a.verdicts) a.verdicts[k] = v;
       if (a.accept && v.kind == 0) atomicOr(a.accept + (k >> 5), 1u << (k & 31));
       if (a.work) atomicAdd(a.work, (unsigned long long)(v.resamples + v.rounds_run));

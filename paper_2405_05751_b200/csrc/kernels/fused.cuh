@@ -41,6 +41,7 @@ struct GqaParams {
 // maps: {W plane 0, W plane 1, X, A / G, W plane 2, W plane 3, A lo plane}
 extern "C" int tpo_skinny_launch(int mode, int stages, int minb, int split, const CUtensorMap *maps,
                                  const SkinnyParams *p, cudaStream_t st);
+extern "C" int tpo_skinny_lora_a_box_cols();
 extern "C" size_t tpo_skinny_smem(int mode, int stages, int minb, int split, const SkinnyParams *p);
 extern "C" int tpo_gqa_launch(int slots, int minb, int split, const CUtensorMap *maps,
                               const GqaParams *p, cudaStream_t st);

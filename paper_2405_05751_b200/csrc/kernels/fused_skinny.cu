@@ -48,7 +48,6 @@ constexpr int kBK = 64;                   // K per pipeline stage (one 128-B swi
 constexpr int kTileN = 128;               // UMMA M (weight columns per tile)
 constexpr uint32_t kWBox = kBK * 128;     // bytes of one 64-col x kBK-row W box
 constexpr int kThreads = 192;
-constexpr int kMaxSplit = 4;
 
 // Pipeline stage layout (one k block of 64):
 //   [W boxes: NP planes x 2 x 8 KB] [B operand tile] [RMS: raw X, G | LoRA: A box(es)]
@@ -75,23 +74,42 @@ struct Cfg {
   static constexpr int kTokN = MODE == MODE_LORA && SPLIT ? 32 : 16;  // UMMA N
   static constexpr uint32_t kXTileB = kTokN * 128;        // B operand tile bytes
   static constexpr bool kTmaX = MODE != MODE_RMS;        // per-stage B tile via TMA
-  static constexpr uint32_t kAOff = 0;                   // W boxes lead the stage
-  static constexpr uint32_t kBOff = kAOff + NP * 2 * kWBox;
+  // LoRA XA: by default the epilogue warps' mma.sync from the ring stage
+  // (kXaRing).  TPO_LORA_XA_MMA (experiment, measured slower: 10.7 vs 8.35
+  // us per evaluation — the second M = 128 UMMA per k step doubles the
+  // MMA time in every stage's turnaround, profiles/r02/lora_xa.txt) puts
+  // XA on the tensor cores: the stage then leads with the X^T
+  // tile (the XA MMA's A operand: rows 16.. of its M = 128 fall on the W
+  // boxes that follow, garbage TMEM lanes never read), then the W boxes,
+  // then the A box(es) as two [64 k][8 r] boxes per plane (the XA MMA's
+  // B operand: MN-major, no swizzle)
+#ifdef TPO_LORA_XA_MMA
+  static constexpr bool kXaMma = MODE == MODE_LORA;
+#else
+  static constexpr bool kXaMma = false;
+#endif
+  static constexpr bool kXaRing = MODE == MODE_LORA && !kXaMma;
+  static constexpr int kNABox = SPLIT ? 2 : 1;             // LoRA A planes
+  static constexpr uint32_t kABox = 2048;                  // LoRA A per plane [64 k][16 r]
+  static constexpr uint32_t kAOff = kXaMma ? kXTileB : 0;  // W boxes
+  static constexpr uint32_t kBOff = kXaMma ? 0 : kAOff + NP * 2 * kWBox;  // B operand (X^T) tile
   static constexpr uint32_t kXRawBytes = SPLIT ? 2048 : 1024;  // RMS X box [8][64] (fp32 | bf16)
   static constexpr uint32_t kGBytes = SPLIT ? 256 : 128;       // RMS G box [64]
   static constexpr uint32_t kXRawOff = kBOff + kXTileB;    // RMS raw X
   static constexpr uint32_t kGOff = kXRawOff + kXRawBytes; // RMS G
-  static constexpr uint32_t kABox = 2048;                  // LoRA A box [64 k][16 r]
-  static constexpr int kNABox = SPLIT ? 2 : 1;             // LoRA A planes
-  static constexpr uint32_t kLAOff = kBOff + kXTileB;      // LoRA A box(es) in the stage
-  static constexpr uint32_t kStage = MODE == MODE_RMS    ? kGOff + 1024
-                                     : MODE == MODE_LORA ? kLAOff + kNABox * kABox
-                                                         : kBOff + kXTileB;
+  static constexpr uint32_t kLAOff = kXaMma ? kAOff + NP * 2 * kWBox : kBOff + kXTileB;  // LoRA A box(es)
+  static constexpr uint32_t kXaCol = kTokN;                // LoRA TMEM columns of XA^T (kXaMma)
+  // TMEM columns: GatedMLP two accumulators, LoRA (kXaMma) acc + XA^T
+  static constexpr uint32_t kTmemCols = kXaMma && kTokN == 32 ? 64 : 32;  // SPLIT LoRA: acc 0-31, XA 32-47
+  static constexpr uint32_t kStage = MODE == MODE_RMS               ? kGOff + 1024
+                                     : MODE == MODE_LORA              ? kLAOff + kNABox * kABox
+                                                                      : kBOff + kXTileB;
   static constexpr uint32_t kFullBytes = MODE == MODE_RMS ? NP * 2 * kWBox : kStage;
   static constexpr uint32_t kXGBytes = kXRawBytes + kGBytes;  // RMS: X box [8][64] + G box [64]
   static constexpr int kSide = MODE == MODE_RMS ? 8 : 0;  // RMS: Σx² per token, exchanged
   // stage releases: the UMMA commit, plus (LoRA) the four epilogue warps
-  static constexpr uint32_t kEmptyCount = MODE == MODE_LORA ? 5 : 1;
+  static constexpr uint32_t kEmptyCount = kXaRing ? 5 : 1;
+
   static_assert(kStage % 1024 == 0, "stages must keep the 1024-B swizzle alignment");
 };
 
@@ -144,14 +162,19 @@ __global__ void __launch_bounds__(kThreads, MINB)
   // its rank, minus one above the owner's own)
   float *side = red + (S > 1 ? (S - 1) * (kTileN / S) * 16 : 0);
   float *xa_tot = side + S * kSide;         // side: [S][kSide]; xa_tot: LoRA [16][16] (this CTA)
-  float *xa_w = xa_tot + (MODE == MODE_LORA ? 256 : 0);  // LoRA: per-warp XA partials [4][16][16]
-  Bars *bars = reinterpret_cast<Bars *>(xa_w + (MODE == MODE_LORA ? 1024 : 0));
+  float *xa_w = xa_tot + (MODE == MODE_LORA ? 256 : 0);  // LoRA XA-ring path: per-warp partials [4][16][16]
+  Bars *bars = reinterpret_cast<Bars *>(xa_w + (C::kXaRing ? 1024 : 0));
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   unsigned long long *dbg = p.dbg ? p.dbg + blockIdx.x * 16 : nullptr;
 #define TPO_T(slot) \
   if (dbg) dbg[slot] = globaltimer();
   if (threadIdx.x == 0) TPO_T(0);
+  if (dbg && threadIdx.x == 0) {  // ring slot 14: the SM this CTA runs on
+    uint32_t sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    dbg[14] = sm + 1;
+  }
   const uint32_t rank = S > 1 ? cluster_rank() : 0;
   const int n0 = (blockIdx.x / S) * kTileN;
   const int kbase = int(rank) * p.k_per_cta;
@@ -159,7 +182,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&bars->full[s], 1);
-      mbar_init(&bars->empty[s], C::kEmptyCount);
+      // experiment 16 (LoRA): stages released by the UMMA commit alone (no XA)
+      mbar_init(&bars->empty[s], (p.dbg_flags & 16) ? 1u : C::kEmptyCount);
       mbar_init(&bars->xg_full[s], 1);
       mbar_init(&bars->b_full[s], 4);
     }
@@ -176,7 +200,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
     if (MODE != MODE_GATED) tma_prefetch(&tmA);
     if (MODE == MODE_LORA && SPLIT) tma_prefetch(&tmA1);
   }
-  if (warp == 1) tmem_alloc<32>(&bars->tmem_base);
+  if (warp == 1) tmem_alloc<C::kTmemCols>(&bars->tmem_base);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -192,6 +216,21 @@ __global__ void __launch_bounds__(kThreads, MINB)
   // stream) may stream before the programmatic dependency resolves: the
   // producer issues the W (and LoRA A) boxes of the first pipeline stages,
   // then waits; X is read only after the wait.
+  // LoRA A box(es) of k block k0 into stage st: [64 k][16 r] per plane
+  // (XA-ring path) or two [64 k][8 r] boxes per plane (kXaMma: 16-byte rows,
+  // i.e. UMMA no-swizzle core matrices; r 0-7 at +0, r 8-15 at +1 KB)
+  auto lora_a = [&](uint8_t *st, uint64_t *bar, int k0) {
+#pragma unroll
+    for (int h = 0; h < C::kNABox; ++h) {
+      const CUtensorMap *m = h ? &tmA1 : &tmA;
+      if (C::kXaMma) {
+        tma_load_2d(st + C::kLAOff + h * C::kABox, m, bar, 0, k0);
+        tma_load_2d(st + C::kLAOff + h * C::kABox + 1024, m, bar, 8, k0);
+      } else {
+        tma_load_2d(st + C::kLAOff + h * C::kABox, m, bar, 0, k0);
+      }
+    }
+  };
   const int npre_max = (nkb < STAGES ? nkb : STAGES) - p.pre_cut;
   const int npre = p.prefetch_static ? (npre_max > 0 ? npre_max : 0) : 0;
   if (warp == 0 && elect_one()) {
@@ -205,10 +244,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         tma_load_2d(wt + 2 * w * kWBox, wmap[w], &bars->full[kb], n0, k0);
         tma_load_2d(wt + (2 * w + 1) * kWBox, wmap[w], &bars->full[kb], n0 + 64, k0);
       }
-      if (MODE == MODE_LORA) {  // A: static
-        tma_load_2d(st + C::kLAOff, &tmA, &bars->full[kb], 0, k0);
-        if (SPLIT) tma_load_2d(st + C::kLAOff + C::kABox, &tmA1, &bars->full[kb], 0, k0);
-      }
+      if (MODE == MODE_LORA) lora_a(st, &bars->full[kb], k0);  // A: static
     }
   }
   pdl_wait();  // inputs may be produced by the preceding kernel
@@ -274,10 +310,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
           tma_load_2d(wt + (2 * w + 1) * kWBox, wmap[w], &bars->full[s], n0 + 64, k0);
         }
         if (C::kTmaX) tma_load_2d(st + C::kBOff, &tmX, &bars->full[s], k0, 0);
-        if (MODE == MODE_LORA) {
-          tma_load_2d(st + C::kLAOff, &tmA, &bars->full[s], 0, k0);
-          if (SPLIT) tma_load_2d(st + C::kLAOff + C::kABox, &tmA1, &bars->full[s], 0, k0);
-        }
+        if (MODE == MODE_LORA) lora_a(st, &bars->full[s], k0);
         // experiment (TPO_TRIG_EARLY = D): release the dependent grid D
         // k blocks before the last issue (one thread triggers the CTA)
         if (p.trig_early > 0 && kb == nkb - 1 - p.trig_early) pdl_launch();
@@ -289,6 +322,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
   } else if (warp == 1) {
     // -------------------------------------------------------- MMA issuer
     constexpr uint32_t idesc = idesc_bf16(kTileN, C::kTokN, /*a MN-major*/ true, /*b K-major*/ false);
+    // LoRA XA: M = 128 (tokens, padded), N = 16 (r); a K-major, b MN-major
+    constexpr uint32_t xa_idesc = idesc_bf16(128, 16, false, true);
     for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % STAGES;
       mbar_wait(&bars->full[s], (kb / STAGES) & 1);
@@ -317,6 +352,19 @@ __global__ void __launch_bounds__(kThreads, MINB)
             const int acc = SPLIT ? w / 2 : w;
             const uint64_t adesc = sdesc_sw128(smem_u32(wt + w * 2 * kWBox) + kk * 16 * 128, kWBox, 1024);
             umma_bf16(tmem + acc * C::kTokN, adesc, bdesc, idesc, (kb | kk) != 0 || (SPLIT && (w & 1)));
+          }
+          if (C::kXaMma) {
+            // XA[t, r] += X[t, k] A[k, r]: A operand = the X^T tile as an
+            // M = 128 K-major operand (rows t >= 16 (SPLIT 32) read the W
+            // boxes behind it: garbage TMEM lanes, never read); B operand =
+            // the A box, N = 16, MN-major without swizzle (core matrix = 8 k
+            // rows x 16 B of r: LBO 128 B along k, SBO 1 KB along r)
+#pragma unroll
+            for (int h = 0; h < C::kNABox; ++h) {
+              const uint64_t adx = sdesc_sw128(xs + kk * 32, 16, 1024);
+              const uint64_t bda = sdesc_none(smem_u32(st + C::kLAOff + h * C::kABox) + kk * 256, 128, 1024);
+              umma_bf16(tmem + C::kXaCol, adx, bda, xa_idesc, (kb | kk | h) != 0);
+            }
           }
         }
         umma_commit(&bars->empty[s]);
@@ -397,7 +445,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
 #pragma unroll
       for (int o = 8; o; o >>= 1) sumsq += __shfl_xor_sync(0xffffffffu, sumsq, o);
     }
-    if (MODE == MODE_LORA) {
+    if (MODE == MODE_LORA && C::kXaRing) {
       // XA_s = X·A over this CTA's K range (16 tokens x 16 ranks) on the
       // warp MMA path of the otherwise idle epilogue warps, stage by stage
       // from the ring's X^T tile (K-major, 128-B swizzle) and A box
@@ -412,7 +460,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
       const int kch = 2 * q + (mi >> 1);
       const uint32_t a_off = (tok >> 3) * 1024 + (tok & 7) * 128 + ((kch ^ (tok & 7)) << 4);
       const uint32_t b_off = (16 * q + ri + 8 * (mi & 1)) * 32 + (mi >> 1) * 16;
-      for (int kb = 0; kb < nkb; ++kb) {
+      for (int kb = 0; kb < ((p.dbg_flags & 16) ? 0 : nkb); ++kb) {  // experiment 16: no XA
         const int s = kb % STAGES;
         mbar_wait(&bars->full[s], (kb / STAGES) & 1);
         const uint32_t st = smem_u32(stages + s * C::kStage);
@@ -502,7 +550,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         post[tk] = 1.0f / sqrtf(ss * dsc);
       }
     }
-    if (MODE == MODE_LORA) {
+    if (MODE == MODE_LORA && C::kXaRing) {
       // (XA_s·B̄)[t, n] for this thread's row n, every token t
 #pragma unroll
       for (int tk = 0; tk < 16; ++tk) {
@@ -523,7 +571,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
     // ---- critical path: last MMA -> TMEM -> DSMEM -> owner -> HBM
     // pin the post-loop operands here: without this the compiler may sink
     // their computation past the waits below, onto the critical path
-    if ((MODE == MODE_RMS && (mine || atomic_epi)) || MODE == MODE_LORA) {
+    if ((MODE == MODE_RMS && (mine || atomic_epi)) || C::kXaRing) {
 #pragma unroll
       for (int tk = 0; tk < T; ++tk) asm volatile("" : "+f"(post[tk]));
     }
@@ -531,6 +579,40 @@ __global__ void __launch_bounds__(kThreads, MINB)
     if (threadIdx.x == 64) TPO_T(5);
     __syncwarp();  // tcgen05.ld is .sync.aligned: the warp must be converged
     tc_fence_after();
+    if (C::kXaMma) {
+      // XA_s sits in TMEM lanes 0-15 (tokens; SPLIT: lo tokens in lanes
+      // 16-31), columns kXaCol.. (r): the lane-quarter-0 warp stages it as
+      // xa_tot[t][r], then every thread forms (XA_s·B̄)[t, n] for its row
+      if (q == 0) {
+        float xv[16];
+        tmem_ld16(tmem + C::kXaCol, xv);
+        if (SPLIT) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) xv[i] += __shfl_down_sync(0xffffffffu, xv[i], 16);
+        }
+        if (lane < 16) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            *reinterpret_cast<float4 *>(xa_tot + lane * 16 + 4 * i) =
+                make_float4(xv[4 * i], xv[4 * i + 1], xv[4 * i + 2], xv[4 * i + 3]);
+        }
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+#pragma unroll
+      for (int tk = 0; tk < 16; ++tk) {
+        const float4 *xr = reinterpret_cast<const float4 *>(xa_tot + tk * 16);
+        float o = 0.f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float4 x = xr[i];
+          o = fmaf(x.x, bcol[4 * i], o);
+          o = fmaf(x.y, bcol[4 * i + 1], o);
+          o = fmaf(x.z, bcol[4 * i + 2], o);
+          o = fmaf(x.w, bcol[4 * i + 3], o);
+        }
+        post[tk] = o;
+      }
+    }
     float acc[16];
     {
       float v[16];
@@ -615,7 +697,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
   if (threadIdx.x == 0) TPO_T(12);
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<32>(tmem);
+    tmem_dealloc<C::kTmemCols>(tmem);
   }
   if (threadIdx.x == 0) TPO_T(7);
 #undef TPO_T
@@ -628,7 +710,7 @@ size_t skinny_smem(const SkinnyParams &p) {
   (void)nkb;
   size_t b = size_t(STAGES) * C::kStage +
              (S > 1 ? size_t(S - 1) * (kTileN / S) * 16 * 4 : 0) + size_t(S) * C::kSide * 4 +
-             (MODE == MODE_LORA ? (256 + 1024) * 4 : 0) + sizeof(Bars);
+             (MODE == MODE_LORA ? (C::kXaRing ? 256 + 1024 : 256) * 4 : 0) + sizeof(Bars);
   return b + 1024;
 }
 
@@ -671,7 +753,9 @@ using namespace tpo_fused;
   X(MODE_LORA, 8, 2, 1, false) X(MODE_LORA, 6, 1, 1, false)                                           \
   X(MODE_GATED, 3, 1, 1, true) X(MODE_GATED, 3, 2, 1, true) X(MODE_RMS, 5, 1, 1, true)                \
   X(MODE_RMS, 5, 2, 1, true) X(MODE_RMS, 5, 4, 1, true) X(MODE_LORA, 5, 1, 1, true)                   \
-  X(MODE_LORA, 5, 2, 1, true) X(MODE_LORA, 5, 4, 1, true)
+  X(MODE_LORA, 5, 2, 1, true) X(MODE_LORA, 5, 4, 1, true)                                           \
+  X(MODE_RMS, 5, 8, 2, false) X(MODE_RMS, 4, 8, 2, false) X(MODE_RMS, 3, 8, 3, false)                 \
+  X(MODE_LORA, 5, 8, 2, false) X(MODE_LORA, 4, 8, 2, false)
 
 extern "C" int tpo_skinny_launch(int mode, int stages, int minb, int split, const CUtensorMap *maps,
                                  const SkinnyParams *p, cudaStream_t st) {
@@ -693,3 +777,7 @@ extern "C" size_t tpo_skinny_smem(int mode, int stages, int minb, int split, con
 #undef TPO_CASE
   return 0;
 }
+
+// Columns of one LoRA A box (the host's tensor-map box width): 8 for the
+// tensor-core XA path (two boxes per plane), 16 for the XA-ring path.
+extern "C" int tpo_skinny_lora_a_box_cols() { return Cfg<MODE_LORA, false>::kXaMma ? 8 : 16; }

@@ -161,6 +161,18 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t smem_addr, uint32_t lbo
   return d;
 }
 
+// UMMA shared-memory descriptor, no swizzle (core matrices of 8 rows x 16 B):
+// lbo / sbo as for the swizzled forms (MN-major: lbo along MN, sbo along K).
+__device__ __forceinline__ uint64_t sdesc_none(uint32_t smem_addr, uint32_t lbo_bytes,
+                                               uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= uint64_t((smem_addr >> 4) & 0x3FFFu);
+  d |= uint64_t((lbo_bytes >> 4) & 0x3FFFu) << 16;
+  d |= uint64_t((sbo_bytes >> 4) & 0x3FFFu) << 32;
+  d |= uint64_t(1) << 46;  // version (sm100); layout type 0 = SWIZZLE_NONE
+  return d;
+}
+
 // Instruction descriptor, kind::f16: bf16 x bf16 -> fp32, A/B major, M x N.
 __host__ __device__ constexpr uint32_t idesc_bf16(uint32_t M, uint32_t N, bool a_mn_major,
                                                   bool b_mn_major) {

@@ -123,6 +123,44 @@ def main():
         sk["first_full_spread"].append((ff.max() - ff.min()) / 1e3)
     if sk["grid_spread"]:
         print("  skew " + "  ".join(f"{k} {np.mean(v):.2f}" for k, v in sk.items()))
+    # placement: CTAs of the same launch sharing an SM (slot 14 = smid + 1)
+    # and whether they are the stragglers of the last MMA
+    pl = {"ctas_doubled": [], "lm_doubled": [], "lm_single": []}
+    for i in range(3, K):
+        b = order[i]
+        n = int((h[b, :, 0] > 0).sum())
+        sm = h[b, :n, 14]
+        if (sm <= 0).any():
+            continue
+        lm = h[b, :n, 3].astype(np.float64) / 1e3
+        if (lm <= 0).any():
+            continue
+        cnt = np.bincount(sm.astype(np.int64))
+        dbl = cnt[sm] > 1
+        pl["ctas_doubled"].append(int(dbl.sum()))
+        rel = lm - lm.min()
+        if dbl.any():
+            pl["lm_doubled"].append(rel[dbl].mean())
+        if (~dbl).any():
+            pl["lm_single"].append(rel[~dbl].mean())
+    if pl["ctas_doubled"]:
+        print("  placement " + "  ".join(f"{k} {np.mean(v):.2f}" for k, v in pl.items() if v))
+    # tail sub-phases per CTA, relative to the CTA's own last MMA (median over
+    # CTAs and launches): MMA completion, DSMEM send / receive, owner store,
+    # teardown
+    sub = {5: "tmem_full", 4: "sent", 6: "recv_done", 11: "owner_done", 2: "epi_done", 13: "pre_sync",
+           12: "synced", 7: "end"}
+    acc = {k: [] for k in sub}
+    for i in range(3, K):
+        b = order[i]
+        n = int((h[b, :, 0] > 0).sum())
+        lm = h[b, :n, 3]
+        for k in sub:
+            v = h[b, :n, k]
+            ok = (v > 0) & (lm > 0)
+            if ok.any():
+                acc[k].append(np.median((v[ok] - lm[ok]) / 1e3))
+    print("  tail(per CTA, from its last MMA) " + "  ".join(f"{sub[k]} {np.mean(v):.2f}" for k, v in acc.items() if v))
     per = np.diff(np.array(ends[2:], dtype=np.float64)) / 1e3
     print(f"  period (end to end) mean {per.mean():.2f} us  min {per.min():.2f}  max {per.max():.2f}")
 

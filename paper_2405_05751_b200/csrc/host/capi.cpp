@@ -282,6 +282,8 @@ void run_verify(Ctx &C, const Batch &bt, const tpo_verify_cfg &cfg, const tpo_fi
   tpo_ff::VerifyArgs a{};
   a.field = fs.fc;
   a.tables = static_cast<const uint16_t *>(fs.dev.ptr);
+  static const bool eager = std::getenv("TPO_VM_EAGER") != nullptr;  // A/B: no lazy input sampling
+  a.eager_inputs = eager ? 1 : 0;
   auto *dcode = static_cast<TpoVmInstr *>(C.code.get(bt.code.size() * sizeof(TpoVmInstr) + 1));
   auto *dgraphs = static_cast<TpoVmGraph *>(C.graphs.get(bt.graphs.size() * sizeof(TpoVmGraph)));
   check_cuda(cudaMemcpyAsync(dcode, bt.code.data(), bt.code.size() * sizeof(TpoVmInstr),

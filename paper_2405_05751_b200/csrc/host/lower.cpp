@@ -269,10 +269,14 @@ class Lowerer {
     kbuf_.assign(g.tensors.size(), UINT32_MAX);
     kqd_.assign(g.tensors.size(), 1);
     uint32_t off = in_base;
+    lazy_ok_ = in_base == 0 && g.inputs.size() <= TPO_VM_MAX_GEN;
     for (TensorId t : g.inputs) {
       if (kbuf_[size_t(t)] == UINT32_MAX) {
         kbuf_[size_t(t)] = off;
+        in_ranges_.push_back({off, uint32_t(numel(g.tensor(t).shape))});
         off += uint32_t(numel(g.tensor(t).shape));
+      } else {
+        lazy_ok_ = false;  // a repeated input: words and draw order differ
       }
       p_.in_shapes.push_back(g.tensor(t).shape);
     }
@@ -313,6 +317,7 @@ class Lowerer {
       if (raise_at_ < 0 || int64_t(k) > raise_at_ || gd_of_[k] != raise_gd_) p_.code[k].b0n = 0;
     plan_memory();
     mark_phases(p_.code);
+    if (field_ && lazy_ok_) lazy_inputs();
     p_.desc.words = p_.region_words;
     p_.desc.code_len = uint32_t(p_.code.size());
     p_.desc.poisoned = p_.poisoned;
@@ -336,6 +341,8 @@ class Lowerer {
   std::vector<int64_t> vsize_;                    // words per virtual buffer
   std::vector<uint32_t> kbuf_;
   std::vector<uint8_t> kqd_;
+  std::vector<std::pair<uint32_t, uint32_t>> in_ranges_;  // input words (offset, count), input order
+  bool lazy_ok_ = false;
   VmProgram p_;
 
   // Buffers are virtual until plan_memory() assigns addresses.
@@ -456,6 +463,86 @@ class Lowerer {
     for (uint32_t i = 0; i < p_.desc.n_out; ++i) fix(p_.desc.out_off[i]);
     p_.pinned_words = uint32_t(pinned);
     p_.region_words = uint32_t(std::max(peak, base) - region_);
+  }
+
+  // Lazy input sampling (FF verifier): per input, the first instruction
+  // whose read hull (instr_access, over every loop iteration) touches its
+  // words; opaque instructions count as reading everything.  The draws of
+  // an input are independent of when they are made (closed-form stream),
+  // so drawing it right before its first reader gives the reference's
+  // values; an attempt that resamples earlier never draws it.  Inputs whose
+  // first readers are not separated by an instruction that can resample
+  // (sqrt, division, a fused sqrt, VM_RAISE) are drawn together at the
+  // earlier point, contiguous ranges merged; when that leaves one group the
+  // graph draws everything up front (n_gen = 0: no barrier overhead).
+  void lazy_inputs() {
+    const size_t ni = in_ranges_.size(), nc = p_.code.size();
+    std::vector<uint32_t> first(ni, uint32_t(nc));
+    std::vector<char> event(nc, 0);
+    int64_t trips = 1;
+    for (size_t k = 0; k < nc; ++k) {
+      const TpoVmInstr &I = p_.code[k];
+      if (I.op == VM_LOOP) {
+        trips = int64_t(I.n);
+        continue;
+      }
+      if (I.op == VM_ENDLOOP) {
+        trips = 1;
+        continue;
+      }
+      event[k] = I.op == VM_RAISE || (I.op == VM_UNARY && I.sub == VM_SQRT) ||
+                 (I.op == VM_BINARY && (I.sub == VM_DIV || I.pre_a == 1 + VM_SQRT || I.pre_b == 1 + VM_SQRT));
+      if (I.op == VM_RAISE) continue;
+      const Access A = instr_access(I, trips);
+      for (size_t i = 0; i < ni; ++i) {
+        if (first[i] != nc) continue;
+        const int64_t lo = in_ranges_[i].first, hi = lo + in_ranges_[i].second;
+        bool rd = A.opaque;
+        for (const Span &sp : A.rd) rd = rd || (sp.lo < hi && lo < sp.hi);
+        if (rd) first[i] = uint32_t(k);
+      }
+    }
+    std::vector<size_t> ord(ni);
+    std::iota(ord.begin(), ord.end(), size_t(0));
+    std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return first[a] < first[b]; });
+    // group: an input joins the current group unless an event-capable
+    // instruction lies between the group's draw point and its first reader
+    std::vector<uint32_t> at(ni);
+    uint32_t gpc = ni ? first[ord[0]] : 0;
+    int groups = ni ? 1 : 0;
+    for (size_t j = 0; j < ni; ++j) {
+      const uint32_t f = first[ord[j]];
+      bool ev = false;
+      for (uint32_t k = gpc; k < f && k < nc; ++k) ev = ev || event[k];
+      static const bool nogroup = [] {  // experiment: one draw point per input
+        const char *e = std::getenv("TPO_VM_LAZY_GROUP");
+        return e && e[0] == '0';
+      }();
+      if (ev || (nogroup && f != gpc)) {
+        gpc = f;
+        ++groups;
+      }
+      at[ord[j]] = gpc;
+    }
+    if (groups <= 1) return;
+    // entries by (draw point, word offset), contiguous ranges of one point merged
+    std::vector<size_t> ent(ni);
+    std::iota(ent.begin(), ent.end(), size_t(0));
+    std::sort(ent.begin(), ent.end(), [&](size_t a, size_t b) {
+      return at[a] != at[b] ? at[a] < at[b] : in_ranges_[a].first < in_ranges_[b].first;
+    });
+    uint8_t n = 0;
+    for (size_t i : ent) {
+      if (n && p_.desc.gen_pc[n - 1] == at[i] && p_.desc.gen_e0[n - 1] + p_.desc.gen_len[n - 1] == in_ranges_[i].first) {
+        p_.desc.gen_len[n - 1] += in_ranges_[i].second;
+        continue;
+      }
+      p_.desc.gen_pc[n] = at[i];
+      p_.desc.gen_e0[n] = in_ranges_[i].first;
+      p_.desc.gen_len[n] = in_ranges_[i].second;
+      ++n;
+    }
+    p_.desc.n_gen = n;
   }
 
   uint32_t buf(TensorId t) {

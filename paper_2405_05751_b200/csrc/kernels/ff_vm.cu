@@ -19,6 +19,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "ff_vm.cuh"
 #include "smem_limit.cuh"
 #include "vm.h"
@@ -30,6 +32,9 @@ namespace tpo_ff {
 
 constexpr uint64_t kGamma = 0x9e3779b97f4a7c15ull;
 
+// splitmix64 finalizer (rng.hpp:38-40)
+// (three-instruction 64-bit multiplies by inline PTX measured slower than
+// the compiler's own expansion in this kernel: RMSNorm pool 24.9 vs 23.5 ms)
 __device__ __forceinline__ uint64_t fin(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
   z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
@@ -123,22 +128,21 @@ __device__ uint32_t seq_uniform(uint64_t &st, uint32_t n, uint64_t thr, uint32_t
   }
 }
 
-// Generate inputs, omega, SiLU tables and the omega power table for one
-// attempt.  Returns omega.  Draw order is sample_inputs (ffeval.cpp:29-40),
-// sample_omega (field.cpp:140-142), SiluTables::sample (ffeval.cpp:20-27).
+// Input words [e0, e1) of an attempt: element e takes draws 2e+1 (xp) and
+// 2e+2 (xq) of the attempt's stream (sample_inputs, ffeval.cpp:29-40).
+// Returns this thread's "slow" flag: some draw may fall in the rejection
+// zone, and only the exact sequential replay can decide (gen_attempt).
 template <typename WT>
-__device__ uint32_t gen_attempt(const SmemT<WT> &s, const FieldConst &f, uint64_t seed, uint64_t stream,
-                                uint32_t n_in, bool silu, int *s_slow, uint32_t *s_omega) {
-  const uint64_t st0 = derive_state(seed, stream);
+__device__ bool gen_inputs(const SmemT<WT> &s, const FieldConst &f, uint64_t st0, uint32_t e0, uint32_t e1) {
   bool slow = false;
   if (f.small) {
     // The rejection zone r < thr (thr < n) needs a zero high word: flag any
     // draw with hi == 0 (p = 2^-32 each) and let the exact sequential replay
-    // below decide.  The draw state advances by a constant per thread.
+    // decide.  The draw state advances by a constant per thread.
     const uint64_t step = 2ull * blockDim.x * kGamma;
-    uint64_t z = st0 + (2ull * threadIdx.x + 1) * kGamma;
+    uint64_t z = st0 + (2ull * (e0 + threadIdx.x) + 1) * kGamma;
     uint32_t hmin = 0xffffffffu;
-    for (uint32_t e = threadIdx.x; e < n_in; e += blockDim.x, z += step) {
+    for (uint32_t e = e0 + threadIdx.x; e < e1; e += blockDim.x, z += step) {
       const uint64_t r1 = fin(z), r2 = fin(z + kGamma);
       const uint32_t h1 = uint32_t(r1 >> 32), h2 = uint32_t(r2 >> 32);
       hmin = min(hmin, min(h1, h2));
@@ -148,7 +152,7 @@ __device__ uint32_t gen_attempt(const SmemT<WT> &s, const FieldConst &f, uint64_
     }
     slow = hmin == 0;
   } else {
-    for (uint32_t e = threadIdx.x; e < n_in; e += blockDim.x) {
+    for (uint32_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
       uint64_t r1 = fin(st0 + (2ull * e + 1) * kGamma);
       uint64_t r2 = fin(st0 + (2ull * e + 2) * kGamma);
       slow |= (r1 < f.thr_p) | (r2 < f.thr_q);
@@ -157,6 +161,16 @@ __device__ uint32_t gen_attempt(const SmemT<WT> &s, const FieldConst &f, uint64_
       s.w[e] = Word<WT>::pack(xp, xq);
     }
   }
+  return slow;
+}
+
+// omega (sample_omega, field.cpp:140-142: draw 2 n_in + 1, thread 0 writes
+// *s_omega) and the SiLU tables (SiluTables::sample, ffeval.cpp:20-27:
+// draws 2 n_in + 2 ..).  Returns this thread's slow flag.
+template <typename WT>
+__device__ bool gen_tables(const SmemT<WT> &s, const FieldConst &f, uint64_t st0, uint32_t n_in, bool silu,
+                           uint32_t *s_omega) {
+  bool slow = false;
   const uint64_t base = 2ull * n_in;  // next draw index
   if (silu) {
     for (uint32_t i = threadIdx.x; i < f.p + f.q; i += blockDim.x) {
@@ -181,12 +195,35 @@ __device__ uint32_t gen_attempt(const SmemT<WT> &s, const FieldConst &f, uint64_
       k >>= 1;
     }
     *s_omega = w;
-    *s_slow = 0;
+  }
+  return slow;
+}
+
+// omega^e mod p for e in [0, q) (EwExp's table); ends with a barrier.
+template <typename WT>
+__device__ void gen_pow(const SmemT<WT> &s, const FieldConst &f, uint32_t omega) {
+  for (uint32_t e = threadIdx.x; e < f.q; e += blockDim.x) {
+    uint32_t w = 1, b = omega, k = e;
+    while (k) {
+      if (k & 1) w = mod32(w * b, f.p, f.magic_p);
+      b = mod32(b * b, f.p, f.magic_p);
+      k >>= 1;
+    }
+    s.pow_w[e] = uint16_t(w);
   }
   __syncthreads();
-  if (slow) atomicOr(s_slow, 1);
-  __syncthreads();
-  if (*s_slow) {
+}
+
+// Generate inputs, omega, SiLU tables and the omega power table for one
+// attempt.  Returns omega.  Draw order is sample_inputs (ffeval.cpp:29-40),
+// sample_omega (field.cpp:140-142), SiluTables::sample (ffeval.cpp:20-27).
+template <typename WT>
+__device__ uint32_t gen_attempt(const SmemT<WT> &s, const FieldConst &f, uint64_t seed, uint64_t stream,
+                                uint32_t n_in, bool silu, int *s_slow, uint32_t *s_omega) {
+  const uint64_t st0 = derive_state(seed, stream);
+  bool slow = gen_inputs(s, f, st0, 0, n_in);
+  slow |= gen_tables(s, f, st0, n_in, silu, s_omega);
+  if (__syncthreads_or(slow)) {
     if (threadIdx.x == 0) {
       uint64_t st = st0;
       for (uint32_t e = 0; e < n_in; ++e) {
@@ -212,18 +249,23 @@ __device__ uint32_t gen_attempt(const SmemT<WT> &s, const FieldConst &f, uint64_
     __syncthreads();
   }
   const uint32_t omega = *s_omega;
-  // omega^e mod p for e in [0, q)
-  for (uint32_t e = threadIdx.x; e < f.q; e += blockDim.x) {
-    uint32_t w = 1, b = omega, k = e;
-    while (k) {
-      if (k & 1) w = mod32(w * b, f.p, f.magic_p);
-      b = mod32(b * b, f.p, f.magic_p);
-      k >>= 1;
-    }
-    s.pow_w[e] = uint16_t(w);
-  }
-  __syncthreads();
+  gen_pow(s, f, omega);
+  (void)s_slow;
   return omega;
+}
+
+// Lazy attempt start (TpoVmGraph::n_gen): omega, the SiLU tables and the
+// power table only; the inputs are drawn by run_program right before their
+// first readers.  Returns false when a draw may be in the rejection zone:
+// the caller then takes gen_attempt (exact replay) and runs eagerly.
+template <typename WT>
+__device__ bool gen_attempt_lazy(const SmemT<WT> &s, const FieldConst &f, uint64_t st0, uint32_t n_in,
+                                 bool silu, uint32_t *s_omega, uint32_t &omega) {
+  const bool slow = gen_tables(s, f, st0, n_in, silu, s_omega);
+  if (__syncthreads_or(slow)) return false;
+  omega = *s_omega;
+  gen_pow(s, f, omega);
+  return true;
 }
 
 // x / d for an instruction's precomputed divisor (vm.h tpo_vm_divisor)
@@ -369,40 +411,54 @@ __device__ __forceinline__ uint32_t ff_exec(const SmemT<WT> &s, const FieldConst
       break;
     }
     case VM_BINARY: {
+      // instruction fields hoisted into registers: the loop's shared-memory
+      // stores could alias the instruction (also in shared memory), so the
+      // compiler would otherwise re-read them per element; the fused
+      // thread-graph pre-ops get their own loop instance
       const uint32_t lim = I.b0n ? I.b0n : n;
-      for (uint32_t i = start; i < n; i += step) {
-        int32_t od = int32_t(i), oa = int32_t(i), ob = int32_t(i);
-        bool wr = true;
-        if (!flat) offsets(I, i, od, oa, ob, wr);
-        uint32_t va = W[I.a + oa], vb = W[I.b + ob];
-        uint32_t ap = va & PM, aq = va >> QS, bp = vb & PM, bq = vb >> QS;
-        if (I.pre_a) bad_pre |= ff_pre(s, f, I.pre_a, I.flags & VM_A_QD, ap, aq) && i < lim;
-        if (I.pre_b) bad_pre |= ff_pre(s, f, I.pre_b, I.flags & VM_B_QD, bp, bq) && i < lim;
-        uint32_t rp, rq = 0;
-        switch (I.sub) {
-          case VM_ADD:
-            rp = ap + bp;
-            rp = rp >= p ? rp - p : rp;
-            if (qd) {
-              rq = aq + bq;
-              rq = rq >= q ? rq - q : rq;
-            }
-            break;
-          case VM_MUL:
-            rp = mod32(ap * bp, p, mp);
-            if (qd) rq = mod32(aq * bq, q, mq);
-            break;
-          default:  // VM_DIV (field.cpp:93-103)
-            bad |= bp == 0 && i < lim;
-            rp = mod32(ap * s.inv_p[bp], p, mp);
-            if (qd) {
-              bad |= bq == 0 && i < lim;
-              rq = mod32(aq * s.inv_q[bq], q, mq);
-            }
-            break;
+      const uint32_t ia = I.a, ib = I.b, idst = I.dst;
+      const uint8_t sub = I.sub, pre_a = I.pre_a, pre_b = I.pre_b;
+      const bool aqd = I.flags & VM_A_QD, bqd = I.flags & VM_B_QD;
+      auto loop = [&](auto pre_tag) {
+        constexpr bool PRE = decltype(pre_tag)::value;
+        for (uint32_t i = start; i < n; i += step) {
+          int32_t od = int32_t(i), oa = int32_t(i), ob = int32_t(i);
+          bool wr = true;
+          if (!flat) offsets(I, i, od, oa, ob, wr);
+          uint32_t va = W[ia + oa], vb = W[ib + ob];
+          uint32_t ap = va & PM, aq = va >> QS, bp = vb & PM, bq = vb >> QS;
+          if (PRE) {
+            if (pre_a) bad_pre |= ff_pre(s, f, pre_a, aqd, ap, aq) && i < lim;
+            if (pre_b) bad_pre |= ff_pre(s, f, pre_b, bqd, bp, bq) && i < lim;
+          }
+          uint32_t rp, rq = 0;
+          switch (sub) {
+            case VM_ADD:
+              rp = ap + bp;
+              rp = rp >= p ? rp - p : rp;
+              if (qd) {
+                rq = aq + bq;
+                rq = rq >= q ? rq - q : rq;
+              }
+              break;
+            case VM_MUL:
+              rp = mod32(ap * bp, p, mp);
+              if (qd) rq = mod32(aq * bq, q, mq);
+              break;
+            default:  // VM_DIV (field.cpp:93-103)
+              bad |= bp == 0 && i < lim;
+              rp = mod32(ap * s.inv_p[bp], p, mp);
+              if (qd) {
+                bad |= bq == 0 && i < lim;
+                rq = mod32(aq * s.inv_q[bq], q, mq);
+              }
+              break;
+          }
+          W[idst + od] = Word<WT>::pack(rp, rq);
         }
-        W[I.dst + od] = Word<WT>::pack(rp, rq);
-      }
+      };
+      if (pre_a | pre_b) loop(std::true_type{});
+      else loop(std::false_type{});
       break;
     }
     case VM_MATMUL: {
@@ -599,15 +655,42 @@ __device__ __forceinline__ uint32_t ff_exec(const SmemT<WT> &s, const FieldConst
 }
 
 // PROF: thread 0 accumulates clock64 per VM opcode into prof[op] (TPO_VM_PROFILE).
+// Lazy input sampling (`lz` = the graph's descriptor, TpoVmGraph::n_gen):
+// before instruction pc, the inputs whose first reader it is are drawn, then
+// a barrier; *gen_next counts the inputs drawn so far.  A draw that may lie
+// in the rejection zone aborts the run with *s_restart set (the caller
+// replays the attempt exactly and reruns eagerly).  Inputs are never written
+// and no instruction before pc reads them, so the barrier may sit inside a
+// barrier phase.
+template <typename WT>
+__device__ bool lazy_gen_until(const SmemT<WT> &s, const FieldConst &f, const TpoVmGraph *lz, uint64_t st0,
+                               uint32_t pc, uint32_t *gen_next, int *s_restart) {
+  uint32_t k = *gen_next;
+  if (k >= lz->n_gen || lz->gen_pc[k] > pc) return true;
+  bool slow = false;
+  for (; k < lz->n_gen && lz->gen_pc[k] <= pc; ++k)
+    slow |= gen_inputs(s, f, st0, lz->gen_e0[k], lz->gen_e0[k] + lz->gen_len[k]);
+  *gen_next = k;
+  if (__syncthreads_or(slow)) {
+    if (threadIdx.x == 0) *s_restart = 1;
+    __syncthreads();
+    return false;
+  }
+  return true;
+}
+
 template <bool PROF, typename WT>
 __device__ bool run_program(const SmemT<WT> &s, const FieldConst &f, const TpoVmInstr *code,
-                            uint32_t len, int *s_flag, unsigned long long *prof) {
+                            uint32_t len, int *s_flag, unsigned long long *prof,
+                            const TpoVmGraph *lz = nullptr, uint64_t st0 = 0, uint32_t *gen_next = nullptr,
+                            int *s_restart = nullptr) {
   uint32_t it = 0, loop_pc = 0, trips = 1;
   long long t_prev = PROF ? clock64() : 0;
   bool phase_bad = false;  // this thread saw an event since the last barrier
   for (uint32_t pc = 0; pc < len; ++pc) {
     const TpoVmInstr &I = code[pc];
     const uint8_t op = I.op;
+    if (lz && !lazy_gen_until(s, f, lz, st0, pc, gen_next, s_restart)) return false;
     if (op == VM_LOOP) {
       trips = I.n;
       it = 0;
@@ -701,7 +784,7 @@ __global__ void __maxnreg__(PROF ? 88 : TPO_VM_REGCAP) verify_kernel(VerifyArgs 
 __global__ void __launch_bounds__(NT, NT == 256 ? 3 : NT == 128 ? 7 : 14) verify_kernel(VerifyArgs a) {
 #endif
   extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ int s_flag, s_slow;
+  __shared__ int s_flag, s_slow, s_restart;
   __shared__ uint32_t s_omega;
   __shared__ unsigned long long s_cand, s_key;
   __shared__ unsigned long long s_prof[32];  // PROF: [0,16) cycles per opcode, [16,32) counts
@@ -794,12 +877,29 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : NT == 128 ? 7 : 14) verify
           __syncthreads();
           ok = run_program<PROF>(s, f, ccode, g2.code_len, &s_flag, s_prof);
         } else {
-          omega = gen_attempt(s, f, seed, stream, a.n_in, silu, &s_slow, &s_omega);
-          if (threadIdx.x == 0) s_flag = 0;
+          // lazy sampling: omega and the tables now, each input right before
+          // the program's first reader of it (an attempt the program
+          // resamples early never draws the rest); the candidate needs every
+          // input, so the rest is drawn before it runs
+          const uint64_t st0 = derive_state(seed, stream);
+          bool lazy = g1.n_gen > 0 && !a.eager_inputs;
+          if (lazy) lazy = gen_attempt_lazy(s, f, st0, a.n_in, silu, &s_omega, omega);
+          if (!lazy) omega = gen_attempt(s, f, seed, stream, a.n_in, silu, &s_slow, &s_omega);
+          if (threadIdx.x == 0) s_flag = 0, s_restart = 0;
           __syncthreads();
           if (PROF && threadIdx.x == 0) s_prof[0] += (unsigned long long)(clock64() - t0), s_prof[16] += 1;
-          ok = run_program<PROF>(s, f, scode, g1.code_len, &s_flag, s_prof) &&
-               run_program<PROF>(s, f, ccode, g2.code_len, &s_flag, s_prof);
+          uint32_t gen_next = 0;
+          ok = run_program<PROF>(s, f, scode, g1.code_len, &s_flag, s_prof, lazy ? &g1 : nullptr, st0, &gen_next,
+                                 &s_restart);
+          if (lazy && ok) ok = lazy_gen_until(s, f, &g1, st0, 0xffffffffu, &gen_next, &s_restart);
+          if (lazy && s_restart) {
+            // a draw may lie in the rejection zone: the exact replay, eagerly
+            omega = gen_attempt(s, f, seed, stream, a.n_in, silu, &s_slow, &s_omega);
+            if (threadIdx.x == 0) s_flag = 0;
+            __syncthreads();
+            ok = run_program<PROF>(s, f, scode, g1.code_len, &s_flag, s_prof);
+          }
+          ok = ok && run_program<PROF>(s, f, ccode, g2.code_len, &s_flag, s_prof);
         }
         if (!ok && (s_flag & 3) == 3) {  // Error(PoisonedExponent) escapes the verifier
           if (t0w) {

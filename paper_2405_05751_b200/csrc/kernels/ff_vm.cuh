@@ -65,6 +65,7 @@ struct VerifyArgs {
   const uint32_t *shared_meta;   // [0] program ok on that stream, [1] omega
   uint64_t shared_seed;
   uint32_t shared_len;
+  int eager_inputs;              // 1: draw every input at attempt start (TPO_VM_EAGER, A/B)
 };
 
 struct EvalArgs {

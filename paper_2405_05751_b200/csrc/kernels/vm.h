@@ -20,6 +20,7 @@
 
 #define TPO_VM_DIMS 7
 #define TPO_VM_MAX_OUTPUTS 8
+#define TPO_VM_MAX_GEN 8
 
 enum TpoVmOp {
   VM_ZERO = 1,   // dst[0..n) = 0 (field zero (0,0,defined) / 0.0)
@@ -128,5 +129,12 @@ struct TpoVmGraph {
   uint8_t out_qd[TPO_VM_MAX_OUTPUTS];
   uint8_t has_silu, poisoned;
   uint8_t err;                  // 0, or 1 + tpo::ErrCode: candidate rejected up front
-  uint8_t pad[5];
+  // FF, lazy input sampling: input words [gen_e0[i], + gen_len[i]) are drawn
+  // right before instruction gen_pc[i], their first reader (gen_pc ascending;
+  // gen_pc == code_len: never read by this graph).  An attempt that resamples
+  // before an input is read never draws it.  n_gen = 0: draw all up front.
+  uint8_t n_gen;
+  uint8_t pad[4];
+  uint32_t gen_pc[TPO_VM_MAX_GEN];
+  uint32_t gen_e0[TPO_VM_MAX_GEN], gen_len[TPO_VM_MAX_GEN];
 };

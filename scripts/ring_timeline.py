@@ -148,7 +148,7 @@ def main():
     # tail sub-phases per CTA, relative to the CTA's own last MMA (median over
     # CTAs and launches): MMA completion, DSMEM send / receive, owner store,
     # teardown
-    sub = {5: "tmem_full", 4: "sent", 6: "recv_done", 11: "owner_done", 2: "epi_done", 13: "pre_sync",
+    sub = {5: "tmem_full", 4: "sent", 6: "recv_done", 15: "summed", 11: "owner_done", 2: "epi_done", 13: "pre_sync",
            12: "synced", 7: "end"}
     acc = {k: [] for k in sub}
     for i in range(3, K):

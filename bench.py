@@ -466,36 +466,53 @@ def cpu_baseline_fused(wl, threads=1, min_seconds=10.0, min_reps=1):
 
 def generic_vm(wl, reps=3):
     """The same µGraph (and its flat program) on the generic GPU VM in the
-    reference's own arithmetic (tpo_gpu_eval_vm: fp64, the reference's
+    reference's own arithmetic (tpo_gpu_eval_vm: fp64 / fp32, the reference's
     operation order; the global-memory executor at these sizes) — the path
-    any µGraph without a hand-written kernel takes.  Wall clock per call,
-    host buffers in and out."""
+    any µGraph without a hand-written kernel takes.  Device time per call
+    (CUDA events; inputs already in one flat device buffer), wall clock per
+    call with host buffers, and the HBM fraction of the device time for the
+    unique input + output bytes in that dtype."""
+    import ctypes as C
     import torch
+    from paper_2405_05751_b200 import _native as N
     from paper_2405_05751_b200.api import Context
     ctx = Context(0)
     ins = [x.float().numpy().astype(np.float64) for x in wl["host"]]
-    dins = [torch.from_numpy(x).cuda() for x in ins]
+    peak = peaks()[0]
     out = {}
-    for tag, g, mode in (("eval_mugraph", wl["mu"], 0), ("eval_program", wl["prog"], 1)):
+    for tag, g, mode in (("eval_mugraph", wl["mu"], 0), ("eval_program", wl["prog"], 1),
+                         ("eval_mugraph_f32", wl["mu"], 2)):
         gg = ctx.compile(g)
-        ctx.eval_vm(gg, ins, mode=mode)  # warm
+        dt, npdt = (torch.float32, np.float32) if mode == 2 else (torch.float64, np.float64)
+        hin = [x.astype(npdt) for x in ins]
+        ctx.eval_vm(gg, hin, mode=mode)  # warm
         t0 = time.perf_counter()
         for _ in range(reps):
-            ctx.eval_vm(gg, ins, mode=mode)
+            ctx.eval_vm(gg, hin, mode=mode)
         wall = (time.perf_counter() - t0) / reps * 1e3
+        flat = torch.cat([torch.from_numpy(x).reshape(-1) for x in hin]).to(dt).cuda()
+        n_out = sum(int(np.prod(sh)) for sh in gg.shapes(True))
+        dout = torch.empty(n_out, dtype=dt, device="cuda")
         st = torch.cuda.current_stream()
-        ctx.eval_vm_dev(gg, dins, mode=mode, stream=st.cuda_stream)
+
+        def run():
+            N.check(N.lib().tpo_gpu_eval_vm_dev(ctx.h, gg.h, mode, C.c_void_p(flat.data_ptr()),
+                                                C.c_void_p(dout.data_ptr()), C.c_void_p(st.cuda_stream)))
+        run()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         e0.record()
         for _ in range(reps):
-            ctx.eval_vm_dev(gg, dins, mode=mode, stream=st.cuda_stream)
+            run()
         e1.record()
         torch.cuda.synchronize()
-        out[tag] = {"device_ms_per_eval": round(e0.elapsed_time(e1) / reps, 3),
-                    "host_buffers_ms_per_eval": round(wall, 3), "dtype": "f64",
-                    "h2d_bytes": int(sum(x.nbytes for x in ins))}
-    out["note"] = "bit-exact with the reference for graphs without exp (tests/test_fp_vm_gpu.py)"
+        ms = e0.elapsed_time(e1) / reps
+        nbytes = int(flat.numel() * flat.element_size() + n_out * dout.element_size())
+        out[tag] = {"device_ms_per_eval": round(ms, 3), "host_buffers_ms_per_eval": round(wall, 3),
+                    "dtype": "f32" if mode == 2 else "f64", "h2d_bytes": int(sum(x.nbytes for x in hin)),
+                    "hbm_frac": round(nbytes / (ms * 1e-3) / (peak * 1e9), 4) if peak else None}
+    out["note"] = ("bit-exact with the reference for graphs without exp (tests/test_fp_vm_gpu.py); "
+                   "f32 = the reference's eval_mugraph_f32 semantics")
     return out
 
 
@@ -653,17 +670,19 @@ def run_verify(dist, n_total, steps=1, warmup=3, pool_fams=("rmsnorm", "gatedmlp
     # of the program's inputs per attempt, +1 for omega, +340 for the SiLU
     # tables when either graph has SiLU
     from paper_2405_05751_b200.graph import has_silu
-    macs = draws = 0.0
+    macs = draws = draws_eager = 0.0
     for f, gp, gs, first, n in jobs:
         v, _ = ctx.verify_pool(gp, gs, first=first, n=n, want_verdicts=True)
+        draws += float(ctx.last_verify_draws())  # draws actually made (lazy input sampling)
         idx = (np.arange(first, first + n) % len(gs))
         cm = np.array([g.madds for g in gs], dtype=np.float64)[idx]
         att = (v["rounds_run"] + v["resamples"]).astype(np.float64)
         macs += float(np.sum(att * 2.0 * (gp.madds + cm)))
         silu = np.array([has_silu(g.spec) or has_silu(gp.spec) for g in gs])[idx]
-        draws += float(np.sum(att * (2.0 * gp.info.input_elems + 1 + 340.0 * silu)))
+        draws_eager += float(np.sum(att * (2.0 * gp.info.input_elems + 1 + 340.0 * silu)))
     macs = dist.sum(macs)
     draws = dist.sum(draws)
+    draws_eager = dist.sum(draws_eager)
     peak = dp4a = None
     try:
         pk = json.load(open(os.path.join(ROOT, "profiles", "int_peak.json")))
@@ -680,12 +699,15 @@ def run_verify(dist, n_total, steps=1, warmup=3, pool_fams=("rmsnorm", "gatedmlp
                     "Field MACs are a minority of the work: per attempt the inputs are "
                     "regenerated (2 splitmix64 draws + a mod per element, the rng term) and "
                     "both graphs interpreted; see issue_utilization"}
-    # the RNG term: a splitmix64 draw + its mod-uniform reduction is ~12
-    # integer instructions (3 IMAD-pipe multiplies + shifts / xors / the
-    # magic-number mod), so 12 x draws / IMAD peak is its instruction share
-    roof["rng"] = {"draws": draws, "draws_per_s": round(draws / t_all, 1),
-                   "instr_per_draw_est": 12,
-                   "frac_of_issue_est": round(12 * draws / t_all / peak, 4) if peak else None}
+    # the RNG term: the input-generation loop is 77 SASS instructions per
+    # element = 2 splitmix64 draws, each reduced mod-uniform by a magic-number
+    # step (cuobjdump of verify_kernel), i.e. ~38.5 thread instructions per
+    # draw, against the SM instruction-issue peak (148 SMs x 4 schedulers x
+    # 32 lanes x the measured clock); draws counted by the kernel
+    issue_peak = 148 * 4 * 32 * 1.9e9
+    roof["rng"] = {"draws": draws, "draws_if_eager": draws_eager, "draws_per_s": round(draws / t_all, 1),
+                   "instr_per_draw": 38.5, "issue_peak_thread_instr_per_s": issue_peak,
+                   "frac_of_issue": round(38.5 * draws / t_all / issue_peak, 4)}
     roof["issue_utilization"] = ncu_issue("verify")
     if dp4a:
         roof["frac_vs_dp4a_2lane"] = round(macs / t_all / (2 * dp4a), 4)
@@ -846,8 +868,8 @@ def search_stream(ctx, dist, fams, pool_fams, per_fam_total=25000):
 
 def ncu_issue(tag):
     """SM instruction-issue utilisation of the kernel from its committed ncu
-    summary (profiles/r01/ncu_<tag>.txt): the bound of an interpreter kernel."""
-    path = os.path.join(ROOT, "profiles", "r01", f"ncu_{tag}.txt")
+    summary (profiles/r02/ncu_<tag>.txt): the bound of an interpreter kernel."""
+    path = os.path.join(ROOT, "profiles", "r02", f"ncu_{tag}.txt")
     out = {"source": os.path.relpath(path, ROOT)}
     try:
         for line in open(path):

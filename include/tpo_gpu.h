@@ -217,6 +217,14 @@ int tpo_gpu_verify_pool(tpo_gpu_ctx *ctx, const tpo_gpu_graph *program,
                         uint32_t *accept_dev, tpo_verdict *verdicts, uint64_t *attempts,
                         void *cuda_stream);
 
+/* splitmix64 draws made by the context's last tpo_gpu_verify_pool call that
+ * requested `attempts` (2 per input element drawn, omega, the SiLU tables):
+ * the verifier's RNG work term.  Inputs are drawn lazily — an
+ * attempt the program resamples before an input's first reader never draws
+ * it — so this is the work actually done, not 2 x inputs x attempts.
+ * Replaces: no reference counterpart (instrumentation). */
+int tpo_gpu_verify_draws(tpo_gpu_ctx *ctx, uint64_t *draws);
+
 /* Generic floating-point evaluation on the GPU µGraph VM (any graph; working
  * sets that fit shared memory run in one CTA, larger ones on the
  * global-memory executor, one grid-wide launch per VM instruction),

@@ -92,6 +92,7 @@ def lib():
                                        C.POINTER(FieldParams), vp, vp]
     L.tpo_gpu_verify_pool.argtypes = [vp, vp, vp, i32, u64, u64, C.POINTER(VerifyCfg),
                                       C.POINTER(FieldParams), vp, vp, vp, vp]
+    L.tpo_gpu_verify_draws.argtypes = [vp, C.POINTER(u64)]
     L.tpo_gpu_enumerate.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, i64, C.POINTER(i64)]
     L.tpo_gpu_abstract_expression.argtypes = [C.c_char_p, C.c_char_p, i64, C.POINTER(i64)]
     L.tpo_gpu_search.argtypes = [vp, vp, C.c_char_p, C.POINTER(VerifyCfg), C.POINTER(FieldParams), vp, i64,

@@ -530,3 +530,9 @@ class Context:
             out.ctypes.data if want_verdicts else None, C.addressof(att),
             C.c_void_p(stream) if stream else None))
         return out, att.value
+
+    def last_verify_draws(self) -> int:
+        """splitmix64 draws of the last verify_pool call (tpo_gpu_verify_draws)."""
+        d = C.c_uint64(0)
+        N.check(N.lib().tpo_gpu_verify_draws(self.h, C.byref(d)))
+        return d.value

@@ -331,10 +331,11 @@ void run_verify(Ctx &C, const Batch &bt, const tpo_verify_cfg &cfg, const tpo_fi
   a.n_in = bt.n_in;
   a.num_tests = cfg.num_tests;
   a.max_resamples = cfg.max_resamples;
-  auto *cnt = static_cast<unsigned long long *>(C.counter.get(16));
-  check_cuda(cudaMemsetAsync(cnt, 0, 16, st), "counter");
+  auto *cnt = static_cast<unsigned long long *>(C.counter.get(24));
+  check_cuda(cudaMemsetAsync(cnt, 0, 24, st), "counter");
   a.counter = cnt;
   a.work = cnt + 1;
+  a.drawn = cnt + 2;
   if (r.verdicts_host) a.verdicts = static_cast<TpoVerdict *>(C.verdicts.get(r.n * sizeof(TpoVerdict)));
   const size_t words = (r.n + 31) / 32;
   uint32_t *acc = r.accept_dev;
@@ -425,11 +426,14 @@ void run_verify(Ctx &C, const Batch &bt, const tpo_verify_cfg &cfg, const tpo_fi
                                cudaMemcpyDeviceToHost, st), "verdicts");
   if (r.accept_host)
     check_cuda(cudaMemcpyAsync(r.accept_host, acc, words * 4, cudaMemcpyDeviceToHost, st), "accept");
-  unsigned long long counters[2] = {0, 0};
+  unsigned long long counters[3] = {0, 0, 0};
   if (r.attempts)
-    check_cuda(cudaMemcpyAsync(counters, cnt, 16, cudaMemcpyDeviceToHost, st), "attempts");
+    check_cuda(cudaMemcpyAsync(counters, cnt, 24, cudaMemcpyDeviceToHost, st), "attempts");
   check_cuda(cudaStreamSynchronize(st), "verify sync");
-  if (r.attempts) *r.attempts = counters[1];
+  if (r.attempts) {
+    *r.attempts = counters[1];
+    C.last_draws = counters[2];
+  }
 }
 
 }  // namespace
@@ -1142,6 +1146,14 @@ int tpo_gpu_verify_pool(tpo_gpu_ctx *ctx, const tpo_gpu_graph *program,
     r.attempts = attempts;
     r.stream = static_cast<cudaStream_t>(cuda_stream);
     run_verify(ctx->c, bt, *cfg, *fp, r);
+    return 0;
+  });
+}
+
+int tpo_gpu_verify_draws(tpo_gpu_ctx *ctx, uint64_t *draws) {
+  return guard([&] {
+    if (!draws) throw Error(ErrCode::ShapeMismatch, "draws is NULL");
+    *draws = ctx->c.last_draws;
     return 0;
   });
 }

@@ -44,6 +44,7 @@ struct Ctx {
   std::map<std::tuple<uint32_t, uint32_t, uint32_t>, std::unique_ptr<FieldState>> fields;
   DevBuf code, graphs, pool, cand, seeds, verdicts, accept, counter, out, status, inputs, ws;
   DevBuf shared_w, shared_tab, shared_meta;  // same-seed verification batches
+  uint64_t last_draws = 0;                     // splitmix64 draws of the last verify call (attempts requested)
   DevBuf vm_in, vm_out;                       // generic-VM evaluation of unfused µGraphs
   // host-buffer fp evaluation (tpo_gpu_eval_mugraph_host): per-input device
   // copies (bf16), fp32 staging for converted inputs, per-output buffers

@@ -289,6 +289,62 @@ __device__ __forceinline__ void offsets(const TpoVmInstr &I, uint32_t idx, int32
   }
 }
 
+// The index views of an instruction with ND <= 3 dims, loaded into
+// registers once per instruction: offsets() re-reads them from shared
+// memory for every element (the element loop's stores may alias the
+// instruction as far as the compiler knows).
+template <int ND>
+struct IdxN {
+  uint32_t d[ND], mul[ND], sh[ND];
+  int32_t sd[ND], sa[ND], sb[ND];
+  uint32_t wm;
+  __device__ __forceinline__ explicit IdxN(const TpoVmInstr &I) {
+#pragma unroll
+    for (int k = 0; k < ND; ++k) {
+      d[k] = I.dims[k], mul[k] = I.dmul[k], sh[k] = I.dsh[k];
+      sd[k] = I.sd[k], sa[k] = I.sa[k], sb[k] = I.sb[k];
+    }
+    wm = I.wmask;
+  }
+  __device__ __forceinline__ void operator()(uint32_t idx, int32_t &od, int32_t &oa, int32_t &ob, bool &wr) const {
+    od = oa = ob = 0;
+    wr = true;
+#pragma unroll
+    for (int k = ND - 1; k >= 0; --k) {
+      const uint32_t qt = k ? fdiv(idx, mul[k], sh[k]) : 0u;  // the outermost dim needs no division
+      const uint32_t c = k ? idx - qt * d[k] : idx;
+      idx = qt;
+      od += int32_t(c) * sd[k];
+      oa += int32_t(c) * sa[k];
+      ob += int32_t(c) * sb[k];
+      if (((wm >> k) & 1u) && c != d[k] - 1) wr = false;
+    }
+  }
+};
+
+// View ranks whose index views are held in registers (IdxN).  Measured per
+// pool (ms per 250k candidates, profiles/r02/verify_idxn_ab.txt): rank 1
+// only is the best total — register-resident rank-3 views cost the GQA pool
+// 10% (register pressure in its 256-thread CTAs), rank 2 gains nothing.
+#ifndef TPO_VM_IDXN_MAX
+#define TPO_VM_IDXN_MAX 1
+#endif
+
+// Any rank: offsets() over the instruction in shared memory.
+struct IdxAny {
+  const TpoVmInstr &I;
+  __device__ __forceinline__ void operator()(uint32_t idx, int32_t &od, int32_t &oa, int32_t &ob, bool &wr) const {
+    offsets(I, idx, od, oa, ob, wr);
+  }
+};
+// Flat: the index is every operand's offset.
+struct IdxFlat {
+  __device__ __forceinline__ void operator()(uint32_t idx, int32_t &od, int32_t &oa, int32_t &ob, bool &wr) const {
+    od = oa = ob = int32_t(idx);
+    wr = true;
+  }
+};
+
 // Runs one graph's bytecode. Returns false (uniformly) when an undefined
 // field operation (zero divisor / non-residue) requires a resample.
 // Block-cooperative copy of `len` instructions (192 B each) global -> smem.
@@ -338,6 +394,67 @@ __device__ __forceinline__ bool ff_pre(const SmemT<WT> &s, const FieldConst &f, 
   return ev;
 }
 
+template <typename WT, class IX>
+__device__ __forceinline__ void copy_loop(WT *W, uint32_t dbase, uint32_t abase, uint32_t start, uint32_t n,
+                                          uint32_t step, const IX &ix) {
+  for (uint32_t i = start; i < n; i += step) {
+    int32_t od, oa, ob;
+    bool wr;
+    ix(i, od, oa, ob, wr);
+    if (wr) W[dbase + od] = W[abase + oa];
+  }
+}
+
+struct BinOp {
+  uint32_t lim, a, b, dst;
+  uint8_t sub, pre_a, pre_b;
+  bool aqd, bqd, qd;
+};
+
+// VM_BINARY over items [start, n): events below `lim` count (b0n)
+template <bool PRE, typename WT, class IX>
+__device__ __forceinline__ void binary_loop(const SmemT<WT> &s, const FieldConst &f, const BinOp &B, uint32_t start,
+                                            uint32_t n, uint32_t step, const IX &ix, bool &bad, bool &bad_pre) {
+  constexpr uint32_t QS = Word<WT>::kShift, PM = Word<WT>::kMask;
+  WT *W = s.w;
+  const uint32_t p = f.p, q = f.q, mp = f.magic_p, mq = f.magic_q;
+  for (uint32_t i = start; i < n; i += step) {
+    int32_t od, oa, ob;
+    bool wr;
+    ix(i, od, oa, ob, wr);
+    const uint32_t va = W[B.a + oa], vb = W[B.b + ob];
+    uint32_t ap = va & PM, aq = va >> QS, bp = vb & PM, bq = vb >> QS;
+    if (PRE) {
+      if (B.pre_a) bad_pre |= ff_pre(s, f, B.pre_a, B.aqd, ap, aq) && i < B.lim;
+      if (B.pre_b) bad_pre |= ff_pre(s, f, B.pre_b, B.bqd, bp, bq) && i < B.lim;
+    }
+    uint32_t rp, rq = 0;
+    switch (B.sub) {
+      case VM_ADD:
+        rp = ap + bp;
+        rp = rp >= p ? rp - p : rp;
+        if (B.qd) {
+          rq = aq + bq;
+          rq = rq >= q ? rq - q : rq;
+        }
+        break;
+      case VM_MUL:
+        rp = mod32(ap * bp, p, mp);
+        if (B.qd) rq = mod32(aq * bq, q, mq);
+        break;
+      default:  // VM_DIV (field.cpp:93-103)
+        bad |= bp == 0 && i < B.lim;
+        rp = mod32(ap * s.inv_p[bp], p, mp);
+        if (B.qd) {
+          bad |= bq == 0 && i < B.lim;
+          rq = mod32(aq * s.inv_q[bq], q, mq);
+        }
+        break;
+    }
+    W[B.dst + od] = Word<WT>::pack(rp, rq);
+  }
+}
+
 // One VM instruction over items [start, n) with stride `step` (the CTA
 // interpreter passes threadIdx / blockDim, the global-memory executor its
 // grid-stride range).  Returns the resample event of an undefined field op,
@@ -368,11 +485,11 @@ __device__ __forceinline__ uint32_t ff_exec(const SmemT<WT> &s, const FieldConst
       if (flat) {
         for (uint32_t i = start; i < n; i += step) W[dbase + i] = W[abase + i];
       } else {
-        for (uint32_t i = start; i < n; i += step) {
-          int32_t od, oa, ob;
-          bool wr;
-          offsets(I, i, od, oa, ob, wr);
-          if (wr) W[dbase + od] = W[abase + oa];
+        switch (TPO_VM_IDXN_MAX >= I.ndim ? I.ndim : 0) {
+          case 1: copy_loop(W, dbase, abase, start, n, step, IdxN<1>(I)); break;
+          case 2: copy_loop(W, dbase, abase, start, n, step, IdxN<2>(I)); break;
+          case 3: copy_loop(W, dbase, abase, start, n, step, IdxN<3>(I)); break;
+          default: copy_loop(W, dbase, abase, start, n, step, IdxAny{I});
         }
       }
       break;
@@ -411,54 +528,33 @@ __device__ __forceinline__ uint32_t ff_exec(const SmemT<WT> &s, const FieldConst
       break;
     }
     case VM_BINARY: {
-      // instruction fields hoisted into registers: the loop's shared-memory
-      // stores could alias the instruction (also in shared memory), so the
-      // compiler would otherwise re-read them per element; the fused
-      // thread-graph pre-ops get their own loop instance
-      const uint32_t lim = I.b0n ? I.b0n : n;
-      const uint32_t ia = I.a, ib = I.b, idst = I.dst;
-      const uint8_t sub = I.sub, pre_a = I.pre_a, pre_b = I.pre_b;
-      const bool aqd = I.flags & VM_A_QD, bqd = I.flags & VM_B_QD;
-      auto loop = [&](auto pre_tag) {
-        constexpr bool PRE = decltype(pre_tag)::value;
-        for (uint32_t i = start; i < n; i += step) {
-          int32_t od = int32_t(i), oa = int32_t(i), ob = int32_t(i);
-          bool wr = true;
-          if (!flat) offsets(I, i, od, oa, ob, wr);
-          uint32_t va = W[ia + oa], vb = W[ib + ob];
-          uint32_t ap = va & PM, aq = va >> QS, bp = vb & PM, bq = vb >> QS;
-          if (PRE) {
-            if (pre_a) bad_pre |= ff_pre(s, f, pre_a, aqd, ap, aq) && i < lim;
-            if (pre_b) bad_pre |= ff_pre(s, f, pre_b, bqd, bp, bq) && i < lim;
-          }
-          uint32_t rp, rq = 0;
-          switch (sub) {
-            case VM_ADD:
-              rp = ap + bp;
-              rp = rp >= p ? rp - p : rp;
-              if (qd) {
-                rq = aq + bq;
-                rq = rq >= q ? rq - q : rq;
-              }
-              break;
-            case VM_MUL:
-              rp = mod32(ap * bp, p, mp);
-              if (qd) rq = mod32(aq * bq, q, mq);
-              break;
-            default:  // VM_DIV (field.cpp:93-103)
-              bad |= bp == 0 && i < lim;
-              rp = mod32(ap * s.inv_p[bp], p, mp);
-              if (qd) {
-                bad |= bq == 0 && i < lim;
-                rq = mod32(aq * s.inv_q[bq], q, mq);
-              }
-              break;
-          }
-          W[idst + od] = Word<WT>::pack(rp, rq);
+      // instruction fields hoisted into registers (binary_loop); the fused
+      // thread-graph pre-ops and each view rank get their own loop instance
+      const BinOp B{I.b0n ? I.b0n : n, I.a, I.b, I.dst, I.sub, I.pre_a, I.pre_b,
+                    bool(I.flags & VM_A_QD), bool(I.flags & VM_B_QD), qd};
+      const bool pre = B.pre_a | B.pre_b;
+      if (flat) {
+        if (pre) binary_loop<true>(s, f, B, start, n, step, IdxFlat{}, bad, bad_pre);
+        else binary_loop<false>(s, f, B, start, n, step, IdxFlat{}, bad, bad_pre);
+      } else {
+        switch (TPO_VM_IDXN_MAX >= I.ndim ? I.ndim : 0) {
+          case 1:
+            if (pre) binary_loop<true>(s, f, B, start, n, step, IdxN<1>(I), bad, bad_pre);
+            else binary_loop<false>(s, f, B, start, n, step, IdxN<1>(I), bad, bad_pre);
+            break;
+          case 2:
+            if (pre) binary_loop<true>(s, f, B, start, n, step, IdxN<2>(I), bad, bad_pre);
+            else binary_loop<false>(s, f, B, start, n, step, IdxN<2>(I), bad, bad_pre);
+            break;
+          case 3:
+            if (pre) binary_loop<true>(s, f, B, start, n, step, IdxN<3>(I), bad, bad_pre);
+            else binary_loop<false>(s, f, B, start, n, step, IdxN<3>(I), bad, bad_pre);
+            break;
+          default:
+            if (pre) binary_loop<true>(s, f, B, start, n, step, IdxAny{I}, bad, bad_pre);
+            else binary_loop<false>(s, f, B, start, n, step, IdxAny{I}, bad, bad_pre);
         }
-      };
-      if (pre_a | pre_b) loop(std::true_type{});
-      else loop(std::false_type{});
+      }
       break;
     }
     case VM_MATMUL: {
@@ -664,12 +760,15 @@ __device__ __forceinline__ uint32_t ff_exec(const SmemT<WT> &s, const FieldConst
 // barrier phase.
 template <typename WT>
 __device__ bool lazy_gen_until(const SmemT<WT> &s, const FieldConst &f, const TpoVmGraph *lz, uint64_t st0,
-                               uint32_t pc, uint32_t *gen_next, int *s_restart) {
+                               uint32_t pc, uint32_t *gen_next, int *s_restart,
+                               unsigned long long *s_drawn = nullptr) {
   uint32_t k = *gen_next;
   if (k >= lz->n_gen || lz->gen_pc[k] > pc) return true;
   bool slow = false;
-  for (; k < lz->n_gen && lz->gen_pc[k] <= pc; ++k)
+  for (; k < lz->n_gen && lz->gen_pc[k] <= pc; ++k) {
     slow |= gen_inputs(s, f, st0, lz->gen_e0[k], lz->gen_e0[k] + lz->gen_len[k]);
+    if (s_drawn && threadIdx.x == 0) *s_drawn += 2ull * lz->gen_len[k];
+  }
   *gen_next = k;
   if (__syncthreads_or(slow)) {
     if (threadIdx.x == 0) *s_restart = 1;
@@ -680,17 +779,17 @@ __device__ bool lazy_gen_until(const SmemT<WT> &s, const FieldConst &f, const Tp
 }
 
 template <bool PROF, typename WT>
-__device__ bool run_program(const SmemT<WT> &s, const FieldConst &f, const TpoVmInstr *code,
+__device__ __forceinline__ bool run_program(const SmemT<WT> &s, const FieldConst &f, const TpoVmInstr *code,
                             uint32_t len, int *s_flag, unsigned long long *prof,
                             const TpoVmGraph *lz = nullptr, uint64_t st0 = 0, uint32_t *gen_next = nullptr,
-                            int *s_restart = nullptr) {
+                            int *s_restart = nullptr, unsigned long long *s_drawn = nullptr) {
   uint32_t it = 0, loop_pc = 0, trips = 1;
   long long t_prev = PROF ? clock64() : 0;
   bool phase_bad = false;  // this thread saw an event since the last barrier
   for (uint32_t pc = 0; pc < len; ++pc) {
     const TpoVmInstr &I = code[pc];
     const uint8_t op = I.op;
-    if (lz && !lazy_gen_until(s, f, lz, st0, pc, gen_next, s_restart)) return false;
+    if (lz && !lazy_gen_until(s, f, lz, st0, pc, gen_next, s_restart, s_drawn)) return false;
     if (op == VM_LOOP) {
       trips = I.n;
       it = 0;
@@ -785,6 +884,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : NT == 128 ? 7 : 14) verify
 #endif
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int s_flag, s_slow, s_restart;
+  __shared__ unsigned long long s_drawn;  // draws made by this CTA (a.drawn)
   __shared__ uint32_t s_omega;
   __shared__ unsigned long long s_cand, s_key;
   __shared__ unsigned long long s_prof[32];  // PROF: [0,16) cycles per opcode, [16,32) counts
@@ -793,6 +893,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : NT == 128 ? 7 : 14) verify
   __shared__ TpoVmGraph s_g1, s_g2;
   __shared__ TpoVerdict s_v;
   if (PROF && threadIdx.x < 32) s_prof[threadIdx.x] = 0;
+  if (threadIdx.x == 0) s_drawn = 0;
   const FieldConst &f = a.field;
   SmemT<WT> s = carve<WT>(smem, f, a.code_smem_bytes);
   load_tables(s, f, a.tables);
@@ -875,32 +976,38 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : NT == 128 ? 7 : 14) verify
           omega = a.shared_meta[1];
           if (threadIdx.x == 0) s_flag = 0;
           __syncthreads();
-          ok = run_program<PROF>(s, f, ccode, g2.code_len, &s_flag, s_prof);
+          ok = true;  // the program's outputs are in place: the candidate runs below
         } else {
           // lazy sampling: omega and the tables now, each input right before
           // the program's first reader of it (an attempt the program
           // resamples early never draws the rest); the candidate needs every
           // input, so the rest is drawn before it runs
           const uint64_t st0 = derive_state(seed, stream);
+          const uint64_t table_draws = 1 + (silu ? f.p + f.q : 0);
           bool lazy = g1.n_gen > 0 && !a.eager_inputs;
           if (lazy) lazy = gen_attempt_lazy(s, f, st0, a.n_in, silu, &s_omega, omega);
           if (!lazy) omega = gen_attempt(s, f, seed, stream, a.n_in, silu, &s_slow, &s_omega);
+          if (threadIdx.x == 0) s_drawn += table_draws + (lazy ? 0 : 2ull * a.n_in);
           if (threadIdx.x == 0) s_flag = 0, s_restart = 0;
           __syncthreads();
           if (PROF && threadIdx.x == 0) s_prof[0] += (unsigned long long)(clock64() - t0), s_prof[16] += 1;
-          uint32_t gen_next = 0;
-          ok = run_program<PROF>(s, f, scode, g1.code_len, &s_flag, s_prof, lazy ? &g1 : nullptr, st0, &gen_next,
-                                 &s_restart);
-          if (lazy && ok) ok = lazy_gen_until(s, f, &g1, st0, 0xffffffffu, &gen_next, &s_restart);
-          if (lazy && s_restart) {
-            // a draw may lie in the rejection zone: the exact replay, eagerly
+          // one call site for the program (and one for the candidate below):
+          // the interpreter stays inlined; a second pass only after a lazy
+          // draw hit the rejection zone (exact replay, eagerly)
+          for (;;) {
+            uint32_t gen_next = 0;
+            ok = run_program<PROF>(s, f, scode, g1.code_len, &s_flag, s_prof, lazy ? &g1 : nullptr, st0,
+                                   &gen_next, &s_restart, &s_drawn);
+            if (lazy && ok) ok = lazy_gen_until(s, f, &g1, st0, 0xffffffffu, &gen_next, &s_restart, &s_drawn);
+            if (!lazy || !s_restart) break;
             omega = gen_attempt(s, f, seed, stream, a.n_in, silu, &s_slow, &s_omega);
+            if (threadIdx.x == 0) s_drawn += table_draws + 2ull * a.n_in;
+            lazy = false;
             if (threadIdx.x == 0) s_flag = 0;
             __syncthreads();
-            ok = run_program<PROF>(s, f, scode, g1.code_len, &s_flag, s_prof);
           }
-          ok = ok && run_program<PROF>(s, f, ccode, g2.code_len, &s_flag, s_prof);
         }
+        ok = ok && run_program<PROF>(s, f, ccode, g2.code_len, &s_flag, s_prof);
         if (!ok && (s_flag & 3) == 3) {  // Error(PoisonedExponent) escapes the verifier
           if (t0w) {
             v.kind = 3;
@@ -956,6 +1063,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : NT == 128 ? 7 : 14) verify
     }
   }
   if (PROF && threadIdx.x < 32 && a.prof) atomicAdd(a.prof + threadIdx.x, s_prof[threadIdx.x]);
+  if (threadIdx.x == 0 && a.drawn) atomicAdd(a.drawn, s_drawn);
 }
 
 // Same-seed batches: attempt (seed, stream 0) of the program, once.  The

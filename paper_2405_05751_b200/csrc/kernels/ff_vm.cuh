@@ -66,6 +66,7 @@ struct VerifyArgs {
   uint64_t shared_seed;
   uint32_t shared_len;
   int eager_inputs;              // 1: draw every input at attempt start (TPO_VM_EAGER, A/B)
+  unsigned long long *drawn;     // optional: splitmix64 draws made (inputs 2 per element, omega, SiLU tables)
 };
 
 struct EvalArgs {

@@ -22,6 +22,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <cstdlib>
+
 #include "fp_vm.cuh"
 #include "smem_limit.cuh"
 #include "vm.h"
@@ -290,7 +292,7 @@ __global__ void __launch_bounds__((TM / RM) * (TN / RN))
 #pragma unroll
       for (int i = 0; i < RM; ++i) a[i] = As[buf][kk][ty * RM + i];
 #pragma unroll
-      for (int j = 0; j < RN; ++j) b[j] = Bs[buf][kk][tx * RN + j];
+      for (int j = 0; j < RN; ++j) b[j] = Bs[buf][kk][tx + j * (TN / RN)];  // strided: conflict-free
 #pragma unroll
       for (int i = 0; i < RM; ++i)
 #pragma unroll
@@ -305,7 +307,7 @@ __global__ void __launch_bounds__((TM / RM) * (TN / RN))
   for (int i = 0; i < RM; ++i)
 #pragma unroll
     for (int j = 0; j < RN; ++j) {
-      const uint32_t m = m0 + ty * RM + i, n = n0 + tx * RN + j;
+      const uint32_t m = m0 + ty * RM + i, n = n0 + tx + j * (TN / RN);
       if (m >= M || n >= N) continue;
       T &dst = W[dbase + uint64_t(m) * N + n];
       dst = (I.flags & VM_ACCUM) ? O::add(dst, acc[i][j]) : acc[i][j];  // acc = add(acc, val)
@@ -486,6 +488,24 @@ extern "C" int tpo_fp_launch_instr(void *W, int f32, const TpoVmInstr *I, uint32
   if (I->op == VM_MATMUL && (I->flags & VM_STRIDED) && I->dims[0] * I->dims[1] * I->dims[2] * I->dims[3] <= 65535u) {
     // tiled by the matrix shape: skinny rows, medium, square
     const uint32_t M = I->dims[4];
+    static const int cfg = [] {  // experiments: skinny-tile variant
+      const char *e = std::getenv("TPO_FP_MM");
+      return e ? std::atoi(e) : 0;
+    }();
+    if (M <= 8 && cfg) {
+      if (f32) {
+        float *w = static_cast<float *>(W);
+        if (cfg == 1) tpo_fp::launch_matmul<float, 8, 128, 1, 4, 16>(w, *I, it, st);
+        else if (cfg == 2) tpo_fp::launch_matmul<float, 8, 64, 1, 2, 32>(w, *I, it, st);
+        else tpo_fp::launch_matmul<float, 8, 256, 1, 8, 16>(w, *I, it, st);
+      } else {
+        double *w = static_cast<double *>(W);
+        if (cfg == 1) tpo_fp::launch_matmul<double, 8, 128, 1, 4, 16>(w, *I, it, st);
+        else if (cfg == 2) tpo_fp::launch_matmul<double, 8, 64, 1, 2, 32>(w, *I, it, st);
+        else tpo_fp::launch_matmul<double, 8, 256, 1, 8, 8>(w, *I, it, st);
+      }
+      return int(cudaGetLastError());
+    }
     if (f32) {
       float *w = static_cast<float *>(W);
       if (M <= 8) tpo_fp::launch_matmul<float, 8, 32, 1, 1, 32>(w, *I, it, st);

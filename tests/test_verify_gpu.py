@@ -480,3 +480,47 @@ def test_attribute_mutants_verified_like_reference(ctx, fam):
         b = ref.eval_mugraph(g, ins, mode=0)
         for x, y in zip(a, b):
             assert np.allclose(x, y, rtol=1e-12, atol=1e-12, equal_nan=True)
+
+
+@pytest.mark.parametrize("fam", list(FAMS))
+def test_lazy_input_sampling_matches_eager(ctx, fam):
+    """Lazy input sampling (each input drawn right before the program's
+    first reader, TpoVmGraph::gen_*) gives the verdicts of drawing every
+    input up front (TPO_VM_EAGER=1, a fresh process) field for field, and
+    the kernel's draw counter accounts for exactly the skipped draws: eager
+    = attempts x (2 x input elements + omega [+ SiLU tables])."""
+    import json
+    import os
+    import subprocess
+    import sys
+    ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    prog, pool = FAMS[fam]
+    graphs = [g for _, g in pool]
+    n = 3000
+    lazy, att = ctx.verify_pool(prog, graphs, first=0, n=n, want_verdicts=True)
+    lazy_draws = ctx.last_verify_draws()
+    code = (
+        "import json, sys; sys.path.insert(0, %r); import numpy as np\n"
+        "from paper_2405_05751_b200 import fixtures as F\n"
+        "from paper_2405_05751_b200.api import Context\n"
+        "prog, pool = F.verify_families()[%r]\n"
+        "ctx = Context(0)\n"
+        "v, att = ctx.verify_pool(prog, [g for _, g in pool], first=0, n=%d, want_verdicts=True)\n"
+        "print(json.dumps({'att': att, 'draws': ctx.last_verify_draws(),"
+        " 'v': {c: v[c].tolist() for c in %r}}))\n" % (ROOT, fam, n, VCOLS))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, check=True,
+                       env=dict(os.environ, TPO_VM_EAGER="1"))
+    eager = json.loads(r.stdout.strip().splitlines()[-1])
+    assert eager["att"] == att
+    for c in VCOLS:
+        assert np.array_equal(np.asarray(eager["v"][c]), lazy[c]), (fam, c)
+    from paper_2405_05751_b200.graph import has_silu
+    idx = np.arange(n) % len(graphs)
+    silu = np.array([has_silu(g) or has_silu(prog) for g in graphs])[idx]
+    a = (lazy["resamples"] + lazy["rounds_run"]).astype(np.int64)
+    n_in = ctx.compile(prog).info.input_elems
+    want_eager = int(np.sum(a * (2 * n_in + 1 + (227 + 113) * silu)))
+    assert eager["draws"] == want_eager
+    assert lazy_draws <= want_eager
+    if fam == "rmsnorm":  # its program resamples at the Sqrt before the Matmul reads W
+        assert lazy_draws < 0.6 * want_eager

@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <vector>
 #include <algorithm>
+#include <array>
 #include <functional>
 #include <map>
 #include <mutex>
@@ -203,8 +204,101 @@ int pick_ksplit(int64_t ntiles, int64_t K, int ctas_per_sm) {
 
 }  // namespace
 
+namespace {
+
+// The paper's LoRA µGraph (Algorithm 1 rediscovers it,
+// tests/test_enumerate.py): kernel op T = Matmul(X, A), then ONE GraphDef
+// over (X, W, B, T) whose for-loop runs ConcatMatmul(X̄, T̄, W̄, B̄) =
+// X̄·W̄ + T̄·B̄ into one φ-Accum — i.e. X·W + (X·A)·B, the function the
+// fused LoRA kernel computes (graph inputs X, W, A, B as in the
+// single-kernel form).  Matched structurally, independent of list order
+// and tensor ids; every InIter map is checked so that the partition covers
+// exactly that function: the loop slices both contractions (X̄ / T̄ along
+// dim 1, W̄ / B̄ along dim 0, or no loop split), the grid splits either the
+// output columns (W̄, B̄, OutSaver along dim 1) or the tokens (X̄, T̄,
+// OutSaver along dim 0).
+bool match_lora_concat(const KernelGraph &g, FusedPlan &p) {
+  if (g.ops.size() != 2 || g.inputs.size() != 4 || g.outputs.size() != 1) return false;
+  const Op &mm = g.ops[0], &gd = g.ops[1];
+  if (mm.type != OpType::Matmul || gd.type != OpType::GraphDef || !gd.block) return false;
+  const TensorId X = g.inputs[0], W = g.inputs[1], A = g.inputs[2], B = g.inputs[3];
+  if (mm.inputs != std::vector<TensorId>{X, A} || mm.outputs.size() != 1) return false;
+  const TensorId T = mm.outputs[0];
+  if (gd.outputs.size() != 1 || gd.outputs[0] != g.outputs[0]) return false;
+  for (TensorId t : {X, W, A, B})
+    if (g.tensor(t).shape.rank() != 2) return false;
+  const int64_t b = g.tensor(X).shape.dims[0], h = g.tensor(X).shape.dims[1];
+  const int64_t n = g.tensor(W).shape.dims[1], r = g.tensor(A).shape.dims[1];
+  if (g.tensor(W).shape.dims[0] != h || g.tensor(A).shape.dims[0] != h || g.tensor(B).shape.dims != std::vector<int64_t>{r, n})
+    return false;
+  const BlockGraph &bg = *gd.block;
+  if (bg.grid[1] != 1 || bg.grid[2] != 1) return false;
+  const int64_t grid = bg.grid[0], fl = bg.forloop;
+  // block tensor -> role (0 X̄, 1 W̄, 2 B̄, 3 T̄) through its InIter
+  std::vector<int> role(bg.tensors.size(), -1);
+  int seen[4] = {0, 0, 0, 0}, n_in = 0, n_cm = 0, n_acc = 0, n_out = 0;
+  const Op *cm = nullptr, *acc = nullptr, *sav = nullptr;
+  const InIterAttrs *it[4] = {nullptr, nullptr, nullptr, nullptr};
+  for (const Op &o : bg.ops) {
+    switch (o.type) {
+      case OpType::InIter: {
+        const auto &a = std::get<InIterAttrs>(o.attrs);
+        if (a.operand < 0 || size_t(a.operand) >= gd.inputs.size()) return false;
+        const TensorId src = gd.inputs[size_t(a.operand)];
+        const int rl = src == X ? 0 : src == W ? 1 : src == B ? 2 : src == T ? 3 : -1;
+        if (rl < 0 || seen[rl]++) return false;
+        role[size_t(o.outputs.at(0))] = rl;
+        it[rl] = &a;
+        ++n_in;
+        break;
+      }
+      case OpType::ConcatMatmul: cm = &o, ++n_cm; break;
+      case OpType::Accum: acc = &o, ++n_acc; break;
+      case OpType::OutSaver: sav = &o, ++n_out; break;
+      default: return false;
+    }
+  }
+  if (n_in != 4 || n_cm != 1 || n_acc != 1 || n_out != 1 || cm->inputs.size() != 4) return false;
+  // ConcatMatmul(a0, a1, b0, b1) = a0·b0 + a1·b1: pairs (X̄, W̄) and (T̄, B̄)
+  std::array<int, 4> cr;
+  for (int k = 0; k < 4; ++k) cr[size_t(k)] = role[size_t(cm->inputs[size_t(k)])];
+  const bool pairs = (cr == std::array<int, 4>{0, 3, 1, 2}) || (cr == std::array<int, 4>{3, 0, 2, 1});
+  if (!pairs) return false;
+  const auto &aa = std::get<AccumAttrs>(acc->attrs);
+  if (acc->inputs.at(0) != cm->outputs.at(0) || aa.fmap.axes() != 1 || aa.fmap.targets[0] != kReplica) return false;
+  if (sav->inputs.at(0) != acc->outputs.at(0)) return false;
+  const auto &om = std::get<OutSaverAttrs>(sav->attrs).omap;
+  auto t0 = [](const DimMap &m) { return m.axes() ? m.targets[0] : kReplica; };
+  // the loop: both contractions sliced consistently, or not split at all
+  const bool loop_ok = fl == 1 || (t0(it[0]->fmap) == 1 && t0(it[3]->fmap) == 1 && t0(it[1]->fmap) == 0 &&
+                                   t0(it[2]->fmap) == 0 && h % fl == 0 && r % fl == 0);
+  // the grid: output columns (W̄, B̄, OutSaver along dim 1) or tokens
+  const bool cols = t0(it[0]->imap) == kReplica && t0(it[3]->imap) == kReplica && t0(it[1]->imap) == 1 &&
+                    t0(it[2]->imap) == 1 && t0(om) == 1;
+  const bool toks = t0(it[0]->imap) == 0 && t0(it[3]->imap) == 0 && t0(it[1]->imap) == kReplica &&
+                    t0(it[2]->imap) == kReplica && t0(om) == 0;
+  if (!loop_ok || !(cols || toks || grid == 1)) return false;
+  p.kind = TPO_FUSED_LORA;
+  p.b = b, p.h = h, p.n = n, p.r = r, p.grid = grid, p.forloop = fl;
+  return true;
+}
+
+}  // namespace
+
 FusedPlan match_fused(const KernelGraph &g) {
   FusedPlan p;
+  if (g.ops.size() == 2) {
+    try {
+      if (match_lora_concat(g, p)) {
+        if (p.r != 16 || p.n % 128 || p.h % 64) {
+          p.kind = TPO_FUSED_NONE;
+          p.why = "LoRA µGraph outside kernel limits (r==16, n%128, h%64)";
+        }
+        return p;
+      }
+    } catch (const std::exception &) {
+    }
+  }
   if (g.ops.size() != 1 || g.ops[0].type != OpType::GraphDef || !g.ops[0].block ||
       g.outputs.size() != 1) {
     p.why = "not a single-GraphDef µGraph";
@@ -226,8 +320,8 @@ FusedPlan match_fused(const KernelGraph &g) {
       in[3].dims == std::vector<int64_t>{1, 1}) {
     int64_t b = in[0].dims[0], h = in[0].dims[1], n = in[2].dims[1];
     if (same(key, {1, b, h, n, 0, grid, fl}, [&] { return rmsnorm_mugraph(b, h, n, grid, fl); })) {
-      if (b > 8 || n % 128 || h % 64) {
-        p.why = "RMSNorm µGraph outside kernel limits (b<=8, n%128, h%64)";
+      if (n % 128 || h % 64) {
+        p.why = "RMSNorm µGraph outside kernel limits (n%128, h%64)";
         return p;
       }
       p.kind = TPO_FUSED_RMSNORM_MATMUL;
@@ -238,8 +332,8 @@ FusedPlan match_fused(const KernelGraph &g) {
   if (in.size() == 3 && r2(0) && r2(1) && r2(2)) {
     int64_t b = in[0].dims[0], h = in[0].dims[1], n = in[1].dims[1];
     if (same(key, {2, b, h, n, 0, grid, fl}, [&] { return gatedmlp_mugraph(b, h, n, grid, fl); })) {
-      if (b > 8 || n % 128 || h % 64) {
-        p.why = "GatedMLP µGraph outside kernel limits (b<=8, n%128, h%64)";
+      if (n % 128 || h % 64) {
+        p.why = "GatedMLP µGraph outside kernel limits (n%128, h%64)";
         return p;
       }
       p.kind = TPO_FUSED_GATED_MLP;
@@ -263,8 +357,8 @@ FusedPlan match_fused(const KernelGraph &g) {
     int64_t b = in[0].dims[0], h = in[0].dims[1], n = in[1].dims[1], r = in[2].dims[1];
     if (same(key, {4, b, h, n, r, grid, fl}, [&] { return lora_mugraph(b, h, n, r, grid, fl); }) ||
         same(key, {5, b, h, n, r, grid, fl}, [&] { return lora_single_mugraph(b, h, n, r, grid, fl); })) {
-      if (b > 16 || r != 16 || n % 128 || h % 64) {
-        p.why = "LoRA µGraph outside kernel limits (b<=16, r==16, n%128, h%64)";
+      if (r != 16 || n % 128 || h % 64) {
+        p.why = "LoRA µGraph outside kernel limits (r==16, n%128, h%64)";
         return p;
       }
       p.kind = TPO_FUSED_LORA;
@@ -502,6 +596,28 @@ std::vector<size_t> input_elems(const FusedPlan &p) {
 }  // namespace
 
 int launch_fused(const FusedPlan &p, const FusedIO &io, cudaStream_t st) {
+  // More tokens than one kernel tile holds (8 for RMSNorm / GatedMLP, 16
+  // for LoRA): one launch per token chunk, X and the output offset by whole
+  // rows — every per-token quantity (Σx², SiLU gate, XA) is row-local, so
+  // the chunks are independent; each re-streams the weights.
+  const int64_t chunk = p.kind == TPO_FUSED_LORA ? 16 : 8;
+  if ((p.kind == TPO_FUSED_RMSNORM_MATMUL || p.kind == TPO_FUSED_GATED_MLP || p.kind == TPO_FUSED_LORA) &&
+      p.b > chunk) {
+    const size_t xel = io.dt[0] == TPO_DTYPE_BF16 ? 2 : io.dt[0] == TPO_DTYPE_F32 ? 4 : 8;
+    const size_t nin = input_elems(p).size();
+    for (int64_t c = 0; c < p.b; c += chunk) {
+      FusedPlan pc = p;
+      pc.b = std::min(chunk, p.b - c);
+      std::vector<const void *> in(io.in, io.in + nin);
+      in[0] = static_cast<const char *>(io.in[0]) + size_t(c) * size_t(p.h) * xel;
+      float *out = io.out[0] + size_t(c) * size_t(p.n);
+      FusedIO ic = io;
+      ic.in = in.data();
+      ic.out = &out;
+      if (int e = launch_fused(pc, ic, st)) return e;
+    }
+    return 0;
+  }
   const std::vector<size_t> ne = input_elems(p);
   const int n_in = int(ne.size());
   bool all_bf16 = true;

@@ -147,3 +147,20 @@ def test_candidates_valid_and_decided_by_the_reference(fam):
         v = ref.random_test_equivalence(prog, g, seed=3)
         kinds[v["kind"]] = kinds.get(v["kind"], 0) + 1
     assert kinds.get(0, 0) > 0, kinds
+
+
+def test_paper_lora_form_dispatches_to_the_fused_kernel():
+    """At the BASELINE LoRA shape the paper's ConcatMatmul µGraph, as Algorithm 1
+    emits it, is matched to the fused LoRA kernel (host-side match, CPU);
+    the other two-kernel form (T = A·B, ConcatMatmul(X̄, X̄, W̄, T̄)) computes
+    the same function another way and stays on the generic VM."""
+    prog = F.family_program("lora", 16, 4096, 4096, 16)
+    cands = api.enumerate_mugraphs(prog, grids=[32], loops=[16], max_kernel_ops=1, max_block_ops=4)
+    forms = {}
+    for g in cands:
+        if [op["type"] for op in g["ops"]] != ["matmul", "graphdef"]:
+            continue
+        if any(o["type"] == "concatmatmul" for o in g["ops"][1]["blockGraph"]["ops"]):
+            forms[tuple(g["ops"][0]["inputs"])] = api.describe(g).splitlines()[-1]
+    assert "fused sm_100a kernel lora" in forms[(0, 2)]
+    assert "no fused kernel" in forms[(2, 3)]

@@ -227,3 +227,47 @@ def test_attribute_mutants_take_the_right_path(ctx, name):
         assert np.array_equal(np.isfinite(o), fin)
         scale = max(np.sqrt(np.mean(r[fin] ** 2)), 1e-30) if fin.any() else 1.0
         assert np.max(np.abs(o[fin] - r[fin]), initial=0.0) <= 1e-3 * scale + 1e-3 * np.max(np.abs(r[fin]), initial=0.0)
+
+
+@pytest.mark.parametrize("args", [(16, 512, 256, 16), (9, 1024, 512, 16)])
+def test_paper_lora_concat_form_runs_fused(ctx, args):
+    """The paper's LoRA µGraph — kernel T = Matmul(X, A),
+    then one GraphDef running ConcatMatmul(X̄, T̄, W̄, B̄) into a φ-Accum —
+    as Algorithm 1 emits it from the flat program, dispatches to the fused
+    LoRA kernel and meets the tolerance against the reference's
+    eval_mugraph of that same µGraph."""
+    from paper_2405_05751_b200 import api
+    b, h, n, r = args
+    prog = F.family_program("lora", b, h, n, r)
+    cands = api.enumerate_mugraphs(prog, grids=[n // 128], loops=[4], max_kernel_ops=1, max_block_ops=4)
+    paper = [g for g in cands if [op["type"] for op in g["ops"]] == ["matmul", "graphdef"]
+             and g["ops"][0]["inputs"] == [0, 2]
+             and any(o["type"] == "concatmatmul" for o in g["ops"][1]["blockGraph"]["ops"])]
+    assert paper
+    g = ctx.compile(paper[0])
+    assert g.fused == "lora", g.fused
+    ins = make_inputs("lora", args, seed=5)
+    out = ctx.eval_mugraph(g, [x.cuda() for x in ins])[0]
+    torch.cuda.synchronize()
+    want = ref.eval_mugraph(paper[0], [x.float().numpy() for x in ins])[0]
+    check(out.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("name,args", [("gatedmlp", (20, 512, 256)), ("rmsnorm", (19, 512, 256)),
+                                       ("lora", (40, 512, 256, 16))])
+def test_more_tokens_than_a_tile_run_fused_in_chunks(ctx, name, args):
+    """Token counts beyond one kernel tile (8, LoRA 16) run the fused kernel
+    once per token chunk (ragged last chunk included), bf16 and fp64 (SPLIT)
+    inputs alike, within the tolerance against the reference."""
+    mu = F.family_mugraph(name, *args, grid=2, forloop=4)
+    g = ctx.compile(mu)
+    assert g.fused == name
+    ins = make_inputs(name, args, seed=7)
+    want = ref.eval_mugraph(mu, [x.float().numpy() for x in ins])[0]
+    out = ctx.eval_mugraph(g, [x.cuda() for x in ins])[0].cpu().numpy()
+    check(out, want)
+    rng = np.random.default_rng(3)
+    d = [rng.standard_normal(tuple(x.shape)) * (float(x.float().std()) if x.numel() > 1 else 1.0) for x in ins]
+    if name == "rmsnorm":
+        d[3] = np.full((1, 1), 1.0 / args[1])
+    check(ctx.eval_mugraph_f64(g, d)[0], ref.eval_mugraph(mu, d)[0])

@@ -1026,12 +1026,20 @@ class Lowerer {
       i.qd = q;
       bqd[size_t(to)] = q;
       if (to_acc) acc_fused[size_t(acc)] = 1;
-      if (field_ && to_acc && bg.forloop > 1 && int64_t(i.a_iter) == K * i.sa[5] &&
+      static const bool fp_hoist = [] {  // experiments: TPO_VM_FP_HOIST=0 keeps fp matmuls in the loop
+        const char *e = std::getenv("TPO_VM_FP_HOIST");
+        return !(e && e[0] == '0');
+      }();
+      if ((field_ || fp_hoist) && to_acc && bg.forloop > 1 && int64_t(i.a_iter) == K * i.sa[5] &&
           int64_t(i.b_iter) == K * i.sb[5] && K * bg.forloop <= INT32_MAX) {
         // both operands walk one k tile per iteration: the loop is just the
-        // continuation of the k sum — one Matmul over K·forloop after it
+        // continuation of the k sum — one Matmul over K·forloop after it.
+        // Field sums reassociate freely; fp keeps the reference's order:
+        // each iteration's K-segment sum is added to the accumulator in
+        // iteration order (kseg, kernels/vm.h)
         i.dims[5] = uint32_t(K * bg.forloop);
         i.a_iter = i.b_iter = 0;
+        if (!field_) i.kseg = uint32_t(K);
         hoisted.push_back(i);
         return;
       }

@@ -162,14 +162,19 @@ __device__ __forceinline__ void exec_instr(T *W, const TpoVmInstr &I, uint32_t i
                       int64_t(gy) * I.sb[1] + int64_t(gz) * I.sb[2] + int64_t(bi) * I.sb[3] +
                       int64_t(c) * snb;
         const uint64_t dbase = uint64_t(I.dst) + ((uint64_t(blk) * Bi + bi) * M + m) * N + c;
+        const uint32_t seg = I.kseg ? I.kseg : K;
         for (uint32_t j = 0; j < tm * tm; ++j) {
           const uint32_t dm = j / tm, dc = j % tm;
-          T acc = T(0);
-          for (uint32_t k = 0; k < K; ++k)
-            acc = O::add(acc, O::mul(pa[int64_t(k) * ska + int64_t(dm) * sma],
-                                     pb[int64_t(k) * skb + int64_t(dc) * snb]));
           T &dst = W[dbase + uint64_t(dm) * N + dc];
-          dst = (I.flags & VM_ACCUM) ? O::add(dst, acc) : acc;  // acc = add(acc, val)
+          T tot = (I.flags & VM_ACCUM) ? dst : T(0);
+          for (uint32_t k0 = 0; k0 < K; k0 += seg) {  // one segment per hoisted loop iteration
+            T acc = T(0);
+            for (uint32_t k = k0; k < k0 + seg && k < K; ++k)
+              acc = O::add(acc, O::mul(pa[int64_t(k) * ska + int64_t(dm) * sma],
+                                       pb[int64_t(k) * skb + int64_t(dc) * snb]));
+            tot = (I.flags & VM_ACCUM) || k0 ? O::add(tot, acc) : acc;  // acc = add(acc, val)
+          }
+          dst = tot;
         }
       }
       break;
@@ -274,11 +279,20 @@ __global__ void __launch_bounds__((TM / RM) * (TN / RN))
       if (e < TK * TN) Bs[buf][e / TN][e % TN] = rb[l];
     }
   };
-  T acc[RM][RN];
+  // kseg (hoisted loop): tot = add(tot, segment sum) every kseg k, in order
+  const uint32_t seg = I.kseg ? I.kseg : K;
+  const bool accum = I.flags & VM_ACCUM;
+  const uint64_t dbase0 = uint64_t(I.dst) + uint64_t(mat) * M * N;
+  T acc[RM][RN], tot[RM][RN];
 #pragma unroll
   for (int i = 0; i < RM; ++i)
 #pragma unroll
-    for (int j = 0; j < RN; ++j) acc[i][j] = T(0);
+    for (int j = 0; j < RN; ++j) {
+      acc[i][j] = T(0);
+      const uint32_t m = m0 + ty * RM + i, n = n0 + tx + j * (TN / RN);
+      tot[i][j] = (accum && m < M && n < N) ? W[dbase0 + uint64_t(m) * N + n] : T(0);
+    }
+  uint32_t kin = 0;  // k index within the current segment
   load(0);
   store(0);
   __syncthreads();
@@ -297,20 +311,29 @@ __global__ void __launch_bounds__((TM / RM) * (TN / RN))
       for (int i = 0; i < RM; ++i)
 #pragma unroll
         for (int j = 0; j < RN; ++j) acc[i][j] = O::add(acc[i][j], O::mul(a[i], b[j]));
+      if (++kin == seg) {  // segment complete: into the running total, in order
+        kin = 0;
+        const bool first = !accum && k0 + kk + 1 == seg;
+#pragma unroll
+        for (int i = 0; i < RM; ++i)
+#pragma unroll
+          for (int j = 0; j < RN; ++j) {
+            tot[i][j] = first ? acc[i][j] : O::add(tot[i][j], acc[i][j]);
+            acc[i][j] = T(0);
+          }
+      }
     }
     if (more) store(buf ^ 1);
     __syncthreads();
     buf ^= 1;
   }
-  const uint64_t dbase = uint64_t(I.dst) + uint64_t(mat) * M * N;
 #pragma unroll
   for (int i = 0; i < RM; ++i)
 #pragma unroll
     for (int j = 0; j < RN; ++j) {
       const uint32_t m = m0 + ty * RM + i, n = n0 + tx + j * (TN / RN);
       if (m >= M || n >= N) continue;
-      T &dst = W[dbase + uint64_t(m) * N + n];
-      dst = (I.flags & VM_ACCUM) ? O::add(dst, acc[i][j]) : acc[i][j];  // acc = add(acc, val)
+      W[dbase0 + uint64_t(m) * N + n] = tot[i][j];  // every segment folded in (K % seg == 0)
     }
 }
 
@@ -488,6 +511,15 @@ extern "C" int tpo_fp_launch_instr(void *W, int f32, const TpoVmInstr *I, uint32
   if (I->op == VM_MATMUL && (I->flags & VM_STRIDED) && I->dims[0] * I->dims[1] * I->dims[2] * I->dims[3] <= 65535u) {
     // tiled by the matrix shape: skinny rows, medium, square
     const uint32_t M = I->dims[4];
+    // tiny outputs (e.g. LoRA's grid-invariant X·A, 16 x 16 over K = 4096):
+    // one output per thread, so the k-ordered chains run on 256 threads
+    // instead of a few
+    const uint32_t N = I->dims[6];
+    if (M <= 16 && N <= 16) {
+      if (f32) tpo_fp::launch_matmul<float, 16, 16, 1, 1, 32>(static_cast<float *>(W), *I, it, st);
+      else tpo_fp::launch_matmul<double, 16, 16, 1, 1, 32>(static_cast<double *>(W), *I, it, st);
+      return int(cudaGetLastError());
+    }
     static const int cfg = [] {  // experiments: skinny-tile variant
       const char *e = std::getenv("TPO_FP_MM");
       return e ? std::atoi(e) : 0;

@@ -77,7 +77,11 @@ struct TpoVmInstr {
   // grid-major evaluation reaches the raising op before any later block);
   // 0 = every index counts
   uint32_t b0n;
-  uint32_t pad3;               // 192 bytes: copied to shared memory as uint4
+  // fp MATMUL hoisted out of the for-loop (VM_ACCUM, K = the loop's whole
+  // contraction): the reference adds each iteration's k-segment sum to the
+  // accumulator, acc = add(acc, Σ_{k in segment} a·b), so the executors sum
+  // every `kseg` consecutive k (ascending) before adding; 0 = one segment
+  uint32_t kseg;               // 192 bytes: copied to shared memory as uint4
 };
 
 // Host helper: the (mul, shift) pair of divisor d >= 1 (CUTLASS-style

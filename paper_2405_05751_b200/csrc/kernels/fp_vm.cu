@@ -520,24 +520,6 @@ extern "C" int tpo_fp_launch_instr(void *W, int f32, const TpoVmInstr *I, uint32
       else tpo_fp::launch_matmul<double, 16, 16, 1, 1, 32>(static_cast<double *>(W), *I, it, st);
       return int(cudaGetLastError());
     }
-    static const int cfg = [] {  // experiments: skinny-tile variant
-      const char *e = std::getenv("TPO_FP_MM");
-      return e ? std::atoi(e) : 0;
-    }();
-    if (M <= 8 && cfg) {
-      if (f32) {
-        float *w = static_cast<float *>(W);
-        if (cfg == 1) tpo_fp::launch_matmul<float, 8, 128, 1, 4, 16>(w, *I, it, st);
-        else if (cfg == 2) tpo_fp::launch_matmul<float, 8, 64, 1, 2, 32>(w, *I, it, st);
-        else tpo_fp::launch_matmul<float, 8, 256, 1, 8, 16>(w, *I, it, st);
-      } else {
-        double *w = static_cast<double *>(W);
-        if (cfg == 1) tpo_fp::launch_matmul<double, 8, 128, 1, 4, 16>(w, *I, it, st);
-        else if (cfg == 2) tpo_fp::launch_matmul<double, 8, 64, 1, 2, 32>(w, *I, it, st);
-        else tpo_fp::launch_matmul<double, 8, 256, 1, 8, 8>(w, *I, it, st);
-      }
-      return int(cudaGetLastError());
-    }
     if (f32) {
       float *w = static_cast<float *>(W);
       if (M <= 8) tpo_fp::launch_matmul<float, 8, 32, 1, 1, 32>(w, *I, it, st);

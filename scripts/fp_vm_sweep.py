@@ -2,7 +2,7 @@
 """Generic fp VM (global-memory executor) on the four BASELINE µGraphs:
 device ms per evaluation (fp64 mode 0, fp32 mode 2; inputs already in one
 flat device buffer) and the HBM fraction of the unique input + output bytes.
-  TPO_FP_MM=<cfg> python scripts/fp_vm_sweep.py      (GPU box)"""
+  python scripts/fp_vm_sweep.py      (GPU box)"""
 import ctypes as C
 import os
 import sys
@@ -44,4 +44,4 @@ for name in ("gatedmlp", "rmsnorm", "lora", "gqa"):
         ms = e0.elapsed_time(e1) / 5
         nb = flat.numel() * flat.element_size() + n_out * out.element_size()
         print(f"{name:9s} {'f64' if mode == 0 else 'f32'} {ms:8.3f} ms  {nb / ms / 1e6:8.1f} GB/s  "
-              f"frac {nb / ms / 1e6 / peak:.3f}  cfg {os.environ.get('TPO_FP_MM', '0')}", flush=True)
+              f"frac {nb / ms / 1e6 / peak:.3f}", flush=True)

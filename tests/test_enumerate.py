@@ -164,3 +164,33 @@ def test_paper_lora_form_dispatches_to_the_fused_kernel():
             forms[tuple(g["ops"][0]["inputs"])] = api.describe(g).splitlines()[-1]
     assert "fused sm_100a kernel lora" in forms[(0, 2)]
     assert "no fused kernel" in forms[(2, 3)]
+
+
+def test_paper_lora_form_match_checks_the_partition():
+    """The structural LoRA match checks every InIter map: the same µGraph
+    with the loop split removed from one contraction (T̄ not walked by the
+    for-loop) computes a different function and is not sent to the fused
+    kernel; neither is one whose ConcatMatmul pairs X̄ with B̄."""
+    import copy
+    prog = F.family_program("lora", 16, 4096, 4096, 16)
+    cands = api.enumerate_mugraphs(prog, grids=[32], loops=[16], max_kernel_ops=1, max_block_ops=4)
+    paper = [g for g in cands if [op["type"] for op in g["ops"]] == ["matmul", "graphdef"]
+             and g["ops"][0]["inputs"] == [0, 2]
+             and any(o["type"] == "concatmatmul" for o in g["ops"][1]["blockGraph"]["ops"])][0]
+    assert "fused sm_100a kernel lora" in api.describe(paper).splitlines()[-1]
+    bad = copy.deepcopy(paper)
+    bg = bad["ops"][1]["blockGraph"]
+    t_operand = bad["ops"][1]["inputs"].index(bad["ops"][0]["outputs"][0])
+    for o in bg["ops"]:
+        if o["type"] == "initer" and o["attrs"]["operand"] == t_operand:
+            o["attrs"]["fmap"] = {"i": "phi"}
+    assert "fused sm_100a kernel" not in api.describe(bad).splitlines()[-1]
+    swapped = copy.deepcopy(paper)
+    for o in swapped["ops"][1]["blockGraph"]["ops"]:
+        if o["type"] == "concatmatmul":
+            o["inputs"] = [o["inputs"][0], o["inputs"][1], o["inputs"][3], o["inputs"][2]]
+    try:
+        line = api.describe(swapped).splitlines()[-1]
+    except Exception:  # the swapped pairing no longer shape-checks
+        line = ""
+    assert "fused sm_100a kernel" not in line

@@ -896,8 +896,17 @@ def cpu_baseline_verify(n=10000):
         _, ms = ref.verify_batch(prog, [g for _, g in pool], 0, n // 4, threads=threads, want=False)
         total_ms += ms
         cnt += n // 4
+    # one thread as well ("Also report 1-thread"): a smaller
+    # stratified sample, 100 candidates per family
+    one_ms, one_cnt = 0.0, 0
+    for f, (prog, pool) in fams.items():
+        _, ms = ref.verify_batch(prog, [g for _, g in pool], 0, 100, threads=1, want=False)
+        one_ms += ms
+        one_cnt += 100
     return {"value": round(cnt / (total_ms / 1e3), 1), "unit": "candidates/s", "cores": threads,
             "kind": "reference",
+            "one_thread": {"value": round(one_cnt / (one_ms / 1e3), 1), "unit": "candidates/s",
+                           "sample": f"{one_cnt} candidates, 100 per family (indices 0..99, seed i)"},
             "sample": f"{cnt} candidates, stratified: {n // 4} per family (indices 0..{n // 4 - 1}, "
                       f"every pool member ~{n // 4 // 45}x, seed i), the same pools, "
                       f"random_test_equivalence on {threads} threads"}

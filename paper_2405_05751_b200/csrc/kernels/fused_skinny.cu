@@ -675,33 +675,13 @@ __global__ void __launch_bounds__(kThreads, MINB)
       }
     }
     if (mine && !atomic_epi && !(p.dbg_flags & 1)) {
-      float *o = acc;  // outputs in place (GatedMLP reads acc[8 + tk] before any is overwritten)
 #pragma unroll
       for (int tk = 0; tk < T; ++tk) {
-        if (MODE == MODE_GATED) o[tk] = silu(acc[tk]) * acc[8 + tk];
-        else if (MODE == MODE_RMS) o[tk] = acc[tk] * post[tk];
-      }
-      if (rows_per >= 32 && !(p.dbg_flags & 32)) {
-        // the warp owns 32 consecutive output columns: transpose through the
-        // drained pipeline stages (every TMA load has landed and every MMA
-        // completed) so each lane stores whole 16-byte column quads of a
-        // token — 4x fewer store instructions than one float per column,
-        // which queue behind the next evaluation's TMA traffic
-        float *tile = reinterpret_cast<float *>(stages) + q * 32 * T;  // [T][32]
-#pragma unroll
-        for (int tk = 0; tk < T; ++tk) tile[tk * 32 + lane] = o[tk];
-        __syncwarp();
-#pragma unroll
-        for (int i = lane; i < T * 8; i += 32) {
-          const int tk = i >> 3, c4 = (i & 7) * 4;
-          if (tk < p.tokens)
-            *reinterpret_cast<float4 *>(p.out + size_t(tk) * p.N + n0 + q * 32 + c4) =
-                *reinterpret_cast<const float4 *>(tile + tk * 32 + c4);
-        }
-      } else {
-#pragma unroll
-        for (int tk = 0; tk < T; ++tk)
-          if (tk < p.tokens) p.out[size_t(tk) * p.N + n] = o[tk];
+        float o;
+        if (MODE == MODE_GATED) o = silu(acc[tk]) * acc[8 + tk];
+        else if (MODE == MODE_RMS) o = acc[tk] * post[tk];
+        else o = acc[tk];
+        if (tk < p.tokens) p.out[size_t(tk) * p.N + n] = o;
       }
       if (lane == 0 && (S == 1 || q == int(rank) * (4 / S))) TPO_T(11);
     }

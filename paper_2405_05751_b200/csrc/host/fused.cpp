@@ -729,16 +729,17 @@ int launch_fused(const FusedPlan &p, const FusedIO &io, cudaStream_t st) {
   } else if (p.kind == TPO_FUSED_LORA) {
     mode = MODE_LORA;
     sp.ksplit = pick_ksplit(p.n / 128, p.h, 1);
-    const int abox = tpo_skinny_lora_a_box_cols();  // A box [64 k][abox r]
+    const int abox = 16;  // A box [64 k][16 r]
     if (split) {  // W hi, W lo | X rows (hi 0-15, lo 16-31) | A hi, A lo | fp32 B
       const void *xs = cv.rows(0, 1, size_t(p.b), size_t(p.h), 16);
       auto w = cv.planes(1, ne[1]);
       auto a = cv.planes(2, ne[2]);
-      sp.lora_b_f32 = cv.f32(3, ne[3]);
+      auto b = cv.planes(3, ne[3]);  // B̄ hi, lo: the tensor-core fold's A operand
       if (cv.err) return cv.err;
       ok = tmap_2d(&maps[0], w.first, p.h, p.n, 64, 64, SW) && tmap_2d(&maps[1], w.second, p.h, p.n, 64, 64, SW) &&
            tmap_2d(&maps[2], xs, 32, p.h, 64, 32, SW) && tmap_2d(&maps[3], a.first, p.h, p.r, abox, 64, NOSW) &&
-           tmap_2d(&maps[6], a.second, p.h, p.r, abox, 64, NOSW);
+           tmap_2d(&maps[6], a.second, p.h, p.r, abox, 64, NOSW) &&
+           tmap_2d(&maps[4], b.first, p.r, p.n, 64, 16, SW) && tmap_2d(&maps[5], b.second, p.r, p.n, 64, 16, SW);
     } else {
       if (cv.err) return cv.err;
       ok = tmap_2d(&maps[0], in[1], p.h, p.n, 64, 64, SW) && tmap_2d(&maps[2], in[0], p.b, p.h, 64, 16, SW) &&
@@ -746,7 +747,6 @@ int launch_fused(const FusedPlan &p, const FusedIO &io, cudaStream_t st) {
       maps[1] = maps[0];
       sp.x = static_cast<const __nv_bfloat16 *>(in[0]);
       sp.lora_a = static_cast<const __nv_bfloat16 *>(in[2]);
-      sp.lora_b = static_cast<const __nv_bfloat16 *>(in[3]);
     }
   } else {
     return int(cudaErrorNotSupported);
@@ -754,8 +754,12 @@ int launch_fused(const FusedPlan &p, const FusedIO &io, cudaStream_t st) {
   if (!ok) return int(cudaErrorInvalidValue);
   for (int i = 4; i < 7; ++i)  // unused plane maps: any valid map
     if (!split) maps[i] = maps[0];
-  if (split && mode != MODE_GATED) maps[4] = maps[5] = maps[0];
+  if (split && mode == MODE_RMS) maps[4] = maps[5] = maps[0];
   if (split && mode != MODE_LORA) maps[6] = maps[0];
+  // bf16 LoRA: B̄ [r][n] for the tensor-core fold of XA_s·B̄ (box [16 r][64 n];
+  // SPLIT: its hi / lo planes, maps 4 and 5)
+  if (!split && mode == MODE_LORA && !tmap_2d(&maps[4], in[3], p.r, p.n, 64, 16, SW))
+    return int(cudaErrorInvalidValue);
   sp.N = int(p.n);
   sp.K = int(p.h);
   sp.tokens = int(p.b);

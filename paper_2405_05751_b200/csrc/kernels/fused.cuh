@@ -16,9 +16,7 @@ struct SkinnyParams {
   const __nv_bfloat16 *g;    // RMS: G [1, K]
   const __nv_bfloat16 *dscale;  // RMS: D [1, 1]
   const __nv_bfloat16 *lora_a;  // LoRA: A [K, 16]
-  const __nv_bfloat16 *lora_b;  // LoRA: B [16, N]
   const float *dscale_f32;   // SPLIT RMS: D [1, 1] fp32
-  const float *lora_b_f32;   // SPLIT LoRA: B [16, N] fp32
   float *out;                // [tokens, N] fp32
   unsigned long long *dbg;   // optional per-CTA phase timestamps (TPO_DEBUG_TIMES)
   int dbg_flags;             // experiments (TPO_DBG_FLAGS): 1 skip finalize
@@ -38,10 +36,9 @@ struct GqaParams {
   int consume_order;         // ring filled K_0, K_1, V_0, K_2, V_1, ... (the MMA issue order)
 };
 
-// maps: {W plane 0, W plane 1, X, A / G, W plane 2, W plane 3, A lo plane}
+// maps: {W plane 0, W plane 1, X, A / G, W plane 2 | LoRA B̄ (hi), W plane 3 | LoRA B̄ lo, A lo plane}
 extern "C" int tpo_skinny_launch(int mode, int stages, int minb, int split, const CUtensorMap *maps,
                                  const SkinnyParams *p, cudaStream_t st);
-extern "C" int tpo_skinny_lora_a_box_cols();
 extern "C" size_t tpo_skinny_smem(int mode, int stages, int minb, int split, const SkinnyParams *p);
 extern "C" int tpo_gqa_launch(int slots, int minb, int split, const CUtensorMap *maps,
                               const GqaParams *p, cudaStream_t st);

@@ -53,7 +53,8 @@ constexpr int kThreads = 192;
 //   [W boxes: NP planes x 2 x 8 KB] [B operand tile] [RMS: raw X, G | LoRA: A box(es)]
 // GATED / LoRA: the B operand tile (X^T, K-major, 128-B swizzle) is a TMA box.
 // LoRA: the stage also carries the A box [64 k][16 r]; the epilogue warps
-// fold it into this CTA's XA partial (warp MMA) and release the stage.
+// fold it into this CTA's XA partial (warp MMA) and release the stage; after
+// the last k block XA_s·B̄ joins the accumulator as two more UMMAs (kFold*).
 // RMS: TMA brings raw X and G; the four epilogue warps build the B tile
 // (x·g as bf16 hi + lo rows) in place while the stage's W boxes land, and
 // release it to the MMA issuer per stage (b_full).
@@ -74,33 +75,20 @@ struct Cfg {
   static constexpr int kTokN = MODE == MODE_LORA && SPLIT ? 32 : 16;  // UMMA N
   static constexpr uint32_t kXTileB = kTokN * 128;        // B operand tile bytes
   static constexpr bool kTmaX = MODE != MODE_RMS;        // per-stage B tile via TMA
-  // LoRA XA: by default the epilogue warps' mma.sync from the ring stage
-  // (kXaRing).  TPO_LORA_XA_MMA (experiment, measured slower: 10.7 vs 8.35
-  // us per evaluation — the second M = 128 UMMA per k step doubles the
-  // MMA time in every stage's turnaround, profiles/r02/lora_xa.txt) puts
-  // XA on the tensor cores: the stage then leads with the X^T
-  // tile (the XA MMA's A operand: rows 16.. of its M = 128 fall on the W
-  // boxes that follow, garbage TMEM lanes never read), then the W boxes,
-  // then the A box(es) as two [64 k][8 r] boxes per plane (the XA MMA's
-  // B operand: MN-major, no swizzle)
-#ifdef TPO_LORA_XA_MMA
-  static constexpr bool kXaMma = MODE == MODE_LORA;
-#else
-  static constexpr bool kXaMma = false;
-#endif
-  static constexpr bool kXaRing = MODE == MODE_LORA && !kXaMma;
+  // LoRA XA on the epilogue warps' mma.sync from the ring stage (measured
+  // against XA as a second M = 128 UMMA per k step: 10.7 vs 8.35 us per
+  // evaluation, profiles/r02/lora_xa.txt — it doubles the MMA time in every
+  // stage's turnaround; removed)
+  static constexpr bool kXaRing = MODE == MODE_LORA;
   static constexpr int kNABox = SPLIT ? 2 : 1;             // LoRA A planes
   static constexpr uint32_t kABox = 2048;                  // LoRA A per plane [64 k][16 r]
-  static constexpr uint32_t kAOff = kXaMma ? kXTileB : 0;  // W boxes
-  static constexpr uint32_t kBOff = kXaMma ? 0 : kAOff + NP * 2 * kWBox;  // B operand (X^T) tile
+  static constexpr uint32_t kAOff = 0;                     // W boxes
+  static constexpr uint32_t kBOff = kAOff + NP * 2 * kWBox;  // B operand (X^T) tile
   static constexpr uint32_t kXRawBytes = SPLIT ? 2048 : 1024;  // RMS X box [8][64] (fp32 | bf16)
   static constexpr uint32_t kGBytes = SPLIT ? 256 : 128;       // RMS G box [64]
   static constexpr uint32_t kXRawOff = kBOff + kXTileB;    // RMS raw X
   static constexpr uint32_t kGOff = kXRawOff + kXRawBytes; // RMS G
-  static constexpr uint32_t kLAOff = kXaMma ? kAOff + NP * 2 * kWBox : kBOff + kXTileB;  // LoRA A box(es)
-  static constexpr uint32_t kXaCol = kTokN;                // LoRA TMEM columns of XA^T (kXaMma)
-  // TMEM columns: GatedMLP two accumulators, LoRA (kXaMma) acc + XA^T
-  static constexpr uint32_t kTmemCols = kXaMma && kTokN == 32 ? 64 : 32;  // SPLIT LoRA: acc 0-31, XA 32-47
+  static constexpr uint32_t kLAOff = kBOff + kXTileB;      // LoRA A box(es)
   static constexpr uint32_t kStage = MODE == MODE_RMS               ? kGOff + 1024
                                      : MODE == MODE_LORA              ? kLAOff + kNABox * kABox
                                                                       : kBOff + kXTileB;
@@ -109,6 +97,16 @@ struct Cfg {
   static constexpr int kSide = MODE == MODE_RMS ? 8 : 0;  // RMS: Σx² per token, exchanged
   // stage releases: the UMMA commit, plus (LoRA) the four epilogue warps
   static constexpr uint32_t kEmptyCount = kXaRing ? 5 : 1;
+  // LoRA: XA_s·B̄ folded into the accumulator on the tensor cores — after
+  // the last k block the MMA issuer adds B̄ (TMA, [16 r][128 n], MN-major
+  // like W; SPLIT: hi and lo planes) times XA_s^T (written by the XA warps
+  // as bf16 hi + lo, K-major) as 2 (SPLIT 4) more K = 16 UMMAs into the hi
+  // token columns, staged in the ring's next stage (free by then).
+  // Replaces 256 FMAs per epilogue thread on the tail (8.36 -> 8.30 us per
+  // evaluation, A/B on one box).
+  static constexpr int kFoldPlanes = SPLIT ? 2 : 1;
+  // stage offsets: B̄ boxes (2 x 2 KB per plane), XA_s^T tile (2 KB)
+  static constexpr uint32_t kFoldB = 0, kFoldX = kFoldPlanes * 4096;
 
   static_assert(kStage % 1024 == 0, "stages must keep the 1024-B swizzle alignment");
 };
@@ -118,6 +116,7 @@ constexpr int kMaxStages = 12;
 struct __align__(8) Bars {
   uint64_t full[kMaxStages], empty[kMaxStages], xg_full[kMaxStages], b_full[kMaxStages];
   uint64_t tmem_full, recv, recv_side, xa_full;
+  uint64_t xb_full, xa_ready;  // LoRA fold: B̄ landed; XA_s^T tile written
   uint32_t tmem_base;
 };
 
@@ -161,8 +160,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
   // red: [S-1 peers][NV/4][rows_per][4] incoming row partials (peer slot:
   // its rank, minus one above the owner's own)
   float *side = red + (S > 1 ? (S - 1) * (kTileN / S) * 16 : 0);
-  float *xa_tot = side + S * kSide;         // side: [S][kSide]; xa_tot: LoRA [16][16] (this CTA)
-  float *xa_w = xa_tot + (MODE == MODE_LORA ? 256 : 0);  // LoRA XA-ring path: per-warp partials [4][16][16]
+  float *xa_w = side + S * kSide;  // side: [S][kSide]; xa_w: LoRA per-warp XA partials [4][16][16]
   Bars *bars = reinterpret_cast<Bars *>(xa_w + (C::kXaRing ? 1024 : 0));
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -188,6 +186,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
       mbar_init(&bars->b_full[s], 4);
     }
     mbar_init(&bars->tmem_full, 1);
+    mbar_init(&bars->xb_full, 1);
+    mbar_init(&bars->xa_ready, 4);
     mbar_init(&bars->recv, 1);
     mbar_init(&bars->recv_side, 1);
     mbar_init(&bars->xa_full, 1);
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
     if (MODE != MODE_GATED) tma_prefetch(&tmA);
     if (MODE == MODE_LORA && SPLIT) tma_prefetch(&tmA1);
   }
-  if (warp == 1) tmem_alloc<C::kTmemCols>(&bars->tmem_base);
+  if (warp == 1) tmem_alloc<32>(&bars->tmem_base);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -217,19 +217,9 @@ __global__ void __launch_bounds__(kThreads, MINB)
   // producer issues the W (and LoRA A) boxes of the first pipeline stages,
   // then waits; X is read only after the wait.
   // LoRA A box(es) of k block k0 into stage st: [64 k][16 r] per plane
-  // (XA-ring path) or two [64 k][8 r] boxes per plane (kXaMma: 16-byte rows,
-  // i.e. UMMA no-swizzle core matrices; r 0-7 at +0, r 8-15 at +1 KB)
   auto lora_a = [&](uint8_t *st, uint64_t *bar, int k0) {
 #pragma unroll
-    for (int h = 0; h < C::kNABox; ++h) {
-      const CUtensorMap *m = h ? &tmA1 : &tmA;
-      if (C::kXaMma) {
-        tma_load_2d(st + C::kLAOff + h * C::kABox, m, bar, 0, k0);
-        tma_load_2d(st + C::kLAOff + h * C::kABox + 1024, m, bar, 8, k0);
-      } else {
-        tma_load_2d(st + C::kLAOff + h * C::kABox, m, bar, 0, k0);
-      }
-    }
+    for (int h = 0; h < C::kNABox; ++h) tma_load_2d(st + C::kLAOff + h * C::kABox, h ? &tmA1 : &tmA, bar, 0, k0);
   };
   const int npre_max = (nkb < STAGES ? nkb : STAGES) - p.pre_cut;
   const int npre = p.prefetch_static ? (npre_max > 0 ? npre_max : 0) : 0;
@@ -315,6 +305,18 @@ __global__ void __launch_bounds__(kThreads, MINB)
         // k blocks before the last issue (one thread triggers the CTA)
         if (p.trig_early > 0 && kb == nkb - 1 - p.trig_early) pdl_launch();
       }
+      if (C::kXaRing) {  // B̄ (static) into the stage after the last k block's, once it drains
+        const int s = nkb % STAGES;
+        mbar_wait(&bars->empty[s], ((nkb / STAGES) & 1) ^ 1);
+        uint8_t *st = stages + s * C::kStage;
+        mbar_expect_tx(&bars->xb_full, C::kFoldPlanes * 4096);
+#pragma unroll
+        for (int h = 0; h < C::kFoldPlanes; ++h) {
+          const CUtensorMap *m = h ? &tmW3 : &tmW2;
+          tma_load_2d(st + C::kFoldB + h * 4096, m, &bars->xb_full, n0, 0);
+          tma_load_2d(st + C::kFoldB + h * 4096 + 2048, m, &bars->xb_full, n0 + 64, 0);
+        }
+      }
       TPO_T(10);
     }
     __syncwarp();
@@ -322,8 +324,6 @@ __global__ void __launch_bounds__(kThreads, MINB)
   } else if (warp == 1) {
     // -------------------------------------------------------- MMA issuer
     constexpr uint32_t idesc = idesc_bf16(kTileN, C::kTokN, /*a MN-major*/ true, /*b K-major*/ false);
-    // LoRA XA: M = 128 (tokens, padded), N = 16 (r); a K-major, b MN-major
-    constexpr uint32_t xa_idesc = idesc_bf16(128, 16, false, true);
     for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % STAGES;
       mbar_wait(&bars->full[s], (kb / STAGES) & 1);
@@ -353,25 +353,32 @@ __global__ void __launch_bounds__(kThreads, MINB)
             const uint64_t adesc = sdesc_sw128(smem_u32(wt + w * 2 * kWBox) + kk * 16 * 128, kWBox, 1024);
             umma_bf16(tmem + acc * C::kTokN, adesc, bdesc, idesc, (kb | kk) != 0 || (SPLIT && (w & 1)));
           }
-          if (C::kXaMma) {
-            // XA[t, r] += X[t, k] A[k, r]: A operand = the X^T tile as an
-            // M = 128 K-major operand (rows t >= 16 (SPLIT 32) read the W
-            // boxes behind it: garbage TMEM lanes, never read); B operand =
-            // the A box, N = 16, MN-major without swizzle (core matrix = 8 k
-            // rows x 16 B of r: LBO 128 B along k, SBO 1 KB along r)
-#pragma unroll
-            for (int h = 0; h < C::kNABox; ++h) {
-              const uint64_t adx = sdesc_sw128(xs + kk * 32, 16, 1024);
-              const uint64_t bda = sdesc_none(smem_u32(st + C::kLAOff + h * C::kABox) + kk * 256, 128, 1024);
-              umma_bf16(tmem + C::kXaCol, adx, bda, xa_idesc, (kb | kk | h) != 0);
-            }
-          }
         }
         umma_commit(&bars->empty[s]);
-        if (kb == nkb - 1) {
+        if (kb == nkb - 1 && !C::kXaRing) {  // LoRA: after the fold below
           umma_commit(&bars->tmem_full);
           TPO_T(3);
         }
+      }
+      __syncwarp();
+    }
+    if (C::kXaRing && !(p.dbg_flags & 4)) {
+      // acc[n][t] += Σ_r B̄[r][n]·XA_s[t][r] (hi, then lo)
+      uint8_t *st = stages + (nkb % STAGES) * C::kStage;
+      mbar_wait(&bars->xb_full, 0);
+      mbar_wait(&bars->xa_ready, 0);
+      tc_fence_after();
+      if (elect_one()) {
+        // N = 16: the hi token columns (SPLIT's lo tokens sit in 16-31)
+        constexpr uint32_t fold_idesc = idesc_bf16(kTileN, 16, true, false);
+#pragma unroll
+        for (int hb = 0; hb < C::kFoldPlanes; ++hb)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            umma_bf16(tmem, sdesc_sw128(smem_u32(st + C::kFoldB + hb * 4096), 2048, 1024),
+                      sdesc_sw128(smem_u32(st + C::kFoldX) + h * 32, 16, 1024), fold_idesc, 1u);
+        umma_commit(&bars->tmem_full);
+        TPO_T(3);
       }
       __syncwarp();
     }
@@ -381,17 +388,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
     const int t = threadIdx.x - 64;
     float sumsq = 0.f;       // RMS: Σx² of token t/16 over this CTA's K range
     // Epilogue operands from global memory are loaded now, off the critical
-    // path (under a saturated HBM a dependent load costs ~1 µs): LoRA B̄
-    // column of the row this thread finalizes, RMS D.
-    const int erow = (warp & 3) * 32 + lane;
-    float bcol[MODE == MODE_LORA ? 16 : 1];
+    // path (under a saturated HBM a dependent load costs ~1 µs): RMS D.
     float dsc = 0.f;
-    if (MODE == MODE_LORA) {  // every CTA folds its own XA partial times B̄ into its rows
-#pragma unroll
-      for (int r = 0; r < 16; ++r)
-        bcol[r] = SPLIT ? p.lora_b_f32[size_t(r) * p.N + n0 + erow]
-                        : __bfloat162float(p.lora_b[size_t(r) * p.N + n0 + erow]);
-    }
     if (MODE == MODE_RMS) dsc = SPLIT ? p.dscale_f32[0] : __bfloat162float(p.dscale[0]);
     if (MODE == MODE_RMS) {
       // Per stage: B tile rows 0-7 = bf16(x·g) (hi), rows 8-15 = the
@@ -505,7 +503,22 @@ __global__ void __launch_bounds__(kThreads, MINB)
       const int i0 = (t >> 3) * 16 + (t & 7) * 2;
       const float xa0 = (xa_w[i0] + xa_w[256 + i0]) + (xa_w[512 + i0] + xa_w[768 + i0]);
       const float xa1 = (xa_w[i0 + 1] + xa_w[256 + i0 + 1]) + (xa_w[512 + i0 + 1] + xa_w[768 + i0 + 1]);
-      *reinterpret_cast<float2 *>(xa_tot + i0) = make_float2(xa0, xa1);
+      {
+        // XA_s^T tile for the tensor-core fold: row = token, k = r (hi,
+        // chunks 0-1) and 16 + r (lo, chunks 2-3), 128-B swizzle
+        const __nv_bfloat162 h = __floats2bfloat162_rn(xa0, xa1);
+        const float2 hf = __bfloat1622float2(h);
+        const __nv_bfloat162 l = __floats2bfloat162_rn(xa0 - hf.x, xa1 - hf.y);
+        const int tok = t >> 3, r = (t & 7) * 2, c = r >> 3;
+        const uint32_t row_off = (tok >> 3) * 1024 + (tok & 7) * 128 + (r & 7) * 2;
+        uint8_t *xt = stages + (nkb % STAGES) * C::kStage + C::kFoldX;
+        mbar_wait(&bars->xb_full, 0);  // the stage has drained (and B̄ landed)
+        *reinterpret_cast<__nv_bfloat162 *>(xt + row_off + ((c ^ (tok & 7)) << 4)) = h;
+        *reinterpret_cast<__nv_bfloat162 *>(xt + row_off + (((c + 2) ^ (tok & 7)) << 4)) = l;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars->xa_ready);
+      }
     }
 
     if (!early_trigger) pdl_launch();
@@ -550,28 +563,15 @@ __global__ void __launch_bounds__(kThreads, MINB)
         post[tk] = 1.0f / sqrtf(ss * dsc);
       }
     }
-    if (MODE == MODE_LORA && C::kXaRing) {
-      // (XA_s·B̄)[t, n] for this thread's row n, every token t
+    if (MODE == MODE_LORA) {
 #pragma unroll
-      for (int tk = 0; tk < 16; ++tk) {
-        const float4 *xr = reinterpret_cast<const float4 *>(xa_tot + tk * 16);
-        float o = 0.f;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float4 x = xr[i];
-          o = fmaf(x.x, bcol[4 * i], o);
-          o = fmaf(x.y, bcol[4 * i + 1], o);
-          o = fmaf(x.z, bcol[4 * i + 2], o);
-          o = fmaf(x.w, bcol[4 * i + 3], o);
-        }
-        post[tk] = o;
-      }
+      for (int tk = 0; tk < 16; ++tk) post[tk] = 0.f;  // XA_s·B̄ is folded into the accumulator
     }
 
     // ---- critical path: last MMA -> TMEM -> DSMEM -> owner -> HBM
     // pin the post-loop operands here: without this the compiler may sink
     // their computation past the waits below, onto the critical path
-    if ((MODE == MODE_RMS && (mine || atomic_epi)) || C::kXaRing) {
+    if (MODE == MODE_RMS && (mine || atomic_epi)) {
 #pragma unroll
       for (int tk = 0; tk < T; ++tk) asm volatile("" : "+f"(post[tk]));
     }
@@ -579,40 +579,6 @@ __global__ void __launch_bounds__(kThreads, MINB)
     if (threadIdx.x == 64) TPO_T(5);
     __syncwarp();  // tcgen05.ld is .sync.aligned: the warp must be converged
     tc_fence_after();
-    if (C::kXaMma) {
-      // XA_s sits in TMEM lanes 0-15 (tokens; SPLIT: lo tokens in lanes
-      // 16-31), columns kXaCol.. (r): the lane-quarter-0 warp stages it as
-      // xa_tot[t][r], then every thread forms (XA_s·B̄)[t, n] for its row
-      if (q == 0) {
-        float xv[16];
-        tmem_ld16(tmem + C::kXaCol, xv);
-        if (SPLIT) {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) xv[i] += __shfl_down_sync(0xffffffffu, xv[i], 16);
-        }
-        if (lane < 16) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            *reinterpret_cast<float4 *>(xa_tot + lane * 16 + 4 * i) =
-                make_float4(xv[4 * i], xv[4 * i + 1], xv[4 * i + 2], xv[4 * i + 3]);
-        }
-      }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-#pragma unroll
-      for (int tk = 0; tk < 16; ++tk) {
-        const float4 *xr = reinterpret_cast<const float4 *>(xa_tot + tk * 16);
-        float o = 0.f;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float4 x = xr[i];
-          o = fmaf(x.x, bcol[4 * i], o);
-          o = fmaf(x.y, bcol[4 * i + 1], o);
-          o = fmaf(x.z, bcol[4 * i + 2], o);
-          o = fmaf(x.w, bcol[4 * i + 3], o);
-        }
-        post[tk] = o;
-      }
-    }
     float acc[16];
     {
       float v[16];
@@ -698,7 +664,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
   if (threadIdx.x == 0) TPO_T(12);
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<C::kTmemCols>(tmem);
+    tmem_dealloc<32>(tmem);
   }
   if (threadIdx.x == 0) TPO_T(7);
 #undef TPO_T
@@ -711,7 +677,7 @@ size_t skinny_smem(const SkinnyParams &p) {
   (void)nkb;
   size_t b = size_t(STAGES) * C::kStage +
              (S > 1 ? size_t(S - 1) * (kTileN / S) * 16 * 4 : 0) + size_t(S) * C::kSide * 4 +
-             (MODE == MODE_LORA ? (C::kXaRing ? 256 + 1024 : 256) * 4 : 0) + sizeof(Bars);
+             (MODE == MODE_LORA ? 1024 * 4 : 0) + sizeof(Bars);
   return b + 1024;
 }
 
@@ -778,7 +744,3 @@ extern "C" size_t tpo_skinny_smem(int mode, int stages, int minb, int split, con
 #undef TPO_CASE
   return 0;
 }
-
-// Columns of one LoRA A box (the host's tensor-map box width): 8 for the
-// tensor-core XA path (two boxes per plane), 16 for the XA-ring path.
-extern "C" int tpo_skinny_lora_a_box_cols() { return Cfg<MODE_LORA, false>::kXaMma ? 8 : 16; }

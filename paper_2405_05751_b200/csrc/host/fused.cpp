@@ -635,7 +635,7 @@ int launch_fused(const FusedPlan &p, const FusedIO &io, cudaStream_t st) {
   // the library wrote an operand on this stream just now: no weight may be
   // read before the PDL wait
   const bool converted = !all_bf16;
-  CUtensorMap maps[7];
+  CUtensorMap maps[8];
   std::memset(maps, 0, sizeof(maps));
   if (p.kind == TPO_FUSED_GQA_DECODE) {
     // K^T [G, hd, L], V [G, L, hd], Q [G, qh, hd]
@@ -765,6 +765,14 @@ int launch_fused(const FusedPlan &p, const FusedIO &io, cudaStream_t st) {
   sp.tokens = int(p.b);
   sp.k_per_cta = int(p.h / sp.ksplit);
   sp.out = io.out[0];
+  // outputs: one TMA tile store per owner warp (TPO_TMA_OUT=0: T coalesced
+  // row stores per thread; LoRA 8.18-8.37 vs 8.20-8.24 us, same box)
+  sp.tma_out = env_int("TPO_TMA_OUT", 1);
+  maps[7] = maps[0];
+  if (sp.tma_out) {
+    const int T = mode == MODE_LORA ? 16 : 8;
+    if (!tmap_2d(&maps[7], sp.out, p.b, p.n, 32, uint32_t(T), NOSW, /*f32*/ true)) return int(cudaErrorInvalidValue);
+  }
   // Weights (W / W1,W3 / A) declared static may stream before the PDL wait,
   // unless the library itself just wrote them (converted operands).
   const uint64_t weights = p.kind == TPO_FUSED_GATED_MLP ? 0x6 : p.kind == TPO_FUSED_LORA ? 0x6 : 0x4;

@@ -25,6 +25,7 @@ struct SkinnyParams {
   int trig_early;            // experiment: producer triggers dependents this many k blocks early
   int pre_cut;               // experiment: prefetch this many fewer static stages
   int l2_ahead;              // weight k blocks requested into L2 ahead of the ring (after the wait)
+  int tma_out;               // outputs by one TMA tile store per owner warp (map 7)
 };
 
 struct GqaParams {
@@ -36,7 +37,7 @@ struct GqaParams {
   int consume_order;         // ring filled K_0, K_1, V_0, K_2, V_1, ... (the MMA issue order)
 };
 
-// maps: {W plane 0, W plane 1, X, A / G, W plane 2 | LoRA B̄ (hi), W plane 3 | LoRA B̄ lo, A lo plane}
+// maps: {W plane 0, W plane 1, X, A / G, W plane 2 | LoRA B̄ (hi), W plane 3 | LoRA B̄ lo, A lo plane, out (fp32, TPO_TMA_OUT)}
 extern "C" int tpo_skinny_launch(int mode, int stages, int minb, int split, const CUtensorMap *maps,
                                  const SkinnyParams *p, cudaStream_t st);
 extern "C" size_t tpo_skinny_smem(int mode, int stages, int minb, int split, const SkinnyParams *p);

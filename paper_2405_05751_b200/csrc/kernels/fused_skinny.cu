@@ -145,7 +145,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
     skinny_kernel(const __grid_constant__ CUtensorMap tmW0, const __grid_constant__ CUtensorMap tmW1,
                   const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmA,
                   const __grid_constant__ CUtensorMap tmW2, const __grid_constant__ CUtensorMap tmW3,
-                  const __grid_constant__ CUtensorMap tmA1, const SkinnyParams p) {
+                  const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmO,
+                  const SkinnyParams p) {
   using C = Cfg<MODE, SPLIT>;
   // weight plane maps: bf16 {W} / {W1, W3}; SPLIT {W hi, W lo} / {W1 hi, W1 lo, W3 hi, W3 lo}
   const CUtensorMap *wmap[4] = {&tmW0, &tmW1, &tmW2, &tmW3};
@@ -641,13 +642,27 @@ __global__ void __launch_bounds__(kThreads, MINB)
       }
     }
     if (mine && !atomic_epi && !(p.dbg_flags & 1)) {
+      // the warp's [T][32] output tile through a drained stage and one TMA
+      // store (rows past p.tokens clip); TPO_TMA_OUT=0: T coalesced row stores
+      float *tile = reinterpret_cast<float *>(stages) + q * 32 * T;
 #pragma unroll
       for (int tk = 0; tk < T; ++tk) {
         float o;
         if (MODE == MODE_GATED) o = silu(acc[tk]) * acc[8 + tk];
         else if (MODE == MODE_RMS) o = acc[tk] * post[tk];
         else o = acc[tk];
-        if (tk < p.tokens) p.out[size_t(tk) * p.N + n] = o;
+        if (p.tma_out) tile[tk * 32 + lane] = o;
+        else if (tk < p.tokens) p.out[size_t(tk) * p.N + n] = o;
+      }
+      if (p.tma_out) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmO, tile, n0 + q * 32, 0);
+          bulk_commit();
+          bulk_wait_read();
+        }
+        __syncwarp();
       }
       if (lane == 0 && (S == 1 || q == int(rank) * (4 / S))) TPO_T(11);
     }
@@ -701,7 +716,7 @@ cudaError_t launch_t(const CUtensorMap *maps, const SkinnyParams &p, cudaStream_
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = std::getenv("TPO_NO_PDL") ? 1 : 2;
-  return cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], p);
+  return cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], maps[6], maps[7], p);
 }
 
 }  // namespace tpo_fused

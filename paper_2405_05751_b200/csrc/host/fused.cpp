@@ -657,6 +657,9 @@ int launch_fused(const FusedPlan &p, const FusedIO &io, cudaStream_t st) {
     int minb = env_int("TPO_MINB", 1);
     if (split) slots = 3, minb = 1;
     gp.consume_order = env_int("TPO_GQA_ORDER", 1);
+    // first ring units + Q into L2 before the PDL wait (22.80 -> 22.26 us
+    // per evaluation at 3 units; 1: 22.47, 2: 22.31, 4: 22.34, all: 28.3)
+    gp.l2_units = env_int("TPO_GQA_L2", 3);
     const int nct_g = int(p.groups) * S;
     gp.dbg = debug_begin(nct_g, st);
     bool ok;
@@ -768,6 +771,9 @@ int launch_fused(const FusedPlan &p, const FusedIO &io, cudaStream_t st) {
   // outputs: one TMA tile store per owner warp (TPO_TMA_OUT=0: T coalesced
   // row stores per thread; LoRA 8.18-8.37 vs 8.20-8.24 us, same box)
   sp.tma_out = env_int("TPO_TMA_OUT", 1);
+  // activations into L2 before the PDL wait (RMS 7.48 -> 7.39, LoRA 8.21 ->
+  // 8.05, GatedMLP 35.4 -> 35.25 us per evaluation, same boxes)
+  sp.x_l2 = env_int("TPO_X_L2", 1);
   maps[7] = maps[0];
   if (sp.tma_out) {
     const int T = mode == MODE_LORA ? 16 : 8;

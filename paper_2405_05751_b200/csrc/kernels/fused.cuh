@@ -26,6 +26,7 @@ struct SkinnyParams {
   int pre_cut;               // experiment: prefetch this many fewer static stages
   int l2_ahead;              // weight k blocks requested into L2 ahead of the ring (after the wait)
   int tma_out;               // outputs by one TMA tile store per owner warp (map 7)
+  int x_l2;                  // activations requested into L2 before the PDL wait
 };
 
 struct GqaParams {
@@ -35,6 +36,7 @@ struct GqaParams {
   float *out;                // [g, qh, hd]
   unsigned long long *dbg;   // optional per-CTA phase timestamps (TPO_DEBUG_TIMES)
   int consume_order;         // ring filled K_0, K_1, V_0, K_2, V_1, ... (the MMA issue order)
+  int l2_units;              // ring units (and Q) requested into L2 before the PDL wait
 };
 
 // maps: {W plane 0, W plane 1, X, A / G, W plane 2 | LoRA B̄ (hi), W plane 3 | LoRA B̄ lo, A lo plane, out (fp32, TPO_TMA_OUT)}

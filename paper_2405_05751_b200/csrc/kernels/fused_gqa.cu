@@ -134,6 +134,30 @@ __global__ void __launch_bounds__(kThreads, MINB)
   if (threadIdx.x == 0) TPO_T(1);
   if (S > 1) cluster_arrive();
   if (threadIdx.x == 0 && S > 1) mbar_expect_tx(&bars->recv, uint32_t((S - 1) * (rows_per * 32 + 32)));
+  // The first ring units (and Q) requested into L2 before the wait: a hint
+  // only — L2 is the point of coherence, every read that uses the data comes
+  // after the wait — so a CTA that becomes resident while the previous grid
+  // drains turns its first post-wait loads into L2 hits.
+  auto unit = [&](int u, bool &isk, int &blk) {
+    // slot u carries K_j or V_j: K_0 V_0 K_1 V_1 ..., or in the MMA issue
+    // order K_0 K_1 V_0 K_2 V_1 ... K_{nb-1} V_{nb-2} V_{nb-1}
+    if (!p.consume_order) isk = !(u & 1), blk = u >> 1;
+    else if (u == 0) isk = true, blk = 0;
+    else if (u & 1) isk = (u + 1) / 2 < nb, blk = isk ? (u + 1) / 2 : nb - 1;
+    else isk = false, blk = u / 2 - 1;
+  };
+  if (warp == 0 && p.l2_units > 0 && elect_one()) {
+    tma_prefetch_l2_3d(&tmQ, 0, 0, g);
+    tma_prefetch_l2_3d(&tmQ, 64, 0, g);
+    for (int u = 0; u < p.l2_units && u < 2 * nb; ++u) {
+      bool isk;
+      int blk;
+      unit(u, isk, blk);
+      const int l = l0 + blk * kBL;
+      if (isk) tma_prefetch_l2_3d(&tmK, l, 0, g), tma_prefetch_l2_3d(&tmK, l + 64, 0, g);
+      else tma_prefetch_l2_3d(&tmV, 0, l, g), tma_prefetch_l2_3d(&tmV, 64, l, g);
+    }
+  }
   pdl_wait();
   pdl_launch();  // every thread: the dependent grid may become resident early
 
@@ -148,14 +172,9 @@ __global__ void __launch_bounds__(kThreads, MINB)
         mbar_wait(&bars->empty[s], ((u / SLOTS) & 1) ^ 1);
         uint8_t *st = stages + s * kSlotB;
         mbar_expect_tx(&bars->full[s], kSlotB);
-        // slot u carries K_j or V_j: K_0 V_0 K_1 V_1 ..., or in the MMA
-        // issue order K_0 K_1 V_0 K_2 V_1 ... K_{nb-1} V_{nb-2} V_{nb-1}
         bool isk;
         int blk;
-        if (!p.consume_order) isk = !(u & 1), blk = u >> 1;
-        else if (u == 0) isk = true, blk = 0;
-        else if (u & 1) isk = (u + 1) / 2 < nb, blk = isk ? (u + 1) / 2 : nb - 1;
-        else isk = false, blk = u / 2 - 1;
+        unit(u, isk, blk);
         const int l = l0 + blk * kBL;
         if (isk) {
           tma_load_3d(st, &tmK, &bars->full[s], l, 0, g);              // K^T[d, l..l+63]

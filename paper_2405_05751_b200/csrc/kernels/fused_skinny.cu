@@ -237,6 +237,21 @@ __global__ void __launch_bounds__(kThreads, MINB)
       }
       if (MODE == MODE_LORA) lora_a(st, &bars->full[kb], k0);  // A: static
     }
+    // The activations (RMS: and G) are requested into L2 before the wait —
+    // a hint only, no data reaches the SM: L2 is the point of coherence, so
+    // a write by the preceding grid still lands in (or updates) those lines,
+    // and every read that uses them comes after the wait.  It turns the
+    // post-wait activation loads from HBM misses into L2 hits (an activation
+    // the preceding grid just wrote is there already).  RMS / LoRA: the
+    // CTA's whole K range (16 boxes); GatedMLP (64 k blocks per CTA): the
+    // prefetched stages' (more costs 1.1 us).  TPO_X_L2=0 disables.
+    if (p.x_l2) {
+      const int nx = MODE == MODE_GATED ? npre : nkb;
+      for (int kb = 0; kb < nx; ++kb) {
+        tma_prefetch_l2_2d(&tmX, kbase + kb * kBK, 0);
+        if (MODE == MODE_RMS) tma_prefetch_l2_2d(&tmA, kbase + kb * kBK, 0);
+      }
+    }
   }
   pdl_wait();  // inputs may be produced by the preceding kernel
   // PDL trigger: by default late — each warp triggers once its streaming

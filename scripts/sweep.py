@@ -47,7 +47,7 @@ def main():
     outs = [torch.empty_like(want) for _ in range(copies)]
     st = torch.cuda.Stream()
     for cfg in cfgs:
-        for k in ("TPO_KSPLIT", "TPO_STAGES", "TPO_MINB", "TPO_NO_PDL", "TPO_DBG_FLAGS", "TPO_EPI_ATOMIC", "TPO_TRIG_EARLY", "TPO_PRE_CUT", "TPO_L2_AHEAD", "TPO_GQA_SLOTS", "TPO_GQA_ORDER"):
+        for k in ("TPO_KSPLIT", "TPO_STAGES", "TPO_MINB", "TPO_NO_PDL", "TPO_DBG_FLAGS", "TPO_EPI_ATOMIC", "TPO_TRIG_EARLY", "TPO_PRE_CUT", "TPO_L2_AHEAD", "TPO_GQA_SLOTS", "TPO_GQA_ORDER", "TPO_GQA_L2", "TPO_X_L2", "TPO_TMA_OUT"):
             os.environ.pop(k, None)
         static = False
         for kv in filter(None, cfg.split(",")):

@@ -827,10 +827,10 @@ int launch_fused(const FusedPlan &p, const FusedIO &io, cudaStream_t st) {
   sp.dbg_flags = env_int("TPO_DBG_FLAGS", 0);
   sp.epi_atomic = env_int("TPO_EPI_ATOMIC", 0);
   // two CTAs per SM: the producer releases the next evaluation a few k
-  // blocks before its last issue (RMS 5, LoRA 3), so the next grid's weight
+  // blocks before its last issue (RMS 5, LoRA 4), so the next grid's weight
   // prefetch overlaps this one's last stages (sweeps: RMS 7.59 vs 7.87 us,
-  // LoRA 8.54 vs 8.84 us)
-  sp.trig_early = env_int("TPO_TRIG_EARLY", !sp.prefetch_static || minb != 2 ? 0 : mode == MODE_RMS ? 5 : 3);
+  // LoRA 8.54 vs 8.84 us; with the L2 hints LoRA 8.06 at 4 vs 8.11 at 3)
+  sp.trig_early = env_int("TPO_TRIG_EARLY", !sp.prefetch_static || minb != 2 ? 0 : mode == MODE_RMS ? 5 : 4);
   sp.pre_cut = env_int("TPO_PRE_CUT", 0);
   // and, behind this evaluation's X, runs two weight k blocks ahead of the
   // ring through L2 (sweeps: RMS 7.52 vs 7.67 us, LoRA 8.37 vs 8.60 us;

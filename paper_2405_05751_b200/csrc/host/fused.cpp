@@ -834,8 +834,11 @@ int launch_fused(const FusedPlan &p, const FusedIO &io, cudaStream_t st) {
   sp.pre_cut = env_int("TPO_PRE_CUT", 0);
   // and, behind this evaluation's X, runs two weight k blocks ahead of the
   // ring through L2 (sweeps: RMS 7.52 vs 7.67 us, LoRA 8.37 vs 8.60 us;
-  // deeper run-ahead is slower, GatedMLP's deep ring gains nothing)
-  sp.l2_ahead = env_int("TPO_L2_AHEAD", sp.prefetch_static && minb == 2 && mode != MODE_GATED ? 2 : 0);
+  // deeper run-ahead is slower, GatedMLP's deep ring gains nothing; with
+  // the activation L2 hints LoRA prefers one block: 7.98 vs 8.06 us at 2)
+  sp.l2_ahead = env_int("TPO_L2_AHEAD", !sp.prefetch_static || minb != 2 || mode == MODE_GATED ? 0
+                                        : mode == MODE_LORA                                     ? 1
+                                                                                                : 2);
   const int nct = int(p.n / 128) * sp.ksplit;
   unsigned long long *dbg = debug_begin(nct, st);
   sp.dbg = dbg;

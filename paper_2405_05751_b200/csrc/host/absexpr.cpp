@@ -66,9 +66,13 @@ Id Pool::add(Id a, Id b) {
 
 Id Pool::sum(uint64_t k, Id a) {
   if (k == 1) return a;
+  auto it = sum_memo_.find({k, a});
+  if (it != sum_memo_.end()) return it->second;
   Poly p = polys_[a];
   for (Mono &m : p.monos) m.count = sat_mul(m.count, k);
-  return intern(std::move(p));
+  const Id r = intern(std::move(p));
+  sum_memo_.emplace(std::make_pair(k, a), r);
+  return r;
 }
 
 // Product of two monomials, then the per-monomial merges: all exp atoms into
@@ -119,7 +123,14 @@ Id Pool::mul(Id a, Id b) {
   return r;
 }
 
-Id Pool::div(Id a, Id b) { return mul(a, atom_poly(atom({AtomKind::Inv, b}))); }
+Id Pool::div(Id a, Id b) {
+  const uint64_t key = (uint64_t(a) << 32) | b;
+  auto it = div_memo_.find(key);
+  if (it != div_memo_.end()) return it->second;
+  const Id r = mul(a, unary(AtomKind::Inv, b));
+  div_memo_.emplace(key, r);
+  return r;
+}
 
 // a·f scaled by c is a sub-multiset of b, for the monomial f and count c
 // that align a's first monomial with one of b's

@@ -306,8 +306,11 @@ class BlockSearch {
       }
       nt.acc = acc;
     }
-    std::vector<TensorShape> sh;
-    for (int i = 0; i < o.nin; ++i) sh.push_back(T_[size_t(o.in[size_t(i)])].shape);
+    // per-arity scratch reused across attempts (element assignment keeps
+    // the dims' capacity: no allocation per attempt)
+    std::vector<TensorShape> &sh = shv_[size_t(o.nin)];
+    if (sh.size() != size_t(o.nin)) sh.resize(size_t(o.nin));
+    for (int i = 0; i < o.nin; ++i) sh[size_t(i)] = T_[size_t(o.in[size_t(i)])].shape;
     ShapeResult s = infer_output_shape(o.type, o.attrs, sh, Level::Block);
     if (!s) {
       ++st_.pruned_shape;
@@ -353,8 +356,9 @@ class BlockSearch {
       for (int i = 0; i < o.nin; ++i) nt.partial = nt.partial || T_[size_t(o.in[size_t(i)])].partial;
     }
     // the abstract expression (Table 2) and the expr check
-    std::vector<Id> ie;
-    for (int i = 0; i < o.nin; ++i) ie.push_back(T_[size_t(o.in[size_t(i)])].e);
+    std::vector<Id> &ie = iev_[size_t(o.nin)];
+    ie.resize(size_t(o.nin));
+    for (int i = 0; i < o.nin; ++i) ie[size_t(i)] = T_[size_t(o.in[size_t(i)])].e;
     if (o.type == OpType::Accum) {
       nt.e = std::get<AccumAttrs>(o.attrs).fmap.targets[0] == kReplica ? P_.sum(uint64_t(job_.fl), ie[0]) : ie[0];
     } else {
@@ -508,6 +512,8 @@ class BlockSearch {
   const EnumConfig &cfg_;
   EnumStats &st_;
   std::vector<KernelGraph> &out_;
+  std::array<std::vector<TensorShape>, 5> shv_;
+  std::array<std::vector<Id>, 5> iev_;
   Pool P_;
   Id eo_ = 0;
   TensorShape out_shape_;

@@ -76,6 +76,7 @@ class Pool {
  private:
   Id unary(AtomKind k, Id a);
   Id intern(Poly &&p);
+  Id add_uncached(Id a, Id b);
   Id atom(Atom a);
   Id atom_poly(Id atom_id);
   Mono mono_mul(const Mono &x, const Mono &y);
@@ -86,6 +87,10 @@ class Pool {
   std::vector<Poly> polys_;
   std::map<std::vector<uint64_t>, Id> poly_ids_;
   std::unordered_map<uint64_t, Id> mul_memo_;
+  // add / unary / div are memoised like mul: the enumerator re-derives the
+  // same (op, operand ids) at every DFS branch sharing a prefix
+  std::unordered_map<uint64_t, Id> add_memo_, unary_memo_, div_memo_;
+  std::map<std::pair<uint64_t, Id>, Id> sum_memo_;
   std::unordered_map<uint64_t, bool> sub_memo_;
 };
 

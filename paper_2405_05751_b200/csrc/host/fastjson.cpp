@@ -13,6 +13,7 @@
 // yields (tests/test_abi.py checks both on every golden graph).
 #include <charconv>
 #include <cstring>
+#include <span>
 #include <string_view>
 
 #include "tpo/ir/serialize.hpp"
@@ -29,7 +30,14 @@ struct Node {
 
 class Tok {
  public:
-  Tok(const char *s, size_t n) : p_(s), e_(s + n), base_(s) {}
+  Tok(const char *s, size_t n) : p_(s), e_(s + n), base_(s) {
+    // ~1 node per 6 bytes of the schema's compact text
+    nodes.reserve(n / 4 + 16);
+    kv.reserve(n / 12 + 8);
+    items.reserve(n / 8 + 8);
+    kstk_.reserve(64);
+    istk_.reserve(256);
+  }
 
   bool parse(uint32_t &root) {
     ws();
@@ -55,6 +63,8 @@ class Tok {
 
  private:
   const char *p_, *e_, *base_;
+  std::vector<std::pair<uint32_t, uint32_t>> kstk_;  // open objects' pairs
+  std::vector<uint32_t> istk_;                       // open arrays' items
 
   void ws() {
     while (p_ < e_ && (*p_ == ' ' || *p_ == '\n' || *p_ == '\r' || *p_ == '\t')) ++p_;
@@ -86,7 +96,9 @@ class Tok {
     const char c = *p_;
     if (c == '{') {
       ++p_;
-      std::vector<std::pair<uint32_t, uint32_t>> mine;
+      // children collect on a shared stack (no allocation per container)
+      // and move to `kv` when the object closes
+      const size_t base = kstk_.size();
       ws();
       if (p_ < e_ && *p_ == '}') {
         ++p_;
@@ -100,9 +112,9 @@ class Tok {
           ++p_;
           ws();
           if (!value(v, depth + 1)) return false;
-          for (auto &pr : mine)
-            if (str(pr.first) == str(k)) return false;  // duplicate key: slow path decides
-          mine.emplace_back(k, v);
+          for (size_t c = base; c < kstk_.size(); ++c)
+            if (str(kstk_[c].first) == str(k)) return false;  // duplicate key: slow path decides
+          kstk_.emplace_back(k, v);
           ws();
           if (p_ < e_ && *p_ == ',') {
             ++p_;
@@ -117,14 +129,15 @@ class Tok {
       }
       Node n{Node::Obj};
       n.a = uint32_t(kv.size());
-      kv.insert(kv.end(), mine.begin(), mine.end());
+      kv.insert(kv.end(), kstk_.begin() + std::ptrdiff_t(base), kstk_.end());
+      kstk_.resize(base);
       n.b = uint32_t(kv.size());
       out = push(n);
       return true;
     }
     if (c == '[') {
       ++p_;
-      std::vector<uint32_t> mine;
+      const size_t base = istk_.size();
       ws();
       if (p_ < e_ && *p_ == ']') {
         ++p_;
@@ -133,7 +146,7 @@ class Tok {
           ws();
           uint32_t v;
           if (!value(v, depth + 1)) return false;
-          mine.push_back(v);
+          istk_.push_back(v);
           ws();
           if (p_ < e_ && *p_ == ',') {
             ++p_;
@@ -148,7 +161,8 @@ class Tok {
       }
       Node n{Node::Arr};
       n.a = uint32_t(items.size());
-      items.insert(items.end(), mine.begin(), mine.end());
+      items.insert(items.end(), istk_.begin() + std::ptrdiff_t(base), istk_.end());
+      istk_.resize(base);
       n.b = uint32_t(items.size());
       out = push(n);
       return true;
@@ -211,10 +225,10 @@ class Builder {
     if (v < 0) throw Fail{};
     return uint32_t(v);
   }
-  std::vector<uint32_t> arr(uint32_t n) const {
+  std::span<const uint32_t> arr(uint32_t n) const {
     const Node &x = t_.node(n);
     if (x.kind != Node::Arr) throw Fail{};
-    return std::vector<uint32_t>(t_.items.begin() + x.a, t_.items.begin() + x.b);
+    return {t_.items.data() + x.a, size_t(x.b - x.a)};
   }
   int64_t i64(uint32_t n) const {
     const Node &x = t_.node(n);
@@ -228,8 +242,10 @@ class Builder {
   }
   template <class I>
   std::vector<I> ints(uint32_t n) const {
+    const auto a = arr(n);
     std::vector<I> out;
-    for (uint32_t c : arr(n)) out.push_back(I(sizeof(I) == 8 ? i64(c) : i32(c)));
+    out.reserve(a.size());
+    for (uint32_t c : a) out.push_back(I(sizeof(I) == 8 ? i64(c) : i32(c)));
     return out;
   }
   std::string_view sv(uint32_t n) const {

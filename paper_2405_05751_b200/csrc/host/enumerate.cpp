@@ -83,6 +83,83 @@ std::vector<Id> graph_exprs(Pool &P, const KernelGraph &g) {
   return e;
 }
 
+// Output shape of a block-level op the enumerator generates, written into
+// `out` without allocating (capacity reused): 1 = shape, 0 = no shape, -1 =
+// not covered (use infer_output_shape).  The same rules as
+// infer_output_shape at Level::Block (ir_core.cpp: contract, broadcast_shapes,
+// Sum, elementwise, Accum) for these ops — inputs are inferred shapes, so
+// valid.
+int block_shape(OpType t, const OpAttrs &at, const std::vector<TensorShape> &in, TensorShape &out) {
+  auto contract = [](const TensorShape &a, const TensorShape &b) {
+    const int r = a.rank();
+    if (r < 2 || b.rank() != r) return false;
+    for (int i = 0; i + 2 < r; ++i)
+      if (a.dims[size_t(i)] != b.dims[size_t(i)]) return false;
+    return a.dims[size_t(r - 1)] == b.dims[size_t(r - 2)];
+  };
+  auto set_contract = [&](const TensorShape &a, const TensorShape &b) {
+    out.dims.assign(a.dims.begin(), a.dims.end());
+    out.dims.back() = b.dims.back();
+  };
+  switch (t) {
+    case OpType::Matmul:
+      if (in.size() != 2 || !contract(in[0], in[1])) return 0;
+      set_contract(in[0], in[1]);
+      return 1;
+    case OpType::ConcatMatmul: {
+      if (in.size() != 4 || !contract(in[0], in[2]) || !contract(in[1], in[3])) return 0;
+      // both products' shapes (a's dims with b's last) must agree
+      const TensorShape &a = in[0], &c = in[1];
+      if (a.rank() != c.rank() || in[2].dims.back() != in[3].dims.back()) return 0;
+      for (int i = 0; i + 1 < a.rank(); ++i)
+        if (a.dims[size_t(i)] != c.dims[size_t(i)]) return 0;
+      set_contract(in[0], in[2]);
+      return 1;
+    }
+    case OpType::Sum: {
+      if (in.size() != 1) return 0;
+      const auto &a = std::get<SumAttrs>(at);
+      if (a.dim < 0 || a.dim >= in[0].rank() || a.group < 1 || in[0].dims[size_t(a.dim)] % a.group) return 0;
+      out.dims.assign(in[0].dims.begin(), in[0].dims.end());
+      out.dims[size_t(a.dim)] /= a.group;
+      return 1;
+    }
+    case OpType::EwAdd:
+    case OpType::EwMul:
+    case OpType::EwDiv: {
+      if (in.size() != 2) return 0;
+      const TensorShape &a = in[0], &b = in[1];
+      const int r = std::max(a.rank(), b.rank());
+      out.dims.resize(size_t(r));
+      for (int i = 0; i < r; ++i) {
+        const int ia = i - (r - a.rank()), ib = i - (r - b.rank());
+        const int64_t x = ia >= 0 ? a.dims[size_t(ia)] : 1, y = ib >= 0 ? b.dims[size_t(ib)] : 1;
+        if (x != y && x != 1 && y != 1) return 0;
+        out.dims[size_t(i)] = x > y ? x : y;
+      }
+      return 1;
+    }
+    case OpType::EwExp:
+    case OpType::Sqr:
+    case OpType::Sqrt:
+    case OpType::SiLU:
+      if (in.size() != 1) return 0;
+      out.dims.assign(in[0].dims.begin(), in[0].dims.end());
+      return 1;
+    case OpType::Accum: {
+      if (in.size() != 1) return 0;
+      const auto &a = std::get<AccumAttrs>(at);
+      if (a.fmap.axes() != 1) return 0;
+      const int d = a.fmap.targets[0];
+      if (d != kReplica && (d < 0 || d >= in[0].rank())) return 0;
+      out.dims.assign(in[0].dims.begin(), in[0].dims.end());
+      return 1;
+    }
+    default:
+      return -1;
+  }
+}
+
 // ------------------------------------------------------------ search jobs
 
 // A kernel-level prefix: pre-defined ops (in rank order) over the program's
@@ -286,7 +363,11 @@ class BlockSearch {
   void construct(const BOp &o) {
     const Rank r = rank_of(o);
     if (!(r > last_)) return;
-    BT nt;
+    // scratch tensor, reused across attempts (copied into T_ on success;
+    // nothing reads it after the recursion)
+    BT &nt = nt_;
+    nt.e = 0, nt.acc = 1, nt.ldim = -1, nt.partial = false, nt.users = 0;
+    nt.lab.fill(-1);
     uint8_t acc = 0;
     for (int i = 0; i < o.nin; ++i) acc |= T_[size_t(o.in[size_t(i)])].acc;
     if (o.type == OpType::Accum) {
@@ -311,12 +392,19 @@ class BlockSearch {
     std::vector<TensorShape> &sh = shv_[size_t(o.nin)];
     if (sh.size() != size_t(o.nin)) sh.resize(size_t(o.nin));
     for (int i = 0; i < o.nin; ++i) sh[size_t(i)] = T_[size_t(o.in[size_t(i)])].shape;
-    ShapeResult s = infer_output_shape(o.type, o.attrs, sh, Level::Block);
-    if (!s) {
+    const int fs = block_shape(o.type, o.attrs, sh, nt.shape);
+    if (fs == 0) {
       ++st_.pruned_shape;
       return;
     }
-    nt.shape = *s.shape;
+    if (fs < 0) {  // an op block_shape does not cover: the generic inference
+      ShapeResult s = infer_output_shape(o.type, o.attrs, sh, Level::Block);
+      if (!s) {
+        ++st_.pruned_shape;
+        return;
+      }
+      nt.shape = *s.shape;
+    }
     const BT &a0 = T_[size_t(o.in[0])];
     // dimension labels: operands must agree on what their aligned dims mean
     // (a shape that matches by coincidence is not a candidate), reductions
@@ -364,7 +452,11 @@ class BlockSearch {
     } else {
       nt.e = op_expr(P_, o.type, o.attrs, ie, sh);
     }
-    if (!P_.subexpr(nt.e, eo_)) {
+    // subexpression-of-the-program test, memoised densely by expression id
+    if (sub_eo_.size() <= nt.e) sub_eo_.resize(size_t(nt.e) + 1024, -1);
+    int8_t &se = sub_eo_[nt.e];
+    if (se < 0) se = P_.subexpr(nt.e, eo_) ? 1 : 0;
+    if (!se) {
       ++st_.pruned_expr;
       return;
     }
@@ -513,6 +605,8 @@ class BlockSearch {
   EnumStats &st_;
   std::vector<KernelGraph> &out_;
   std::array<std::vector<TensorShape>, 5> shv_;
+  BT nt_;
+  std::vector<int8_t> sub_eo_;  // expression id -> subexpr(e, eo_) (-1: not yet asked)
   std::array<std::vector<Id>, 5> iev_;
   Pool P_;
   Id eo_ = 0;

@@ -949,6 +949,8 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : NT == 128 ? 7 : 14) verify
         long long t0 = PROF ? clock64() : 0;
         uint32_t omega;
         bool ok;
+        bool lazy = false, run_prog = false;
+        uint64_t lazy_st0 = 0;
         if (a.shared_w && seed == a.shared_seed && round == 0 && att == 0) {
           // the batch's common first attempt: inputs, tables and the
           // program's outputs were computed once (shared_attempt_kernel)
@@ -984,30 +986,48 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : NT == 128 ? 7 : 14) verify
           // input, so the rest is drawn before it runs
           const uint64_t st0 = derive_state(seed, stream);
           const uint64_t table_draws = 1 + (silu ? f.p + f.q : 0);
-          bool lazy = g1.n_gen > 0 && !a.eager_inputs;
+          lazy = g1.n_gen > 0 && !a.eager_inputs;
           if (lazy) lazy = gen_attempt_lazy(s, f, st0, a.n_in, silu, &s_omega, omega);
           if (!lazy) omega = gen_attempt(s, f, seed, stream, a.n_in, silu, &s_slow, &s_omega);
           if (threadIdx.x == 0) s_drawn += table_draws + (lazy ? 0 : 2ull * a.n_in);
           if (threadIdx.x == 0) s_flag = 0, s_restart = 0;
           __syncthreads();
           if (PROF && threadIdx.x == 0) s_prof[0] += (unsigned long long)(clock64() - t0), s_prof[16] += 1;
-          // one call site for the program (and one for the candidate below):
-          // the interpreter stays inlined; a second pass only after a lazy
-          // draw hit the rejection zone (exact replay, eagerly)
+          lazy_st0 = st0;
+          run_prog = true;
+        }
+        // ONE inlined interpreter call site for the program and the
+        // candidate (pass 0 / pass 1): the kernel's code footprint halves
+        // (two inlined copies overflowed the instruction cache — stall
+        // reason no_instructions 27% on the GQA pool, profiles/r02).  The
+        // program pass repeats only after a lazy draw hit the rejection zone
+        // (exact replay, eagerly).
+        {
+          bool prog = run_prog;
+          uint32_t gen_next = 0;
           for (;;) {
-            uint32_t gen_next = 0;
-            ok = run_program<PROF>(s, f, scode, g1.code_len, &s_flag, s_prof, lazy ? &g1 : nullptr, st0,
-                                   &gen_next, &s_restart, &s_drawn);
-            if (lazy && ok) ok = lazy_gen_until(s, f, &g1, st0, 0xffffffffu, &gen_next, &s_restart, &s_drawn);
-            if (!lazy || !s_restart) break;
-            omega = gen_attempt(s, f, seed, stream, a.n_in, silu, &s_slow, &s_omega);
-            if (threadIdx.x == 0) s_drawn += table_draws + 2ull * a.n_in;
-            lazy = false;
-            if (threadIdx.x == 0) s_flag = 0;
-            __syncthreads();
+            bool r = run_program<PROF>(s, f, prog ? scode : ccode, prog ? g1.code_len : g2.code_len, &s_flag,
+                                       s_prof, prog && lazy ? &g1 : nullptr, lazy_st0, &gen_next, &s_restart,
+                                       &s_drawn);
+            if (!prog) {
+              ok = r;
+              break;
+            }
+            if (lazy && r) r = lazy_gen_until(s, f, &g1, lazy_st0, 0xffffffffu, &gen_next, &s_restart, &s_drawn);
+            if (lazy && s_restart) {
+              omega = gen_attempt(s, f, seed, stream, a.n_in, silu, &s_slow, &s_omega);
+              if (threadIdx.x == 0) s_drawn += 1 + (silu ? f.p + f.q : 0) + 2ull * a.n_in;
+              lazy = false;
+              gen_next = 0;
+              if (threadIdx.x == 0) s_flag = 0;
+              __syncthreads();
+              continue;
+            }
+            ok = r;
+            if (!ok) break;
+            prog = false;
           }
         }
-        ok = ok && run_program<PROF>(s, f, ccode, g2.code_len, &s_flag, s_prof);
         if (!ok && (s_flag & 3) == 3) {  // Error(PoisonedExponent) escapes the verifier
           if (t0w) {
             v.kind = 3;

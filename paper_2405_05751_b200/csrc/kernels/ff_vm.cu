@@ -597,12 +597,15 @@ __device__ __forceinline__ uint32_t ff_exec(const SmemT<WT> &s, const FieldConst
               // adds both k terms of a field in one instruction (exact: the
               // same products, fewer than `lazy` of them per reduction)
               if (ska == 1 && ((reinterpret_cast<uintptr_t>(pa + k0) | reinterpret_cast<uintptr_t>(pa + k0 + sma)) & 3u) == 0) {
+                // walking pointers: no per-step index products
+                const WT *qa = pa + k, *qb = pb + int32_t(k) * skb;
+                const int32_t skb2 = 2 * skb;
 #pragma unroll 2
-                for (; k + 2 <= k1; k += 2) {
-                  const uint32_t a0 = *reinterpret_cast<const uint32_t *>(pa + k);
-                  const uint32_t a1 = *reinterpret_cast<const uint32_t *>(pa + k + sma);
-                  const uint32_t b00 = pb[int32_t(k) * skb], b01 = pb[int32_t(k + 1) * skb];
-                  const uint32_t b10 = pb[int32_t(k) * skb + snb], b11 = pb[int32_t(k + 1) * skb + snb];
+                for (; k + 2 <= k1; k += 2, qa += 2, qb += skb2) {
+                  const uint32_t a0 = *reinterpret_cast<const uint32_t *>(qa);
+                  const uint32_t a1 = *reinterpret_cast<const uint32_t *>(qa + sma);
+                  const uint32_t b00 = qb[0], b01 = qb[skb];
+                  const uint32_t b10 = qb[snb], b11 = qb[skb + snb];
                   const uint32_t b0p = __byte_perm(b00, b01, 0x6420), b0q = __byte_perm(b00, b01, 0x5612);
                   const uint32_t b1p = __byte_perm(b10, b11, 0x6420), b1q = __byte_perm(b10, b11, 0x5612);
                   sp[0] = __dp4a(a0, b0p, sp[0]), sq[0] = __dp4a(a0, b0q, sq[0]);
@@ -612,10 +615,11 @@ __device__ __forceinline__ uint32_t ff_exec(const SmemT<WT> &s, const FieldConst
                 }
               }
             }
+            const WT *qa = pa + int32_t(k) * ska, *qb = pb + int32_t(k) * skb;
 #pragma unroll 2
-            for (; k < k1; ++k) {
-              const uint32_t a0 = pa[int32_t(k) * ska], a1 = pa[int32_t(k) * ska + sma];
-              const uint32_t b0 = pb[int32_t(k) * skb], b1 = pb[int32_t(k) * skb + snb];
+            for (; k < k1; ++k, qa += ska, qb += skb) {
+              const uint32_t a0 = qa[0], a1 = qa[sma];
+              const uint32_t b0 = qb[0], b1 = qb[snb];
               const uint32_t a0p = a0 & PM, a0q = a0 >> QS, a1p = a1 & PM, a1q = a1 >> QS;
               const uint32_t b0p = b0 & PM, b0q = b0 >> QS, b1p = b1 & PM, b1q = b1 >> QS;
               sp[0] += a0p * b0p, sq[0] += a0q * b0q;
@@ -649,16 +653,18 @@ __device__ __forceinline__ uint32_t ff_exec(const SmemT<WT> &s, const FieldConst
           const uint32_t k1 = min(K, k0 + lazy);
           uint32_t p0 = 0, p1 = 0, q0 = 0, q1 = 0;  // 4 independent chains
           uint32_t k = k0;
-          for (; k + 2 <= k1; k += 2) {
-            const uint32_t va0 = pa[int32_t(k) * ska], vb0 = pb[int32_t(k) * skb];
-            const uint32_t va1 = pa[int32_t(k + 1) * ska], vb1 = pb[int32_t(k + 1) * skb];
+          const WT *qa = pa + int32_t(k) * ska, *qb = pb + int32_t(k) * skb;
+          const int32_t ska2 = 2 * ska, skb2 = 2 * skb;
+          for (; k + 2 <= k1; k += 2, qa += ska2, qb += skb2) {
+            const uint32_t va0 = qa[0], vb0 = qb[0];
+            const uint32_t va1 = qa[ska], vb1 = qb[skb];
             p0 += (va0 & PM) * (vb0 & PM);
             q0 += (va0 >> QS) * (vb0 >> QS);
             p1 += (va1 & PM) * (vb1 & PM);
             q1 += (va1 >> QS) * (vb1 >> QS);
           }
           if (k < k1) {
-            const uint32_t va0 = pa[int32_t(k) * ska], vb0 = pb[int32_t(k) * skb];
+            const uint32_t va0 = qa[0], vb0 = qb[0];
             p0 += (va0 & PM) * (vb0 & PM);
             q0 += (va0 >> QS) * (vb0 >> QS);
           }

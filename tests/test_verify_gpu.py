@@ -208,6 +208,11 @@ def test_distinct_candidate_stream_matches_reference(ctx):
             for c in VCOLS:
                 assert got[c][k] == w[c], (fam, k, c)
         assert np.array_equal(acc, got["kind"] == 0)
+        # the handle-array fast path (compile_many(batch=True)): same verdicts
+        gb, st2 = ctx.compile_many(texts, batch=True)
+        assert len(gb) == 300 and all(s == 0 for s in st2)
+        got2, acc2 = ctx.verify_batch(prog, gb, seeds)
+        assert np.array_equal(got2, got) and np.array_equal(acc2, acc)
 
 
 @pytest.mark.parametrize("fam", ["rmsnorm", "lora", "gqa"])

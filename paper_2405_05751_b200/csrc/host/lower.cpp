@@ -54,25 +54,29 @@ struct View {
 };
 
 // Drop unit dims and merge dims that are jointly contiguous for all operands.
+// In place: the kept dims are compacted to the front (w <= k), so no
+// second View is allocated.
 void collapse(View &v) {
-  View o;
-  o.st.resize(v.st.size());
+  size_t w = 0;  // dims kept so far
   for (size_t k = 0; k < v.dims.size(); ++k) {
     if (v.dims[k] == 1) continue;
-    bool merge = !o.dims.empty() && !v.wm[k] && !o.wm.back();
+    bool merge = w > 0 && !v.wm[k] && !v.wm[w - 1];
     if (merge)
       for (size_t p = 0; p < v.st.size(); ++p)
-        if (o.st[p].back() != v.st[p][k] * v.dims[k]) merge = false;
+        if (v.st[p][w - 1] != v.st[p][k] * v.dims[k]) merge = false;
     if (merge) {
-      o.dims.back() *= v.dims[k];
-      for (size_t p = 0; p < v.st.size(); ++p) o.st[p].back() = v.st[p][k];
+      v.dims[w - 1] *= v.dims[k];
+      for (size_t p = 0; p < v.st.size(); ++p) v.st[p][w - 1] = v.st[p][k];
     } else {
-      o.dims.push_back(v.dims[k]);
-      o.wm.push_back(v.wm[k]);
-      for (size_t p = 0; p < v.st.size(); ++p) o.st[p].push_back(v.st[p][k]);
+      v.dims[w] = v.dims[k];
+      v.wm[w] = v.wm[k];
+      for (size_t p = 0; p < v.st.size(); ++p) v.st[p][w] = v.st[p][k];
+      ++w;
     }
   }
-  v = std::move(o);
+  v.dims.resize(w);
+  v.wm.resize(w);
+  for (auto &s : v.st) s.resize(w);
 }
 
 int32_t i32(int64_t x) {
@@ -80,7 +84,7 @@ int32_t i32(int64_t x) {
   return int32_t(x);
 }
 
-TpoVmInstr make(uint8_t op, uint8_t sub, View v, uint32_t dst, uint32_t a, uint32_t b) {
+TpoVmInstr make(uint8_t op, uint8_t sub, View &v, uint32_t dst, uint32_t a, uint32_t b) {  // collapses v
   collapse(v);
   if (v.dims.size() > TPO_VM_DIMS) throw Error(ErrCode::Unsupported, "VM index rank > 7");
   TpoVmInstr in;

@@ -906,12 +906,14 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : NT == 128 ? 7 : 14) verify
   if (threadIdx.x == 0) s_g1 = a.graphs[a.program];
   __syncthreads();
   const TpoVmGraph &g1 = s_g1;
-  // bytecode staged in shared memory: the program once per CTA, each
-  // candidate's code when it changes (instructions are uniform across the
-  // block; smem reads avoid a global round trip per VM instruction)
-  TpoVmInstr *scode = reinterpret_cast<TpoVmInstr *>(smem + f.table_bytes);
-  copy_code(scode, a.code + g1.code_off, g1.code_len);
-  TpoVmInstr *ccode = scode + g1.code_len;
+  // bytecode: by default (a.code_global) read in place from global memory —
+  // block-uniform loads that stay L1-resident; otherwise staged in shared
+  // memory, the program once per CTA and each candidate's code when it
+  // changes (host: run_verify, TPO_VM_CODE_GLOBAL)
+  const bool code_global = a.code_global != 0;
+  TpoVmInstr *scode_s = reinterpret_cast<TpoVmInstr *>(smem + f.table_bytes);
+  if (!code_global) copy_code(scode_s, a.code + g1.code_off, g1.code_len);
+  TpoVmInstr *ccode_s = scode_s + g1.code_len;
   uint32_t staged = 0xffffffffu, desc = 0xffffffffu;  // graph whose code / descriptor is in smem
   for (;;) {
     __syncthreads();
@@ -930,7 +932,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : NT == 128 ? 7 : 14) verify
     const TpoVmGraph &g2 = s_g2;
     const bool silu = g1.has_silu || g2.has_silu;
     if (gi != staged && !g2.err) {
-      copy_code(ccode, a.code + g2.code_off, g2.code_len);
+      if (!code_global) copy_code(ccode_s, a.code + g2.code_off, g2.code_len);
       staged = gi;
     }
 
@@ -1012,7 +1014,10 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : NT == 128 ? 7 : 14) verify
           bool prog = run_prog;
           uint32_t gen_next = 0;
           for (;;) {
-            bool r = run_program<PROF>(s, f, prog ? scode : ccode, prog ? g1.code_len : g2.code_len, &s_flag,
+            // (pointers recomputed from the smem descriptors: fewer live registers)
+            const TpoVmInstr *code = code_global ? a.code + (prog ? g1.code_off : g2.code_off)
+                                                 : (prog ? scode_s : ccode_s);
+            bool r = run_program<PROF>(s, f, code, prog ? g1.code_len : g2.code_len, &s_flag,
                                        s_prof, prog && lazy ? &g1 : nullptr, lazy_st0, &gen_next, &s_restart,
                                        &s_drawn);
             if (!prog) {

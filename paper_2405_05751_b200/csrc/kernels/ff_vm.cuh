@@ -56,6 +56,7 @@ struct VerifyArgs {
   unsigned long long *work;      // optional: attempts actually consumed
   unsigned long long *prof;      // optional (TPO_VM_PROFILE): [16] cycles, [16] counts per opcode
   uint32_t code_smem_bytes;      // smem staging of program + candidate bytecode
+  uint32_t code_global;          // 1: bytecode read in place from `code` (no smem staging)
   // Same-seed batches (a search loop verifying every candidate with the
   // VerifyConfig seed): attempt (shared_seed, round 0, attempt 0) is
   // generated and the program evaluated ONCE (shared_attempt_kernel); the

@@ -1404,7 +1404,11 @@ int stability_batch_smem(tpo_gpu_ctx *ctx, const tpo_gpu_graph *program, const t
       }
       cg[k] = it->second;
     }
-    const size_t code_bytes = size_t(d0.code_len + max_cl) * sizeof(TpoVmInstr);
+    // bytecode read in place (as the field verifier does) unless
+    // TPO_VM_CODE_GLOBAL=0 stages it into shared memory
+    const char *cg_env = std::getenv("TPO_VM_CODE_GLOBAL");
+    const bool code_in_place = !cg_env || std::atoi(cg_env) != 0;
+    const size_t code_bytes = code_in_place ? 0 : size_t(d0.code_len + max_cl) * sizeof(TpoVmInstr);
     const size_t smem = code_bytes + size_t(maxw) * 8;
     if (smem > 232448)
       throw Error(ErrCode::DoesNotFit, "stability working set " + std::to_string(smem) +

@@ -408,11 +408,17 @@ __global__ void __launch_bounds__(kThreads) stability_kernel(StabilityArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int s_fail;
   __shared__ unsigned long long s_cand;
-  TpoVmInstr *pcode = reinterpret_cast<TpoVmInstr *>(smem);
-  TpoVmInstr *ccode = pcode + a.graphs[0].code_len;
+  // bytecode staged in shared memory, or (code_bytes == 0) read in place
+  // from global memory: block-uniform, L1-resident loads, and the fp64
+  // working set alone bounds residency
+  const bool in_place = a.code_bytes == 0;
+  TpoVmInstr *pcode_s = reinterpret_cast<TpoVmInstr *>(smem);
+  TpoVmInstr *ccode_s = pcode_s + a.graphs[0].code_len;
   double *W = reinterpret_cast<double *>(smem + a.code_bytes);
   const TpoVmGraph g1 = a.graphs[0];
-  copy_code(pcode, a.code + g1.code_off, g1.code_len);
+  if (!in_place) copy_code(pcode_s, a.code + g1.code_off, g1.code_len);
+  const TpoVmInstr *pcode = in_place ? a.code + g1.code_off : pcode_s;
+  const TpoVmInstr *ccode = ccode_s;
   uint32_t staged = 0xffffffffu;
   for (;;) {
     __syncthreads();
@@ -427,7 +433,10 @@ __global__ void __launch_bounds__(kThreads) stability_kernel(StabilityArgs a) {
       verdict = -1;
     } else {
       if (gi != staged) {
-        copy_code(ccode, a.code + g2.code_off, g2.code_len);
+        if (in_place)
+          ccode = a.code + g2.code_off;
+        else
+          copy_code(ccode_s, a.code + g2.code_off, g2.code_len);
         staged = gi;
       }
       verdict = 1;

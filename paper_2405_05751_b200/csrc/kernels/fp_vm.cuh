@@ -22,7 +22,7 @@ struct EvalArgs {
 struct StabilityArgs {
   const TpoVmInstr *code;        // batch bytecode
   const TpoVmGraph *graphs;      // graphs[0] = program
-  uint32_t code_bytes;           // smem bytes for program + largest candidate code
+  uint32_t code_bytes;           // smem bytes for program + largest candidate code (0: read in place)
   const uint32_t *cand_graph;    // graph index per candidate
   const uint64_t *seeds;         // per-candidate seed (null: `seed` for all)
   uint64_t seed, n;

@@ -729,12 +729,25 @@ __device__ __forceinline__ uint32_t ff_exec(const SmemT<WT> &s, const FieldConst
             // contiguous group of 16-bit words: two elements per 32-bit
             // load, each field's pair summed by one dp4a against 1-lanes
             if (inner == 1 && (reinterpret_cast<uintptr_t>(pa + g0) & 3u) == 0) {
+              // each thread sums its own contiguous group, and groups sit
+              // at a multiple-of-128-B pitch: all lanes would hit one bank
+              // (32-way).  A power-of-two group of >= 32 starts each lane at its own
+              // rotation (the field sum is order-free; same term count)
+              const uint32_t len = g1 - g0;
+              const uint32_t rr = (len >= 32 && (len & (len - 1)) == 0) ? (2u * o) & (len - 1) : 0u;
 #pragma unroll 4
-              for (; g + 2 <= g1; g += 2) {
-                const uint32_t v2 = *reinterpret_cast<const uint32_t *>(pa + g);
+              for (uint32_t j = rr; j + 2 <= len; j += 2) {
+                const uint32_t v2 = *reinterpret_cast<const uint32_t *>(pa + g0 + j);
                 sp = __dp4a(v2, 0x00010001u, sp);
                 sq = __dp4a(v2, 0x01000100u, sq);
               }
+#pragma unroll 4
+              for (uint32_t j = 0; j < rr; j += 2) {
+                const uint32_t v2 = *reinterpret_cast<const uint32_t *>(pa + g0 + j);
+                sp = __dp4a(v2, 0x00010001u, sp);
+                sq = __dp4a(v2, 0x01000100u, sq);
+              }
+              g = rr ? g1 : g0 + (len & ~1u);
             }
           }
 #pragma unroll 4
